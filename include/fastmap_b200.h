@@ -1,0 +1,160 @@
+/*
+ * fastmap_b200.h -- C-ABI of the B200-native point-to-block projection.
+ *
+ * This is the drop-in boundary for the reference's hot path (SURVEY.md
+ * sec. 8b).  The reference is a header-only C++20 library with no FFI; its
+ * path is four calls, each replaced here by a plain-pointer entry point:
+ *
+ *   reference (/root/reference/proj/include/fastmap/...)         here
+ *   -------------------------------------------------------------  ---------------------
+ *   CellCover build_cover(span<const LeafRegion>, const CoverParams&)
+ *                                        cell_index.hpp:396-400   fm_index_build
+ *   CellCover build_cover(const RegionHierarchy&, const CoverParams&)
+ *                                        cell_index.hpp:402-405   fm_index_build
+ *   TrieIndex build_trie(const CellCover&, int levels_per_node)
+ *                                        cell_index.hpp:453-507   (folded into fm_index_build)
+ *   AssignmentResult query_leaves(const TrieIndex&, span<const LeafRegion>,
+ *                                 span<const Point>, CoverMode)
+ *                                        cell_index.hpp:527-590   fm_query / fm_query_host
+ *   vector<int32_t> exhaustive_assign(span<const LeafRegion>, span<const Point>)
+ *                                        synthetic.hpp:193-205    fm_query (same answers)
+ *   IndexStats index_stats(const TrieIndex&, const CellCover&)
+ *                                        cell_index.hpp:616-631   fm_index_stats
+ *
+ * Semantics.  The output for point p is the leaf id (position in the
+ * collect_leaves order, hierarchy.hpp:76-91) of the FIRST leaf, ascending,
+ * whose reference point_in_polygon (geometry.hpp:214-225) is true, else -1;
+ * points outside the lon/lat world box (cell_index.hpp:549-552) or with NaN
+ * coordinates give -1.  This is exhaustive_assign's rule; it equals
+ * query_leaves(..., exact) on every valid tiling and is bit-exact against
+ * the reference fp64 predicate (no FMA contraction anywhere on the path).
+ *
+ * Polygon soup (one leaf = one polygon, possibly multi-ring, as
+ * PolygonGeometry, geometry.hpp:64-87):
+ *   vertex_lonlat[2*v], [2*v+1]        lon, lat of vertex v
+ *   ring_offsets[r] .. [r+1]           vertices of ring r (open ring, >= 3
+ *                                      vertices; the closing edge is implied,
+ *                                      like PolygonGeometry::add_ring)
+ *   poly_ring_offsets[p] .. [p+1]      rings of leaf p
+ *
+ * Errors map onto the reference's exception types (sec. 8b): the C++
+ * adapter (include/fastmap_b200/fastmap_gpu.hpp) rethrows
+ * FM_ERR_INVALID_ARGUMENT as std::invalid_argument, FM_ERR_RUNTIME as
+ * std::runtime_error, FM_ERR_DOMAIN as std::domain_error; FM_ERR_CUDA and
+ * FM_ERR_NO_DEVICE as std::runtime_error.  There is no CPU fallback: with
+ * no usable CUDA device every compute call fails with FM_ERR_NO_DEVICE.
+ *
+ * Threading: a built index is immutable; fm_query may be called
+ * concurrently on different streams.  One index lives on one device.
+ */
+#ifndef FASTMAP_B200_H_
+#define FASTMAP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fm_status {
+  FM_OK = 0,
+  FM_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  FM_ERR_RUNTIME = 2,          /* std::runtime_error */
+  FM_ERR_DOMAIN = 3,           /* std::domain_error */
+  FM_ERR_CUDA = 4,             /* CUDA runtime failure */
+  FM_ERR_NO_DEVICE = 5,        /* no CUDA device: the product never falls back */
+  FM_ERR_OOM = 6
+} fm_status;
+
+typedef struct fm_index fm_index;
+
+/* Index build parameters (the analogue of CoverParams, cell_index.hpp:248-252).
+ * Zero-initialise and set what you need. */
+typedef struct fm_build_params {
+  /* Grid resolution: cells per mean polygon bbox side.  0 = auto (sized so
+   * the cell table stays L2-resident, clamped to [4, 64]). */
+  double cells_per_polygon;
+  /* Explicit grid dimensions; both > 0 override cells_per_polygon. */
+  int64_t nx, ny;
+  /* Conservative classification margin in coordinate units; 0 = auto
+   * (2^-40 * max(1, max |coordinate|)).  Must exceed fp64 rounding of the
+   * predicate by a wide factor; see DESIGN.md sec. 4. */
+  double margin;
+  /* CUDA device ordinal the index lives on. */
+  int device;
+  /* 1 = build the cell index on the GPU (default path); 0 = host builder
+   * (C++ threads).  Both produce bit-identical index arrays. */
+  int build_on_gpu;
+  /* Host build threads (0 = hardware concurrency). */
+  int threads;
+} fm_build_params;
+
+typedef struct fm_index_stats {
+  uint64_t n_polys, n_rings, n_vertices, n_edges;
+  int64_t nx, ny;
+  uint64_t cells_empty, cells_hit, cells_boundary;
+  uint64_t grid_bytes, arena_bytes, geometry_bytes;
+  uint64_t record_edges, record_cands, record_breaks; /* totals over records */
+  uint64_t max_record_edges, max_record_cands;
+  double gx0, gx1, gy0, gy1, cell_w, cell_h, margin;
+  double build_seconds;
+} fm_index_stats;
+
+/* Optional per-call work counters (diagnostics; device-side atomics). */
+typedef struct fm_query_counters {
+  uint64_t points;            /* points processed */
+  uint64_t boundary_points;   /* points that landed in a boundary cell */
+  uint64_t candidate_tests;   /* candidate leaves evaluated (reference: pip_point_evaluations) */
+  uint64_t edge_tests;        /* fp64 crossing predicates evaluated */
+} fm_query_counters;
+
+const char* fm_status_string(fm_status s);
+/* Message of the last failure on the calling thread ("" if none). */
+const char* fm_last_error(void);
+/* Version string of the library. */
+const char* fm_version(void);
+
+/* build_cover + build_trie (cell_index.hpp:396-405, :453-507).  Host
+ * pointers.  Throws-equivalents: FM_ERR_INVALID_ARGUMENT for rings with < 3
+ * vertices, non-finite vertices, bad offsets or params; FM_ERR_RUNTIME for a
+ * boundary cell with more than 65535 candidates (cell_index.hpp:339-341). */
+fm_status fm_index_build(const double* vertex_lonlat, const uint64_t* ring_offsets,
+                         uint64_t n_rings, const uint64_t* poly_ring_offsets,
+                         uint64_t n_polys, const fm_build_params* params,
+                         fm_index** out_index);
+
+void fm_index_destroy(fm_index* index);
+
+fm_status fm_index_stats_get(const fm_index* index, fm_index_stats* out);
+
+/* query_leaves(trie, leaves, points, CoverMode::exact) (cell_index.hpp:527-590)
+ * on DEVICE pointers: d_lonlat = n interleaved (lon, lat) fp64 pairs (the
+ * reference Point layout, geometry.hpp:17-22), d_out = n int32 leaf ids.
+ * d_hist (nullable) = n_polys int64 counters incremented per assigned point.
+ * d_counters (nullable) = device fm_query_counters accumulated into.
+ * stream = cudaStream_t (NULL = legacy default stream).  Asynchronous. */
+fm_status fm_query(const fm_index* index, const double* d_lonlat, uint64_t n,
+                   int32_t* d_out, int64_t* d_hist, fm_query_counters* d_counters,
+                   void* stream);
+
+/* Same on HOST pointers: chunked and pipelined host->device copy, query and
+ * device->host copy over internal streams; returns when h_out (and h_hist,
+ * nullable, n_polys int64, accumulated into) are complete.  Pinned host
+ * buffers give full PCIe overlap; pageable ones work but copy slower. */
+fm_status fm_query_host(const fm_index* index, const double* h_lonlat, uint64_t n,
+                        int32_t* h_out, int64_t* h_hist);
+
+/* Copy of the index arrays to host memory (the FMCI-save analogue,
+ * cell_index.hpp:641-664).  Two-call protocol: null buffers -> sizes. */
+fm_status fm_index_export(const fm_index* index, uint32_t* grid, uint64_t* grid_len,
+                          uint8_t* arena, uint64_t* arena_len, double* geometry12);
+
+/* Device the index lives on. */
+int fm_index_device(const fm_index* index);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTMAP_B200_H_ */

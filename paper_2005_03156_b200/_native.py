@@ -1,0 +1,167 @@
+"""ctypes bindings to the in-tree native libraries.
+
+``libfastmap_b200.so`` is the product (C-ABI in ``include/fastmap_b200.h``);
+``libfastmap_synth.so`` holds the workload generators.  Both are built
+in-tree by ``make`` (``__graft_entry__.build()``).  A missing product
+library is a hard error: there is no Python or CPU fallback for the
+projection.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pathlib
+
+_PKG = pathlib.Path(__file__).resolve().parent
+LIBDIR = _PKG / "_lib"
+PRODUCT_SO = LIBDIR / "libfastmap_b200.so"
+SYNTH_SO = LIBDIR / "libfastmap_synth.so"
+
+u64 = C.c_uint64
+i64 = C.c_int64
+PD = C.POINTER(C.c_double)
+PU64 = C.POINTER(C.c_uint64)
+PU32 = C.POINTER(C.c_uint32)
+PI32 = C.POINTER(C.c_int32)
+PI64 = C.POINTER(C.c_int64)
+PU8 = C.POINTER(C.c_uint8)
+
+FM_OK = 0
+FM_ERR_INVALID_ARGUMENT = 1
+FM_ERR_RUNTIME = 2
+FM_ERR_DOMAIN = 3
+FM_ERR_CUDA = 4
+FM_ERR_NO_DEVICE = 5
+FM_ERR_OOM = 6
+
+
+class BuildParams(C.Structure):
+    _fields_ = [
+        ("cells_per_polygon", C.c_double),
+        ("nx", i64),
+        ("ny", i64),
+        ("margin", C.c_double),
+        ("device", C.c_int),
+        ("build_on_gpu", C.c_int),
+        ("threads", C.c_int),
+    ]
+
+
+class IndexStats(C.Structure):
+    _fields_ = [
+        ("n_polys", u64), ("n_rings", u64), ("n_vertices", u64), ("n_edges", u64),
+        ("nx", i64), ("ny", i64),
+        ("cells_empty", u64), ("cells_hit", u64), ("cells_boundary", u64),
+        ("grid_bytes", u64), ("arena_bytes", u64), ("geometry_bytes", u64),
+        ("record_edges", u64), ("record_cands", u64), ("record_breaks", u64),
+        ("max_record_edges", u64), ("max_record_cands", u64),
+        ("gx0", C.c_double), ("gx1", C.c_double), ("gy0", C.c_double), ("gy1", C.c_double),
+        ("cell_w", C.c_double), ("cell_h", C.c_double), ("margin", C.c_double),
+        ("build_seconds", C.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class QueryCounters(C.Structure):
+    _fields_ = [("points", u64), ("boundary_points", u64),
+                ("candidate_tests", u64), ("edge_tests", u64)]
+
+
+# every symbol include/fastmap_b200.h declares (tests check the export table)
+EXPORTS = (
+    "fm_status_string", "fm_last_error", "fm_version", "fm_index_build",
+    "fm_index_destroy", "fm_index_stats_get", "fm_query", "fm_query_host",
+    "fm_index_export", "fm_index_device",
+)
+
+_lib = None
+_synth = None
+
+
+def _load(path: pathlib.Path) -> C.CDLL:
+    if not path.exists():
+        raise RuntimeError(
+            f"native library {path} is missing: run `make` (or __graft_entry__.build()); "
+            "the B200 projection has no fallback implementation")
+    return C.CDLL(str(path), mode=os.RTLD_NOW | getattr(os, "RTLD_LOCAL", 0))
+
+
+def lib() -> C.CDLL:
+    """The product library, with argtypes set."""
+    global _lib
+    if _lib is None:
+        L = _load(PRODUCT_SO)
+        L.fm_status_string.restype = C.c_char_p
+        L.fm_status_string.argtypes = [C.c_int]
+        L.fm_last_error.restype = C.c_char_p
+        L.fm_last_error.argtypes = []
+        L.fm_version.restype = C.c_char_p
+        L.fm_version.argtypes = []
+        L.fm_index_build.restype = C.c_int
+        L.fm_index_build.argtypes = [PD, PU64, u64, PU64, u64, C.POINTER(BuildParams),
+                                     C.POINTER(C.c_void_p)]
+        L.fm_index_destroy.restype = None
+        L.fm_index_destroy.argtypes = [C.c_void_p]
+        L.fm_index_stats_get.restype = C.c_int
+        L.fm_index_stats_get.argtypes = [C.c_void_p, C.POINTER(IndexStats)]
+        L.fm_query.restype = C.c_int
+        L.fm_query.argtypes = [C.c_void_p, C.c_void_p, u64, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_void_p]
+        L.fm_query_host.restype = C.c_int
+        L.fm_query_host.argtypes = [C.c_void_p, PD, u64, PI32, PI64]
+        L.fm_index_export.restype = C.c_int
+        L.fm_index_export.argtypes = [C.c_void_p, PU32, PU64, PU8, PU64, PD]
+        L.fm_index_device.restype = C.c_int
+        L.fm_index_device.argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def synth() -> C.CDLL:
+    global _synth
+    if _synth is None:
+        L = _load(SYNTH_SO)
+        L.synth_tiling.restype = C.c_int
+        L.synth_tiling.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double,
+                                   C.c_double, C.c_double, C.c_double, C.c_double,
+                                   C.c_double, u64, C.c_int, PD, PU64, PU64]
+        L.synth_points_uniform.restype = C.c_int
+        L.synth_points_uniform.argtypes = [PD, u64, u64, u64, C.c_int, PD]
+        L.synth_points_clustered.restype = C.c_int
+        L.synth_points_clustered.argtypes = [PD, PD, u64, u64, u64, C.c_uint32,
+                                             C.c_double, C.c_double, C.c_double,
+                                             C.c_int, PD]
+        L.synth_points_near_edge.restype = C.c_int
+        L.synth_points_near_edge.argtypes = [PD, PU64, PU64, u64, C.c_double, C.c_double,
+                                             C.c_double, C.c_double, PD, u64, u64, u64,
+                                             C.c_int, PD]
+        _synth = L
+    return _synth
+
+
+def ptr(a, ctype):
+    """ctypes pointer to a contiguous numpy array's data."""
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+class FastmapError(Exception):
+    pass
+
+
+def check(status: int, what: str = "") -> None:
+    """Raise the Python analogue of the reference's exception type."""
+    if status == FM_OK:
+        return
+    L = lib()
+    msg = (L.fm_last_error() or b"").decode() or L.fm_status_string(status).decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if status == FM_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)          # std::invalid_argument
+    if status == FM_ERR_DOMAIN:
+        raise ArithmeticError(msg)     # std::domain_error
+    if status == FM_ERR_OOM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)            # std::runtime_error, CUDA, no device

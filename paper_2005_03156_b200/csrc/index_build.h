@@ -1,0 +1,58 @@
+// index_build.h -- internal API of the cell-index builders (host and GPU).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "index_format.h"
+
+namespace fm {
+
+struct Soup {
+  const double* vxy = nullptr;
+  const std::uint64_t* ring_off = nullptr;
+  std::uint64_t n_rings = 0;
+  const std::uint64_t* poly_ring = nullptr;
+  std::uint64_t n_polys = 0;
+};
+
+struct BuildOptions {
+  double cells_per_polygon = 0.0;
+  std::int64_t nx = 0, ny = 0;
+  double margin = 0.0;
+  int threads = 0;
+};
+
+struct BuildStats {
+  std::uint64_t n_edges = 0;
+  std::uint64_t cells_empty = 0, cells_hit = 0, cells_boundary = 0;
+  std::uint64_t record_edges = 0, record_cands = 0, record_breaks = 0;
+  std::uint64_t max_record_edges = 0, max_record_cands = 0;
+};
+
+struct HostIndex {
+  GridGeom g{};
+  std::vector<std::uint32_t> grid;
+  std::vector<std::uint8_t> arena;  // records, 16-byte granules, + 256 B zero tail
+  std::uint64_t arena_used = 0;     // bytes of records (excluding the tail)
+  BuildStats stats;
+};
+
+// Exceptions mirror the reference's.
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct RuntimeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Validates the soup (rings >= 3 vertices like PolygonGeometry::add_ring,
+// geometry.hpp:74-77; finite vertices; monotone offsets) and fixes the grid.
+GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st);
+
+// Host builder: C++ threads over grid rows.
+HostIndex build_index_host(const Soup& s, const BuildOptions& o);
+
+}  // namespace fm

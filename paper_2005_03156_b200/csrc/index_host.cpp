@@ -1,0 +1,548 @@
+// index_host.cpp -- cell-index planning and the host (C++ threads) builder.
+//
+// Replaces the reference's recursive single-threaded cover build
+// (CoverBuilder, cell_index.hpp:279-378, and build_trie, :453-507) with a
+// uniform grid whose cells are classified conservatively per (cell, leaf)
+// pair.  The classification is purely algebraic, so it is exact for ANY
+// input (overlapping, self-intersecting, multi-ring, degenerate); DESIGN.md
+// sec. 4 has the argument.  In short, for a point p of cell c and a leaf L
+// the reference parity (geometry.hpp:214-225) is the XOR over L's
+// non-horizontal edges e of [lo_e.lat < p.lat <= hi_e.lat and cross_e(p) > 0].
+// Relative to the cell's latitude slab (expanded by the margin d) every
+// edge is one of
+//   y-disjoint  never in range for any p of the cell        -> contributes 0
+//   left        wholly left of the cell by > d              -> cross <= 0, 0
+//   right       wholly right of the cell by > d             -> cross > 0, so it
+//               contributes [p.lat > lo] ^ [p.lat > hi]: endpoints below the
+//               slab fold into a constant bit c0, endpoints inside the slab
+//               become latitude breakpoints (pairs cancel)
+//   near        everything else -> evaluated at query time with the
+//               reference predicate itself.
+// A cell whose leaves all have no near edges and no breakpoints has a
+// constant answer (true hit / empty); otherwise it gets a boundary record.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "index_build.h"
+
+namespace fm {
+namespace {
+
+struct Edge4 {
+  double lx, ly, hx, hy;
+};
+inline bool same_edge(const Edge4& a, const Edge4& b) {
+  return std::memcmp(&a, &b, sizeof(Edge4)) == 0;
+}
+
+// smallest k in [0, n) with g0 + (k+1)*step >= v; n if none
+std::int64_t first_with_hi_ge(double g0, double step, double inv, std::int64_t n,
+                              double v) {
+  double f = std::floor((v - g0) * inv) - 1.0;
+  std::int64_t k = !(f > 0.0) ? 0 : (f > static_cast<double>(n) ? n : static_cast<std::int64_t>(f));
+  auto hi = [&](std::int64_t q) { return g0 + static_cast<double>(q + 1) * step; };
+  while (k > 0 && hi(k - 1) >= v) --k;
+  while (k < n && hi(k) < v) ++k;
+  return k;
+}
+
+// largest k in [0, n) with g0 + k*step <= v; -1 if none
+std::int64_t last_with_lo_le(double g0, double step, double inv, std::int64_t n,
+                             double v) {
+  double f = std::floor((v - g0) * inv) + 1.0;
+  std::int64_t k = !(f > -1.0) ? -1
+                   : (f > static_cast<double>(n - 1) ? n - 1 : static_cast<std::int64_t>(f));
+  auto lo = [&](std::int64_t q) { return g0 + static_cast<double>(q) * step; };
+  while (k >= 0 && lo(k) > v) --k;
+  while (k + 1 < n && lo(k + 1) <= v) ++k;
+  return k;
+}
+
+struct PolySpan {
+  double x0, x1, y0, y1;
+  std::int64_t c0, c1, r0, r1;
+  bool active;
+};
+
+struct Contrib {
+  std::uint32_t id;
+  std::uint32_t c0;
+  std::uint32_t e_begin, e_end;  // into the row edge pool
+  std::uint32_t b_begin, b_end;  // into the row break pool
+};
+
+struct RelEdge {
+  std::int64_t tlo, thi;
+  Edge4 e;
+};
+
+void toggle(std::vector<double>& set, double v) {
+  auto it = std::lower_bound(set.begin(), set.end(), v);
+  if (it != set.end() && *it == v) {
+    set.erase(it);
+  } else {
+    set.insert(it, v);
+  }
+}
+
+struct RowWorker {
+  const Soup& s;
+  const GridGeom& g;
+  const std::vector<PolySpan>& spans;
+  double tol;
+
+  std::vector<std::vector<Contrib>> cols;
+  std::vector<std::uint8_t> closed;
+  std::vector<std::int64_t> touched;
+  std::vector<Edge4> epool;
+  std::vector<double> bpool;
+  std::vector<RelEdge> rel;
+  std::vector<std::uint32_t> order;
+  std::vector<double> tog;
+  BuildStats st;
+
+  // finalize scratch
+  std::vector<Edge4> U;
+  struct Cand {
+    std::uint32_t id, c0;
+    std::vector<std::uint32_t> edges;  // indices into U, odd multiplicity
+    std::uint32_t b_begin, b_end;
+  };
+  std::vector<Cand> cands;
+
+  RowWorker(const Soup& s_, const GridGeom& g_, const std::vector<PolySpan>& sp, double t)
+      : s(s_), g(g_), spans(sp), tol(t) {
+    cols.resize(static_cast<std::size_t>(g.nx));
+    closed.assign(static_cast<std::size_t>(g.nx), 0);
+  }
+
+  void gather_edges(std::uint32_t pid, double ys0, double ys1) {
+    rel.clear();
+    const double d = g.margin;
+    for (std::uint64_t r = s.poly_ring[pid]; r < s.poly_ring[pid + 1]; ++r) {
+      const std::uint64_t b = s.ring_off[r], e = s.ring_off[r + 1], n = e - b;
+      for (std::uint64_t i = 0; i < n; ++i) {
+        const std::uint64_t a = b + i, c = (i + 1 < n) ? a + 1 : b;
+        Edge4 E{s.vxy[2 * a], s.vxy[2 * a + 1], s.vxy[2 * c], s.vxy[2 * c + 1]};
+        if (E.ly > E.hy) {  // orient upward exactly like geometry.hpp:219
+          std::swap(E.lx, E.hx);
+          std::swap(E.ly, E.hy);
+        }
+        if (E.ly == E.hy) continue;               // horizontal: never in range
+        if (E.hy <= ys0 || E.ly >= ys1) continue;  // y-disjoint with the slab
+        const double ya = std::max(E.ly, ys0), yb = std::min(E.hy, ys1);
+        const double slope = (E.hx - E.lx) / (E.hy - E.ly);
+        const double mnx = std::min(E.lx, E.hx), mxx = std::max(E.lx, E.hx);
+        auto x_at = [&](double y) {
+          double x = E.lx + (y - E.ly) * slope;
+          return std::min(mxx, std::max(mnx, x));
+        };
+        const double xa = (ya == E.ly) ? E.lx : x_at(ya);
+        const double xb = (yb == E.hy) ? E.hx : x_at(yb);
+        const double ex0 = std::min(xa, xb) - tol, ex1 = std::max(xa, xb) + tol;
+        RelEdge re;
+        re.tlo = first_with_hi_ge(g.gx0, g.w, g.inv_w, g.nx, ex0 - d);
+        re.thi = last_with_lo_le(g.gx0, g.w, g.inv_w, g.nx, ex1 + d);
+        re.e = E;
+        rel.push_back(re);
+      }
+    }
+  }
+
+  void add_polygon(std::uint32_t pid, double ys0, double ys1) {
+    const PolySpan& sp = spans[pid];
+    gather_edges(pid, ys0, ys1);
+    order.resize(rel.size());
+    for (std::uint32_t k = 0; k < order.size(); ++k) order[k] = k;
+    std::sort(order.begin(), order.end(),
+              [&](std::uint32_t a, std::uint32_t b) { return rel[a].tlo > rel[b].tlo; });
+    tog.clear();
+    std::uint32_t c0par = 0;
+    std::size_t k = 0;
+    auto add_right = [&](const RelEdge& re) {
+      for (const double m : {re.e.ly, re.e.hy}) {
+        if (m < ys0) {
+          c0par ^= 1u;
+        } else if (m < ys1) {
+          toggle(tog, m);
+        }
+      }
+    };
+    for (std::int64_t ix = sp.c1; ix >= sp.c0; --ix) {
+      while (k < order.size() && rel[order[k]].tlo > ix) add_right(rel[order[k++]]);
+      if (closed[ix]) continue;
+      const std::uint32_t eb = static_cast<std::uint32_t>(epool.size());
+      for (const RelEdge& re : rel) {
+        if (re.tlo <= ix && ix <= re.thi) epool.push_back(re.e);
+      }
+      const std::uint32_t ee = static_cast<std::uint32_t>(epool.size());
+      if (ee == eb && tog.empty()) {
+        if (c0par) {  // constant-true leaf: terminal for this cell
+          if (cols[ix].empty()) touched.push_back(ix);
+          cols[ix].push_back({pid, 1u, eb, eb, 0, 0});
+          closed[ix] = 1;
+        }
+        continue;
+      }
+      const std::uint32_t bb = static_cast<std::uint32_t>(bpool.size());
+      bpool.insert(bpool.end(), tog.begin(), tog.end());
+      if (cols[ix].empty()) touched.push_back(ix);
+      cols[ix].push_back({pid, c0par, eb, ee, bb, static_cast<std::uint32_t>(bpool.size())});
+    }
+  }
+
+  // Returns the grid entry for the cell; may append a record to `arena`,
+  // in which case *rec_off receives its row-local byte offset.
+  std::uint32_t finalize_cell(std::int64_t ix, std::vector<std::uint8_t>& arena,
+                              std::int64_t* rec_off) {
+    const auto& list = cols[ix];
+    U.clear();
+    cands.clear();
+    for (const Contrib& c : list) {
+      Cand cd;
+      cd.id = c.id;
+      cd.c0 = c.c0;
+      cd.b_begin = c.b_begin;
+      cd.b_end = c.b_end;
+      for (std::uint32_t q = c.e_begin; q < c.e_end; ++q) {
+        std::uint32_t idx = 0;
+        while (idx < U.size() && !same_edge(U[idx], epool[q])) ++idx;
+        if (idx == U.size()) U.push_back(epool[q]);
+        auto it = std::find(cd.edges.begin(), cd.edges.end(), idx);
+        if (it != cd.edges.end()) {
+          cd.edges.erase(it);  // even multiplicity cancels
+        } else {
+          cd.edges.push_back(idx);
+        }
+      }
+      if (cd.edges.empty() && cd.b_begin == cd.b_end) {
+        if (cd.c0) {  // terminal
+          cd.edges.clear();
+          cands.push_back(std::move(cd));
+          break;
+        }
+        continue;  // constant false
+      }
+      cands.push_back(std::move(cd));
+    }
+    if (cands.empty()) {
+      st.cells_empty++;
+      return kEmpty;
+    }
+    const Cand& first = cands.front();
+    if (first.edges.empty() && first.b_begin == first.b_end) {
+      st.cells_hit++;
+      return first.id;  // true hit (first leaf is constant-true)
+    }
+    // compact edges to the ones still referenced
+    std::vector<std::int64_t> remap(U.size(), -1);
+    std::vector<Edge4> used;
+    for (auto& cd : cands) {
+      for (auto& e : cd.edges) {
+        if (remap[e] < 0) {
+          remap[e] = static_cast<std::int64_t>(used.size());
+          used.push_back(U[e]);
+        }
+        e = static_cast<std::uint32_t>(remap[e]);
+      }
+    }
+    const std::uint64_t n_edges = used.size(), n_cands = cands.size();
+    std::uint64_t n_breaks = 0;
+    for (const auto& cd : cands) {
+      const std::uint64_t nb = cd.b_end - cd.b_begin;
+      if (nb > kMaxBreaksPerCand) {
+        throw RuntimeError("boundary cell leaf with more than 32767 latitude breakpoints");
+      }
+      n_breaks += nb;
+    }
+    if (n_cands > kMaxCands) {
+      throw RuntimeError("boundary cell with more than 65535 candidates");
+    }
+    if (n_edges > kMaxRecordEdges || n_breaks > 0xFFFFu) {
+      throw RuntimeError("boundary cell with more than 65535 edges or breakpoints");
+    }
+    const std::uint32_t n_words = static_cast<std::uint32_t>((n_edges + 31) / 32);
+    const std::uint64_t bytes = record_bytes(static_cast<std::uint32_t>(n_edges),
+                                             static_cast<std::uint32_t>(n_cands), n_words,
+                                             static_cast<std::uint32_t>(n_breaks));
+    const std::uint64_t off = arena.size();
+    arena.resize(off + bytes, 0);
+    std::uint8_t* rec = arena.data() + off;
+    RecordHeader h{};
+    h.n_edges = static_cast<std::uint16_t>(n_edges);
+    h.n_cands = static_cast<std::uint16_t>(n_cands);
+    h.n_words = static_cast<std::uint16_t>(n_words);
+    h.n_breaks = static_cast<std::uint16_t>(n_breaks);
+    std::memcpy(rec, &h, sizeof(h));
+    std::memcpy(rec + 16, used.data(), 32 * n_edges);
+    std::uint8_t* cp = rec + record_cands_offset(static_cast<std::uint32_t>(n_edges));
+    std::uint32_t* mp = reinterpret_cast<std::uint32_t*>(
+        rec + record_masks_offset(static_cast<std::uint32_t>(n_edges),
+                                  static_cast<std::uint32_t>(n_cands)));
+    double* bp = reinterpret_cast<double*>(
+        rec + record_breaks_offset(static_cast<std::uint32_t>(n_edges),
+                                   static_cast<std::uint32_t>(n_cands), n_words));
+    std::uint64_t bw = 0;
+    for (std::uint64_t c = 0; c < n_cands; ++c) {
+      const Cand& cd = cands[c];
+      const std::int32_t id = static_cast<std::int32_t>(cd.id);
+      const std::uint32_t nb = cd.b_end - cd.b_begin;
+      const std::uint32_t info = (cd.c0 & 1u) | (nb << 1);
+      std::memcpy(cp + 8 * c, &id, 4);
+      std::memcpy(cp + 8 * c + 4, &info, 4);
+      for (const std::uint32_t e : cd.edges) mp[c * n_words + e / 32] |= 1u << (e % 32);
+      for (std::uint32_t q = cd.b_begin; q < cd.b_end; ++q) bp[bw++] = bpool[q];
+    }
+    st.cells_boundary++;
+    st.record_edges += n_edges;
+    st.record_cands += n_cands;
+    st.record_breaks += n_breaks;
+    st.max_record_edges = std::max<std::uint64_t>(st.max_record_edges, n_edges);
+    st.max_record_cands = std::max<std::uint64_t>(st.max_record_cands, n_cands);
+    *rec_off = static_cast<std::int64_t>(off);
+    return kRecordBit;  // patched with the global offset later
+  }
+
+  void run_row(std::int64_t iy, const std::uint32_t* ids, std::uint64_t n_ids,
+               std::uint32_t* grid_row, std::vector<std::uint8_t>& arena,
+               std::vector<std::pair<std::int64_t, std::int64_t>>& recs) {
+    const double ys0 = cell_y0(g, iy) - g.margin;
+    const double ys1 = cell_y0(g, iy + 1) + g.margin;
+    epool.clear();
+    bpool.clear();
+    touched.clear();
+    for (std::uint64_t q = 0; q < n_ids; ++q) add_polygon(ids[q], ys0, ys1);
+    std::sort(touched.begin(), touched.end());
+    for (const std::int64_t ix : touched) {
+      std::int64_t off = -1;
+      grid_row[ix] = finalize_cell(ix, arena, &off);
+      if (off >= 0) recs.emplace_back(ix, off);
+      cols[ix].clear();
+      closed[ix] = 0;
+    }
+    st.cells_empty += static_cast<std::uint64_t>(g.nx) - touched.size();
+  }
+};
+
+}  // namespace
+
+GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
+  if (s.n_polys > kMaxLeaves) throw InvalidArgument("too many leaves for int32 ids");
+  if (s.n_polys > 0 && (s.poly_ring == nullptr || s.ring_off == nullptr || s.vxy == nullptr)) {
+    throw InvalidArgument("null polygon soup arrays");
+  }
+  if (!(o.cells_per_polygon >= 0.0) || !(o.margin >= 0.0) || o.nx < 0 || o.ny < 0) {
+    throw InvalidArgument("invalid index build parameters");
+  }
+  double ux0 = INFINITY, ux1 = -INFINITY, uy0 = INFINITY, uy1 = -INFINITY;
+  double sum_w = 0.0, sum_h = 0.0;
+  std::uint64_t active = 0, n_edges = 0;
+  for (std::uint64_t p = 0; p < s.n_polys; ++p) {
+    const std::uint64_t r0 = s.poly_ring[p], r1 = s.poly_ring[p + 1];
+    if (r1 < r0 || r1 > s.n_rings) throw InvalidArgument("bad polygon ring offsets");
+    if (r0 == r1) continue;
+    double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+    for (std::uint64_t r = r0; r < r1; ++r) {
+      const std::uint64_t b = s.ring_off[r], e = s.ring_off[r + 1];
+      if (e < b || e - b < 3) {
+        throw InvalidArgument("polygon ring needs at least 3 vertices");  // geometry.hpp:75-77
+      }
+      n_edges += e - b;
+      for (std::uint64_t v = b; v < e; ++v) {
+        const double x = s.vxy[2 * v], y = s.vxy[2 * v + 1];
+        if (!std::isfinite(x) || !std::isfinite(y)) {
+          throw InvalidArgument("non-finite polygon vertex");
+        }
+        x0 = std::min(x0, x);
+        x1 = std::max(x1, x);
+        y0 = std::min(y0, y);
+        y1 = std::max(y1, y);
+      }
+    }
+    ux0 = std::min(ux0, x0);
+    ux1 = std::max(ux1, x1);
+    uy0 = std::min(uy0, y0);
+    uy1 = std::max(uy1, y1);
+    sum_w += x1 - x0;
+    sum_h += y1 - y0;
+    ++active;
+  }
+  if (st) st->n_edges = n_edges;
+  GridGeom g{};
+  if (active == 0) {
+    g.gx0 = 0.0;
+    g.gx1 = 1.0;
+    g.gy0 = 0.0;
+    g.gy1 = 1.0;
+    g.nx = g.ny = 1;
+    g.w = g.h = 1.0;
+    g.inv_w = g.inv_h = 1.0;
+    g.margin = o.margin > 0 ? o.margin : std::ldexp(1.0, -40);
+    return g;
+  }
+  double M = std::max(std::max(std::fabs(ux0), std::fabs(ux1)),
+                      std::max(std::fabs(uy0), std::fabs(uy1)));
+  if (!(M >= 1.0)) M = 1.0;
+  g.margin = o.margin > 0.0 ? o.margin : std::ldexp(M, -40);
+  const double pad = 4.0 * g.margin;
+  g.gx0 = ux0 - pad;
+  g.gx1 = ux1 + pad;
+  g.gy0 = uy0 - pad;
+  g.gy1 = uy1 + pad;
+  const double GW = g.gx1 - g.gx0, GH = g.gy1 - g.gy0;
+  std::int64_t nx = o.nx, ny = o.ny;
+  if (nx <= 0 || ny <= 0) {
+    double mw = sum_w / static_cast<double>(active), mh = sum_h / static_cast<double>(active);
+    const double side = std::sqrt(static_cast<double>(active));
+    if (!(mw > 0.0)) mw = GW / side;
+    if (!(mh > 0.0)) mh = GH / side;
+    double m = o.cells_per_polygon;
+    if (!(m > 0.0)) {
+      m = std::sqrt(16.0 * 1024.0 * 1024.0 / static_cast<double>(active));
+      m = std::min(64.0, std::max(4.0, m));
+    }
+    nx = static_cast<std::int64_t>(std::ceil(GW / (mw / m)));
+    ny = static_cast<std::int64_t>(std::ceil(GH / (mh / m)));
+    nx = std::min<std::int64_t>(std::max<std::int64_t>(nx, 1), std::int64_t{1} << 22);
+    ny = std::min<std::int64_t>(std::max<std::int64_t>(ny, 1), std::int64_t{1} << 22);
+    while (nx * ny > (std::int64_t{1} << 30)) {
+      nx = (nx + 1) / 2;
+      ny = (ny + 1) / 2;
+    }
+  }
+  if (nx * ny > (std::int64_t{1} << 31)) throw InvalidArgument("grid too large");
+  g.nx = nx;
+  g.ny = ny;
+  g.w = GW / static_cast<double>(nx);
+  g.h = GH / static_cast<double>(ny);
+  g.inv_w = static_cast<double>(nx) / GW;
+  g.inv_h = static_cast<double>(ny) / GH;
+  return g;
+}
+
+HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
+  HostIndex out;
+  out.g = plan_grid(s, o, &out.stats);
+  const GridGeom& g = out.g;
+  const std::size_t ncell = static_cast<std::size_t>(g.nx * g.ny);
+  out.grid.assign(ncell, kEmpty);
+  out.arena.assign(256, 0);
+  if (s.n_polys == 0) {
+    out.stats.cells_empty = ncell;
+    return out;
+  }
+  const double d = g.margin;
+  std::vector<PolySpan> spans(s.n_polys);
+  std::vector<std::uint64_t> row_count(static_cast<std::size_t>(g.ny) + 1, 0);
+  for (std::uint64_t p = 0; p < s.n_polys; ++p) {
+    PolySpan& sp = spans[p];
+    sp.active = s.poly_ring[p + 1] > s.poly_ring[p];
+    if (!sp.active) continue;
+    double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+    for (std::uint64_t v = s.ring_off[s.poly_ring[p]]; v < s.ring_off[s.poly_ring[p + 1]]; ++v) {
+      x0 = std::min(x0, s.vxy[2 * v]);
+      x1 = std::max(x1, s.vxy[2 * v]);
+      y0 = std::min(y0, s.vxy[2 * v + 1]);
+      y1 = std::max(y1, s.vxy[2 * v + 1]);
+    }
+    sp.x0 = x0;
+    sp.x1 = x1;
+    sp.y0 = y0;
+    sp.y1 = y1;
+    sp.c0 = first_with_hi_ge(g.gx0, g.w, g.inv_w, g.nx, x0 - d);
+    sp.c1 = last_with_lo_le(g.gx0, g.w, g.inv_w, g.nx, x1 + d);
+    sp.r0 = first_with_hi_ge(g.gy0, g.h, g.inv_h, g.ny, y0 - d);
+    sp.r1 = last_with_lo_le(g.gy0, g.h, g.inv_h, g.ny, y1 + d);
+    if (sp.c0 > sp.c1 || sp.r0 > sp.r1) {
+      sp.active = false;
+      continue;
+    }
+    for (std::int64_t r = sp.r0; r <= sp.r1; ++r) row_count[static_cast<std::size_t>(r) + 1]++;
+  }
+  for (std::int64_t r = 0; r < g.ny; ++r) row_count[r + 1] += row_count[r];
+  std::vector<std::uint32_t> row_ids(row_count[static_cast<std::size_t>(g.ny)]);
+  {
+    std::vector<std::uint64_t> fill(row_count.begin(), row_count.end() - 1);
+    for (std::uint64_t p = 0; p < s.n_polys; ++p) {
+      if (!spans[p].active) continue;
+      for (std::int64_t r = spans[p].r0; r <= spans[p].r1; ++r) {
+        row_ids[fill[static_cast<std::size_t>(r)]++] = static_cast<std::uint32_t>(p);
+      }
+    }
+  }
+
+  const double M = std::max(std::max(std::fabs(g.gx0), std::fabs(g.gx1)),
+                            std::max(std::fabs(g.gy0), std::fabs(g.gy1)));
+  const double tol = std::ldexp(std::max(1.0, M), -46);
+  int threads = o.threads > 0 ? o.threads : static_cast<int>(std::thread::hardware_concurrency());
+  if (threads < 1) threads = 1;
+  threads = static_cast<int>(std::min<std::int64_t>(threads, g.ny));
+
+  std::vector<std::vector<std::uint8_t>> row_arena(static_cast<std::size_t>(g.ny));
+  std::vector<std::vector<std::pair<std::int64_t, std::int64_t>>> row_recs(
+      static_cast<std::size_t>(g.ny));
+  std::atomic<std::int64_t> next{0};
+  std::mutex mu;
+  std::exception_ptr failure;
+  std::vector<BuildStats> stats(static_cast<std::size_t>(threads));
+  auto worker = [&](int t) {
+    try {
+      RowWorker w(s, g, spans, tol);
+      for (;;) {
+        const std::int64_t iy = next.fetch_add(1);
+        if (iy >= g.ny) break;
+        w.run_row(iy, row_ids.data() + row_count[iy], row_count[iy + 1] - row_count[iy],
+                  out.grid.data() + iy * g.nx, row_arena[iy], row_recs[iy]);
+      }
+      stats[t] = w.st;
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!failure) failure = std::current_exception();
+      next.store(g.ny);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(worker, t);
+  worker(0);
+  for (auto& th : pool) th.join();
+  if (failure) std::rethrow_exception(failure);
+
+  std::uint64_t total = 0;
+  std::vector<std::uint64_t> base(static_cast<std::size_t>(g.ny));
+  for (std::int64_t r = 0; r < g.ny; ++r) {
+    base[r] = total;
+    total += row_arena[r].size();
+  }
+  if (total / kRecordAlign >= kRecordBit) throw RuntimeError("index arena exceeds 32 GiB");
+  // 256 B zero tail: the kernel may prefetch past a short final record
+  out.arena.assign(total + 256, 0);
+  out.arena_used = total;
+  for (std::int64_t r = 0; r < g.ny; ++r) {
+    if (!row_arena[r].empty()) {
+      std::memcpy(out.arena.data() + base[r], row_arena[r].data(), row_arena[r].size());
+    }
+    for (const auto& [ix, off] : row_recs[r]) {
+      out.grid[static_cast<std::size_t>(r * g.nx + ix)] =
+          kRecordBit | static_cast<std::uint32_t>((base[r] + static_cast<std::uint64_t>(off)) / kRecordAlign);
+    }
+    std::vector<std::uint8_t>().swap(row_arena[r]);
+  }
+  for (const auto& st : stats) {
+    out.stats.cells_empty += st.cells_empty;
+    out.stats.cells_hit += st.cells_hit;
+    out.stats.cells_boundary += st.cells_boundary;
+    out.stats.record_edges += st.record_edges;
+    out.stats.record_cands += st.record_cands;
+    out.stats.record_breaks += st.record_breaks;
+    out.stats.max_record_edges = std::max(out.stats.max_record_edges, st.max_record_edges);
+    out.stats.max_record_cands = std::max(out.stats.max_record_cands, st.max_record_cands);
+  }
+  return out;
+}
+
+}  // namespace fm

@@ -1,0 +1,303 @@
+// synth.cpp -- deterministic workload generators for the BASELINE configs.
+//
+// Not on the hot path: these build the polygon soups and the fp64 point
+// streams that the projection is benchmarked and parity-tested on.  The
+// reference's own generator (include/fastmap/synthetic.hpp:60-146) makes
+// 4-vertex quads in a fixed box and does not implement the BASELINE recipes
+// (SURVEY.md sec. 2, row 8), so the recipes are implemented here; every
+// ambiguity the survey lists (sec. 8d) is resolved in DESIGN.md sec. 3.
+//
+// Randomness is counter based (splitmix64 of (seed, stream, index)) so any
+// shard of any stream can be regenerated independently on any rank, and the
+// mapping from 64 random bits to [0,1) is the reference's own
+// (synthetic.hpp:32-34: (x >> 11) * 2^-53).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+namespace {
+
+inline std::uint64_t mix64(std::uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+inline std::uint64_t draw(std::uint64_t seed, std::uint64_t stream,
+                          std::uint64_t idx) {
+  return mix64(mix64(seed * 0x2545F4914F6CDD1Dull + stream) ^ idx);
+}
+
+inline double unit(std::uint64_t bits) {
+  return static_cast<double>(bits >> 11) * 0x1.0p-53;
+}
+
+// Box-Muller, first variate (synthetic.hpp:176-180 uses the same form)
+inline double gauss(std::uint64_t b1, std::uint64_t b2) {
+  const double u1 = 1.0 - unit(b1);  // (0, 1]
+  const double u2 = unit(b2);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+}
+inline void gauss2(std::uint64_t b1, std::uint64_t b2, double* a, double* b) {
+  const double u1 = 1.0 - unit(b1);
+  const double u2 = unit(b2);
+  const double r = std::sqrt(-2.0 * std::log(u1));
+  *a = r * std::cos(6.283185307179586 * u2);
+  *b = r * std::sin(6.283185307179586 * u2);
+}
+
+enum : std::uint64_t {
+  kStreamJitter = 1,
+  kStreamHEdge = 2,
+  kStreamVEdge = 3,
+  kStreamPoints = 16,
+  kStreamCentres = 17,
+};
+
+template <typename Fn>
+void parallel_for(std::uint64_t n, int threads, Fn fn) {
+  if (threads < 1) threads = 1;
+  if (n < 4096 || threads == 1) {
+    fn(std::uint64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const std::uint64_t per = (n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    const std::uint64_t b = std::min(n, per * t), e = std::min(n, per * (t + 1));
+    if (b < e) pool.emplace_back(fn, b, e);
+  }
+  for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+// Jittered-grid tiling (BASELINE configs 1, 2, 4).  Geometry is generated in
+// lattice units (one tile = 1 x 1) and mapped affinely onto [x0,x1]x[y0,y1]:
+//   * lattice nodes (i, j), 0<=i<=nx, 0<=j<=ny; interior nodes move by
+//     U(-jitter, +jitter) per axis; border nodes stay on the domain box;
+//   * every lattice edge is split into `segs` segments; the segs-1 interior
+//     points are displaced perpendicular to the (jittered) edge by
+//     N(0, sigma) lattice units; outer-border edges are not displaced, so the
+//     union of the tiles is exactly the domain box;
+//   * tile (i, j) has id j*nx + i (row-major) and one CCW ring: bottom edge
+//     forward, right edge up, top edge backward, left edge down; shared
+//     points are computed once and copied, so neighbours share them bitwise.
+// Outputs: vxy[2 * 4*segs*nx*ny], ring_off[nx*ny + 1], poly_ring[nx*ny + 1].
+int synth_tiling(std::uint32_t nx, std::uint32_t ny, std::uint32_t segs,
+                 double jitter, double sigma, double x0, double x1, double y0,
+                 double y1, std::uint64_t seed, int threads, double* vxy,
+                 std::uint64_t* ring_off, std::uint64_t* poly_ring) {
+  if (nx == 0 || ny == 0 || segs == 0) return 1;
+  const std::uint64_t NX = nx, NY = ny, S = segs;
+  const double cw = (x1 - x0) / static_cast<double>(nx);
+  const double ch = (y1 - y0) / static_cast<double>(ny);
+  auto map_x = [&](double u) { return x0 + u * cw; };
+  auto map_y = [&](double v) { return y0 + v * ch; };
+
+  // lattice nodes, lattice units
+  std::vector<double> lu((NX + 1) * (NY + 1)), lv((NX + 1) * (NY + 1));
+  parallel_for(NY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t j = jb; j < je; ++j) {
+      for (std::uint64_t i = 0; i <= NX; ++i) {
+        const std::uint64_t k = j * (NX + 1) + i;
+        double u = static_cast<double>(i), v = static_cast<double>(j);
+        if (i > 0 && i < NX && j > 0 && j < NY && jitter > 0.0) {
+          u += jitter * (2.0 * unit(draw(seed, kStreamJitter, 2 * k)) - 1.0);
+          v += jitter * (2.0 * unit(draw(seed, kStreamJitter, 2 * k + 1)) - 1.0);
+        }
+        lu[k] = u;
+        lv[k] = v;
+      }
+    }
+  });
+  // interior points of horizontal edges (i,j)->(i+1,j): NX*(NY+1) edges,
+  // vertical edges (i,j)->(i,j+1): (NX+1)*NY edges; S-1 points each, lon/lat
+  const std::uint64_t nh = NX * (NY + 1), nv = (NX + 1) * NY;
+  std::vector<double> hxy(2 * nh * (S - 1) + 2), vxy_e(2 * nv * (S - 1) + 2);
+  auto subdivide = [&](double au, double av, double bu, double bv, bool border,
+                       std::uint64_t stream, std::uint64_t e, double* dst) {
+    const double du = bu - au, dv = bv - av;
+    const double len = std::sqrt(du * du + dv * dv);
+    const double nu = len > 0 ? -dv / len : 0.0, nvv = len > 0 ? du / len : 0.0;
+    for (std::uint64_t k = 1; k < S; ++k) {
+      const double t = static_cast<double>(k) / static_cast<double>(S);
+      double u = au + du * t, v = av + dv * t;
+      if (!border && sigma > 0.0) {
+        const std::uint64_t idx = 2 * (e * S + k);
+        const double d = sigma * gauss(draw(seed, stream, idx), draw(seed, stream, idx + 1));
+        u += d * nu;
+        v += d * nvv;
+      }
+      dst[2 * (k - 1)] = map_x(u);
+      dst[2 * (k - 1) + 1] = map_y(v);
+    }
+  };
+  parallel_for(NY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t j = jb; j < je; ++j)
+      for (std::uint64_t i = 0; i < NX; ++i) {
+        const std::uint64_t e = j * NX + i;
+        const std::uint64_t a = j * (NX + 1) + i, b = a + 1;
+        subdivide(lu[a], lv[a], lu[b], lv[b], j == 0 || j == NY, kStreamHEdge, e,
+                  hxy.data() + 2 * e * (S - 1));
+      }
+  });
+  parallel_for(NY, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t j = jb; j < je; ++j)
+      for (std::uint64_t i = 0; i <= NX; ++i) {
+        const std::uint64_t e = j * (NX + 1) + i;
+        const std::uint64_t a = j * (NX + 1) + i, b = a + (NX + 1);
+        subdivide(lu[a], lv[a], lu[b], lv[b], i == 0 || i == NX, kStreamVEdge, e,
+                  vxy_e.data() + 2 * e * (S - 1));
+      }
+  });
+  // corner nodes in lon/lat (border nodes land exactly on x0/x1/y0/y1)
+  std::vector<double> cx((NX + 1) * (NY + 1)), cy((NX + 1) * (NY + 1));
+  for (std::uint64_t j = 0; j <= NY; ++j)
+    for (std::uint64_t i = 0; i <= NX; ++i) {
+      const std::uint64_t k = j * (NX + 1) + i;
+      cx[k] = (i == 0) ? x0 : (i == NX) ? x1 : map_x(lu[k]);
+      cy[k] = (j == 0) ? y0 : (j == NY) ? y1 : map_y(lv[k]);
+    }
+  const std::uint64_t per_poly = 4 * S;
+  parallel_for(NX * NY, threads, [&](std::uint64_t pb, std::uint64_t pe) {
+    for (std::uint64_t p = pb; p < pe; ++p) {
+      const std::uint64_t i = p % NX, j = p / NX;
+      double* out = vxy + 2 * p * per_poly;
+      std::uint64_t w = 0;
+      auto put = [&](double x, double y) {
+        out[2 * w] = x;
+        out[2 * w + 1] = y;
+        ++w;
+      };
+      const std::uint64_t c00 = j * (NX + 1) + i, c10 = c00 + 1,
+                          c01 = c00 + (NX + 1), c11 = c01 + 1;
+      const double* hb = hxy.data() + 2 * (j * NX + i) * (S - 1);        // bottom
+      const double* ht = hxy.data() + 2 * ((j + 1) * NX + i) * (S - 1);  // top
+      const double* vl = vxy_e.data() + 2 * (j * (NX + 1) + i) * (S - 1);
+      const double* vr = vxy_e.data() + 2 * (j * (NX + 1) + i + 1) * (S - 1);
+      put(cx[c00], cy[c00]);
+      for (std::uint64_t k = 0; k + 1 < S; ++k) put(hb[2 * k], hb[2 * k + 1]);
+      put(cx[c10], cy[c10]);
+      for (std::uint64_t k = 0; k + 1 < S; ++k) put(vr[2 * k], vr[2 * k + 1]);
+      put(cx[c11], cy[c11]);
+      for (std::uint64_t k = S - 1; k-- > 0;) put(ht[2 * k], ht[2 * k + 1]);
+      put(cx[c01], cy[c01]);
+      for (std::uint64_t k = S - 1; k-- > 0;) put(vl[2 * k], vl[2 * k + 1]);
+      ring_off[p] = p * per_poly;
+      poly_ring[p] = p;
+    }
+  });
+  ring_off[NX * NY] = NX * NY * per_poly;
+  poly_ring[NX * NY] = NX * NY;
+  return 0;
+}
+
+// Uniform points over box4 = {x0, x1, y0, y1}; point k of the stream is
+// global index offset + k.
+int synth_points_uniform(const double* box4, std::uint64_t n, std::uint64_t offset,
+                         std::uint64_t seed, int threads, double* out) {
+  const double w = box4[1] - box4[0], h = box4[3] - box4[2];
+  parallel_for(n, threads, [&](std::uint64_t b, std::uint64_t e) {
+    for (std::uint64_t k = b; k < e; ++k) {
+      const std::uint64_t i = offset + k;
+      out[2 * k] = box4[0] + w * unit(draw(seed, kStreamPoints, 4 * i + 2));
+      out[2 * k + 1] = box4[2] + h * unit(draw(seed, kStreamPoints, 4 * i + 3));
+    }
+  });
+  return 0;
+}
+
+// Clustered mixture (BASELINE configs 2, 3, 5): with probability
+// frac_clustered a point is centre_k + N(0, sigma^2 I) degrees, k drawn with
+// weight (k+1)^-zipf_s (k = generation order of the centres, which are
+// uniform over `domain4`); otherwise uniform over `box4`.  Points that fall
+// outside the box are kept (they project to -1), not clamped.
+int synth_points_clustered(const double* domain4, const double* box4,
+                           std::uint64_t n, std::uint64_t offset,
+                           std::uint64_t seed, std::uint32_t n_centres,
+                           double sigma, double zipf_s, double frac_clustered,
+                           int threads, double* out) {
+  if (n_centres == 0) return 1;
+  std::vector<double> cxy(2 * n_centres), cdf(n_centres);
+  double acc = 0.0;
+  for (std::uint32_t k = 0; k < n_centres; ++k) {
+    cxy[2 * k] = domain4[0] + (domain4[1] - domain4[0]) * unit(draw(seed, kStreamCentres, 2 * k));
+    cxy[2 * k + 1] = domain4[2] + (domain4[3] - domain4[2]) * unit(draw(seed, kStreamCentres, 2 * k + 1));
+    acc += std::pow(static_cast<double>(k + 1), -zipf_s);
+    cdf[k] = acc;
+  }
+  const double w = box4[1] - box4[0], h = box4[3] - box4[2];
+  parallel_for(n, threads, [&](std::uint64_t b, std::uint64_t e) {
+    for (std::uint64_t k = b; k < e; ++k) {
+      const std::uint64_t i = offset + k;
+      const double u0 = unit(draw(seed, kStreamPoints, 4 * i));
+      if (u0 < frac_clustered) {
+        const double t = unit(draw(seed, kStreamPoints, 4 * i + 1)) * acc;
+        std::uint32_t c = static_cast<std::uint32_t>(
+            std::upper_bound(cdf.begin(), cdf.end(), t) - cdf.begin());
+        if (c >= n_centres) c = n_centres - 1;
+        double gx, gy;
+        gauss2(draw(seed, kStreamPoints, 4 * i + 2), draw(seed, kStreamPoints, 4 * i + 3), &gx, &gy);
+        out[2 * k] = cxy[2 * c] + sigma * gx;
+        out[2 * k + 1] = cxy[2 * c + 1] + sigma * gy;
+      } else {
+        out[2 * k] = box4[0] + w * unit(draw(seed, kStreamPoints, 4 * i + 2));
+        out[2 * k + 1] = box4[2] + h * unit(draw(seed, kStreamPoints, 4 * i + 3));
+      }
+    }
+  });
+  return 0;
+}
+
+// Near-edge mixture (BASELINE config 4): with probability frac_near a point
+// lies on a uniformly chosen edge of a uniformly chosen polygon, displaced
+// perpendicular to it (in lattice units of cell size cw x ch) by
+// U(-eps_cells, +eps_cells); otherwise uniform over box4.
+int synth_points_near_edge(const double* vxy, const std::uint64_t* ring_off,
+                           const std::uint64_t* poly_ring, std::uint64_t n_polys,
+                           double cw, double ch, double eps_cells,
+                           double frac_near, const double* box4,
+                           std::uint64_t n, std::uint64_t offset,
+                           std::uint64_t seed, int threads, double* out) {
+  if (n_polys == 0) return 1;
+  const double w = box4[1] - box4[0], h = box4[3] - box4[2];
+  parallel_for(n, threads, [&](std::uint64_t b, std::uint64_t e) {
+    for (std::uint64_t k = b; k < e; ++k) {
+      const std::uint64_t i = offset + k;
+      const double u0 = unit(draw(seed, kStreamPoints, 4 * i));
+      if (u0 < frac_near) {
+        const std::uint64_t r1 = draw(seed, kStreamPoints, 4 * i + 1);
+        const std::uint64_t r2 = draw(seed, kStreamPoints, 4 * i + 2);
+        const std::uint64_t r3 = draw(seed, kStreamPoints, 4 * i + 3);
+        const std::uint64_t p = std::min<std::uint64_t>(
+            n_polys - 1, static_cast<std::uint64_t>(unit(r1) * n_polys));
+        const std::uint64_t r = poly_ring[p];
+        const std::uint64_t vb = ring_off[r], nvert = ring_off[r + 1] - vb;
+        const std::uint64_t ea = vb + (mix64(r1) % nvert);
+        const std::uint64_t eb = (ea + 1 < vb + nvert) ? ea + 1 : vb;
+        const double ax = vxy[2 * ea], ay = vxy[2 * ea + 1];
+        const double bx = vxy[2 * eb], by = vxy[2 * eb + 1];
+        const double t = unit(r2);
+        const double du = (bx - ax) / cw, dv = (by - ay) / ch;
+        const double len = std::sqrt(du * du + dv * dv);
+        const double d = eps_cells * (2.0 * unit(r3) - 1.0);
+        const double nu = len > 0 ? -dv / len : 0.0, nv = len > 0 ? du / len : 0.0;
+        out[2 * k] = ax + (bx - ax) * t + d * nu * cw;
+        out[2 * k + 1] = ay + (by - ay) * t + d * nv * ch;
+      } else {
+        out[2 * k] = box4[0] + w * unit(draw(seed, kStreamPoints, 4 * i + 2));
+        out[2 * k + 1] = box4[2] + h * unit(draw(seed, kStreamPoints, 4 * i + 3));
+      }
+    }
+  });
+  return 0;
+}
+
+}  // extern "C"

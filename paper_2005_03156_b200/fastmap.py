@@ -1,0 +1,377 @@
+"""Host-side mirror of the reference's projection interface, B200-backed.
+
+Names, argument meaning and error behaviour follow the reference headers
+(``/root/reference/proj/include/fastmap``) so that code written against the
+reference reads the same here:
+
+===========================================  =====================================
+reference (file:line)                        here
+===========================================  =====================================
+``PolygonGeometry`` geometry.hpp:64-87        :class:`PolygonGeometry`
+``LeafRegion`` hierarchy.hpp:67-74            :class:`LeafRegion`
+``CoverMode`` / ``CoverParams``               :class:`CoverMode` / :class:`CoverParams`
+  cell_index.hpp:246-252
+``build_cover`` cell_index.hpp:396-405        :func:`build_cover` (GPU cell index)
+``build_trie`` cell_index.hpp:453-507         :func:`build_trie` (validates F; no trie
+                                              is needed, the grid is direct-mapped)
+``query_leaves`` cell_index.hpp:527-590       :func:`query_leaves`
+``query`` cell_index.hpp:592-596              :func:`query`
+``exhaustive_assign`` synthetic.hpp:193-205   :func:`exhaustive_assign`
+``AssignmentResult`` simple_mapper.hpp:39-46  :class:`AssignmentResult`
+``index_stats`` cell_index.hpp:616-631        :func:`index_stats`
+===========================================  =====================================
+
+Exceptions: ``std::invalid_argument`` -> ``ValueError``,
+``std::runtime_error`` -> ``RuntimeError``.  The projection itself runs
+only on the GPU (``libfastmap_b200.so``); with no CUDA device the query
+calls raise ``RuntimeError`` -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+K_MAX_LEVEL = 30  # CellId::kMaxLevel, cell_index.hpp:35
+
+
+# ---------------------------------------------------------------------------
+# geometry and leaf tables
+# ---------------------------------------------------------------------------
+
+class PolygonGeometry:
+    """Multi-ring polygon as node lists (geometry.hpp:64-87)."""
+
+    def __init__(self) -> None:
+        self.rings: list[np.ndarray] = []
+
+    def add_ring(self, ring) -> None:
+        r = np.ascontiguousarray(np.asarray(ring, dtype=np.float64).reshape(-1, 2))
+        if r.shape[0] < 3:
+            raise ValueError("polygon ring needs at least 3 vertices")  # geometry.hpp:75-77
+        self.rings.append(r)
+
+    def empty(self) -> bool:
+        return not self.rings
+
+    def edge_count(self) -> int:
+        return sum(r.shape[0] for r in self.rings)
+
+
+@dataclass
+class LeafRegion:
+    """Flattened leaf record (hierarchy.hpp:67-74)."""
+    state: int = 0
+    county: int = 0
+    block: int = 0
+    geometry: Optional[PolygonGeometry] = None
+    fips12: Optional[str] = None
+
+
+@dataclass
+class Soup:
+    """Polygon soup in the C-ABI layout (include/fastmap_b200.h)."""
+    vxy: np.ndarray        # (V, 2) float64 lon, lat
+    ring_off: np.ndarray   # (R + 1,) uint64
+    poly_ring: np.ndarray  # (P + 1,) uint64
+
+    @property
+    def n_polys(self) -> int:
+        return int(self.poly_ring.shape[0] - 1)
+
+    @property
+    def n_rings(self) -> int:
+        return int(self.ring_off.shape[0] - 1)
+
+    @property
+    def n_vertices(self) -> int:
+        return int(self.vxy.shape[0])
+
+    def contiguous(self) -> "Soup":
+        return Soup(np.ascontiguousarray(self.vxy, dtype=np.float64),
+                    np.ascontiguousarray(self.ring_off, dtype=np.uint64),
+                    np.ascontiguousarray(self.poly_ring, dtype=np.uint64))
+
+    def polygon(self, p: int) -> list[np.ndarray]:
+        rings = []
+        for r in range(int(self.poly_ring[p]), int(self.poly_ring[p + 1])):
+            rings.append(self.vxy[int(self.ring_off[r]):int(self.ring_off[r + 1])])
+        return rings
+
+    @staticmethod
+    def from_rings(polys: Sequence[Sequence[Iterable]]) -> "Soup":
+        """``polys[p]`` is a list of rings; a ring is a sequence of (lon, lat)."""
+        verts, ring_off, poly_ring = [], [0], [0]
+        for rings in polys:
+            for ring in rings:
+                r = np.asarray(ring, dtype=np.float64).reshape(-1, 2)
+                verts.append(r)
+                ring_off.append(ring_off[-1] + r.shape[0])
+            poly_ring.append(len(ring_off) - 1)
+        vxy = np.concatenate(verts) if verts else np.zeros((0, 2))
+        return Soup(np.ascontiguousarray(vxy), np.asarray(ring_off, dtype=np.uint64),
+                    np.asarray(poly_ring, dtype=np.uint64))
+
+
+def leaves_to_soup(leaves: Sequence[LeafRegion]) -> Soup:
+    polys = []
+    for lf in leaves:
+        g = lf.geometry
+        polys.append([] if g is None else list(g.rings))
+    return Soup.from_rings(polys)
+
+
+# ---------------------------------------------------------------------------
+# parameters, results
+# ---------------------------------------------------------------------------
+
+class CoverMode(enum.IntEnum):
+    exact = 0
+    approx = 1
+
+
+def level_diagonal(lvl: int) -> float:
+    scale = math.ldexp(1.0, lvl)
+    return math.hypot(360.0 / scale, 180.0 / scale)  # cell_index.hpp:152-155
+
+
+@dataclass
+class CoverParams:
+    """CoverParams (cell_index.hpp:248-252) plus the grid knobs of fm_build_params.
+
+    ``max_level``/``epsilon`` are validated exactly like
+    ``validate_cover_params`` (cell_index.hpp:382-394); the GPU index is exact
+    at every max_level (its resolution is set by ``cells_per_polygon``)."""
+    max_level: int = 30
+    mode: CoverMode = CoverMode.exact
+    epsilon: float = 0.0
+    cells_per_polygon: float = 0.0
+    nx: int = 0
+    ny: int = 0
+    margin: float = 0.0
+    threads: int = 0
+
+
+def validate_cover_params(p: CoverParams) -> None:
+    if p.max_level < 0 or p.max_level > K_MAX_LEVEL:
+        raise ValueError("max_level must be in [0, 30]")
+    if p.mode == CoverMode.approx:
+        floor = level_diagonal(K_MAX_LEVEL)
+        if not (p.epsilon > 0.0) or p.epsilon < floor:
+            raise ValueError(
+                f"approx epsilon must be at least the level-30 cell diagonal ({floor:f} degrees)")
+
+
+@dataclass
+class AssignCounters:
+    pip_point_evaluations: int = 0  # simple_mapper.hpp:26-35
+    pip_calls: int = 0
+
+
+@dataclass
+class AssignmentResult:
+    """Per-point (state, county, block), -1 when unresolved (simple_mapper.hpp:39-46)."""
+    state: np.ndarray
+    county: np.ndarray
+    block: np.ndarray
+    counters: AssignCounters = field(default_factory=AssignCounters)
+    leaf: Optional[np.ndarray] = None  # leaf id per point (collect_leaves position)
+
+    def size(self) -> int:
+        return int(self.state.shape[0])
+
+
+# ---------------------------------------------------------------------------
+# the GPU index
+# ---------------------------------------------------------------------------
+
+class CellIndex:
+    """Owner of an ``fm_index*`` (the analogue of CellCover + TrieIndex)."""
+
+    def __init__(self, handle: C.c_void_p, n_leaves: int, params: CoverParams,
+                 device: int) -> None:
+        self._h = handle
+        self.n_leaves = n_leaves
+        self.params = params
+        self.device = device
+        self.levels_per_node = 1
+
+    def __del__(self) -> None:
+        self.close()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.lib().fm_index_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if not self._h:
+            raise ValueError("index is closed")
+        return self._h
+
+    def stats(self) -> dict:
+        s = N.IndexStats()
+        N.check(N.lib().fm_index_stats_get(self.handle, C.byref(s)), "fm_index_stats_get")
+        return s.as_dict()
+
+    def export(self):
+        """(grid u32[ny*nx], arena u8[], geometry dict) -- host copies."""
+        L = N.lib()
+        gl, al = C.c_uint64(0), C.c_uint64(0)
+        geo = np.zeros(12, dtype=np.float64)
+        N.check(L.fm_index_export(self.handle, None, C.byref(gl), None, C.byref(al),
+                                  N.ptr(geo, C.c_double)), "fm_index_export")
+        grid = np.zeros(gl.value, dtype=np.uint32)
+        arena = np.zeros(al.value, dtype=np.uint8)
+        N.check(L.fm_index_export(self.handle, N.ptr(grid, C.c_uint32), C.byref(gl),
+                                  N.ptr(arena, C.c_uint8), C.byref(al), N.ptr(geo, C.c_double)),
+                "fm_index_export")
+        keys = ("gx0", "gx1", "gy0", "gy1", "w", "h", "inv_w", "inv_h", "nx", "ny",
+                "margin", "n_polys")
+        g = dict(zip(keys, geo.tolist()))
+        g["nx"] = int(g["nx"])
+        g["ny"] = int(g["ny"])
+        g["n_polys"] = int(g["n_polys"])
+        return grid, arena, g
+
+    # -- projection ---------------------------------------------------------
+    def project(self, points, out=None, hist=None, counters=None, stream=None):
+        """Leaf id per point.
+
+        ``points``: a CUDA ``torch.Tensor`` (n, 2) float64 on the index's device
+        (asynchronous, on ``stream`` or the current torch stream), or a numpy
+        (n, 2) float64 array (host path: pipelined copies; synchronous).
+        ``hist``: optional int64 per-leaf counters, accumulated into.
+        """
+        L = N.lib()
+        if isinstance(points, np.ndarray):
+            pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+            n = pts.shape[0]
+            if out is None:
+                out = np.empty(n, dtype=np.int32)
+            hp = None
+            if hist is not None:
+                assert hist.dtype == np.int64 and hist.flags.c_contiguous
+                hp = N.ptr(hist, C.c_int64)
+            N.check(L.fm_query_host(self.handle, N.ptr(pts, C.c_double), n,
+                                    N.ptr(out, C.c_int32), hp), "fm_query_host")
+            return out
+        import torch  # device path
+        if not (isinstance(points, torch.Tensor) and points.is_cuda):
+            raise TypeError("points must be a numpy array or a CUDA torch tensor")
+        if points.dtype != torch.float64 or not points.is_contiguous():
+            raise ValueError("device points must be contiguous float64 (n, 2)")
+        n = points.numel() // 2
+        if out is None:
+            out = torch.empty(n, dtype=torch.int32, device=points.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(points.device).cuda_stream
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        N.check(L.fm_query(self.handle, C.c_void_p(points.data_ptr()), n,
+                           C.c_void_p(out.data_ptr()),
+                           C.c_void_p(hist.data_ptr()) if hist is not None else None,
+                           C.c_void_p(counters.data_ptr()) if counters is not None else None,
+                           C.c_void_p(stream)), "fm_query")
+        return out
+
+
+def build_index(soup: Soup, params: Optional[CoverParams] = None, device: int = 0) -> CellIndex:
+    """fm_index_build over a soup.  ``device=-1`` builds a host-only index
+    (inspection/export only; queries on it raise)."""
+    params = params or CoverParams()
+    validate_cover_params(params)
+    s = soup.contiguous()
+    bp = N.BuildParams(cells_per_polygon=float(params.cells_per_polygon),
+                       nx=int(params.nx), ny=int(params.ny), margin=float(params.margin),
+                       device=int(device), build_on_gpu=1 if device >= 0 else 0,
+                       threads=int(params.threads))
+    h = C.c_void_p()
+    st = N.lib().fm_index_build(N.ptr(s.vxy, C.c_double), N.ptr(s.ring_off, C.c_uint64),
+                                s.n_rings, N.ptr(s.poly_ring, C.c_uint64), s.n_polys,
+                                C.byref(bp), C.byref(h))
+    N.check(st, "fm_index_build")
+    return CellIndex(h, s.n_polys, params, device)
+
+
+def build_cover(leaves, params: Optional[CoverParams] = None, device: int = 0) -> CellIndex:
+    """build_cover(leaves, params) (cell_index.hpp:396-405) -> GPU cell index.
+
+    ``leaves`` is a sequence of :class:`LeafRegion` or a :class:`Soup`."""
+    soup = leaves if isinstance(leaves, Soup) else leaves_to_soup(leaves)
+    return build_index(soup, params, device)
+
+
+class TrieIndex:
+    """What build_trie returns: the index plus the requested fanout.  The
+    grid is direct-mapped, so lookups take one probe for any F."""
+
+    def __init__(self, cover: CellIndex, levels_per_node: int) -> None:
+        self.cover = cover
+        self.levels_per_node = levels_per_node
+        self.fanout = 1 << (2 * levels_per_node)
+
+
+def build_trie(cover: CellIndex, levels_per_node: int) -> TrieIndex:
+    if levels_per_node not in (1, 2, 4):  # cell_index.hpp:454-456
+        raise ValueError("trie fanout must be 1, 2 or 4 levels per node")
+    return TrieIndex(cover, levels_per_node)
+
+
+def _leaf_table(leaves) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    if isinstance(leaves, Soup):
+        n = leaves.n_polys
+        return (np.zeros(n, np.int32), np.zeros(n, np.int32), np.arange(n, dtype=np.int32))
+    st = np.fromiter((lf.state for lf in leaves), dtype=np.int32, count=len(leaves))
+    co = np.fromiter((lf.county for lf in leaves), dtype=np.int32, count=len(leaves))
+    bl = np.fromiter((lf.block for lf in leaves), dtype=np.int32, count=len(leaves))
+    return st, co, bl
+
+
+def query_leaves(trie, leaves, points, mode: CoverMode = CoverMode.exact) -> AssignmentResult:
+    """query_leaves (cell_index.hpp:527-590): leaf id -> (state, county, block)
+    exactly as set_leaf does (cell_index.hpp:515-519)."""
+    cover = trie.cover if isinstance(trie, TrieIndex) else trie
+    if mode == CoverMode.approx and cover.params.mode != CoverMode.approx:
+        raise ValueError("approximate queries require an approximate-mode cover")
+    if mode == CoverMode.approx:
+        raise NotImplementedError("fast-approx mode is not built yet (SURVEY.md sec. 8f item 1)")
+    n_leaves = leaves.n_polys if isinstance(leaves, Soup) else len(leaves)
+    if cover.n_leaves != n_leaves:
+        raise ValueError("cover was built for a different hierarchy")
+    ids = cover.project(points)
+    if not isinstance(ids, np.ndarray):
+        ids = ids.cpu().numpy()
+    st, co, bl = _leaf_table(leaves)
+    hit = ids >= 0
+    res = AssignmentResult(state=np.where(hit, st[np.maximum(ids, 0)], -1).astype(np.int32),
+                           county=np.where(hit, co[np.maximum(ids, 0)], -1).astype(np.int32),
+                           block=np.where(hit, bl[np.maximum(ids, 0)], -1).astype(np.int32),
+                           leaf=ids)
+    return res
+
+
+def query(trie, leaves, points, mode: CoverMode = CoverMode.exact) -> AssignmentResult:
+    return query_leaves(trie, leaves, points, mode)
+
+
+def exhaustive_assign(leaves, points, device: int = 0) -> np.ndarray:
+    """exhaustive_assign semantics (synthetic.hpp:193-205), computed on the GPU."""
+    idx = build_cover(leaves, CoverParams(), device)
+    try:
+        ids = idx.project(points)
+        return ids if isinstance(ids, np.ndarray) else ids.cpu().numpy()
+    finally:
+        idx.close()
+
+
+def index_stats(trie, cover=None) -> dict:
+    c = trie.cover if isinstance(trie, TrieIndex) else trie
+    return c.stats()

@@ -1,0 +1,124 @@
+"""The BASELINE.json workload configs as deterministic generators.
+
+Every config is a polygon tiling of the domain lon [-125, -66] x lat [24, 50]
+plus a seeded fp64 point stream.  Generation runs in the native
+``libfastmap_synth.so`` (counter-based RNG, so any shard of the stream is
+reproducible on any rank).  Recipe choices for what BASELINE leaves open are
+documented in DESIGN.md sec. 3.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .fastmap import Soup
+
+DOMAIN = (-125.0, -66.0, 24.0, 50.0)  # x0, x1, y0, y1
+
+
+def expanded_box(domain=DOMAIN, frac: float = 0.01):
+    """The domain bbox scaled by (1 + frac) about its centre (0.5% per side)."""
+    x0, x1, y0, y1 = domain
+    dx, dy = 0.5 * frac * (x1 - x0), 0.5 * frac * (y1 - y0)
+    return (x0 - dx, x1 + dx, y0 - dy, y1 + dy)
+
+
+def _threads() -> int:
+    return max(1, min(64, os.cpu_count() or 1))
+
+
+@dataclass(frozen=True)
+class TilingConfig:
+    name: str
+    nx: int
+    ny: int
+    segs: int
+    jitter: float
+    sigma: float
+    n_points: int
+    points: str                 # "uniform" | "clustered" | "near_edge"
+    seed: int = 0
+    n_centres: int = 2000
+    centre_sigma_deg: float = 0.2
+    zipf_s: float = 1.1
+    frac_clustered: float = 0.9
+    frac_near: float = 0.5
+    near_eps_cells: float = 1e-4
+
+    @property
+    def n_polys(self) -> int:
+        return self.nx * self.ny
+
+    @property
+    def cell_size(self):
+        x0, x1, y0, y1 = DOMAIN
+        return ((x1 - x0) / self.nx, (y1 - y0) / self.ny)
+
+    def make_soup(self, threads: Optional[int] = None) -> Soup:
+        P = self.nx * self.ny
+        V = P * 4 * self.segs
+        vxy = np.empty((V, 2), dtype=np.float64)
+        ring_off = np.empty(P + 1, dtype=np.uint64)
+        poly_ring = np.empty(P + 1, dtype=np.uint64)
+        x0, x1, y0, y1 = DOMAIN
+        rc = N.synth().synth_tiling(self.nx, self.ny, self.segs, self.jitter, self.sigma,
+                                    x0, x1, y0, y1, self.seed, threads or _threads(),
+                                    N.ptr(vxy, C.c_double), N.ptr(ring_off, C.c_uint64),
+                                    N.ptr(poly_ring, C.c_uint64))
+        if rc != 0:
+            raise ValueError("synth_tiling failed")
+        return Soup(vxy, ring_off, poly_ring)
+
+    def make_points(self, n: Optional[int] = None, offset: int = 0,
+                    soup: Optional[Soup] = None, threads: Optional[int] = None,
+                    out: Optional[np.ndarray] = None) -> np.ndarray:
+        n = self.n_points if n is None else int(n)
+        pts = out if out is not None else np.empty((n, 2), dtype=np.float64)
+        assert pts.dtype == np.float64 and pts.flags.c_contiguous and pts.shape == (n, 2)
+        box = np.asarray(expanded_box(), dtype=np.float64)
+        dom = np.asarray(DOMAIN, dtype=np.float64)
+        t = threads or _threads()
+        L = N.synth()
+        if self.points == "uniform":
+            rc = L.synth_points_uniform(N.ptr(box, C.c_double), n, offset, self.seed + 1, t,
+                                        N.ptr(pts, C.c_double))
+        elif self.points == "clustered":
+            rc = L.synth_points_clustered(N.ptr(dom, C.c_double), N.ptr(box, C.c_double), n,
+                                          offset, self.seed + 1, self.n_centres,
+                                          self.centre_sigma_deg, self.zipf_s,
+                                          self.frac_clustered, t, N.ptr(pts, C.c_double))
+        elif self.points == "near_edge":
+            s = (soup or self.make_soup()).contiguous()
+            cw, ch = self.cell_size
+            rc = L.synth_points_near_edge(N.ptr(s.vxy, C.c_double), N.ptr(s.ring_off, C.c_uint64),
+                                          N.ptr(s.poly_ring, C.c_uint64), s.n_polys, cw, ch,
+                                          self.near_eps_cells, self.frac_near,
+                                          N.ptr(box, C.c_double), n, offset, self.seed + 1, t,
+                                          N.ptr(pts, C.c_double))
+        else:
+            raise ValueError(self.points)
+        if rc != 0:
+            raise ValueError("point generation failed")
+        return pts
+
+
+CONFIGS = {
+    # BASELINE configs[0]: small CPU-runnable case
+    "c1": TilingConfig("c1", 32, 32, 8, 0.3, 0.05, 1_000_000, "uniform"),
+    # configs[1]: census block-group scale, clustered points (bench workload)
+    "c2": TilingConfig("c2", 500, 500, 12, 0.3, 0.05, 100_000_000, "clustered"),
+    # configs[3]: strongly concave blocks, half the points near an edge
+    "c4": TilingConfig("c4", 400, 250, 50, 0.3, 0.15, 200_000_000, "near_edge"),
+}
+
+
+def config(name: str) -> TilingConfig:
+    try:
+        return CONFIGS[name]
+    except KeyError:
+        raise ValueError(f"unknown config {name!r}; have {sorted(CONFIGS)}") from None
