@@ -1,0 +1,351 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 point-to-block projection (BASELINE.json metric:
+points projected/sec, device-timed, plus % of roofline, next to the
+reference CPU path).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+  python bench.py --impl reference ...      # the reference's CPU path
+
+One step = one projection pass (fm_query, one kernel launch) over this
+rank's resident point shard.  Under torchrun each rank owns a contiguous
+shard of the global point stream (weak scaling: per-GPU work is fixed) and
+its own replica of the index; the only collective is the optional per-block
+histogram reduce (--hist).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "points projected/sec (device-timed)"
+UNIT = "points/s"
+
+WORKLOADS = {
+    "c1": "c1: 1,024-polygon 32x32 jittered tiling (8 segs/edge, ~32 v), 1M uniform fp64 points",
+    "c2": "c2: 250,000-polygon 500x500 jittered tiling (12 segs/edge, ~48 v), "
+          "100M clustered fp64 points (2000 Zipf(1.1) centres, sigma 0.2 deg, 10% uniform)",
+    "c4": "c4: 100,000-polygon 400x250 jittered tiling (50 segs/edge, sigma 0.15, ~200 v), "
+          "200M fp64 points (50% uniform, 50% within 1e-4 cell of an edge)",
+}
+# reference cover depth for the CPU arm (SURVEY.md sec. 6 probes: best per config)
+REF_MAX_LEVEL = {"c1": 12, "c2": 16, "c4": 16}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--points", type=int, default=0, help="points per GPU (default: config size)")
+    ap.add_argument("--hist", action="store_true", help="also build the per-block int64 histogram")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=3.0,
+                    help="target seconds per CPU reference pass (bounded sample)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), f[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for _, _, r in rows for k in range(4) if r[k] == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_reference_leg(cfg_name, soup, pts_host, threads, target_s, repeats=3, warmup=1):
+    """Time the reference CPU path (oracle/_ref: query_leaves via run_chunked,
+    F=4) on a bounded prefix of this rank's points.  Returns a dict."""
+    import oracle
+    cores = threads or (os.cpu_count() or 1)
+    if oracle.ref_available():
+        m = oracle.RefModel(soup)
+        bi = m.build_index(REF_MAX_LEVEL[cfg_name], 4)
+        probe = pts_host[: min(len(pts_host), 500_000)]
+        _, t = m.query_leaves(probe, threads=cores, want_ids=False)
+        rate = len(probe) / max(t["seconds"], 1e-9)
+        n = int(min(len(pts_host), max(len(probe), rate * target_s)))
+        sample = np.ascontiguousarray(pts_host[:n])
+        for _ in range(warmup):
+            m.query_leaves(sample, threads=cores, want_ids=False)
+        times = []
+        for _ in range(repeats):
+            _, t = m.query_leaves(sample, threads=cores, want_ids=False)
+            times.append(t["seconds"])
+        best = min(times)
+        return {"value": n / best, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"first {n} points of this config's stream; reference "
+                          f"query_leaves(exact) via run_chunked, cover max_level "
+                          f"{REF_MAX_LEVEL[cfg_name]}, trie F=4; best of {repeats} after "
+                          f"{warmup} warm-up (bench.hpp:82-94); cover build "
+                          f"{bi['seconds']:.1f} s not counted",
+                "times_s": times, "n": n}
+    # oracle port (bucketed exhaustive_assign restatement) when _ref is absent
+    probe = pts_host[: min(len(pts_host), 200_000)]
+    t0 = time.perf_counter()
+    oracle.assign(soup, probe, threads=cores)
+    rate = len(probe) / max(time.perf_counter() - t0, 1e-9)
+    n = int(min(len(pts_host), max(len(probe), rate * target_s)))
+    sample = np.ascontiguousarray(pts_host[:n])
+    times = []
+    for _ in range(warmup + repeats):
+        t0 = time.perf_counter()
+        oracle.assign(soup, sample, threads=cores)
+        times.append(time.perf_counter() - t0)
+    best = min(times[warmup:])
+    return {"value": n / best, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"first {n} points; oracle/oracle.c bucketed exhaustive_assign "
+                      f"restatement (oracle/_ref absent)", "times_s": times[warmup:], "n": n}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2005_03156_b200 import synth
+    cfg = synth.config(args.config)
+    soup = cfg.make_soup()
+    n_total = args.points or cfg.n_points
+    # a bounded prefix of the stream is generated: the CPU arm times a sample
+    probe_n = min(n_total, 20_000_000)
+    pts = cfg.make_points(probe_n, soup=soup)
+    leg = cpu_reference_leg(args.config, soup, pts, 0, args.cpu_seconds,
+                            repeats=max(1, args.steps), warmup=max(1, args.warmup))
+    step_s = statistics.mean(leg["times_s"])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": leg["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": len(leg["times_s"]), "warmup": max(1, args.warmup),
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "sample_points": leg["n"],
+                   "parallelism": "host threads (run_chunked)"},
+        "cpu_baseline": {k: leg[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": leg["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_03156_b200 import fastmap, synth
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+
+    cfg = synth.config(args.config)
+    soup = cfg.make_soup()
+    n = args.points or cfg.n_points
+    offset = rank * n  # contiguous shard of the global stream
+    pts_host = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    cfg.make_points(n, offset=offset, soup=soup, out=pts_host.numpy())
+
+    t0 = time.perf_counter()
+    idx = fastmap.build_index(soup, fastmap.CoverParams(), device=local)
+    build_s = time.perf_counter() - t0
+    st = idx.stats()
+
+    d_pts = pts_host.to(dev, non_blocking=False)
+    d_out = torch.empty(n, dtype=torch.int32, device=dev)
+    d_hist = torch.zeros(soup.n_polys, dtype=torch.int64, device=dev) if args.hist else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        idx.project(d_pts, out=d_out, hist=d_hist, stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        if d_hist is not None and world > 1:
+            dist.all_reduce(d_hist)  # the one collective: per-block counts over NVLink
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = n * world * args.steps / (ms_max / 1e3)
+    launch_ms = ms / args.steps
+
+    # correctness spot check of the timed output against the oracle (rank-local)
+    import oracle
+    chk = np.random.default_rng(rank).choice(n, size=min(n, 20_000), replace=False)
+    got = d_out.cpu().numpy()[chk]
+    want = oracle.assign(soup, pts_host.numpy()[chk])
+    mismatches = int((got != want).sum())
+
+    # e2e: the public host-buffer API (fm_query_host), copies inside the region
+    e2e = None
+    if not args.no_e2e:
+        out_host = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        ph, oh = pts_host.numpy(), out_host.numpy()
+        hist_h = np.zeros(soup.n_polys, dtype=np.int64) if args.hist else None
+        idx.project(ph, out=oh, hist=hist_h)  # warm (allocates staging)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            idx.project(ph, out=oh, hist=hist_h)
+        el = time.perf_counter() - t0
+        tt = torch.tensor([el], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * world * args.e2e_steps / float(tt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 4 * n,
+               "path": "fm_query_host (pinned host buffers, 3-stream chunked H2D/kernel/D2H)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        leg = cpu_reference_leg(args.config, soup, pts_host.numpy(), 0, args.cpu_seconds)
+        cpu = {k: leg[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    peak, peak_kind = measured_peaks()
+    alg_bytes = 20.0 * n + 16.0 * soup.n_vertices  # SURVEY.md sec. 8d per-point + index once
+    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_{args.config}_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except (ValueError, OSError):
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE recipe; see DESIGN.md sec. 3)",
+            "config": {
+                "workload": WORKLOADS[args.config], "points_per_gpu": n,
+                "global_points": n * world, "polygons": soup.n_polys,
+                "vertices": soup.n_vertices, "histogram": bool(args.hist),
+                "parallelism": f"point shards x{world}, index replicated",
+                "l2": "inputs larger than L2 (16 B/pt stream), no flush",
+                "index": {k: st[k] for k in ("nx", "ny", "cells_hit", "cells_boundary",
+                                             "grid_bytes", "arena_bytes")},
+                "index_build_s": build_s,
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_kind,
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel": "project_kernel", "launch_ms": launch_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "parity": {"checked_points": int(len(chk)), "mismatches_vs_oracle": mismatches},
+        }
+        print(json.dumps(line), flush=True)
+    idx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if mismatches == 0 else 3
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

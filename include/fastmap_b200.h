@@ -146,9 +146,11 @@ fm_status fm_query_host(const fm_index* index, const double* h_lonlat, uint64_t 
                         int32_t* h_out, int64_t* h_hist);
 
 /* Copy of the index arrays to host memory (the FMCI-save analogue,
- * cell_index.hpp:641-664).  Two-call protocol: null buffers -> sizes. */
+ * cell_index.hpp:641-664).  Two-call protocol: null buffers -> sizes.
+ * geometry16 (nullable) receives gx0, gx1, gy0, gy1, cell_w, cell_h, inv_w,
+ * inv_h, nx, ny, margin, n_polys, granule, 0, 0, 0. */
 fm_status fm_index_export(const fm_index* index, uint32_t* grid, uint64_t* grid_len,
-                          uint8_t* arena, uint64_t* arena_len, double* geometry12);
+                          uint8_t* arena, uint64_t* arena_len, double* geometry16);
 
 /* Device the index lives on. */
 int fm_index_device(const fm_index* index);

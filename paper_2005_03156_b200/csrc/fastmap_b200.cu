@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -34,7 +35,6 @@ fm_status set_err(fm_status s, const std::string& msg) {
 }
 
 constexpr int kBlock = 256;
-constexpr int kUnroll = 4;
 constexpr int kStreams = 3;
 constexpr std::uint64_t kChunkPoints = std::uint64_t{1} << 23;  // 8M points = 128 MiB
 
@@ -58,54 +58,217 @@ struct DeviceGuard {
     }                                                                        \
   } while (0)
 
+// Kernel configuration.  kWarps warps per CTA; each warp streams tiles of
+// 32*kU points.  Points in boundary cells are parked in a per-warp
+// shared-memory queue and resolved up to 32 at a time with all lanes busy:
+// the batch's records (their sizes come from the grid entries) are copied
+// into a per-warp shared pool by cooperative cp.async -- half a warp per
+// record, so one instruction moves two records -- in a single round trip,
+// then each lane evaluates its own record from shared memory.  A point in
+// a split cell is re-queued with the child's entry.
+constexpr int kWarps = 8;
+constexpr int kU = 2;
+constexpr int kQCap = 32 * kU + 32;
+constexpr int kPool = 4096;  // bytes of record staging per warp
+
+struct WarpSmem {
+  double qx[kQCap];
+  double qy[kQCap];
+  unsigned long long qi[kQCap];
+  std::uint32_t qe[kQCap];
+  std::uint32_t bstart[32];  // pool offset (16-byte chunks) per batch slot
+  std::uint32_t bsize[32];   // chunks per batch slot
+  alignas(16) std::uint8_t pool[kPool];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <bool kHist>
+__device__ __forceinline__ void emit(int* __restrict__ out, unsigned long long* __restrict__ hist,
+                                     std::uint64_t i, int id) {
+  __stcs(out + i, id);
+  if (kHist && id >= 0) atomicAdd(hist + id, 1ull);
+}
+
+constexpr int kRequeue = INT_MIN;
+
+// Resolve the batch S.q*[k0 .. k0+cnt-1] (cnt <= 32; lane l owns item
+// k0 + l).  Returns the leaf id, -1, or kRequeue with *next_e set.
+template <bool kCount>
+__device__ __forceinline__ int resolve_batch(const fm::KParams& P, WarpSmem& S, int lane,
+                                             int k0, int cnt, std::uint32_t* next_e,
+                                             fm::WorkCount& wc) {
+  const bool mine = lane < cnt;
+  const std::uint32_t e = mine ? S.qe[k0 + lane] : 0u;
+  const std::uint32_t chunks = mine ? fm::entry_fetch_bytes(e) / 16 : 0u;
+  // exclusive scan of chunk counts -> pool layout
+  std::uint32_t incl = chunks;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const std::uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const std::uint32_t start = incl - chunks;
+  S.bstart[lane] = start;
+  S.bsize[lane] = chunks;
+  __syncwarp();
+  // cooperative copy: iteration m moves slots 2m (lanes 0-15) and 2m+1 (16-31)
+  const int half = lane >> 4, c = lane & 15;
+  for (int m = 0; 2 * m < cnt; ++m) {
+    const int slot = 2 * m + half;
+    if (slot < cnt && static_cast<std::uint32_t>(c) < S.bsize[slot]) {
+      const std::uint8_t* rec = fm::record_ptr(P, S.qe[k0 + slot]);
+      cp_async16(S.pool + 16 * (S.bstart[slot] + c), rec + 16 * c);
+    }
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  if (!mine) return -1;
+  const double px = S.qx[k0 + lane], py = S.qy[k0 + lane];
+  const fm::SmemReader W{S.pool + 16 * start};
+  const std::uint32_t h = W.u32(0);
+  const std::uint32_t kind = h & 0xFFu;
+  if (kind == fm::kKindSplit) {
+    const double x0 = W.f64(8), y0 = W.f64(16), ihw = W.f64(24), ihh = W.f64(32);
+    int i = static_cast<int>(__dmul_rn(__dsub_rn(px, x0), ihw));
+    int j = static_cast<int>(__dmul_rn(__dsub_rn(py, y0), ihh));
+    i = min(max(i, 0), 1);
+    j = min(max(j, 0), 1);
+    const std::uint32_t ce = W.u32(40 + 4 * (2 * j + i));
+    if (ce == fm::kEmpty) return -1;
+    if (ce < fm::kRecordBit) return static_cast<int>(ce);
+    *next_e = ce;
+    return kRequeue;
+  }
+  if (kCount) wc.boundary++;
+  if (kind == fm::kKindCompact) {
+    const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
+    if (fm::compact_bytes(nv, nc, nb) <= 16u * chunks) {
+      return fm::resolve_compact<kCount>(W, h, px, py, wc);
+    }
+    return fm::resolve_compact<kCount>(fm::GlobalReader{fm::record_ptr(P, e)}, h, px, py, wc);
+  }
+  return fm::resolve_wide<kCount>(fm::record_ptr(P, e), px, py, wc);
+}
+
+// Pop up to 32 items off the top of the queue (as many as the pool holds),
+// resolve them, emit the finished ones and push split descents back.
 template <bool kHist, bool kCount>
-__global__ void __launch_bounds__(kBlock)
+__device__ __forceinline__ void drain_once(const fm::KParams& P, WarpSmem& S, int lane, int& qn,
+                                           int* __restrict__ out,
+                                           unsigned long long* __restrict__ hist,
+                                           fm::WorkCount& wc) {
+  const int cnt = min(qn, 32);
+  // the batch is the top `take` items, as many as fit the pool (items are at
+  // most 256 bytes, so at least 16 always fit): scan sizes from the top
+  const std::uint32_t bytes = lane < cnt ? fm::entry_fetch_bytes(S.qe[qn - 1 - lane]) : 0u;
+  std::uint32_t incl = bytes;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const std::uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int take = __popc(__ballot_sync(0xFFFFFFFFu, lane < cnt && incl <= kPool));
+  const int b0 = qn - take;
+  const double px = lane < take ? S.qx[b0 + lane] : 0.0;
+  const double py = lane < take ? S.qy[b0 + lane] : 0.0;
+  const std::uint64_t i = lane < take ? S.qi[b0 + lane] : 0ull;
+  std::uint32_t ne = 0;
+  const int id = resolve_batch<kCount>(P, S, lane, b0, take, &ne, wc);
+  __syncwarp();
+  qn = b0;
+  const bool requeue = lane < take && id == kRequeue;
+  if (lane < take && !requeue) emit<kHist>(out, hist, i, id);
+  const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, requeue);
+  if (requeue) {
+    const int pos = qn + __popc(b & ((1u << lane) - 1u));
+    S.qx[pos] = px;
+    S.qy[pos] = py;
+    S.qi[pos] = i;
+    S.qe[pos] = ne;
+  }
+  qn += __popc(b);
+  __syncwarp();
+}
+
+template <bool kHist, bool kCount>
+__global__ void __launch_bounds__(kWarps * 32)
     project_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
                    int* __restrict__ out, unsigned long long* __restrict__ hist,
                    unsigned long long* __restrict__ counters) {
-  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  extern __shared__ __align__(16) unsigned char dsmem[];
+  WarpSmem* smem = reinterpret_cast<WarpSmem*>(dsmem);
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  WarpSmem& S = smem[wid];
+  const std::uint32_t lt_mask = (1u << lane) - 1u;
+  const std::uint64_t tile = 32ull * kU;
+  const std::uint64_t n_tiles = (n + tile - 1) / tile;
+  const std::uint64_t gwarp = static_cast<std::uint64_t>(blockIdx.x) * kWarps + wid;
+  const std::uint64_t nwarps = static_cast<std::uint64_t>(gridDim.x) * kWarps;
   fm::WorkCount wc;
   unsigned long long n_done = 0;
-  for (std::uint64_t i0 = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-       i0 < n; i0 += stride * kUnroll) {
-    double2 p[kUnroll];
-    std::uint32_t e[kUnroll];
+  int qn = 0;
+  double2 pn[kU];  // next tile's points, loaded one tile ahead
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const std::uint64_t i = i0 + u * stride;
-      p[u] = (i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) e[u] = fm::locate(P, p[u].x, p[u].y);
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const std::uint64_t i = i0 + u * stride;
-      if (i < n) {
-        int id;
-        if (e[u] < fm::kRecordBit) {
-          id = static_cast<int>(e[u]);
-        } else if (e[u] == fm::kEmpty) {
-          id = -1;
-        } else {
-          id = fm::resolve_record<kCount>(P.arena, e[u], p[u].x, p[u].y, wc);
-        }
-        __stcs(out + i, id);
-        if (kHist && id >= 0) atomicAdd(hist + id, 1ull);
-        if (kCount) ++n_done;
-      }
-    }
+  for (int u = 0; u < kU; ++u) {
+    const std::uint64_t i = gwarp * tile + u * 32 + lane;
+    pn[u] = (gwarp < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
   }
+  for (std::uint64_t t = gwarp; t < n_tiles; t += nwarps) {
+    const std::uint64_t base = t * tile;
+    double2 p[kU];
+    std::uint32_t e[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) p[u] = pn[u];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) e[u] = fm::locate(P, p[u].x, p[u].y);
+    const std::uint64_t tn = t + nwarps;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const std::uint64_t i = tn * tile + u * 32 + lane;
+      pn[u] = (tn < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const std::uint64_t i = base + u * 32 + lane;
+      const bool valid = i < n;
+      const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
+      if (valid && !is_rec) emit<kHist>(out, hist, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
+      if (kCount && valid) ++n_done;
+      const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec);
+      if (is_rec) {
+        const int pos = qn + __popc(b & lt_mask);
+        S.qx[pos] = p[u].x;
+        S.qy[pos] = p[u].y;
+        S.qi[pos] = i;
+        S.qe[pos] = e[u];
+      }
+      qn += __popc(b);
+    }
+    __syncwarp();
+    while (qn >= 32) drain_once<kHist, kCount>(P, S, lane, qn, out, hist, wc);
+  }
+  while (qn > 0) drain_once<kHist, kCount>(P, S, lane, qn, out, hist, wc);
   if (kCount) {
     unsigned long long v[4] = {n_done, wc.boundary, wc.cands, wc.edges};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xFFFFFFFFu, v[k], o);
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
       for (int k = 0; k < 4; ++k) atomicAdd(counters + k, v[k]);
     }
   }
 }
+
+constexpr int kSmemBytes = static_cast<int>(sizeof(WarpSmem)) * kWarps;
 
 int grid_size_for(int device, std::uint64_t n, const void* kernel) {
   // resident CTAs per SM x SM count, cached per (device, kernel)
@@ -125,13 +288,14 @@ int grid_size_for(int device, std::uint64_t n, const void* kernel) {
     if (blocks == 0) {
       int sms = 0, per_sm = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0);
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, kSmemBytes);
       blocks = std::max(1, sms) * std::max(1, per_sm);
       cache.push_back({device, kernel, blocks});
     }
   }
-  const std::uint64_t need = (n + static_cast<std::uint64_t>(kBlock) * kUnroll - 1) /
-                             (static_cast<std::uint64_t>(kBlock) * kUnroll);
+  const std::uint64_t per_cta = static_cast<std::uint64_t>(kBlock) * kU;
+  const std::uint64_t need = (n + per_cta - 1) / per_cta;
   return static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(need, blocks)));
 }
 
@@ -143,7 +307,7 @@ struct fm_index {
   double ax0 = 0, ax1 = 0, ay0 = 0, ay1 = 0;
   std::uint32_t* d_grid = nullptr;
   std::uint8_t* d_arena = nullptr;
-  std::uint64_t grid_len = 0, arena_len = 0;
+  std::uint64_t grid_len = 0, arena_len = 0, granule = 16;
   fm::HostIndex host;  // retained only for host-only (device < 0) indexes
   fm_index_stats stats{};
   // fm_query_host staging
@@ -171,6 +335,7 @@ fm::KParams kparams(const fm_index* ix) {
   P.ay1 = ix->ay1;
   P.nx = static_cast<int>(ix->g.nx);
   P.ny = static_cast<int>(ix->g.ny);
+  P.granule = ix->granule;
   return P;
 }
 
@@ -181,16 +346,16 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
   const double2* pts = reinterpret_cast<const double2*>(d_pts);
   if (d_hist && d_counters) {
     auto k = project_kernel<true, true>;
-    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, 0, stream>>>(P, pts, n, d_out, d_hist, d_counters);
+    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, kSmemBytes, stream>>>(P, pts, n, d_out, d_hist, d_counters);
   } else if (d_hist) {
     auto k = project_kernel<true, false>;
-    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, 0, stream>>>(P, pts, n, d_out, d_hist, d_counters);
+    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, kSmemBytes, stream>>>(P, pts, n, d_out, d_hist, d_counters);
   } else if (d_counters) {
     auto k = project_kernel<false, true>;
-    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, 0, stream>>>(P, pts, n, d_out, d_hist, d_counters);
+    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, kSmemBytes, stream>>>(P, pts, n, d_out, d_hist, d_counters);
   } else {
     auto k = project_kernel<false, false>;
-    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, 0, stream>>>(P, pts, n, d_out, d_hist, d_counters);
+    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, kSmemBytes, stream>>>(P, pts, n, d_out, d_hist, d_counters);
   }
   FM_CUDA(cudaGetLastError());
   return FM_OK;
@@ -296,6 +461,7 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   ix->ay1 = std::min(ix->g.gy1, 90.0);
   ix->grid_len = ix->host.grid.size();
   ix->arena_len = ix->host.arena.size();
+  ix->granule = ix->host.granule;
 
   fm_index_stats& s = ix->stats;
   s.n_polys = n_polys;
@@ -435,16 +601,17 @@ fm_status fm_query_host(const fm_index* cindex, const double* h_lonlat, std::uin
 }
 
 fm_status fm_index_export(const fm_index* index, std::uint32_t* grid, std::uint64_t* grid_len,
-                          std::uint8_t* arena, std::uint64_t* arena_len, double* geometry12) {
+                          std::uint8_t* arena, std::uint64_t* arena_len, double* geometry16) {
   if (!index || !grid_len || !arena_len) return set_err(FM_ERR_INVALID_ARGUMENT, "null argument");
   *grid_len = index->grid_len;
   *arena_len = index->arena_len;
-  if (geometry12) {
+  if (geometry16) {
     const fm::GridGeom& g = index->g;
-    const double v[12] = {g.gx0, g.gx1, g.gy0, g.gy1, g.w, g.h, g.inv_w, g.inv_h,
+    const double v[16] = {g.gx0, g.gx1, g.gy0, g.gy1, g.w, g.h, g.inv_w, g.inv_h,
                           static_cast<double>(g.nx), static_cast<double>(g.ny), g.margin,
-                          static_cast<double>(index->stats.n_polys)};
-    std::memcpy(geometry12, v, sizeof(v));
+                          static_cast<double>(index->stats.n_polys),
+                          static_cast<double>(index->granule), 0.0, 0.0, 0.0};
+    std::memcpy(geometry16, v, sizeof(v));
   }
   if (!grid && !arena) return FM_OK;
   if (index->device < 0) {

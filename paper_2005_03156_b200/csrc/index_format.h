@@ -7,27 +7,57 @@
 // One u32 entry per cell, row-major:
 //   0xFFFFFFFF            empty: no leaf contains any point of the cell
 //   < 0x80000000          true hit: every point of the cell maps to this leaf
-//   0x80000000 | k        boundary: record at arena byte offset 16*k
+//   1 | s(4) | k(27)      boundary: record of min(256, 16*(s+1)) bytes at
+//                         arena byte offset k * granule (granule = 16, 32,
+//                         64 ... chosen per index so the arena fits 27 bits);
+//                         s = 15 also marks "256 bytes or more / wide".
+// The size code lets the kernel fetch exactly a record's bytes in one
+// round trip, without reading a header first.
 //
-// Boundary record (16-byte aligned, little endian):
-//   u16 n_edges, u16 n_cands, u16 n_words, u16 n_breaks   (header, 16 B)
-//   u32 reserved[2]
-//   n_edges x {f64 lo.lon, lo.lat, hi.lon, hi.lat}   oriented edges,
-//       lo.lat < hi.lat, exactly the (lo, hi) the reference forms in
-//       point_in_polygon (geometry.hpp:217-219); deduplicated across leaves
-//   n_cands x {i32 leaf, u32 info}   ascending leaf id; info bit 0 = c0
-//       (constant parity of the leaf's edges that lie wholly right of the
-//       cell), bits 1..15 = number of latitude breakpoints of this leaf
-//   n_cands x n_words x u32          per-leaf edge membership masks
-//       (bit k set iff edge k occurs an odd number of times in the leaf)
-//   pad to 8 B
-//   n_breaks x f64                   breakpoints, per leaf in leaf order
-//   pad to 16 B
-// Point p in the cell maps to the first candidate whose parity
-//   c0 ^ popc(cross_mask & mask) ^ #{b : p.lat > b}
-// is odd, where bit k of cross_mask is the reference predicate of edge k at
-// p.  A candidate with no edges and no breakpoints and c0 = 1 is a
-// terminal: it always wins, and nothing after it is stored.
+// A boundary record lists, for the cell, the candidate leaves in ascending
+// id order and the exact (fp64) polygon edges near the cell.  Point p maps
+// to the first candidate whose parity
+//     c0  ^  popc(cross_mask & edge_mask)  ^  popc(break_mask & {b : p.lat > b})
+// is odd, where bit i of cross_mask is the reference predicate
+// (geometry.hpp:214-225) of edge i at p.  c0 is the constant parity of the
+// leaf's edges lying wholly right of the cell; the breakpoints are the
+// latitudes where that constant changes inside the cell's slab.  A
+// candidate with no edges, no breakpoints and c0 = 1 is terminal.
+//
+// Compact record (kind 1; fits when n_verts <= 32, n_cands <= 15,
+// n_breaks <= 7), 16-byte aligned, little endian:
+//   +0   u8 kind=1, u8 n_verts, u8 n_cands, u8 n_breaks
+//   +4   u32 chain_mask        bit i set: vertex i starts a new chain
+//   +8   n_cands x {i32 leaf, u32 edge_mask}
+//        n_cands x u8 info     bit 7 = c0, bits 0..6 = break_mask
+//        pad to 8
+//        n_breaks x f64        breakpoint latitudes
+//        pad to 16
+//        n_verts x {f64 lon, f64 lat}
+//   Edge i joins vertex i and vertex i+1 unless bit i+1 of chain_mask is
+//   set; it is oriented exactly like the reference (lo = lower latitude,
+//   geometry.hpp:219), which reproduces its (lo, hi) bit for bit.
+//
+// Split record (kind 3): a boundary cell whose leaf record would not fit
+// one kRecordWindow-byte fetch is split 2x2 (recursively, up to
+// kMaxSplitDepth levels):
+//   +0   u8 kind=3, u8 0, u16 0, u32 0
+//   +8   f64 x0, f64 y0          lower-left corner of the split cell
+//   +24  f64 inv_hw, f64 inv_hh  1 / child width, 1 / child height
+//   +40  u32 child[4]            grid-format entries, index 2*j + i
+//   +56  pad to 64
+// Child (i, j) covers [x0 + i*hw, x0 + (i+1)*hw] x [y0 + j*hh, ...]; a
+// point goes to i = clamp(int((lon - x0) * inv_hw), 0, 1) (same for j).
+//
+// Wide record (kind 2; anything else):
+//   +0   u8 kind=2, u8 0, u16 n_words, u16 n_edges, u16 n_cands,
+//        u16 n_breaks, u16 0, u32 0
+//   +16  n_edges x {f64 lo.lon, lo.lat, hi.lon, hi.lat}  (lo.lat < hi.lat)
+//        n_cands x {i32 leaf, u32 info}  info bit 0 = c0, bits 1..15 = #breaks
+//        n_cands x n_words x u32        edge masks
+//        pad to 8
+//        sum(#breaks) x f64             per-candidate breakpoints, in order
+//        pad to 16
 #pragma once
 
 #include <cstdint>
@@ -48,38 +78,58 @@ constexpr std::uint32_t kMaxCands = 0xFFFFu;  // cell_index.hpp:339-341 limit
 constexpr std::uint32_t kMaxRecordEdges = 0xFFFFu;
 constexpr std::uint32_t kMaxBreaksPerCand = 0x7FFFu;
 
-struct RecordHeader {
-  std::uint16_t n_edges;
-  std::uint16_t n_cands;
-  std::uint16_t n_words;
-  std::uint16_t n_breaks;
-  std::uint32_t reserved0;
-  std::uint32_t reserved1;
-};
-static_assert(sizeof(RecordHeader) == 16, "record header is 16 bytes");
+constexpr std::uint8_t kKindCompact = 1;
+constexpr std::uint8_t kKindWide = 2;
+constexpr std::uint8_t kKindSplit = 3;
+constexpr std::uint64_t kRecordWindow = 256;  // max bytes fetched in one round per record
+constexpr std::uint32_t kOffsetBits = 27;
+constexpr std::uint32_t kOffsetMask = (1u << kOffsetBits) - 1u;
 
-FM_HD std::uint64_t record_bytes(std::uint32_t n_edges, std::uint32_t n_cands,
-                                 std::uint32_t n_words, std::uint32_t n_breaks) {
-  std::uint64_t b = 16 + 32ull * n_edges + 8ull * n_cands + 4ull * n_cands * n_words;
-  b = (b + 7) & ~std::uint64_t{7};
-  b += 8ull * n_breaks;
-  return (b + 15) & ~std::uint64_t{15};
+FM_HD std::uint32_t record_entry(std::uint64_t unit_off, std::uint64_t bytes) {
+  const std::uint64_t code = bytes >= 256 ? 15 : (bytes + 15) / 16 - 1;
+  return 0x80000000u | static_cast<std::uint32_t>(code << kOffsetBits) |
+         static_cast<std::uint32_t>(unit_off);
 }
-FM_HD std::uint64_t record_cands_offset(std::uint32_t n_edges) {
-  return 16 + 32ull * n_edges;
+FM_HD std::uint32_t entry_fetch_bytes(std::uint32_t e) {
+  return 16u * (((e >> kOffsetBits) & 15u) + 1u);
 }
-FM_HD std::uint64_t record_masks_offset(std::uint32_t n_edges, std::uint32_t n_cands) {
-  return 16 + 32ull * n_edges + 8ull * n_cands;
+constexpr int kMaxSplitDepth = 6;
+constexpr std::uint64_t kSplitBytes = 64;
+constexpr std::uint32_t kCompactMaxVerts = 32;
+constexpr std::uint32_t kCompactMaxCands = 15;
+constexpr std::uint32_t kCompactMaxBreaks = 7;
+
+FM_HD std::uint64_t align_up(std::uint64_t v, std::uint64_t a) { return (v + a - 1) & ~(a - 1); }
+
+// ---- compact record offsets ----
+FM_HD std::uint64_t compact_info_offset(std::uint32_t nc) { return 8 + 8ull * nc; }
+FM_HD std::uint64_t compact_breaks_offset(std::uint32_t nc) {
+  return align_up(8 + 8ull * nc + nc, 8);
 }
-FM_HD std::uint64_t record_breaks_offset(std::uint32_t n_edges, std::uint32_t n_cands,
-                                         std::uint32_t n_words) {
-  std::uint64_t b = 16 + 32ull * n_edges + 8ull * n_cands + 4ull * n_cands * n_words;
-  return (b + 7) & ~std::uint64_t{7};
+FM_HD std::uint64_t compact_verts_offset(std::uint32_t nc, std::uint32_t nb) {
+  return align_up(compact_breaks_offset(nc) + 8ull * nb, 16);
+}
+FM_HD std::uint64_t compact_bytes(std::uint32_t nv, std::uint32_t nc, std::uint32_t nb) {
+  return compact_verts_offset(nc, nb) + 16ull * nv;
 }
 
-// Grid geometry.  Cell rectangles are always formed by these two functions
-// (builder) and points are always located by cell_of (kernel); the margin
-// absorbs their rounding disagreement.
+// ---- wide record offsets ----
+FM_HD std::uint64_t wide_cands_offset(std::uint32_t ne) { return 16 + 32ull * ne; }
+FM_HD std::uint64_t wide_masks_offset(std::uint32_t ne, std::uint32_t nc) {
+  return 16 + 32ull * ne + 8ull * nc;
+}
+FM_HD std::uint64_t wide_breaks_offset(std::uint32_t ne, std::uint32_t nc, std::uint32_t nw) {
+  return align_up(wide_masks_offset(ne, nc) + 4ull * nc * nw, 8);
+}
+FM_HD std::uint64_t wide_bytes(std::uint32_t ne, std::uint32_t nc, std::uint32_t nw,
+                               std::uint32_t nb) {
+  return align_up(wide_breaks_offset(ne, nc, nw) + 8ull * nb, 16);
+}
+
+// Grid geometry.  Cell rectangles are always formed by cell_x0/cell_y0
+// (builder) and points are always located by the kernel's
+// (p - g0) * inv truncation; the margin absorbs their rounding
+// disagreement.
 struct GridGeom {
   double gx0, gx1, gy0, gy1;  // padded domain
   double w, h;                // cell size

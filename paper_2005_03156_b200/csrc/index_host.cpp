@@ -29,16 +29,10 @@
 #include <vector>
 
 #include "index_build.h"
+#include "record_encode.h"
 
 namespace fm {
 namespace {
-
-struct Edge4 {
-  double lx, ly, hx, hy;
-};
-inline bool same_edge(const Edge4& a, const Edge4& b) {
-  return std::memcmp(&a, &b, sizeof(Edge4)) == 0;
-}
 
 // smallest k in [0, n) with g0 + (k+1)*step >= v; n if none
 std::int64_t first_with_hi_ge(double g0, double step, double inv, std::int64_t n,
@@ -106,14 +100,9 @@ struct RowWorker {
   std::vector<double> tog;
   BuildStats st;
 
-  // finalize scratch
-  std::vector<Edge4> U;
-  struct Cand {
-    std::uint32_t id, c0;
-    std::vector<std::uint32_t> edges;  // indices into U, odd multiplicity
-    std::uint32_t b_begin, b_end;
-  };
-  std::vector<Cand> cands;
+  EncodeStats es;
+  std::vector<std::uint8_t> scratch;
+  std::vector<std::uint64_t>* rec_starts = nullptr;  // row-local record offsets, ascending
 
   RowWorker(const Soup& s_, const GridGeom& g_, const std::vector<PolySpan>& sp, double t)
       : s(s_), g(g_), spans(sp), tol(t) {
@@ -196,23 +185,82 @@ struct RowWorker {
     }
   }
 
-  // Returns the grid entry for the cell; may append a record to `arena`,
-  // in which case *rec_off receives its row-local byte offset.
-  std::uint32_t finalize_cell(std::int64_t ix, std::vector<std::uint8_t>& arena,
-                              std::int64_t* rec_off) {
-    const auto& list = cols[ix];
-    U.clear();
-    cands.clear();
-    for (const Contrib& c : list) {
-      Cand cd;
-      cd.id = c.id;
-      cd.c0 = c.c0;
-      cd.b_begin = c.b_begin;
-      cd.b_end = c.b_end;
-      for (std::uint32_t q = c.e_begin; q < c.e_end; ++q) {
+  // One leaf's contribution to a rectangle: its near edges, the constant
+  // parity c0 of the edges wholly right of it, and the breakpoints.
+  struct PolyC {
+    std::uint32_t id = 0, c0 = 0;
+    std::vector<Edge4> near;
+    std::vector<double> breaks;  // ascending, distinct
+    bool constant() const { return near.empty() && breaks.empty(); }
+  };
+
+  // Re-derive a leaf's contribution for a sub-rectangle of the rectangle
+  // `par` was computed for: edges right of the parent
+  // stay right of the child, so only the parent's near edges need
+  // reclassifying, and the parent's breakpoints fold into the child's c0
+  // (below the child slab), stay breakpoints (inside) or vanish (above).
+  void reclassify(const PolyC& par, double rx0, double rx1, double ry0, double ry1,
+                  PolyC& ch) const {
+    const double d = g.margin;
+    const double ys0 = ry0 - d, ys1 = ry1 + d, xs0 = rx0 - d, xs1 = rx1 + d;
+    ch.id = par.id;
+    ch.near.clear();
+    ch.breaks.clear();
+    std::uint32_t c0 = par.c0;
+    for (const double b : par.breaks) {
+      if (b < ys0) {
+        c0 ^= 1u;
+      } else if (b < ys1) {
+        ch.breaks.push_back(b);
+      }
+    }
+    for (const Edge4& E : par.near) {
+      if (E.hy <= ys0 || E.ly >= ys1) continue;
+      const double ya = std::max(E.ly, ys0), yb = std::min(E.hy, ys1);
+      const double slope = (E.hx - E.lx) / (E.hy - E.ly);
+      const double mnx = std::min(E.lx, E.hx), mxx = std::max(E.lx, E.hx);
+      auto x_at = [&](double y) {
+        const double x = E.lx + (y - E.ly) * slope;
+        return std::min(mxx, std::max(mnx, x));
+      };
+      const double xa = (ya == E.ly) ? E.lx : x_at(ya);
+      const double xb = (yb == E.hy) ? E.hx : x_at(yb);
+      const double ex0 = std::min(xa, xb) - tol, ex1 = std::max(xa, xb) + tol;
+      if (ex1 < xs0) continue;  // left of the child: never crosses
+      if (ex0 > xs1) {          // right of the child: fold into c0 / breakpoints
+        for (const double m : {E.ly, E.hy}) {
+          if (m < ys0) {
+            c0 ^= 1u;
+          } else if (m < ys1) {
+            toggle(ch.breaks, m);
+          }
+        }
+        continue;
+      }
+      ch.near.push_back(E);
+    }
+    ch.c0 = c0;
+  }
+
+  // Entry for a rectangle given its leaves' contributions (ascending ids).
+  // Appends records to `arena` (row-local offsets; every u32 that holds a
+  // row-local record entry is listed in `patches` for relocation).
+  std::uint32_t finalize(const std::vector<PolyC>& list, double rx0, double ry0, double cw,
+                         double chh, int depth, std::vector<std::uint8_t>& arena,
+                         std::vector<std::uint64_t>& patches) {
+    std::vector<Edge4> U;
+    std::vector<CandIn> cin;
+    std::vector<std::size_t> src;  // index into list per candidate
+    for (std::size_t q = 0; q < list.size(); ++q) {
+      const PolyC& pc = list[q];
+      CandIn cd;
+      cd.id = pc.id;
+      cd.c0 = pc.c0;
+      cd.breaks = pc.breaks;
+      for (const Edge4& E : pc.near) {
         std::uint32_t idx = 0;
-        while (idx < U.size() && !same_edge(U[idx], epool[q])) ++idx;
-        if (idx == U.size()) U.push_back(epool[q]);
+        while (idx < U.size() && !same_edge(U[idx], E)) ++idx;
+        if (idx == U.size()) U.push_back(E);
         auto it = std::find(cd.edges.begin(), cd.edges.end(), idx);
         if (it != cd.edges.end()) {
           cd.edges.erase(it);  // even multiplicity cancels
@@ -220,29 +268,23 @@ struct RowWorker {
           cd.edges.push_back(idx);
         }
       }
-      if (cd.edges.empty() && cd.b_begin == cd.b_end) {
-        if (cd.c0) {  // terminal
-          cd.edges.clear();
-          cands.push_back(std::move(cd));
+      if (cd.edges.empty() && cd.breaks.empty()) {
+        if (cd.c0) {  // constant true: terminal
+          cin.push_back(std::move(cd));
+          src.push_back(q);
           break;
         }
         continue;  // constant false
       }
-      cands.push_back(std::move(cd));
+      cin.push_back(std::move(cd));
+      src.push_back(q);
     }
-    if (cands.empty()) {
-      st.cells_empty++;
-      return kEmpty;
-    }
-    const Cand& first = cands.front();
-    if (first.edges.empty() && first.b_begin == first.b_end) {
-      st.cells_hit++;
-      return first.id;  // true hit (first leaf is constant-true)
-    }
-    // compact edges to the ones still referenced
+    if (cin.empty()) return kEmpty;
+    if (cin.front().edges.empty() && cin.front().breaks.empty()) return cin.front().id;
+    // drop edges no candidate references any more
     std::vector<std::int64_t> remap(U.size(), -1);
     std::vector<Edge4> used;
-    for (auto& cd : cands) {
+    for (auto& cd : cin) {
       for (auto& e : cd.edges) {
         if (remap[e] < 0) {
           remap[e] = static_cast<std::int64_t>(used.size());
@@ -251,66 +293,60 @@ struct RowWorker {
         e = static_cast<std::uint32_t>(remap[e]);
       }
     }
-    const std::uint64_t n_edges = used.size(), n_cands = cands.size();
-    std::uint64_t n_breaks = 0;
-    for (const auto& cd : cands) {
-      const std::uint64_t nb = cd.b_end - cd.b_begin;
-      if (nb > kMaxBreaksPerCand) {
-        throw RuntimeError("boundary cell leaf with more than 32767 latitude breakpoints");
+    scratch.clear();
+    EncodeStats tmp;
+    encode_record(used, cin, scratch, &tmp);
+    const bool fits = tmp.compact == 1 && scratch.size() <= kRecordWindow;
+    if (!fits && depth < kMaxSplitDepth && cw > 256.0 * g.margin && chh > 256.0 * g.margin) {
+      // split 2x2: child (i, j) covers [rx0 + i*cw/2, rx0 + (i+1)*cw/2] x ...
+      const double hw = 0.5 * cw, hh = 0.5 * chh;
+      std::uint32_t child[4];
+      for (int j = 0; j < 2; ++j) {
+        for (int i = 0; i < 2; ++i) {
+          const double cx0 = rx0 + i * hw, cy0 = ry0 + j * hh;
+          std::vector<PolyC> sub;
+          for (const std::size_t q : src) {
+            PolyC pc;
+            reclassify(list[q], cx0, cx0 + hw, cy0, cy0 + hh, pc);
+            if (pc.constant()) {
+              if (pc.c0) {
+                sub.push_back(std::move(pc));
+                break;
+              }
+              continue;
+            }
+            sub.push_back(std::move(pc));
+          }
+          child[2 * j + i] = finalize(sub, cx0, cy0, hw, hh, depth + 1, arena, patches);
+        }
       }
-      n_breaks += nb;
+      const std::uint64_t off = arena.size();
+      encode_split(rx0, ry0, 1.0 / hw, 1.0 / hh, child, arena, &patches);
+      rec_starts->push_back(off);
+      st.cells_split++;
+      return kRecordBit | static_cast<std::uint32_t>(off / kRecordAlign);
     }
-    if (n_cands > kMaxCands) {
-      throw RuntimeError("boundary cell with more than 65535 candidates");
-    }
-    if (n_edges > kMaxRecordEdges || n_breaks > 0xFFFFu) {
-      throw RuntimeError("boundary cell with more than 65535 edges or breakpoints");
-    }
-    const std::uint32_t n_words = static_cast<std::uint32_t>((n_edges + 31) / 32);
-    const std::uint64_t bytes = record_bytes(static_cast<std::uint32_t>(n_edges),
-                                             static_cast<std::uint32_t>(n_cands), n_words,
-                                             static_cast<std::uint32_t>(n_breaks));
     const std::uint64_t off = arena.size();
-    arena.resize(off + bytes, 0);
-    std::uint8_t* rec = arena.data() + off;
-    RecordHeader h{};
-    h.n_edges = static_cast<std::uint16_t>(n_edges);
-    h.n_cands = static_cast<std::uint16_t>(n_cands);
-    h.n_words = static_cast<std::uint16_t>(n_words);
-    h.n_breaks = static_cast<std::uint16_t>(n_breaks);
-    std::memcpy(rec, &h, sizeof(h));
-    std::memcpy(rec + 16, used.data(), 32 * n_edges);
-    std::uint8_t* cp = rec + record_cands_offset(static_cast<std::uint32_t>(n_edges));
-    std::uint32_t* mp = reinterpret_cast<std::uint32_t*>(
-        rec + record_masks_offset(static_cast<std::uint32_t>(n_edges),
-                                  static_cast<std::uint32_t>(n_cands)));
-    double* bp = reinterpret_cast<double*>(
-        rec + record_breaks_offset(static_cast<std::uint32_t>(n_edges),
-                                   static_cast<std::uint32_t>(n_cands), n_words));
-    std::uint64_t bw = 0;
-    for (std::uint64_t c = 0; c < n_cands; ++c) {
-      const Cand& cd = cands[c];
-      const std::int32_t id = static_cast<std::int32_t>(cd.id);
-      const std::uint32_t nb = cd.b_end - cd.b_begin;
-      const std::uint32_t info = (cd.c0 & 1u) | (nb << 1);
-      std::memcpy(cp + 8 * c, &id, 4);
-      std::memcpy(cp + 8 * c + 4, &info, 4);
-      for (const std::uint32_t e : cd.edges) mp[c * n_words + e / 32] |= 1u << (e % 32);
-      for (std::uint32_t q = cd.b_begin; q < cd.b_end; ++q) bp[bw++] = bpool[q];
-    }
-    st.cells_boundary++;
-    st.record_edges += n_edges;
-    st.record_cands += n_cands;
+    arena.insert(arena.end(), scratch.begin(), scratch.end());
+    rec_starts->push_back(off);
+    es.compact += tmp.compact;
+    es.wide += tmp.wide;
+    std::uint64_t n_breaks = 0;
+    for (const auto& c : cin) n_breaks += c.breaks.size();
+    st.records++;
+    st.record_edges += used.size();
+    st.record_cands += cin.size();
     st.record_breaks += n_breaks;
-    st.max_record_edges = std::max<std::uint64_t>(st.max_record_edges, n_edges);
-    st.max_record_cands = std::max<std::uint64_t>(st.max_record_cands, n_cands);
-    *rec_off = static_cast<std::int64_t>(off);
-    return kRecordBit;  // patched with the global offset later
+    st.max_record_edges = std::max<std::uint64_t>(st.max_record_edges, used.size());
+    st.max_record_cands = std::max<std::uint64_t>(st.max_record_cands, cin.size());
+    return kRecordBit | static_cast<std::uint32_t>(off / kRecordAlign);
   }
 
   void run_row(std::int64_t iy, const std::uint32_t* ids, std::uint64_t n_ids,
                std::uint32_t* grid_row, std::vector<std::uint8_t>& arena,
-               std::vector<std::pair<std::int64_t, std::int64_t>>& recs) {
+               std::vector<std::int64_t>& rec_cols, std::vector<std::uint64_t>& patches,
+               std::vector<std::uint64_t>& starts) {
+    rec_starts = &starts;
     const double ys0 = cell_y0(g, iy) - g.margin;
     const double ys1 = cell_y0(g, iy + 1) + g.margin;
     epool.clear();
@@ -318,10 +354,28 @@ struct RowWorker {
     touched.clear();
     for (std::uint64_t q = 0; q < n_ids; ++q) add_polygon(ids[q], ys0, ys1);
     std::sort(touched.begin(), touched.end());
+    std::vector<PolyC> list;
     for (const std::int64_t ix : touched) {
-      std::int64_t off = -1;
-      grid_row[ix] = finalize_cell(ix, arena, &off);
-      if (off >= 0) recs.emplace_back(ix, off);
+      list.clear();
+      for (const Contrib& c : cols[ix]) {
+        PolyC pc;
+        pc.id = c.id;
+        pc.c0 = c.c0;
+        pc.near.assign(epool.begin() + c.e_begin, epool.begin() + c.e_end);
+        pc.breaks.assign(bpool.begin() + c.b_begin, bpool.begin() + c.b_end);
+        list.push_back(std::move(pc));
+      }
+      const std::uint32_t e = finalize(list, cell_x0(g, ix), cell_y0(g, iy), g.w, g.h, 0,
+                                       arena, patches);
+      grid_row[ix] = e;
+      if (e == kEmpty) {
+        st.cells_empty++;
+      } else if (e < kRecordBit) {
+        st.cells_hit++;
+      } else {
+        st.cells_boundary++;
+        rec_cols.push_back(ix);
+      }
       cols[ix].clear();
       closed[ix] = 0;
     }
@@ -431,7 +485,8 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
   const GridGeom& g = out.g;
   const std::size_t ncell = static_cast<std::size_t>(g.nx * g.ny);
   out.grid.assign(ncell, kEmpty);
-  out.arena.assign(256, 0);
+  out.arena.assign(512, 0);
+  out.granule = kRecordAlign;
   if (s.n_polys == 0) {
     out.stats.cells_empty = ncell;
     return out;
@@ -484,8 +539,9 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
   threads = static_cast<int>(std::min<std::int64_t>(threads, g.ny));
 
   std::vector<std::vector<std::uint8_t>> row_arena(static_cast<std::size_t>(g.ny));
-  std::vector<std::vector<std::pair<std::int64_t, std::int64_t>>> row_recs(
-      static_cast<std::size_t>(g.ny));
+  std::vector<std::vector<std::int64_t>> row_recs(static_cast<std::size_t>(g.ny));
+  std::vector<std::vector<std::uint64_t>> row_patches(static_cast<std::size_t>(g.ny));
+  std::vector<std::vector<std::uint64_t>> row_starts(static_cast<std::size_t>(g.ny));
   std::atomic<std::int64_t> next{0};
   std::mutex mu;
   std::exception_ptr failure;
@@ -497,9 +553,12 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
         const std::int64_t iy = next.fetch_add(1);
         if (iy >= g.ny) break;
         w.run_row(iy, row_ids.data() + row_count[iy], row_count[iy + 1] - row_count[iy],
-                  out.grid.data() + iy * g.nx, row_arena[iy], row_recs[iy]);
+                  out.grid.data() + iy * g.nx, row_arena[iy], row_recs[iy], row_patches[iy],
+                  row_starts[iy]);
       }
       stats[t] = w.st;
+      stats[t].records_compact = w.es.compact;
+      stats[t].records_wide = w.es.wide;
     } catch (...) {
       std::lock_guard<std::mutex> lk(mu);
       if (!failure) failure = std::current_exception();
@@ -512,23 +571,60 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
   for (auto& th : pool) th.join();
   if (failure) std::rethrow_exception(failure);
 
-  std::uint64_t total = 0;
-  std::vector<std::uint64_t> base(static_cast<std::size_t>(g.ny));
-  for (std::int64_t r = 0; r < g.ny; ++r) {
-    base[r] = total;
-    total += row_arena[r].size();
-  }
-  if (total / kRecordAlign >= kRecordBit) throw RuntimeError("index arena exceeds 32 GiB");
-  // 256 B zero tail: the kernel may prefetch past a short final record
-  out.arena.assign(total + 256, 0);
-  out.arena_used = total;
-  for (std::int64_t r = 0; r < g.ny; ++r) {
-    if (!row_arena[r].empty()) {
-      std::memcpy(out.arena.data() + base[r], row_arena[r].data(), row_arena[r].size());
+  // Lay the rows' records out in one arena with granule G (the smallest
+  // power of two >= 16 for which every offset fits kOffsetBits), and rewrite
+  // every record entry (grid cells and split children) as
+  // record_entry(offset / G, size).
+  auto rec_size = [&](std::int64_t r, std::size_t k) {
+    const auto& st = row_starts[r];
+    return (k + 1 < st.size() ? st[k + 1] : row_arena[r].size()) - st[k];
+  };
+  std::uint64_t G = kRecordAlign;
+  for (;; G *= 2) {
+    std::uint64_t units = 0;
+    for (std::int64_t r = 0; r < g.ny; ++r) {
+      for (std::size_t k = 0; k < row_starts[r].size(); ++k) units += (rec_size(r, k) + G - 1) / G;
     }
-    for (const auto& [ix, off] : row_recs[r]) {
-      out.grid[static_cast<std::size_t>(r * g.nx + ix)] =
-          kRecordBit | static_cast<std::uint32_t>((base[r] + static_cast<std::uint64_t>(off)) / kRecordAlign);
+    if (units < (std::uint64_t{1} << kOffsetBits)) break;
+    if (G >= 4096) throw RuntimeError("index arena too large for 27-bit record offsets");
+  }
+  std::vector<std::vector<std::uint64_t>> new_off(static_cast<std::size_t>(g.ny));
+  std::uint64_t total = 0;
+  for (std::int64_t r = 0; r < g.ny; ++r) {
+    new_off[r].resize(row_starts[r].size());
+    for (std::size_t k = 0; k < row_starts[r].size(); ++k) {
+      new_off[r][k] = total;
+      total += (rec_size(r, k) + G - 1) / G * G;
+    }
+  }
+  out.granule = G;
+  out.arena_used = total;
+  out.arena.assign(total + 512, 0);  // zero tail: fixed-size fetches may run past the end
+  auto find_rec = [&](std::int64_t r, std::uint64_t local) {
+    const auto& st = row_starts[r];
+    return static_cast<std::size_t>(std::upper_bound(st.begin(), st.end(), local) - st.begin() - 1);
+  };
+  auto relocate = [&](std::int64_t r, std::uint32_t e) {
+    const std::uint64_t local = static_cast<std::uint64_t>(e & ~kRecordBit) * kRecordAlign;
+    const std::size_t k = find_rec(r, local);
+    return record_entry(new_off[r][k] / G, rec_size(r, k));
+  };
+  for (std::int64_t r = 0; r < g.ny; ++r) {
+    for (std::size_t k = 0; k < row_starts[r].size(); ++k) {
+      std::memcpy(out.arena.data() + new_off[r][k], row_arena[r].data() + row_starts[r][k],
+                  rec_size(r, k));
+    }
+    for (const std::int64_t ix : row_recs[r]) {
+      std::uint32_t& e = out.grid[static_cast<std::size_t>(r * g.nx + ix)];
+      e = relocate(r, e);
+    }
+    for (const std::uint64_t pos : row_patches[r]) {
+      const std::size_t k = find_rec(r, pos);
+      const std::uint64_t at = new_off[r][k] + (pos - row_starts[r][k]);
+      std::uint32_t v;
+      std::memcpy(&v, out.arena.data() + at, 4);
+      v = relocate(r, v);
+      std::memcpy(out.arena.data() + at, &v, 4);
     }
     std::vector<std::uint8_t>().swap(row_arena[r]);
   }
@@ -541,6 +637,10 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
     out.stats.record_breaks += st.record_breaks;
     out.stats.max_record_edges = std::max(out.stats.max_record_edges, st.max_record_edges);
     out.stats.max_record_cands = std::max(out.stats.max_record_cands, st.max_record_cands);
+    out.stats.records_compact += st.records_compact;
+    out.stats.records += st.records;
+    out.stats.cells_split += st.cells_split;
+    out.stats.records_wide += st.records_wide;
   }
   return out;
 }

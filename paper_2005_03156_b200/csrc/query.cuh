@@ -1,13 +1,12 @@
 // query.cuh -- device side of the projection: point location and the exact
-// fp64 crossing-number evaluation of boundary records.
+// fp64 crossing-number evaluation of boundary records (index_format.h).
 //
 // Parity with the reference rests on ray_crosses below evaluating
 //   (hi.lon - lo.lon) * (p.lat - lo.lat) - (hi.lat - lo.lat) * (p.lon - lo.lon) > 0
-// (geometry.hpp:170-174) as three rounded subtractions, two rounded
-// products and one rounded subtraction -- never a fused multiply-add.  The
-// __dsub_rn/__dmul_rn intrinsics are never contracted by nvcc, and the
-// library is additionally compiled with --fmad=false; tests/test_sass.py
-// checks the SASS of every kernel for DFMA.
+// (geometry.hpp:170-174) as rounded subtractions and rounded products --
+// never a fused multiply-add.  __dsub_rn/__dmul_rn are never contracted by
+// nvcc, the library is also compiled with --fmad=false, and
+// tests/test_sass.py checks the shipped SASS for DFMA.
 #pragma once
 
 #include <cstdint>
@@ -22,13 +21,27 @@ struct KParams {
   double gx0, gy0, inv_w, inv_h;
   double ax0, ax1, ay0, ay1;  // acceptance box = padded domain intersect world box
   int nx, ny;
+  std::uint64_t granule;     // record offset unit (bytes)
 };
+
+__device__ __forceinline__ const std::uint8_t* record_ptr(const KParams& P, std::uint32_t e) {
+  return P.arena + static_cast<std::size_t>(e & kOffsetMask) * P.granule;
+}
 
 __device__ __forceinline__ bool ray_crosses(double px, double py, double lx,
                                             double ly, double hx, double hy) {
   const double a = __dmul_rn(__dsub_rn(hx, lx), __dsub_rn(py, ly));
   const double b = __dmul_rn(__dsub_rn(hy, ly), __dsub_rn(px, lx));
   return __dsub_rn(a, b) > 0.0;
+}
+
+// Crossing bit of the edge (a, b) at p, oriented like geometry.hpp:217-220.
+__device__ __forceinline__ std::uint32_t edge_bit(double px, double py, double ax,
+                                                  double ay, double bx, double by) {
+  const bool up = ay < by;
+  const double lx = up ? ax : bx, ly = up ? ay : by;
+  const double hx = up ? bx : ax, hy = up ? by : ay;
+  return (ly < py && py <= hy && ray_crosses(px, py, lx, ly, hx, hy)) ? 1u : 0u;
 }
 
 // Grid entry for p, or kEmpty when p is outside the acceptance box (which
@@ -46,46 +59,18 @@ struct WorkCount {
   unsigned long long boundary = 0, cands = 0, edges = 0;
 };
 
-// Resolve a point inside a boundary cell (format: index_format.h).
+// Wide records (rare): evaluated straight from global memory.
 template <bool kCount>
-__device__ __noinline__ int resolve_record(const std::uint8_t* __restrict__ arena,
-                                           std::uint32_t entry, double px, double py,
-                                           WorkCount& wc) {
-  const std::uint8_t* rec = arena + static_cast<std::size_t>(entry & ~kRecordBit) * kRecordAlign;
+__device__ __noinline__ int resolve_wide(const std::uint8_t* __restrict__ rec, double px,
+                                         double py, WorkCount& wc) {
   const uint4 h = __ldg(reinterpret_cast<const uint4*>(rec));
-  const std::uint32_t n_edges = h.x & 0xFFFFu, n_cands = h.x >> 16, n_words = h.y & 0xFFFFu;
+  const std::uint32_t n_words = h.x >> 16, n_edges = h.y & 0xFFFFu, n_cands = h.y >> 16;
   const double2* E = reinterpret_cast<const double2*>(rec + 16);
-  const int2* C = reinterpret_cast<const int2*>(rec + record_cands_offset(n_edges));
+  const int2* C = reinterpret_cast<const int2*>(rec + wide_cands_offset(n_edges));
   const std::uint32_t* Mk =
-      reinterpret_cast<const std::uint32_t*>(rec + record_masks_offset(n_edges, n_cands));
+      reinterpret_cast<const std::uint32_t*>(rec + wide_masks_offset(n_edges, n_cands));
   const double* B =
-      reinterpret_cast<const double*>(rec + record_breaks_offset(n_edges, n_cands, n_words));
-  if (kCount) wc.boundary++;
-  if (n_words <= 1) {
-    std::uint32_t m = 0;
-    for (std::uint32_t k = 0; k < n_edges; ++k) {
-      const double2 lo = __ldg(E + 2 * k);
-      const double2 hi = __ldg(E + 2 * k + 1);
-      if (lo.y < py && py <= hi.y) {
-        if (kCount) wc.edges++;
-        if (ray_crosses(px, py, lo.x, lo.y, hi.x, hi.y)) m |= 1u << k;
-      }
-    }
-    std::uint32_t boff = 0;
-    for (std::uint32_t c = 0; c < n_cands; ++c) {
-      const int2 cd = __ldg(C + c);
-      const std::uint32_t info = static_cast<std::uint32_t>(cd.y);
-      const std::uint32_t nb = info >> 1;
-      const std::uint32_t mk = n_words ? __ldg(Mk + c) : 0u;
-      std::uint32_t par = (info & 1u) ^ static_cast<std::uint32_t>(__popc(m & mk));
-      for (std::uint32_t b = 0; b < nb; ++b) par ^= (py > __ldg(B + boff + b)) ? 1u : 0u;
-      boff += nb;
-      if (kCount) wc.cands++;
-      if (par & 1u) return cd.x;
-    }
-    return -1;
-  }
-  // wide record (> 32 edges): evaluate each candidate's edges directly
+      reinterpret_cast<const double*>(rec + wide_breaks_offset(n_edges, n_cands, n_words));
   std::uint32_t boff = 0;
   for (std::uint32_t c = 0; c < n_cands; ++c) {
     const int2 cd = __ldg(C + c);
@@ -109,6 +94,61 @@ __device__ __noinline__ int resolve_record(const std::uint8_t* __restrict__ aren
     boff += nb;
     if (kCount) wc.cands++;
     if (par & 1u) return cd.x;
+  }
+  return -1;
+}
+
+// Compact record.  `Rd` reads the record: from a shared-memory window
+// (WinReader, fast path) or from global memory (GlobalReader).
+struct GlobalReader {
+  const std::uint8_t* __restrict__ rec;
+  __device__ __forceinline__ double f64(std::uint32_t off) const {
+    return __ldg(reinterpret_cast<const double*>(rec + off));
+  }
+  __device__ __forceinline__ std::uint32_t u32(std::uint32_t off) const {
+    return __ldg(reinterpret_cast<const std::uint32_t*>(rec + off));
+  }
+};
+
+// Record bytes staged in shared memory.
+struct SmemReader {
+  const std::uint8_t* win;
+  __device__ __forceinline__ double f64(std::uint32_t off) const {
+    return *reinterpret_cast<const double*>(win + off);
+  }
+  __device__ __forceinline__ std::uint32_t u32(std::uint32_t off) const {
+    return *reinterpret_cast<const std::uint32_t*>(win + off);
+  }
+};
+
+template <bool kCount, typename Rd>
+__device__ __forceinline__ int resolve_compact(const Rd& R, std::uint32_t h, double px,
+                                               double py, WorkCount& wc) {
+  const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
+  const std::uint32_t chain = R.u32(4);
+  const std::uint32_t voff = static_cast<std::uint32_t>(compact_verts_offset(nc, nb));
+  // crossing mask over the vertex chains
+  std::uint32_t m = 0;
+  double ax = R.f64(voff), ay = R.f64(voff + 8);
+  for (std::uint32_t i = 0; i + 1 < nv; ++i) {
+    const double bx = R.f64(voff + 16 * (i + 1)), by = R.f64(voff + 16 * (i + 1) + 8);
+    if (!((chain >> (i + 1)) & 1u)) {
+      if (kCount) wc.edges++;
+      m |= edge_bit(px, py, ax, ay, bx, by) << i;
+    }
+    ax = bx;
+    ay = by;
+  }
+  std::uint32_t bm = 0;
+  const std::uint32_t boff = static_cast<std::uint32_t>(compact_breaks_offset(nc));
+  for (std::uint32_t j = 0; j < nb; ++j) bm |= (py > R.f64(boff + 8 * j)) ? (1u << j) : 0u;
+  const std::uint32_t ioff = static_cast<std::uint32_t>(compact_info_offset(nc));
+  for (std::uint32_t c = 0; c < nc; ++c) {
+    const std::uint32_t mask = R.u32(12 + 8 * c);
+    const std::uint32_t info = (R.u32((ioff + c) & ~3u) >> (8 * ((ioff + c) & 3u))) & 0xFFu;
+    const std::uint32_t par = (info >> 7) ^ __popc(m & mask) ^ __popc(bm & info & 0x7Fu);
+    if (kCount) wc.cands++;
+    if (par & 1u) return static_cast<int>(R.u32(8 + 8 * c));
   }
   return -1;
 }

@@ -225,7 +225,7 @@ class CellIndex:
         """(grid u32[ny*nx], arena u8[], geometry dict) -- host copies."""
         L = N.lib()
         gl, al = C.c_uint64(0), C.c_uint64(0)
-        geo = np.zeros(12, dtype=np.float64)
+        geo = np.zeros(16, dtype=np.float64)
         N.check(L.fm_index_export(self.handle, None, C.byref(gl), None, C.byref(al),
                                   N.ptr(geo, C.c_double)), "fm_index_export")
         grid = np.zeros(gl.value, dtype=np.uint32)
@@ -234,8 +234,9 @@ class CellIndex:
                                   N.ptr(arena, C.c_uint8), C.byref(al), N.ptr(geo, C.c_double)),
                 "fm_index_export")
         keys = ("gx0", "gx1", "gy0", "gy1", "w", "h", "inv_w", "inv_h", "nx", "ny",
-                "margin", "n_polys")
+                "margin", "n_polys", "granule")
         g = dict(zip(keys, geo.tolist()))
+        g["granule"] = int(g["granule"])
         g["nx"] = int(g["nx"])
         g["ny"] = int(g["ny"])
         g["n_polys"] = int(g["n_polys"])

@@ -34,23 +34,66 @@ def locate(g: dict, grid: np.ndarray, pts: np.ndarray) -> np.ndarray:
     return np.where(inside, e, np.uint32(K_EMPTY)).astype(np.uint32)
 
 
-def parse_record(arena: np.ndarray, entry: int):
-    off = (entry & ~K_RECORD) * 16
+def _align(v, a):
+    return (v + a - 1) & ~(a - 1)
+
+
+OFFSET_MASK = (1 << 27) - 1
+
+
+def resolve(arena: np.ndarray, entry: int, px: float, py: float, granule: int = 16) -> int:
+    off = (entry & OFFSET_MASK) * granule
     buf = arena.data
-    n_edges, n_cands, n_words, n_breaks = struct.unpack_from("<4H", buf, off)
+    kind = arena[off]
+    while kind == 3:  # split record: descend to the child cell
+        x0, y0, ihw, ihh = struct.unpack_from("<4d", buf, off + 8)
+        child = struct.unpack_from("<4I", buf, off + 40)
+        i = min(max(int((px - x0) * ihw), 0), 1)
+        j = min(max(int((py - y0) * ihh), 0), 1)
+        e = child[2 * j + i]
+        if e == K_EMPTY:
+            return -1
+        if e < K_RECORD:
+            return e
+        off = (e & OFFSET_MASK) * granule
+        kind = arena[off]
+    if kind == 1:  # compact (index_format.h)
+        nv, nc, nb = int(arena[off + 1]), int(arena[off + 2]), int(arena[off + 3])
+        chain = struct.unpack_from("<I", buf, off + 4)[0]
+        cands = np.frombuffer(buf, dtype="<u4", count=2 * nc, offset=off + 8).reshape(-1, 2)
+        info = arena[off + 8 + 8 * nc: off + 8 + 9 * nc]
+        bo = _align(8 + 9 * nc, 8)
+        breaks = np.frombuffer(buf, dtype="<f8", count=nb, offset=off + bo)
+        vo = _align(bo + 8 * nb, 16)
+        v = np.frombuffer(buf, dtype="<f8", count=2 * nv, offset=off + vo).reshape(-1, 2).tolist()
+        m = 0
+        for i in range(nv - 1):
+            if (chain >> (i + 1)) & 1:
+                continue
+            (ax, ay), (bx, by) = v[i], v[i + 1]
+            lx, ly, hx, hy = (ax, ay, bx, by) if ay < by else (bx, by, ax, ay)
+            if ly < py <= hy and _cross(px, py, lx, ly, hx, hy):
+                m |= 1 << i
+        bm = 0
+        for j, b in enumerate(breaks.tolist()):
+            if py > b:
+                bm |= 1 << j
+        for c in range(nc):
+            leaf, mask = int(cands[c, 0]), int(cands[c, 1])
+            inf = int(info[c])
+            par = (inf >> 7) ^ bin(m & mask).count("1") ^ bin(bm & inf & 0x7F).count("1")
+            if par & 1:
+                return leaf - (1 << 32) if leaf >= (1 << 31) else leaf
+        return -1
+    assert kind == 2, f"bad record kind {kind}"
+    n_words, n_edges, n_cands, n_breaks = struct.unpack_from("<4H", buf, off + 2)
     edges = np.frombuffer(buf, dtype="<f8", count=4 * n_edges, offset=off + 16).reshape(-1, 4)
     co = off + 16 + 32 * n_edges
     cands = np.frombuffer(buf, dtype="<i4", count=2 * n_cands, offset=co).reshape(-1, 2)
     mo = co + 8 * n_cands
-    masks = np.frombuffer(buf, dtype="<u4", count=n_cands * n_words, offset=mo).reshape(n_cands, n_words) \
-        if n_words else np.zeros((n_cands, 0), dtype=np.uint32)
-    bo = (mo + 4 * n_cands * n_words + 7) & ~7
+    masks = np.frombuffer(buf, dtype="<u4", count=n_cands * n_words, offset=mo).reshape(n_cands, n_words)
+    bo = off + _align(mo - off + 4 * n_cands * n_words, 8)
     breaks = np.frombuffer(buf, dtype="<f8", count=n_breaks, offset=bo)
-    return edges, cands, masks, breaks
-
-
-def resolve(arena: np.ndarray, entry: int, px: float, py: float) -> int:
-    edges, cands, masks, breaks = parse_record(arena, entry)
     bits = []
     for lx, ly, hx, hy in edges.tolist():
         bits.append(1 if (ly < py <= hy and _cross(px, py, lx, ly, hx, hy)) else 0)
@@ -60,10 +103,10 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float) -> int:
         nb = info >> 1
         par = info & 1
         for w in range(masks.shape[1]):
-            m = int(masks[c, w])
-            while m:
-                k = (m & -m).bit_length() - 1
-                m &= m - 1
+            mm = int(masks[c, w])
+            while mm:
+                k = (mm & -mm).bit_length() - 1
+                mm &= mm - 1
                 par ^= bits[w * 32 + k]
         for b in breaks[boff:boff + nb].tolist():
             par ^= 1 if py > b else 0
@@ -73,6 +116,14 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float) -> int:
     return -1
 
 
+def record_kinds(index_export) -> dict:
+    grid, arena, g = index_export
+    recs = np.unique(grid[(grid >= K_RECORD) & (grid != K_EMPTY)])
+    kinds = arena[((recs & np.uint32(OFFSET_MASK)).astype(np.int64)) * g["granule"]]
+    return {"compact": int((kinds == 1).sum()), "wide": int((kinds == 2).sum()),
+            "split": int((kinds == 3).sum())}
+
+
 def walk(index_export, pts: np.ndarray) -> np.ndarray:
     grid, arena, g = index_export
     pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 2)
@@ -80,5 +131,5 @@ def walk(index_export, pts: np.ndarray) -> np.ndarray:
     out = np.where(e < K_RECORD, e.astype(np.int64), -1).astype(np.int32)
     rec = np.nonzero((e >= K_RECORD) & (e != K_EMPTY))[0]
     for i in rec.tolist():
-        out[i] = resolve(arena, int(e[i]), float(pts[i, 0]), float(pts[i, 1]))
+        out[i] = resolve(arena, int(e[i]), float(pts[i, 0]), float(pts[i, 1]), g["granule"])
     return out

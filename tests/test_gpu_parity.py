@@ -1,0 +1,102 @@
+"""GPU parity: the sm_100a projection (through the C-ABI) against the CPU
+oracle, bit-exact, on the BASELINE configs and on edge cases."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from paper_2005_03156_b200 import fastmap, synth  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def project_device(idx, pts, dev):
+    d = torch.from_numpy(np.ascontiguousarray(pts)).to(dev)
+    out = idx.project(d)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def test_c1_full_million_points_bit_exact(dev):
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    pts = cfg.make_points()
+    idx = fastmap.build_index(soup, device=0)
+    got = project_device(idx, pts, dev)
+    want = oracle.assign(soup, pts)
+    assert np.array_equal(got, want)
+    assert (want >= 0).mean() > 0.97 and (want == -1).sum() > 0
+
+
+@pytest.mark.parametrize("name,n", [("c2", 2_000_000), ("c4", 1_000_000)])
+def test_large_configs_sampled_bit_exact(dev, name, n):
+    cfg = synth.config(name)
+    soup = cfg.make_soup()
+    pts = cfg.make_points(n, soup=soup)
+    idx = fastmap.build_index(soup, device=0)
+    got = project_device(idx, pts, dev)
+    want = oracle.assign(soup, pts)
+    assert int((got != want).sum()) == 0
+
+
+def test_host_path_and_histogram(dev):
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    pts = cfg.make_points(300_000, offset=5_000_000)
+    idx = fastmap.build_index(soup, device=0)
+    hist = np.zeros(soup.n_polys, dtype=np.int64)
+    got = idx.project(pts, hist=hist)
+    want = oracle.assign(soup, pts)
+    assert np.array_equal(got, want)
+    assert np.array_equal(hist, np.bincount(want[want >= 0], minlength=soup.n_polys))
+    # device histogram accumulates
+    dh = torch.zeros(soup.n_polys, dtype=torch.int64, device=dev)
+    d = torch.from_numpy(pts).to(dev)
+    idx.project(d, hist=dh)
+    idx.project(d, hist=dh)
+    torch.cuda.synchronize()
+    assert np.array_equal(dh.cpu().numpy(), 2 * hist)
+
+
+def test_counters(dev):
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    pts = cfg.make_points(100_000)
+    idx = fastmap.build_index(soup, device=0)
+    c = torch.zeros(4, dtype=torch.int64, device=dev)
+    d = torch.from_numpy(pts).to(dev)
+    out = idx.project(d, counters=c)
+    torch.cuda.synchronize()
+    c = c.cpu().numpy()
+    assert c[0] == len(pts) and 0 < c[1] < len(pts) and c[2] >= c[1]
+    assert np.array_equal(out.cpu().numpy(), oracle.assign(soup, pts))
+
+
+def test_edge_cases_bit_exact(dev):
+    import edge_cases
+    soup, pts = edge_cases.build()
+    idx = fastmap.build_index(soup, device=0)
+    got = project_device(idx, pts, dev)
+    want = oracle.exhaustive_assign(soup, pts)
+    assert np.array_equal(got, want)
+
+
+def test_empty_and_tiny_inputs(dev):
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    idx = fastmap.build_index(soup, device=0)
+    empty = torch.zeros((0, 2), dtype=torch.float64, device=dev)
+    assert idx.project(empty).numel() == 0
+    one = np.array([[-100.0, 35.0]])
+    assert np.array_equal(project_device(idx, one, dev), oracle.assign(soup, one))
+    # no polygons at all: everything is -1
+    none = fastmap.Soup.from_rings([])
+    idx0 = fastmap.build_index(none, device=0)
+    pts = cfg.make_points(1000)
+    assert (project_device(idx0, pts, dev) == -1).all()
