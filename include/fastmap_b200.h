@@ -72,8 +72,8 @@ typedef struct fm_index fm_index;
 /* Index build parameters (the analogue of CoverParams, cell_index.hpp:248-252).
  * Zero-initialise and set what you need. */
 typedef struct fm_build_params {
-  /* Grid resolution: cells per mean polygon bbox side.  0 = auto (sized so
-   * the cell table stays L2-resident, clamped to [4, 64]). */
+  /* Grid resolution: cells per mean polygon bbox side.  0 = auto
+   * (about 40M cells in total, clamped to [4, 64] per polygon side). */
   double cells_per_polygon;
   /* Explicit grid dimensions; both > 0 override cells_per_polygon. */
   int64_t nx, ny;

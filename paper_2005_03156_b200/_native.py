@@ -14,7 +14,8 @@ import pathlib
 
 _PKG = pathlib.Path(__file__).resolve().parent
 LIBDIR = _PKG / "_lib"
-PRODUCT_SO = LIBDIR / "libfastmap_b200.so"
+# FASTMAP_B200_LIB selects an alternate build of the product (tuning sweeps)
+PRODUCT_SO = pathlib.Path(os.environ.get("FASTMAP_B200_LIB", LIBDIR / "libfastmap_b200.so"))
 SYNTH_SO = LIBDIR / "libfastmap_synth.so"
 
 u64 = C.c_uint64

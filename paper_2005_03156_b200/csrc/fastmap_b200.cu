@@ -34,7 +34,15 @@ fm_status set_err(fm_status s, const std::string& msg) {
   return s;
 }
 
-constexpr int kBlock = 256;
+#ifndef FM_KU
+#define FM_KU 2
+#endif
+#ifndef FM_BWARPS
+#define FM_BWARPS 8
+#endif
+#ifndef FM_BPOOL
+#define FM_BPOOL 3072
+#endif
 constexpr int kStreams = 3;
 constexpr std::uint64_t kChunkPoints = std::uint64_t{1} << 23;  // 8M points = 128 MiB
 
@@ -58,35 +66,51 @@ struct DeviceGuard {
     }                                                                        \
   } while (0)
 
-// Kernel configuration.  kWarps warps per CTA; each warp streams tiles of
-// 32*kU points.  Points in boundary cells are parked in a per-warp
-// shared-memory queue and resolved up to 32 at a time with all lanes busy:
-// the batch's records (their sizes come from the grid entries) are copied
-// into a per-warp shared pool by cooperative cp.async -- half a warp per
-// record, so one instruction moves two records -- in a single round trip,
-// then each lane evaluates its own record from shared memory.  A point in
-// a split cell is re-queued with the child's entry.
-constexpr int kWarps = 8;
-constexpr int kU = 2;
-constexpr int kQCap = 32 * kU + 32;
-constexpr int kPool = 4096;  // bytes of record staging per warp
+// Two kernels per query:
+//  stream_kernel  -- the HBM stream.  Each warp walks tiles of 32*kU points
+//    (next tile loaded one tile ahead), locates each point's cell, answers
+//    true-hit / empty cells at once, and appends boundary points (24-byte
+//    items) to its own private region of a global queue: no atomics, fully
+//    coalesced appends.  Small shared/register footprint -> high occupancy.
+//  resolve_kernel -- one warp per queue region.  Items are taken 32 at a
+//    time; the records of batch k+1 (sizes come from the grid entries) are
+//    copied into a double-buffered shared pool by cooperative cp.async while
+//    batch k is evaluated, so record latency overlaps compute.  Evaluation
+//    spreads the (item, edge) crossing tests over all 32 lanes.
+constexpr int kU = FM_KU;
+constexpr int kAWarps = 8;
+constexpr int kBWarps = FM_BWARPS;
+constexpr int kPool = FM_BPOOL;  // bytes per pool buffer (two per warp)
 
-struct WarpSmem {
-  double qx[kQCap];
-  double qy[kQCap];
-  unsigned long long qi[kQCap];
-  std::uint32_t qe[kQCap];
-  std::uint32_t bstart[32];  // pool offset (16-byte chunks) per batch slot
-  std::uint32_t bsize[32];   // chunks per batch slot
+struct QItem {  // 24 bytes
+  double px, py;
+  std::uint32_t i;  // point index within the launch
+  std::uint32_t e;  // grid entry of the boundary cell
+};
+
+struct BatchSmem {
+  const std::uint8_t* bsrc[32];  // record address per item
+  std::uint32_t bstart[32];      // pool chunk per item
+  std::uint8_t ctab[kPool / 16]; // pool chunk -> item
   alignas(16) std::uint8_t pool[kPool];
+};
+
+struct WarpSmemB {
+  BatchSmem buf[2];
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait0() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 template <bool kHist>
@@ -96,126 +120,33 @@ __device__ __forceinline__ void emit(int* __restrict__ out, unsigned long long* 
   if (kHist && id >= 0) atomicAdd(hist + id, 1ull);
 }
 
-constexpr int kRequeue = INT_MIN;
-
-// Resolve the batch S.q*[k0 .. k0+cnt-1] (cnt <= 32; lane l owns item
-// k0 + l).  Returns the leaf id, -1, or kRequeue with *next_e set.
-template <bool kCount>
-__device__ __forceinline__ int resolve_batch(const fm::KParams& P, WarpSmem& S, int lane,
-                                             int k0, int cnt, std::uint32_t* next_e,
-                                             fm::WorkCount& wc) {
-  const bool mine = lane < cnt;
-  const std::uint32_t e = mine ? S.qe[k0 + lane] : 0u;
-  const std::uint32_t chunks = mine ? fm::entry_fetch_bytes(e) / 16 : 0u;
-  // exclusive scan of chunk counts -> pool layout
-  std::uint32_t incl = chunks;
+__device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, int lane,
+                                                        std::uint32_t* total) {
+  std::uint32_t incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const std::uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= o) incl += v;
+    const std::uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += t;
   }
-  const std::uint32_t start = incl - chunks;
-  S.bstart[lane] = start;
-  S.bsize[lane] = chunks;
-  __syncwarp();
-  // cooperative copy: iteration m moves slots 2m (lanes 0-15) and 2m+1 (16-31)
-  const int half = lane >> 4, c = lane & 15;
-  for (int m = 0; 2 * m < cnt; ++m) {
-    const int slot = 2 * m + half;
-    if (slot < cnt && static_cast<std::uint32_t>(c) < S.bsize[slot]) {
-      const std::uint8_t* rec = fm::record_ptr(P, S.qe[k0 + slot]);
-      cp_async16(S.pool + 16 * (S.bstart[slot] + c), rec + 16 * c);
-    }
-  }
-  cp_async_wait_all();
-  __syncwarp();
-  if (!mine) return -1;
-  const double px = S.qx[k0 + lane], py = S.qy[k0 + lane];
-  const fm::SmemReader W{S.pool + 16 * start};
-  const std::uint32_t h = W.u32(0);
-  const std::uint32_t kind = h & 0xFFu;
-  if (kind == fm::kKindSplit) {
-    const double x0 = W.f64(8), y0 = W.f64(16), ihw = W.f64(24), ihh = W.f64(32);
-    int i = static_cast<int>(__dmul_rn(__dsub_rn(px, x0), ihw));
-    int j = static_cast<int>(__dmul_rn(__dsub_rn(py, y0), ihh));
-    i = min(max(i, 0), 1);
-    j = min(max(j, 0), 1);
-    const std::uint32_t ce = W.u32(40 + 4 * (2 * j + i));
-    if (ce == fm::kEmpty) return -1;
-    if (ce < fm::kRecordBit) return static_cast<int>(ce);
-    *next_e = ce;
-    return kRequeue;
-  }
-  if (kCount) wc.boundary++;
-  if (kind == fm::kKindCompact) {
-    const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
-    if (fm::compact_bytes(nv, nc, nb) <= 16u * chunks) {
-      return fm::resolve_compact<kCount>(W, h, px, py, wc);
-    }
-    return fm::resolve_compact<kCount>(fm::GlobalReader{fm::record_ptr(P, e)}, h, px, py, wc);
-  }
-  return fm::resolve_wide<kCount>(fm::record_ptr(P, e), px, py, wc);
-}
-
-// Pop up to 32 items off the top of the queue (as many as the pool holds),
-// resolve them, emit the finished ones and push split descents back.
-template <bool kHist, bool kCount>
-__device__ __forceinline__ void drain_once(const fm::KParams& P, WarpSmem& S, int lane, int& qn,
-                                           int* __restrict__ out,
-                                           unsigned long long* __restrict__ hist,
-                                           fm::WorkCount& wc) {
-  const int cnt = min(qn, 32);
-  // the batch is the top `take` items, as many as fit the pool (items are at
-  // most 256 bytes, so at least 16 always fit): scan sizes from the top
-  const std::uint32_t bytes = lane < cnt ? fm::entry_fetch_bytes(S.qe[qn - 1 - lane]) : 0u;
-  std::uint32_t incl = bytes;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const std::uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const int take = __popc(__ballot_sync(0xFFFFFFFFu, lane < cnt && incl <= kPool));
-  const int b0 = qn - take;
-  const double px = lane < take ? S.qx[b0 + lane] : 0.0;
-  const double py = lane < take ? S.qy[b0 + lane] : 0.0;
-  const std::uint64_t i = lane < take ? S.qi[b0 + lane] : 0ull;
-  std::uint32_t ne = 0;
-  const int id = resolve_batch<kCount>(P, S, lane, b0, take, &ne, wc);
-  __syncwarp();
-  qn = b0;
-  const bool requeue = lane < take && id == kRequeue;
-  if (lane < take && !requeue) emit<kHist>(out, hist, i, id);
-  const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, requeue);
-  if (requeue) {
-    const int pos = qn + __popc(b & ((1u << lane) - 1u));
-    S.qx[pos] = px;
-    S.qy[pos] = py;
-    S.qi[pos] = i;
-    S.qe[pos] = ne;
-  }
-  qn += __popc(b);
-  __syncwarp();
+  *total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  return incl - v;
 }
 
 template <bool kHist, bool kCount>
-__global__ void __launch_bounds__(kWarps * 32)
-    project_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
-                   int* __restrict__ out, unsigned long long* __restrict__ hist,
-                   unsigned long long* __restrict__ counters) {
-  extern __shared__ __align__(16) unsigned char dsmem[];
-  WarpSmem* smem = reinterpret_cast<WarpSmem*>(dsmem);
+__global__ void __launch_bounds__(kAWarps * 32)
+    stream_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
+                  int* __restrict__ out, unsigned long long* __restrict__ hist,
+                  QItem* __restrict__ q, std::uint32_t* __restrict__ qcount,
+                  std::uint64_t region_cap, unsigned long long* __restrict__ counters) {
   const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  WarpSmem& S = smem[wid];
-  const std::uint32_t lt_mask = (1u << lane) - 1u;
   const std::uint64_t tile = 32ull * kU;
   const std::uint64_t n_tiles = (n + tile - 1) / tile;
-  const std::uint64_t gwarp = static_cast<std::uint64_t>(blockIdx.x) * kWarps + wid;
-  const std::uint64_t nwarps = static_cast<std::uint64_t>(gridDim.x) * kWarps;
-  fm::WorkCount wc;
-  unsigned long long n_done = 0;
-  int qn = 0;
-  double2 pn[kU];  // next tile's points, loaded one tile ahead
+  const std::uint64_t gwarp = static_cast<std::uint64_t>(blockIdx.x) * kAWarps + (threadIdx.x >> 5);
+  const std::uint64_t nwarps = static_cast<std::uint64_t>(gridDim.x) * kAWarps;
+  QItem* __restrict__ my = q + gwarp * region_cap;
+  std::uint32_t cnt = 0;
+  const std::uint32_t lt_mask = (1u << lane) - 1u;
+  double2 pn[kU];
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const std::uint64_t i = gwarp * tile + u * 32 + lane;
@@ -241,37 +172,168 @@ __global__ void __launch_bounds__(kWarps * 32)
       const bool valid = i < n;
       const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
       if (valid && !is_rec) emit<kHist>(out, hist, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
-      if (kCount && valid) ++n_done;
       const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec);
       if (is_rec) {
-        const int pos = qn + __popc(b & lt_mask);
-        S.qx[pos] = p[u].x;
-        S.qy[pos] = p[u].y;
-        S.qi[pos] = i;
-        S.qe[pos] = e[u];
+        QItem it;
+        it.px = p[u].x;
+        it.py = p[u].y;
+        it.i = static_cast<std::uint32_t>(i);
+        it.e = e[u];
+        my[cnt + __popc(b & lt_mask)] = it;
       }
-      qn += __popc(b);
+      cnt += __popc(b);
     }
-    __syncwarp();
-    while (qn >= 32) drain_once<kHist, kCount>(P, S, lane, qn, out, hist, wc);
   }
-  while (qn > 0) drain_once<kHist, kCount>(P, S, lane, qn, out, hist, wc);
+  if (gwarp < nwarps && lane == 0) qcount[gwarp] = cnt;
   if (kCount) {
-    unsigned long long v[4] = {n_done, wc.boundary, wc.cands, wc.edges};
+    unsigned long long v = 0;
+    for (std::uint64_t t = gwarp; t < n_tiles; t += nwarps) {
+      const std::uint64_t base = t * tile;
+      v += min(tile, n - base);
+    }
+    if (lane == 0) atomicAdd(counters + 0, v);
+  }
+}
+
+// Split cells (rare): descend from global memory, then resolve the leaf.
+template <bool kCount>
+__device__ __noinline__ int resolve_global(const fm::KParams& P, const std::uint8_t* rec,
+                                           double px, double py, fm::WorkCount& wc) {
+  for (int depth = 0; depth <= fm::kMaxSplitDepth + 1; ++depth) {
+    const std::uint32_t h = __ldg(reinterpret_cast<const std::uint32_t*>(rec));
+    const std::uint32_t kind = h & 0xFFu;
+    if (kind == fm::kKindCompact) {
+      return fm::resolve_compact<kCount>(fm::GlobalReader{rec}, h, px, py, wc);
+    }
+    if (kind == fm::kKindWide) return fm::resolve_wide<kCount>(rec, px, py, wc);
+    const double* d = reinterpret_cast<const double*>(rec + 8);
+    const double x0 = __ldg(d), y0 = __ldg(d + 1), ihw = __ldg(d + 2), ihh = __ldg(d + 3);
+    int ci = static_cast<int>(__dmul_rn(__dsub_rn(px, x0), ihw));
+    int cj = static_cast<int>(__dmul_rn(__dsub_rn(py, y0), ihh));
+    ci = min(max(ci, 0), 1);
+    cj = min(max(cj, 0), 1);
+    const std::uint32_t ce = __ldg(reinterpret_cast<const std::uint32_t*>(rec + 40) + 2 * cj + ci);
+    if (ce == fm::kEmpty) return -1;
+    if (ce < fm::kRecordBit) return static_cast<int>(ce);
+    rec = fm::record_ptr(P, ce);
+  }
+  return -1;  // unreachable for a well-formed index
+}
+
+// Choose the next batch (items [next, next+take) of the region, as many as
+// fit the pool, <= 32) and start copying its records into `B`.
+__device__ __forceinline__ int stage_batch(const fm::KParams& P, const QItem* __restrict__ items,
+                                           std::uint32_t next, std::uint32_t cnt, BatchSmem& B,
+                                           int lane, QItem* it) {
+  const std::uint32_t avail = min(cnt - next, 32u);
+  const bool have = static_cast<std::uint32_t>(lane) < avail;
+  if (have) *it = items[next + lane];
+  const std::uint32_t bytes = have ? fm::entry_fetch_bytes(it->e) : 0u;
+  std::uint32_t tot;
+  const std::uint32_t before = warp_excl_scan(bytes, lane, &tot);
+  const bool fits = have && before + bytes <= static_cast<std::uint32_t>(kPool);
+  const int take = __popc(__ballot_sync(0xFFFFFFFFu, fits));
+  const std::uint32_t chunks = fits ? bytes / 16 : 0u;
+  std::uint32_t C;
+  const std::uint32_t start = warp_excl_scan(chunks, lane, &C);
+  if (fits) {
+    B.bstart[lane] = start;
+    B.bsrc[lane] = fm::record_ptr(P, it->e);
+    for (std::uint32_t c = 0; c < chunks; ++c) B.ctab[start + c] = static_cast<std::uint8_t>(lane);
+  }
+  __syncwarp();
+  for (std::uint32_t j = lane; j < C; j += 32) {
+    const int L = B.ctab[j];
+    cp_async16(B.pool + 16 * j, B.bsrc[L] + 16 * (j - B.bstart[L]));
+  }
+  cp_async_commit();
+  return take;
+}
+
+// Evaluate a staged batch of `take` items (lane l owns item l).
+template <bool kHist, bool kCount>
+__device__ __forceinline__ void evaluate_batch(const fm::KParams& P, const BatchSmem& B, int lane,
+                                               int take, const QItem& it, int* __restrict__ out,
+                                               unsigned long long* __restrict__ hist,
+                                               fm::WorkCount& wc) {
+  if (lane < take) {
+    const fm::SmemReader R{B.pool + 16 * B.bstart[lane]};
+    const std::uint32_t h = R.u32(0);
+    const std::uint32_t kind = h & 0xFFu;
+    const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
+    int id;
+    if (kind == fm::kKindCompact && fm::compact_bytes(nv, nc, nb) <= fm::entry_fetch_bytes(it.e)) {
+      if (kCount) wc.boundary++;
+      id = fm::resolve_compact<kCount>(R, h, it.px, it.py, wc);
+    } else {  // split cells, oversized and wide records: from global memory
+      if (kCount && kind != fm::kKindSplit) wc.boundary++;
+      id = resolve_global<kCount>(P, fm::record_ptr(P, it.e), it.px, it.py, wc);
+    }
+    emit<kHist>(out, hist, it.i, id);
+  }
+  __syncwarp();
+}
+
+template <bool kHist, bool kCount>
+__global__ void __launch_bounds__(kBWarps * 32)
+    resolve_kernel(fm::KParams P, const QItem* __restrict__ q,
+                   const std::uint32_t* __restrict__ qcount, std::uint64_t n_regions,
+                   std::uint64_t region_cap, unsigned long long* __restrict__ next_region,
+                   int* __restrict__ out, unsigned long long* __restrict__ hist,
+                   unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char dsmem[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  WarpSmemB& S = reinterpret_cast<WarpSmemB*>(dsmem)[wid];
+  fm::WorkCount wc;
+  for (;;) {
+    std::uint64_t region = 0;
+    if (lane == 0) region = atomicAdd(next_region, 1ull);
+    region = __shfl_sync(0xFFFFFFFFu, region, 0);
+    if (region >= n_regions) break;
+    const QItem* items = q + region * region_cap;
+    const std::uint32_t cnt = qcount[region];
+    std::uint32_t next = 0;
+    int cur = 0;
+    QItem it{};
+    int take = 0;
+    if (cnt > 0) {
+      take = stage_batch(P, items, 0, cnt, S.buf[0], lane, &it);
+      next = static_cast<std::uint32_t>(take);
+    }
+    while (take > 0) {
+      QItem it_next{};
+      int take_next = 0;
+      if (next < cnt) {
+        take_next = stage_batch(P, items, next, cnt, S.buf[cur ^ 1], lane, &it_next);
+        cp_async_wait1();
+      } else {
+        cp_async_wait0();
+      }
+      __syncwarp();
+      evaluate_batch<kHist, kCount>(P, S.buf[cur], lane, take, it, out, hist, wc);
+      next += static_cast<std::uint32_t>(take_next);
+      take = take_next;
+      it = it_next;
+      cur ^= 1;
+    }
+  }
+  if (kCount) {
+    unsigned long long v[3] = {wc.boundary, wc.cands, wc.edges};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 3; ++k) {
       for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xFFFFFFFFu, v[k], o);
     }
     if (lane == 0) {
-      for (int k = 0; k < 4; ++k) atomicAdd(counters + k, v[k]);
+      for (int k = 0; k < 3; ++k) atomicAdd(counters + 1 + k, v[k]);
     }
   }
 }
 
-constexpr int kSmemBytes = static_cast<int>(sizeof(WarpSmem)) * kWarps;
+constexpr int kSmemB = static_cast<int>(sizeof(WarpSmemB)) * kBWarps;
 
-int grid_size_for(int device, std::uint64_t n, const void* kernel) {
-  // resident CTAs per SM x SM count, cached per (device, kernel)
+int resident_blocks(int device, const void* kernel, int block, int smem) {
+  // SM count x resident CTAs per SM, cached per (device, kernel)
   struct Slot {
     int device;
     const void* kernel;
@@ -279,24 +341,17 @@ int grid_size_for(int device, std::uint64_t n, const void* kernel) {
   };
   static std::mutex mu;
   static std::vector<Slot> cache;
-  int blocks = 0;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    for (const Slot& s : cache) {
-      if (s.device == device && s.kernel == kernel) blocks = s.blocks;
-    }
-    if (blocks == 0) {
-      int sms = 0, per_sm = 0;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, kSmemBytes);
-      blocks = std::max(1, sms) * std::max(1, per_sm);
-      cache.push_back({device, kernel, blocks});
-    }
+  std::lock_guard<std::mutex> lk(mu);
+  for (const Slot& s : cache) {
+    if (s.device == device && s.kernel == kernel) return s.blocks;
   }
-  const std::uint64_t per_cta = static_cast<std::uint64_t>(kBlock) * kU;
-  const std::uint64_t need = (n + per_cta - 1) / per_cta;
-  return static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(need, blocks)));
+  int sms = 0, per_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+  const int blocks = std::max(1, sms) * std::max(1, per_sm);
+  cache.push_back({device, kernel, blocks});
+  return blocks;
 }
 
 }  // namespace
@@ -339,25 +394,66 @@ fm::KParams kparams(const fm_index* ix) {
   return P;
 }
 
+template <bool kHist, bool kCount>
+fm_status launch_t(const fm_index* ix, const double2* pts, std::uint64_t n, int* d_out,
+                   unsigned long long* d_hist, unsigned long long* d_counters,
+                   cudaStream_t stream) {
+  const fm::KParams P = kparams(ix);
+  auto ka = stream_kernel<kHist, kCount>;
+  auto kb = resolve_kernel<kHist, kCount>;
+  const int blk_a = kAWarps * 32;
+  const std::uint64_t tile = 32ull * kU;
+  const std::uint64_t n_tiles = (n + tile - 1) / tile;
+  const int grid_a = static_cast<int>(std::max<std::uint64_t>(
+      1, std::min<std::uint64_t>((n_tiles + kAWarps - 1) / kAWarps,
+                                 resident_blocks(ix->device, (const void*)ka, blk_a, 0))));
+  const std::uint64_t n_regions = static_cast<std::uint64_t>(grid_a) * kAWarps;
+  const std::uint64_t region_cap = (n_tiles + n_regions - 1) / n_regions * tile;
+  // stream-ordered scratch: the boundary queue (24 B/item) and its counts
+  void* scratch = nullptr;
+  const std::uint64_t qbytes = n_regions * region_cap * sizeof(QItem);
+  FM_CUDA(cudaMallocAsync(&scratch, qbytes + n_regions * 4 + 16, stream));
+  QItem* q = static_cast<QItem*>(scratch);
+  std::uint32_t* qcount = reinterpret_cast<std::uint32_t*>(static_cast<char*>(scratch) + qbytes);
+  unsigned long long* next_region =
+      reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) + qbytes + n_regions * 4);
+  if ((reinterpret_cast<std::uintptr_t>(next_region) & 7u) != 0) {
+    next_region = reinterpret_cast<unsigned long long*>((reinterpret_cast<std::uintptr_t>(next_region) + 7) & ~std::uintptr_t{7});
+  }
+  FM_CUDA(cudaMemsetAsync(next_region, 0, 8, stream));
+  ka<<<grid_a, blk_a, 0, stream>>>(P, pts, n, d_out, d_hist, q, qcount, region_cap, d_counters);
+  // persistent resolve grid: resident CTAs pull regions from a counter
+  const int grid_b = static_cast<int>(std::min<std::uint64_t>(
+      (n_regions + kBWarps - 1) / kBWarps,
+      resident_blocks(ix->device, (const void*)kb, kBWarps * 32, kSmemB)));
+  kb<<<grid_b, kBWarps * 32, kSmemB, stream>>>(P, q, qcount, n_regions, region_cap, next_region,
+                                               d_out, d_hist, d_counters);
+  const cudaError_t err = cudaGetLastError();
+  FM_CUDA(cudaFreeAsync(scratch, stream));
+  if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));
+  return FM_OK;
+}
+
 fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* d_out,
                  unsigned long long* d_hist, unsigned long long* d_counters,
                  cudaStream_t stream) {
-  const fm::KParams P = kparams(ix);
   const double2* pts = reinterpret_cast<const double2*>(d_pts);
-  if (d_hist && d_counters) {
-    auto k = project_kernel<true, true>;
-    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, kSmemBytes, stream>>>(P, pts, n, d_out, d_hist, d_counters);
-  } else if (d_hist) {
-    auto k = project_kernel<true, false>;
-    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, kSmemBytes, stream>>>(P, pts, n, d_out, d_hist, d_counters);
-  } else if (d_counters) {
-    auto k = project_kernel<false, true>;
-    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, kSmemBytes, stream>>>(P, pts, n, d_out, d_hist, d_counters);
-  } else {
-    auto k = project_kernel<false, false>;
-    k<<<grid_size_for(ix->device, n, (const void*)k), kBlock, kSmemBytes, stream>>>(P, pts, n, d_out, d_hist, d_counters);
+  // slices of 2^28 points bound the queue scratch (24 B/point) to 6.4 GB
+  const std::uint64_t slice = std::uint64_t{1} << 28;
+  for (std::uint64_t off = 0; off < n; off += slice) {
+    const std::uint64_t m = std::min(slice, n - off);
+    fm_status st;
+    if (d_hist && d_counters) {
+      st = launch_t<true, true>(ix, pts + off, m, d_out + off, d_hist, d_counters, stream);
+    } else if (d_hist) {
+      st = launch_t<true, false>(ix, pts + off, m, d_out + off, d_hist, d_counters, stream);
+    } else if (d_counters) {
+      st = launch_t<false, true>(ix, pts + off, m, d_out + off, d_hist, d_counters, stream);
+    } else {
+      st = launch_t<false, false>(ix, pts + off, m, d_out + off, d_hist, d_counters, stream);
+    }
+    if (st != FM_OK) return st;
   }
-  FM_CUDA(cudaGetLastError());
   return FM_OK;
 }
 
@@ -508,6 +604,12 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
       free_device(ix);
       delete ix;
       return set_err(FM_ERR_CUDA, "index upload failed");
+    }
+    // keep stream-ordered scratch (the boundary queue) cached between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ix->device) == cudaSuccess) {
+      std::uint64_t thr = ~std::uint64_t{0};
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     // the device copy is authoritative; drop the host arrays
     std::vector<std::uint32_t>().swap(ix->host.grid);
