@@ -1,0 +1,91 @@
+"""The index builder, checked on the CPU: a host-only index (device=-1) is
+exported and walked by tests/index_walk.py (a Python restatement of the
+query kernel's record walk) and compared with the oracle bit for bit."""
+import numpy as np
+import pytest
+
+import edge_cases
+import index_walk
+import oracle
+from paper_2005_03156_b200 import fastmap, synth
+
+
+def walk(soup, pts, **params):
+    idx = fastmap.build_index(soup, fastmap.CoverParams(**params), device=-1)
+    ex = idx.export()
+    return index_walk.walk(ex, pts), idx, ex
+
+
+def test_c1_index_exact():
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    pts = cfg.make_points(100_000, offset=777)
+    got, idx, ex = walk(soup, pts)
+    assert np.array_equal(got, oracle.assign(soup, pts))
+    st = idx.stats()
+    assert st["cells_boundary"] > 0 and st["cells_hit"] > st["cells_boundary"]
+
+
+@pytest.mark.parametrize("name,m", [("c2", 6), ("c2", 14), ("c4", 12), ("c4", 24)])
+def test_large_config_index_exact_sampled(name, m):
+    cfg = synth.config(name)
+    soup = cfg.make_soup()
+    pts = cfg.make_points(8_000, soup=soup, offset=12345)
+    got, _, _ = walk(soup, pts, cells_per_polygon=m)
+    assert np.array_equal(got, oracle.assign(soup, pts))
+
+
+@pytest.mark.parametrize("grid", [(1, 1), (2, 3), (7, 5), (97, 13), (400, 300)])
+def test_edge_cases_every_resolution(grid):
+    soup, pts = edge_cases.build()
+    got, _, ex = walk(soup, pts, nx=grid[0], ny=grid[1])
+    assert np.array_equal(got, oracle.exhaustive_assign(soup, pts))
+
+
+def test_edge_cases_use_wide_and_split_records():
+    soup, pts = edge_cases.build()
+    _, _, ex = walk(soup, pts, nx=1, ny=1)
+    kinds = index_walk.record_kinds(ex)
+    assert kinds["split"] >= 1
+    got, _, _ = walk(soup, pts, nx=1, ny=1)
+    assert np.array_equal(got, oracle.exhaustive_assign(soup, pts))
+
+
+def test_acceptance_fixture_index_exact():
+    import pathlib
+    g = np.load(pathlib.Path(__file__).parent / "golden" / "acceptance_4x4x25.npz")
+    soup = fastmap.Soup(g["vxy"], g["ring_off"], g["poly_ring"])
+    got, _, _ = walk(soup, g["pts"])
+    assert np.array_equal(got, g["exhaustive"])
+
+
+def test_empty_soup_and_zero_ring_polygons():
+    empty = fastmap.Soup.from_rings([])
+    got, idx, _ = walk(empty, np.array([[0.0, 0.0], [10.0, 10.0]]))
+    assert (got == -1).all()
+    soup = fastmap.Soup.from_rings([[], [[(0, 0), (1, 0), (1, 1), (0, 1)]], []])
+    pts = np.array([[0.5, 0.5], [2.0, 2.0], [0.0, 0.0]])
+    got, _, _ = walk(soup, pts)
+    assert np.array_equal(got, oracle.exhaustive_assign(soup, pts))
+    assert got[0] == 1
+
+
+def test_record_invariants():
+    """Compact records: ascending candidate ids, chain vertices oriented
+    edges never horizontal, masks inside the vertex range."""
+    import struct
+    cfg = synth.config("c1")
+    _, _, (grid, arena, g) = walk(cfg.make_soup(), np.zeros((1, 2)))
+    recs = np.unique(grid[(grid >= 0x80000000) & (grid != 0xFFFFFFFF)])[:2000]
+    for e in recs.tolist():
+        off = (e & ((1 << 27) - 1)) * g["granule"]
+        kind, nv, nc, nb = arena[off:off + 4].tolist()
+        if kind != 1:
+            continue
+        ids = [struct.unpack_from("<i", arena.data, off + 8 + 8 * c)[0] for c in range(nc)]
+        masks = [struct.unpack_from("<I", arena.data, off + 12 + 8 * c)[0] for c in range(nc)]
+        assert ids == sorted(ids) and len(set(ids)) == len(ids)
+        for mk in masks:
+            assert mk < (1 << max(nv - 1, 0)) or mk == 0
+        size = (e >> 27) & 15
+        assert 16 * (size + 1) >= 8  # size code present
