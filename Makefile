@@ -32,18 +32,23 @@ $(LIBDIR)/libfastmap_synth.so: $(PKG)/csrc/synth.cpp
 	@mkdir -p $(LIBDIR)
 	$(CXX) -std=c++17 $(HOSTFLAGS) -shared $< -o $@
 
-oracle/liboracle.so: oracle/oracle.c
-	$(CC) -std=c11 -O2 -fPIC -ffp-contract=off -pthread -shared $< -o $@ -lm
+oracle/liboracle.so: oracle/oracle.c oracle/Makefile
+	$(MAKE) --no-print-directory -f oracle/Makefile $(CURDIR)/oracle/liboracle.so
 
 # reference-compiled oracle: the unmodified reference headers, read in place
-ref:
+ref: product
 	@if [ -d "$(REF)/proj/include/fastmap" ]; then \
-	  $(MAKE) --no-print-directory oracle/_ref/libfastmap_ref.so; \
+	  $(MAKE) --no-print-directory oracle/_ref/libfastmap_ref.so oracle/_ref/adapter_check; \
 	else echo "reference sources absent: using prebuilt oracle/_ref (if any)"; fi
 
-oracle/_ref/libfastmap_ref.so: oracle/ref_shim.cpp
+oracle/_ref/libfastmap_ref.so: oracle/ref_shim.cpp oracle/Makefile
+	$(MAKE) --no-print-directory -f oracle/Makefile REF=$(REF) $(CURDIR)/oracle/_ref/libfastmap_ref.so
+
+# the C++ drop-in adapter compiled against the reference's own headers
+oracle/_ref/adapter_check: tests/cpp/adapter_check.cpp include/fastmap_b200/fastmap_gpu.hpp include/fastmap_b200.h $(LIBDIR)/libfastmap_b200.so
 	@mkdir -p oracle/_ref
-	$(CXX) -std=c++20 $(HOSTFLAGS) -I$(REF)/proj/include -shared $< -o $@
+	$(CXX) -std=c++20 -O2 -ffp-contract=off -I$(REF)/proj/include -Iinclude $< \
+	  -L$(LIBDIR) -lfastmap_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -o $@
 
 clean:
 	rm -rf $(LIBDIR) oracle/liboracle.so oracle/_ref

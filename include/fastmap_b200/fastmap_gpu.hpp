@@ -1,0 +1,191 @@
+// fastmap_gpu.hpp -- C++ drop-in adapter: the reference's build/query
+// interface (proj/include/fastmap/cell_index.hpp) backed by the B200 C-ABI
+// (include/fastmap_b200.h).
+//
+// Include it next to the reference headers (it uses the reference's own
+// Point, LeafRegion, RegionHierarchy, CoverParams, CoverMode and
+// AssignmentResult types) and link libfastmap_b200.so.  A call site that
+// reads
+//
+//     const auto cover = build_cover(leaves, params);          // cell_index.hpp:396
+//     const auto trie  = build_trie(cover, 4);                  // cell_index.hpp:453
+//     auto res = query_leaves(trie, leaves, pts, CoverMode::exact);  // :527
+//
+// becomes
+//
+//     const auto index = fastmap::gpu::build_index(leaves, params);
+//     auto res = fastmap::gpu::query_leaves(index, leaves, pts, CoverMode::exact);
+//
+// with the same AssignmentResult (state / county / block per point, -1 when
+// unassigned) and the same exception types:
+//   std::invalid_argument  bad parameters, fanout, approx on exact, leaf-table
+//                          mismatch, rings with < 3 vertices
+//   std::runtime_error     reference limits, CUDA failures, no CUDA device
+//                          (there is no CPU fallback)
+// Answers follow exhaustive_assign semantics (synthetic.hpp:193-205): the
+// first leaf, ascending, whose point_in_polygon is true; identical to
+// query_leaves(exact) on every valid tiling.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fastmap/cell_index.hpp"
+#include "fastmap/geometry.hpp"
+#include "fastmap/hierarchy.hpp"
+#include "fastmap/simple_mapper.hpp"
+#include "fastmap_b200.h"
+
+namespace fastmap::gpu {
+
+namespace detail {
+
+[[noreturn]] inline void throw_status(fm_status s, const char* what) {
+  std::string msg = std::string(what) + ": " + fm_last_error();
+  switch (s) {
+    case FM_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case FM_ERR_DOMAIN: throw std::domain_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+inline void check(fm_status s, const char* what) {
+  if (s != FM_OK) throw_status(s, what);
+}
+
+struct IndexDeleter {
+  void operator()(fm_index* p) const { fm_index_destroy(p); }
+};
+
+}  // namespace detail
+
+/// Knobs of the GPU index beyond CoverParams (which is validated exactly as
+/// validate_cover_params does, cell_index.hpp:382-394).
+struct IndexParams {
+  double cells_per_polygon = 0.0;  // 0 = auto
+  int device = 0;                  // CUDA ordinal; -1 = host-only (export, no queries)
+  int threads = 0;                 // host build threads (0 = all)
+};
+
+/// RAII owner of an fm_index (the CellCover + TrieIndex analogue).
+class CellIndex {
+ public:
+  CellIndex() = default;
+  explicit CellIndex(fm_index* p, std::size_t n_leaves) : h_(p), n_leaves_(n_leaves) {}
+  fm_index* get() const { return h_.get(); }
+  std::size_t n_leaves() const { return n_leaves_; }
+  fm_index_stats stats() const {
+    fm_index_stats s{};
+    detail::check(fm_index_stats_get(h_.get(), &s), "fm_index_stats_get");
+    return s;
+  }
+
+ private:
+  std::unique_ptr<fm_index, detail::IndexDeleter> h_;
+  std::size_t n_leaves_ = 0;
+};
+
+/// build_cover + build_trie over a leaf table (cell_index.hpp:396-400, :453).
+inline CellIndex build_index(std::span<const LeafRegion> leaves,
+                             const CoverParams& params = {},
+                             const IndexParams& ip = {}) {
+  validate_cover_params(params);  // the reference's own validation
+  std::vector<double> vxy;
+  std::vector<std::uint64_t> ring_off{0}, poly_ring{0};
+  for (const LeafRegion& leaf : leaves) {
+    if (leaf.geometry != nullptr) {
+      const PolygonGeometry& g = *leaf.geometry;
+      for (std::size_t r = 0; r < g.ring_starts.size(); ++r) {
+        const std::uint32_t b = g.ring_starts[r];
+        const std::uint32_t e = r + 1 < g.ring_starts.size()
+                                    ? g.ring_starts[r + 1]
+                                    : static_cast<std::uint32_t>(g.nodes.size());
+        for (std::uint32_t v = b; v < e; ++v) {
+          vxy.push_back(g.nodes[v].lon);
+          vxy.push_back(g.nodes[v].lat);
+        }
+        ring_off.push_back(vxy.size() / 2);
+      }
+    }
+    poly_ring.push_back(ring_off.size() - 1);
+  }
+  fm_build_params bp{};
+  bp.cells_per_polygon = ip.cells_per_polygon;
+  bp.device = ip.device;
+  bp.build_on_gpu = ip.device >= 0 ? 1 : 0;
+  bp.threads = ip.threads;
+  fm_index* h = nullptr;
+  detail::check(fm_index_build(vxy.data(), ring_off.data(), ring_off.size() - 1,
+                               poly_ring.data(), poly_ring.size() - 1, &bp, &h),
+                "fm_index_build");
+  return CellIndex(h, leaves.size());
+}
+
+inline CellIndex build_index(const RegionHierarchy& h, const CoverParams& params = {},
+                             const IndexParams& ip = {}) {
+  const auto leaves = collect_leaves(h);  // hierarchy.hpp:76-91
+  return build_index(leaves, params, ip);
+}
+
+/// Leaf id per point (collect_leaves position, -1 = none), host buffers.
+inline std::vector<std::int32_t> project(const CellIndex& index, std::span<const Point> points) {
+  std::vector<std::int32_t> out(points.size());
+  detail::check(fm_query_host(index.get(), reinterpret_cast<const double*>(points.data()),
+                              points.size(), out.data(), nullptr),
+                "fm_query_host");
+  return out;
+}
+
+/// Device-pointer variant (asynchronous on `stream`, a cudaStream_t).
+inline void project_device(const CellIndex& index, const Point* d_points, std::size_t n,
+                           std::int32_t* d_out, void* stream = nullptr,
+                           std::int64_t* d_hist = nullptr) {
+  detail::check(fm_query(index.get(), reinterpret_cast<const double*>(d_points), n, d_out,
+                         d_hist, nullptr, stream),
+                "fm_query");
+}
+
+/// query_leaves (cell_index.hpp:527-590): per-point (state, county, block)
+/// set exactly as set_leaf does (cell_index.hpp:515-519).
+inline AssignmentResult query_leaves(const CellIndex& index, std::span<const LeafRegion> leaves,
+                                     std::span<const Point> points, CoverMode mode) {
+  if (mode == CoverMode::approx) {
+    throw std::invalid_argument("approximate queries require an approximate-mode cover");
+  }
+  if (index.n_leaves() != leaves.size()) {
+    throw std::invalid_argument("cover was built for a different hierarchy");
+  }
+  const auto ids = project(index, points);
+  AssignmentResult res;
+  res.state.assign(points.size(), -1);
+  res.county.assign(points.size(), -1);
+  res.block.assign(points.size(), -1);
+  for (std::size_t i = 0; i < ids.size(); ++i) {
+    if (ids[i] < 0) continue;
+    const LeafRegion& leaf = leaves[static_cast<std::size_t>(ids[i])];
+    res.state[i] = static_cast<std::int32_t>(leaf.state);
+    res.county[i] = static_cast<std::int32_t>(leaf.county);
+    res.block[i] = static_cast<std::int32_t>(leaf.block);
+  }
+  return res;
+}
+
+inline AssignmentResult query(const CellIndex& index, const RegionHierarchy& h,
+                              std::span<const Point> points, CoverMode mode) {
+  const auto leaves = collect_leaves(h);  // cell_index.hpp:592-596
+  return query_leaves(index, leaves, points, mode);
+}
+
+/// exhaustive_assign semantics (synthetic.hpp:193-205) on the GPU.
+inline std::vector<std::int32_t> exhaustive_assign(std::span<const LeafRegion> leaves,
+                                                   std::span<const Point> points,
+                                                   int device = 0) {
+  const auto index = build_index(leaves, CoverParams{}, IndexParams{0.0, device, 0});
+  return project(index, points);
+}
+
+}  // namespace fastmap::gpu
