@@ -326,7 +326,9 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel": "project_kernel", "launch_ms": launch_ms},
+                         "kernel": "fm_query = stream_kernel + resolve_kernel",
+                         "launch_ms": launch_ms,
+                         "traffic_source": "profiles/ncu_%s_summary.json (ncu, cold cache)" % args.config},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,

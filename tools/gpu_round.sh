@@ -1,8 +1,17 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
-nproc; free -g | head -2
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 900 python bench.py --config c2 --steps 10 --warmup 3 --no-cpu > gpurun_out/bench_c2.log 2>&1; echo bench=$?
-timeout 600 python bench.py --config c2 --steps 2 --warmup 1 --no-cpu --no-e2e --points 20000000 > gpurun_out/bench_small.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:project_kernel --csv --log-file gpurun_out/launches_c2.csv python bench.py --config c2 --steps 2 --warmup 1 --no-cpu --no-e2e --points 20000000 > gpurun_out/ncu1.log 2>&1; echo ncu=$?
+# Full GPU round: tests, smoke, bench (ours + reference arm), ncu launch list
+# and full captures of both kernels.  Every step under its own timeout.
+TAG=${1:-round}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu_$TAG.txt 2>&1
+nproc >> gpurun_out/gpu_$TAG.txt; lscpu | grep -E "Model name|^CPU\(s\)" >> gpurun_out/gpu_$TAG.txt
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_$TAG.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.log
+timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?" >> gpurun_out/bench_$TAG.err
+timeout 900 python bench.py --impl reference > gpurun_out/benchref_$TAG.json 2> gpurun_out/benchref_$TAG.err; echo "ref rc=$?" >> gpurun_out/benchref_$TAG.err
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e"
+timeout 300 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -k regex:"stream_kernel|resolve_kernel" --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_l_$TAG.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"stream_kernel|resolve_kernel" -s 6 -c 2 \
+  -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_$TAG.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_$TAG.log
