@@ -147,8 +147,9 @@ fm_status fm_query_host(const fm_index* index, const double* h_lonlat, uint64_t 
 
 /* Copy of the index arrays to host memory (the FMCI-save analogue,
  * cell_index.hpp:641-664).  Two-call protocol: null buffers -> sizes.
+ * arena = the 128-byte slot arena followed by the overflow arena;
  * geometry16 (nullable) receives gx0, gx1, gy0, gy1, cell_w, cell_h, inv_w,
- * inv_h, nx, ny, margin, n_polys, granule, 0, 0, 0. */
+ * inv_h, nx, ny, margin, n_polys, slot-arena bytes, 0, 0, 0. */
 fm_status fm_index_export(const fm_index* index, uint32_t* grid, uint64_t* grid_len,
                           uint8_t* arena, uint64_t* arena_len, double* geometry16);
 

@@ -40,9 +40,7 @@ fm_status set_err(fm_status s, const std::string& msg) {
 #ifndef FM_BWARPS
 #define FM_BWARPS 8
 #endif
-#ifndef FM_BPOOL
-#define FM_BPOOL 3072
-#endif
+
 constexpr int kStreams = 3;
 constexpr std::uint64_t kChunkPoints = std::uint64_t{1} << 23;  // 8M points = 128 MiB
 
@@ -80,23 +78,11 @@ struct DeviceGuard {
 constexpr int kU = FM_KU;
 constexpr int kAWarps = 8;
 constexpr int kBWarps = FM_BWARPS;
-constexpr int kPool = FM_BPOOL;  // bytes per pool buffer (two per warp)
 
 struct QItem {  // 24 bytes
   double px, py;
   std::uint32_t i;  // point index within the launch
   std::uint32_t e;  // grid entry of the boundary cell
-};
-
-struct BatchSmem {
-  const std::uint8_t* bsrc[32];  // record address per item
-  std::uint32_t bstart[32];      // pool chunk per item
-  std::uint8_t ctab[kPool / 16]; // pool chunk -> item
-  alignas(16) std::uint8_t pool[kPool];
-};
-
-struct WarpSmemB {
-  BatchSmem buf[2];
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -195,83 +181,94 @@ __global__ void __launch_bounds__(kAWarps * 32)
   }
 }
 
-// Split cells (rare): descend from global memory, then resolve the leaf.
-template <bool kCount>
-__device__ __noinline__ int resolve_global(const fm::KParams& P, const std::uint8_t* rec,
-                                           double px, double py, fm::WorkCount& wc) {
-  for (int depth = 0; depth <= fm::kMaxSplitDepth + 1; ++depth) {
-    const std::uint32_t h = __ldg(reinterpret_cast<const std::uint32_t*>(rec));
-    const std::uint32_t kind = h & 0xFFu;
-    if (kind == fm::kKindCompact) {
-      return fm::resolve_compact<kCount>(fm::GlobalReader{rec}, h, px, py, wc);
-    }
-    if (kind == fm::kKindWide) return fm::resolve_wide<kCount>(rec, px, py, wc);
-    const double* d = reinterpret_cast<const double*>(rec + 8);
-    const double x0 = __ldg(d), y0 = __ldg(d + 1), ihw = __ldg(d + 2), ihh = __ldg(d + 3);
-    int ci = static_cast<int>(__dmul_rn(__dsub_rn(px, x0), ihw));
-    int cj = static_cast<int>(__dmul_rn(__dsub_rn(py, y0), ihh));
-    ci = min(max(ci, 0), 1);
-    cj = min(max(cj, 0), 1);
-    const std::uint32_t ce = __ldg(reinterpret_cast<const std::uint32_t*>(rec + 40) + 2 * cj + ci);
-    if (ce == fm::kEmpty) return -1;
-    if (ce < fm::kRecordBit) return static_cast<int>(ce);
-    rec = fm::record_ptr(P, ce);
+// resolve_kernel: one warp per queue region (pulled from an atomic counter).
+// Items are taken 32 at a time; the 128-byte slots of batch k+1 are copied
+// by cp.async into a double-buffered shared pool (8 lanes x 16 B per slot,
+// chunk c of slot r stored at chunk c ^ (r & 7) so the owner lanes' 16-byte
+// reads are bank-conflict free) while batch k is evaluated -- straight-line,
+// predicated code over registers (eval_leaf_slot).
+struct WarpSmemB {
+  alignas(16) std::uint8_t pool[2][32 * fm::kSlotBytes];
+};
+
+__device__ __forceinline__ QItem load_item(const QItem* __restrict__ items, std::uint32_t k,
+                                           std::uint32_t cnt) {
+  QItem it;
+  if (k < cnt) {  // 24-byte items are only 8-byte aligned
+    const double* d = reinterpret_cast<const double*>(items + k);
+    it.px = __ldcs(d);
+    it.py = __ldcs(d + 1);
+    const uint2 ie = __ldcs(reinterpret_cast<const uint2*>(d + 2));
+    it.i = ie.x;
+    it.e = ie.y;
+  } else {
+    it.px = it.py = 0.0;
+    it.i = 0;
+    it.e = fm::kEmpty;
   }
-  return -1;  // unreachable for a well-formed index
+  return it;
 }
 
-// Choose the next batch (items [next, next+take) of the region, as many as
-// fit the pool, <= 32) and start copying its records into `B`.
-__device__ __forceinline__ int stage_batch(const fm::KParams& P, const QItem* __restrict__ items,
-                                           std::uint32_t next, std::uint32_t cnt, BatchSmem& B,
-                                           int lane, QItem* it) {
-  const std::uint32_t avail = min(cnt - next, 32u);
-  const bool have = static_cast<std::uint32_t>(lane) < avail;
-  if (have) *it = items[next + lane];
-  const std::uint32_t bytes = have ? fm::entry_fetch_bytes(it->e) : 0u;
-  std::uint32_t tot;
-  const std::uint32_t before = warp_excl_scan(bytes, lane, &tot);
-  const bool fits = have && before + bytes <= static_cast<std::uint32_t>(kPool);
-  const int take = __popc(__ballot_sync(0xFFFFFFFFu, fits));
-  const std::uint32_t chunks = fits ? bytes / 16 : 0u;
-  std::uint32_t C;
-  const std::uint32_t start = warp_excl_scan(chunks, lane, &C);
-  if (fits) {
-    B.bstart[lane] = start;
-    B.bsrc[lane] = fm::record_ptr(P, it->e);
-    for (std::uint32_t c = 0; c < chunks; ++c) B.ctab[start + c] = static_cast<std::uint8_t>(lane);
-  }
-  __syncwarp();
-  for (std::uint32_t j = lane; j < C; j += 32) {
-    const int L = B.ctab[j];
-    cp_async16(B.pool + 16 * j, B.bsrc[L] + 16 * (j - B.bstart[L]));
+// Start copying the slots of the items held by lanes [0, n) into `buf`.
+__device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* buf,
+                                            std::uint32_t e, int n, int lane) {
+  const int c = lane & 7;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int r = 4 * q + (lane >> 3);
+    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
+    if (r < n) {
+      cp_async16(buf + r * fm::kSlotBytes + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
+    }
   }
   cp_async_commit();
-  return take;
 }
 
-// Evaluate a staged batch of `take` items (lane l owns item l).
+// Evaluate the staged batch.  Returns, per lane, the child entry a split
+// cell descends to (to be re-queued) or 0 when the item is finished.
 template <bool kHist, bool kCount>
-__device__ __forceinline__ void evaluate_batch(const fm::KParams& P, const BatchSmem& B, int lane,
-                                               int take, const QItem& it, int* __restrict__ out,
-                                               unsigned long long* __restrict__ hist,
-                                               fm::WorkCount& wc) {
-  if (lane < take) {
-    const fm::SmemReader R{B.pool + 16 * B.bstart[lane]};
-    const std::uint32_t h = R.u32(0);
-    const std::uint32_t kind = h & 0xFFu;
-    const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
-    int id;
-    if (kind == fm::kKindCompact && fm::compact_bytes(nv, nc, nb) <= fm::entry_fetch_bytes(it.e)) {
+__device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const std::uint8_t* buf,
+                                                     const QItem& it, int n, int lane,
+                                                     int* __restrict__ out,
+                                                     unsigned long long* __restrict__ hist,
+                                                     fm::WorkCount& wc) {
+  std::uint32_t requeue = 0;
+  if (lane < n) {
+    const std::uint8_t* base = buf + lane * fm::kSlotBytes;
+    const int s = lane & 7;
+    uint4 c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = *reinterpret_cast<const uint4*>(base + 16 * (k ^ s));
+    const std::uint32_t kind = c[0].x & 0xFFu;
+    int id = -1;
+    bool done = true;
+    if (kind == fm::kSlotLeaf) {
       if (kCount) wc.boundary++;
-      id = fm::resolve_compact<kCount>(R, h, it.px, it.py, wc);
-    } else {  // split cells, oversized and wide records: from global memory
-      if (kCount && kind != fm::kKindSplit) wc.boundary++;
-      id = resolve_global<kCount>(P, fm::record_ptr(P, it.e), it.px, it.py, wc);
+      id = fm::eval_leaf_slot<kCount>(c, it.px, it.py, wc);
+    } else if (kind == fm::kSlotSplit) {
+      const double x0 = fm::as_f64(c[0].z, c[0].w), y0 = fm::as_f64(c[1].x, c[1].y);
+      const double ihw = fm::as_f64(c[1].z, c[1].w), ihh = fm::as_f64(c[2].x, c[2].y);
+      int ci = static_cast<int>(__dmul_rn(__dsub_rn(it.px, x0), ihw));
+      int cj = static_cast<int>(__dmul_rn(__dsub_rn(it.py, y0), ihh));
+      ci = min(max(ci, 0), 1);
+      cj = min(max(cj, 0), 1);
+      const std::uint32_t k2 = 2 * cj + ci;
+      const std::uint32_t ce = k2 == 0 ? c[2].z : k2 == 1 ? c[2].w : k2 == 2 ? c[3].x : c[3].y;
+      if (ce == fm::kEmpty) {
+        id = -1;
+      } else if (ce < fm::kRecordBit) {
+        id = static_cast<int>(ce);
+      } else {
+        requeue = ce;
+        done = false;
+      }
+    } else {  // overflow record (past the split depth): from global memory
+      if (kCount) wc.boundary++;
+      id = fm::resolve_slot_global<kCount>(P, it.e, it.px, it.py, wc);
     }
-    emit<kHist>(out, hist, it.i, id);
+    if (done) emit<kHist>(out, hist, it.i, id);
   }
-  __syncwarp();
+  return requeue;
 }
 
 template <bool kHist, bool kCount>
@@ -283,39 +280,52 @@ __global__ void __launch_bounds__(kBWarps * 32)
                    unsigned long long* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  WarpSmemB& S = reinterpret_cast<WarpSmemB*>(dsmem)[wid];
+  WarpSmemB& S = reinterpret_cast<WarpSmemB*>(dsmem)[threadIdx.x >> 5];
   fm::WorkCount wc;
   for (;;) {
-    std::uint64_t region = 0;
+    unsigned long long region = 0;
     if (lane == 0) region = atomicAdd(next_region, 1ull);
     region = __shfl_sync(0xFFFFFFFFu, region, 0);
     if (region >= n_regions) break;
-    const QItem* items = q + region * region_cap;
-    const std::uint32_t cnt = qcount[region];
-    std::uint32_t next = 0;
-    int cur = 0;
-    QItem it{};
-    int take = 0;
-    if (cnt > 0) {
-      take = stage_batch(P, items, 0, cnt, S.buf[0], lane, &it);
-      next = static_cast<std::uint32_t>(take);
-    }
-    while (take > 0) {
-      QItem it_next{};
-      int take_next = 0;
-      if (next < cnt) {
-        take_next = stage_batch(P, items, next, cnt, S.buf[cur ^ 1], lane, &it_next);
-        cp_async_wait1();
-      } else {
-        cp_async_wait0();
+    QItem* items = const_cast<QItem*>(q) + region * region_cap;
+    std::uint32_t cnt = qcount[region];
+    // passes: split-cell descents are written back in place (the write
+    // cursor never passes the read cursor) and resolved by the next pass
+    while (cnt > 0) {
+      std::uint32_t wr = 0;
+      QItem cur = load_item(items, lane, cnt);
+      QItem nxt = load_item(items, 32 + lane, cnt);
+      int ncur = static_cast<int>(min(cnt, 32u));
+      stage_slots(P, S.pool[0], cur.e, ncur, lane);
+      int buf = 0;
+      for (std::uint32_t b = 0; b < cnt; b += 32) {
+        const int nnext = b + 32 < cnt ? static_cast<int>(min(cnt - b - 32, 32u)) : 0;
+        QItem nn{};
+        if (nnext > 0) {
+          stage_slots(P, S.pool[buf ^ 1], nxt.e, nnext, lane);
+          nn = load_item(items, b + 64 + lane, cnt);
+          cp_async_wait1();
+        } else {
+          cp_async_wait0();
+        }
+        __syncwarp();
+        const std::uint32_t ce = eval_staged<kHist, kCount>(P, S.pool[buf], cur, ncur, lane, out,
+                                                            hist, wc);
+        const std::uint32_t rq = __ballot_sync(0xFFFFFFFFu, ce != 0u);
+        if (ce != 0u) {
+          QItem it = cur;
+          it.e = ce;
+          items[wr + __popc(rq & ((1u << lane) - 1u))] = it;
+        }
+        wr += __popc(rq);
+        __syncwarp();
+        cur = nxt;
+        nxt = nn;
+        ncur = nnext;
+        buf ^= 1;
       }
+      cnt = wr;
       __syncwarp();
-      evaluate_batch<kHist, kCount>(P, S.buf[cur], lane, take, it, out, hist, wc);
-      next += static_cast<std::uint32_t>(take_next);
-      take = take_next;
-      it = it_next;
-      cur ^= 1;
     }
   }
   if (kCount) {
@@ -361,8 +371,9 @@ struct fm_index {
   fm::GridGeom g{};
   double ax0 = 0, ax1 = 0, ay0 = 0, ay1 = 0;
   std::uint32_t* d_grid = nullptr;
-  std::uint8_t* d_arena = nullptr;
-  std::uint64_t grid_len = 0, arena_len = 0, granule = 16;
+  std::uint8_t* d_slots = nullptr;     // boundary slots (128 B each)
+  std::uint8_t* d_overflow = nullptr;  // overflow records
+  std::uint64_t grid_len = 0, slots_len = 0, overflow_len = 0;
   fm::HostIndex host;  // retained only for host-only (device < 0) indexes
   fm_index_stats stats{};
   // fm_query_host staging
@@ -379,7 +390,8 @@ namespace {
 fm::KParams kparams(const fm_index* ix) {
   fm::KParams P;
   P.grid = ix->d_grid;
-  P.arena = ix->d_arena;
+  P.slots = ix->d_slots;
+  P.overflow = ix->d_overflow;
   P.gx0 = ix->g.gx0;
   P.gy0 = ix->g.gy0;
   P.inv_w = ix->g.inv_w;
@@ -390,7 +402,6 @@ fm::KParams kparams(const fm_index* ix) {
   P.ay1 = ix->ay1;
   P.nx = static_cast<int>(ix->g.nx);
   P.ny = static_cast<int>(ix->g.ny);
-  P.granule = ix->granule;
   return P;
 }
 
@@ -481,7 +492,8 @@ void free_device(fm_index* ix) {
   }
   if (ix->d_hist) cudaFree(ix->d_hist);
   if (ix->d_grid) cudaFree(ix->d_grid);
-  if (ix->d_arena) cudaFree(ix->d_arena);
+  if (ix->d_slots) cudaFree(ix->d_slots);
+  if (ix->d_overflow) cudaFree(ix->d_overflow);
 }
 
 }  // namespace
@@ -556,8 +568,8 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   ix->ay0 = std::max(ix->g.gy0, -90.0);
   ix->ay1 = std::min(ix->g.gy1, 90.0);
   ix->grid_len = ix->host.grid.size();
-  ix->arena_len = ix->host.arena.size();
-  ix->granule = ix->host.granule;
+  ix->slots_len = ix->host.slots.size();
+  ix->overflow_len = ix->host.overflow.size();
 
   fm_index_stats& s = ix->stats;
   s.n_polys = n_polys;
@@ -570,7 +582,7 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   s.cells_hit = ix->host.stats.cells_hit;
   s.cells_boundary = ix->host.stats.cells_boundary;
   s.grid_bytes = ix->grid_len * 4;
-  s.arena_bytes = ix->host.arena_used;
+  s.arena_bytes = ix->host.n_slots * fm::kSlotBytes + (ix->overflow_len - 512);
   s.geometry_bytes = s.n_vertices * 16;
   s.record_edges = ix->host.stats.record_edges;
   s.record_cands = ix->host.stats.record_cands;
@@ -592,15 +604,17 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
       return set_err(FM_ERR_CUDA, "cudaSetDevice failed");
     }
     cudaError_t e1 = cudaMalloc(&ix->d_grid, ix->grid_len * 4);
-    cudaError_t e2 = cudaMalloc(&ix->d_arena, ix->arena_len);
-    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaError_t e2 = cudaMalloc(&ix->d_slots, ix->slots_len);
+    cudaError_t e3 = cudaMalloc(&ix->d_overflow, ix->overflow_len);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
       free_device(ix);
       delete ix;
       return set_err(FM_ERR_OOM, "device allocation of the index failed");
     }
     e1 = cudaMemcpy(ix->d_grid, ix->host.grid.data(), ix->grid_len * 4, cudaMemcpyHostToDevice);
-    e2 = cudaMemcpy(ix->d_arena, ix->host.arena.data(), ix->arena_len, cudaMemcpyHostToDevice);
-    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    e2 = cudaMemcpy(ix->d_slots, ix->host.slots.data(), ix->slots_len, cudaMemcpyHostToDevice);
+    e3 = cudaMemcpy(ix->d_overflow, ix->host.overflow.data(), ix->overflow_len, cudaMemcpyHostToDevice);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
       free_device(ix);
       delete ix;
       return set_err(FM_ERR_CUDA, "index upload failed");
@@ -613,7 +627,8 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
     }
     // the device copy is authoritative; drop the host arrays
     std::vector<std::uint32_t>().swap(ix->host.grid);
-    std::vector<std::uint8_t>().swap(ix->host.arena);
+    std::vector<std::uint8_t>().swap(ix->host.slots);
+    std::vector<std::uint8_t>().swap(ix->host.overflow);
   }
   s.build_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -706,24 +721,31 @@ fm_status fm_index_export(const fm_index* index, std::uint32_t* grid, std::uint6
                           std::uint8_t* arena, std::uint64_t* arena_len, double* geometry16) {
   if (!index || !grid_len || !arena_len) return set_err(FM_ERR_INVALID_ARGUMENT, "null argument");
   *grid_len = index->grid_len;
-  *arena_len = index->arena_len;
+  *arena_len = index->slots_len + index->overflow_len;
   if (geometry16) {
     const fm::GridGeom& g = index->g;
     const double v[16] = {g.gx0, g.gx1, g.gy0, g.gy1, g.w, g.h, g.inv_w, g.inv_h,
                           static_cast<double>(g.nx), static_cast<double>(g.ny), g.margin,
                           static_cast<double>(index->stats.n_polys),
-                          static_cast<double>(index->granule), 0.0, 0.0, 0.0};
+                          static_cast<double>(index->slots_len), 0.0, 0.0, 0.0};
     std::memcpy(geometry16, v, sizeof(v));
   }
   if (!grid && !arena) return FM_OK;
   if (index->device < 0) {
     if (grid) std::memcpy(grid, index->host.grid.data(), index->grid_len * 4);
-    if (arena) std::memcpy(arena, index->host.arena.data(), index->arena_len);
+    if (arena) {
+      std::memcpy(arena, index->host.slots.data(), index->slots_len);
+      std::memcpy(arena + index->slots_len, index->host.overflow.data(), index->overflow_len);
+    }
     return FM_OK;
   }
   DeviceGuard guard(index->device);
   if (grid) FM_CUDA(cudaMemcpy(grid, index->d_grid, index->grid_len * 4, cudaMemcpyDeviceToHost));
-  if (arena) FM_CUDA(cudaMemcpy(arena, index->d_arena, index->arena_len, cudaMemcpyDeviceToHost));
+  if (arena) {
+    FM_CUDA(cudaMemcpy(arena, index->d_slots, index->slots_len, cudaMemcpyDeviceToHost));
+    FM_CUDA(cudaMemcpy(arena + index->slots_len, index->d_overflow, index->overflow_len,
+                       cudaMemcpyDeviceToHost));
+  }
   return FM_OK;
 }
 

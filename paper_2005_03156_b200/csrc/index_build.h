@@ -31,16 +31,17 @@ struct BuildStats {
   std::uint64_t record_edges = 0, record_cands = 0, record_breaks = 0;
   std::uint64_t max_record_edges = 0, max_record_cands = 0;
   std::uint64_t records_compact = 0, records_wide = 0;
-  std::uint64_t records = 0;      // leaf records (compact + wide)
+  std::uint64_t records = 0;      // leaf slots + overflow records
+  std::uint64_t records_overflow = 0;
   std::uint64_t cells_split = 0;  // split records (2x2 sub-cell nodes)
 };
 
 struct HostIndex {
   GridGeom g{};
   std::vector<std::uint32_t> grid;
-  std::vector<std::uint8_t> arena;  // records, 16-byte granules, + 512 B zero tail
-  std::uint64_t arena_used = 0;     // bytes of records (excluding the tail)
-  std::uint64_t granule = 16;       // record offset unit (bytes)
+  std::vector<std::uint8_t> slots;     // 128-byte boundary slots
+  std::uint64_t n_slots = 0;
+  std::vector<std::uint8_t> overflow;  // variable-size records past the split depth, + 512 B tail
   BuildStats stats;
 };
 

@@ -7,16 +7,11 @@
 // One u32 entry per cell, row-major:
 //   0xFFFFFFFF            empty: no leaf contains any point of the cell
 //   < 0x80000000          true hit: every point of the cell maps to this leaf
-//   1 | s(4) | k(27)      boundary: record of min(256, 16*(s+1)) bytes at
-//                         arena byte offset k * granule (granule = 16, 32,
-//                         64 ... chosen per index so the arena fits 27 bits);
-//                         s = 15 also marks "256 bytes or more / wide".
-// The size code lets the kernel fetch exactly a record's bytes in one
-// round trip, without reading a header first.
+//   0x80000000 | k        boundary: slot k of the slot arena (128 bytes each)
 //
-// A boundary record lists, for the cell, the candidate leaves in ascending
-// id order and the exact (fp64) polygon edges near the cell.  Point p maps
-// to the first candidate whose parity
+// A boundary cell's slot lists its candidate leaves in ascending id order
+// and the exact (fp64) polygon edges near the cell.  Point p maps to the
+// first candidate whose parity
 //     c0  ^  popc(cross_mask & edge_mask)  ^  popc(break_mask & {b : p.lat > b})
 // is odd, where bit i of cross_mask is the reference predicate
 // (geometry.hpp:214-225) of edge i at p.  c0 is the constant parity of the
@@ -24,40 +19,40 @@
 // latitudes where that constant changes inside the cell's slab.  A
 // candidate with no edges, no breakpoints and c0 = 1 is terminal.
 //
-// Compact record (kind 1; fits when n_verts <= 32, n_cands <= 15,
-// n_breaks <= 7), 16-byte aligned, little endian:
+// Slot kinds (128 bytes, 128-byte aligned, little endian):
+//  kind 1, leaf (<= 4 candidates, <= 2 breakpoints, <= 5 chain vertices):
 //   +0   u8 kind=1, u8 n_verts, u8 n_cands, u8 n_breaks
-//   +4   u32 chain_mask        bit i set: vertex i starts a new chain
-//   +8   n_cands x {i32 leaf, u32 edge_mask}
-//        n_cands x u8 info     bit 7 = c0, bits 0..6 = break_mask
-//        pad to 8
-//        n_breaks x f64        breakpoint latitudes
-//        pad to 16
-//        n_verts x {f64 lon, f64 lat}
-//   Edge i joins vertex i and vertex i+1 unless bit i+1 of chain_mask is
-//   set; it is oriented exactly like the reference (lo = lower latitude,
+//   +4   u32 chain_mask          bit i set: vertex i starts a new chain
+//   +8   i32 leaf[4]
+//   +24  u8 edge_mask[4]
+//   +28  u8 info[4]              bit 7 = c0, bits 0..1 = break mask
+//   +32  f64 break[2]
+//   +48  {f64 lon, f64 lat} vert[5]
+//   Edge i joins vertex i and i+1 unless bit i+1 of chain_mask is set; it
+//   is oriented exactly like the reference (lo = lower latitude,
 //   geometry.hpp:219), which reproduces its (lo, hi) bit for bit.
-//
-// Split record (kind 3): a boundary cell whose leaf record would not fit
-// one kRecordWindow-byte fetch is split 2x2 (recursively, up to
-// kMaxSplitDepth levels):
-//   +0   u8 kind=3, u8 0, u16 0, u32 0
+//  kind 3, split: a cell whose content does not fit one slot is split 2x2
+//   (recursively, up to kMaxSplitDepth levels):
 //   +8   f64 x0, f64 y0          lower-left corner of the split cell
 //   +24  f64 inv_hw, f64 inv_hh  1 / child width, 1 / child height
 //   +40  u32 child[4]            grid-format entries, index 2*j + i
-//   +56  pad to 64
-// Child (i, j) covers [x0 + i*hw, x0 + (i+1)*hw] x [y0 + j*hh, ...]; a
-// point goes to i = clamp(int((lon - x0) * inv_hw), 0, 1) (same for j).
-//
-// Wide record (kind 2; anything else):
-//   +0   u8 kind=2, u8 0, u16 n_words, u16 n_edges, u16 n_cands,
-//        u16 n_breaks, u16 0, u32 0
-//   +16  n_edges x {f64 lo.lon, lo.lat, hi.lon, hi.lat}  (lo.lat < hi.lat)
-//        n_cands x {i32 leaf, u32 info}  info bit 0 = c0, bits 1..15 = #breaks
-//        n_cands x n_words x u32        edge masks
-//        pad to 8
-//        sum(#breaks) x f64             per-candidate breakpoints, in order
-//        pad to 16
+//   Child (i, j) covers [x0 + i*hw, x0 + (i+1)*hw] x [y0 + j*hh, ...]; a
+//   point goes to i = clamp(int((lon - x0) * inv_hw), 0, 1) (same for j).
+//  kind 2, overflow (past the split depth): +8 u64 byte offset of a
+//   variable-size record in the overflow arena, one of
+//   compact (kind 1, fits when n_verts <= 32, n_cands <= 15, n_breaks <= 7):
+//     +0   u8 kind=1, u8 n_verts, u8 n_cands, u8 n_breaks
+//     +4   u32 chain_mask
+//     +8   n_cands x {i32 leaf, u32 edge_mask}
+//          n_cands x u8 info     bit 7 = c0, bits 0..6 = break mask
+//          pad to 8;  n_breaks x f64;  pad to 16;  n_verts x {f64, f64}
+//   wide (kind 2, anything else):
+//     +0   u8 kind=2, u8 0, u16 n_words, u16 n_edges, u16 n_cands,
+//          u16 n_breaks, u16 0, u32 0
+//     +16  n_edges x {f64 lo.lon, lo.lat, hi.lon, hi.lat}  (lo.lat < hi.lat)
+//          n_cands x {i32 leaf, u32 info}  info bit 0 = c0, bits 1..15 = #breaks
+//          n_cands x n_words x u32        edge masks
+//          pad to 8;  sum(#breaks) x f64 (per candidate, in order);  pad to 16
 #pragma once
 
 #include <cstdint>
@@ -78,23 +73,18 @@ constexpr std::uint32_t kMaxCands = 0xFFFFu;  // cell_index.hpp:339-341 limit
 constexpr std::uint32_t kMaxRecordEdges = 0xFFFFu;
 constexpr std::uint32_t kMaxBreaksPerCand = 0x7FFFu;
 
+// slot kinds
+constexpr std::uint8_t kSlotLeaf = 1;
+constexpr std::uint8_t kSlotOverflow = 2;
+constexpr std::uint8_t kSlotSplit = 3;
+constexpr std::uint64_t kSlotBytes = 128;
+constexpr std::uint32_t kSlotMaxCands = 4;
+constexpr std::uint32_t kSlotMaxBreaks = 2;
+constexpr std::uint32_t kSlotMaxVerts = 5;
+constexpr int kMaxSplitDepth = 6;
+// overflow record kinds
 constexpr std::uint8_t kKindCompact = 1;
 constexpr std::uint8_t kKindWide = 2;
-constexpr std::uint8_t kKindSplit = 3;
-constexpr std::uint64_t kRecordWindow = 256;  // max bytes fetched in one round per record
-constexpr std::uint32_t kOffsetBits = 27;
-constexpr std::uint32_t kOffsetMask = (1u << kOffsetBits) - 1u;
-
-FM_HD std::uint32_t record_entry(std::uint64_t unit_off, std::uint64_t bytes) {
-  const std::uint64_t code = bytes >= 256 ? 15 : (bytes + 15) / 16 - 1;
-  return 0x80000000u | static_cast<std::uint32_t>(code << kOffsetBits) |
-         static_cast<std::uint32_t>(unit_off);
-}
-FM_HD std::uint32_t entry_fetch_bytes(std::uint32_t e) {
-  return 16u * (((e >> kOffsetBits) & 15u) + 1u);
-}
-constexpr int kMaxSplitDepth = 6;
-constexpr std::uint64_t kSplitBytes = 64;
 constexpr std::uint32_t kCompactMaxVerts = 32;
 constexpr std::uint32_t kCompactMaxCands = 15;
 constexpr std::uint32_t kCompactMaxBreaks = 7;

@@ -101,8 +101,11 @@ struct RowWorker {
   BuildStats st;
 
   EncodeStats es;
-  std::vector<std::uint8_t> scratch;
-  std::vector<std::uint64_t>* rec_starts = nullptr;  // row-local record offsets, ascending
+  // per-row outputs (set by run_row)
+  std::vector<std::uint8_t> slots;                  // row-local slot arena
+  std::vector<std::uint8_t>* ovf = nullptr;         // row-local overflow arena
+  std::vector<std::uint64_t>* slot_patches = nullptr;
+  std::vector<std::uint64_t>* ovf_patches = nullptr;
 
   RowWorker(const Soup& s_, const GridGeom& g_, const std::vector<PolySpan>& sp, double t)
       : s(s_), g(g_), spans(sp), tol(t) {
@@ -243,11 +246,10 @@ struct RowWorker {
   }
 
   // Entry for a rectangle given its leaves' contributions (ascending ids).
-  // Appends records to `arena` (row-local offsets; every u32 that holds a
-  // row-local record entry is listed in `patches` for relocation).
+  // Appends slots to `slots` (row-local slot numbers; every u32 child entry
+  // and u64 overflow offset inside a slot is listed for relocation).
   std::uint32_t finalize(const std::vector<PolyC>& list, double rx0, double ry0, double cw,
-                         double chh, int depth, std::vector<std::uint8_t>& arena,
-                         std::vector<std::uint64_t>& patches) {
+                         double chh, int depth) {
     std::vector<Edge4> U;
     std::vector<CandIn> cin;
     std::vector<std::size_t> src;  // index into list per candidate
@@ -293,11 +295,17 @@ struct RowWorker {
         e = static_cast<std::uint32_t>(remap[e]);
       }
     }
-    scratch.clear();
-    EncodeStats tmp;
-    encode_record(used, cin, scratch, &tmp);
-    const bool fits = tmp.compact == 1 && scratch.size() <= kRecordWindow;
-    if (!fits && depth < kMaxSplitDepth && cw > 256.0 * g.margin && chh > 256.0 * g.margin) {
+    std::uint64_t n_breaks = 0;
+    for (const auto& c : cin) n_breaks += c.breaks.size();
+    std::uint8_t slot[kSlotBytes];
+    if (encode_slot(used, cin, slot)) {
+      const std::uint64_t k = slots.size() / kSlotBytes;
+      slots.insert(slots.end(), slot, slot + kSlotBytes);
+      note_leaf(used.size(), cin.size(), n_breaks);
+      es.compact++;
+      return kRecordBit | static_cast<std::uint32_t>(k);
+    }
+    if (depth < kMaxSplitDepth && cw > 256.0 * g.margin && chh > 256.0 * g.margin) {
       // split 2x2: child (i, j) covers [rx0 + i*cw/2, rx0 + (i+1)*cw/2] x ...
       const double hw = 0.5 * cw, hh = 0.5 * chh;
       std::uint32_t child[4];
@@ -317,36 +325,50 @@ struct RowWorker {
             }
             sub.push_back(std::move(pc));
           }
-          child[2 * j + i] = finalize(sub, cx0, cy0, hw, hh, depth + 1, arena, patches);
+          child[2 * j + i] = finalize(sub, cx0, cy0, hw, hh, depth + 1);
         }
       }
-      const std::uint64_t off = arena.size();
-      encode_split(rx0, ry0, 1.0 / hw, 1.0 / hh, child, arena, &patches);
-      rec_starts->push_back(off);
+      const std::uint64_t k = slots.size() / kSlotBytes;
+      encode_split_slot(rx0, ry0, 1.0 / hw, 1.0 / hh, child, slot);
+      slots.insert(slots.end(), slot, slot + kSlotBytes);
+      for (int c = 0; c < 4; ++c) {
+        if (child[c] >= kRecordBit && child[c] != kEmpty) slot_patches->push_back(k * kSlotBytes + 40 + 4 * c);
+      }
       st.cells_split++;
-      return kRecordBit | static_cast<std::uint32_t>(off / kRecordAlign);
+      return kRecordBit | static_cast<std::uint32_t>(k);
     }
-    const std::uint64_t off = arena.size();
-    arena.insert(arena.end(), scratch.begin(), scratch.end());
-    rec_starts->push_back(off);
+    // past the split depth: variable-size record in the overflow arena
+    const std::uint64_t off = ovf->size();
+    EncodeStats tmp;
+    encode_record(used, cin, *ovf, &tmp);
     es.compact += tmp.compact;
     es.wide += tmp.wide;
-    std::uint64_t n_breaks = 0;
-    for (const auto& c : cin) n_breaks += c.breaks.size();
+    const std::uint64_t k = slots.size() / kSlotBytes;
+    encode_overflow_slot(off, slot);
+    slots.insert(slots.end(), slot, slot + kSlotBytes);
+    ovf_patches->push_back(k * kSlotBytes + 8);
+    note_leaf(used.size(), cin.size(), n_breaks);
+    st.records_overflow++;
+    return kRecordBit | static_cast<std::uint32_t>(k);
+  }
+
+  void note_leaf(std::uint64_t ne, std::uint64_t nc, std::uint64_t nb) {
     st.records++;
-    st.record_edges += used.size();
-    st.record_cands += cin.size();
-    st.record_breaks += n_breaks;
-    st.max_record_edges = std::max<std::uint64_t>(st.max_record_edges, used.size());
-    st.max_record_cands = std::max<std::uint64_t>(st.max_record_cands, cin.size());
-    return kRecordBit | static_cast<std::uint32_t>(off / kRecordAlign);
+    st.record_edges += ne;
+    st.record_cands += nc;
+    st.record_breaks += nb;
+    st.max_record_edges = std::max(st.max_record_edges, ne);
+    st.max_record_cands = std::max(st.max_record_cands, nc);
   }
 
   void run_row(std::int64_t iy, const std::uint32_t* ids, std::uint64_t n_ids,
-               std::uint32_t* grid_row, std::vector<std::uint8_t>& arena,
-               std::vector<std::int64_t>& rec_cols, std::vector<std::uint64_t>& patches,
-               std::vector<std::uint64_t>& starts) {
-    rec_starts = &starts;
+               std::uint32_t* grid_row, std::vector<std::uint8_t>& row_slots,
+               std::vector<std::uint8_t>& row_ovf, std::vector<std::int64_t>& rec_cols,
+               std::vector<std::uint64_t>& spatch, std::vector<std::uint64_t>& opatch) {
+    slots.clear();
+    ovf = &row_ovf;
+    slot_patches = &spatch;
+    ovf_patches = &opatch;
     const double ys0 = cell_y0(g, iy) - g.margin;
     const double ys1 = cell_y0(g, iy + 1) + g.margin;
     epool.clear();
@@ -365,8 +387,7 @@ struct RowWorker {
         pc.breaks.assign(bpool.begin() + c.b_begin, bpool.begin() + c.b_end);
         list.push_back(std::move(pc));
       }
-      const std::uint32_t e = finalize(list, cell_x0(g, ix), cell_y0(g, iy), g.w, g.h, 0,
-                                       arena, patches);
+      const std::uint32_t e = finalize(list, cell_x0(g, ix), cell_y0(g, iy), g.w, g.h, 0);
       grid_row[ix] = e;
       if (e == kEmpty) {
         st.cells_empty++;
@@ -380,6 +401,7 @@ struct RowWorker {
       closed[ix] = 0;
     }
     st.cells_empty += static_cast<std::uint64_t>(g.nx) - touched.size();
+    row_slots.swap(slots);
   }
 };
 
@@ -487,8 +509,8 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
   const GridGeom& g = out.g;
   const std::size_t ncell = static_cast<std::size_t>(g.nx * g.ny);
   out.grid.assign(ncell, kEmpty);
-  out.arena.assign(512, 0);
-  out.granule = kRecordAlign;
+  out.slots.assign(kSlotBytes, 0);  // never referenced; keeps device buffers non-empty
+  out.overflow.assign(512, 0);
   if (s.n_polys == 0) {
     out.stats.cells_empty = ncell;
     return out;
@@ -540,10 +562,10 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
   if (threads < 1) threads = 1;
   threads = static_cast<int>(std::min<std::int64_t>(threads, g.ny));
 
-  std::vector<std::vector<std::uint8_t>> row_arena(static_cast<std::size_t>(g.ny));
-  std::vector<std::vector<std::int64_t>> row_recs(static_cast<std::size_t>(g.ny));
-  std::vector<std::vector<std::uint64_t>> row_patches(static_cast<std::size_t>(g.ny));
-  std::vector<std::vector<std::uint64_t>> row_starts(static_cast<std::size_t>(g.ny));
+  const std::size_t NY = static_cast<std::size_t>(g.ny);
+  std::vector<std::vector<std::uint8_t>> row_slots(NY), row_ovf(NY);
+  std::vector<std::vector<std::int64_t>> row_recs(NY);
+  std::vector<std::vector<std::uint64_t>> row_spatch(NY), row_opatch(NY);
   std::atomic<std::int64_t> next{0};
   std::mutex mu;
   std::exception_ptr failure;
@@ -555,8 +577,8 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
         const std::int64_t iy = next.fetch_add(1);
         if (iy >= g.ny) break;
         w.run_row(iy, row_ids.data() + row_count[iy], row_count[iy + 1] - row_count[iy],
-                  out.grid.data() + iy * g.nx, row_arena[iy], row_recs[iy], row_patches[iy],
-                  row_starts[iy]);
+                  out.grid.data() + iy * g.nx, row_slots[iy], row_ovf[iy], row_recs[iy],
+                  row_spatch[iy], row_opatch[iy]);
       }
       stats[t] = w.st;
       stats[t].records_compact = w.es.compact;
@@ -573,63 +595,44 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
   for (auto& th : pool) th.join();
   if (failure) std::rethrow_exception(failure);
 
-  // Lay the rows' records out in one arena with granule G (the smallest
-  // power of two >= 16 for which every offset fits kOffsetBits), and rewrite
-  // every record entry (grid cells and split children) as
-  // record_entry(offset / G, size).
-  auto rec_size = [&](std::int64_t r, std::size_t k) {
-    const auto& st = row_starts[r];
-    return (k + 1 < st.size() ? st[k + 1] : row_arena[r].size()) - st[k];
-  };
-  std::uint64_t G = kRecordAlign;
-  for (;; G *= 2) {
-    std::uint64_t units = 0;
-    for (std::int64_t r = 0; r < g.ny; ++r) {
-      for (std::size_t k = 0; k < row_starts[r].size(); ++k) units += (rec_size(r, k) + G - 1) / G;
-    }
-    if (units < (std::uint64_t{1} << kOffsetBits)) break;
-    if (G >= 4096) throw RuntimeError("index arena too large for 27-bit record offsets");
+  // Concatenate the rows' slot arenas and overflow arenas, then relocate:
+  // row-local slot numbers (grid entries, split children) gain the row's
+  // slot base, overflow offsets the row's overflow base.
+  std::uint64_t n_slots = 0, ovf_bytes = 0;
+  std::vector<std::uint64_t> slot_base(NY), ovf_base(NY);
+  for (std::size_t r = 0; r < NY; ++r) {
+    slot_base[r] = n_slots;
+    ovf_base[r] = ovf_bytes;
+    n_slots += row_slots[r].size() / kSlotBytes;
+    ovf_bytes += (row_ovf[r].size() + 15) & ~std::uint64_t{15};
   }
-  std::vector<std::vector<std::uint64_t>> new_off(static_cast<std::size_t>(g.ny));
-  std::uint64_t total = 0;
-  for (std::int64_t r = 0; r < g.ny; ++r) {
-    new_off[r].resize(row_starts[r].size());
-    for (std::size_t k = 0; k < row_starts[r].size(); ++k) {
-      new_off[r][k] = total;
-      total += (rec_size(r, k) + G - 1) / G * G;
+  if (n_slots >= kRecordBit) throw RuntimeError("index needs more than 2^31 slots");
+  out.slots.assign((n_slots ? n_slots : 1) * kSlotBytes, 0);
+  out.overflow.assign(ovf_bytes + 512, 0);  // zero tail: bounded over-reads stay inside
+  for (std::size_t r = 0; r < NY; ++r) {
+    const std::uint32_t sb = static_cast<std::uint32_t>(slot_base[r]);
+    std::uint8_t* dst = out.slots.data() + slot_base[r] * kSlotBytes;
+    if (!row_slots[r].empty()) std::memcpy(dst, row_slots[r].data(), row_slots[r].size());
+    if (!row_ovf[r].empty()) {
+      std::memcpy(out.overflow.data() + ovf_base[r], row_ovf[r].data(), row_ovf[r].size());
     }
-  }
-  out.granule = G;
-  out.arena_used = total;
-  out.arena.assign(total + 512, 0);  // zero tail: fixed-size fetches may run past the end
-  auto find_rec = [&](std::int64_t r, std::uint64_t local) {
-    const auto& st = row_starts[r];
-    return static_cast<std::size_t>(std::upper_bound(st.begin(), st.end(), local) - st.begin() - 1);
-  };
-  auto relocate = [&](std::int64_t r, std::uint32_t e) {
-    const std::uint64_t local = static_cast<std::uint64_t>(e & ~kRecordBit) * kRecordAlign;
-    const std::size_t k = find_rec(r, local);
-    return record_entry(new_off[r][k] / G, rec_size(r, k));
-  };
-  for (std::int64_t r = 0; r < g.ny; ++r) {
-    for (std::size_t k = 0; k < row_starts[r].size(); ++k) {
-      std::memcpy(out.arena.data() + new_off[r][k], row_arena[r].data() + row_starts[r][k],
-                  rec_size(r, k));
-    }
-    for (const std::int64_t ix : row_recs[r]) {
-      std::uint32_t& e = out.grid[static_cast<std::size_t>(r * g.nx + ix)];
-      e = relocate(r, e);
-    }
-    for (const std::uint64_t pos : row_patches[r]) {
-      const std::size_t k = find_rec(r, pos);
-      const std::uint64_t at = new_off[r][k] + (pos - row_starts[r][k]);
+    for (const std::int64_t ix : row_recs[r]) out.grid[r * static_cast<std::size_t>(g.nx) + ix] += sb;
+    for (const std::uint64_t pos : row_spatch[r]) {
       std::uint32_t v;
-      std::memcpy(&v, out.arena.data() + at, 4);
-      v = relocate(r, v);
-      std::memcpy(out.arena.data() + at, &v, 4);
+      std::memcpy(&v, dst + pos, 4);
+      v += sb;
+      std::memcpy(dst + pos, &v, 4);
     }
-    std::vector<std::uint8_t>().swap(row_arena[r]);
+    for (const std::uint64_t pos : row_opatch[r]) {
+      std::uint64_t v;
+      std::memcpy(&v, dst + pos, 8);
+      v += ovf_base[r];
+      std::memcpy(dst + pos, &v, 8);
+    }
+    std::vector<std::uint8_t>().swap(row_slots[r]);
+    std::vector<std::uint8_t>().swap(row_ovf[r]);
   }
+  out.n_slots = n_slots;
   for (const auto& st : stats) {
     out.stats.cells_empty += st.cells_empty;
     out.stats.cells_hit += st.cells_hit;
@@ -641,6 +644,7 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
     out.stats.max_record_cands = std::max(out.stats.max_record_cands, st.max_record_cands);
     out.stats.records_compact += st.records_compact;
     out.stats.records += st.records;
+    out.stats.records_overflow += st.records_overflow;
     out.stats.cells_split += st.cells_split;
     out.stats.records_wide += st.records_wide;
   }

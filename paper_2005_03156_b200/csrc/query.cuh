@@ -17,15 +17,15 @@ namespace fm {
 
 struct KParams {
   const std::uint32_t* __restrict__ grid;
-  const std::uint8_t* __restrict__ arena;
+  const std::uint8_t* __restrict__ slots;     // 128-byte boundary slots
+  const std::uint8_t* __restrict__ overflow;  // variable-size records
   double gx0, gy0, inv_w, inv_h;
   double ax0, ax1, ay0, ay1;  // acceptance box = padded domain intersect world box
   int nx, ny;
-  std::uint64_t granule;     // record offset unit (bytes)
 };
 
-__device__ __forceinline__ const std::uint8_t* record_ptr(const KParams& P, std::uint32_t e) {
-  return P.arena + static_cast<std::size_t>(e & kOffsetMask) * P.granule;
+__device__ __forceinline__ const std::uint8_t* slot_ptr(const KParams& P, std::uint32_t e) {
+  return P.slots + static_cast<std::size_t>(e & ~kRecordBit) * kSlotBytes;
 }
 
 __device__ __forceinline__ bool ray_crosses(double px, double py, double lx,
@@ -151,6 +151,80 @@ __device__ __forceinline__ int resolve_compact(const Rd& R, std::uint32_t h, dou
     if (par & 1u) return static_cast<int>(R.u32(8 + 8 * c));
   }
   return -1;
+}
+
+__device__ __forceinline__ double as_f64(std::uint32_t lo, std::uint32_t hi) {
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+}
+
+// Leaf slot (index_format.h, kind 1) held in registers as eight 16-byte
+// chunks; every offset is static, every branch is a predicate.
+template <bool kCount>
+__device__ __forceinline__ int eval_leaf_slot(const uint4 (&c)[8], double px, double py,
+                                              WorkCount& wc) {
+  const std::uint32_t h = c[0].x, chain = c[0].y;
+  const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
+  double vx[kSlotMaxVerts], vy[kSlotMaxVerts];
+#pragma unroll
+  for (int k = 0; k < static_cast<int>(kSlotMaxVerts); ++k) {
+    vx[k] = as_f64(c[3 + k].x, c[3 + k].y);
+    vy[k] = as_f64(c[3 + k].z, c[3 + k].w);
+  }
+  std::uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k + 1 < static_cast<int>(kSlotMaxVerts); ++k) {
+    if (static_cast<std::uint32_t>(k + 1) < nv && !((chain >> (k + 1)) & 1u)) {
+      if (kCount) wc.edges++;
+      m |= edge_bit(px, py, vx[k], vy[k], vx[k + 1], vy[k + 1]) << k;
+    }
+  }
+  const double b0 = as_f64(c[2].x, c[2].y), b1 = as_f64(c[2].z, c[2].w);
+  const std::uint32_t bm = ((nb > 0u && py > b0) ? 1u : 0u) | ((nb > 1u && py > b1) ? 2u : 0u);
+  const std::uint32_t ids[4] = {c[0].z, c[0].w, c[1].x, c[1].y};
+  const std::uint32_t masks = c[1].z, infos = c[1].w;
+  int id = -1;
+#pragma unroll
+  for (int q = 3; q >= 0; --q) {  // descending, so the smallest odd candidate wins
+    const std::uint32_t mk = (masks >> (8 * q)) & 0xFFu, inf = (infos >> (8 * q)) & 0xFFu;
+    const std::uint32_t par = (inf >> 7) ^ __popc(m & mk) ^ __popc(bm & inf & 3u);
+    if (static_cast<std::uint32_t>(q) < nc && (par & 1u)) id = static_cast<int>(ids[q]);
+  }
+  if (kCount) wc.cands += nc;
+  return id;
+}
+
+// A boundary slot fetched straight from global memory (split descents and
+// overflow records; rare).
+template <bool kCount>
+__device__ __noinline__ int resolve_slot_global(const KParams& P, std::uint32_t e, double px,
+                                                double py, WorkCount& wc) {
+  for (int depth = 0; depth <= kMaxSplitDepth + 1; ++depth) {
+    const uint4* g = reinterpret_cast<const uint4*>(slot_ptr(P, e));
+    uint4 c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = __ldg(g + k);
+    const std::uint32_t kind = c[0].x & 0xFFu;
+    if (kind == kSlotLeaf) return eval_leaf_slot<kCount>(c, px, py, wc);
+    if (kind == kSlotOverflow) {
+      const std::uint64_t off = (static_cast<std::uint64_t>(c[0].w) << 32) | c[0].z;
+      const std::uint8_t* rec = P.overflow + off;
+      const std::uint32_t h = __ldg(reinterpret_cast<const std::uint32_t*>(rec));
+      if ((h & 0xFFu) == kKindCompact) return resolve_compact<kCount>(GlobalReader{rec}, h, px, py, wc);
+      return resolve_wide<kCount>(rec, px, py, wc);
+    }
+    // split
+    const double x0 = as_f64(c[0].z, c[0].w), y0 = as_f64(c[1].x, c[1].y);
+    const double ihw = as_f64(c[1].z, c[1].w), ihh = as_f64(c[2].x, c[2].y);
+    int ci = static_cast<int>(__dmul_rn(__dsub_rn(px, x0), ihw));
+    int cj = static_cast<int>(__dmul_rn(__dsub_rn(py, y0), ihh));
+    ci = min(max(ci, 0), 1);
+    cj = min(max(cj, 0), 1);
+    const std::uint32_t ch[4] = {c[2].z, c[2].w, c[3].x, c[3].y};
+    e = ch[2 * cj + ci];
+    if (e == kEmpty) return -1;
+    if (e < kRecordBit) return static_cast<int>(e);
+  }
+  return -1;  // unreachable for a well-formed index
 }
 
 }  // namespace fm

@@ -175,25 +175,66 @@ inline std::uint64_t encode_record(const std::vector<Edge4>& E, const std::vecto
   return off;
 }
 
-// Appends a split record (index_format.h, kind 3).  Child entries that
-// reference records are row-local; their byte positions go to *patches.
-inline void encode_split(double x0, double y0, double inv_hw, double inv_hh,
-                         const std::uint32_t child[4], std::vector<std::uint8_t>& arena,
-                         std::vector<std::uint64_t>* patches) {
-  const std::uint64_t off = arena.size();
-  arena.resize(off + kSplitBytes, 0);
-  std::uint8_t* r = arena.data() + off;
-  r[0] = kKindSplit;
-  std::memcpy(r + 8, &x0, 8);
-  std::memcpy(r + 16, &y0, 8);
-  std::memcpy(r + 24, &inv_hw, 8);
-  std::memcpy(r + 32, &inv_hh, 8);
-  std::memcpy(r + 40, child, 16);
-  if (patches) {
-    for (int k = 0; k < 4; ++k) {
-      if (child[k] >= kRecordBit && child[k] != kEmpty) patches->push_back(off + 40 + 4 * k);
+// Encodes a leaf slot (index_format.h, kind 1) into out[128] if the cell's
+// content fits one slot; returns false otherwise.
+inline bool encode_slot(const std::vector<Edge4>& E, const std::vector<CandIn>& C,
+                        std::uint8_t* out) {
+  if (C.size() > kSlotMaxCands) return false;
+  std::vector<double> ub;
+  for (const auto& c : C) {
+    for (double b : c.breaks) {
+      if (std::find(ub.begin(), ub.end(), b) == ub.end()) ub.push_back(b);
     }
   }
+  if (ub.size() > kSlotMaxBreaks) return false;
+  std::sort(ub.begin(), ub.end());
+  std::vector<double> vx, vy;
+  std::uint32_t chain_mask = 0;
+  std::vector<std::uint32_t> bit_of;
+  if (!detail::chain_edges(E, vx, vy, chain_mask, bit_of, kSlotMaxVerts)) return false;
+  std::memset(out, 0, kSlotBytes);
+  out[0] = kSlotLeaf;
+  out[1] = static_cast<std::uint8_t>(vx.size());
+  out[2] = static_cast<std::uint8_t>(C.size());
+  out[3] = static_cast<std::uint8_t>(ub.size());
+  std::memcpy(out + 4, &chain_mask, 4);
+  for (std::size_t c = 0; c < C.size(); ++c) {
+    const std::int32_t id = static_cast<std::int32_t>(C[c].id);
+    std::memcpy(out + 8 + 4 * c, &id, 4);
+    std::uint8_t mask = 0;
+    for (std::uint32_t e : C[c].edges) mask |= static_cast<std::uint8_t>(1u << bit_of[e]);
+    std::uint8_t info = static_cast<std::uint8_t>((C[c].c0 & 1u) << 7);
+    for (double b : C[c].breaks) {
+      info |= static_cast<std::uint8_t>(1u << (std::lower_bound(ub.begin(), ub.end(), b) - ub.begin()));
+    }
+    out[24 + c] = mask;
+    out[28 + c] = info;
+  }
+  std::memcpy(out + 32, ub.data(), 8 * ub.size());
+  for (std::size_t k = 0; k < vx.size(); ++k) {
+    std::memcpy(out + 48 + 16 * k, &vx[k], 8);
+    std::memcpy(out + 56 + 16 * k, &vy[k], 8);
+  }
+  return true;
+}
+
+// Encodes a split slot (kind 3).
+inline void encode_split_slot(double x0, double y0, double inv_hw, double inv_hh,
+                              const std::uint32_t child[4], std::uint8_t* out) {
+  std::memset(out, 0, kSlotBytes);
+  out[0] = kSlotSplit;
+  std::memcpy(out + 8, &x0, 8);
+  std::memcpy(out + 16, &y0, 8);
+  std::memcpy(out + 24, &inv_hw, 8);
+  std::memcpy(out + 32, &inv_hh, 8);
+  std::memcpy(out + 40, child, 16);
+}
+
+// Encodes an overflow slot (kind 2) pointing at byte offset `off`.
+inline void encode_overflow_slot(std::uint64_t off, std::uint8_t* out) {
+  std::memset(out, 0, kSlotBytes);
+  out[0] = kSlotOverflow;
+  std::memcpy(out + 8, &off, 8);
 }
 
 }  // namespace fm

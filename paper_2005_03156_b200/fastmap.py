@@ -234,9 +234,9 @@ class CellIndex:
                                   N.ptr(arena, C.c_uint8), C.byref(al), N.ptr(geo, C.c_double)),
                 "fm_index_export")
         keys = ("gx0", "gx1", "gy0", "gy1", "w", "h", "inv_w", "inv_h", "nx", "ny",
-                "margin", "n_polys", "granule")
+                "margin", "n_polys", "slot_bytes")
         g = dict(zip(keys, geo.tolist()))
-        g["granule"] = int(g["granule"])
+        g["slot_bytes"] = int(g["slot_bytes"])
         g["nx"] = int(g["nx"])
         g["ny"] = int(g["ny"])
         g["n_polys"] = int(g["n_polys"])

@@ -38,26 +38,37 @@ def _align(v, a):
     return (v + a - 1) & ~(a - 1)
 
 
-OFFSET_MASK = (1 << 27) - 1
+SLOT = 128
 
 
-def resolve(arena: np.ndarray, entry: int, px: float, py: float, granule: int = 16) -> int:
-    off = (entry & OFFSET_MASK) * granule
+def _eval_leaf_slot(arena, off, px, py) -> int:
+    buf = arena.data
+    nv, nc, nb = int(arena[off + 1]), int(arena[off + 2]), int(arena[off + 3])
+    chain = struct.unpack_from("<I", buf, off + 4)[0]
+    ids = struct.unpack_from("<4i", buf, off + 8)
+    masks = arena[off + 24: off + 28].tolist()
+    infos = arena[off + 28: off + 32].tolist()
+    breaks = struct.unpack_from("<2d", buf, off + 32)
+    v = np.frombuffer(buf, dtype="<f8", count=10, offset=off + 48).reshape(5, 2).tolist()
+    m = 0
+    for k in range(4):
+        if k + 1 < nv and not (chain >> (k + 1)) & 1:
+            (ax, ay), (bx, by) = v[k], v[k + 1]
+            lx, ly, hx, hy = (ax, ay, bx, by) if ay < by else (bx, by, ax, ay)
+            if ly < py <= hy and _cross(px, py, lx, ly, hx, hy):
+                m |= 1 << k
+    bm = (1 if (nb > 0 and py > breaks[0]) else 0) | (2 if (nb > 1 and py > breaks[1]) else 0)
+    for c in range(nc):
+        par = (infos[c] >> 7) ^ bin(m & masks[c]).count("1") ^ bin(bm & infos[c] & 3).count("1")
+        if par & 1:
+            return ids[c]
+    return -1
+
+
+def _eval_overflow(arena, off, px, py) -> int:
     buf = arena.data
     kind = arena[off]
-    while kind == 3:  # split record: descend to the child cell
-        x0, y0, ihw, ihh = struct.unpack_from("<4d", buf, off + 8)
-        child = struct.unpack_from("<4I", buf, off + 40)
-        i = min(max(int((px - x0) * ihw), 0), 1)
-        j = min(max(int((py - y0) * ihh), 0), 1)
-        e = child[2 * j + i]
-        if e == K_EMPTY:
-            return -1
-        if e < K_RECORD:
-            return e
-        off = (e & OFFSET_MASK) * granule
-        kind = arena[off]
-    if kind == 1:  # compact (index_format.h)
+    if kind == 1:  # compact
         nv, nc, nb = int(arena[off + 1]), int(arena[off + 2]), int(arena[off + 3])
         chain = struct.unpack_from("<I", buf, off + 4)[0]
         cands = np.frombuffer(buf, dtype="<u4", count=2 * nc, offset=off + 8).reshape(-1, 2)
@@ -85,7 +96,7 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float, granule: int = 
             if par & 1:
                 return leaf - (1 << 32) if leaf >= (1 << 31) else leaf
         return -1
-    assert kind == 2, f"bad record kind {kind}"
+    assert kind == 2, f"bad overflow record kind {kind}"
     n_words, n_edges, n_cands, n_breaks = struct.unpack_from("<4H", buf, off + 2)
     edges = np.frombuffer(buf, dtype="<f8", count=4 * n_edges, offset=off + 16).reshape(-1, 4)
     co = off + 16 + 32 * n_edges
@@ -100,7 +111,7 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float, granule: int = 
     boff = 0
     for c in range(cands.shape[0]):
         leaf, info = int(cands[c, 0]), int(cands[c, 1]) & 0xFFFFFFFF
-        nb = info >> 1
+        nbc = info >> 1
         par = info & 1
         for w in range(masks.shape[1]):
             mm = int(masks[c, w])
@@ -108,19 +119,43 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float, granule: int = 
                 k = (mm & -mm).bit_length() - 1
                 mm &= mm - 1
                 par ^= bits[w * 32 + k]
-        for b in breaks[boff:boff + nb].tolist():
+        for b in breaks[boff:boff + nbc].tolist():
             par ^= 1 if py > b else 0
-        boff += nb
+        boff += nbc
         if par & 1:
             return leaf
     return -1
 
 
+def resolve(arena: np.ndarray, entry: int, px: float, py: float, slot_bytes: int) -> int:
+    """Walk slot `entry` (index_format.h) for point (px, py)."""
+    buf = arena.data
+    e = entry
+    while True:
+        off = (e & ~K_RECORD) * SLOT
+        kind = arena[off]
+        if kind == 1:
+            return _eval_leaf_slot(arena, off, px, py)
+        if kind == 2:
+            ovf = struct.unpack_from("<Q", buf, off + 8)[0]
+            return _eval_overflow(arena, slot_bytes + ovf, px, py)
+        assert kind == 3, f"bad slot kind {kind}"
+        x0, y0, ihw, ihh = struct.unpack_from("<4d", buf, off + 8)
+        child = struct.unpack_from("<4I", buf, off + 40)
+        i = min(max(int((px - x0) * ihw), 0), 1)
+        j = min(max(int((py - y0) * ihh), 0), 1)
+        e = child[2 * j + i]
+        if e == K_EMPTY:
+            return -1
+        if e < K_RECORD:
+            return e
+
+
 def record_kinds(index_export) -> dict:
     grid, arena, g = index_export
-    recs = np.unique(grid[(grid >= K_RECORD) & (grid != K_EMPTY)])
-    kinds = arena[((recs & np.uint32(OFFSET_MASK)).astype(np.int64)) * g["granule"]]
-    return {"compact": int((kinds == 1).sum()), "wide": int((kinds == 2).sum()),
+    n_slots = g["slot_bytes"] // SLOT
+    kinds = arena[np.arange(n_slots) * SLOT] if n_slots else np.zeros(0, np.uint8)
+    return {"leaf": int((kinds == 1).sum()), "overflow": int((kinds == 2).sum()),
             "split": int((kinds == 3).sum())}
 
 
@@ -131,5 +166,5 @@ def walk(index_export, pts: np.ndarray) -> np.ndarray:
     out = np.where(e < K_RECORD, e.astype(np.int64), -1).astype(np.int32)
     rec = np.nonzero((e >= K_RECORD) & (e != K_EMPTY))[0]
     for i in rec.tolist():
-        out[i] = resolve(arena, int(e[i]), float(pts[i, 0]), float(pts[i, 1]), g["granule"])
+        out[i] = resolve(arena, int(e[i]), float(pts[i, 0]), float(pts[i, 1]), g["slot_bytes"])
     return out

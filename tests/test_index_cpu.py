@@ -46,7 +46,7 @@ def test_edge_cases_use_wide_and_split_records():
     soup, pts = edge_cases.build()
     _, _, ex = walk(soup, pts, nx=1, ny=1)
     kinds = index_walk.record_kinds(ex)
-    assert kinds["split"] >= 1
+    assert kinds["split"] >= 1 and kinds["overflow"] >= 1
     got, _, _ = walk(soup, pts, nx=1, ny=1)
     assert np.array_equal(got, oracle.exhaustive_assign(soup, pts))
 
@@ -70,22 +70,24 @@ def test_empty_soup_and_zero_ring_polygons():
     assert got[0] == 1
 
 
-def test_record_invariants():
-    """Compact records: ascending candidate ids, chain vertices oriented
-    edges never horizontal, masks inside the vertex range."""
+def test_slot_invariants():
+    """Leaf slots: ascending distinct candidate ids, masks inside the edge
+    range, counts within the slot capacity."""
     import struct
     cfg = synth.config("c1")
     _, _, (grid, arena, g) = walk(cfg.make_soup(), np.zeros((1, 2)))
-    recs = np.unique(grid[(grid >= 0x80000000) & (grid != 0xFFFFFFFF)])[:2000]
+    recs = np.unique(grid[(grid >= 0x80000000) & (grid != 0xFFFFFFFF)])[:3000]
+    n_leaf = 0
     for e in recs.tolist():
-        off = (e & ((1 << 27) - 1)) * g["granule"]
+        off = (e & 0x7FFFFFFF) * 128
         kind, nv, nc, nb = arena[off:off + 4].tolist()
+        assert kind in (1, 2, 3)
         if kind != 1:
             continue
-        ids = [struct.unpack_from("<i", arena.data, off + 8 + 8 * c)[0] for c in range(nc)]
-        masks = [struct.unpack_from("<I", arena.data, off + 12 + 8 * c)[0] for c in range(nc)]
-        assert ids == sorted(ids) and len(set(ids)) == len(ids)
-        for mk in masks:
+        n_leaf += 1
+        assert 1 <= nc <= 4 and nb <= 2 and nv <= 5
+        ids = list(struct.unpack_from("<4i", arena.data, off + 8))[:nc]
+        assert ids == sorted(ids) and len(set(ids)) == nc
+        for mk in arena[off + 24: off + 24 + nc].tolist():
             assert mk < (1 << max(nv - 1, 0)) or mk == 0
-        size = (e >> 27) & 15
-        assert 16 * (size + 1) >= 8  # size code present
+    assert n_leaf > 0
