@@ -128,6 +128,9 @@ def synth() -> C.CDLL:
         L.synth_tiling.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double,
                                    C.c_double, C.c_double, C.c_double, C.c_double,
                                    C.c_double, u64, C.c_int, PD, PU64, PU64]
+        L.synth_nested.restype = C.c_int
+        L.synth_nested.argtypes = [C.c_uint32] * 7 + [C.c_double] * 6 + [u64, C.c_int, PD, PU64,
+                                                                        PU64, PU32]
         L.synth_points_uniform.restype = C.c_int
         L.synth_points_uniform.argtypes = [PD, u64, u64, u64, C.c_int, PD]
         L.synth_points_clustered.restype = C.c_int

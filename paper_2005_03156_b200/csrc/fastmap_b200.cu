@@ -271,8 +271,11 @@ __device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const
   return requeue;
 }
 
+#ifndef FM_BMINB
+#define FM_BMINB 1
+#endif
 template <bool kHist, bool kCount>
-__global__ void __launch_bounds__(kBWarps * 32)
+__global__ void __launch_bounds__(kBWarps * 32, FM_BMINB)
     resolve_kernel(fm::KParams P, const QItem* __restrict__ q,
                    const std::uint32_t* __restrict__ qcount, std::uint64_t n_regions,
                    std::uint64_t region_cap, unsigned long long* __restrict__ next_region,

@@ -199,6 +199,185 @@ int synth_tiling(std::uint32_t nx, std::uint32_t ny, std::uint32_t segs,
   return 0;
 }
 
+// Three-level nested tiling (BASELINE config 3): sx x sy states, each split
+// into cx x cy counties, each split into bx x by blocks (the leaves).  One
+// global block lattice of (sx*cx*bx + 1) x (sy*cy*by + 1) nodes is placed
+// hierarchically, in lattice units:
+//   * state corners are jittered by U(+-jitter) state cells (interior only);
+//   * county corners are bilinear in their state's four corners, then
+//     jittered by U(+-jitter) county cells unless they lie on a state edge,
+//     where they stay on that (straight) edge;
+//   * block corners likewise inside their county, jittered by U(+-jitter)
+//     block cells unless on a county edge.
+// So every level is a jittered tiling conformal to (clipped exactly to) its
+// parent.  Block edges are split into `segs` segments whose interior points
+// are displaced perpendicular by N(0, sigma) block cells (not on the outer
+// border), shared bitwise by the two blocks of an edge.  Leaves are written
+// in collect_leaves order (hierarchy.hpp:76-91): state (row-major), county
+// within state (row-major), block within county (row-major); scb receives
+// (state, county, block) per leaf.
+int synth_nested(std::uint32_t sx, std::uint32_t sy, std::uint32_t cx, std::uint32_t cy,
+                 std::uint32_t bx, std::uint32_t by, std::uint32_t segs, double jitter,
+                 double sigma, double x0, double x1, double y0, double y1, std::uint64_t seed,
+                 int threads, double* vxy, std::uint64_t* ring_off, std::uint64_t* poly_ring,
+                 std::uint32_t* scb) {
+  if (!sx || !sy || !cx || !cy || !bx || !by || !segs) return 1;
+  const std::uint64_t NX = std::uint64_t{sx} * cx * bx, NY = std::uint64_t{sy} * cy * by;
+  const std::uint64_t S = segs;
+  const std::uint64_t CX = std::uint64_t{cx} * bx, CY = std::uint64_t{cy} * by;  // blocks per state
+  const double cw = (x1 - x0) / static_cast<double>(NX);
+  const double ch = (y1 - y0) / static_cast<double>(NY);
+  auto map_x = [&](double u) { return x0 + u * cw; };
+  auto map_y = [&](double v) { return y0 + v * ch; };
+  // state corners (lattice units of blocks)
+  std::vector<double> su((sx + 1) * (sy + 1)), sv((sx + 1) * (sy + 1));
+  for (std::uint32_t j = 0; j <= sy; ++j)
+    for (std::uint32_t i = 0; i <= sx; ++i) {
+      const std::uint64_t k = std::uint64_t{j} * (sx + 1) + i;
+      double u = static_cast<double>(i * CX), v = static_cast<double>(j * CY);
+      if (i > 0 && i < sx && j > 0 && j < sy && jitter > 0) {
+        u += jitter * CX * (2.0 * unit(draw(seed, 31, 2 * k)) - 1.0);
+        v += jitter * CY * (2.0 * unit(draw(seed, 31, 2 * k + 1)) - 1.0);
+      }
+      su[k] = u;
+      sv[k] = v;
+    }
+  // county corners: global county lattice (sx*cx + 1) x (sy*cy + 1)
+  const std::uint64_t KX = std::uint64_t{sx} * cx, KY = std::uint64_t{sy} * cy;
+  std::vector<double> ku((KX + 1) * (KY + 1)), kv((KX + 1) * (KY + 1));
+  auto bilerp = [](const double* q, double a, double b) {  // q: 00, 10, 01, 11
+    return (1 - a) * (1 - b) * q[0] + a * (1 - b) * q[1] + (1 - a) * b * q[2] + a * b * q[3];
+  };
+  parallel_for(KY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t J = jb; J < je; ++J)
+      for (std::uint64_t I = 0; I <= KX; ++I) {
+        const std::uint64_t si = std::min<std::uint64_t>(I / cx, sx - 1), sj = std::min<std::uint64_t>(J / cy, sy - 1);
+        const double a = static_cast<double>(I - si * cx) / cx, b = static_cast<double>(J - sj * cy) / cy;
+        const std::uint64_t c00 = sj * (sx + 1) + si;
+        const double qu[4] = {su[c00], su[c00 + 1], su[c00 + sx + 1], su[c00 + sx + 2]};
+        const double qv[4] = {sv[c00], sv[c00 + 1], sv[c00 + sx + 1], sv[c00 + sx + 2]};
+        double u = bilerp(qu, a, b), v = bilerp(qv, a, b);
+        const bool on_state_edge = (I % cx == 0) || (J % cy == 0);
+        if (!on_state_edge && jitter > 0) {
+          const std::uint64_t k = J * (KX + 1) + I;
+          u += jitter * bx * (2.0 * unit(draw(seed, 32, 2 * k)) - 1.0);
+          v += jitter * by * (2.0 * unit(draw(seed, 32, 2 * k + 1)) - 1.0);
+        }
+        ku[J * (KX + 1) + I] = u;
+        kv[J * (KX + 1) + I] = v;
+      }
+  });
+  // block lattice nodes (global), lattice units
+  std::vector<double> lu((NX + 1) * (NY + 1)), lv((NX + 1) * (NY + 1));
+  parallel_for(NY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t J = jb; J < je; ++J)
+      for (std::uint64_t I = 0; I <= NX; ++I) {
+        const std::uint64_t ki = std::min<std::uint64_t>(I / bx, KX - 1), kj = std::min<std::uint64_t>(J / by, KY - 1);
+        const double a = static_cast<double>(I - ki * bx) / bx, b = static_cast<double>(J - kj * by) / by;
+        const std::uint64_t c00 = kj * (KX + 1) + ki;
+        const double qu[4] = {ku[c00], ku[c00 + 1], ku[c00 + KX + 1], ku[c00 + KX + 2]};
+        const double qv[4] = {kv[c00], kv[c00 + 1], kv[c00 + KX + 1], kv[c00 + KX + 2]};
+        double u = bilerp(qu, a, b), v = bilerp(qv, a, b);
+        const bool on_county_edge = (I % bx == 0) || (J % by == 0);
+        if (!on_county_edge && jitter > 0) {
+          const std::uint64_t k = J * (NX + 1) + I;
+          u += jitter * (2.0 * unit(draw(seed, kStreamJitter, 2 * k)) - 1.0);
+          v += jitter * (2.0 * unit(draw(seed, kStreamJitter, 2 * k + 1)) - 1.0);
+        }
+        lu[J * (NX + 1) + I] = u;
+        lv[J * (NX + 1) + I] = v;
+      }
+  });
+  // edge subdivision points (lon/lat), shared by both neighbours
+  const std::uint64_t nh = NX * (NY + 1), nv = (NX + 1) * NY;
+  std::vector<double> hxy(2 * nh * (S - 1) + 2), vxy_e(2 * nv * (S - 1) + 2);
+  auto subdivide = [&](double au, double av, double bu, double bv, bool border,
+                       std::uint64_t stream, std::uint64_t e, double* dst) {
+    const double du = bu - au, dv = bv - av;
+    const double len = std::sqrt(du * du + dv * dv);
+    const double nu = len > 0 ? -dv / len : 0.0, nvv = len > 0 ? du / len : 0.0;
+    for (std::uint64_t k = 1; k < S; ++k) {
+      const double t = static_cast<double>(k) / static_cast<double>(S);
+      double u = au + du * t, v = av + dv * t;
+      if (!border && sigma > 0.0) {
+        const std::uint64_t idx = 2 * (e * S + k);
+        const double d = sigma * gauss(draw(seed, stream, idx), draw(seed, stream, idx + 1));
+        u += d * nu;
+        v += d * nvv;
+      }
+      dst[2 * (k - 1)] = map_x(u);
+      dst[2 * (k - 1) + 1] = map_y(v);
+    }
+  };
+  parallel_for(NY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t j = jb; j < je; ++j)
+      for (std::uint64_t i = 0; i < NX; ++i) {
+        const std::uint64_t e = j * NX + i, a = j * (NX + 1) + i;
+        subdivide(lu[a], lv[a], lu[a + 1], lv[a + 1], j == 0 || j == NY, kStreamHEdge, e,
+                  hxy.data() + 2 * e * (S - 1));
+      }
+  });
+  parallel_for(NY, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t j = jb; j < je; ++j)
+      for (std::uint64_t i = 0; i <= NX; ++i) {
+        const std::uint64_t e = j * (NX + 1) + i, a = e;
+        subdivide(lu[a], lv[a], lu[a + NX + 1], lv[a + NX + 1], i == 0 || i == NX, kStreamVEdge, e,
+                  vxy_e.data() + 2 * e * (S - 1));
+      }
+  });
+  std::vector<double> gx((NX + 1) * (NY + 1)), gy((NX + 1) * (NY + 1));
+  for (std::uint64_t j = 0; j <= NY; ++j)
+    for (std::uint64_t i = 0; i <= NX; ++i) {
+      const std::uint64_t k = j * (NX + 1) + i;
+      gx[k] = (i == 0) ? x0 : (i == NX) ? x1 : map_x(lu[k]);
+      gy[k] = (j == 0) ? y0 : (j == NY) ? y1 : map_y(lv[k]);
+    }
+  std::vector<double>().swap(lu);
+  std::vector<double>().swap(lv);
+  const std::uint64_t per_poly = 4 * S;
+  const std::uint64_t P = NX * NY;
+  const std::uint64_t per_state = CX * CY, per_county = std::uint64_t{bx} * by;
+  parallel_for(P, threads, [&](std::uint64_t pb, std::uint64_t pe) {
+    for (std::uint64_t p = pb; p < pe; ++p) {
+      // leaf p in collect_leaves order -> (state, county, block) -> lattice cell (i, j)
+      const std::uint64_t s = p / per_state, rem = p % per_state;
+      const std::uint64_t c = rem / per_county, b = rem % per_county;
+      const std::uint64_t si = s % sx, sj = s / sx, ci = c % cx, cj = c / cx, bi = b % bx, bj = b / bx;
+      const std::uint64_t i = (si * cx + ci) * bx + bi, j = (sj * cy + cj) * by + bj;
+      double* out = vxy + 2 * p * per_poly;
+      std::uint64_t w = 0;
+      auto put = [&](double x, double y) {
+        out[2 * w] = x;
+        out[2 * w + 1] = y;
+        ++w;
+      };
+      const std::uint64_t c00 = j * (NX + 1) + i, c10 = c00 + 1, c01 = c00 + (NX + 1), c11 = c01 + 1;
+      const double* hb = hxy.data() + 2 * (j * NX + i) * (S - 1);
+      const double* ht = hxy.data() + 2 * ((j + 1) * NX + i) * (S - 1);
+      const double* vl = vxy_e.data() + 2 * (j * (NX + 1) + i) * (S - 1);
+      const double* vr = vxy_e.data() + 2 * (j * (NX + 1) + i + 1) * (S - 1);
+      put(gx[c00], gy[c00]);
+      for (std::uint64_t k = 0; k + 1 < S; ++k) put(hb[2 * k], hb[2 * k + 1]);
+      put(gx[c10], gy[c10]);
+      for (std::uint64_t k = 0; k + 1 < S; ++k) put(vr[2 * k], vr[2 * k + 1]);
+      put(gx[c11], gy[c11]);
+      for (std::uint64_t k = S - 1; k-- > 0;) put(ht[2 * k], ht[2 * k + 1]);
+      put(gx[c01], gy[c01]);
+      for (std::uint64_t k = S - 1; k-- > 0;) put(vl[2 * k], vl[2 * k + 1]);
+      ring_off[p] = p * per_poly;
+      poly_ring[p] = p;
+      if (scb) {
+        scb[3 * p] = static_cast<std::uint32_t>(s);
+        scb[3 * p + 1] = static_cast<std::uint32_t>(c);
+        scb[3 * p + 2] = static_cast<std::uint32_t>(b);
+      }
+    }
+  });
+  ring_off[P] = P * per_poly;
+  poly_ring[P] = P;
+  return 0;
+}
+
 // Uniform points over box4 = {x0, x1, y0, y1}; point k of the stream is
 // global index offset + k.
 int synth_points_uniform(const double* box4, std::uint64_t n, std::uint64_t offset,

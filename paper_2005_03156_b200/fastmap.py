@@ -207,7 +207,9 @@ class CellIndex:
 
     def close(self) -> None:
         if getattr(self, "_h", None):
-            N.lib().fm_index_destroy(self._h)
+            lib = N.lib() if N is not None else None
+            if lib is not None:
+                lib.fm_index_destroy(self._h)
             self._h = None
 
     @property

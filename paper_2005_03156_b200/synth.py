@@ -107,6 +107,65 @@ class TilingConfig:
         return pts
 
 
+@dataclass(frozen=True)
+class NestedConfig:
+    """BASELINE config 3 (and 5): states -> counties -> blocks, conformal
+    nested jittered tilings; leaves are the blocks in collect_leaves order."""
+    name: str
+    sx: int
+    sy: int
+    cx: int
+    cy: int
+    bx: int
+    by: int
+    segs: int
+    jitter: float
+    sigma: float
+    n_points: int
+    seed: int = 0
+    n_centres: int = 20_000
+    centre_sigma_deg: float = 0.2
+    zipf_s: float = 1.1
+    frac_clustered: float = 0.9
+    points: str = "clustered"
+
+    @property
+    def n_polys(self) -> int:
+        return self.sx * self.sy * self.cx * self.cy * self.bx * self.by
+
+    def make_soup(self, threads: Optional[int] = None, with_scb: bool = False):
+        P = self.n_polys
+        vxy = np.empty((P * 4 * self.segs, 2), dtype=np.float64)
+        ring_off = np.empty(P + 1, dtype=np.uint64)
+        poly_ring = np.empty(P + 1, dtype=np.uint64)
+        scb = np.empty((P, 3), dtype=np.uint32)
+        x0, x1, y0, y1 = DOMAIN
+        rc = N.synth().synth_nested(self.sx, self.sy, self.cx, self.cy, self.bx, self.by,
+                                    self.segs, self.jitter, self.sigma, x0, x1, y0, y1,
+                                    self.seed, threads or _threads(), N.ptr(vxy, C.c_double),
+                                    N.ptr(ring_off, C.c_uint64), N.ptr(poly_ring, C.c_uint64),
+                                    N.ptr(scb, C.c_uint32))
+        if rc != 0:
+            raise ValueError("synth_nested failed")
+        soup = Soup(vxy, ring_off, poly_ring)
+        return (soup, scb) if with_scb else soup
+
+    def make_points(self, n: Optional[int] = None, offset: int = 0, soup=None,
+                    threads: Optional[int] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
+        n = self.n_points if n is None else int(n)
+        pts = out if out is not None else np.empty((n, 2), dtype=np.float64)
+        box = np.asarray(expanded_box(), dtype=np.float64)
+        dom = np.asarray(DOMAIN, dtype=np.float64)
+        rc = N.synth().synth_points_clustered(N.ptr(dom, C.c_double), N.ptr(box, C.c_double), n,
+                                              offset, self.seed + 1, self.n_centres,
+                                              self.centre_sigma_deg, self.zipf_s,
+                                              self.frac_clustered, threads or _threads(),
+                                              N.ptr(pts, C.c_double))
+        if rc != 0:
+            raise ValueError("point generation failed")
+        return pts
+
+
 CONFIGS = {
     # BASELINE configs[0]: small CPU-runnable case
     "c1": TilingConfig("c1", 32, 32, 8, 0.3, 0.05, 1_000_000, "uniform"),
@@ -114,6 +173,12 @@ CONFIGS = {
     "c2": TilingConfig("c2", 500, 500, 12, 0.3, 0.05, 100_000_000, "clustered"),
     # configs[3]: strongly concave blocks, half the points near an edge
     "c4": TilingConfig("c4", 400, 250, 50, 0.3, 0.15, 200_000_000, "near_edge"),
+    # configs[2]: 10x5 states, 20x20 counties each, 25x25 blocks each (12.5M leaves)
+    "c3": NestedConfig("c3", 10, 5, 20, 20, 25, 25, 6, 0.3, 0.05, 1_000_000_000),
+    # configs[4]: the c3 index with 8B points (sharded over GPUs) + histogram
+    "c5": NestedConfig("c5", 10, 5, 20, 20, 25, 25, 6, 0.3, 0.05, 8_000_000_000),
+    # reduced c3 with the same recipe, for parity tests (4 states, 40,000 leaves)
+    "c3mini": NestedConfig("c3mini", 2, 2, 4, 4, 25, 25, 6, 0.3, 0.05, 2_000_000),
 }
 
 

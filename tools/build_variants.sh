@@ -1,13 +1,13 @@
-# tuning variants of the product library (same sources, different -D knobs)
+# tuning variants of the product library: args like B8_U2_M3 (resolve warps,
+# stream points per lane, resolve min blocks per SM for __launch_bounds__)
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p paper_2005_03156_b200/_lib/var
 for v in "$@"; do
-  # v like W8_U2_P3072
-  W=$(echo $v | sed 's/W\([0-9]*\)_.*/\1/'); U=$(echo $v | sed 's/.*_U\([0-9]*\)_.*/\1/'); P=$(echo $v | sed 's/.*_P\([0-9]*\)/\1/')
+  B=$(echo $v | sed 's/B\([0-9]*\)_.*/\1/'); U=$(echo $v | sed 's/.*_U\([0-9]*\)_.*/\1/'); M=$(echo $v | sed 's/.*_M\([0-9]*\)/\1/')
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 \
-    -DFM_BWARPS=$W -DFM_KU=$U -DFM_BPOOL=$P -Xcompiler -fPIC,-O3,-ffp-contract=off,-pthread -shared \
+    -DFM_BWARPS=$B -DFM_KU=$U -DFM_BMINB=$M -Xcompiler -fPIC,-O3,-ffp-contract=off,-pthread -shared \
     paper_2005_03156_b200/csrc/fastmap_b200.cu paper_2005_03156_b200/csrc/index_host.cpp \
-    -o paper_2005_03156_b200/_lib/var/lib_$v.so &
+    -o paper_2005_03156_b200/_lib/var/lib_$v.so -Xptxas -v 2> paper_2005_03156_b200/_lib/var/ptxas_$v.log &
 done
 wait
