@@ -99,6 +99,11 @@ typedef struct fm_index_stats {
   uint64_t max_record_edges, max_record_cands;
   double gx0, gx1, gy0, gy1, cell_w, cell_h, margin;
   double build_seconds;
+  int32_t built_on_gpu;   /* 1 when fm_index_build ran the GPU builder */
+  int32_t reserved0;
+  uint64_t cells_split;   /* 2x2 split nodes */
+  uint64_t slots_phase1;  /* slots of cells that fit one slot */
+  uint64_t slots_total;
 } fm_index_stats;
 
 /* Optional per-call work counters (diagnostics; device-side atomics). */

@@ -59,6 +59,8 @@ class IndexStats(C.Structure):
         ("gx0", C.c_double), ("gx1", C.c_double), ("gy0", C.c_double), ("gy1", C.c_double),
         ("cell_w", C.c_double), ("cell_h", C.c_double), ("margin", C.c_double),
         ("build_seconds", C.c_double),
+        ("built_on_gpu", C.c_int32), ("reserved0", C.c_int32),
+        ("cells_split", u64), ("slots_phase1", u64), ("slots_total", u64),
     ]
 
     def as_dict(self) -> dict:

@@ -106,17 +106,6 @@ __device__ __forceinline__ void emit(int* __restrict__ out, unsigned long long* 
   if (kHist && id >= 0) atomicAdd(hist + id, 1ull);
 }
 
-__device__ __forceinline__ std::uint32_t warp_excl_scan(std::uint32_t v, int lane,
-                                                        std::uint32_t* total) {
-  std::uint32_t incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const std::uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  *total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-  return incl - v;
-}
 
 template <bool kHist, bool kCount>
 __global__ void __launch_bounds__(kAWarps * 32)
@@ -272,7 +261,7 @@ __device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const
 }
 
 #ifndef FM_BMINB
-#define FM_BMINB 1
+#define FM_BMINB 2
 #endif
 template <bool kHist, bool kCount>
 __global__ void __launch_bounds__(kBWarps * 32, FM_BMINB)
@@ -549,8 +538,15 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   fm_index* ix = new (std::nothrow) fm_index();
   if (!ix) return set_err(FM_ERR_OOM, "host allocation failed");
   const auto t0 = std::chrono::steady_clock::now();
+  const bool on_gpu = p.build_on_gpu && p.device >= 0;
   try {
-    ix->host = fm::build_index_host(soup, opt);
+    if (on_gpu) {
+      fm::build_index_gpu(soup, opt, p.device, ix->host, &ix->d_grid, &ix->d_slots, &ix->slots_len,
+                          &ix->d_overflow, &ix->overflow_len);
+      ix->device = p.device;
+    } else {
+      ix->host = fm::build_index_host(soup, opt);
+    }
   } catch (const fm::InvalidArgument& e) {
     delete ix;
     return set_err(FM_ERR_INVALID_ARGUMENT, e.what());
@@ -570,9 +566,11 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   ix->ax1 = std::min(ix->g.gx1, 180.0);
   ix->ay0 = std::max(ix->g.gy0, -90.0);
   ix->ay1 = std::min(ix->g.gy1, 90.0);
-  ix->grid_len = ix->host.grid.size();
-  ix->slots_len = ix->host.slots.size();
-  ix->overflow_len = ix->host.overflow.size();
+  ix->grid_len = static_cast<std::uint64_t>(ix->g.nx * ix->g.ny);
+  if (!on_gpu) {
+    ix->slots_len = ix->host.slots.size();
+    ix->overflow_len = ix->host.overflow.size();
+  }
 
   fm_index_stats& s = ix->stats;
   s.n_polys = n_polys;
@@ -586,6 +584,10 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   s.cells_boundary = ix->host.stats.cells_boundary;
   s.grid_bytes = ix->grid_len * 4;
   s.arena_bytes = ix->host.n_slots * fm::kSlotBytes + (ix->overflow_len - 512);
+  s.built_on_gpu = on_gpu ? 1 : 0;
+  s.cells_split = ix->host.stats.cells_split;
+  s.slots_phase1 = ix->host.n_phase1_slots;
+  s.slots_total = ix->host.n_slots;
   s.geometry_bytes = s.n_vertices * 16;
   s.record_edges = ix->host.stats.record_edges;
   s.record_cands = ix->host.stats.record_cands;
@@ -600,7 +602,7 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   s.cell_h = ix->g.h;
   s.margin = ix->g.margin;
 
-  if (ix->device >= 0) {
+  if (ix->device >= 0 && !on_gpu) {
     DeviceGuard guard(ix->device);
     if (!guard.ok) {
       delete ix;
@@ -622,16 +624,19 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
       delete ix;
       return set_err(FM_ERR_CUDA, "index upload failed");
     }
+    // the device copy is authoritative; drop the host arrays
+    std::vector<std::uint32_t>().swap(ix->host.grid);
+    std::vector<std::uint8_t>().swap(ix->host.slots);
+    std::vector<std::uint8_t>().swap(ix->host.overflow);
+  }
+  if (ix->device >= 0) {
+    DeviceGuard guard(ix->device);
     // keep stream-ordered scratch (the boundary queue) cached between calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, ix->device) == cudaSuccess) {
       std::uint64_t thr = ~std::uint64_t{0};
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    // the device copy is authoritative; drop the host arrays
-    std::vector<std::uint32_t>().swap(ix->host.grid);
-    std::vector<std::uint8_t>().swap(ix->host.slots);
-    std::vector<std::uint8_t>().swap(ix->host.overflow);
   }
   s.build_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -41,6 +41,7 @@ struct HostIndex {
   std::vector<std::uint32_t> grid;
   std::vector<std::uint8_t> slots;     // 128-byte boundary slots
   std::uint64_t n_slots = 0;
+  std::uint64_t n_phase1_slots = 0;    // slots of cells that fit one slot (row-major first)
   std::vector<std::uint8_t> overflow;  // variable-size records past the split depth, + 512 B tail
   BuildStats stats;
 };
@@ -57,7 +58,27 @@ struct RuntimeError : std::runtime_error {
 // geometry.hpp:74-77; finite vertices; monotone offsets) and fixes the grid.
 GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st);
 
-// Host builder: C++ threads over grid rows.
+// Host builder: C++ threads over grid rows.  Slot order (shared with the
+// GPU builder, so both emit identical arrays): phase 1 -- every cell whose
+// content fits one slot, row-major; phase 2 -- the split / overflow subtree
+// of every other boundary cell, row-major, each subtree in post-order.
 HostIndex build_index_host(const Soup& s, const BuildOptions& o);
+
+// Phase 2 for cells the GPU builder deferred (linear ids, row-major, with
+// their candidate leaves as a CSR); appends after `slot_base` slots and
+// writes their grid entries.
+void finish_deferred_cells(const Soup& s, const GridGeom& g, const BuildOptions& o,
+                           const std::vector<std::int64_t>& cells,
+                           const std::vector<std::uint64_t>& cand_off,
+                           const std::vector<std::uint32_t>& cand_ids, std::uint64_t slot_base,
+                           std::vector<std::uint32_t>& grid, std::vector<std::uint8_t>& slots_out,
+                           std::vector<std::uint8_t>& ovf_out, BuildStats& stats);
+
+// GPU builder (index_gpu.cu): same arrays as build_index_host, built on
+// `device`; returns the device arrays (ownership to the caller) and fills
+// out.g / out.stats / out.n_slots (no host copies of the arrays).
+void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex& out,
+                     std::uint32_t** dev_grid, std::uint8_t** dev_slots, std::uint64_t* slots_len,
+                     std::uint8_t** dev_overflow, std::uint64_t* overflow_len);
 
 }  // namespace fm

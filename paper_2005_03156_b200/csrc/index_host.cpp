@@ -30,42 +30,15 @@
 
 #include "index_build.h"
 #include "record_encode.h"
+#include "sweep.h"
 
 namespace fm {
 namespace {
 
-// smallest k in [0, n) with g0 + (k+1)*step >= v; n if none
-std::int64_t first_with_hi_ge(double g0, double step, double inv, std::int64_t n,
-                              double v) {
-  double f = std::floor((v - g0) * inv) - 1.0;
-  std::int64_t k = !(f > 0.0) ? 0 : (f > static_cast<double>(n) ? n : static_cast<std::int64_t>(f));
-  auto hi = [&](std::int64_t q) { return g0 + static_cast<double>(q + 1) * step; };
-  while (k > 0 && hi(k - 1) >= v) --k;
-  while (k < n && hi(k) < v) ++k;
-  return k;
-}
-
-// largest k in [0, n) with g0 + k*step <= v; -1 if none
-std::int64_t last_with_lo_le(double g0, double step, double inv, std::int64_t n,
-                             double v) {
-  double f = std::floor((v - g0) * inv) + 1.0;
-  std::int64_t k = !(f > -1.0) ? -1
-                   : (f > static_cast<double>(n - 1) ? n - 1 : static_cast<std::int64_t>(f));
-  auto lo = [&](std::int64_t q) { return g0 + static_cast<double>(q) * step; };
-  while (k >= 0 && lo(k) > v) --k;
-  while (k + 1 < n && lo(k + 1) <= v) ++k;
-  return k;
-}
-
-struct PolySpan {
-  double x0, x1, y0, y1;
-  std::int64_t c0, c1, r0, r1;
-  bool active;
-};
-
 struct Contrib {
   std::uint32_t id;
   std::uint32_t c0;
+  std::uint32_t force_defer;     // phase-1 capacity rule hit (sweep.h)
   std::uint32_t e_begin, e_end;  // into the row edge pool
   std::uint32_t b_begin, b_end;  // into the row break pool
 };
@@ -83,6 +56,21 @@ void toggle(std::vector<double>& set, double v) {
     set.insert(it, v);
   }
 }
+
+// One leaf's contribution to a rectangle: its near edges, the constant
+// parity c0 of the edges wholly right of it, and the breakpoints.
+struct PolyC {
+  std::uint32_t id = 0, c0 = 0;
+  bool force_defer = false;  // phase-1 capacity rule hit (sweep.h)
+  std::vector<Edge4> near;
+  std::vector<double> breaks;  // ascending, distinct
+  bool constant() const { return near.empty() && breaks.empty(); }
+};
+
+struct Deferred {
+  std::int64_t ix;
+  std::vector<PolyC> list;
+};
 
 struct RowWorker {
   const Soup& s;
@@ -115,33 +103,16 @@ struct RowWorker {
 
   void gather_edges(std::uint32_t pid, double ys0, double ys1) {
     rel.clear();
-    const double d = g.margin;
     for (std::uint64_t r = s.poly_ring[pid]; r < s.poly_ring[pid + 1]; ++r) {
       const std::uint64_t b = s.ring_off[r], e = s.ring_off[r + 1], n = e - b;
       for (std::uint64_t i = 0; i < n; ++i) {
         const std::uint64_t a = b + i, c = (i + 1 < n) ? a + 1 : b;
-        Edge4 E{s.vxy[2 * a], s.vxy[2 * a + 1], s.vxy[2 * c], s.vxy[2 * c + 1]};
-        if (E.ly > E.hy) {  // orient upward exactly like geometry.hpp:219
-          std::swap(E.lx, E.hx);
-          std::swap(E.ly, E.hy);
+        SlabEdge se;
+        if (!slab_edge(g, tol, ys0, ys1, s.vxy[2 * a], s.vxy[2 * a + 1], s.vxy[2 * c],
+                       s.vxy[2 * c + 1], &se)) {
+          continue;
         }
-        if (E.ly == E.hy) continue;               // horizontal: never in range
-        if (E.hy <= ys0 || E.ly >= ys1) continue;  // y-disjoint with the slab
-        const double ya = std::max(E.ly, ys0), yb = std::min(E.hy, ys1);
-        const double slope = (E.hx - E.lx) / (E.hy - E.ly);
-        const double mnx = std::min(E.lx, E.hx), mxx = std::max(E.lx, E.hx);
-        auto x_at = [&](double y) {
-          double x = E.lx + (y - E.ly) * slope;
-          return std::min(mxx, std::max(mnx, x));
-        };
-        const double xa = (ya == E.ly) ? E.lx : x_at(ya);
-        const double xb = (yb == E.hy) ? E.hx : x_at(yb);
-        const double ex0 = std::min(xa, xb) - tol, ex1 = std::max(xa, xb) + tol;
-        RelEdge re;
-        re.tlo = first_with_hi_ge(g.gx0, g.w, g.inv_w, g.nx, ex0 - d);
-        re.thi = last_with_lo_le(g.gx0, g.w, g.inv_w, g.nx, ex1 + d);
-        re.e = E;
-        rel.push_back(re);
+        rel.push_back({se.tlo, se.thi, Edge4{se.lx, se.ly, se.hx, se.hy}});
       }
     }
   }
@@ -156,15 +127,18 @@ struct RowWorker {
     tog.clear();
     std::uint32_t c0par = 0;
     std::size_t k = 0;
+    std::size_t raw_breaks = 0;  // in-slab endpoints of right edges (sweep.h cap)
     auto add_right = [&](const RelEdge& re) {
       for (const double m : {re.e.ly, re.e.hy}) {
         if (m < ys0) {
           c0par ^= 1u;
         } else if (m < ys1) {
           toggle(tog, m);
+          ++raw_breaks;
         }
       }
     };
+    const bool rel_over = rel.size() > static_cast<std::size_t>(kRelCap);
     for (std::int64_t ix = sp.c1; ix >= sp.c0; --ix) {
       while (k < order.size() && rel[order[k]].tlo > ix) add_right(rel[order[k++]]);
       if (closed[ix]) continue;
@@ -173,10 +147,13 @@ struct RowWorker {
         if (re.tlo <= ix && ix <= re.thi) epool.push_back(re.e);
       }
       const std::uint32_t ee = static_cast<std::uint32_t>(epool.size());
-      if (ee == eb && tog.empty()) {
+      const std::uint32_t force = (rel_over || ee - eb > static_cast<std::uint32_t>(kNearCap) ||
+                                   tog.size() > static_cast<std::size_t>(kBreakCap) ||
+                                   raw_breaks > static_cast<std::size_t>(kBreakRawCap)) ? 1u : 0u;
+      if (ee == eb && tog.empty() && !force) {
         if (c0par) {  // constant-true leaf: terminal for this cell
           if (cols[ix].empty()) touched.push_back(ix);
-          cols[ix].push_back({pid, 1u, eb, eb, 0, 0});
+          cols[ix].push_back({pid, 1u, 0u, eb, eb, 0, 0});
           closed[ix] = 1;
         }
         continue;
@@ -184,18 +161,9 @@ struct RowWorker {
       const std::uint32_t bb = static_cast<std::uint32_t>(bpool.size());
       bpool.insert(bpool.end(), tog.begin(), tog.end());
       if (cols[ix].empty()) touched.push_back(ix);
-      cols[ix].push_back({pid, c0par, eb, ee, bb, static_cast<std::uint32_t>(bpool.size())});
+      cols[ix].push_back({pid, c0par, force, eb, ee, bb, static_cast<std::uint32_t>(bpool.size())});
     }
   }
-
-  // One leaf's contribution to a rectangle: its near edges, the constant
-  // parity c0 of the edges wholly right of it, and the breakpoints.
-  struct PolyC {
-    std::uint32_t id = 0, c0 = 0;
-    std::vector<Edge4> near;
-    std::vector<double> breaks;  // ascending, distinct
-    bool constant() const { return near.empty() && breaks.empty(); }
-  };
 
   // Re-derive a leaf's contribution for a sub-rectangle of the rectangle
   // `par` was computed for: edges right of the parent
@@ -249,12 +217,16 @@ struct RowWorker {
   // Appends slots to `slots` (row-local slot numbers; every u32 child entry
   // and u64 overflow offset inside a slot is listed for relocation).
   std::uint32_t finalize(const std::vector<PolyC>& list, double rx0, double ry0, double cw,
-                         double chh, int depth) {
+                         double chh, int depth, bool* deferred = nullptr) {
     std::vector<Edge4> U;
     std::vector<CandIn> cin;
     std::vector<std::size_t> src;  // index into list per candidate
     for (std::size_t q = 0; q < list.size(); ++q) {
       const PolyC& pc = list[q];
+      if (deferred && pc.force_defer) {  // phase-1 capacity rules (sweep.h)
+        *deferred = true;
+        return kEmpty;
+      }
       CandIn cd;
       cd.id = pc.id;
       cd.c0 = pc.c0;
@@ -281,6 +253,11 @@ struct RowWorker {
       cin.push_back(std::move(cd));
       src.push_back(q);
     }
+    if (deferred && (cin.size() > static_cast<std::size_t>(kCellCands) ||
+                     U.size() > static_cast<std::size_t>(kCellEdges))) {
+      *deferred = true;  // phase-1 per-cell limits (sweep.h)
+      return kEmpty;
+    }
     if (cin.empty()) return kEmpty;
     if (cin.front().edges.empty() && cin.front().breaks.empty()) return cin.front().id;
     // drop edges no candidate references any more
@@ -304,6 +281,10 @@ struct RowWorker {
       note_leaf(used.size(), cin.size(), n_breaks);
       es.compact++;
       return kRecordBit | static_cast<std::uint32_t>(k);
+    }
+    if (deferred) {  // phase 1: cells that need a split or overflow wait for phase 2
+      *deferred = true;
+      return kEmpty;
     }
     if (depth < kMaxSplitDepth && cw > 256.0 * g.margin && chh > 256.0 * g.margin) {
       // split 2x2: child (i, j) covers [rx0 + i*cw/2, rx0 + (i+1)*cw/2] x ...
@@ -361,14 +342,13 @@ struct RowWorker {
     st.max_record_cands = std::max(st.max_record_cands, nc);
   }
 
+  // Phase 1 for one grid row: classify every cell; hits and empties go to
+  // the grid, cells that fit one slot get it (row-local numbering), the
+  // rest are deferred with their contributions.
   void run_row(std::int64_t iy, const std::uint32_t* ids, std::uint64_t n_ids,
                std::uint32_t* grid_row, std::vector<std::uint8_t>& row_slots,
-               std::vector<std::uint8_t>& row_ovf, std::vector<std::int64_t>& rec_cols,
-               std::vector<std::uint64_t>& spatch, std::vector<std::uint64_t>& opatch) {
+               std::vector<std::int64_t>& rec_cols, std::vector<Deferred>& deferred) {
     slots.clear();
-    ovf = &row_ovf;
-    slot_patches = &spatch;
-    ovf_patches = &opatch;
     const double ys0 = cell_y0(g, iy) - g.margin;
     const double ys1 = cell_y0(g, iy + 1) + g.margin;
     epool.clear();
@@ -383,25 +363,89 @@ struct RowWorker {
         PolyC pc;
         pc.id = c.id;
         pc.c0 = c.c0;
+        pc.force_defer = c.force_defer != 0;
         pc.near.assign(epool.begin() + c.e_begin, epool.begin() + c.e_end);
         pc.breaks.assign(bpool.begin() + c.b_begin, bpool.begin() + c.b_end);
         list.push_back(std::move(pc));
       }
-      const std::uint32_t e = finalize(list, cell_x0(g, ix), cell_y0(g, iy), g.w, g.h, 0);
-      grid_row[ix] = e;
-      if (e == kEmpty) {
-        st.cells_empty++;
-      } else if (e < kRecordBit) {
-        st.cells_hit++;
-      } else {
+      bool defer = false;
+      const std::uint32_t e = finalize(list, cell_x0(g, ix), cell_y0(g, iy), g.w, g.h, 0, &defer);
+      if (defer) {
+        deferred.push_back({ix, std::move(list)});
+        list = {};
+        grid_row[ix] = kEmpty;  // set in phase 2
         st.cells_boundary++;
-        rec_cols.push_back(ix);
+      } else {
+        grid_row[ix] = e;
+        if (e == kEmpty) {
+          st.cells_empty++;
+        } else if (e < kRecordBit) {
+          st.cells_hit++;
+        } else {
+          st.cells_boundary++;
+          rec_cols.push_back(ix);
+        }
       }
       cols[ix].clear();
       closed[ix] = 0;
     }
     st.cells_empty += static_cast<std::uint64_t>(g.nx) - touched.size();
     row_slots.swap(slots);
+  }
+
+  // Phase 2 for one grid row: the deferred cells' split / overflow subtrees
+  // (row-local slot numbers and overflow offsets, patch lists for both).
+  void run_deferred(std::int64_t iy, const std::vector<Deferred>& deferred,
+                    std::vector<std::uint8_t>& row_slots, std::vector<std::uint8_t>& row_ovf,
+                    std::vector<std::uint64_t>& spatch, std::vector<std::uint64_t>& opatch,
+                    std::vector<std::uint32_t>& entries) {
+    slots.clear();
+    ovf = &row_ovf;
+    slot_patches = &spatch;
+    ovf_patches = &opatch;
+    entries.clear();
+    for (const Deferred& d : deferred) {
+      entries.push_back(finalize(d.list, cell_x0(g, d.ix), cell_y0(g, iy), g.w, g.h, 0));
+    }
+    row_slots.swap(slots);
+  }
+
+  // Contributions of the given leaves (ascending ids) to cell (ix, iy),
+  // computed directly -- the same arithmetic as the row sweep (used for the
+  // cells the GPU builder hands back).
+  void cell_contribs(std::int64_t ix, std::int64_t iy, const std::uint32_t* ids, std::uint64_t n,
+                     std::vector<PolyC>& list) {
+    list.clear();
+    const double ys0 = cell_y0(g, iy) - g.margin;
+    const double ys1 = cell_y0(g, iy + 1) + g.margin;
+    for (std::uint64_t q = 0; q < n; ++q) {
+      gather_edges(ids[q], ys0, ys1);
+      PolyC pc;
+      pc.id = ids[q];
+      std::uint32_t c0 = 0;
+      for (const RelEdge& re : rel) {
+        if (re.tlo > ix) {
+          for (const double m : {re.e.ly, re.e.hy}) {
+            if (m < ys0) {
+              c0 ^= 1u;
+            } else if (m < ys1) {
+              toggle(pc.breaks, m);
+            }
+          }
+        } else if (re.thi >= ix) {
+          pc.near.push_back(re.e);
+        }
+      }
+      pc.c0 = c0;
+      if (pc.constant()) {
+        if (c0) {
+          list.push_back(std::move(pc));
+          return;  // terminal: later leaves never matter
+        }
+        continue;
+      }
+      list.push_back(std::move(pc));
+    }
   }
 };
 
@@ -503,6 +547,157 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
   return g;
 }
 
+namespace {
+
+std::vector<PolySpan> compute_spans(const Soup& s, const GridGeom& g) {
+  std::vector<PolySpan> spans(s.n_polys);
+  for (std::uint64_t p = 0; p < s.n_polys; ++p) {
+    PolySpan& sp = spans[p];
+    sp.active = 0;
+    if (s.poly_ring[p + 1] <= s.poly_ring[p]) continue;
+    double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+    for (std::uint64_t v = s.ring_off[s.poly_ring[p]]; v < s.ring_off[s.poly_ring[p + 1]]; ++v) {
+      x0 = std::min(x0, s.vxy[2 * v]);
+      x1 = std::max(x1, s.vxy[2 * v]);
+      y0 = std::min(y0, s.vxy[2 * v + 1]);
+      y1 = std::max(y1, s.vxy[2 * v + 1]);
+    }
+    polygon_span(g, x0, x1, y0, y1, &sp);
+  }
+  return spans;
+}
+
+// Row -> leaves CSR (ascending ids per row).
+void row_lists(const std::vector<PolySpan>& spans, const GridGeom& g,
+               std::vector<std::uint64_t>& row_count, std::vector<std::uint32_t>& row_ids) {
+  row_count.assign(static_cast<std::size_t>(g.ny) + 1, 0);
+  for (const PolySpan& sp : spans) {
+    if (!sp.active) continue;
+    for (std::int64_t r = sp.r0; r <= sp.r1; ++r) row_count[static_cast<std::size_t>(r) + 1]++;
+  }
+  for (std::int64_t r = 0; r < g.ny; ++r) row_count[r + 1] += row_count[r];
+  row_ids.resize(row_count[static_cast<std::size_t>(g.ny)]);
+  std::vector<std::uint64_t> fill(row_count.begin(), row_count.end() - 1);
+  for (std::uint64_t p = 0; p < spans.size(); ++p) {
+    if (!spans[p].active) continue;
+    for (std::int64_t r = spans[p].r0; r <= spans[p].r1; ++r) {
+      row_ids[fill[static_cast<std::size_t>(r)]++] = static_cast<std::uint32_t>(p);
+    }
+  }
+}
+
+template <typename Fn>
+void parallel_rows(std::int64_t ny, int threads, Fn fn) {
+  std::atomic<std::int64_t> next{0};
+  std::mutex mu;
+  std::exception_ptr failure;
+  auto worker = [&](int t) {
+    try {
+      fn(t, next);
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!failure) failure = std::current_exception();
+      next.store(ny);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(worker, t);
+  worker(0);
+  for (auto& th : pool) th.join();
+  if (failure) std::rethrow_exception(failure);
+}
+
+int thread_count(const BuildOptions& o, std::int64_t ny) {
+  int threads = o.threads > 0 ? o.threads : static_cast<int>(std::thread::hardware_concurrency());
+  if (threads < 1) threads = 1;
+  return static_cast<int>(std::min<std::int64_t>(threads, std::max<std::int64_t>(ny, 1)));
+}
+
+void merge_stats(BuildStats& into, const BuildStats& st) {
+  into.cells_empty += st.cells_empty;
+  into.cells_hit += st.cells_hit;
+  into.cells_boundary += st.cells_boundary;
+  into.record_edges += st.record_edges;
+  into.record_cands += st.record_cands;
+  into.record_breaks += st.record_breaks;
+  into.max_record_edges = std::max(into.max_record_edges, st.max_record_edges);
+  into.max_record_cands = std::max(into.max_record_cands, st.max_record_cands);
+  into.records_compact += st.records_compact;
+  into.records_wide += st.records_wide;
+  into.records += st.records;
+  into.records_overflow += st.records_overflow;
+  into.cells_split += st.cells_split;
+}
+
+}  // namespace
+
+// Phase 2 (shared by the host and GPU builders): the deferred cells of each
+// row, in row-major order, get their split / overflow subtrees appended
+// after `slot_base` slots; their grid entries are written into `grid`.
+void finish_deferred(const Soup& s, const GridGeom& g, const BuildOptions& o,
+                     std::vector<std::vector<Deferred>>& deferred, std::uint64_t slot_base,
+                     std::vector<std::uint32_t>& grid, std::vector<std::uint8_t>& slots_out,
+                     std::vector<std::uint8_t>& ovf_out, BuildStats& stats) {
+  const std::size_t NY = deferred.size();
+  const int threads = thread_count(o, static_cast<std::int64_t>(NY));
+  std::vector<std::vector<std::uint8_t>> rs(NY), ro(NY);
+  std::vector<std::vector<std::uint64_t>> sp(NY), op(NY);
+  std::vector<std::vector<std::uint32_t>> ent(NY);
+  std::vector<BuildStats> st(static_cast<std::size_t>(threads));
+  std::vector<PolySpan> no_spans;
+  const double tol = classify_tol(g);
+  parallel_rows(static_cast<std::int64_t>(NY), threads, [&](int t, std::atomic<std::int64_t>& next) {
+    RowWorker w(s, g, no_spans, tol);
+    for (;;) {
+      const std::int64_t r = next.fetch_add(1);
+      if (r >= static_cast<std::int64_t>(NY)) break;
+      if (deferred[r].empty()) continue;
+      w.run_deferred(r, deferred[r], rs[r], ro[r], sp[r], op[r], ent[r]);
+    }
+    st[t] = w.st;
+    st[t].records_compact = w.es.compact;
+    st[t].records_wide = w.es.wide;
+  });
+  std::uint64_t n_slots = 0, ovf_bytes = 0;
+  std::vector<std::uint64_t> sb(NY), ob(NY);
+  for (std::size_t r = 0; r < NY; ++r) {
+    sb[r] = slot_base + n_slots;
+    ob[r] = ovf_bytes;
+    n_slots += rs[r].size() / kSlotBytes;
+    ovf_bytes += (ro[r].size() + 15) & ~std::uint64_t{15};
+  }
+  if (slot_base + n_slots >= kRecordBit) throw RuntimeError("index needs more than 2^31 slots");
+  slots_out.assign(n_slots * kSlotBytes, 0);
+  ovf_out.assign(ovf_bytes, 0);
+  std::uint64_t so = 0;
+  for (std::size_t r = 0; r < NY; ++r) {
+    if (rs[r].empty() && ent[r].empty()) continue;
+    const std::uint32_t base = static_cast<std::uint32_t>(sb[r]);
+    std::uint8_t* dst = slots_out.data() + so;
+    if (!rs[r].empty()) std::memcpy(dst, rs[r].data(), rs[r].size());
+    if (!ro[r].empty()) std::memcpy(ovf_out.data() + ob[r], ro[r].data(), ro[r].size());
+    for (const std::uint64_t pos : sp[r]) {
+      std::uint32_t v;
+      std::memcpy(&v, dst + pos, 4);
+      v += base;
+      std::memcpy(dst + pos, &v, 4);
+    }
+    for (const std::uint64_t pos : op[r]) {
+      std::uint64_t v;
+      std::memcpy(&v, dst + pos, 8);
+      v += ob[r];
+      std::memcpy(dst + pos, &v, 8);
+    }
+    for (std::size_t k = 0; k < deferred[r].size(); ++k) {
+      std::uint32_t e = ent[r][k];
+      if (e >= kRecordBit && e != kEmpty) e += base;
+      grid[r * static_cast<std::size_t>(g.nx) + static_cast<std::size_t>(deferred[r][k].ix)] = e;
+    }
+    so += rs[r].size();
+  }
+  for (const auto& x : st) merge_stats(stats, x);
+}
+
 HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
   HostIndex out;
   out.g = plan_grid(s, o, &out.stats);
@@ -515,140 +710,83 @@ HostIndex build_index_host(const Soup& s, const BuildOptions& o) {
     out.stats.cells_empty = ncell;
     return out;
   }
-  const double d = g.margin;
-  std::vector<PolySpan> spans(s.n_polys);
-  std::vector<std::uint64_t> row_count(static_cast<std::size_t>(g.ny) + 1, 0);
-  for (std::uint64_t p = 0; p < s.n_polys; ++p) {
-    PolySpan& sp = spans[p];
-    sp.active = s.poly_ring[p + 1] > s.poly_ring[p];
-    if (!sp.active) continue;
-    double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
-    for (std::uint64_t v = s.ring_off[s.poly_ring[p]]; v < s.ring_off[s.poly_ring[p + 1]]; ++v) {
-      x0 = std::min(x0, s.vxy[2 * v]);
-      x1 = std::max(x1, s.vxy[2 * v]);
-      y0 = std::min(y0, s.vxy[2 * v + 1]);
-      y1 = std::max(y1, s.vxy[2 * v + 1]);
-    }
-    sp.x0 = x0;
-    sp.x1 = x1;
-    sp.y0 = y0;
-    sp.y1 = y1;
-    sp.c0 = first_with_hi_ge(g.gx0, g.w, g.inv_w, g.nx, x0 - d);
-    sp.c1 = last_with_lo_le(g.gx0, g.w, g.inv_w, g.nx, x1 + d);
-    sp.r0 = first_with_hi_ge(g.gy0, g.h, g.inv_h, g.ny, y0 - d);
-    sp.r1 = last_with_lo_le(g.gy0, g.h, g.inv_h, g.ny, y1 + d);
-    if (sp.c0 > sp.c1 || sp.r0 > sp.r1) {
-      sp.active = false;
-      continue;
-    }
-    for (std::int64_t r = sp.r0; r <= sp.r1; ++r) row_count[static_cast<std::size_t>(r) + 1]++;
-  }
-  for (std::int64_t r = 0; r < g.ny; ++r) row_count[r + 1] += row_count[r];
-  std::vector<std::uint32_t> row_ids(row_count[static_cast<std::size_t>(g.ny)]);
-  {
-    std::vector<std::uint64_t> fill(row_count.begin(), row_count.end() - 1);
-    for (std::uint64_t p = 0; p < s.n_polys; ++p) {
-      if (!spans[p].active) continue;
-      for (std::int64_t r = spans[p].r0; r <= spans[p].r1; ++r) {
-        row_ids[fill[static_cast<std::size_t>(r)]++] = static_cast<std::uint32_t>(p);
-      }
-    }
-  }
-
-  const double M = std::max(std::max(std::fabs(g.gx0), std::fabs(g.gx1)),
-                            std::max(std::fabs(g.gy0), std::fabs(g.gy1)));
-  const double tol = std::ldexp(std::max(1.0, M), -46);
-  int threads = o.threads > 0 ? o.threads : static_cast<int>(std::thread::hardware_concurrency());
-  if (threads < 1) threads = 1;
-  threads = static_cast<int>(std::min<std::int64_t>(threads, g.ny));
-
+  const std::vector<PolySpan> spans = compute_spans(s, g);
+  std::vector<std::uint64_t> row_count;
+  std::vector<std::uint32_t> row_ids;
+  row_lists(spans, g, row_count, row_ids);
+  const double tol = classify_tol(g);
+  const int threads = thread_count(o, g.ny);
   const std::size_t NY = static_cast<std::size_t>(g.ny);
-  std::vector<std::vector<std::uint8_t>> row_slots(NY), row_ovf(NY);
-  std::vector<std::vector<std::int64_t>> row_recs(NY);
-  std::vector<std::vector<std::uint64_t>> row_spatch(NY), row_opatch(NY);
-  std::atomic<std::int64_t> next{0};
-  std::mutex mu;
-  std::exception_ptr failure;
-  std::vector<BuildStats> stats(static_cast<std::size_t>(threads));
-  auto worker = [&](int t) {
-    try {
-      RowWorker w(s, g, spans, tol);
-      for (;;) {
-        const std::int64_t iy = next.fetch_add(1);
-        if (iy >= g.ny) break;
-        w.run_row(iy, row_ids.data() + row_count[iy], row_count[iy + 1] - row_count[iy],
-                  out.grid.data() + iy * g.nx, row_slots[iy], row_ovf[iy], row_recs[iy],
-                  row_spatch[iy], row_opatch[iy]);
-      }
-      stats[t] = w.st;
-      stats[t].records_compact = w.es.compact;
-      stats[t].records_wide = w.es.wide;
-    } catch (...) {
-      std::lock_guard<std::mutex> lk(mu);
-      if (!failure) failure = std::current_exception();
-      next.store(g.ny);
-    }
-  };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < threads; ++t) pool.emplace_back(worker, t);
-  worker(0);
-  for (auto& th : pool) th.join();
-  if (failure) std::rethrow_exception(failure);
 
-  // Concatenate the rows' slot arenas and overflow arenas, then relocate:
-  // row-local slot numbers (grid entries, split children) gain the row's
-  // slot base, overflow offsets the row's overflow base.
-  std::uint64_t n_slots = 0, ovf_bytes = 0;
-  std::vector<std::uint64_t> slot_base(NY), ovf_base(NY);
+  // phase 1: every row in parallel
+  std::vector<std::vector<std::uint8_t>> row_slots(NY);
+  std::vector<std::vector<std::int64_t>> row_recs(NY);
+  std::vector<std::vector<Deferred>> deferred(NY);
+  std::vector<BuildStats> stats(static_cast<std::size_t>(threads));
+  parallel_rows(g.ny, threads, [&](int t, std::atomic<std::int64_t>& next) {
+    RowWorker w(s, g, spans, tol);
+    for (;;) {
+      const std::int64_t iy = next.fetch_add(1);
+      if (iy >= g.ny) break;
+      w.run_row(iy, row_ids.data() + row_count[iy], row_count[iy + 1] - row_count[iy],
+                out.grid.data() + iy * g.nx, row_slots[iy], row_recs[iy], deferred[iy]);
+    }
+    stats[t] = w.st;
+    stats[t].records_compact = w.es.compact;
+    stats[t].records_wide = w.es.wide;
+  });
+  for (const auto& st : stats) merge_stats(out.stats, st);
+  // phase-1 slots in row-major order
+  std::uint64_t n1 = 0;
+  std::vector<std::uint64_t> base1(NY);
   for (std::size_t r = 0; r < NY; ++r) {
-    slot_base[r] = n_slots;
-    ovf_base[r] = ovf_bytes;
-    n_slots += row_slots[r].size() / kSlotBytes;
-    ovf_bytes += (row_ovf[r].size() + 15) & ~std::uint64_t{15};
+    base1[r] = n1;
+    n1 += row_slots[r].size() / kSlotBytes;
   }
-  if (n_slots >= kRecordBit) throw RuntimeError("index needs more than 2^31 slots");
+  std::vector<std::uint8_t> slots2, ovf2;
+  finish_deferred(s, g, o, deferred, n1, out.grid, slots2, ovf2, out.stats);
+  const std::uint64_t n_slots = n1 + slots2.size() / kSlotBytes;
   out.slots.assign((n_slots ? n_slots : 1) * kSlotBytes, 0);
-  out.overflow.assign(ovf_bytes + 512, 0);  // zero tail: bounded over-reads stay inside
   for (std::size_t r = 0; r < NY; ++r) {
-    const std::uint32_t sb = static_cast<std::uint32_t>(slot_base[r]);
-    std::uint8_t* dst = out.slots.data() + slot_base[r] * kSlotBytes;
-    if (!row_slots[r].empty()) std::memcpy(dst, row_slots[r].data(), row_slots[r].size());
-    if (!row_ovf[r].empty()) {
-      std::memcpy(out.overflow.data() + ovf_base[r], row_ovf[r].data(), row_ovf[r].size());
+    if (!row_slots[r].empty()) {
+      std::memcpy(out.slots.data() + base1[r] * kSlotBytes, row_slots[r].data(), row_slots[r].size());
     }
-    for (const std::int64_t ix : row_recs[r]) out.grid[r * static_cast<std::size_t>(g.nx) + ix] += sb;
-    for (const std::uint64_t pos : row_spatch[r]) {
-      std::uint32_t v;
-      std::memcpy(&v, dst + pos, 4);
-      v += sb;
-      std::memcpy(dst + pos, &v, 4);
-    }
-    for (const std::uint64_t pos : row_opatch[r]) {
-      std::uint64_t v;
-      std::memcpy(&v, dst + pos, 8);
-      v += ovf_base[r];
-      std::memcpy(dst + pos, &v, 8);
-    }
+    const std::uint32_t b = static_cast<std::uint32_t>(base1[r]);
+    for (const std::int64_t ix : row_recs[r]) out.grid[r * static_cast<std::size_t>(g.nx) + static_cast<std::size_t>(ix)] += b;
     std::vector<std::uint8_t>().swap(row_slots[r]);
-    std::vector<std::uint8_t>().swap(row_ovf[r]);
   }
+  if (!slots2.empty()) std::memcpy(out.slots.data() + n1 * kSlotBytes, slots2.data(), slots2.size());
+  out.overflow = std::move(ovf2);
+  out.overflow.resize(out.overflow.size() + 512, 0);  // zero tail
   out.n_slots = n_slots;
-  for (const auto& st : stats) {
-    out.stats.cells_empty += st.cells_empty;
-    out.stats.cells_hit += st.cells_hit;
-    out.stats.cells_boundary += st.cells_boundary;
-    out.stats.record_edges += st.record_edges;
-    out.stats.record_cands += st.record_cands;
-    out.stats.record_breaks += st.record_breaks;
-    out.stats.max_record_edges = std::max(out.stats.max_record_edges, st.max_record_edges);
-    out.stats.max_record_cands = std::max(out.stats.max_record_cands, st.max_record_cands);
-    out.stats.records_compact += st.records_compact;
-    out.stats.records += st.records;
-    out.stats.records_overflow += st.records_overflow;
-    out.stats.cells_split += st.cells_split;
-    out.stats.records_wide += st.records_wide;
-  }
+  out.n_phase1_slots = n1;
   return out;
+}
+
+// For the GPU builder: phase 2 for the cells it deferred.  `cells` are
+// linear cell ids in row-major order with their candidate leaves (CSR,
+// ascending ids).
+void finish_deferred_cells(const Soup& s, const GridGeom& g, const BuildOptions& o,
+                           const std::vector<std::int64_t>& cells,
+                           const std::vector<std::uint64_t>& cand_off,
+                           const std::vector<std::uint32_t>& cand_ids, std::uint64_t slot_base,
+                           std::vector<std::uint32_t>& grid, std::vector<std::uint8_t>& slots_out,
+                           std::vector<std::uint8_t>& ovf_out, BuildStats& stats) {
+  const std::size_t NY = static_cast<std::size_t>(g.ny);
+  std::vector<std::vector<Deferred>> deferred(NY);
+  std::vector<PolySpan> no_spans;
+  const double tol = classify_tol(g);
+  // contributions per deferred cell (cheap: deferred cells are a few percent)
+  {
+    RowWorker w(s, g, no_spans, tol);
+    std::vector<PolyC> list;
+    for (std::size_t k = 0; k < cells.size(); ++k) {
+      const std::int64_t iy = cells[k] / g.nx, ix = cells[k] % g.nx;
+      w.cell_contribs(ix, iy, cand_ids.data() + cand_off[k], cand_off[k + 1] - cand_off[k], list);
+      deferred[static_cast<std::size_t>(iy)].push_back({ix, list});
+    }
+  }
+  finish_deferred(s, g, o, deferred, slot_base, grid, slots_out, ovf_out, stats);
 }
 
 }  // namespace fm
