@@ -510,6 +510,23 @@ __global__ void compact_kernel(const std::uint8_t* kind, std::uint64_t n, int wa
   if (i < n && kind[i] == want) out[pos[i]] = static_cast<long long>(i);
 }
 
+// candidate lists of the deferred cells, packed (cand_off = exclusive scan of their lengths)
+__global__ void gather_cands_kernel(const long long* cells, std::uint64_t n,
+                                    const unsigned long long* off, const std::uint32_t* cand,
+                                    const unsigned long long* cand_off, std::uint32_t* out) {
+  const std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const unsigned long long b = off[cells[k]], e = off[cells[k] + 1];
+  for (unsigned long long q = b; q < e; ++q) out[cand_off[k] + (q - b)] = cand[q];
+}
+
+__global__ void deferred_len_kernel(const long long* cells, std::uint64_t n,
+                                    const unsigned long long* off, unsigned long long* len) {
+  const std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (k < n) len[k] = off[cells[k] + 1] - off[cells[k]];
+  if (k == n) len[k] = 0;
+}
+
 __global__ void scatter_kernel(const long long* cells, const std::uint32_t* vals, std::uint64_t n,
                                std::uint32_t* grid) {
   const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
@@ -675,19 +692,22 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
     compact_kernel<<<grid1d(n_cells), 256>>>(d_kind.as<std::uint8_t>(), n_cells, kCellDefer,
                                              d_pos.as<unsigned long long>(), d_cells.as<long long>());
     ck(cudaMemcpy(cells.data(), d_cells.p, 8 * nd, cudaMemcpyDeviceToHost), "deferred cells");
-    std::vector<unsigned long long> off_h(n_cells + 1);
-    ck(cudaMemcpy(off_h.data(), d_off.p, 8 * (n_cells + 1), cudaMemcpyDeviceToHost), "offsets");
-    for (std::uint64_t k = 0; k < nd; ++k) {
-      cand_off[k + 1] = cand_off[k] + (off_h[cells[k] + 1] - off_h[cells[k]]);
-    }
+    DevBuf d_len, d_coff, d_cids;
+    dalloc<unsigned long long>(d_len, nd + 1, "deferred lens");
+    dalloc<unsigned long long>(d_coff, nd + 1, "deferred cand_off");
+    deferred_len_kernel<<<grid1d(nd + 1), 256>>>(d_cells.as<long long>(), nd,
+                                                 d_off.as<unsigned long long>(),
+                                                 d_len.as<unsigned long long>());
+    exclusive_scan_u64(d_len.as<unsigned long long>(), d_coff.as<unsigned long long>(), nd + 1);
+    ck(cudaMemcpy(cand_off.data(), d_coff.p, 8 * (nd + 1), cudaMemcpyDeviceToHost), "cand_off");
     cand_ids.resize(cand_off[nd]);
-    for (std::uint64_t k = 0; k < nd; ++k) {
-      const std::uint64_t c = static_cast<std::uint64_t>(cells[k]);
-      if (off_h[c + 1] > off_h[c]) {
-        ck(cudaMemcpy(cand_ids.data() + cand_off[k], d_cand.as<std::uint32_t>() + off_h[c],
-                      4 * (off_h[c + 1] - off_h[c]), cudaMemcpyDeviceToHost),
-           "candidates");
-      }
+    dalloc<std::uint32_t>(d_cids, cand_off[nd], "deferred cands");
+    gather_cands_kernel<<<grid1d(nd), 256>>>(d_cells.as<long long>(), nd,
+                                             d_off.as<unsigned long long>(), d_cand.as<std::uint32_t>(),
+                                             d_coff.as<unsigned long long>(), d_cids.as<std::uint32_t>());
+    ck(cudaGetLastError(), "gather_cands_kernel");
+    if (cand_off[nd]) {
+      ck(cudaMemcpy(cand_ids.data(), d_cids.p, 4 * cand_off[nd], cudaMemcpyDeviceToHost), "cands");
     }
   }
   // stats of the GPU phase (cell kinds)

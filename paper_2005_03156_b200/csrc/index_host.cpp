@@ -776,15 +776,26 @@ void finish_deferred_cells(const Soup& s, const GridGeom& g, const BuildOptions&
   std::vector<std::vector<Deferred>> deferred(NY);
   std::vector<PolySpan> no_spans;
   const double tol = classify_tol(g);
-  // contributions per deferred cell (cheap: deferred cells are a few percent)
-  {
+  // contributions per deferred cell, threads over blocks of cells (the
+  // per-row lists stay in row-major, column-ascending order)
+  std::vector<std::vector<PolyC>> lists(cells.size());
+  const int threads = thread_count(o, static_cast<std::int64_t>(cells.size() / 64 + 1));
+  const std::int64_t n_blocks = static_cast<std::int64_t>((cells.size() + 255) / 256);
+  parallel_rows(n_blocks, threads, [&](int, std::atomic<std::int64_t>& next) {
     RowWorker w(s, g, no_spans, tol);
-    std::vector<PolyC> list;
-    for (std::size_t k = 0; k < cells.size(); ++k) {
-      const std::int64_t iy = cells[k] / g.nx, ix = cells[k] % g.nx;
-      w.cell_contribs(ix, iy, cand_ids.data() + cand_off[k], cand_off[k + 1] - cand_off[k], list);
-      deferred[static_cast<std::size_t>(iy)].push_back({ix, list});
+    for (;;) {
+      const std::int64_t b = next.fetch_add(1);
+      if (b >= n_blocks) break;
+      const std::size_t k1 = std::min(cells.size(), static_cast<std::size_t>(b + 1) * 256);
+      for (std::size_t k = static_cast<std::size_t>(b) * 256; k < k1; ++k) {
+        const std::int64_t iy = cells[k] / g.nx, ix = cells[k] % g.nx;
+        w.cell_contribs(ix, iy, cand_ids.data() + cand_off[k], cand_off[k + 1] - cand_off[k], lists[k]);
+      }
     }
+  });
+  for (std::size_t k = 0; k < cells.size(); ++k) {
+    const std::int64_t iy = cells[k] / g.nx, ix = cells[k] % g.nx;
+    deferred[static_cast<std::size_t>(iy)].push_back({ix, std::move(lists[k])});
   }
   finish_deferred(s, g, o, deferred, slot_base, grid, slots_out, ovf_out, stats);
 }
