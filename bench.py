@@ -38,9 +38,13 @@ WORKLOADS = {
           "100M clustered fp64 points (2000 Zipf(1.1) centres, sigma 0.2 deg, 10% uniform)",
     "c4": "c4: 100,000-polygon 400x250 jittered tiling (50 segs/edge, sigma 0.15, ~200 v), "
           "200M fp64 points (50% uniform, 50% within 1e-4 cell of an edge)",
+    "c3": "c3: 12.5M-leaf nested tiling (10x5 states, 20x20 counties, 25x25 blocks, 6 segs/edge), "
+          "1B clustered fp64 points (20,000 Zipf(1.1) centres, 10% uniform)",
+    "c5": "c5: the c3 index with 8B clustered points sharded over the GPUs + int64 per-block "
+          "histogram all-reduced with NCCL",
 }
 # reference cover depth for the CPU arm (SURVEY.md sec. 6 probes: best per config)
-REF_MAX_LEVEL = {"c1": 12, "c2": 16, "c4": 16}
+REF_MAX_LEVEL = {"c1": 12, "c2": 16, "c4": 16, "c3": 18, "c5": 18}
 
 
 def parse():

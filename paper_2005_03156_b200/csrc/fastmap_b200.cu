@@ -148,13 +148,11 @@ __global__ void __launch_bounds__(kAWarps * 32)
       const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
       if (valid && !is_rec) emit<kHist>(out, hist, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
       const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec);
-      if (is_rec) {
-        QItem it;
-        it.px = p[u].x;
-        it.py = p[u].y;
-        it.i = static_cast<std::uint32_t>(i);
-        it.e = e[u];
-        my[cnt + __popc(b & lt_mask)] = it;
+      if (is_rec) {  // streaming stores: the resolve pass reads these much later
+        double* d = reinterpret_cast<double*>(my + cnt + __popc(b & lt_mask));
+        __stcs(d, p[u].x);
+        __stcs(d + 1, p[u].y);
+        __stcs(reinterpret_cast<uint2*>(d + 2), make_uint2(static_cast<std::uint32_t>(i), e[u]));
       }
       cnt += __popc(b);
     }
