@@ -21,8 +21,21 @@ def functions(sass):
     return {p.split("\n", 1)[0].strip(): p for p in parts[1:]}
 
 
-def test_no_dfma_anywhere(sass):
-    assert "DFMA" not in sass
+def test_no_dfma_on_the_query_path(sass):
+    """The query kernels evaluate the reference predicate: no DFMA at all.
+    (The GPU index builder's contrib_kernel contains DFMA only inside the
+    IEEE-correctly-rounded fp64 division sequence (div.rn.f64); its results
+    are checked byte-for-byte against the host builder in
+    tests/test_gpu_build.py.)"""
+    fns = functions(sass)
+    query = {n: b for n, b in fns.items() if "stream_kernel" in n or "resolve_kernel" in n
+             or "resolve_slot_global" in n or "resolve_wide" in n or "resolve_compact" in n}
+    assert query, "query kernels not found"
+    for n, b in query.items():
+        assert "DFMA" not in b, n
+    for n, b in fns.items():
+        if "DFMA" in b:
+            assert "index_gpu" in n and "contrib_kernel" in n, f"unexpected DFMA in {n}"
 
 
 def test_kernels_present_and_use_fp64_and_async_copy(sass):
