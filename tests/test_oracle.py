@@ -115,7 +115,7 @@ def test_live_reference_pip_random_and_on_edge():
 def test_live_reference_exhaustive_on_c4_sample():
     cfg = synth.config("c4")
     soup = cfg.make_soup()
-    pts = cfg.make_points(400, soup=soup, offset=7)
+    pts = cfg.make_points(120, soup=soup, offset=7)
     m = oracle.RefModel(soup)
     assert np.array_equal(m.exhaustive_assign(pts), oracle.assign(soup, pts))
 
