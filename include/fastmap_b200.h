@@ -88,7 +88,17 @@ typedef struct fm_build_params {
   int build_on_gpu;
   /* Host build threads (0 = hardware concurrency). */
   int threads;
+  /* > 0: also build the fast-approx cover (CoverMode::approx with this
+   * epsilon, cell_index.hpp:248-252, :313-316): the grid is refined until
+   * every cell's (margin-expanded) diagonal is <= epsilon and each boundary
+   * cell gets a deemed leaf.  0 = exact-only index.  Values in
+   * (0, level-30 cell diagonal) are rejected like validate_cover_params
+   * (cell_index.hpp:382-394). */
+  double approx_epsilon;
 } fm_build_params;
+
+/* CoverMode (cell_index.hpp:246). */
+typedef enum fm_mode { FM_MODE_EXACT = 0, FM_MODE_APPROX = 1 } fm_mode;
 
 typedef struct fm_index_stats {
   uint64_t n_polys, n_rings, n_vertices, n_edges;
@@ -104,6 +114,8 @@ typedef struct fm_index_stats {
   uint64_t cells_split;   /* 2x2 split nodes */
   uint64_t slots_phase1;  /* slots of cells that fit one slot */
   uint64_t slots_total;
+  double approx_epsilon;      /* 0 for an exact-only index */
+  uint64_t approx_grid_bytes; /* deemed-leaf grid of the approx cover */
 } fm_index_stats;
 
 /* Optional per-call work counters (diagnostics; device-side atomics). */
@@ -149,6 +161,21 @@ fm_status fm_query(const fm_index* index, const double* d_lonlat, uint64_t n,
  * buffers give full PCIe overlap; pageable ones work but copy slower. */
 fm_status fm_query_host(const fm_index* index, const double* h_lonlat, uint64_t n,
                         int32_t* h_out, int64_t* h_hist);
+
+/* query_leaves(trie, leaves, points, mode) (cell_index.hpp:527-590) with an
+ * explicit CoverMode.  FM_MODE_EXACT is fm_query.  FM_MODE_APPROX answers
+ * boundary cells with their deemed leaf -- no crossing tests at all
+ * (cell_index.hpp:558-560); it needs an index built with approx_epsilon > 0
+ * (else FM_ERR_INVALID_ARGUMENT, cell_index.hpp:532-535).  A point whose
+ * approx answer differs from the exact one lies within epsilon of the
+ * answered leaf, and the answer is never -1 there. */
+fm_status fm_query_mode(const fm_index* index, int mode, const double* d_lonlat, uint64_t n,
+                        int32_t* d_out, int64_t* d_hist, fm_query_counters* d_counters,
+                        void* stream);
+
+/* fm_query_host with an explicit CoverMode. */
+fm_status fm_query_host_mode(const fm_index* index, int mode, const double* h_lonlat,
+                             uint64_t n, int32_t* h_out, int64_t* h_hist);
 
 /* Copy of the index arrays to host memory (the FMCI-save analogue,
  * cell_index.hpp:641-664).  Two-call protocol: null buffers -> sizes.

@@ -18,7 +18,8 @@
 //
 // with the same AssignmentResult (state / county / block per point, -1 when
 // unassigned) and the same exception types:
-//   std::invalid_argument  bad parameters, fanout, approx on exact, leaf-table
+//   std::invalid_argument  bad parameters, fanout, approx query on an exact-only
+//                          index, leaf-table
 //                          mismatch, rings with < 3 vertices
 //   std::runtime_error     reference limits, CUDA failures, no CUDA device
 //                          (there is no CPU fallback)
@@ -118,6 +119,7 @@ inline CellIndex build_index(std::span<const LeafRegion> leaves,
   bp.device = ip.device;
   bp.build_on_gpu = ip.device >= 0 ? 1 : 0;
   bp.threads = ip.threads;
+  bp.approx_epsilon = params.mode == CoverMode::approx ? params.epsilon : 0.0;
   fm_index* h = nullptr;
   detail::check(fm_index_build(vxy.data(), ring_off.data(), ring_off.size() - 1,
                                poly_ring.data(), poly_ring.size() - 1, &bp, &h),
@@ -132,10 +134,13 @@ inline CellIndex build_index(const RegionHierarchy& h, const CoverParams& params
 }
 
 /// Leaf id per point (collect_leaves position, -1 = none), host buffers.
-inline std::vector<std::int32_t> project(const CellIndex& index, std::span<const Point> points) {
+inline std::vector<std::int32_t> project(const CellIndex& index, std::span<const Point> points,
+                                         CoverMode mode = CoverMode::exact) {
   std::vector<std::int32_t> out(points.size());
-  detail::check(fm_query_host(index.get(), reinterpret_cast<const double*>(points.data()),
-                              points.size(), out.data(), nullptr),
+  detail::check(fm_query_host_mode(index.get(),
+                                   mode == CoverMode::approx ? FM_MODE_APPROX : FM_MODE_EXACT,
+                                   reinterpret_cast<const double*>(points.data()), points.size(),
+                                   out.data(), nullptr),
                 "fm_query_host");
   return out;
 }
@@ -153,13 +158,13 @@ inline void project_device(const CellIndex& index, const Point* d_points, std::s
 /// set exactly as set_leaf does (cell_index.hpp:515-519).
 inline AssignmentResult query_leaves(const CellIndex& index, std::span<const LeafRegion> leaves,
                                      std::span<const Point> points, CoverMode mode) {
-  if (mode == CoverMode::approx) {
+  if (mode == CoverMode::approx && index.stats().approx_epsilon <= 0.0) {  // :532-535
     throw std::invalid_argument("approximate queries require an approximate-mode cover");
   }
   if (index.n_leaves() != leaves.size()) {
     throw std::invalid_argument("cover was built for a different hierarchy");
   }
-  const auto ids = project(index, points);
+  const auto ids = project(index, points, mode);
   AssignmentResult res;
   res.state.assign(points.size(), -1);
   res.county.assign(points.size(), -1);

@@ -53,6 +53,8 @@ def lib():
         L.orc_assign.argtypes = [PD, PU64, PU64, u64, PD, u64, C.c_int, C.c_int, PI32]
         L.orc_count_containing.restype = None
         L.orc_count_containing.argtypes = [PD, PU64, PU64, u64, PD, u64, PI32]
+        L.orc_point_polygon_distance.argtypes = [C.c_double, C.c_double, PD, PU64, PU64, u64]
+        L.orc_point_polygon_distance.restype = C.c_double
         _orc = L
     return _orc
 
@@ -140,6 +142,13 @@ def count_containing(soup, pts) -> np.ndarray:
                                soup.n_polys, _p(pts, C.c_double), pts.shape[0],
                                _p(out, C.c_int32))
     return out
+
+
+def point_polygon_distance(soup, poly: int, px: float, py: float) -> float:
+    """tests/oracles.hpp:92-95: 0 inside, else the nearest-edge distance."""
+    vxy, ro, pr = _soup_arrays(soup)
+    return float(lib().orc_point_polygon_distance(px, py, _p(vxy, C.c_double), _p(ro, C.c_uint64),
+                                                  _p(pr, C.c_uint64), poly))
 
 
 # -- the reference itself ------------------------------------------------------

@@ -289,3 +289,34 @@ void orc_count_containing(const double* vxy, const uint64_t* ring_off,
   }
   grid_free(g);
 }
+
+/* tests/oracles.hpp:68-80: distance from p to segment ab (clamped projection). */
+static double seg_distance(double px, double py, double ax, double ay, double bx, double by) {
+  const double dx = bx - ax, dy = by - ay;
+  const double len2 = dx * dx + dy * dy;
+  double t = 0.0;
+  if (len2 > 0.0) {
+    t = ((px - ax) * dx + (py - ay) * dy) / len2;
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  }
+  const double ex = px - (ax + t * dx), ey = py - (ay + t * dy);
+  return sqrt(ex * ex + ey * ey);
+}
+
+/* tests/oracles.hpp:92-95: distance to the polygon as a region -- zero
+ * inside (parity rule), else the smallest edge distance over all rings. */
+double orc_point_polygon_distance(double px, double py, const double* vxy,
+                                  const uint64_t* ring_off, const uint64_t* poly_ring,
+                                  uint64_t poly) {
+  if (orc_point_in_polygon(px, py, vxy, ring_off, poly_ring, poly)) return 0.0;
+  double best = INFINITY;
+  for (uint64_t r = poly_ring[poly]; r < poly_ring[poly + 1]; ++r) {
+    const uint64_t b = ring_off[r], n = ring_off[r + 1] - b;
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t a = b + i, c = (i + 1 < n) ? a + 1 : b;
+      const double d = seg_distance(px, py, vxy[2 * a], vxy[2 * a + 1], vxy[2 * c], vxy[2 * c + 1]);
+      if (d < best) best = d;
+    }
+  }
+  return best;
+}

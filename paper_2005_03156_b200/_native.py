@@ -45,6 +45,7 @@ class BuildParams(C.Structure):
         ("device", C.c_int),
         ("build_on_gpu", C.c_int),
         ("threads", C.c_int),
+        ("approx_epsilon", C.c_double),
     ]
 
 
@@ -61,6 +62,7 @@ class IndexStats(C.Structure):
         ("build_seconds", C.c_double),
         ("built_on_gpu", C.c_int32), ("reserved0", C.c_int32),
         ("cells_split", u64), ("slots_phase1", u64), ("slots_total", u64),
+        ("approx_epsilon", C.c_double), ("approx_grid_bytes", u64),
     ]
 
     def as_dict(self) -> dict:
@@ -76,8 +78,10 @@ class QueryCounters(C.Structure):
 EXPORTS = (
     "fm_status_string", "fm_last_error", "fm_version", "fm_index_build",
     "fm_index_destroy", "fm_index_stats_get", "fm_query", "fm_query_host",
-    "fm_index_export", "fm_index_device",
+    "fm_index_export", "fm_index_device", "fm_query_mode", "fm_query_host_mode",
 )
+
+MODE_EXACT, MODE_APPROX = 0, 1  # fm_mode (CoverMode, cell_index.hpp:246)
 
 _lib = None
 _synth = None
@@ -114,6 +118,12 @@ def lib() -> C.CDLL:
                                C.c_void_p, C.c_void_p]
         L.fm_query_host.restype = C.c_int
         L.fm_query_host.argtypes = [C.c_void_p, PD, u64, PI32, PI64]
+        L.fm_query_host.restype = C.c_int
+        L.fm_query_mode.argtypes = [C.c_void_p, C.c_int, C.c_void_p, u64, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p]
+        L.fm_query_mode.restype = C.c_int
+        L.fm_query_host_mode.argtypes = [C.c_void_p, C.c_int, PD, u64, PI32, PI64]
+        L.fm_query_host_mode.restype = C.c_int
         L.fm_index_export.restype = C.c_int
         L.fm_index_export.argtypes = [C.c_void_p, PU32, PU64, PU8, PU64, PD]
         L.fm_index_device.restype = C.c_int

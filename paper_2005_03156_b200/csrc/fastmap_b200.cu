@@ -332,6 +332,92 @@ __global__ void __launch_bounds__(kBWarps * 32, FM_BMINB)
 
 constexpr int kSmemB = static_cast<int>(sizeof(WarpSmemB)) * kBWarps;
 
+// ---------------------------------------------------------------------------
+// Fast-approx mode (CoverMode::approx, cell_index.hpp:558-560).  The approx
+// cover is a second u32 grid over the same cells: hits and empties as in the
+// exact grid, boundary cells replaced by their deemed leaf.  A query is one
+// 16-byte point read, one 4-byte gather and one 4-byte write -- no queue, no
+// crossing tests.
+constexpr int kXThreads = 256;
+constexpr int kXU = 4;
+
+template <bool kHist, bool kCount>
+__global__ void __launch_bounds__(kXThreads)
+    approx_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
+                  int* __restrict__ out, unsigned long long* __restrict__ hist,
+                  unsigned long long* __restrict__ counters) {
+  const std::uint64_t chunk = static_cast<std::uint64_t>(kXThreads) * kXU;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * chunk;
+  unsigned long long done = 0;
+  for (std::uint64_t b = blockIdx.x * chunk + threadIdx.x; b < n + threadIdx.x; b += stride) {
+    double2 p[kXU];
+#pragma unroll
+    for (int u = 0; u < kXU; ++u) {
+      const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kXThreads;
+      p[u] = i < n ? __ldcs(pts + i) : make_double2(NAN, NAN);
+    }
+#pragma unroll
+    for (int u = 0; u < kXU; ++u) {
+      const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kXThreads;
+      if (i < n) {
+        emit<kHist>(out, hist, i, static_cast<int>(fm::locate(P, p[u].x, p[u].y)));
+        if (kCount) ++done;
+      }
+    }
+  }
+  if (kCount) {
+    for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(0xFFFFFFFFu, done, o);
+    if ((threadIdx.x & 31) == 0 && done) atomicAdd(counters + 0, done);
+  }
+}
+
+// Boundary cells of the exact grid -> (centre point, cell) lists.
+__global__ void __launch_bounds__(256)
+    deem_collect_kernel(const std::uint32_t* __restrict__ grid, std::uint64_t ncell,
+                        std::uint64_t nx, double gx0, double gy0, double w, double h,
+                        double2* __restrict__ centres, std::uint64_t* __restrict__ cells,
+                        unsigned long long* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t b0 = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
+       b0 < ncell; b0 += stride) {
+    const std::uint64_t c = b0 + lane;
+    bool rec = false;
+    if (c < ncell) {
+      const std::uint32_t e = grid[c];
+      rec = e != fm::kEmpty && (e & fm::kRecordBit);
+    }
+    const std::uint32_t m = __ballot_sync(0xFFFFFFFFu, rec);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(count, static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (rec) {
+      const std::uint64_t k = base + __popc(m & ((1u << lane) - 1u));
+      const std::uint64_t iy = c / nx, ix = c - iy * nx;
+      centres[k] = make_double2(gx0 + (static_cast<double>(ix) + 0.5) * w,
+                                gy0 + (static_cast<double>(iy) + 0.5) * h);
+      cells[k] = c;
+    }
+  }
+}
+
+// Deemed leaf: the exact answer at the cell centre when it has one (every
+// point of the cell is then within half the diagonal of it), else the
+// smallest candidate the cell's records list (min_leaf_of_entry).
+__global__ void __launch_bounds__(256)
+    deem_finish_kernel(fm::KParams P, const std::uint64_t* __restrict__ cells,
+                       const int* __restrict__ centre_id, std::uint64_t nb,
+                       std::uint32_t* __restrict__ agrid) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t k = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < nb;
+       k += stride) {
+    const std::uint64_t c = cells[k];
+    const int id = centre_id[k];
+    agrid[c] = id >= 0 ? static_cast<std::uint32_t>(id) : fm::min_leaf_of_entry(P, P.grid[c]);
+  }
+}
+
 int resident_blocks(int device, const void* kernel, int block, int smem) {
   // SM count x resident CTAs per SM, cached per (device, kernel)
   struct Slot {
@@ -361,6 +447,7 @@ struct fm_index {
   fm::GridGeom g{};
   double ax0 = 0, ax1 = 0, ay0 = 0, ay1 = 0;
   std::uint32_t* d_grid = nullptr;
+  std::uint32_t* d_agrid = nullptr;    // fast-approx grid (deemed leaves), or null
   std::uint8_t* d_slots = nullptr;     // boundary slots (128 B each)
   std::uint8_t* d_overflow = nullptr;  // overflow records
   std::uint64_t grid_len = 0, slots_len = 0, overflow_len = 0;
@@ -435,10 +522,33 @@ fm_status launch_t(const fm_index* ix, const double2* pts, std::uint64_t n, int*
   return FM_OK;
 }
 
+template <bool kHist, bool kCount>
+fm_status launch_approx_t(const fm_index* ix, const double2* pts, std::uint64_t n, int* d_out,
+                          unsigned long long* d_hist, unsigned long long* d_counters,
+                          cudaStream_t stream) {
+  fm::KParams P = kparams(ix);
+  P.grid = ix->d_agrid;
+  auto k = approx_kernel<kHist, kCount>;
+  const std::uint64_t chunk = static_cast<std::uint64_t>(kXThreads) * kXU;
+  const int grid = static_cast<int>(std::max<std::uint64_t>(
+      1, std::min<std::uint64_t>((n + chunk - 1) / chunk,
+                                 resident_blocks(ix->device, (const void*)k, kXThreads, 0))));
+  k<<<grid, kXThreads, 0, stream>>>(P, pts, n, d_out, d_hist, d_counters);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));
+  return FM_OK;
+}
+
 fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* d_out,
                  unsigned long long* d_hist, unsigned long long* d_counters,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, int mode = FM_MODE_EXACT) {
   const double2* pts = reinterpret_cast<const double2*>(d_pts);
+  if (mode == FM_MODE_APPROX) {
+    if (d_hist && d_counters) return launch_approx_t<true, true>(ix, pts, n, d_out, d_hist, d_counters, stream);
+    if (d_hist) return launch_approx_t<true, false>(ix, pts, n, d_out, d_hist, d_counters, stream);
+    if (d_counters) return launch_approx_t<false, true>(ix, pts, n, d_out, d_hist, d_counters, stream);
+    return launch_approx_t<false, false>(ix, pts, n, d_out, d_hist, d_counters, stream);
+  }
   // slices of 2^28 points bound the queue scratch (24 B/point) to 6.4 GB
   const std::uint64_t slice = std::uint64_t{1} << 28;
   for (std::uint64_t off = 0; off < n; off += slice) {
@@ -455,6 +565,47 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
     }
     if (st != FM_OK) return st;
   }
+  return FM_OK;
+}
+
+// The approx cover: copy the exact grid, query every boundary cell's centre
+// through the exact path, then write the deemed leaves.
+fm_status build_approx(fm_index* ix) {
+  const std::uint64_t ncell = ix->grid_len;
+  const std::uint64_t nb = ix->stats.cells_boundary;
+  FM_CUDA(cudaMalloc(&ix->d_agrid, ncell * 4));
+  FM_CUDA(cudaMemcpy(ix->d_agrid, ix->d_grid, ncell * 4, cudaMemcpyDeviceToDevice));
+  if (nb == 0) return FM_OK;
+  void* scratch = nullptr;
+  const std::uint64_t bytes = nb * (16 + 8 + 4) + 64;
+  FM_CUDA(cudaMalloc(&scratch, bytes));
+  double2* centres = static_cast<double2*>(scratch);
+  std::uint64_t* cells = reinterpret_cast<std::uint64_t*>(centres + nb);
+  int* ids = reinterpret_cast<int*>(cells + nb);
+  unsigned long long* count = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<std::uintptr_t>(ids + nb) + 7) & ~std::uintptr_t{7});
+  fm_status st = FM_OK;
+  cudaError_t e = cudaMemset(count, 0, 8);
+  if (e == cudaSuccess) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    const int blocks = std::max(1, sms) * 8;
+    deem_collect_kernel<<<blocks, 256>>>(ix->d_grid, ncell, static_cast<std::uint64_t>(ix->g.nx),
+                                         ix->g.gx0, ix->g.gy0, ix->g.w, ix->g.h, centres, cells,
+                                         count);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      st = launch(ix, reinterpret_cast<const double*>(centres), nb, ids, nullptr, nullptr, 0);
+      if (st == FM_OK) {
+        deem_finish_kernel<<<blocks, 256>>>(kparams(ix), cells, ids, nb, ix->d_agrid);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      }
+    }
+  }
+  cudaFree(scratch);
+  if (st != FM_OK) return st;
+  if (e != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("approx cover: ") + cudaGetErrorString(e));
   return FM_OK;
 }
 
@@ -482,6 +633,7 @@ void free_device(fm_index* ix) {
   }
   if (ix->d_hist) cudaFree(ix->d_hist);
   if (ix->d_grid) cudaFree(ix->d_grid);
+  if (ix->d_agrid) cudaFree(ix->d_agrid);
   if (ix->d_slots) cudaFree(ix->d_slots);
   if (ix->d_overflow) cudaFree(ix->d_overflow);
 }
@@ -532,6 +684,15 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   opt.ny = p.ny;
   opt.margin = p.margin;
   opt.threads = p.threads;
+  // validate_cover_params (cell_index.hpp:382-394): the level-30 diagonal floor
+  const double eps_floor = std::hypot(360.0 / 1073741824.0, 180.0 / 1073741824.0);
+  if (std::isnan(p.approx_epsilon) || p.approx_epsilon < 0.0 ||
+      (p.approx_epsilon > 0.0 && p.approx_epsilon < eps_floor)) {
+    return set_err(FM_ERR_INVALID_ARGUMENT,
+                   "approx epsilon must be at least the level-30 cell diagonal (" +
+                       std::to_string(eps_floor) + " degrees)");
+  }
+  opt.approx_epsilon = p.approx_epsilon;
 
   fm_index* ix = new (std::nothrow) fm_index();
   if (!ix) return set_err(FM_ERR_OOM, "host allocation failed");
@@ -636,6 +797,17 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
+  s.approx_epsilon = p.approx_epsilon;
+  if (ix->device >= 0 && p.approx_epsilon > 0.0) {
+    DeviceGuard guard(ix->device);
+    const fm_status st = build_approx(ix);
+    if (st != FM_OK) {
+      free_device(ix);
+      delete ix;
+      return st;
+    }
+    s.approx_grid_bytes = ix->grid_len * 4;
+  }
   s.build_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out_index = ix;
@@ -656,11 +828,39 @@ fm_status fm_index_stats_get(const fm_index* index, fm_index_stats* out) {
 
 int fm_index_device(const fm_index* index) { return index ? index->device : -1; }
 
+}  // extern "C"
+
+namespace {
+fm_status check_mode(const fm_index* index, int mode) {
+  if (mode != FM_MODE_EXACT && mode != FM_MODE_APPROX) {
+    return set_err(FM_ERR_INVALID_ARGUMENT, "unknown cover mode");
+  }
+  if (mode == FM_MODE_APPROX && index->stats.approx_epsilon <= 0.0) {  // cell_index.hpp:532-535
+    return set_err(FM_ERR_INVALID_ARGUMENT, "approximate queries require an approximate-mode cover");
+  }
+  return FM_OK;
+}
+}  // namespace
+
+extern "C" {
+
 fm_status fm_query(const fm_index* index, const double* d_lonlat, std::uint64_t n,
                    std::int32_t* d_out, std::int64_t* d_hist, fm_query_counters* d_counters,
                    void* stream) {
+  return fm_query_mode(index, FM_MODE_EXACT, d_lonlat, n, d_out, d_hist, d_counters, stream);
+}
+
+fm_status fm_query_host(const fm_index* index, const double* h_lonlat, std::uint64_t n,
+                        std::int32_t* h_out, std::int64_t* h_hist) {
+  return fm_query_host_mode(index, FM_MODE_EXACT, h_lonlat, n, h_out, h_hist);
+}
+
+fm_status fm_query_mode(const fm_index* index, int mode, const double* d_lonlat, std::uint64_t n,
+                        std::int32_t* d_out, std::int64_t* d_hist, fm_query_counters* d_counters,
+                        void* stream) {
   g_err.clear();
   if (!index) return set_err(FM_ERR_INVALID_ARGUMENT, "index is null");
+  if (check_mode(index, mode) != FM_OK) return FM_ERR_INVALID_ARGUMENT;
   if (index->device < 0) {
     return set_err(FM_ERR_NO_DEVICE, "index was built host-only (device < 0); no CPU query path exists");
   }
@@ -671,13 +871,14 @@ fm_status fm_query(const fm_index* index, const double* d_lonlat, std::uint64_t 
   return launch(index, d_lonlat, n, reinterpret_cast<int*>(d_out),
                 reinterpret_cast<unsigned long long*>(d_hist),
                 reinterpret_cast<unsigned long long*>(d_counters),
-                static_cast<cudaStream_t>(stream));
+                static_cast<cudaStream_t>(stream), mode);
 }
 
-fm_status fm_query_host(const fm_index* cindex, const double* h_lonlat, std::uint64_t n,
-                        std::int32_t* h_out, std::int64_t* h_hist) {
+fm_status fm_query_host_mode(const fm_index* cindex, int mode, const double* h_lonlat,
+                             std::uint64_t n, std::int32_t* h_out, std::int64_t* h_hist) {
   g_err.clear();
   if (!cindex) return set_err(FM_ERR_INVALID_ARGUMENT, "index is null");
+  if (check_mode(cindex, mode) != FM_OK) return FM_ERR_INVALID_ARGUMENT;
   fm_index* index = const_cast<fm_index*>(cindex);  // staging buffers are mutable state
   if (index->device < 0) {
     return set_err(FM_ERR_NO_DEVICE, "index was built host-only (device < 0); no CPU query path exists");
@@ -709,7 +910,8 @@ fm_status fm_query_host(const fm_index* cindex, const double* h_lonlat, std::uin
     const std::uint64_t m = std::min(kChunkPoints, n - off);
     FM_CUDA(cudaMemcpyAsync(index->d_in[s], h_lonlat + 2 * off, m * 16, cudaMemcpyHostToDevice,
                             index->streams[s]));
-    const fm_status st = launch(index, index->d_in[s], m, index->d_out[s], dh, nullptr, index->streams[s]);
+    const fm_status st = launch(index, index->d_in[s], m, index->d_out[s], dh, nullptr,
+                                index->streams[s], mode);
     if (st != FM_OK) return st;
     FM_CUDA(cudaMemcpyAsync(h_out + off, index->d_out[s], m * 4, cudaMemcpyDeviceToHost,
                             index->streams[s]));

@@ -23,6 +23,7 @@ struct BuildOptions {
   std::int64_t nx = 0, ny = 0;
   double margin = 0.0;
   int threads = 0;
+  double approx_epsilon = 0.0;  // > 0: cell diagonal bound of a fast-approx cover
 };
 
 struct BuildStats {

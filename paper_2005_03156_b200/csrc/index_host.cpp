@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -537,6 +538,20 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
       ny = (ny + 1) / 2;
     }
   }
+  if (o.approx_epsilon > 0.0) {
+    // fast-approx covers (cell_index.hpp:313-316): every boundary cell's
+    // margin-expanded diagonal must be <= epsilon, so raise the resolution
+    const double side = o.approx_epsilon / std::sqrt(2.0) * (1.0 - 1e-9) - 2.0 * g.margin;
+    if (!(side > 0.0)) throw InvalidArgument("approx epsilon is below the classification margin");
+    const double ex = std::ceil(GW / side), ey = std::ceil(GH / side);
+    if (ex * ey > static_cast<double>(std::int64_t{1} << 31)) {
+      throw InvalidArgument("approx epsilon " + std::to_string(o.approx_epsilon) + " needs " +
+                            std::to_string(ex * ey) +
+                            " uniform-grid cells over this extent (limit 2^31)");
+    }
+    nx = std::max(nx, static_cast<std::int64_t>(ex));
+    ny = std::max(ny, static_cast<std::int64_t>(ey));
+  }
   if (nx * ny > (std::int64_t{1} << 31)) throw InvalidArgument("grid too large");
   g.nx = nx;
   g.ny = ny;
@@ -544,6 +559,10 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
   g.h = GH / static_cast<double>(ny);
   g.inv_w = static_cast<double>(nx) / GW;
   g.inv_h = static_cast<double>(ny) / GH;
+  if (o.approx_epsilon > 0.0 &&
+      !(std::hypot(g.w + 2.0 * g.margin, g.h + 2.0 * g.margin) <= o.approx_epsilon)) {
+    throw InvalidArgument("grid cells exceed the approx epsilon");
+  }
   return g;
 }
 

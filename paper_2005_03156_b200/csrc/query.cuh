@@ -227,4 +227,43 @@ __device__ __noinline__ int resolve_slot_global(const KParams& P, std::uint32_t 
   return -1;  // unreachable for a well-formed index
 }
 
+// Smallest leaf id that a boundary entry's records list (its first
+// candidate; split cells: the minimum over the subtree), kEmpty if none.
+// Every listed candidate has boundary, breakpoints or a terminal inside the
+// margin-expanded cell, so any point of the cell lies within the expanded
+// cell diagonal of it -- the fast-approx fallback.
+__device__ __noinline__ std::uint32_t min_leaf_of_entry(const KParams& P, std::uint32_t e) {
+  std::uint32_t best = kEmpty, stack[4 * (kMaxSplitDepth + 2)];
+  int sp = 0;
+  stack[sp++] = e;
+  while (sp > 0) {
+    const std::uint32_t x = stack[--sp];
+    if (x == kEmpty) continue;
+    if (x < kRecordBit) {
+      best = min(best, x);
+      continue;
+    }
+    const std::uint8_t* s = slot_ptr(P, x);
+    const std::uint32_t h = __ldg(reinterpret_cast<const std::uint32_t*>(s));
+    const std::uint32_t kind = h & 0xFFu;
+    if (kind == kSlotLeaf) {
+      if ((h >> 16) & 0xFFu) best = min(best, __ldg(reinterpret_cast<const std::uint32_t*>(s + 8)));
+    } else if (kind == kSlotSplit) {
+      for (int k = 0; k < 4 && sp < static_cast<int>(sizeof(stack) / 4); ++k) {
+        stack[sp++] = __ldg(reinterpret_cast<const std::uint32_t*>(s + 40) + k);
+      }
+    } else {  // overflow record
+      const std::uint64_t off = __ldg(reinterpret_cast<const unsigned long long*>(s + 8));
+      const std::uint8_t* rec = P.overflow + off;
+      const uint2 rh = __ldg(reinterpret_cast<const uint2*>(rec));
+      if ((rh.x & 0xFFu) == kKindCompact) {
+        if ((rh.x >> 16) & 0xFFu) best = min(best, __ldg(reinterpret_cast<const std::uint32_t*>(rec + 8)));
+      } else if (rh.y >> 16) {  // wide: n_edges = rh.y & 0xFFFF, n_cands = rh.y >> 16
+        best = min(best, __ldg(reinterpret_cast<const std::uint32_t*>(rec + wide_cands_offset(rh.y & 0xFFFFu))));
+      }
+    }
+  }
+  return best;
+}
+
 }  // namespace fm

@@ -245,8 +245,12 @@ class CellIndex:
         return grid, arena, g
 
     # -- projection ---------------------------------------------------------
-    def project(self, points, out=None, hist=None, counters=None, stream=None):
+    def project(self, points, out=None, hist=None, counters=None, stream=None,
+                mode: "CoverMode" = None):
         """Leaf id per point.
+
+        ``mode``: CoverMode.exact (default) or CoverMode.approx (an index built
+        with an approx-mode CoverParams; deemed leaves for boundary cells).
 
         ``points``: a CUDA ``torch.Tensor`` (n, 2) float64 on the index's device
         (asynchronous, on ``stream`` or the current torch stream), or a numpy
@@ -254,6 +258,7 @@ class CellIndex:
         ``hist``: optional int64 per-leaf counters, accumulated into.
         """
         L = N.lib()
+        m = int(CoverMode.exact if mode is None else mode)
         if isinstance(points, np.ndarray):
             pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
             n = pts.shape[0]
@@ -263,8 +268,8 @@ class CellIndex:
             if hist is not None:
                 assert hist.dtype == np.int64 and hist.flags.c_contiguous
                 hp = N.ptr(hist, C.c_int64)
-            N.check(L.fm_query_host(self.handle, N.ptr(pts, C.c_double), n,
-                                    N.ptr(out, C.c_int32), hp), "fm_query_host")
+            N.check(L.fm_query_host_mode(self.handle, m, N.ptr(pts, C.c_double), n,
+                                         N.ptr(out, C.c_int32), hp), "fm_query_host")
             return out
         import torch  # device path
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
@@ -278,7 +283,7 @@ class CellIndex:
             stream = torch.cuda.current_stream(points.device).cuda_stream
         elif hasattr(stream, "cuda_stream"):
             stream = stream.cuda_stream
-        N.check(L.fm_query(self.handle, C.c_void_p(points.data_ptr()), n,
+        N.check(L.fm_query_mode(self.handle, m, C.c_void_p(points.data_ptr()), n,
                            C.c_void_p(out.data_ptr()),
                            C.c_void_p(hist.data_ptr()) if hist is not None else None,
                            C.c_void_p(counters.data_ptr()) if counters is not None else None,
@@ -295,7 +300,9 @@ def build_index(soup: Soup, params: Optional[CoverParams] = None, device: int = 
     bp = N.BuildParams(cells_per_polygon=float(params.cells_per_polygon),
                        nx=int(params.nx), ny=int(params.ny), margin=float(params.margin),
                        device=int(device), build_on_gpu=1 if device >= 0 else 0,
-                       threads=int(params.threads))
+                       threads=int(params.threads),
+                       approx_epsilon=float(params.epsilon) if params.mode == CoverMode.approx
+                       else 0.0)
     h = C.c_void_p()
     st = N.lib().fm_index_build(N.ptr(s.vxy, C.c_double), N.ptr(s.ring_off, C.c_uint64),
                                 s.n_rings, N.ptr(s.poly_ring, C.c_uint64), s.n_polys,
@@ -344,12 +351,10 @@ def query_leaves(trie, leaves, points, mode: CoverMode = CoverMode.exact) -> Ass
     cover = trie.cover if isinstance(trie, TrieIndex) else trie
     if mode == CoverMode.approx and cover.params.mode != CoverMode.approx:
         raise ValueError("approximate queries require an approximate-mode cover")
-    if mode == CoverMode.approx:
-        raise NotImplementedError("fast-approx mode is not built yet (SURVEY.md sec. 8f item 1)")
     n_leaves = leaves.n_polys if isinstance(leaves, Soup) else len(leaves)
     if cover.n_leaves != n_leaves:
         raise ValueError("cover was built for a different hierarchy")
-    ids = cover.project(points)
+    ids = cover.project(points, mode=mode)
     if not isinstance(ids, np.ndarray):
         ids = ids.cpu().numpy()
     st, co, bl = _leaf_table(leaves)

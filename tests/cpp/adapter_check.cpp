@@ -4,6 +4,8 @@
 //            ("no CUDA device" / "host-only"), i.e. no CPU fallback.
 //   GPU    : query_leaves == reference exhaustive_assign on the reference's
 //            acceptance-style synthetic hierarchy (generate_synthetic).
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -15,6 +17,78 @@
 #include "fastmap_b200/fastmap_gpu.hpp"
 
 using namespace fastmap;
+
+// distance from p to a leaf as a region: 0 inside, else the nearest edge
+// (the measure test_cell_index.cpp:381-435 bounds by epsilon)
+static double region_distance(Point p, const PolygonGeometry& g) {
+  if (point_in_polygon(p, g)) return 0.0;
+  double best = 1e300;
+  for (std::size_t r = 0; r < g.ring_starts.size(); ++r) {
+    const std::size_t b = g.ring_starts[r];
+    const std::size_t e = r + 1 < g.ring_starts.size() ? g.ring_starts[r + 1] : g.nodes.size();
+    for (std::size_t i = b; i < e; ++i) {
+      const Point a = g.nodes[i], c = g.nodes[i + 1 < e ? i + 1 : b];
+      const double dx = c.lon - a.lon, dy = c.lat - a.lat, l2 = dx * dx + dy * dy;
+      double t = l2 > 0 ? ((p.lon - a.lon) * dx + (p.lat - a.lat) * dy) / l2 : 0.0;
+      t = t < 0 ? 0 : (t > 1 ? 1 : t);
+      const double ex = p.lon - (a.lon + t * dx), ey = p.lat - (a.lat + t * dy);
+      best = std::min(best, std::sqrt(ex * ex + ey * ey));
+    }
+  }
+  return best;
+}
+
+// fast-approx mode, shaped like test_cell_index.cpp:381-435
+static int check_approx() {
+  const auto h = generate_synthetic({.seed = 37, .n_states = 2, .counties_per_state = 2,
+                                     .blocks_per_county = 9, .jitter = 0.2});
+  const auto leaves = collect_leaves(h);
+  const double eps = 2e-3;
+  CoverParams ap;
+  ap.mode = CoverMode::approx;
+  ap.epsilon = eps;
+  const auto aidx = gpu::build_index(leaves, ap);
+  const auto exact_idx = gpu::build_index(leaves);
+  const auto pts = sample_uniform(hierarchy_bbox(h), 20000, 55);
+  const auto approx = gpu::query_leaves(aidx, leaves, pts, CoverMode::approx);
+  const auto exact = gpu::query_leaves(exact_idx, leaves, pts, CoverMode::exact);
+  const auto exact_on_approx = gpu::query_leaves(aidx, leaves, pts, CoverMode::exact);
+  std::size_t dis = 0, bad = 0;
+  double worst = 0.0;
+  for (std::size_t i = 0; i < pts.size(); ++i) {
+    if (exact_on_approx.block[i] != exact.block[i] || exact_on_approx.county[i] != exact.county[i] ||
+        exact_on_approx.state[i] != exact.state[i]) {
+      ++bad;  // an exact query against the approximate cover is exact
+    }
+    if (approx.block[i] == exact.block[i] && approx.county[i] == exact.county[i] &&
+        approx.state[i] == exact.state[i]) {
+      continue;
+    }
+    ++dis;
+    if (approx.block[i] < 0) {
+      ++bad;  // a disagreement always has a deemed leaf
+      continue;
+    }
+    for (const auto& leaf : leaves) {
+      if (static_cast<int>(leaf.state) == approx.state[i] &&
+          static_cast<int>(leaf.county) == approx.county[i] &&
+          static_cast<int>(leaf.block) == approx.block[i]) {
+        const double d = region_distance(pts[i], *leaf.geometry);
+        worst = std::max(worst, d);
+        if (d > eps) ++bad;
+      }
+    }
+  }
+  try {
+    gpu::query_leaves(exact_idx, leaves, pts, CoverMode::approx);
+    std::puts("FAIL: approx query on an exact-only index");
+    return 1;
+  } catch (const std::invalid_argument&) {
+  }
+  std::printf("%s approx: %zu disagreements of %zu, worst distance %.3g <= %.3g\n",
+              bad ? "FAIL" : "OK", dis, pts.size(), worst, eps);
+  return bad ? 1 : 0;
+}
 
 int main(int argc, char** argv) {
   const bool have_gpu = argc > 1 && std::string(argv[1]) == "gpu";
@@ -64,5 +138,6 @@ int main(int argc, char** argv) {
     bad += ok ? 0 : 1;
   }
   std::printf("%s (GPU): %zu of %zu points differ\n", bad ? "FAIL" : "OK", bad, pts.size());
-  return bad ? 1 : 0;
+  if (bad) return 1;
+  return check_approx();
 }

@@ -82,3 +82,28 @@ def test_error_mapping_matches_reference_exceptions():
     with pytest.raises(ValueError, match="approximate-mode cover"):  # cell_index.hpp:532-535
         fastmap.query_leaves(trie, synth.config("c1").make_soup(), np.zeros((1, 2)),
                              fastmap.CoverMode.approx)
+
+
+def test_approx_cover_params_and_resolution():
+    """fast-approx covers: the C-ABI validates epsilon like
+    validate_cover_params (cell_index.hpp:386-392) and refines the grid until
+    every margin-expanded cell diagonal is <= epsilon (cell_index.hpp:313-316)."""
+    soup = synth.config("c1").make_soup().contiguous()
+    bp = N.BuildParams(device=-1, build_on_gpu=0, approx_epsilon=1e-9)
+    h = C.c_void_p()
+    st = N.lib().fm_index_build(N.ptr(soup.vxy, C.c_double), N.ptr(soup.ring_off, C.c_uint64),
+                                soup.n_rings, N.ptr(soup.poly_ring, C.c_uint64), soup.n_polys,
+                                C.byref(bp), C.byref(h))
+    assert st == 1 and b"level-30" in N.lib().fm_last_error()
+    eps = 0.03
+    P = fastmap.CoverParams(mode=fastmap.CoverMode.approx, epsilon=eps)
+    idx = fastmap.build_index(soup, P, device=-1)
+    s = idx.stats()
+    assert s["approx_epsilon"] == eps
+    assert np.hypot(s["cell_w"] + 2 * s["margin"], s["cell_h"] + 2 * s["margin"]) <= eps
+    assert np.hypot(2 * s["cell_w"], 2 * s["cell_h"]) > eps  # not needlessly fine
+    exact = fastmap.build_index(soup, device=-1).stats()
+    assert s["nx"] * s["ny"] >= exact["nx"] * exact["ny"]
+    with pytest.raises(ValueError, match="needs .* cells"):  # bounded uniform grid
+        fastmap.build_index(soup, fastmap.CoverParams(mode=fastmap.CoverMode.approx,
+                                                      epsilon=1e-6), device=-1)
