@@ -337,11 +337,12 @@ def run_ours(args):
             "config": {
                 "workload": WORKLOADS[args.config], "points_per_gpu": n,
                 "global_points": n * world, "polygons": soup.n_polys,
-                "vertices": soup.n_vertices, "histogram": bool(args.hist),
+                "vertices": soup.n_vertices, "histogram": bool(args.hist), "mode": args.mode,
+                "epsilon": args.epsilon if approx else None,
                 "parallelism": f"point shards x{world}, index replicated",
                 "l2": "inputs larger than L2 (16 B/pt stream), no flush",
                 "index": {k: st[k] for k in ("nx", "ny", "cells_hit", "cells_boundary",
-                                             "grid_bytes", "arena_bytes")},
+                                             "grid_bytes", "arena_bytes", "approx_grid_bytes")},
                 "index_build_s": build_s,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -25,6 +25,8 @@
 #include "index_format.h"
 #include "query.cuh"
 
+#include <cub/cub.cuh>
+
 namespace {
 
 thread_local std::string g_err;
@@ -204,7 +206,7 @@ __device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* 
   for (int q = 0; q < 8; ++q) {
     const int r = 4 * q + (lane >> 3);
     const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
-    if (r < n) {
+    if (r < n && (c < 4 || !(er & fm::kHalfBit))) {  // half slots: first 64 bytes only
       cp_async16(buf + r * fm::kSlotBytes + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
     }
   }
@@ -334,16 +336,42 @@ constexpr int kSmemB = static_cast<int>(sizeof(WarpSmemB)) * kBWarps;
 
 // ---------------------------------------------------------------------------
 // Fast-approx mode (CoverMode::approx, cell_index.hpp:558-560).  The approx
-// cover is a second u32 grid over the same cells: hits and empties as in the
-// exact grid, boundary cells replaced by their deemed leaf.  A query is one
-// 16-byte point read, one 4-byte gather and one 4-byte write -- no queue, no
-// crossing tests.
+// cover assigns every cell of an epsilon-fine grid one answer: hits and
+// empties as in the exact grid, boundary cells their deemed leaf.  It is
+// stored two-level so the first level stays L2-resident: blocks of S x S
+// fine cells (S a power of two) hold either their common answer or, when
+// the block is not uniform, kRecordBit | k -> sub-block k (S*S u32, row-
+// major).  A query is one 16-byte point read, one or two 4-byte gathers and
+// one 4-byte write -- no queue, no crossing tests.
 constexpr int kXThreads = 256;
 constexpr int kXU = 4;
 
+struct AParams {
+  const std::uint32_t* __restrict__ blocks;
+  const std::uint32_t* __restrict__ sub;
+  double gx0, gy0, inv_w, inv_h;
+  double ax0, ax1, ay0, ay1;
+  int nx, ny;       // fine grid
+  int bnx;          // blocks per row
+  int ls;           // log2 S
+};
+
+__device__ __forceinline__ std::uint32_t approx_lookup(const AParams& A, double px, double py) {
+  if (!(px >= A.ax0 && px <= A.ax1 && py >= A.ay0 && py <= A.ay1)) return fm::kEmpty;
+  int ix = static_cast<int>(__dmul_rn(__dsub_rn(px, A.gx0), A.inv_w));
+  int iy = static_cast<int>(__dmul_rn(__dsub_rn(py, A.gy0), A.inv_h));
+  ix = min(max(ix, 0), A.nx - 1);
+  iy = min(max(iy, 0), A.ny - 1);
+  const std::uint32_t e = __ldg(A.blocks + static_cast<std::size_t>(iy >> A.ls) * A.bnx + (ix >> A.ls));
+  if (e == fm::kEmpty || e < fm::kRecordBit) return e;
+  const int m = (1 << A.ls) - 1;
+  return __ldg(A.sub + (static_cast<std::size_t>(e & ~fm::kRecordBit) << (2 * A.ls)) +
+               ((iy & m) << A.ls) + (ix & m));
+}
+
 template <bool kHist, bool kCount>
 __global__ void __launch_bounds__(kXThreads)
-    approx_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
+    approx_kernel(AParams A, const double2* __restrict__ pts, std::uint64_t n,
                   int* __restrict__ out, unsigned long long* __restrict__ hist,
                   unsigned long long* __restrict__ counters) {
   const std::uint64_t chunk = static_cast<std::uint64_t>(kXThreads) * kXU;
@@ -356,11 +384,14 @@ __global__ void __launch_bounds__(kXThreads)
       const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kXThreads;
       p[u] = i < n ? __ldcs(pts + i) : make_double2(NAN, NAN);
     }
+    std::uint32_t e[kXU];
+#pragma unroll
+    for (int u = 0; u < kXU; ++u) e[u] = approx_lookup(A, p[u].x, p[u].y);
 #pragma unroll
     for (int u = 0; u < kXU; ++u) {
       const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kXThreads;
       if (i < n) {
-        emit<kHist>(out, hist, i, static_cast<int>(fm::locate(P, p[u].x, p[u].y)));
+        emit<kHist>(out, hist, i, static_cast<int>(e[u]));
         if (kCount) ++done;
       }
     }
@@ -368,6 +399,53 @@ __global__ void __launch_bounds__(kXThreads)
   if (kCount) {
     for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(0xFFFFFFFFu, done, o);
     if ((threadIdx.x & 31) == 0 && done) atomicAdd(counters + 0, done);
+  }
+}
+
+// Per block of S x S fine cells: 1 when its answers are not all equal.
+__global__ void __launch_bounds__(256)
+    block_flag_kernel(const std::uint32_t* __restrict__ fine, int nx, int ny, int bnx, int bny,
+                      int ls, unsigned long long* __restrict__ flag) {
+  const std::uint64_t b = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= static_cast<std::uint64_t>(bnx) * bny) return;
+  const int by = static_cast<int>(b / bnx), bx = static_cast<int>(b - static_cast<std::uint64_t>(by) * bnx);
+  const int S = 1 << ls;
+  const int x0 = bx << ls, y0 = by << ls;
+  const std::uint32_t v0 = fine[static_cast<std::size_t>(y0) * nx + x0];
+  bool uni = true;
+  for (int j = 0; j < S && y0 + j < ny && uni; ++j) {
+    for (int i = 0; i < S && x0 + i < nx; ++i) {
+      if (fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] != v0) {
+        uni = false;
+        break;
+      }
+    }
+  }
+  flag[b] = uni ? 0ull : 1ull;
+}
+
+__global__ void __launch_bounds__(256)
+    block_write_kernel(const std::uint32_t* __restrict__ fine, int nx, int ny, int bnx, int bny,
+                       int ls, const unsigned long long* __restrict__ flag,
+                       const unsigned long long* __restrict__ idx, std::uint32_t* __restrict__ blocks,
+                       std::uint32_t* __restrict__ sub) {
+  const std::uint64_t b = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= static_cast<std::uint64_t>(bnx) * bny) return;
+  const int by = static_cast<int>(b / bnx), bx = static_cast<int>(b - static_cast<std::uint64_t>(by) * bnx);
+  const int S = 1 << ls;
+  const int x0 = bx << ls, y0 = by << ls;
+  if (!flag[b]) {
+    blocks[b] = fine[static_cast<std::size_t>(y0) * nx + x0];
+    return;
+  }
+  const unsigned long long k = idx[b];
+  blocks[b] = fm::kRecordBit | static_cast<std::uint32_t>(k);
+  std::uint32_t* dst = sub + (k << (2 * ls));
+  for (int j = 0; j < S; ++j) {
+    for (int i = 0; i < S; ++i) {
+      const bool in = y0 + j < ny && x0 + i < nx;
+      dst[(j << ls) + i] = in ? fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] : fm::kEmpty;
+    }
   }
 }
 
@@ -447,7 +525,9 @@ struct fm_index {
   fm::GridGeom g{};
   double ax0 = 0, ax1 = 0, ay0 = 0, ay1 = 0;
   std::uint32_t* d_grid = nullptr;
-  std::uint32_t* d_agrid = nullptr;    // fast-approx grid (deemed leaves), or null
+  std::uint32_t* d_ablocks = nullptr;  // fast-approx cover: block level, or null
+  std::uint32_t* d_asub = nullptr;     // fast-approx cover: non-uniform sub-blocks
+  int a_ls = 0, a_bnx = 0, a_bny = 0;
   std::uint8_t* d_slots = nullptr;     // boundary slots (128 B each)
   std::uint8_t* d_overflow = nullptr;  // overflow records
   std::uint64_t grid_len = 0, slots_len = 0, overflow_len = 0;
@@ -526,14 +606,27 @@ template <bool kHist, bool kCount>
 fm_status launch_approx_t(const fm_index* ix, const double2* pts, std::uint64_t n, int* d_out,
                           unsigned long long* d_hist, unsigned long long* d_counters,
                           cudaStream_t stream) {
-  fm::KParams P = kparams(ix);
-  P.grid = ix->d_agrid;
+  AParams A;
+  A.blocks = ix->d_ablocks;
+  A.sub = ix->d_asub;
+  A.gx0 = ix->g.gx0;
+  A.gy0 = ix->g.gy0;
+  A.inv_w = ix->g.inv_w;
+  A.inv_h = ix->g.inv_h;
+  A.ax0 = ix->ax0;
+  A.ax1 = ix->ax1;
+  A.ay0 = ix->ay0;
+  A.ay1 = ix->ay1;
+  A.nx = static_cast<int>(ix->g.nx);
+  A.ny = static_cast<int>(ix->g.ny);
+  A.bnx = ix->a_bnx;
+  A.ls = ix->a_ls;
   auto k = approx_kernel<kHist, kCount>;
   const std::uint64_t chunk = static_cast<std::uint64_t>(kXThreads) * kXU;
   const int grid = static_cast<int>(std::max<std::uint64_t>(
       1, std::min<std::uint64_t>((n + chunk - 1) / chunk,
                                  resident_blocks(ix->device, (const void*)k, kXThreads, 0))));
-  k<<<grid, kXThreads, 0, stream>>>(P, pts, n, d_out, d_hist, d_counters);
+  k<<<grid, kXThreads, 0, stream>>>(A, pts, n, d_out, d_hist, d_counters);
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));
   return FM_OK;
@@ -569,41 +662,102 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
 }
 
 // The approx cover: copy the exact grid, query every boundary cell's centre
-// through the exact path, then write the deemed leaves.
+// through the exact path, write the deemed leaves, then fold the fine grid
+// into S x S blocks (the smallest S whose block level fits kBlockBudget).
+constexpr std::uint64_t kBlockBudget = std::uint64_t{48} << 20;
+
 fm_status build_approx(fm_index* ix) {
   const std::uint64_t ncell = ix->grid_len;
   const std::uint64_t nb = ix->stats.cells_boundary;
-  FM_CUDA(cudaMalloc(&ix->d_agrid, ncell * 4));
-  FM_CUDA(cudaMemcpy(ix->d_agrid, ix->d_grid, ncell * 4, cudaMemcpyDeviceToDevice));
-  if (nb == 0) return FM_OK;
-  void* scratch = nullptr;
-  const std::uint64_t bytes = nb * (16 + 8 + 4) + 64;
-  FM_CUDA(cudaMalloc(&scratch, bytes));
-  double2* centres = static_cast<double2*>(scratch);
-  std::uint64_t* cells = reinterpret_cast<std::uint64_t*>(centres + nb);
-  int* ids = reinterpret_cast<int*>(cells + nb);
-  unsigned long long* count = reinterpret_cast<unsigned long long*>(
-      (reinterpret_cast<std::uintptr_t>(ids + nb) + 7) & ~std::uintptr_t{7});
+  std::uint32_t* fine = nullptr;
+  FM_CUDA(cudaMalloc(&fine, ncell * 4));
+  FM_CUDA(cudaMemcpy(fine, ix->d_grid, ncell * 4, cudaMemcpyDeviceToDevice));
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+  const int blocks = std::max(1, sms) * 8;
   fm_status st = FM_OK;
-  cudaError_t e = cudaMemset(count, 0, 8);
-  if (e == cudaSuccess) {
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
-    const int blocks = std::max(1, sms) * 8;
-    deem_collect_kernel<<<blocks, 256>>>(ix->d_grid, ncell, static_cast<std::uint64_t>(ix->g.nx),
-                                         ix->g.gx0, ix->g.gy0, ix->g.w, ix->g.h, centres, cells,
-                                         count);
-    e = cudaGetLastError();
+  cudaError_t e = cudaSuccess;
+  if (nb > 0) {
+    void* scratch = nullptr;
+    const std::uint64_t bytes = nb * (16 + 8 + 4) + 64;
+    e = cudaMalloc(&scratch, bytes);
     if (e == cudaSuccess) {
-      st = launch(ix, reinterpret_cast<const double*>(centres), nb, ids, nullptr, nullptr, 0);
-      if (st == FM_OK) {
-        deem_finish_kernel<<<blocks, 256>>>(kparams(ix), cells, ids, nb, ix->d_agrid);
+      double2* centres = static_cast<double2*>(scratch);
+      std::uint64_t* cells = reinterpret_cast<std::uint64_t*>(centres + nb);
+      int* ids = reinterpret_cast<int*>(cells + nb);
+      unsigned long long* count = reinterpret_cast<unsigned long long*>(
+          (reinterpret_cast<std::uintptr_t>(ids + nb) + 7) & ~std::uintptr_t{7});
+      e = cudaMemset(count, 0, 8);
+      if (e == cudaSuccess) {
+        deem_collect_kernel<<<blocks, 256>>>(ix->d_grid, ncell, static_cast<std::uint64_t>(ix->g.nx),
+                                             ix->g.gx0, ix->g.gy0, ix->g.w, ix->g.h, centres,
+                                             cells, count);
         e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaDeviceSynchronize();
       }
+      if (e == cudaSuccess) {
+        st = launch(ix, reinterpret_cast<const double*>(centres), nb, ids, nullptr, nullptr, 0);
+        if (st == FM_OK) {
+          deem_finish_kernel<<<blocks, 256>>>(kparams(ix), cells, ids, nb, fine);
+          e = cudaGetLastError();
+          if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        }
+      }
+      cudaFree(scratch);
     }
   }
-  cudaFree(scratch);
+  if (st == FM_OK && e == cudaSuccess) {
+    const int nx = static_cast<int>(ix->g.nx), ny = static_cast<int>(ix->g.ny);
+    int ls = 0;
+    while (ls < 4 && static_cast<std::uint64_t>((nx + (1 << ls) - 1) >> ls) *
+                             static_cast<std::uint64_t>((ny + (1 << ls) - 1) >> ls) * 4 > kBlockBudget) {
+      ++ls;
+    }
+    const int bnx = (nx + (1 << ls) - 1) >> ls, bny = (ny + (1 << ls) - 1) >> ls;
+    const std::uint64_t nblk = static_cast<std::uint64_t>(bnx) * bny;
+    ix->a_ls = ls;
+    ix->a_bnx = bnx;
+    ix->a_bny = bny;
+    if (ls == 0) {  // the fine grid is small enough to be the block level
+      ix->d_ablocks = fine;
+      fine = nullptr;
+      FM_CUDA(cudaMalloc(&ix->d_asub, 64));
+    } else {
+      unsigned long long *flag = nullptr, *idx = nullptr;
+      void* tmp = nullptr;
+      std::size_t tmp_bytes = 0;
+      e = cudaMalloc(&flag, (nblk + 1) * 8);
+      if (e == cudaSuccess) e = cudaMalloc(&idx, (nblk + 1) * 8);
+      if (e == cudaSuccess) e = cudaMemset(flag + nblk, 0, 8);
+      const unsigned g1 = static_cast<unsigned>((nblk + 255) / 256);
+      if (e == cudaSuccess) {
+        block_flag_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) {
+        e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, idx, static_cast<std::int64_t>(nblk + 1));
+      }
+      if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes + 16);
+      if (e == cudaSuccess) {
+        e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, idx, static_cast<std::int64_t>(nblk + 1));
+      }
+      unsigned long long n_sub = 0;
+      if (e == cudaSuccess) e = cudaMemcpy(&n_sub, idx + nblk, 8, cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess) e = cudaMalloc(&ix->d_ablocks, nblk * 4);
+      if (e == cudaSuccess) e = cudaMalloc(&ix->d_asub, std::max<std::uint64_t>(n_sub, 1) << (2 * ls + 2));
+      if (e == cudaSuccess) {
+        block_write_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag, idx, ix->d_ablocks,
+                                        ix->d_asub);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      ix->stats.approx_grid_bytes = nblk * 4 + (n_sub << (2 * ls + 2));
+      cudaFree(tmp);
+      cudaFree(flag);
+      cudaFree(idx);
+    }
+    if (ls == 0) ix->stats.approx_grid_bytes = ncell * 4;
+  }
+  if (fine) cudaFree(fine);
   if (st != FM_OK) return st;
   if (e != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("approx cover: ") + cudaGetErrorString(e));
   return FM_OK;
@@ -633,7 +787,8 @@ void free_device(fm_index* ix) {
   }
   if (ix->d_hist) cudaFree(ix->d_hist);
   if (ix->d_grid) cudaFree(ix->d_grid);
-  if (ix->d_agrid) cudaFree(ix->d_agrid);
+  if (ix->d_ablocks) cudaFree(ix->d_ablocks);
+  if (ix->d_asub) cudaFree(ix->d_asub);
   if (ix->d_slots) cudaFree(ix->d_slots);
   if (ix->d_overflow) cudaFree(ix->d_overflow);
 }
@@ -806,7 +961,6 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
       delete ix;
       return st;
     }
-    s.approx_grid_bytes = ix->grid_len * 4;
   }
   s.build_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -7,7 +7,10 @@
 // One u32 entry per cell, row-major:
 //   0xFFFFFFFF            empty: no leaf contains any point of the cell
 //   < 0x80000000          true hit: every point of the cell maps to this leaf
-//   0x80000000 | k        boundary: slot k of the slot arena (128 bytes each)
+//   0x80000000 | h<<30 | k boundary: slot k (< 2^30 - 1) of the slot arena
+//                         (128 bytes each); h = 1 when the slot's content
+//                         lies in its first 64 bytes, so the query fetches
+//                         only those (two sectors instead of four)
 //
 // A boundary cell's slot lists its candidate leaves in ascending id order
 // and the exact (fp64) polygon edges near the cell.  Point p maps to the
@@ -20,14 +23,21 @@
 // candidate with no edges, no breakpoints and c0 = 1 is terminal.
 //
 // Slot kinds (128 bytes, 128-byte aligned, little endian):
-//  kind 1, leaf (<= 4 candidates, <= 2 breakpoints, <= 5 chain vertices):
+//  kind 1, leaf (<= 4 candidates, <= 2 breakpoints, <= 5 chain vertices),
+//  laid out so the common cells -- <= 2 candidates and either <= 2
+//  vertices with <= 1 breakpoint or 3 vertices with none -- live in the
+//  first 64 bytes:
 //   +0   u8 kind=1, u8 n_verts, u8 n_cands, u8 n_breaks
-//   +4   u32 chain_mask          bit i set: vertex i starts a new chain
-//   +8   i32 leaf[4]
-//   +24  u8 edge_mask[4]
-//   +28  u8 info[4]              bit 7 = c0, bits 0..1 = break mask
-//   +32  f64 break[2]
-//   +48  {f64 lon, f64 lat} vert[5]
+//   +4   u8 edge_mask[0..1], u8 info[0..1]   info: bit 7 = c0, bits 0..1 = break mask
+//   +8   i32 leaf[0..1]
+//   +16  {f64 lon, f64 lat} vert[0..1]
+//   +48  n_verts >= 3: vert[2];  else f64 break[0], 8 zero bytes
+//   +64  u32 chain_mask          bit i set: vertex i starts a new chain
+//                                (<= 3 vertices are always one chain)
+//   +68  u8 edge_mask[2..3], u8 info[2..3]
+//   +72  i32 leaf[2..3]
+//   +80  n_verts >= 3: f64 break[0..1];  else f64 break[1], 8 zero bytes
+//   +96  {f64 lon, f64 lat} vert[3..4]
 //   Edge i joins vertex i and i+1 unless bit i+1 of chain_mask is set; it
 //   is oriented exactly like the reference (lo = lower latitude,
 //   geometry.hpp:219), which reproduces its (lo, hi) bit for bit.
@@ -67,6 +77,9 @@ namespace fm {
 
 constexpr std::uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr std::uint32_t kRecordBit = 0x80000000u;
+constexpr std::uint32_t kHalfBit = 0x40000000u;     // slot content fits 64 bytes
+constexpr std::uint32_t kSlotIndexMask = 0x3FFFFFFFu;
+constexpr std::uint64_t kMaxSlots = 0x3FFFFFFFull;  // k + flags never equals kEmpty
 constexpr std::uint32_t kMaxLeaves = 0x7FFFFFFEu;
 constexpr std::uint64_t kRecordAlign = 16;
 constexpr std::uint32_t kMaxCands = 0xFFFFu;  // cell_index.hpp:339-341 limit
@@ -82,6 +95,22 @@ constexpr std::uint32_t kSlotMaxCands = 4;
 constexpr std::uint32_t kSlotMaxBreaks = 2;
 constexpr std::uint32_t kSlotMaxVerts = 5;
 constexpr int kMaxSplitDepth = 6;
+
+// Grid/child entry of slot k: split and overflow slots use only their first
+// 64 bytes; so does a leaf slot with <= 2 candidates and either <= 2
+// vertices and <= 1 breakpoint or 3 vertices and none (the layout above).
+FM_HD bool leaf_slot_half(std::uint32_t nv, std::uint32_t nc, std::uint32_t nb) {
+  return nc <= 2 && ((nv <= 2 && nb <= 1) || (nv == 3 && nb == 0));
+}
+FM_HD std::uint32_t slot_entry(std::uint64_t k, std::uint32_t kind, std::uint32_t nv,
+                               std::uint32_t nc, std::uint32_t nb) {
+  const bool half = kind != kSlotLeaf || leaf_slot_half(nv, nc, nb);
+  return kRecordBit | (half ? kHalfBit : 0u) | static_cast<std::uint32_t>(k);
+}
+// same, from the slot's first 4 bytes (u8 kind, nv, nc, nb)
+FM_HD std::uint32_t slot_entry_hdr(std::uint64_t k, std::uint32_t h) {
+  return slot_entry(k, h & 0xFFu, (h >> 8) & 0xFFu, (h >> 16) & 0xFFu, h >> 24);
+}
 // overflow record kinds
 constexpr std::uint8_t kKindCompact = 1;
 constexpr std::uint8_t kKindWide = 2;

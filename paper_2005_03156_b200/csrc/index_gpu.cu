@@ -444,30 +444,29 @@ __device__ int finalize_cell(const DevSoup& s, const Contrib* recs, std::uint64_
     for (int k = 0; k < 32; ++k) w[k] = 0;
     w[0] = kSlotLeaf | (static_cast<std::uint32_t>(nv) << 8) | (static_cast<std::uint32_t>(nc) << 16) |
            (static_cast<std::uint32_t>(nub) << 24);
-    w[1] = chain_mask;
-    std::uint32_t masks = 0, infos = 0;
+    w[16] = nv > 3 ? chain_mask : 0u;  // <= 3 vertices: one chain, implied
     for (int c = 0; c < nc; ++c) {
-      w[2 + c] = cid[c];
+      const int hi = c < 2 ? 0 : 16, j = c & 1;
+      w[hi + 2 + j] = cid[c];
       std::uint32_t mask = 0;
       for (int k = 0; k < nced[c]; ++k) mask |= 1u << bit_of[ced[c][k]];
       std::uint32_t info = (cc0[c] & 1u) << 7;
       for (int k = 0; k < cnb[c]; ++k) info |= (cbr[c][k] == ub[0]) ? 1u : 2u;
-      masks |= (mask & 0xFFu) << (8 * c);
-      infos |= (info & 0xFFu) << (8 * c);
+      w[hi + 1] |= ((mask & 0xFFu) << (8 * j)) | ((info & 0xFFu) << (16 + 8 * j));
     }
-    w[6] = masks;
-    w[7] = infos;
     for (int j = 0; j < nub; ++j) {
       const unsigned long long b = __double_as_longlong(ub[j]);
-      w[8 + 2 * j] = static_cast<std::uint32_t>(b);
-      w[9 + 2 * j] = static_cast<std::uint32_t>(b >> 32);
+      const int o = nv >= 3 ? 20 + 2 * j : (j == 0 ? 12 : 20);
+      w[o] = static_cast<std::uint32_t>(b);
+      w[o + 1] = static_cast<std::uint32_t>(b >> 32);
     }
     for (int k = 0; k < nv; ++k) {
       const unsigned long long x = __double_as_longlong(vx[k]), y = __double_as_longlong(vy[k]);
-      w[12 + 4 * k] = static_cast<std::uint32_t>(x);
-      w[13 + 4 * k] = static_cast<std::uint32_t>(x >> 32);
-      w[14 + 4 * k] = static_cast<std::uint32_t>(y);
-      w[15 + 4 * k] = static_cast<std::uint32_t>(y >> 32);
+      const int o = k < 3 ? 4 + 4 * k : 24 + 4 * (k - 3);
+      w[o] = static_cast<std::uint32_t>(x);
+      w[o + 1] = static_cast<std::uint32_t>(x >> 32);
+      w[o + 2] = static_cast<std::uint32_t>(y);
+      w[o + 3] = static_cast<std::uint32_t>(y >> 32);
     }
     uint4* dst = reinterpret_cast<uint4*>(slot);
     for (int k = 0; k < 8; ++k) dst[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
@@ -494,8 +493,9 @@ __global__ void write_slots_kernel(DevSoup s, const unsigned long long* off, con
   if (cell >= n_cells || kind[cell] != kCellSlot) return;
   std::uint32_t hit = 0;
   const unsigned long long k = slot_idx[cell];
-  finalize_cell(s, recs + off[cell], off[cell + 1] - off[cell], &hit, slots + k * kSlotBytes);
-  grid[cell] = kRecordBit | static_cast<std::uint32_t>(k);
+  std::uint8_t* slot = slots + k * kSlotBytes;
+  finalize_cell(s, recs + off[cell], off[cell + 1] - off[cell], &hit, slot);
+  grid[cell] = slot_entry_hdr(k, *reinterpret_cast<const std::uint32_t*>(slot));
 }
 
 __global__ void flag_kernel(const std::uint8_t* kind, std::uint64_t n, int want,
@@ -674,6 +674,7 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
     return total;
   };
   const unsigned long long n1 = count_kind(kCellSlot);
+  if (n1 > kMaxSlots) throw RuntimeError("index needs more than 2^30 slots");
   DevBuf d_slots1;
   dalloc<std::uint8_t>(d_slots1, std::max<unsigned long long>(n1, 1) * kSlotBytes, "slots");
   write_slots_kernel<<<grid1d(n_cells, 128), 128>>>(ds, d_off.as<unsigned long long>(), d_rec.as<Contrib>(),

@@ -281,7 +281,7 @@ struct RowWorker {
       slots.insert(slots.end(), slot, slot + kSlotBytes);
       note_leaf(used.size(), cin.size(), n_breaks);
       es.compact++;
-      return kRecordBit | static_cast<std::uint32_t>(k);
+      return slot_entry(k, slot[0], slot[1], slot[2], slot[3]);
     }
     if (deferred) {  // phase 1: cells that need a split or overflow wait for phase 2
       *deferred = true;
@@ -317,7 +317,7 @@ struct RowWorker {
         if (child[c] >= kRecordBit && child[c] != kEmpty) slot_patches->push_back(k * kSlotBytes + 40 + 4 * c);
       }
       st.cells_split++;
-      return kRecordBit | static_cast<std::uint32_t>(k);
+      return slot_entry(k, kSlotSplit, 0, 0, 0);
     }
     // past the split depth: variable-size record in the overflow arena
     const std::uint64_t off = ovf->size();
@@ -331,7 +331,7 @@ struct RowWorker {
     ovf_patches->push_back(k * kSlotBytes + 8);
     note_leaf(used.size(), cin.size(), n_breaks);
     st.records_overflow++;
-    return kRecordBit | static_cast<std::uint32_t>(k);
+    return slot_entry(k, kSlotOverflow, 0, 0, 0);
   }
 
   void note_leaf(std::uint64_t ne, std::uint64_t nc, std::uint64_t nb) {
@@ -685,7 +685,7 @@ void finish_deferred(const Soup& s, const GridGeom& g, const BuildOptions& o,
     n_slots += rs[r].size() / kSlotBytes;
     ovf_bytes += (ro[r].size() + 15) & ~std::uint64_t{15};
   }
-  if (slot_base + n_slots >= kRecordBit) throw RuntimeError("index needs more than 2^31 slots");
+  if (slot_base + n_slots > kMaxSlots) throw RuntimeError("index needs more than 2^30 slots");
   slots_out.assign(n_slots * kSlotBytes, 0);
   ovf_out.assign(ovf_bytes, 0);
   std::uint64_t so = 0;

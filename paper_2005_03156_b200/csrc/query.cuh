@@ -25,7 +25,7 @@ struct KParams {
 };
 
 __device__ __forceinline__ const std::uint8_t* slot_ptr(const KParams& P, std::uint32_t e) {
-  return P.slots + static_cast<std::size_t>(e & ~kRecordBit) * kSlotBytes;
+  return P.slots + static_cast<std::size_t>(e & kSlotIndexMask) * kSlotBytes;
 }
 
 __device__ __forceinline__ bool ray_crosses(double px, double py, double lx,
@@ -158,17 +158,21 @@ __device__ __forceinline__ double as_f64(std::uint32_t lo, std::uint32_t hi) {
 }
 
 // Leaf slot (index_format.h, kind 1) held in registers as eight 16-byte
-// chunks; every offset is static, every branch is a predicate.
+// chunks; every offset is static, every branch is a predicate.  For a
+// half slot (kHalfBit) chunks 4..7 may hold stale bytes: every value read
+// from them is masked by n_verts / n_cands / n_breaks.
 template <bool kCount>
 __device__ __forceinline__ int eval_leaf_slot(const uint4 (&c)[8], double px, double py,
                                               WorkCount& wc) {
-  const std::uint32_t h = c[0].x, chain = c[0].y;
+  const std::uint32_t h = c[0].x;
   const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
+  const std::uint32_t chain = nv <= 3u ? 1u : c[4].x;  // <= 3 vertices: one chain
   double vx[kSlotMaxVerts], vy[kSlotMaxVerts];
 #pragma unroll
   for (int k = 0; k < static_cast<int>(kSlotMaxVerts); ++k) {
-    vx[k] = as_f64(c[3 + k].x, c[3 + k].y);
-    vy[k] = as_f64(c[3 + k].z, c[3 + k].w);
+    const uint4 v = c[k < 3 ? 1 + k : 3 + k];
+    vx[k] = as_f64(v.x, v.y);
+    vy[k] = as_f64(v.z, v.w);
   }
   std::uint32_t m = 0;
 #pragma unroll
@@ -178,10 +182,14 @@ __device__ __forceinline__ int eval_leaf_slot(const uint4 (&c)[8], double px, do
       m |= edge_bit(px, py, vx[k], vy[k], vx[k + 1], vy[k + 1]) << k;
     }
   }
-  const double b0 = as_f64(c[2].x, c[2].y), b1 = as_f64(c[2].z, c[2].w);
+  const bool v3 = nv >= 3u;
+  const double b0 = v3 ? as_f64(c[5].x, c[5].y) : as_f64(c[3].x, c[3].y);
+  const double b1 = v3 ? as_f64(c[5].z, c[5].w) : as_f64(c[5].x, c[5].y);
   const std::uint32_t bm = ((nb > 0u && py > b0) ? 1u : 0u) | ((nb > 1u && py > b1) ? 2u : 0u);
-  const std::uint32_t ids[4] = {c[0].z, c[0].w, c[1].x, c[1].y};
-  const std::uint32_t masks = c[1].z, infos = c[1].w;
+  const std::uint32_t ids[4] = {c[0].z, c[0].w, c[4].z, c[4].w};
+  const std::uint32_t lo = c[0].y, hi = c[4].y;  // {mask, mask, info, info} per pair
+  const std::uint32_t masks = (lo & 0xFFFFu) | (hi << 16);
+  const std::uint32_t infos = (lo >> 16) | (hi & 0xFFFF0000u);
   int id = -1;
 #pragma unroll
   for (int q = 3; q >= 0; --q) {  // descending, so the smallest odd candidate wins

@@ -197,23 +197,29 @@ inline bool encode_slot(const std::vector<Edge4>& E, const std::vector<CandIn>& 
   out[1] = static_cast<std::uint8_t>(vx.size());
   out[2] = static_cast<std::uint8_t>(C.size());
   out[3] = static_cast<std::uint8_t>(ub.size());
-  std::memcpy(out + 4, &chain_mask, 4);
+  if (vx.size() > 3) std::memcpy(out + 64, &chain_mask, 4);  // <= 3 vertices: implied
   for (std::size_t c = 0; c < C.size(); ++c) {
     const std::int32_t id = static_cast<std::int32_t>(C[c].id);
-    std::memcpy(out + 8 + 4 * c, &id, 4);
+    const std::size_t hi = c < 2 ? 0 : 64, j = c & 1;
+    std::memcpy(out + hi + 8 + 4 * j, &id, 4);
     std::uint8_t mask = 0;
     for (std::uint32_t e : C[c].edges) mask |= static_cast<std::uint8_t>(1u << bit_of[e]);
     std::uint8_t info = static_cast<std::uint8_t>((C[c].c0 & 1u) << 7);
     for (double b : C[c].breaks) {
       info |= static_cast<std::uint8_t>(1u << (std::lower_bound(ub.begin(), ub.end(), b) - ub.begin()));
     }
-    out[24 + c] = mask;
-    out[28 + c] = info;
+    out[hi + 4 + j] = mask;
+    out[hi + 6 + j] = info;
   }
-  std::memcpy(out + 32, ub.data(), 8 * ub.size());
+  const bool v3 = vx.size() >= 3;
+  for (std::size_t j = 0; j < ub.size(); ++j) {
+    const std::size_t o = v3 ? 80 + 8 * j : (j == 0 ? 48 : 80);
+    std::memcpy(out + o, &ub[j], 8);
+  }
   for (std::size_t k = 0; k < vx.size(); ++k) {
-    std::memcpy(out + 48 + 16 * k, &vx[k], 8);
-    std::memcpy(out + 56 + 16 * k, &vy[k], 8);
+    const std::size_t o = k < 3 ? 16 + 16 * k : 96 + 16 * (k - 3);
+    std::memcpy(out + o, &vx[k], 8);
+    std::memcpy(out + o + 8, &vy[k], 8);
   }
   return true;
 }

@@ -13,6 +13,8 @@ import numpy as np
 
 K_EMPTY = 0xFFFFFFFF
 K_RECORD = 0x80000000
+K_HALF = 0x40000000      # slot content fits its first 64 bytes
+K_INDEX = 0x3FFFFFFF
 
 
 def _cross(px, py, lx, ly, hx, hy) -> bool:
@@ -41,15 +43,23 @@ def _align(v, a):
 SLOT = 128
 
 
+def leaf_half(nv, nc, nb) -> bool:
+    return nc <= 2 and ((nv <= 2 and nb <= 1) or (nv == 3 and nb == 0))
+
+
 def _eval_leaf_slot(arena, off, px, py) -> int:
     buf = arena.data
     nv, nc, nb = int(arena[off + 1]), int(arena[off + 2]), int(arena[off + 3])
-    chain = struct.unpack_from("<I", buf, off + 4)[0]
-    ids = struct.unpack_from("<4i", buf, off + 8)
-    masks = arena[off + 24: off + 28].tolist()
-    infos = arena[off + 28: off + 32].tolist()
-    breaks = struct.unpack_from("<2d", buf, off + 32)
-    v = np.frombuffer(buf, dtype="<f8", count=10, offset=off + 48).reshape(5, 2).tolist()
+    chain = 1 if nv <= 3 else struct.unpack_from("<I", buf, off + 64)[0]
+    ids = struct.unpack_from("<2i", buf, off + 8) + struct.unpack_from("<2i", buf, off + 72)
+    masks = arena[off + 4: off + 6].tolist() + arena[off + 68: off + 70].tolist()
+    infos = arena[off + 6: off + 8].tolist() + arena[off + 70: off + 72].tolist()
+    if nv >= 3:
+        breaks = struct.unpack_from("<2d", buf, off + 80)
+    else:
+        breaks = struct.unpack_from("<d", buf, off + 48) + struct.unpack_from("<d", buf, off + 80)
+    v = (np.frombuffer(buf, dtype="<f8", count=6, offset=off + 16).reshape(3, 2).tolist()
+         + np.frombuffer(buf, dtype="<f8", count=4, offset=off + 96).reshape(2, 2).tolist())
     m = 0
     for k in range(4):
         if k + 1 < nv and not (chain >> (k + 1)) & 1:
@@ -132,8 +142,12 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float, slot_bytes: int
     buf = arena.data
     e = entry
     while True:
-        off = (e & ~K_RECORD) * SLOT
+        off = (e & K_INDEX) * SLOT
         kind = arena[off]
+        half = kind != 1 or leaf_half(*arena[off + 1: off + 4].tolist())
+        assert bool(e & K_HALF) == half, "half-slot flag disagrees with the slot"
+        if half:  # the flag promises nothing past byte 64 is needed
+            assert not arena[off + 64: off + SLOT].any()
         if kind == 1:
             return _eval_leaf_slot(arena, off, px, py)
         if kind == 2:

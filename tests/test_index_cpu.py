@@ -76,18 +76,29 @@ def test_slot_invariants():
     import struct
     cfg = synth.config("c1")
     _, _, (grid, arena, g) = walk(cfg.make_soup(), np.zeros((1, 2)))
-    recs = np.unique(grid[(grid >= 0x80000000) & (grid != 0xFFFFFFFF)])[:3000]
+    recs = np.unique(grid[(grid >= 0x80000000) & (grid != 0xFFFFFFFF)])
+    recs = np.random.default_rng(0).choice(recs, min(3000, recs.size), replace=False)
     n_leaf = 0
+    n_half = 0
     for e in recs.tolist():
-        off = (e & 0x7FFFFFFF) * 128
+        off = (e & 0x3FFFFFFF) * 128
         kind, nv, nc, nb = arena[off:off + 4].tolist()
         assert kind in (1, 2, 3)
+        half = bool(e & 0x40000000)
+        n_half += half
         if kind != 1:
+            assert half and not arena[off + 64: off + 128].any()
             continue
         n_leaf += 1
         assert 1 <= nc <= 4 and nb <= 2 and nv <= 5
-        ids = list(struct.unpack_from("<4i", arena.data, off + 8))[:nc]
+        assert half == (nc <= 2 and ((nv <= 2 and nb <= 1) or (nv == 3 and nb == 0)))
+        if half:
+            assert not arena[off + 64: off + 128].any()
+        ids = (list(struct.unpack_from("<2i", arena.data, off + 8))
+               + list(struct.unpack_from("<2i", arena.data, off + 72)))[:nc]
         assert ids == sorted(ids) and len(set(ids)) == nc
-        for mk in arena[off + 24: off + 24 + nc].tolist():
+        masks = arena[off + 4: off + 6].tolist() + arena[off + 68: off + 70].tolist()
+        for mk in masks[:nc]:
             assert mk < (1 << max(nv - 1, 0)) or mk == 0
+    assert n_half > 0
     assert n_leaf > 0
