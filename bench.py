@@ -321,7 +321,8 @@ def run_ours(args):
     alg_bytes = 20.0 * n + 16.0 * soup.n_vertices  # SURVEY.md sec. 8d per-point + index once
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
-    prof = ROOT / "profiles" / f"ncu_{args.config}_summary.json"
+    prof = ROOT / "profiles" / (f"ncu_{args.config}_approx_summary.json" if approx
+                                else f"ncu_{args.config}_summary.json")
     if prof.exists():
         try:
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
@@ -352,7 +353,7 @@ def run_ours(args):
                          "kernel": ("fm_query_mode(approx) = approx_kernel" if approx else
                                     "fm_query = stream_kernel + resolve_kernel"),
                          "launch_ms": launch_ms,
-                         "traffic_source": "profiles/ncu_%s_summary.json (ncu, cold cache)" % args.config},
+                         "traffic_source": "profiles/%s (ncu, cold cache)" % prof.name},
             "cpu_baseline": cpu,
             "e2e": e2e,
             # our kernels per step: stream_kernel + resolve_kernel (exact) or

@@ -15,3 +15,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"stream_kernel|resolve_kernel" -s 6 -c 2 \
   -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_$TAG.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_$TAG.log
+# fast-approx leg: bench line + launch list of approx_kernel
+ACMD="python bench.py --mode approx --epsilon 5e-3 --steps 3 --warmup 3 --no-cpu --no-e2e"
+timeout 600 python bench.py --mode approx --epsilon 5e-3 --no-cpu > gpurun_out/bench_approx_$TAG.json 2> gpurun_out/bench_approx_$TAG.err
+timeout 300 $ACMD > gpurun_out/plain_approx_$TAG.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -k regex:"approx_kernel" --csv --log-file gpurun_out/launches_approx_$TAG.csv $ACMD > gpurun_out/ncu_la_$TAG.log 2>&1
+echo "approx ncu rc=$?" >> gpurun_out/ncu_la_$TAG.log

@@ -25,10 +25,13 @@ def kernel_name(full: str) -> str:
     return head.split("::")[-1].strip()
 
 
-def main(tag, config="c2", points=100_000_000):
+def main(tag, config="c2", points=100_000_000, mode="exact"):
+    """mode "approx": gpurun_out/launches_approx_<tag>.csv (approx_kernel) ->
+    profiles/<tag>/approx_summary.json and profiles/ncu_<config>_approx_summary.json."""
     out = ROOT / "profiles" / tag
     out.mkdir(parents=True, exist_ok=True)
-    lcsv = ROOT / "gpurun_out" / f"launches_{tag}.csv"
+    sfx = "" if mode == "exact" else "approx_"
+    lcsv = ROOT / "gpurun_out" / f"launches_{sfx}{tag}.csv"
     rows = [r for r in csv.reader(open(lcsv)) if len(r) > 10 and r[0] != "ID"]
     per = defaultdict(lambda: defaultdict(list))
     for r in rows:
@@ -53,9 +56,9 @@ def main(tag, config="c2", points=100_000_000):
     summ["fm_query_ns_ncu"] = total_ns
     for k in per:
         summ[k]["share_of_fm_query"] = summ[k]["mean_ns"] / total_ns
-    shutil.copy(lcsv, out / "launches.csv")
+    shutil.copy(lcsv, out / f"launches{'' if mode == 'exact' else '_approx'}.csv")
     rep = ROOT / "gpurun_out" / f"prof_{tag}.ncu-rep"
-    if rep.exists():
+    if rep.exists() and mode == "exact":
         txt = subprocess.run(["ncu", "-i", str(rep), "--page", "details", "--csv"],
                              capture_output=True, text=True).stdout
         by_k = defaultdict(list)
@@ -65,10 +68,12 @@ def main(tag, config="c2", points=100_000_000):
                            f"{d['Metric Value']} {d['Metric Unit']}")
         for k, lines in by_k.items():
             (out / f"details_{k}.txt").write_text("\n".join(lines) + "\n")
-    (out / "summary.json").write_text(json.dumps(summ, indent=1) + "\n")
-    shutil.copy(out / "summary.json", ROOT / "profiles" / f"ncu_{config}_summary.json")
+    name = "summary.json" if mode == "exact" else "approx_summary.json"
+    (out / name).write_text(json.dumps(summ, indent=1) + "\n")
+    shutil.copy(out / name, ROOT / "profiles" / (f"ncu_{config}_summary.json" if mode == "exact"
+                                                 else f"ncu_{config}_approx_summary.json"))
     print(json.dumps(summ, indent=1))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:2])
+    main(sys.argv[1], mode=sys.argv[2] if len(sys.argv) > 2 else "exact")
