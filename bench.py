@@ -343,7 +343,9 @@ def run_ours(args):
                 "parallelism": f"point shards x{world}, index replicated",
                 "l2": "inputs larger than L2 (16 B/pt stream), no flush",
                 "index": {k: st[k] for k in ("nx", "ny", "cells_hit", "cells_boundary",
-                                             "grid_bytes", "arena_bytes", "approx_grid_bytes")},
+                                             "grid_bytes", "arena_bytes", "query_grid_bytes",
+                                             "query_block_log2", "approx_grid_bytes",
+                                             "approx_block_log2")},
                 "index_build_s": build_s,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

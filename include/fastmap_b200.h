@@ -73,7 +73,7 @@ typedef struct fm_index fm_index;
  * Zero-initialise and set what you need. */
 typedef struct fm_build_params {
   /* Grid resolution: cells per mean polygon bbox side.  0 = auto
-   * (about 40M cells in total, clamped to [4, 64] per polygon side). */
+   * (about 160M cells in total, clamped to [4, 64] per polygon side). */
   double cells_per_polygon;
   /* Explicit grid dimensions; both > 0 override cells_per_polygon. */
   int64_t nx, ny;
@@ -116,6 +116,9 @@ typedef struct fm_index_stats {
   uint64_t slots_total;
   double approx_epsilon;      /* 0 for an exact-only index */
   uint64_t approx_grid_bytes; /* deemed-leaf grid of the approx cover */
+  uint64_t query_grid_bytes;  /* query-side folded copy of the grid (blocks + sub-blocks) */
+  int32_t query_block_log2;   /* its block side, log2 cells (0 = the flat grid itself) */
+  int32_t approx_block_log2;  /* same for the approx cover */
 } fm_index_stats;
 
 /* Optional per-call work counters (diagnostics; device-side atomics). */

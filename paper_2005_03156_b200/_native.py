@@ -63,6 +63,8 @@ class IndexStats(C.Structure):
         ("built_on_gpu", C.c_int32), ("reserved0", C.c_int32),
         ("cells_split", u64), ("slots_phase1", u64), ("slots_total", u64),
         ("approx_epsilon", C.c_double), ("approx_grid_bytes", u64),
+        ("query_grid_bytes", u64), ("query_block_log2", C.c_int32),
+        ("approx_block_log2", C.c_int32),
     ]
 
     def as_dict(self) -> dict:

@@ -346,32 +346,9 @@ constexpr int kSmemB = static_cast<int>(sizeof(WarpSmemB)) * kBWarps;
 constexpr int kXThreads = 256;
 constexpr int kXU = 4;
 
-struct AParams {
-  const std::uint32_t* __restrict__ blocks;
-  const std::uint32_t* __restrict__ sub;
-  double gx0, gy0, inv_w, inv_h;
-  double ax0, ax1, ay0, ay1;
-  int nx, ny;       // fine grid
-  int bnx;          // blocks per row
-  int ls;           // log2 S
-};
-
-__device__ __forceinline__ std::uint32_t approx_lookup(const AParams& A, double px, double py) {
-  if (!(px >= A.ax0 && px <= A.ax1 && py >= A.ay0 && py <= A.ay1)) return fm::kEmpty;
-  int ix = static_cast<int>(__dmul_rn(__dsub_rn(px, A.gx0), A.inv_w));
-  int iy = static_cast<int>(__dmul_rn(__dsub_rn(py, A.gy0), A.inv_h));
-  ix = min(max(ix, 0), A.nx - 1);
-  iy = min(max(iy, 0), A.ny - 1);
-  const std::uint32_t e = __ldg(A.blocks + static_cast<std::size_t>(iy >> A.ls) * A.bnx + (ix >> A.ls));
-  if (e == fm::kEmpty || e < fm::kRecordBit) return e;
-  const int m = (1 << A.ls) - 1;
-  return __ldg(A.sub + (static_cast<std::size_t>(e & ~fm::kRecordBit) << (2 * A.ls)) +
-               ((iy & m) << A.ls) + (ix & m));
-}
-
 template <bool kHist, bool kCount>
 __global__ void __launch_bounds__(kXThreads)
-    approx_kernel(AParams A, const double2* __restrict__ pts, std::uint64_t n,
+    approx_kernel(fm::KParams A, const double2* __restrict__ pts, std::uint64_t n,
                   int* __restrict__ out, unsigned long long* __restrict__ hist,
                   unsigned long long* __restrict__ counters) {
   const std::uint64_t chunk = static_cast<std::uint64_t>(kXThreads) * kXU;
@@ -386,7 +363,7 @@ __global__ void __launch_bounds__(kXThreads)
     }
     std::uint32_t e[kXU];
 #pragma unroll
-    for (int u = 0; u < kXU; ++u) e[u] = approx_lookup(A, p[u].x, p[u].y);
+    for (int u = 0; u < kXU; ++u) e[u] = fm::locate(A, p[u].x, p[u].y);
 #pragma unroll
     for (int u = 0; u < kXU; ++u) {
       const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kXThreads;
@@ -421,6 +398,9 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+  // a slot reference must sit in a sub-block (block entries with kRecordBit
+  // are sub-block pointers)
+  if (v0 != fm::kEmpty && v0 >= fm::kRecordBit) uni = false;
   flag[b] = uni ? 0ull : 1ull;
 }
 
@@ -518,6 +498,22 @@ int resident_blocks(int device, const void* kernel, int block, int smem) {
   return blocks;
 }
 
+// A grid folded into blocks of 2^ls x 2^ls cells (see KParams).  `owned`
+// is false when `blocks` aliases the flat grid (ls = 0).
+struct Folded {
+  std::uint32_t* blocks = nullptr;
+  std::uint32_t* sub = nullptr;
+  int ls = 0, bnx = 0, bny = 0;
+  bool owned = false;
+  std::uint64_t bytes = 0;
+  void release() {
+    if (owned && blocks) cudaFree(blocks);
+    if (sub) cudaFree(sub);
+    blocks = nullptr;
+    sub = nullptr;
+  }
+};
+
 }  // namespace
 
 struct fm_index {
@@ -525,9 +521,8 @@ struct fm_index {
   fm::GridGeom g{};
   double ax0 = 0, ax1 = 0, ay0 = 0, ay1 = 0;
   std::uint32_t* d_grid = nullptr;
-  std::uint32_t* d_ablocks = nullptr;  // fast-approx cover: block level, or null
-  std::uint32_t* d_asub = nullptr;     // fast-approx cover: non-uniform sub-blocks
-  int a_ls = 0, a_bnx = 0, a_bny = 0;
+  Folded qgrid;                        // query-side folded copy of the exact grid
+  Folded agrid;                        // fast-approx cover (folded), or empty
   std::uint8_t* d_slots = nullptr;     // boundary slots (128 B each)
   std::uint8_t* d_overflow = nullptr;  // overflow records
   std::uint64_t grid_len = 0, slots_len = 0, overflow_len = 0;
@@ -559,6 +554,10 @@ fm::KParams kparams(const fm_index* ix) {
   P.ay1 = ix->ay1;
   P.nx = static_cast<int>(ix->g.nx);
   P.ny = static_cast<int>(ix->g.ny);
+  P.blocks = ix->qgrid.blocks;
+  P.sub = ix->qgrid.sub;
+  P.bnx = ix->qgrid.bnx;
+  P.ls = ix->qgrid.ls;
   return P;
 }
 
@@ -606,21 +605,11 @@ template <bool kHist, bool kCount>
 fm_status launch_approx_t(const fm_index* ix, const double2* pts, std::uint64_t n, int* d_out,
                           unsigned long long* d_hist, unsigned long long* d_counters,
                           cudaStream_t stream) {
-  AParams A;
-  A.blocks = ix->d_ablocks;
-  A.sub = ix->d_asub;
-  A.gx0 = ix->g.gx0;
-  A.gy0 = ix->g.gy0;
-  A.inv_w = ix->g.inv_w;
-  A.inv_h = ix->g.inv_h;
-  A.ax0 = ix->ax0;
-  A.ax1 = ix->ax1;
-  A.ay0 = ix->ay0;
-  A.ay1 = ix->ay1;
-  A.nx = static_cast<int>(ix->g.nx);
-  A.ny = static_cast<int>(ix->g.ny);
-  A.bnx = ix->a_bnx;
-  A.ls = ix->a_ls;
+  fm::KParams A = kparams(ix);
+  A.blocks = ix->agrid.blocks;
+  A.sub = ix->agrid.sub;
+  A.bnx = ix->agrid.bnx;
+  A.ls = ix->agrid.ls;
   auto k = approx_kernel<kHist, kCount>;
   const std::uint64_t chunk = static_cast<std::uint64_t>(kXThreads) * kXU;
   const int grid = static_cast<int>(std::max<std::uint64_t>(
@@ -660,6 +649,73 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
   }
   return FM_OK;
 }
+
+// Fold a flat nx x ny grid into blocks (KParams): the smallest ls <= max_ls
+// whose block level fits `budget` bytes.  ls = 0 aliases the flat grid.
+fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, int max_ls,
+                    Folded* out) {
+  int ls = 0;
+  while (ls < max_ls && static_cast<std::uint64_t>((nx + (1 << ls) - 1) >> ls) *
+                                static_cast<std::uint64_t>((ny + (1 << ls) - 1) >> ls) * 4 > budget) {
+    ++ls;
+  }
+  const int bnx = (nx + (1 << ls) - 1) >> ls, bny = (ny + (1 << ls) - 1) >> ls;
+  const std::uint64_t nblk = static_cast<std::uint64_t>(bnx) * bny;
+  out->ls = ls;
+  out->bnx = bnx;
+  out->bny = bny;
+  if (ls == 0) {
+    out->blocks = fine;
+    out->owned = false;
+    FM_CUDA(cudaMalloc(&out->sub, 64));
+    out->bytes = nblk * 4;
+    return FM_OK;
+  }
+  unsigned long long *flag = nullptr, *idx = nullptr;
+  void* tmp = nullptr;
+  std::size_t tmp_bytes = 0;
+  unsigned long long n_sub = 0;
+  cudaError_t e = cudaMalloc(&flag, (nblk + 1) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&idx, (nblk + 1) * 8);
+  if (e == cudaSuccess) e = cudaMemset(flag + nblk, 0, 8);
+  const unsigned g1 = static_cast<unsigned>((nblk + 255) / 256);
+  if (e == cudaSuccess) {
+    block_flag_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, idx, static_cast<std::int64_t>(nblk + 1));
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes + 16);
+  if (e == cudaSuccess) {
+    e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, idx, static_cast<std::int64_t>(nblk + 1));
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(&n_sub, idx + nblk, 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) {
+    out->owned = true;
+    e = cudaMalloc(&out->blocks, nblk * 4);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&out->sub, std::max<std::uint64_t>(n_sub, 1) << (2 * ls + 2));
+  if (e == cudaSuccess) {
+    block_write_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag, idx, out->blocks, out->sub);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  out->bytes = nblk * 4 + (n_sub << (2 * ls + 2));
+  cudaFree(tmp);
+  cudaFree(flag);
+  cudaFree(idx);
+  if (e != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("grid folding: ") + cudaGetErrorString(e));
+  return FM_OK;
+}
+
+// Query-side block level of the exact grid: a 2x2 fold when the flat grid
+// exceeds kQueryBudget (c2: 105 MB flat -> 26 MB blocks + 16-byte sub-blocks).
+constexpr std::uint64_t kQueryBudget = std::uint64_t{32} << 20;
+#ifndef FM_QUERY_MAX_LS
+#define FM_QUERY_MAX_LS 2
+#endif
+constexpr int kQueryMaxLs = FM_QUERY_MAX_LS;
 
 // The approx cover: copy the exact grid, query every boundary cell's centre
 // through the exact path, write the deemed leaves, then fold the fine grid
@@ -706,56 +762,14 @@ fm_status build_approx(fm_index* ix) {
     }
   }
   if (st == FM_OK && e == cudaSuccess) {
-    const int nx = static_cast<int>(ix->g.nx), ny = static_cast<int>(ix->g.ny);
-    int ls = 0;
-    while (ls < 4 && static_cast<std::uint64_t>((nx + (1 << ls) - 1) >> ls) *
-                             static_cast<std::uint64_t>((ny + (1 << ls) - 1) >> ls) * 4 > kBlockBudget) {
-      ++ls;
-    }
-    const int bnx = (nx + (1 << ls) - 1) >> ls, bny = (ny + (1 << ls) - 1) >> ls;
-    const std::uint64_t nblk = static_cast<std::uint64_t>(bnx) * bny;
-    ix->a_ls = ls;
-    ix->a_bnx = bnx;
-    ix->a_bny = bny;
-    if (ls == 0) {  // the fine grid is small enough to be the block level
-      ix->d_ablocks = fine;
+    st = fold_grid(fine, static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny), kBlockBudget, 4,
+                   &ix->agrid);
+    if (st == FM_OK && ix->agrid.ls == 0) {
+      ix->agrid.owned = true;  // the approx copy itself is the block level
       fine = nullptr;
-      FM_CUDA(cudaMalloc(&ix->d_asub, 64));
-    } else {
-      unsigned long long *flag = nullptr, *idx = nullptr;
-      void* tmp = nullptr;
-      std::size_t tmp_bytes = 0;
-      e = cudaMalloc(&flag, (nblk + 1) * 8);
-      if (e == cudaSuccess) e = cudaMalloc(&idx, (nblk + 1) * 8);
-      if (e == cudaSuccess) e = cudaMemset(flag + nblk, 0, 8);
-      const unsigned g1 = static_cast<unsigned>((nblk + 255) / 256);
-      if (e == cudaSuccess) {
-        block_flag_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag);
-        e = cudaGetLastError();
-      }
-      if (e == cudaSuccess) {
-        e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, idx, static_cast<std::int64_t>(nblk + 1));
-      }
-      if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes + 16);
-      if (e == cudaSuccess) {
-        e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, idx, static_cast<std::int64_t>(nblk + 1));
-      }
-      unsigned long long n_sub = 0;
-      if (e == cudaSuccess) e = cudaMemcpy(&n_sub, idx + nblk, 8, cudaMemcpyDeviceToHost);
-      if (e == cudaSuccess) e = cudaMalloc(&ix->d_ablocks, nblk * 4);
-      if (e == cudaSuccess) e = cudaMalloc(&ix->d_asub, std::max<std::uint64_t>(n_sub, 1) << (2 * ls + 2));
-      if (e == cudaSuccess) {
-        block_write_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag, idx, ix->d_ablocks,
-                                        ix->d_asub);
-        e = cudaGetLastError();
-      }
-      if (e == cudaSuccess) e = cudaDeviceSynchronize();
-      ix->stats.approx_grid_bytes = nblk * 4 + (n_sub << (2 * ls + 2));
-      cudaFree(tmp);
-      cudaFree(flag);
-      cudaFree(idx);
     }
-    if (ls == 0) ix->stats.approx_grid_bytes = ncell * 4;
+    ix->stats.approx_grid_bytes = ix->agrid.bytes;
+    ix->stats.approx_block_log2 = ix->agrid.ls;
   }
   if (fine) cudaFree(fine);
   if (st != FM_OK) return st;
@@ -787,8 +801,8 @@ void free_device(fm_index* ix) {
   }
   if (ix->d_hist) cudaFree(ix->d_hist);
   if (ix->d_grid) cudaFree(ix->d_grid);
-  if (ix->d_ablocks) cudaFree(ix->d_ablocks);
-  if (ix->d_asub) cudaFree(ix->d_asub);
+  ix->qgrid.release();
+  ix->agrid.release();
   if (ix->d_slots) cudaFree(ix->d_slots);
   if (ix->d_overflow) cudaFree(ix->d_overflow);
 }
@@ -951,6 +965,18 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
       std::uint64_t thr = ~std::uint64_t{0};
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+  }
+  if (ix->device >= 0) {
+    DeviceGuard guard(ix->device);
+    const fm_status st = fold_grid(ix->d_grid, static_cast<int>(ix->g.nx),
+                                   static_cast<int>(ix->g.ny), kQueryBudget, kQueryMaxLs, &ix->qgrid);
+    if (st != FM_OK) {
+      free_device(ix);
+      delete ix;
+      return st;
+    }
+    s.query_grid_bytes = ix->qgrid.bytes;
+    s.query_block_log2 = ix->qgrid.ls;
   }
   s.approx_epsilon = p.approx_epsilon;
   if (ix->device >= 0 && p.approx_epsilon > 0.0) {

@@ -524,9 +524,10 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
     if (!(mh > 0.0)) mh = GH / side;
     double m = o.cells_per_polygon;
     if (!(m > 0.0)) {
-      // ~40M cells (160 MB of u32 entries): fine enough that boundary cells
-      // are a minority and their records short
-      m = std::sqrt(40.0 * 1024.0 * 1024.0 / static_cast<double>(active));
+      // ~160M cells: fine enough that boundary cells are a minority and
+      // their records short, while the query's folded copy of the grid
+      // keeps an L2-resident block level
+      m = std::sqrt(160.0e6 / static_cast<double>(active));
       m = std::min(64.0, std::max(4.0, m));
     }
     nx = static_cast<std::int64_t>(std::ceil(GW / (mw / m)));

@@ -16,12 +16,19 @@
 namespace fm {
 
 struct KParams {
-  const std::uint32_t* __restrict__ grid;
+  const std::uint32_t* __restrict__ grid;     // flat grid (index_format.h)
   const std::uint8_t* __restrict__ slots;     // 128-byte boundary slots
   const std::uint8_t* __restrict__ overflow;  // variable-size records
+  // The query-side copy of the grid, folded into blocks of 2^ls x 2^ls
+  // cells: a block entry is the common entry of a uniform block, or
+  // kRecordBit | k for sub-block k (2^(2 ls) entries, row-major) -- so the
+  // first level stays L2-resident.
+  const std::uint32_t* __restrict__ blocks;
+  const std::uint32_t* __restrict__ sub;
   double gx0, gy0, inv_w, inv_h;
   double ax0, ax1, ay0, ay1;  // acceptance box = padded domain intersect world box
   int nx, ny;
+  int bnx, ls;                // blocks per row, log2 block side
 };
 
 __device__ __forceinline__ const std::uint8_t* slot_ptr(const KParams& P, std::uint32_t e) {
@@ -52,7 +59,12 @@ __device__ __forceinline__ std::uint32_t locate(const KParams& P, double px, dou
   int iy = static_cast<int>(__dmul_rn(__dsub_rn(py, P.gy0), P.inv_h));
   ix = min(max(ix, 0), P.nx - 1);
   iy = min(max(iy, 0), P.ny - 1);
-  return __ldg(P.grid + static_cast<std::size_t>(iy) * static_cast<std::size_t>(P.nx) + ix);
+  const std::uint32_t e =
+      __ldg(P.blocks + static_cast<std::size_t>(iy >> P.ls) * static_cast<std::size_t>(P.bnx) + (ix >> P.ls));
+  if (P.ls == 0 || e == kEmpty || e < kRecordBit) return e;  // ls = 0: the flat grid itself
+  const int m = (1 << P.ls) - 1;
+  return __ldg(P.sub + (static_cast<std::size_t>(e & ~kRecordBit) << (2 * P.ls)) + ((iy & m) << P.ls) +
+               (ix & m));
 }
 
 struct WorkCount {

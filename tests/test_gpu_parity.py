@@ -100,3 +100,17 @@ def test_empty_and_tiny_inputs(dev):
     idx0 = fastmap.build_index(none, device=0)
     pts = cfg.make_points(1000)
     assert (project_device(idx0, pts, dev) == -1).all()
+
+
+def test_folded_query_grid_odd_dims(dev):
+    """The query-side 2x2 fold of the grid (KParams.blocks/sub) at odd grid
+    dimensions (partial edge blocks) gives the flat grid's answers."""
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    idx = fastmap.build_index(soup, fastmap.CoverParams(nx=4097, ny=2049), device=0)
+    st = idx.stats()
+    assert st["query_block_log2"] == 1 and st["query_grid_bytes"] < st["grid_bytes"]
+    pts = cfg.make_points(1_000_000, offset=77)
+    assert np.array_equal(project_device(idx, pts, dev), oracle.assign(soup, pts))
+    c2 = fastmap.build_index(synth.config("c2").make_soup(), device=0).stats()
+    assert c2["query_block_log2"] >= 1

@@ -26,7 +26,7 @@ def test_c1_index_exact():
     assert st["cells_boundary"] > 0 and st["cells_hit"] > st["cells_boundary"]
 
 
-@pytest.mark.parametrize("name,m", [("c2", 6), ("c2", 14), ("c4", 24), ("c3mini", 0)])
+@pytest.mark.parametrize("name,m", [("c2", 6), ("c2", 14), ("c4", 24), ("c3mini", 16)])
 def test_large_config_index_exact_sampled(name, m):
     cfg = synth.config(name)
     soup = cfg.make_soup()

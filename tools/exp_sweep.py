@@ -47,6 +47,7 @@ for m in ms_list:
     print(json.dumps({"lib": lib, "m": m, "nx": st["nx"], "ny": st["ny"], "ms": ms,
                       "pts_per_s": N / ms * 1e3, "grid_MB": st["grid_bytes"] / 1e6,
                       "arena_MB": st["arena_bytes"] / 1e6,
+                      "query_grid_MB": st["query_grid_bytes"] / 1e6, "ls": st["query_block_log2"],
                       "boundary_frac": c[1] / N, "cands_per_bpt": c[2] / max(1, c[1]),
                       "edges_per_bpt": c[3] / max(1, c[1])}), flush=True)
     idx.close()
