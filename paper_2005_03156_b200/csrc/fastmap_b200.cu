@@ -379,46 +379,89 @@ __global__ void __launch_bounds__(kXThreads)
   }
 }
 
-// Per block of S x S fine cells: 1 when its answers are not all equal.
+// Per block of S x S fine cells: 0 when its answers are all equal, 1 when
+// a palette sub-block holds it (<= 3 distinct values, palette allowed:
+// ls in [1, 3]), 1 << 32 when a full sub-block does.  The exclusive scan of
+// these u64 flags numbers both kinds at once.
 __global__ void __launch_bounds__(256)
     block_flag_kernel(const std::uint32_t* __restrict__ fine, int nx, int ny, int bnx, int bny,
-                      int ls, unsigned long long* __restrict__ flag) {
+                      int ls, int palette, unsigned long long* __restrict__ flag) {
   const std::uint64_t b = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= static_cast<std::uint64_t>(bnx) * bny) return;
   const int by = static_cast<int>(b / bnx), bx = static_cast<int>(b - static_cast<std::uint64_t>(by) * bnx);
   const int S = 1 << ls;
   const int x0 = bx << ls, y0 = by << ls;
-  const std::uint32_t v0 = fine[static_cast<std::size_t>(y0) * nx + x0];
-  bool uni = true;
-  for (int j = 0; j < S && y0 + j < ny && uni; ++j) {
-    for (int i = 0; i < S && x0 + i < nx; ++i) {
-      if (fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] != v0) {
-        uni = false;
-        break;
+  std::uint32_t v[3];
+  int nd = 0;
+  bool rec = false;
+  for (int j = 0; j < S; ++j) {
+    for (int i = 0; i < S; ++i) {
+      const bool in = y0 + j < ny && x0 + i < nx;
+      const std::uint32_t x = in ? fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] : fm::kEmpty;
+      // a slot reference must sit in a full sub-block (record-flagged block
+      // entries are sub-block pointers)
+      if (x != fm::kEmpty && x >= fm::kRecordBit) rec = true;
+      if (!in && j + i > 0) continue;  // outside cells never take part in uniformity
+      bool seen = false;
+      for (int q = 0; q < nd && q < 3; ++q) seen |= v[q] == x;
+      if (!seen) {
+        if (nd < 3) v[nd] = x;
+        ++nd;
       }
     }
   }
-  // a slot reference must sit in a sub-block (block entries with kRecordBit
-  // are sub-block pointers)
-  if (v0 != fm::kEmpty && v0 >= fm::kRecordBit) uni = false;
-  flag[b] = uni ? 0ull : 1ull;
+  unsigned long long f;
+  if (nd == 1 && !rec) f = 0ull;
+  else if (palette && !rec && nd <= 3) f = 1ull;
+  else f = 1ull << 32;
+  flag[b] = f;
 }
+
+// Palette sub-block (approx covers): u32 palette[3], then 2-bit codes per
+// cell in row-major order -- 16 bytes for ls <= 2 (codes at +12), 32 bytes
+// for ls = 3 (codes at +16).
+__host__ __device__ constexpr int palette_words(int ls) { return ls <= 2 ? 4 : 8; }
 
 __global__ void __launch_bounds__(256)
     block_write_kernel(const std::uint32_t* __restrict__ fine, int nx, int ny, int bnx, int bny,
                        int ls, const unsigned long long* __restrict__ flag,
                        const unsigned long long* __restrict__ idx, std::uint32_t* __restrict__ blocks,
-                       std::uint32_t* __restrict__ sub) {
+                       std::uint32_t* __restrict__ sub, std::uint32_t* __restrict__ pal) {
   const std::uint64_t b = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= static_cast<std::uint64_t>(bnx) * bny) return;
   const int by = static_cast<int>(b / bnx), bx = static_cast<int>(b - static_cast<std::uint64_t>(by) * bnx);
   const int S = 1 << ls;
   const int x0 = bx << ls, y0 = by << ls;
-  if (!flag[b]) {
+  const unsigned long long f = flag[b];
+  if (!f) {
     blocks[b] = fine[static_cast<std::size_t>(y0) * nx + x0];
     return;
   }
-  const unsigned long long k = idx[b];
+  if (f == 1ull) {  // palette
+    const unsigned long long k = idx[b] & 0xFFFFFFFFull;
+    blocks[b] = fm::kRecordBit | fm::kHalfBit | static_cast<std::uint32_t>(k);
+    std::uint32_t* dst = pal + k * palette_words(ls);
+    std::uint32_t v[3] = {fm::kEmpty, fm::kEmpty, fm::kEmpty};
+    int nd = 0;
+    const int cw = ls <= 2 ? 3 : 4;
+    for (int w = 0; w < palette_words(ls); ++w) dst[w] = 0;
+    for (int j = 0; j < S; ++j) {
+      for (int i = 0; i < S; ++i) {
+        const bool in = y0 + j < ny && x0 + i < nx;
+        const std::uint32_t x = in ? fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] : v[0];
+        int code = 0;
+        while (code < nd && v[code] != x) ++code;
+        if (code == nd) v[nd++] = x;
+        const int c = (j << ls) + i;
+        dst[cw + (c >> 4)] |= static_cast<std::uint32_t>(code) << (2 * (c & 15));
+      }
+    }
+    dst[0] = v[0];
+    dst[1] = v[1];
+    dst[2] = v[2];
+    return;
+  }
+  const unsigned long long k = idx[b] >> 32;
   blocks[b] = fm::kRecordBit | static_cast<std::uint32_t>(k);
   std::uint32_t* dst = sub + (k << (2 * ls));
   for (int j = 0; j < S; ++j) {
@@ -503,14 +546,17 @@ int resident_blocks(int device, const void* kernel, int block, int smem) {
 struct Folded {
   std::uint32_t* blocks = nullptr;
   std::uint32_t* sub = nullptr;
+  std::uint32_t* pal = nullptr;  // palette sub-blocks (approx covers)
   int ls = 0, bnx = 0, bny = 0;
   bool owned = false;
   std::uint64_t bytes = 0;
   void release() {
     if (owned && blocks) cudaFree(blocks);
     if (sub) cudaFree(sub);
+    if (pal) cudaFree(pal);
     blocks = nullptr;
     sub = nullptr;
+    pal = nullptr;
   }
 };
 
@@ -556,6 +602,7 @@ fm::KParams kparams(const fm_index* ix) {
   P.ny = static_cast<int>(ix->g.ny);
   P.blocks = ix->qgrid.blocks;
   P.sub = ix->qgrid.sub;
+  P.pal = ix->qgrid.pal;
   P.bnx = ix->qgrid.bnx;
   P.ls = ix->qgrid.ls;
   return P;
@@ -608,6 +655,7 @@ fm_status launch_approx_t(const fm_index* ix, const double2* pts, std::uint64_t 
   fm::KParams A = kparams(ix);
   A.blocks = ix->agrid.blocks;
   A.sub = ix->agrid.sub;
+  A.pal = ix->agrid.pal;
   A.bnx = ix->agrid.bnx;
   A.ls = ix->agrid.ls;
   auto k = approx_kernel<kHist, kCount>;
@@ -653,7 +701,7 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
 // Fold a flat nx x ny grid into blocks (KParams): the smallest ls <= max_ls
 // whose block level fits `budget` bytes.  ls = 0 aliases the flat grid.
 fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, int max_ls,
-                    Folded* out) {
+                    bool palette, Folded* out) {
   int ls = 0;
   while (ls < max_ls && static_cast<std::uint64_t>((nx + (1 << ls) - 1) >> ls) *
                                 static_cast<std::uint64_t>((ny + (1 << ls) - 1) >> ls) * 4 > budget) {
@@ -668,19 +716,20 @@ fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, i
     out->blocks = fine;
     out->owned = false;
     FM_CUDA(cudaMalloc(&out->sub, 64));
+    FM_CUDA(cudaMalloc(&out->pal, 64));
     out->bytes = nblk * 4;
     return FM_OK;
   }
   unsigned long long *flag = nullptr, *idx = nullptr;
   void* tmp = nullptr;
   std::size_t tmp_bytes = 0;
-  unsigned long long n_sub = 0;
+  unsigned long long tot = 0;
   cudaError_t e = cudaMalloc(&flag, (nblk + 1) * 8);
   if (e == cudaSuccess) e = cudaMalloc(&idx, (nblk + 1) * 8);
   if (e == cudaSuccess) e = cudaMemset(flag + nblk, 0, 8);
   const unsigned g1 = static_cast<unsigned>((nblk + 255) / 256);
   if (e == cudaSuccess) {
-    block_flag_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag);
+    block_flag_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, palette && ls <= 3 ? 1 : 0, flag);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) {
@@ -690,18 +739,21 @@ fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, i
   if (e == cudaSuccess) {
     e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, idx, static_cast<std::int64_t>(nblk + 1));
   }
-  if (e == cudaSuccess) e = cudaMemcpy(&n_sub, idx + nblk, 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&tot, idx + nblk, 8, cudaMemcpyDeviceToHost);
+  const std::uint64_t n_pal = tot & 0xFFFFFFFFull, n_sub = tot >> 32;
   if (e == cudaSuccess) {
     out->owned = true;
     e = cudaMalloc(&out->blocks, nblk * 4);
   }
   if (e == cudaSuccess) e = cudaMalloc(&out->sub, std::max<std::uint64_t>(n_sub, 1) << (2 * ls + 2));
+  if (e == cudaSuccess) e = cudaMalloc(&out->pal, std::max<std::uint64_t>(n_pal, 1) * palette_words(ls) * 4);
   if (e == cudaSuccess) {
-    block_write_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag, idx, out->blocks, out->sub);
+    block_write_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag, idx, out->blocks, out->sub,
+                                    out->pal);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  out->bytes = nblk * 4 + (n_sub << (2 * ls + 2));
+  out->bytes = nblk * 4 + (n_sub << (2 * ls + 2)) + n_pal * palette_words(ls) * 4;
   cudaFree(tmp);
   cudaFree(flag);
   cudaFree(idx);
@@ -762,8 +814,8 @@ fm_status build_approx(fm_index* ix) {
     }
   }
   if (st == FM_OK && e == cudaSuccess) {
-    st = fold_grid(fine, static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny), kBlockBudget, 4,
-                   &ix->agrid);
+    st = fold_grid(fine, static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny), kBlockBudget, 3,
+                   true, &ix->agrid);
     if (st == FM_OK && ix->agrid.ls == 0) {
       ix->agrid.owned = true;  // the approx copy itself is the block level
       fine = nullptr;
@@ -969,7 +1021,8 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   if (ix->device >= 0) {
     DeviceGuard guard(ix->device);
     const fm_status st = fold_grid(ix->d_grid, static_cast<int>(ix->g.nx),
-                                   static_cast<int>(ix->g.ny), kQueryBudget, kQueryMaxLs, &ix->qgrid);
+                                   static_cast<int>(ix->g.ny), kQueryBudget, kQueryMaxLs, false,
+                                   &ix->qgrid);
     if (st != FM_OK) {
       free_device(ix);
       delete ix;

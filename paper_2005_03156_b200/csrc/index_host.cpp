@@ -550,8 +550,11 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
                             std::to_string(ex * ey) +
                             " uniform-grid cells over this extent (limit 2^31)");
     }
-    nx = std::max(nx, static_cast<std::int64_t>(ex));
-    ny = std::max(ny, static_cast<std::int64_t>(ey));
+    // auto resolution: exactly what epsilon needs (the reference's approx
+    // cover stops refining there too); explicit resolutions are only raised
+    const bool explicit_res = (o.nx > 0 && o.ny > 0) || o.cells_per_polygon > 0.0;
+    nx = explicit_res ? std::max(nx, static_cast<std::int64_t>(ex)) : static_cast<std::int64_t>(ex);
+    ny = explicit_res ? std::max(ny, static_cast<std::int64_t>(ey)) : static_cast<std::int64_t>(ey);
   }
   if (nx * ny > (std::int64_t{1} << 31)) throw InvalidArgument("grid too large");
   g.nx = nx;

@@ -25,6 +25,7 @@ struct KParams {
   // first level stays L2-resident.
   const std::uint32_t* __restrict__ blocks;
   const std::uint32_t* __restrict__ sub;
+  const std::uint32_t* __restrict__ pal;      // palette sub-blocks (kRecordBit | kHalfBit | k)
   double gx0, gy0, inv_w, inv_h;
   double ax0, ax1, ay0, ay1;  // acceptance box = padded domain intersect world box
   int nx, ny;
@@ -63,8 +64,20 @@ __device__ __forceinline__ std::uint32_t locate(const KParams& P, double px, dou
       __ldg(P.blocks + static_cast<std::size_t>(iy >> P.ls) * static_cast<std::size_t>(P.bnx) + (ix >> P.ls));
   if (P.ls == 0 || e == kEmpty || e < kRecordBit) return e;  // ls = 0: the flat grid itself
   const int m = (1 << P.ls) - 1;
-  return __ldg(P.sub + (static_cast<std::size_t>(e & ~kRecordBit) << (2 * P.ls)) + ((iy & m) << P.ls) +
-               (ix & m));
+  const int c = ((iy & m) << P.ls) + (ix & m);
+  if (e & kHalfBit) {  // palette sub-block: u32 value[3], 2-bit codes (ls <= 3)
+    const std::size_t k = e & kSlotIndexMask;
+    if (P.ls <= 2) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(P.pal) + k);
+      const std::uint32_t code = (v.w >> (2 * c)) & 3u;
+      return code == 0 ? v.x : (code == 1 ? v.y : v.z);
+    }
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(P.pal) + 2 * k);
+    const std::uint32_t w = __ldg(P.pal + 8 * k + 4 + (c >> 4));
+    const std::uint32_t code = (w >> (2 * (c & 15))) & 3u;
+    return code == 0 ? v.x : (code == 1 ? v.y : v.z);
+  }
+  return __ldg(P.sub + (static_cast<std::size_t>(e & ~kRecordBit) << (2 * P.ls)) + c);
 }
 
 struct WorkCount {

@@ -102,8 +102,10 @@ def test_approx_cover_params_and_resolution():
     assert s["approx_epsilon"] == eps
     assert np.hypot(s["cell_w"] + 2 * s["margin"], s["cell_h"] + 2 * s["margin"]) <= eps
     assert np.hypot(2 * s["cell_w"], 2 * s["cell_h"]) > eps  # not needlessly fine
-    exact = fastmap.build_index(soup, device=-1).stats()
-    assert s["nx"] * s["ny"] >= exact["nx"] * exact["ny"]
+    # an explicit resolution is only ever raised to meet epsilon
+    fine = fastmap.build_index(soup, fastmap.CoverParams(mode=fastmap.CoverMode.approx, epsilon=eps,
+                                                         nx=5000, ny=300), device=-1).stats()
+    assert fine["nx"] == 5000 and fine["ny"] == s["ny"]
     with pytest.raises(ValueError, match="needs .* cells"):  # bounded uniform grid
         fastmap.build_index(soup, fastmap.CoverParams(mode=fastmap.CoverMode.approx,
                                                       epsilon=1e-6), device=-1)

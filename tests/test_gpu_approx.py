@@ -36,8 +36,9 @@ def check_approx(soup, pts, got, want, eps, max_checks=4000):
 
 @pytest.mark.parametrize("name,eps,n", [("c1", 0.02, 1_000_000), ("c3mini", 0.02, 500_000),
                                         ("c4", 0.05, 300_000),
-                                        # fine grid > 48 MB: two-level (block + sub-block) cover
-                                        ("c1", 0.005, 1_000_000)])
+                                        # fine grid > 48 MB: two-level covers with 4x4
+                                        # and 8x8 blocks (palette + full sub-blocks)
+                                        ("c1", 0.005, 1_000_000), ("c1", 0.0025, 1_000_000)])
 def test_approx_error_bound_and_zero_tests(dev, name, eps, n):
     cfg = synth.config(name)
     soup = cfg.make_soup()
@@ -46,7 +47,7 @@ def test_approx_error_bound_and_zero_tests(dev, name, eps, n):
     st = idx.stats()
     assert st["approx_epsilon"] == eps and st["approx_grid_bytes"] > 0
     if st["grid_bytes"] > 48 << 20:
-        assert st["approx_grid_bytes"] < st["grid_bytes"]
+        assert st["approx_grid_bytes"] < st["grid_bytes"] and st["approx_block_log2"] >= 2
     assert np.hypot(st["cell_w"] + 2 * st["margin"], st["cell_h"] + 2 * st["margin"]) <= eps
     want = oracle.assign(soup, pts)
     d = torch.from_numpy(pts).to(dev)
