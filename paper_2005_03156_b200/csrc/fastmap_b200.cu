@@ -135,8 +135,7 @@ __global__ void __launch_bounds__(kAWarps * 32)
     std::uint32_t e[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) p[u] = pn[u];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) e[u] = fm::locate(P, p[u].x, p[u].y);
+    fm::locate_n<kU, true>(P, p, e);
     const std::uint64_t tn = t + nwarps;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -362,8 +361,7 @@ __global__ void __launch_bounds__(kXThreads)
       p[u] = i < n ? __ldcs(pts + i) : make_double2(NAN, NAN);
     }
     std::uint32_t e[kXU];
-#pragma unroll
-    for (int u = 0; u < kXU; ++u) e[u] = fm::locate(A, p[u].x, p[u].y);
+    fm::locate_n<kXU, false>(A, p, e);
 #pragma unroll
     for (int u = 0; u < kXU; ++u) {
       const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kXThreads;
@@ -379,29 +377,37 @@ __global__ void __launch_bounds__(kXThreads)
   }
 }
 
-// Per block of S x S fine cells: 0 when its answers are all equal, 1 when
-// a palette sub-block holds it (<= 3 distinct values, palette allowed:
-// ls in [1, 3]), 1 << 32 when a full sub-block does.  The exclusive scan of
-// these u64 flags numbers both kinds at once.
+// Per block of S x S fine cells: 0 when its entries are all equal, 1 when a
+// compact sub-block holds it, 1 << 32 when a full sub-block does.  The
+// exclusive scan of these u64 flags numbers both kinds at once.  Compact
+// kinds (`mode`): 1 = approx palette (<= 3 distinct answers, ls <= 3);
+// 2 = exact compact (<= 3 distinct hit/empty entries plus <= 12 phase-1
+// slot references with consecutive indices, ls <= 2 -- see renumber_slots).
 __global__ void __launch_bounds__(256)
     block_flag_kernel(const std::uint32_t* __restrict__ fine, int nx, int ny, int bnx, int bny,
-                      int ls, int palette, unsigned long long* __restrict__ flag) {
+                      int ls, int mode, std::uint64_t n1, unsigned long long* __restrict__ flag) {
   const std::uint64_t b = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= static_cast<std::uint64_t>(bnx) * bny) return;
   const int by = static_cast<int>(b / bnx), bx = static_cast<int>(b - static_cast<std::uint64_t>(by) * bnx);
   const int S = 1 << ls;
   const int x0 = bx << ls, y0 = by << ls;
   std::uint32_t v[3];
-  int nd = 0;
-  bool rec = false;
+  int nd = 0, nrec = 0;
+  bool far_rec = false;
+  std::uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
   for (int j = 0; j < S; ++j) {
     for (int i = 0; i < S; ++i) {
       const bool in = y0 + j < ny && x0 + i < nx;
-      const std::uint32_t x = in ? fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] : fm::kEmpty;
-      // a slot reference must sit in a full sub-block (record-flagged block
-      // entries are sub-block pointers)
-      if (x != fm::kEmpty && x >= fm::kRecordBit) rec = true;
-      if (!in && j + i > 0) continue;  // outside cells never take part in uniformity
+      if (!in && j + i > 0) continue;  // outside cells never take part
+      const std::uint32_t x = fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i];
+      if (x != fm::kEmpty && x >= fm::kRecordBit) {  // slot reference
+        const std::uint32_t k = x & fm::kSlotIndexMask;
+        ++nrec;
+        far_rec |= k >= n1;
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+        continue;
+      }
       bool seen = false;
       for (int q = 0; q < nd && q < 3; ++q) seen |= v[q] == x;
       if (!seen) {
@@ -411,9 +417,16 @@ __global__ void __launch_bounds__(256)
     }
   }
   unsigned long long f;
-  if (nd == 1 && !rec) f = 0ull;
-  else if (palette && !rec && nd <= 3) f = 1ull;
-  else f = 1ull << 32;
+  if (nrec == 0 && nd == 1) {
+    f = 0ull;
+  } else if (mode == 1 && nrec == 0 && nd <= 3 && ls <= 3) {
+    f = 1ull;
+  } else if (mode == 2 && ls <= 2 && nd <= 3 && nrec <= 12 && !far_rec &&
+             (nrec == 0 || kmax - kmin + 1 == static_cast<std::uint32_t>(nrec))) {
+    f = 1ull;
+  } else {
+    f = 1ull << 32;
+  }
   flag[b] = f;
 }
 
@@ -424,7 +437,7 @@ __host__ __device__ constexpr int palette_words(int ls) { return ls <= 2 ? 4 : 8
 
 __global__ void __launch_bounds__(256)
     block_write_kernel(const std::uint32_t* __restrict__ fine, int nx, int ny, int bnx, int bny,
-                       int ls, const unsigned long long* __restrict__ flag,
+                       int ls, int mode, const unsigned long long* __restrict__ flag,
                        const unsigned long long* __restrict__ idx, std::uint32_t* __restrict__ blocks,
                        std::uint32_t* __restrict__ sub, std::uint32_t* __restrict__ pal) {
   const std::uint64_t b = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -435,6 +448,49 @@ __global__ void __launch_bounds__(256)
   const unsigned long long f = flag[b];
   if (!f) {
     blocks[b] = fine[static_cast<std::size_t>(y0) * nx + x0];
+    return;
+  }
+  if (f == 1ull && mode == 2) {  // exact compact sub-block (32 bytes)
+    const unsigned long long k = idx[b] & 0xFFFFFFFFull;
+    blocks[b] = fm::kRecordBit | fm::kHalfBit | static_cast<std::uint32_t>(k);
+    std::uint32_t* dst = pal + k * 8;
+    std::uint32_t v[3] = {fm::kEmpty, fm::kEmpty, fm::kEmpty};
+    int nd = 0;
+    std::uint32_t base = 0xFFFFFFFFu;
+    for (int j = 0; j < S; ++j) {
+      for (int i = 0; i < S; ++i) {
+        if (y0 + j >= ny || x0 + i >= nx) continue;
+        const std::uint32_t x = fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i];
+        if (x != fm::kEmpty && x >= fm::kRecordBit) base = min(base, x & fm::kSlotIndexMask);
+      }
+    }
+    std::uint32_t codes[2] = {0u, 0u}, half = 0u;
+    for (int j = 0; j < S; ++j) {
+      for (int i = 0; i < S; ++i) {
+        const bool in = y0 + j < ny && x0 + i < nx;
+        const std::uint32_t x = in ? fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] : fm::kEmpty;
+        std::uint32_t code;
+        if (in && x != fm::kEmpty && x >= fm::kRecordBit) {
+          const std::uint32_t off = (x & fm::kSlotIndexMask) - base;
+          code = 4u + off;
+          if (x & fm::kHalfBit) half |= 1u << off;
+        } else {
+          code = 0;
+          while (static_cast<int>(code) < nd && v[code] != x) ++code;
+          if (static_cast<int>(code) == nd) v[nd++] = x;
+        }
+        const int c = (j << ls) + i;
+        codes[c >> 3] |= code << (4 * (c & 7));
+      }
+    }
+    dst[0] = v[0];
+    dst[1] = v[1];
+    dst[2] = v[2];
+    dst[3] = base;
+    dst[4] = codes[0];
+    dst[5] = codes[1];
+    dst[6] = half;
+    dst[7] = 0;
     return;
   }
   if (f == 1ull) {  // palette
@@ -470,6 +526,50 @@ __global__ void __launch_bounds__(256)
       dst[(j << ls) + i] = in ? fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] : fm::kEmpty;
     }
   }
+}
+
+// Block-major renumbering of the phase-1 slots (renumber_slots): position p
+// walks blocks of 2^ls x 2^ls cells in row-major block order, cells
+// row-major inside each block.
+__device__ __forceinline__ bool block_major_cell(std::uint64_t p, int ls, int bnx, int nx, int ny,
+                                                 std::uint64_t* cell) {
+  const std::uint64_t b = p >> (2 * ls);
+  const int o = static_cast<int>(p & ((1ull << (2 * ls)) - 1));
+  const int by = static_cast<int>(b / bnx), bx = static_cast<int>(b - static_cast<std::uint64_t>(by) * bnx);
+  const int x = (bx << ls) + (o & ((1 << ls) - 1)), y = (by << ls) + (o >> ls);
+  if (x >= nx || y >= ny) return false;
+  *cell = static_cast<std::uint64_t>(y) * nx + x;
+  return true;
+}
+
+__global__ void __launch_bounds__(256)
+    renum_flag_kernel(const std::uint32_t* __restrict__ grid, int nx, int ny, int bnx, int ls,
+                      std::uint64_t n_pos, std::uint64_t n1, std::uint32_t* __restrict__ flag) {
+  const std::uint64_t p = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n_pos) return;
+  std::uint64_t c;
+  std::uint32_t f = 0;
+  if (block_major_cell(p, ls, bnx, nx, ny, &c)) {
+    const std::uint32_t e = grid[c];
+    f = (e != fm::kEmpty && e >= fm::kRecordBit && (e & fm::kSlotIndexMask) < n1) ? 1u : 0u;
+  }
+  flag[p] = f;
+}
+
+__global__ void __launch_bounds__(256)
+    renum_apply_kernel(std::uint32_t* __restrict__ grid, int nx, int ny, int bnx, int ls,
+                       std::uint64_t n_pos, const std::uint32_t* __restrict__ flag,
+                       const std::uint32_t* __restrict__ idx, const uint4* __restrict__ old_slots,
+                       uint4* __restrict__ new_slots) {
+  const std::uint64_t p = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n_pos || !flag[p]) return;
+  std::uint64_t c;
+  block_major_cell(p, ls, bnx, nx, ny, &c);
+  const std::uint32_t e = grid[c];
+  const std::uint64_t ko = e & fm::kSlotIndexMask, kn = idx[p];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) new_slots[kn * 8 + q] = old_slots[ko * 8 + q];
+  grid[c] = (e & ~fm::kSlotIndexMask) | static_cast<std::uint32_t>(kn);
 }
 
 // Boundary cells of the exact grid -> (centre point, cell) lists.
@@ -546,8 +646,9 @@ int resident_blocks(int device, const void* kernel, int block, int smem) {
 struct Folded {
   std::uint32_t* blocks = nullptr;
   std::uint32_t* sub = nullptr;
-  std::uint32_t* pal = nullptr;  // palette sub-blocks (approx covers)
+  std::uint32_t* pal = nullptr;  // compact sub-blocks (approx palettes / exact compact)
   int ls = 0, bnx = 0, bny = 0;
+  int compact = 0;               // 1: `pal` holds exact compact sub-blocks
   bool owned = false;
   std::uint64_t bytes = 0;
   void release() {
@@ -603,6 +704,7 @@ fm::KParams kparams(const fm_index* ix) {
   P.blocks = ix->qgrid.blocks;
   P.sub = ix->qgrid.sub;
   P.pal = ix->qgrid.pal;
+  P.compact = ix->qgrid.compact;
   P.bnx = ix->qgrid.bnx;
   P.ls = ix->qgrid.ls;
   return P;
@@ -656,6 +758,7 @@ fm_status launch_approx_t(const fm_index* ix, const double2* pts, std::uint64_t 
   A.blocks = ix->agrid.blocks;
   A.sub = ix->agrid.sub;
   A.pal = ix->agrid.pal;
+  A.compact = ix->agrid.compact;
   A.bnx = ix->agrid.bnx;
   A.ls = ix->agrid.ls;
   auto k = approx_kernel<kHist, kCount>;
@@ -700,16 +803,24 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
 
 // Fold a flat nx x ny grid into blocks (KParams): the smallest ls <= max_ls
 // whose block level fits `budget` bytes.  ls = 0 aliases the flat grid.
-fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, int max_ls,
-                    bool palette, Folded* out) {
+int fold_ls(int nx, int ny, std::uint64_t budget, int max_ls) {
   int ls = 0;
   while (ls < max_ls && static_cast<std::uint64_t>((nx + (1 << ls) - 1) >> ls) *
                                 static_cast<std::uint64_t>((ny + (1 << ls) - 1) >> ls) * 4 > budget) {
     ++ls;
   }
+  return ls;
+}
+
+// mode: 0 = full sub-blocks only, 1 = approx palettes, 2 = exact compact
+// sub-blocks (slot references < n1 must be numbered block-major).
+fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, int max_ls,
+                    int mode, std::uint64_t n1, Folded* out) {
+  const int ls = fold_ls(nx, ny, budget, max_ls);
   const int bnx = (nx + (1 << ls) - 1) >> ls, bny = (ny + (1 << ls) - 1) >> ls;
   const std::uint64_t nblk = static_cast<std::uint64_t>(bnx) * bny;
   out->ls = ls;
+  out->compact = mode == 2 ? 1 : 0;
   out->bnx = bnx;
   out->bny = bny;
   if (ls == 0) {
@@ -729,7 +840,7 @@ fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, i
   if (e == cudaSuccess) e = cudaMemset(flag + nblk, 0, 8);
   const unsigned g1 = static_cast<unsigned>((nblk + 255) / 256);
   if (e == cudaSuccess) {
-    block_flag_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, palette && ls <= 3 ? 1 : 0, flag);
+    block_flag_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, mode, n1, flag);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) {
@@ -746,18 +857,71 @@ fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, i
     e = cudaMalloc(&out->blocks, nblk * 4);
   }
   if (e == cudaSuccess) e = cudaMalloc(&out->sub, std::max<std::uint64_t>(n_sub, 1) << (2 * ls + 2));
-  if (e == cudaSuccess) e = cudaMalloc(&out->pal, std::max<std::uint64_t>(n_pal, 1) * palette_words(ls) * 4);
+  const int pw = mode == 2 ? 8 : palette_words(ls);
+  if (e == cudaSuccess) e = cudaMalloc(&out->pal, std::max<std::uint64_t>(n_pal, 1) * pw * 4);
   if (e == cudaSuccess) {
-    block_write_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, flag, idx, out->blocks, out->sub,
-                                    out->pal);
+    block_write_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, mode, flag, idx, out->blocks,
+                                    out->sub, out->pal);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  out->bytes = nblk * 4 + (n_sub << (2 * ls + 2)) + n_pal * palette_words(ls) * 4;
+  out->bytes = nblk * 4 + (n_sub << (2 * ls + 2)) + n_pal * pw * 4;
   cudaFree(tmp);
   cudaFree(flag);
   cudaFree(idx);
   if (e != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("grid folding: ") + cudaGetErrorString(e));
+  return FM_OK;
+}
+
+// Renumber the phase-1 slots in block-major order for blocks of 2^ls cells,
+// so every block's phase-1 slots are consecutive and its sub-block can name
+// them as base + offset (exact compact sub-blocks).  Phase-2 slots (split /
+// overflow subtrees, referenced from split slots) keep their numbers.
+fm_status renumber_slots(fm_index* ix, int ls) {
+  const std::uint64_t n1 = ix->host.n_phase1_slots;
+  if (ls == 0 || n1 == 0) return FM_OK;
+  const int nx = static_cast<int>(ix->g.nx), ny = static_cast<int>(ix->g.ny);
+  const int bnx = (nx + (1 << ls) - 1) >> ls, bny = (ny + (1 << ls) - 1) >> ls;
+  const std::uint64_t n_pos = (static_cast<std::uint64_t>(bnx) * bny) << (2 * ls);
+  std::uint32_t *flag = nullptr, *idx = nullptr;
+  std::uint8_t* fresh = nullptr;
+  void* tmp = nullptr;
+  std::size_t tmp_bytes = 0;
+  cudaError_t e = cudaMalloc(&flag, n_pos * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&idx, n_pos * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&fresh, ix->slots_len);
+  const unsigned g1 = static_cast<unsigned>((n_pos + 255) / 256);
+  if (e == cudaSuccess) {
+    renum_flag_kernel<<<g1, 256>>>(ix->d_grid, nx, ny, bnx, ls, n_pos, n1, flag);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, idx, static_cast<std::int64_t>(n_pos));
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes + 16);
+  if (e == cudaSuccess) {
+    e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, idx, static_cast<std::int64_t>(n_pos));
+  }
+  if (e == cudaSuccess) {
+    renum_apply_kernel<<<g1, 256>>>(ix->d_grid, nx, ny, bnx, ls, n_pos, flag, idx,
+                                    reinterpret_cast<const uint4*>(ix->d_slots),
+                                    reinterpret_cast<uint4*>(fresh));
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && ix->slots_len > n1 * fm::kSlotBytes) {  // phase-2 tail
+    e = cudaMemcpy(fresh + n1 * fm::kSlotBytes, ix->d_slots + n1 * fm::kSlotBytes,
+                   ix->slots_len - n1 * fm::kSlotBytes, cudaMemcpyDeviceToDevice);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(tmp);
+  cudaFree(flag);
+  cudaFree(idx);
+  if (e != cudaSuccess) {
+    cudaFree(fresh);
+    return set_err(FM_ERR_CUDA, std::string("slot renumbering: ") + cudaGetErrorString(e));
+  }
+  cudaFree(ix->d_slots);
+  ix->d_slots = fresh;
   return FM_OK;
 }
 
@@ -815,7 +979,7 @@ fm_status build_approx(fm_index* ix) {
   }
   if (st == FM_OK && e == cudaSuccess) {
     st = fold_grid(fine, static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny), kBlockBudget, 3,
-                   true, &ix->agrid);
+                   1, 0, &ix->agrid);
     if (st == FM_OK && ix->agrid.ls == 0) {
       ix->agrid.owned = true;  // the approx copy itself is the block level
       fine = nullptr;
@@ -1020,9 +1184,13 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   }
   if (ix->device >= 0) {
     DeviceGuard guard(ix->device);
-    const fm_status st = fold_grid(ix->d_grid, static_cast<int>(ix->g.nx),
-                                   static_cast<int>(ix->g.ny), kQueryBudget, kQueryMaxLs, false,
-                                   &ix->qgrid);
+    const int qls = fold_ls(static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny), kQueryBudget,
+                            kQueryMaxLs);
+    fm_status st = renumber_slots(ix, qls);
+    if (st == FM_OK) {
+      st = fold_grid(ix->d_grid, static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny),
+                     kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots, &ix->qgrid);
+    }
     if (st != FM_OK) {
       free_device(ix);
       delete ix;

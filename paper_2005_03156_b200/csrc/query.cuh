@@ -30,6 +30,7 @@ struct KParams {
   double ax0, ax1, ay0, ay1;  // acceptance box = padded domain intersect world box
   int nx, ny;
   int bnx, ls;                // blocks per row, log2 block side
+  int compact;                // `pal` format: 0 approx palettes, 1 exact compact sub-blocks
 };
 
 __device__ __forceinline__ const std::uint8_t* slot_ptr(const KParams& P, std::uint32_t e) {
@@ -52,32 +53,60 @@ __device__ __forceinline__ std::uint32_t edge_bit(double px, double py, double a
   return (ly < py && py <= hy && ray_crosses(px, py, lx, ly, hx, hy)) ? 1u : 0u;
 }
 
-// Grid entry for p, or kEmpty when p is outside the acceptance box (which
-// also rejects NaN: every comparison with NaN is false).
-__device__ __forceinline__ std::uint32_t locate(const KParams& P, double px, double py) {
-  if (!(px >= P.ax0 && px <= P.ax1 && py >= P.ay0 && py <= P.ay1)) return kEmpty;
-  int ix = static_cast<int>(__dmul_rn(__dsub_rn(px, P.gx0), P.inv_w));
-  int iy = static_cast<int>(__dmul_rn(__dsub_rn(py, P.gy0), P.inv_h));
-  ix = min(max(ix, 0), P.nx - 1);
-  iy = min(max(iy, 0), P.ny - 1);
-  const std::uint32_t e =
-      __ldg(P.blocks + static_cast<std::size_t>(iy >> P.ls) * static_cast<std::size_t>(P.bnx) + (ix >> P.ls));
-  if (P.ls == 0 || e == kEmpty || e < kRecordBit) return e;  // ls = 0: the flat grid itself
+// Grid entries of kN points (kEmpty outside the acceptance box, which also
+// rejects NaN: every comparison with NaN is false), phased so every point's
+// loads are in flight together: block entries first, then the second level
+// as predicated loads rather than divergent branches, then the decode.
+// kExact: exact grid (compact sub-blocks: two 16-byte loads;
+// full: one 4-byte load); else an approx cover (palettes: one 16-byte load,
+// or two for 8x8 blocks; full: one 4-byte load).
+template <int kN, bool kExact>
+__device__ __forceinline__ void locate_n(const KParams& P, const double2 (&p)[kN],
+                                         std::uint32_t (&e)[kN]) {
+  std::uint32_t be[kN];
+  int cc[kN];
   const int m = (1 << P.ls) - 1;
-  const int c = ((iy & m) << P.ls) + (ix & m);
-  if (e & kHalfBit) {  // palette sub-block: u32 value[3], 2-bit codes (ls <= 3)
-    const std::size_t k = e & kSlotIndexMask;
-    if (P.ls <= 2) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(P.pal) + k);
-      const std::uint32_t code = (v.w >> (2 * c)) & 3u;
-      return code == 0 ? v.x : (code == 1 ? v.y : v.z);
-    }
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(P.pal) + 2 * k);
-    const std::uint32_t w = __ldg(P.pal + 8 * k + 4 + (c >> 4));
-    const std::uint32_t code = (w >> (2 * (c & 15))) & 3u;
-    return code == 0 ? v.x : (code == 1 ? v.y : v.z);
+#pragma unroll
+  for (int u = 0; u < kN; ++u) {
+    const double px = p[u].x, py = p[u].y;
+    const bool in = px >= P.ax0 && px <= P.ax1 && py >= P.ay0 && py <= P.ay1;
+    int ix = in ? static_cast<int>(__dmul_rn(__dsub_rn(px, P.gx0), P.inv_w)) : 0;
+    int iy = in ? static_cast<int>(__dmul_rn(__dsub_rn(py, P.gy0), P.inv_h)) : 0;
+    ix = min(max(ix, 0), P.nx - 1);
+    iy = min(max(iy, 0), P.ny - 1);
+    cc[u] = ((iy & m) << P.ls) + (ix & m);
+    be[u] = in ? __ldg(P.blocks + static_cast<std::size_t>(iy >> P.ls) * static_cast<std::size_t>(P.bnx) +
+                       (ix >> P.ls))
+               : kEmpty;
   }
-  return __ldg(P.sub + (static_cast<std::size_t>(e & ~kRecordBit) << (2 * P.ls)) + c);
+  const uint4* pal4 = reinterpret_cast<const uint4*>(P.pal);
+  const bool two = kExact || P.ls == 3;  // 32-byte compact sub-blocks
+#pragma unroll
+  for (int u = 0; u < kN; ++u) {
+    const std::uint32_t x = be[u];
+    const bool rec = P.ls != 0 && x != kEmpty && x >= kRecordBit;
+    const bool cmp = rec && (x & kHalfBit);
+    const std::size_t k = x & kSlotIndexMask;
+    uint4 a = make_uint4(0u, 0u, 0u, 0u), b = a;
+    std::uint32_t f = x;
+    if (cmp) a = __ldg(pal4 + (two ? 2 * k : k));
+    if (cmp && two) b = __ldg(pal4 + 2 * k + 1);
+    if (rec && !cmp) f = __ldg(P.sub + (k << (2 * P.ls)) + cc[u]);
+    const int c = cc[u];
+    std::uint32_t ce;
+    if (kExact) {  // value[3], slot base, 4-bit codes[16], half mask
+      const std::uint32_t code = ((c < 8 ? b.x : b.y) >> (4 * (c & 7))) & 15u;
+      const std::uint32_t off = (code - 4u) & 31u;
+      ce = code < 3u ? (code == 0 ? a.x : (code == 1 ? a.y : a.z))
+                     : (kRecordBit | (((b.z >> off) & 1u) ? kHalfBit : 0u) | (a.w + off));
+    } else {  // value[3], 2-bit codes
+      const std::uint32_t wsel = (c >> 4) == 0 ? b.x : ((c >> 4) == 1 ? b.y : ((c >> 4) == 2 ? b.z : b.w));
+      const std::uint32_t word = two ? wsel : a.w;
+      const std::uint32_t code = (word >> (2 * (c & 15))) & 3u;
+      ce = code == 0 ? a.x : (code == 1 ? a.y : a.z);
+    }
+    e[u] = cmp ? ce : f;
+  }
 }
 
 struct WorkCount {

@@ -291,15 +291,17 @@ class CellIndex:
         return out
 
 
-def build_index(soup: Soup, params: Optional[CoverParams] = None, device: int = 0) -> CellIndex:
+def build_index(soup: Soup, params: Optional[CoverParams] = None, device: int = 0,
+                on_gpu: bool = True) -> CellIndex:
     """fm_index_build over a soup.  ``device=-1`` builds a host-only index
-    (inspection/export only; queries on it raise)."""
+    (inspection/export only; queries on it raise).  ``on_gpu=False`` runs the
+    host builder and uploads the result (same arrays as the GPU builder)."""
     params = params or CoverParams()
     validate_cover_params(params)
     s = soup.contiguous()
     bp = N.BuildParams(cells_per_polygon=float(params.cells_per_polygon),
                        nx=int(params.nx), ny=int(params.ny), margin=float(params.margin),
-                       device=int(device), build_on_gpu=1 if device >= 0 else 0,
+                       device=int(device), build_on_gpu=1 if (device >= 0 and on_gpu) else 0,
                        threads=int(params.threads),
                        approx_epsilon=float(params.epsilon) if params.mode == CoverMode.approx
                        else 0.0)

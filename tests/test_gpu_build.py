@@ -13,8 +13,10 @@ from paper_2005_03156_b200 import fastmap, synth  # noqa: E402
 
 
 def both(soup, **params):
+    """Host builder and GPU builder, both into device indexes (so both get the
+    same query-layout pass: block-major phase-1 slot numbering)."""
     p = fastmap.CoverParams(**params)
-    h = fastmap.build_index(soup, p, device=-1)
+    h = fastmap.build_index(soup, p, device=0, on_gpu=False)
     g = fastmap.build_index(soup, p, device=0)
     return h, g
 
@@ -29,7 +31,7 @@ def assert_identical(h, g):
     assert g.stats()["built_on_gpu"] == 1 and h.stats()["built_on_gpu"] == 0
 
 
-@pytest.mark.parametrize("name,m", [("c1", 0), ("c1", 7), ("c2", 0), ("c4", 0), ("c3mini", 0)])
+@pytest.mark.parametrize("name,m", [("c1", 0), ("c1", 7), ("c2", 0), ("c4", 0), ("c3mini", 20)])
 def test_gpu_build_identical_to_host(name, m):
     cfg = synth.config(name)
     soup = cfg.make_soup()
@@ -54,3 +56,21 @@ def test_c3mini_parity_on_gpu_built_index():
     idx = fastmap.build_index(soup, device=0)
     got = idx.project(torch.from_numpy(pts).cuda()).cpu().numpy()
     assert np.array_equal(got, oracle.assign(soup, pts))
+
+
+def test_block_major_renumbering_preserves_the_index():
+    """The device-side slot renumbering (block-major phase-1 order) is a pure
+    relabelling: walking the host-only (row-major) and the device index
+    gives the same answers."""
+    import index_walk
+    cfg = synth.config("c2")
+    soup = cfg.make_soup()
+    p = fastmap.CoverParams(cells_per_polygon=14)
+    h = fastmap.build_index(soup, p, device=-1)
+    g = fastmap.build_index(soup, p, device=0)
+    assert g.stats()["query_block_log2"] >= 1
+    pts = cfg.make_points(200_000, offset=31)
+    wh = index_walk.walk(h.export(), pts)
+    wg = index_walk.walk(g.export(), pts)
+    assert np.array_equal(wh, wg)
+    assert np.array_equal(g.project(torch.from_numpy(pts).cuda()).cpu().numpy(), wh)
