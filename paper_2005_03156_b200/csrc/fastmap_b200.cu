@@ -147,7 +147,13 @@ __global__ void __launch_bounds__(kAWarps * 32)
       const std::uint64_t i = base + u * 32 + lane;
       const bool valid = i < n;
       const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
-      if (valid && !is_rec) emit<kHist>(out, hist, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
+      // every lane stores (boundary lanes a placeholder the resolve pass
+      // overwrites), so output sectors are written whole, not masked
+      if (valid) {
+        const int id = is_rec ? -2 : (e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
+        __stcs(out + i, id);
+        if (kHist && id >= 0) atomicAdd(hist + id, 1ull);
+      }
       const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec);
       if (is_rec) {  // streaming stores: the resolve pass reads these much later
         double* d = reinterpret_cast<double*>(my + cnt + __popc(b & lt_mask));
