@@ -821,7 +821,7 @@ int fold_ls(int nx, int ny, std::uint64_t budget, int max_ls) {
 // mode: 0 = full sub-blocks only, 1 = approx palettes, 2 = exact compact
 // sub-blocks (slot references < n1 must be numbered block-major).
 fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, int max_ls,
-                    int mode, std::uint64_t n1, Folded* out) {
+                    int mode, std::uint64_t n1, double max_ratio, Folded* out) {
   const int ls = fold_ls(nx, ny, budget, max_ls);
   const int bnx = (nx + (1 << ls) - 1) >> ls, bny = (ny + (1 << ls) - 1) >> ls;
   const std::uint64_t nblk = static_cast<std::uint64_t>(bnx) * bny;
@@ -858,6 +858,25 @@ fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, i
   }
   if (e == cudaSuccess) e = cudaMemcpy(&tot, idx + nblk, 8, cudaMemcpyDeviceToHost);
   const std::uint64_t n_pal = tot & 0xFFFFFFFFull, n_sub = tot >> 32;
+  const int pw0 = mode == 2 ? 8 : palette_words(ls);
+  const double folded = static_cast<double>(nblk * 4 + (n_sub << (2 * ls + 2)) + n_pal * pw0 * 4);
+  if (e == cudaSuccess && folded > max_ratio * 4.0 * nx * static_cast<double>(ny)) {
+    // the fold would not shrink the grid enough to pay for its second
+    // gather (c3: 67% boundary cells): query the flat grid directly
+    cudaFree(tmp);
+    cudaFree(flag);
+    cudaFree(idx);
+    out->ls = 0;
+    out->bnx = nx;
+    out->bny = ny;
+    out->compact = 0;
+    out->blocks = fine;
+    out->owned = false;
+    FM_CUDA(cudaMalloc(&out->sub, 64));
+    FM_CUDA(cudaMalloc(&out->pal, 64));
+    out->bytes = static_cast<std::uint64_t>(nx) * ny * 4;
+    return FM_OK;
+  }
   if (e == cudaSuccess) {
     out->owned = true;
     e = cudaMalloc(&out->blocks, nblk * 4);
@@ -938,6 +957,8 @@ constexpr std::uint64_t kQueryBudget = std::uint64_t{32} << 20;
 #define FM_QUERY_MAX_LS 2
 #endif
 constexpr int kQueryMaxLs = FM_QUERY_MAX_LS;
+// ...and only when the folded copy is at most this fraction of the flat grid
+constexpr double kQueryMaxRatio = 0.75;
 
 // The approx cover: copy the exact grid, query every boundary cell's centre
 // through the exact path, write the deemed leaves, then fold the fine grid
@@ -985,7 +1006,7 @@ fm_status build_approx(fm_index* ix) {
   }
   if (st == FM_OK && e == cudaSuccess) {
     st = fold_grid(fine, static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny), kBlockBudget, 3,
-                   1, 0, &ix->agrid);
+                   1, 0, 1e30, &ix->agrid);
     if (st == FM_OK && ix->agrid.ls == 0) {
       ix->agrid.owned = true;  // the approx copy itself is the block level
       fine = nullptr;
@@ -1195,7 +1216,8 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
     fm_status st = renumber_slots(ix, qls);
     if (st == FM_OK) {
       st = fold_grid(ix->d_grid, static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny),
-                     kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots, &ix->qgrid);
+                     kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots, kQueryMaxRatio,
+                     &ix->qgrid);
     }
     if (st != FM_OK) {
       free_device(ix);

@@ -65,11 +65,10 @@ def test_block_major_renumbering_preserves_the_index():
     import index_walk
     cfg = synth.config("c2")
     soup = cfg.make_soup()
-    p = fastmap.CoverParams(cells_per_polygon=14)
-    h = fastmap.build_index(soup, p, device=-1)
-    g = fastmap.build_index(soup, p, device=0)
-    assert g.stats()["query_block_log2"] >= 1
-    pts = cfg.make_points(200_000, offset=31)
+    h = fastmap.build_index(soup, device=-1)
+    g = fastmap.build_index(soup, device=0)
+    assert g.stats()["query_block_log2"] == 2  # 4x4 blocks, compact sub-blocks
+    pts = cfg.make_points(100_000, offset=31)
     wh = index_walk.walk(h.export(), pts)
     wg = index_walk.walk(g.export(), pts)
     assert np.array_equal(wh, wg)
