@@ -39,6 +39,9 @@ fm_status set_err(fm_status s, const std::string& msg) {
 #ifndef FM_KU
 #define FM_KU 2
 #endif
+#ifndef FM_AMINB
+#define FM_AMINB 6
+#endif
 #ifndef FM_BWARPS
 #define FM_BWARPS 8
 #endif
@@ -110,7 +113,7 @@ __device__ __forceinline__ void emit(int* __restrict__ out, unsigned long long* 
 
 
 template <bool kHist, bool kCount>
-__global__ void __launch_bounds__(kAWarps * 32)
+__global__ void __launch_bounds__(kAWarps * 32, FM_AMINB)
     stream_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
                   int* __restrict__ out, unsigned long long* __restrict__ hist,
                   QItem* __restrict__ q, std::uint32_t* __restrict__ qcount,
