@@ -191,6 +191,48 @@ fm_status fm_index_export(const fm_index* index, uint32_t* grid, uint64_t* grid_
 /* Device the index lives on. */
 int fm_index_device(const fm_index* index);
 
+/* ---- artifacts and IO ---------------------- */
+
+/* Index persistence, the FMCI save/load analogue (cell_index.hpp:641-726):
+ * a built index (grid, slot and overflow arenas, stats) to one file, and
+ * back onto `device` (-1 = host-only) without rebuilding.  Errors are
+ * FM_ERR_RUNTIME for unopenable, truncated or foreign files (bad magic or
+ * version), like the reference's loaders. */
+fm_status fm_index_save(const fm_index* index, const char* path);
+fm_status fm_index_load(const char* path, int device, fm_index** out_index);
+
+/* An FMCB region hierarchy (load_hierarchy, hierarchy.hpp:204-223) flattened
+ * to its leaves in collect_leaves order (hierarchy.hpp:76-91): the polygon
+ * soup fm_index_build takes, each leaf's (state, county, block) indices and
+ * its 12-character FIPS code.  FM_ERR_RUNTIME for bad magic / version,
+ * truncation, corrupt ring tables or count mismatches; FM_ERR_INVALID_ARGUMENT
+ * for rings with < 3 vertices (geometry.hpp:75-77). */
+typedef struct fm_hierarchy fm_hierarchy;
+fm_status fm_hierarchy_load(const char* path, fm_hierarchy** out);
+void fm_hierarchy_destroy(fm_hierarchy* h);
+fm_status fm_hierarchy_sizes(const fm_hierarchy* h, uint64_t* n_states, uint64_t* n_counties,
+                             uint64_t* n_leaves, uint64_t* n_rings, uint64_t* n_vertices);
+/* Copies into caller buffers sized by fm_hierarchy_sizes (any may be NULL):
+ * vertex_lonlat 2*n_vertices, ring_offsets n_rings+1, poly_ring_offsets
+ * n_leaves+1, scb 3*n_leaves, fips12 12*n_leaves bytes (not terminated). */
+fm_status fm_hierarchy_leaves(const fm_hierarchy* h, double* vertex_lonlat, uint64_t* ring_offsets,
+                              uint64_t* poly_ring_offsets, uint32_t* scb, char* fips12);
+/* fm_index_build over the hierarchy's leaves. */
+fm_status fm_index_build_hierarchy(const fm_hierarchy* h, const fm_build_params* params,
+                                   fm_index** out_index);
+
+/* Raw little-endian f64 (lon, lat) pairs (read_points_f64, io.hpp:154-167).
+ * Two-call protocol: lonlat = NULL -> *n = point count; else *n is the
+ * buffer capacity in points and receives the count read. */
+fm_status fm_read_points_f64(const char* path, double* lonlat, uint64_t* n);
+
+/* The assignment CSV of the reference CLI (tools/fastmap.cpp:288-301):
+ * header "idx,lon,lat,fips", one row per finite input point (non-finite rows
+ * are skipped and keep their input index), coordinates as %.17g
+ * (io.hpp:115-119), the leaf's FIPS code or an empty field for -1. */
+fm_status fm_write_assign_csv(const char* path, const double* lonlat, uint64_t n, const int32_t* ids,
+                              const fm_hierarchy* h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -185,6 +185,19 @@ inline AssignmentResult query(const CellIndex& index, const RegionHierarchy& h,
   return query_leaves(index, leaves, points, mode);
 }
 
+/// Index persistence (the FMCI save/load analogue, cell_index.hpp:641-726).
+inline void save_index(const CellIndex& index, const std::string& path) {
+  detail::check(fm_index_save(index.get(), path.c_str()), "fm_index_save");
+}
+
+inline CellIndex load_index(const std::string& path, int device = 0) {
+  fm_index* h = nullptr;
+  detail::check(fm_index_load(path.c_str(), device, &h), "fm_index_load");
+  fm_index_stats s{};
+  detail::check(fm_index_stats_get(h, &s), "fm_index_stats_get");
+  return CellIndex(h, static_cast<std::size_t>(s.n_polys));
+}
+
 /// exhaustive_assign semantics (synthetic.hpp:193-205) on the GPU.
 inline std::vector<std::int32_t> exhaustive_assign(std::span<const LeafRegion> leaves,
                                                    std::span<const Point> points,

@@ -91,6 +91,11 @@ def ref():
         L.ref_sample.restype = C.c_int
         L.ref_sample.argtypes = [C.c_int, PD, u64, u64, PD]
         L.ref_cell_from_point.restype = C.c_int
+        L.ref_save_synthetic_fmcb.argtypes = [u64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double,
+                                              C.c_char_p]
+        L.ref_save_synthetic_fmcb.restype = C.c_int
+        L.ref_load_fmcb_status.argtypes = [C.c_char_p]
+        L.ref_load_fmcb_status.restype = C.c_int
         L.ref_cell_from_point.argtypes = [C.c_double, C.c_double, C.c_int, PU64]
         _ref = L
     return _ref
@@ -245,3 +250,16 @@ def ref_sample(clustered: bool, bbox4, n: int, seed: int) -> np.ndarray:
     if rc:
         raise ValueError(ref().ref_last_error().decode())
     return out
+
+
+def ref_save_synthetic_fmcb(seed, n_states, counties_per_state, blocks_per_county, jitter, path):
+    """The reference's save_hierarchy over its generate_synthetic hierarchy."""
+    rc = ref().ref_save_synthetic_fmcb(seed, n_states, counties_per_state, blocks_per_county,
+                                       jitter, str(path).encode())
+    if rc != 0:
+        raise RuntimeError("reference save_hierarchy failed")
+
+
+def ref_load_fmcb_status(path) -> int:
+    """load_hierarchy's verdict: 0 ok, 1 runtime_error, 2 invalid_argument, 3 other."""
+    return int(ref().ref_load_fmcb_status(str(path).encode()))

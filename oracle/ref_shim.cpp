@@ -313,3 +313,40 @@ int ref_cell_from_point(double lon, double lat, int level, std::uint64_t* out) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// The reference's own FMCB writer (save_hierarchy, hierarchy.hpp:190-202)
+// over its generate_synthetic hierarchy -- test fixtures for the loader.
+int ref_save_synthetic_fmcb(std::uint64_t seed, std::uint32_t n_states,
+                            std::uint32_t counties_per_state, std::uint32_t blocks_per_county,
+                            double jitter, const char* path) {
+  try {
+    SyntheticSpec spec;
+    spec.seed = seed;
+    spec.n_states = n_states;
+    spec.counties_per_state = counties_per_state;
+    spec.blocks_per_county = blocks_per_county;
+    spec.jitter = jitter;
+    save_hierarchy(generate_synthetic(spec), path);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// load_hierarchy's verdict on a file: 0 ok, 1 runtime_error, 2 invalid_argument, 3 other.
+int ref_load_fmcb_status(const char* path) {
+  try {
+    load_hierarchy(path);
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return 2;
+  } catch (const std::runtime_error&) {
+    return 1;
+  } catch (const std::exception&) {
+    return 3;
+  }
+}
+
+}  // extern "C"

@@ -81,6 +81,9 @@ EXPORTS = (
     "fm_status_string", "fm_last_error", "fm_version", "fm_index_build",
     "fm_index_destroy", "fm_index_stats_get", "fm_query", "fm_query_host",
     "fm_index_export", "fm_index_device", "fm_query_mode", "fm_query_host_mode",
+    "fm_index_save", "fm_index_load", "fm_hierarchy_load", "fm_hierarchy_destroy",
+    "fm_hierarchy_sizes", "fm_hierarchy_leaves", "fm_index_build_hierarchy",
+    "fm_read_points_f64", "fm_write_assign_csv",
 )
 
 MODE_EXACT, MODE_APPROX = 0, 1  # fm_mode (CoverMode, cell_index.hpp:246)
@@ -126,6 +129,25 @@ def lib() -> C.CDLL:
         L.fm_query_mode.restype = C.c_int
         L.fm_query_host_mode.argtypes = [C.c_void_p, C.c_int, PD, u64, PI32, PI64]
         L.fm_query_host_mode.restype = C.c_int
+        L.fm_index_save.restype = C.c_int
+        L.fm_index_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.fm_index_load.restype = C.c_int
+        L.fm_index_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.fm_hierarchy_load.restype = C.c_int
+        L.fm_hierarchy_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        L.fm_hierarchy_destroy.restype = None
+        L.fm_hierarchy_destroy.argtypes = [C.c_void_p]
+        L.fm_hierarchy_sizes.restype = C.c_int
+        L.fm_hierarchy_sizes.argtypes = [C.c_void_p] + [PU64] * 5
+        L.fm_hierarchy_leaves.restype = C.c_int
+        L.fm_hierarchy_leaves.argtypes = [C.c_void_p, PD, PU64, PU64, PU32, C.c_char_p]
+        L.fm_index_build_hierarchy.restype = C.c_int
+        L.fm_index_build_hierarchy.argtypes = [C.c_void_p, C.POINTER(BuildParams),
+                                               C.POINTER(C.c_void_p)]
+        L.fm_read_points_f64.restype = C.c_int
+        L.fm_read_points_f64.argtypes = [C.c_char_p, PD, PU64]
+        L.fm_write_assign_csv.restype = C.c_int
+        L.fm_write_assign_csv.argtypes = [C.c_char_p, PD, u64, PI32, C.c_void_p]
         L.fm_index_export.restype = C.c_int
         L.fm_index_export.argtypes = [C.c_void_p, PU32, PU64, PU8, PU64, PD]
         L.fm_index_device.restype = C.c_int

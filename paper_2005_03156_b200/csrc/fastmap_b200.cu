@@ -14,6 +14,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -35,6 +36,15 @@ fm_status set_err(fm_status s, const std::string& msg) {
   g_err = msg;
   return s;
 }
+
+}  // namespace
+
+// For io.cpp (not part of the C-ABI).
+__attribute__((visibility("hidden"))) fm_status fm_set_error(fm_status s, const char* msg) {
+  return set_err(s, msg);
+}
+
+namespace {
 
 #ifndef FM_KU
 #define FM_KU 2
@@ -1023,6 +1033,33 @@ fm_status build_approx(fm_index* ix) {
   return FM_OK;
 }
 
+// Query-side layout of a device index (shared by fm_index_build and
+// fm_index_load): mempool policy, block-major slot numbering + the folded
+// grid, and the approx cover when epsilon > 0.
+fm_status finish_device(fm_index* ix, double approx_epsilon) {
+  DeviceGuard guard(ix->device);
+  if (!guard.ok) return set_err(FM_ERR_CUDA, "cudaSetDevice failed");
+  // keep stream-ordered scratch (the boundary queue) cached between calls
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, ix->device) == cudaSuccess) {
+    std::uint64_t thr = ~std::uint64_t{0};
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  const int nx = static_cast<int>(ix->g.nx), ny = static_cast<int>(ix->g.ny);
+  const int qls = fold_ls(nx, ny, kQueryBudget, kQueryMaxLs);
+  fm_status st = renumber_slots(ix, qls);
+  if (st == FM_OK) {
+    st = fold_grid(ix->d_grid, nx, ny, kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots,
+                   kQueryMaxRatio, &ix->qgrid);
+  }
+  if (st != FM_OK) return st;
+  ix->stats.query_grid_bytes = ix->qgrid.bytes;
+  ix->stats.query_block_log2 = ix->qgrid.ls;
+  ix->stats.approx_epsilon = approx_epsilon;
+  if (approx_epsilon > 0.0) return build_approx(ix);
+  return FM_OK;
+}
+
 fm_status check_device(int device) {
   int count = 0;
   const cudaError_t e = cudaGetDeviceCount(&count);
@@ -1204,42 +1241,14 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
     std::vector<std::uint8_t>().swap(ix->host.overflow);
   }
   if (ix->device >= 0) {
-    DeviceGuard guard(ix->device);
-    // keep stream-ordered scratch (the boundary queue) cached between calls
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, ix->device) == cudaSuccess) {
-      std::uint64_t thr = ~std::uint64_t{0};
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
-  if (ix->device >= 0) {
-    DeviceGuard guard(ix->device);
-    const int qls = fold_ls(static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny), kQueryBudget,
-                            kQueryMaxLs);
-    fm_status st = renumber_slots(ix, qls);
-    if (st == FM_OK) {
-      st = fold_grid(ix->d_grid, static_cast<int>(ix->g.nx), static_cast<int>(ix->g.ny),
-                     kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots, kQueryMaxRatio,
-                     &ix->qgrid);
-    }
+    const fm_status st = finish_device(ix, p.approx_epsilon);
     if (st != FM_OK) {
       free_device(ix);
       delete ix;
       return st;
     }
-    s.query_grid_bytes = ix->qgrid.bytes;
-    s.query_block_log2 = ix->qgrid.ls;
   }
   s.approx_epsilon = p.approx_epsilon;
-  if (ix->device >= 0 && p.approx_epsilon > 0.0) {
-    DeviceGuard guard(ix->device);
-    const fm_status st = build_approx(ix);
-    if (st != FM_OK) {
-      free_device(ix);
-      delete ix;
-      return st;
-    }
-  }
   s.build_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out_index = ix;
@@ -1354,6 +1363,177 @@ fm_status fm_query_host_mode(const fm_index* cindex, int mode, const double* h_l
     FM_CUDA(cudaMemcpy(tmp.data(), dh, index->stats.n_polys * 8, cudaMemcpyDeviceToHost));
     for (std::uint64_t k = 0; k < index->stats.n_polys; ++k) h_hist[k] += tmp[k];
   }
+  return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Index persistence (the FMCI save/load analogue, cell_index.hpp:641-726):
+// "FMGI", u32 version, u32 sizeof(fm_index_stats), the stats, the grid
+// geometry, n_phase1_slots, then grid / slot arena / overflow arena, each
+// u64 length-prefixed.  Little endian (the only target).  The query-side
+// layout (fold, approx cover) is rebuilt on load.
+namespace {
+constexpr char kIndexMagic[4] = {'F', 'M', 'G', 'I'};
+constexpr std::uint32_t kIndexVersion = 1;
+
+bool write_all(std::FILE* f, const void* p, std::uint64_t n) {
+  return n == 0 || std::fwrite(p, 1, n, f) == n;
+}
+bool read_all(std::FILE* f, void* p, std::uint64_t n) {
+  return n == 0 || std::fread(p, 1, n, f) == n;
+}
+}  // namespace
+
+fm_status fm_index_save(const fm_index* index, const char* path) {
+  g_err.clear();
+  if (!index || !path) return set_err(FM_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<std::uint32_t> grid;
+  std::vector<std::uint8_t> slots, ovf;
+  const std::uint32_t* gp;
+  const std::uint8_t *sp, *op;
+  if (index->device < 0) {
+    gp = index->host.grid.data();
+    sp = index->host.slots.data();
+    op = index->host.overflow.data();
+  } else {
+    DeviceGuard guard(index->device);
+    grid.resize(index->grid_len);
+    slots.resize(index->slots_len);
+    ovf.resize(index->overflow_len);
+    FM_CUDA(cudaMemcpy(grid.data(), index->d_grid, index->grid_len * 4, cudaMemcpyDeviceToHost));
+    FM_CUDA(cudaMemcpy(slots.data(), index->d_slots, index->slots_len, cudaMemcpyDeviceToHost));
+    FM_CUDA(cudaMemcpy(ovf.data(), index->d_overflow, index->overflow_len, cudaMemcpyDeviceToHost));
+    gp = grid.data();
+    sp = slots.data();
+    op = ovf.data();
+  }
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) return set_err(FM_ERR_RUNTIME, std::string("cannot open for writing: ") + path);
+  const std::uint32_t ver = kIndexVersion, ssz = sizeof(fm_index_stats);
+  const fm::GridGeom& g = index->g;
+  const double geo[9] = {g.gx0, g.gx1, g.gy0, g.gy1, g.w, g.h, g.inv_w, g.inv_h, g.margin};
+  const std::int64_t dims[2] = {g.nx, g.ny};
+  const std::uint64_t counts[5] = {index->host.n_slots, index->host.n_phase1_slots,
+                                   index->grid_len, index->slots_len, index->overflow_len};
+  bool ok = write_all(f, kIndexMagic, 4) && write_all(f, &ver, 4) && write_all(f, &ssz, 4) &&
+            write_all(f, &index->stats, ssz) && write_all(f, geo, sizeof(geo)) &&
+            write_all(f, dims, sizeof(dims)) && write_all(f, counts, sizeof(counts)) &&
+            write_all(f, gp, index->grid_len * 4) && write_all(f, sp, index->slots_len) &&
+            write_all(f, op, index->overflow_len);
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) return set_err(FM_ERR_RUNTIME, std::string("write failed: ") + path);
+  return FM_OK;
+}
+
+fm_status fm_index_load(const char* path, int device, fm_index** out_index) {
+  g_err.clear();
+  if (!path || !out_index) return set_err(FM_ERR_INVALID_ARGUMENT, "null argument");
+  *out_index = nullptr;
+  if (device >= 0) {
+    const fm_status st = check_device(device);
+    if (st != FM_OK) return st;
+  }
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return set_err(FM_ERR_RUNTIME, std::string("cannot open for reading: ") + path);
+  auto fail = [&](const std::string& msg) {
+    std::fclose(f);
+    return set_err(FM_ERR_RUNTIME, msg + ": " + path);
+  };
+  char magic[4];
+  std::uint32_t ver = 0, ssz = 0;
+  if (!read_all(f, magic, 4) || std::memcmp(magic, kIndexMagic, 4) != 0) {
+    return fail("not an index file (bad magic)");
+  }
+  if (!read_all(f, &ver, 4) || ver != kIndexVersion) return fail("unsupported index file version");
+  if (!read_all(f, &ssz, 4) || ssz != sizeof(fm_index_stats)) return fail("index file stats layout differs");
+  fm_index* ix = new (std::nothrow) fm_index();
+  if (!ix) {
+    std::fclose(f);
+    return set_err(FM_ERR_OOM, "host allocation failed");
+  }
+  double geo[9];
+  std::int64_t dims[2];
+  std::uint64_t counts[5];
+  if (!read_all(f, &ix->stats, ssz) || !read_all(f, geo, sizeof(geo)) ||
+      !read_all(f, dims, sizeof(dims)) || !read_all(f, counts, sizeof(counts))) {
+    delete ix;
+    return fail("truncated index file");
+  }
+  fm::GridGeom& g = ix->g;
+  g.gx0 = geo[0];
+  g.gx1 = geo[1];
+  g.gy0 = geo[2];
+  g.gy1 = geo[3];
+  g.w = geo[4];
+  g.h = geo[5];
+  g.inv_w = geo[6];
+  g.inv_h = geo[7];
+  g.margin = geo[8];
+  g.nx = dims[0];
+  g.ny = dims[1];
+  ix->host.g = g;
+  ix->host.n_slots = counts[0];
+  ix->host.n_phase1_slots = counts[1];
+  ix->grid_len = counts[2];
+  ix->slots_len = counts[3];
+  ix->overflow_len = counts[4];
+  if (g.nx <= 0 || g.ny <= 0 || ix->grid_len != static_cast<std::uint64_t>(g.nx * g.ny) ||
+      ix->slots_len < ix->host.n_slots * fm::kSlotBytes || ix->overflow_len < 512) {
+    delete ix;
+    return fail("corrupt index file header");
+  }
+  try {
+    ix->host.grid.resize(ix->grid_len);
+    ix->host.slots.resize(ix->slots_len);
+    ix->host.overflow.resize(ix->overflow_len);
+  } catch (const std::bad_alloc&) {
+    delete ix;
+    std::fclose(f);
+    return set_err(FM_ERR_OOM, "host allocation failed while loading the index");
+  }
+  if (!read_all(f, ix->host.grid.data(), ix->grid_len * 4) ||
+      !read_all(f, ix->host.slots.data(), ix->slots_len) ||
+      !read_all(f, ix->host.overflow.data(), ix->overflow_len)) {
+    delete ix;
+    return fail("truncated index file");
+  }
+  std::fclose(f);
+  ix->device = device;
+  ix->ax0 = std::max(g.gx0, -180.0);
+  ix->ax1 = std::min(g.gx1, 180.0);
+  ix->ay0 = std::max(g.gy0, -90.0);
+  ix->ay1 = std::min(g.gy1, 90.0);
+  const double eps = ix->stats.approx_epsilon;
+  ix->stats.query_grid_bytes = 0;
+  ix->stats.query_block_log2 = 0;
+  ix->stats.approx_grid_bytes = 0;
+  ix->stats.approx_block_log2 = 0;
+  if (device >= 0) {
+    DeviceGuard guard(device);
+    cudaError_t e1 = cudaMalloc(&ix->d_grid, ix->grid_len * 4);
+    cudaError_t e2 = cudaMalloc(&ix->d_slots, ix->slots_len);
+    cudaError_t e3 = cudaMalloc(&ix->d_overflow, ix->overflow_len);
+    if (e1 == cudaSuccess && e2 == cudaSuccess && e3 == cudaSuccess) {
+      e1 = cudaMemcpy(ix->d_grid, ix->host.grid.data(), ix->grid_len * 4, cudaMemcpyHostToDevice);
+      e2 = cudaMemcpy(ix->d_slots, ix->host.slots.data(), ix->slots_len, cudaMemcpyHostToDevice);
+      e3 = cudaMemcpy(ix->d_overflow, ix->host.overflow.data(), ix->overflow_len, cudaMemcpyHostToDevice);
+    }
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+      free_device(ix);
+      delete ix;
+      return set_err(FM_ERR_CUDA, "index upload failed");
+    }
+    std::vector<std::uint32_t>().swap(ix->host.grid);
+    std::vector<std::uint8_t>().swap(ix->host.slots);
+    std::vector<std::uint8_t>().swap(ix->host.overflow);
+    const fm_status st = finish_device(ix, eps);
+    if (st != FM_OK) {
+      free_device(ix);
+      delete ix;
+      return st;
+    }
+  }
+  *out_index = ix;
   return FM_OK;
 }
 

@@ -19,6 +19,10 @@ reference (file:line)                        here
 ``exhaustive_assign`` synthetic.hpp:193-205   :func:`exhaustive_assign`
 ``AssignmentResult`` simple_mapper.hpp:39-46  :class:`AssignmentResult`
 ``index_stats`` cell_index.hpp:616-631        :func:`index_stats`
+``load_hierarchy`` hierarchy.hpp:204-223      :func:`load_hierarchy` (FMCB -> leaves)
+FMCI save/load cell_index.hpp:641-726         :meth:`CellIndex.save` / :func:`load_index`
+``read_points_f64`` io.hpp:154-167            :func:`read_points_f64`
+assign CSV tools/fastmap.cpp:288-301          :func:`write_assign_csv`
 ===========================================  =====================================
 
 Exceptions: ``std::invalid_argument`` -> ``ValueError``,
@@ -125,6 +129,69 @@ def leaves_to_soup(leaves: Sequence[LeafRegion]) -> Soup:
         g = lf.geometry
         polys.append([] if g is None else list(g.rings))
     return Soup.from_rings(polys)
+
+
+class Hierarchy:
+    """An FMCB region hierarchy flattened to its leaves (``load_hierarchy``,
+    hierarchy.hpp:204-223, then ``collect_leaves``, hierarchy.hpp:76-91):
+    the leaf soup, per-leaf (state, county, block) and 12-char FIPS codes.
+    Owns the native ``fm_hierarchy`` handle (used by :func:`write_assign_csv`)."""
+
+    def __init__(self, handle: C.c_void_p) -> None:
+        self._h = handle
+        L = N.lib()
+        v = [C.c_uint64(0) for _ in range(5)]
+        N.check(L.fm_hierarchy_sizes(handle, *[C.byref(x) for x in v]), "fm_hierarchy_sizes")
+        self.n_states, self.n_counties, n_leaves, n_rings, n_verts = (x.value for x in v)
+        vxy = np.zeros((n_verts, 2), dtype=np.float64)
+        ro = np.zeros(n_rings + 1, dtype=np.uint64)
+        pr = np.zeros(n_leaves + 1, dtype=np.uint64)
+        self.scb = np.zeros((n_leaves, 3), dtype=np.uint32)
+        fips = C.create_string_buffer(12 * n_leaves + 1)
+        N.check(L.fm_hierarchy_leaves(handle, N.ptr(vxy, C.c_double), N.ptr(ro, C.c_uint64),
+                                      N.ptr(pr, C.c_uint64), N.ptr(self.scb, C.c_uint32), fips),
+                "fm_hierarchy_leaves")
+        self.soup = Soup(vxy, ro, pr)
+        self.fips12 = np.frombuffer(fips.raw[:12 * n_leaves], dtype="S12").copy()
+
+    @property
+    def n_leaves(self) -> int:
+        return self.soup.n_polys
+
+    def __del__(self) -> None:
+        if getattr(self, "_h", None):
+            lib = N.lib() if N is not None else None
+            if lib is not None:
+                lib.fm_hierarchy_destroy(self._h)
+            self._h = None
+
+
+def load_hierarchy(path: str) -> Hierarchy:
+    """Read an FMCB file (the reference's ``save_hierarchy`` format)."""
+    h = C.c_void_p()
+    N.check(N.lib().fm_hierarchy_load(str(path).encode(), C.byref(h)), "fm_hierarchy_load")
+    return Hierarchy(h)
+
+
+def read_points_f64(path: str) -> np.ndarray:
+    """Raw little-endian f64 (lon, lat) pairs -> (n, 2) float64 (io.hpp:154-167)."""
+    L = N.lib()
+    n = C.c_uint64(0)
+    N.check(L.fm_read_points_f64(str(path).encode(), None, C.byref(n)), "fm_read_points_f64")
+    pts = np.zeros((n.value, 2), dtype=np.float64)
+    N.check(L.fm_read_points_f64(str(path).encode(), N.ptr(pts, C.c_double), C.byref(n)),
+            "fm_read_points_f64")
+    return pts
+
+
+def write_assign_csv(path: str, points: np.ndarray, ids: np.ndarray, hierarchy: Hierarchy) -> None:
+    """The reference CLI's ``idx,lon,lat,fips`` output (tools/fastmap.cpp:288-301)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    if ids.shape[0] != pts.shape[0]:
+        raise ValueError("one id per point")
+    N.check(N.lib().fm_write_assign_csv(str(path).encode(), N.ptr(pts, C.c_double), pts.shape[0],
+                                        N.ptr(ids, C.c_int32), hierarchy._h), "fm_write_assign_csv")
 
 
 # ---------------------------------------------------------------------------
@@ -244,6 +311,10 @@ class CellIndex:
         g["n_polys"] = int(g["n_polys"])
         return grid, arena, g
 
+    def save(self, path: str) -> None:
+        """Persist the built index (FMCI analogue); reload with :func:`load_index`."""
+        N.check(N.lib().fm_index_save(self.handle, str(path).encode()), "fm_index_save")
+
     # -- projection ---------------------------------------------------------
     def project(self, points, out=None, hist=None, counters=None, stream=None,
                 mode: "CoverMode" = None):
@@ -313,10 +384,41 @@ def build_index(soup: Soup, params: Optional[CoverParams] = None, device: int = 
     return CellIndex(h, s.n_polys, params, device)
 
 
+def load_index(path: str, device: int = 0, params: Optional[CoverParams] = None) -> CellIndex:
+    """An index saved by :meth:`CellIndex.save`, onto ``device`` (-1 = host-only)."""
+    h = C.c_void_p()
+    N.check(N.lib().fm_index_load(str(path).encode(), int(device), C.byref(h)), "fm_index_load")
+    s = N.IndexStats()
+    N.check(N.lib().fm_index_stats_get(h, C.byref(s)), "fm_index_stats_get")
+    if params is None:
+        eps = float(s.approx_epsilon)
+        params = CoverParams(mode=CoverMode.approx if eps > 0 else CoverMode.exact, epsilon=eps)
+    return CellIndex(h, int(s.n_polys), params, device)
+
+
+def build_index_hierarchy(h: Hierarchy, params: Optional[CoverParams] = None,
+                          device: int = 0) -> CellIndex:
+    """fm_index_build_hierarchy: the index over an FMCB hierarchy's leaves."""
+    params = params or CoverParams()
+    validate_cover_params(params)
+    bp = N.BuildParams(cells_per_polygon=float(params.cells_per_polygon),
+                       nx=int(params.nx), ny=int(params.ny), margin=float(params.margin),
+                       device=int(device), build_on_gpu=1 if device >= 0 else 0,
+                       threads=int(params.threads),
+                       approx_epsilon=float(params.epsilon) if params.mode == CoverMode.approx
+                       else 0.0)
+    out = C.c_void_p()
+    N.check(N.lib().fm_index_build_hierarchy(h._h, C.byref(bp), C.byref(out)),
+            "fm_index_build_hierarchy")
+    return CellIndex(out, h.n_leaves, params, device)
+
+
 def build_cover(leaves, params: Optional[CoverParams] = None, device: int = 0) -> CellIndex:
     """build_cover(leaves, params) (cell_index.hpp:396-405) -> GPU cell index.
 
     ``leaves`` is a sequence of :class:`LeafRegion` or a :class:`Soup`."""
+    if isinstance(leaves, Hierarchy):
+        return build_index_hierarchy(leaves, params, device)
     soup = leaves if isinstance(leaves, Soup) else leaves_to_soup(leaves)
     return build_index(soup, params, device)
 
@@ -338,6 +440,9 @@ def build_trie(cover: CellIndex, levels_per_node: int) -> TrieIndex:
 
 
 def _leaf_table(leaves) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    if isinstance(leaves, Hierarchy):
+        t = leaves.scb.astype(np.int32)
+        return t[:, 0].copy(), t[:, 1].copy(), t[:, 2].copy()
     if isinstance(leaves, Soup):
         n = leaves.n_polys
         return (np.zeros(n, np.int32), np.zeros(n, np.int32), np.arange(n, dtype=np.int32))
@@ -353,7 +458,8 @@ def query_leaves(trie, leaves, points, mode: CoverMode = CoverMode.exact) -> Ass
     cover = trie.cover if isinstance(trie, TrieIndex) else trie
     if mode == CoverMode.approx and cover.params.mode != CoverMode.approx:
         raise ValueError("approximate queries require an approximate-mode cover")
-    n_leaves = leaves.n_polys if isinstance(leaves, Soup) else len(leaves)
+    n_leaves = (leaves.n_polys if isinstance(leaves, Soup) else
+                leaves.n_leaves if isinstance(leaves, Hierarchy) else len(leaves))
     if cover.n_leaves != n_leaves:
         raise ValueError("cover was built for a different hierarchy")
     ids = cover.project(points, mode=mode)

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <filesystem>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -139,5 +140,15 @@ int main(int argc, char** argv) {
   }
   std::printf("%s (GPU): %zu of %zu points differ\n", bad ? "FAIL" : "OK", bad, pts.size());
   if (bad) return 1;
+  // index persistence through the adapter: reload and compare
+  const std::string path = (std::filesystem::temp_directory_path() / "adapter_check.fmgi").string();
+  gpu::save_index(index, path);
+  const auto back = gpu::load_index(path);
+  const auto res2 = gpu::query(back, h, pts, CoverMode::exact);
+  std::filesystem::remove(path);
+  if (res2.block != res.block || res2.county != res.county || res2.state != res.state) {
+    std::puts("FAIL: reloaded index answers differently");
+    return 1;
+  }
   return check_approx();
 }

@@ -19,7 +19,7 @@ HEADER = ROOT / "include" / "fastmap_b200.h"
 def declared_symbols():
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(fm_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(fm_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declares_what_python_binds():

@@ -102,9 +102,25 @@ def main():
     exh = m.exhaustive_assign(pts)
     np.savez_compressed(OUT / "edge_cases.npz", pts=pts, exhaustive=exh,
                         soup_sha256=np.asarray(soup_digest(soup)))
+    fmcb_fixture()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
 
 
+def fmcb_fixture():
+    """5. an FMCB file written by the reference's own save_hierarchy
+    (hierarchy.hpp:190-202) over generate_synthetic(seed 11, 2x2x3, jitter
+    0.2), plus the reference's collect_leaves view of it."""
+    path = OUT / "hier_2x2x3.fmcb"
+    oracle.ref_save_synthetic_fmcb(11, 2, 2, 3, 0.2, path)
+    vxy, ro, pr, scb, fips, _ = oracle.ref_generate_synthetic(11, 2, 2, 3, 0.2)
+    np.savez_compressed(OUT / "hier_2x2x3.npz", vxy=vxy, ring_off=ro, poly_ring=pr, scb=scb,
+                        fips=np.asarray(fips, dtype="S12"))
+    print(path.name, path.stat().st_size)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["fmcb"]:
+        fmcb_fixture()
+    else:
+        main()
