@@ -226,6 +226,33 @@ fm_status fm_index_build_hierarchy(const fm_hierarchy* h, const fm_build_params*
  * buffer capacity in points and receives the count read. */
 fm_status fm_read_points_f64(const char* path, double* lonlat, uint64_t* n);
 
+/* ---- the simple engine ---------------------- */
+
+/* The paper's hierarchical descent, assign(h, points, mode)
+ * (simple_mapper.hpp:119-166), on the GPU: per level, the parent's children
+ * whose file bbox strictly contains the point; strict mode takes the first
+ * whose polygon holds it; relaxed mode takes a single candidate untested and
+ * otherwise the first holding polygon, else the highest-indexed candidate.
+ * Outputs are local (state, county-in-state, block-in-county) indices, -1
+ * where unresolved. */
+typedef enum fm_assign_mode { FM_ASSIGN_RELAXED = 0, FM_ASSIGN_STRICT = 1 } fm_assign_mode;  /* simple_mapper.hpp:24 */
+typedef struct fm_assign_counters {  /* AssignCounters, simple_mapper.hpp:26-35 */
+  uint64_t pip_point_evaluations;    /* (point, region) polygon tests */
+  uint64_t pip_calls;                /* regions that received a polygon test */
+} fm_assign_counters;
+typedef struct fm_simple fm_simple;
+fm_status fm_simple_build(const fm_hierarchy* h, int device, fm_simple** out);
+void fm_simple_destroy(fm_simple* s);
+/* Device pointers, asynchronous on `stream` unless `counters` (host struct,
+ * accumulated into) is given, which makes the call synchronous. */
+fm_status fm_simple_assign(const fm_simple* s, int mode, const double* d_lonlat, uint64_t n,
+                           int32_t* d_state, int32_t* d_county, int32_t* d_block,
+                           fm_assign_counters* counters, void* stream);
+/* Host pointers (chunked copies); one batch for the counters. */
+fm_status fm_simple_assign_host(const fm_simple* s, int mode, const double* lonlat, uint64_t n,
+                                int32_t* state, int32_t* county, int32_t* block,
+                                fm_assign_counters* counters);
+
 /* The assignment CSV of the reference CLI (tools/fastmap.cpp:288-301):
  * header "idx,lon,lat,fips", one row per finite input point (non-finite rows
  * are skipped and keep their input index), coordinates as %.17g

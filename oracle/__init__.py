@@ -96,6 +96,8 @@ def ref():
         L.ref_save_synthetic_fmcb.restype = C.c_int
         L.ref_load_fmcb_status.argtypes = [C.c_char_p]
         L.ref_load_fmcb_status.restype = C.c_int
+        L.ref_simple_assign_fmcb.argtypes = [C.c_char_p, PD, u64, C.c_int, PI32, PI32, PI32, PU64]
+        L.ref_simple_assign_fmcb.restype = C.c_int
         L.ref_cell_from_point.argtypes = [C.c_double, C.c_double, C.c_int, PU64]
         _ref = L
     return _ref
@@ -263,3 +265,18 @@ def ref_save_synthetic_fmcb(seed, n_states, counties_per_state, blocks_per_count
 def ref_load_fmcb_status(path) -> int:
     """load_hierarchy's verdict: 0 ok, 1 runtime_error, 2 invalid_argument, 3 other."""
     return int(ref().ref_load_fmcb_status(str(path).encode()))
+
+
+def ref_simple_assign(path, pts, strict: bool):
+    """The reference's simple engine (simple_mapper.hpp:119-166) on an FMCB file:
+    (state, county, block, (pip_point_evaluations, pip_calls))."""
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 2)
+    n = pts.shape[0]
+    st, co, bl = (np.empty(n, dtype=np.int32) for _ in range(3))
+    cnt = np.zeros(2, dtype=np.uint64)
+    rc = ref().ref_simple_assign_fmcb(str(path).encode(), _p(pts, C.c_double), n, 1 if strict else 0,
+                                      _p(st, C.c_int32), _p(co, C.c_int32), _p(bl, C.c_int32),
+                                      _p(cnt, C.c_uint64))
+    if rc:
+        raise RuntimeError("reference assign failed")
+    return st, co, bl, (int(cnt[0]), int(cnt[1]))

@@ -350,3 +350,31 @@ int ref_load_fmcb_status(const char* path) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// The reference's simple engine, assign(h, points, mode) (simple_mapper.hpp:
+// 119-166), over an FMCB file.  mode 0 relaxed, 1 strict.  counters[2] =
+// {pip_point_evaluations, pip_calls}.  Returns 0, or 1 on any exception.
+int ref_simple_assign_fmcb(const char* path, const double* lonlat, std::uint64_t n, int mode,
+                           std::int32_t* st, std::int32_t* co, std::int32_t* bl,
+                           std::uint64_t* counters) {
+  try {
+    const RegionHierarchy h = load_hierarchy(path);
+    std::vector<Point> pts(n);
+    for (std::uint64_t i = 0; i < n; ++i) pts[i] = {lonlat[2 * i], lonlat[2 * i + 1]};
+    const auto r = assign(h, pts, mode == 1 ? AssignMode::strict : AssignMode::relaxed);
+    for (std::uint64_t i = 0; i < n; ++i) {
+      st[i] = r.state[i];
+      co[i] = r.county[i];
+      bl[i] = r.block[i];
+    }
+    counters[0] = r.counters.pip_point_evaluations;
+    counters[1] = r.counters.pip_calls;
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+}  // extern "C"

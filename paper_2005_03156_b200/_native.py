@@ -71,6 +71,10 @@ class IndexStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class AssignCountersC(C.Structure):
+    _fields_ = [("pip_point_evaluations", u64), ("pip_calls", u64)]
+
+
 class QueryCounters(C.Structure):
     _fields_ = [("points", u64), ("boundary_points", u64),
                 ("candidate_tests", u64), ("edge_tests", u64)]
@@ -83,7 +87,8 @@ EXPORTS = (
     "fm_index_export", "fm_index_device", "fm_query_mode", "fm_query_host_mode",
     "fm_index_save", "fm_index_load", "fm_hierarchy_load", "fm_hierarchy_destroy",
     "fm_hierarchy_sizes", "fm_hierarchy_leaves", "fm_index_build_hierarchy",
-    "fm_read_points_f64", "fm_write_assign_csv",
+    "fm_read_points_f64", "fm_write_assign_csv", "fm_simple_build", "fm_simple_destroy",
+    "fm_simple_assign", "fm_simple_assign_host",
 )
 
 MODE_EXACT, MODE_APPROX = 0, 1  # fm_mode (CoverMode, cell_index.hpp:246)
@@ -148,6 +153,16 @@ def lib() -> C.CDLL:
         L.fm_read_points_f64.argtypes = [C.c_char_p, PD, PU64]
         L.fm_write_assign_csv.restype = C.c_int
         L.fm_write_assign_csv.argtypes = [C.c_char_p, PD, u64, PI32, C.c_void_p]
+        L.fm_simple_build.restype = C.c_int
+        L.fm_simple_build.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.fm_simple_destroy.restype = None
+        L.fm_simple_destroy.argtypes = [C.c_void_p]
+        L.fm_simple_assign.restype = C.c_int
+        L.fm_simple_assign.argtypes = [C.c_void_p, C.c_int, C.c_void_p, u64, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.POINTER(AssignCountersC), C.c_void_p]
+        L.fm_simple_assign_host.restype = C.c_int
+        L.fm_simple_assign_host.argtypes = [C.c_void_p, C.c_int, PD, u64, PI32, PI32, PI32,
+                                            C.POINTER(AssignCountersC)]
         L.fm_index_export.restype = C.c_int
         L.fm_index_export.argtypes = [C.c_void_p, PU32, PU64, PU8, PU64, PD]
         L.fm_index_device.restype = C.c_int

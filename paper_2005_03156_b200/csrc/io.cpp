@@ -17,18 +17,10 @@
 #include <vector>
 
 #include "../../include/fastmap_b200.h"
+#include "hierarchy.h"
 
 // Defined in fastmap_b200.cu: the calling thread's last error message.
 __attribute__((visibility("hidden"))) fm_status fm_set_error(fm_status s, const char* msg);
-
-struct fm_hierarchy {
-  std::uint64_t n_states = 0, n_counties = 0, n_leaves = 0;
-  std::vector<double> vxy;              // leaf vertices, collect_leaves order
-  std::vector<std::uint64_t> ring_off;  // n_rings + 1
-  std::vector<std::uint64_t> poly_ring; // n_leaves + 1
-  std::vector<std::uint32_t> scb;       // n_leaves x (state, county, block)
-  std::vector<char> fips;               // n_leaves x 12
-};
 
 namespace {
 
@@ -65,14 +57,15 @@ class Reader {
   std::string path_;
 };
 
-// One node (read_node, hierarchy.hpp:141-186).  Leaves (depth 2) append their
-// rings to the soup; upper levels are parsed for structure and validation.
+// One node (read_node, hierarchy.hpp:141-186), appended to its level with
+// its rings, its file bbox and (depth < 2) its children's index range.
 void read_node(Reader& in, int depth, fm_hierarchy& h, std::uint32_t s, std::uint32_t c,
                std::uint32_t b, const std::string& path) {
+  fm::HierLevel& L = h.level[depth];
   in.get<std::uint64_t>();  // fp code
   char fips[kFips];
   if (depth == 2) in.bytes(fips, kFips);
-  for (int k = 0; k < 4; ++k) in.f64();  // bbox (recomputed by the builder)
+  for (int k = 0; k < 4; ++k) L.bbox.push_back(in.f64());
   const std::uint32_t nv = in.get<std::uint32_t>();
   std::vector<double> v(2 * static_cast<std::size_t>(nv));
   for (std::uint32_t k = 0; k < nv; ++k) {
@@ -89,14 +82,14 @@ void read_node(Reader& in, int depth, fm_hierarchy& h, std::uint32_t s, std::uin
       throw LoadError{FM_ERR_INVALID_ARGUMENT, "polygon ring needs at least 3 vertices"};
     }
   }
+  // rings as add_ring builds them; a ringless payload has no edges
+  for (std::uint32_t r = 0; r < nr; ++r) {
+    const std::uint32_t begin = starts[r], end = r + 1 < nr ? starts[r + 1] : nv;
+    L.vxy.insert(L.vxy.end(), v.begin() + 2 * begin, v.begin() + 2 * end);
+    L.ring_off.push_back(L.vxy.size() / 2);
+  }
+  L.poly_ring.push_back(L.ring_off.size() - 1);
   if (depth == 2) {
-    // rings as add_ring builds them; a ringless payload has no edges
-    for (std::uint32_t r = 0; r < nr; ++r) {
-      const std::uint32_t begin = starts[r], end = r + 1 < nr ? starts[r + 1] : nv;
-      h.vxy.insert(h.vxy.end(), v.begin() + 2 * begin, v.begin() + 2 * end);
-      h.ring_off.push_back(h.vxy.size() / 2);
-    }
-    h.poly_ring.push_back(h.ring_off.size() - 1);
     h.scb.push_back(s);
     h.scb.push_back(c);
     h.scb.push_back(b);
@@ -106,10 +99,14 @@ void read_node(Reader& in, int depth, fm_hierarchy& h, std::uint32_t s, std::uin
   }
   const std::uint32_t nch = in.get<std::uint32_t>();
   if (depth == 0) h.n_counties += nch;
+  const std::size_t slot = L.child_lo.size();
+  L.child_lo.push_back(static_cast<std::uint32_t>(h.level[depth + 1].n_regions()));
+  L.child_hi.push_back(0);
   for (std::uint32_t i = 0; i < nch; ++i) {
     if (depth == 0) read_node(in, 1, h, s, i, 0, path);
     else read_node(in, 2, h, s, c, i, path);
   }
+  L.child_hi[slot] = static_cast<std::uint32_t>(h.level[depth + 1].n_regions());
 }
 
 }  // namespace
@@ -140,8 +137,6 @@ fm_status fm_hierarchy_load(const char* path, fm_hierarchy** out) {
     }
     const std::uint64_t ns = in.get<std::uint64_t>(), nc = in.get<std::uint64_t>(),
                         nb = in.get<std::uint64_t>();
-    h->ring_off.push_back(0);
-    h->poly_ring.push_back(0);
     for (std::uint64_t s = 0; s < ns; ++s) read_node(in, 0, *h, static_cast<std::uint32_t>(s), 0, 0, path);
     h->n_states = ns;
     if (h->n_counties != nc || h->n_leaves != nb) {  // hierarchy.hpp:218-221
@@ -169,17 +164,18 @@ fm_status fm_hierarchy_sizes(const fm_hierarchy* h, uint64_t* n_states, uint64_t
   if (n_states) *n_states = h->n_states;
   if (n_counties) *n_counties = h->n_counties;
   if (n_leaves) *n_leaves = h->n_leaves;
-  if (n_rings) *n_rings = h->ring_off.size() - 1;
-  if (n_vertices) *n_vertices = h->vxy.size() / 2;
+  if (n_rings) *n_rings = h->level[2].ring_off.size() - 1;
+  if (n_vertices) *n_vertices = h->level[2].vxy.size() / 2;
   return FM_OK;
 }
 
 fm_status fm_hierarchy_leaves(const fm_hierarchy* h, double* vertex_lonlat, uint64_t* ring_offsets,
                               uint64_t* poly_ring_offsets, uint32_t* scb, char* fips12) {
   if (!h) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "null hierarchy");
-  if (vertex_lonlat) std::memcpy(vertex_lonlat, h->vxy.data(), h->vxy.size() * 8);
-  if (ring_offsets) std::memcpy(ring_offsets, h->ring_off.data(), h->ring_off.size() * 8);
-  if (poly_ring_offsets) std::memcpy(poly_ring_offsets, h->poly_ring.data(), h->poly_ring.size() * 8);
+  const fm::HierLevel& L = h->level[2];
+  if (vertex_lonlat) std::memcpy(vertex_lonlat, L.vxy.data(), L.vxy.size() * 8);
+  if (ring_offsets) std::memcpy(ring_offsets, L.ring_off.data(), L.ring_off.size() * 8);
+  if (poly_ring_offsets) std::memcpy(poly_ring_offsets, L.poly_ring.data(), L.poly_ring.size() * 8);
   if (scb) std::memcpy(scb, h->scb.data(), h->scb.size() * 4);
   if (fips12) std::memcpy(fips12, h->fips.data(), h->fips.size());
   return FM_OK;
@@ -188,8 +184,9 @@ fm_status fm_hierarchy_leaves(const fm_hierarchy* h, double* vertex_lonlat, uint
 fm_status fm_index_build_hierarchy(const fm_hierarchy* h, const fm_build_params* params,
                                    fm_index** out_index) {
   if (!h) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "null hierarchy");
-  return fm_index_build(h->vxy.data(), h->ring_off.data(), h->ring_off.size() - 1,
-                        h->poly_ring.data(), h->n_leaves, params, out_index);
+  const fm::HierLevel& L = h->level[2];
+  return fm_index_build(L.vxy.data(), L.ring_off.data(), L.ring_off.size() - 1, L.poly_ring.data(),
+                        h->n_leaves, params, out_index);
 }
 
 fm_status fm_read_points_f64(const char* path, double* lonlat, uint64_t* n) {

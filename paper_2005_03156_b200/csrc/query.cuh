@@ -294,7 +294,7 @@ __device__ __noinline__ int resolve_slot_global(const KParams& P, std::uint32_t 
 // Every listed candidate has boundary, breakpoints or a terminal inside the
 // margin-expanded cell, so any point of the cell lies within the expanded
 // cell diagonal of it -- the fast-approx fallback.
-__device__ __noinline__ std::uint32_t min_leaf_of_entry(const KParams& P, std::uint32_t e) {
+static __device__ __noinline__ std::uint32_t min_leaf_of_entry(const KParams& P, std::uint32_t e) {
   std::uint32_t best = kEmpty, stack[4 * (kMaxSplitDepth + 2)];
   int sp = 0;
   stack[sp++] = e;

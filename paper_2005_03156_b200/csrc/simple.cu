@@ -1,0 +1,491 @@
+// simple.cu -- the reference's simple engine (the paper's hierarchical
+// descent, simple_mapper.hpp:62-166) on the GPU.  SURVEY.md sec. 8f item 2.
+//
+// Per point and level (states, then the chosen state's counties, then the
+// chosen county's blocks):
+//   cand = the parent's children whose file bbox strictly contains p
+//          (bbox_membership, geometry.hpp:125-162), ascending
+//   strict  (AssignMode::strict):  the first candidate whose polygon holds p
+//          (points_in_polygon, geometry.hpp:184-210), else unresolved
+//   relaxed (AssignMode::relaxed): a single candidate is taken without a
+//          polygon test; with >= 2 the first whose polygon holds p, else the
+//          highest-indexed candidate (simple_mapper.hpp:104-111)
+// An unresolved level leaves it and the levels below at -1.  Results are
+// local indices (state; county within the state; block within the county).
+//
+// Device layout per level: the regions' file bboxes, children ranges, their
+// non-horizontal edges oriented upward (lo = lower latitude, as
+// geometry.hpp:200-201), a per-region latitude band index over the edges,
+// and a uniform bbox grid listing, per cell, the regions whose bbox meets
+// it (ascending).  Band and grid cells are located with the same IEEE
+// (x - x0) * inv products on host and device, which are monotone in x, so a
+// point strictly inside a bbox / inside an edge's latitude range always
+// lands in a cell / band that lists it.  The polygon test is the exact
+// reference predicate (query.cuh ray_crosses: no FMA).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/fastmap_b200.h"
+#include "hierarchy.h"
+#include "query.cuh"
+
+__attribute__((visibility("hidden"))) fm_status fm_set_error(fm_status s, const char* msg);
+
+namespace {
+
+struct LevelDev {
+  int n = 0;
+  const double* bbox = nullptr;           // 4 per region
+  const std::uint32_t* child_lo = nullptr;
+  const std::uint32_t* child_hi = nullptr;
+  const double4* edges = nullptr;         // (lx, ly, hx, hy)
+  const double* band_y0 = nullptr;        // per region
+  const double* band_inv = nullptr;
+  const std::uint32_t* band_n = nullptr;
+  const std::uint64_t* band_base = nullptr;  // first band of the region in band_off
+  const std::uint64_t* band_off = nullptr;   // CSR into band_edges
+  const std::uint32_t* band_edges = nullptr; // global edge indices
+  double gx0 = 0, gy0 = 0, inv_w = 0, inv_h = 0;
+  int gnx = 1, gny = 1;
+  const std::uint64_t* cell_off = nullptr;
+  const std::uint32_t* cell_ids = nullptr;
+  unsigned char* tested = nullptr;  // per region: received a polygon test (pip_calls)
+};
+
+struct SimpleParams {
+  LevelDev L[3];
+};
+
+struct HostLevel {
+  std::vector<double4> edges;
+  std::vector<double> band_y0, band_inv;
+  std::vector<std::uint32_t> band_n;
+  std::vector<std::uint64_t> band_base, band_off{0};
+  std::vector<std::uint32_t> band_edges;
+  double gx0 = 0, gy0 = 0, inv_w = 0, inv_h = 0;
+  int gnx = 1, gny = 1;
+  std::vector<std::uint64_t> cell_off;
+  std::vector<std::uint32_t> cell_ids;
+};
+
+// floor((v - x0) * inv) clamped to [0, n) -- the same IEEE operations the
+// device uses, so the map is monotone in v on both sides.
+inline long cell_of(double v, double x0, double inv, long n) {
+  const double t = (v - x0) * inv;
+  if (!(t > 0.0)) return 0;
+  if (t >= static_cast<double>(n)) return n - 1;
+  return std::min(static_cast<long>(t), n - 1);
+}
+
+void build_level(const fm::HierLevel& L, HostLevel& H) {
+  const std::uint64_t n = L.n_regions();
+  H.band_y0.resize(n);
+  H.band_inv.resize(n);
+  H.band_n.resize(n);
+  H.band_base.resize(n);
+  for (std::uint64_t r = 0; r < n; ++r) {
+    const std::size_t e0 = H.edges.size();
+    for (std::uint64_t k = L.poly_ring[r]; k < L.poly_ring[r + 1]; ++k) {
+      const std::uint64_t b = L.ring_off[k], e = L.ring_off[k + 1], m = e - b;
+      for (std::uint64_t i = 0; i < m; ++i) {  // closed ring (add_ring, geometry.hpp:73-85)
+        const std::uint64_t a = b + i, c = b + (i + 1 < m ? i + 1 : 0);
+        double lx = L.vxy[2 * a], ly = L.vxy[2 * a + 1], hx = L.vxy[2 * c], hy = L.vxy[2 * c + 1];
+        if (ly == hy) continue;  // horizontal edges never cross the ray
+        if (ly > hy) {
+          std::swap(lx, hx);
+          std::swap(ly, hy);
+        }
+        H.edges.push_back(make_double4(lx, ly, hx, hy));
+      }
+    }
+    const std::size_t ne = H.edges.size() - e0;
+    double y0 = 0.0, y1 = 0.0;
+    if (ne) {
+      y0 = H.edges[e0].y;
+      y1 = H.edges[e0].w;
+      for (std::size_t k = e0; k < H.edges.size(); ++k) {
+        y0 = std::min(y0, H.edges[k].y);
+        y1 = std::max(y1, H.edges[k].w);
+      }
+    }
+    std::uint32_t nb = static_cast<std::uint32_t>(std::clamp<std::size_t>(ne / 4, 1, 4096));
+    double inv = 0.0;
+    if (y1 > y0) inv = static_cast<double>(nb) / (y1 - y0);
+    else nb = 1;
+    H.band_y0[r] = y0;
+    H.band_inv[r] = inv;
+    H.band_n[r] = nb;
+    H.band_base[r] = H.band_off.size() - 1;
+    std::vector<std::vector<std::uint32_t>> bands(nb);
+    for (std::size_t k = e0; k < H.edges.size(); ++k) {
+      const long lo = cell_of(H.edges[k].y, y0, inv, nb), hi = cell_of(H.edges[k].w, y0, inv, nb);
+      for (long q = lo; q <= hi; ++q) bands[static_cast<std::size_t>(q)].push_back(static_cast<std::uint32_t>(k));
+    }
+    for (const auto& bl : bands) {
+      H.band_edges.insert(H.band_edges.end(), bl.begin(), bl.end());
+      H.band_off.push_back(H.band_edges.size());
+    }
+  }
+  // bbox grid over the union of the regions' (finite) file bboxes
+  double ux0 = INFINITY, ux1 = -INFINITY, uy0 = INFINITY, uy1 = -INFINITY;
+  for (std::uint64_t r = 0; r < n; ++r) {
+    const double* bb = &L.bbox[4 * r];
+    if (!(std::isfinite(bb[0]) && std::isfinite(bb[1]) && std::isfinite(bb[2]) && std::isfinite(bb[3]))) continue;
+    ux0 = std::min(ux0, bb[0]);
+    ux1 = std::max(ux1, bb[1]);
+    uy0 = std::min(uy0, bb[2]);
+    uy1 = std::max(uy1, bb[3]);
+  }
+  if (!(ux1 > ux0 && uy1 > uy0)) {
+    ux0 = uy0 = 0.0;
+    ux1 = uy1 = 1.0;
+  }
+  const double W = ux1 - ux0, Hh = uy1 - uy0;
+  const double target = std::max<double>(1.0, 4.0 * static_cast<double>(n));
+  H.gnx = static_cast<int>(std::clamp(std::ceil(std::sqrt(target * W / Hh)), 1.0, 65536.0));
+  H.gny = static_cast<int>(std::clamp(std::ceil(target / H.gnx), 1.0, 65536.0));
+  H.gx0 = ux0;
+  H.gy0 = uy0;
+  H.inv_w = H.gnx / W;
+  H.inv_h = H.gny / Hh;
+  std::vector<std::uint32_t> count(static_cast<std::size_t>(H.gnx) * H.gny, 0);
+  auto span = [&](std::uint64_t r, long* cx0, long* cx1, long* cy0, long* cy1) {
+    const double* bb = &L.bbox[4 * r];
+    if (!(bb[0] < bb[1] && bb[2] < bb[3])) return false;  // no point is strictly inside
+    *cx0 = cell_of(bb[0], H.gx0, H.inv_w, H.gnx);
+    *cx1 = cell_of(bb[1], H.gx0, H.inv_w, H.gnx);
+    *cy0 = cell_of(bb[2], H.gy0, H.inv_h, H.gny);
+    *cy1 = cell_of(bb[3], H.gy0, H.inv_h, H.gny);
+    return true;
+  };
+  long a0, a1, b0, b1;
+  for (std::uint64_t r = 0; r < n; ++r) {
+    if (!span(r, &a0, &a1, &b0, &b1)) continue;
+    for (long y = b0; y <= b1; ++y)
+      for (long x = a0; x <= a1; ++x) ++count[static_cast<std::size_t>(y) * H.gnx + x];
+  }
+  H.cell_off.assign(count.size() + 1, 0);
+  for (std::size_t c = 0; c < count.size(); ++c) H.cell_off[c + 1] = H.cell_off[c] + count[c];
+  H.cell_ids.resize(H.cell_off.back());
+  std::vector<std::uint64_t> fill(H.cell_off.begin(), H.cell_off.end() - 1);
+  for (std::uint64_t r = 0; r < n; ++r) {  // ascending ids per cell
+    if (!span(r, &a0, &a1, &b0, &b1)) continue;
+    for (long y = b0; y <= b1; ++y)
+      for (long x = a0; x <= a1; ++x) H.cell_ids[fill[static_cast<std::size_t>(y) * H.gnx + x]++] = static_cast<std::uint32_t>(r);
+  }
+}
+
+__device__ __forceinline__ bool strictly_inside(const double* bb, double px, double py) {
+  return bb[0] < px && px < bb[1] && bb[2] < py && py < bb[3];  // bbox_contains, geometry.hpp:54-57
+}
+
+__device__ __forceinline__ int band_of(double v, double y0, double inv, int nb) {
+  const double t = __dmul_rn(__dsub_rn(v, y0), inv);
+  if (!(t > 0.0)) return 0;
+  if (t >= static_cast<double>(nb)) return nb - 1;
+  return min(static_cast<int>(t), nb - 1);
+}
+
+// points_in_polygon's parity for one region (geometry.hpp:184-210).
+__device__ bool region_pip(const LevelDev& L, int r, double px, double py) {
+  const int nb = static_cast<int>(L.band_n[r]);
+  const int b = band_of(py, L.band_y0[r], L.band_inv[r], nb);
+  const std::uint64_t q = L.band_base[r] + static_cast<std::uint64_t>(b);
+  std::uint32_t par = 0;
+  for (std::uint64_t k = L.band_off[q]; k < L.band_off[q + 1]; ++k) {
+    const double4 e = L.edges[L.band_edges[k]];
+    if (e.y < py && py <= e.w && fm::ray_crosses(px, py, e.x, e.y, e.z, e.w)) par ^= 1u;
+  }
+  return par != 0;
+}
+
+template <bool kStrict, bool kCount>
+__global__ void __launch_bounds__(256)
+    simple_kernel(SimpleParams P, const double2* __restrict__ pts, std::uint64_t n,
+                  std::int32_t* __restrict__ st, std::int32_t* __restrict__ co,
+                  std::int32_t* __restrict__ bl, unsigned long long* __restrict__ evals) {
+  unsigned long long ev = 0;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const double2 p = pts[i];
+    int res[3] = {-1, -1, -1};
+    std::uint32_t lo = 0, hi = static_cast<std::uint32_t>(P.L[0].n);
+#pragma unroll 1
+    for (int l = 0; l < 3 && lo < hi; ++l) {
+      const LevelDev& L = P.L[l];
+      // cells clamp; NaN maps to cell 0 and fails every strict bbox test
+      const int cx = band_of(p.x, L.gx0, L.inv_w, L.gnx), cy = band_of(p.y, L.gy0, L.inv_h, L.gny);
+      const std::uint64_t c = static_cast<std::uint64_t>(cy) * L.gnx + cx;
+      const std::uint64_t k0 = L.cell_off[c], k1 = L.cell_off[c + 1];
+      int cnt = 0, last = -1;
+      for (std::uint64_t k = k0; k < k1; ++k) {
+        const std::uint32_t r = L.cell_ids[k];
+        if (r >= lo && r < hi && strictly_inside(L.bbox + 4 * r, p.x, p.y)) {
+          ++cnt;
+          last = static_cast<int>(r);
+        }
+      }
+      if (cnt == 0) break;
+      int win = -1;
+      if (cnt >= (kStrict ? 1 : 2)) {  // the polygon-tested ("pending") points
+        for (std::uint64_t k = k0; k < k1; ++k) {
+          const std::uint32_t r = L.cell_ids[k];
+          if (r >= lo && r < hi && strictly_inside(L.bbox + 4 * r, p.x, p.y)) {
+            if (kCount) {
+              ++ev;
+              L.tested[r] = 1;
+            }
+            if (region_pip(L, static_cast<int>(r), p.x, p.y)) {
+              win = static_cast<int>(r);
+              break;  // first hit wins (simple_mapper.hpp:98-101)
+            }
+          }
+        }
+      }
+      if (win < 0 && !kStrict) win = last;  // unique or highest-indexed candidate
+      if (win < 0) break;
+      res[l] = win - static_cast<int>(lo);
+      if (l < 2) {
+        lo = L.child_lo[win];
+        hi = L.child_hi[win];
+      }
+    }
+    st[i] = res[0];
+    co[i] = res[1];
+    bl[i] = res[2];
+  }
+  if (kCount) {
+    for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(0xFFFFFFFFu, ev, o);
+    if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
+  }
+}
+
+template <typename T>
+bool upload(const std::vector<T>& v, T** d) {
+  const std::size_t bytes = std::max<std::size_t>(1, v.size()) * sizeof(T);
+  if (cudaMalloc(d, bytes) != cudaSuccess) return false;
+  return v.empty() || cudaMemcpy(*d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess;
+}
+
+}  // namespace
+
+struct fm_simple {
+  int device = -1;
+  SimpleParams P;
+  std::vector<void*> allocs;
+  std::uint64_t n_regions[3] = {0, 0, 0};
+  unsigned long long* d_evals = nullptr;
+};
+
+namespace {
+
+void release(fm_simple* s) {
+  if (s->device >= 0) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    for (void* p : s->allocs) cudaFree(p);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete s;
+}
+
+template <typename T>
+bool add(fm_simple* s, const std::vector<T>& v, const T** out) {
+  T* d = nullptr;
+  if (!upload(v, &d)) return false;
+  s->allocs.push_back(d);
+  *out = d;
+  return true;
+}
+
+fm_status launch_simple(const fm_simple* s, int mode, const double* d_lonlat, std::uint64_t n,
+                        std::int32_t* st, std::int32_t* co, std::int32_t* bl, bool count,
+                        cudaStream_t stream) {
+  if (n == 0) return FM_OK;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+  const std::uint64_t want = (n + 255) / 256;
+  const int grid = static_cast<int>(std::min<std::uint64_t>(want, static_cast<std::uint64_t>(std::max(1, sms)) * 16));
+  const double2* p = reinterpret_cast<const double2*>(d_lonlat);
+  const bool strict = mode == FM_ASSIGN_STRICT;
+  if (strict && count) simple_kernel<true, true><<<grid, 256, 0, stream>>>(s->P, p, n, st, co, bl, s->d_evals);
+  else if (strict) simple_kernel<true, false><<<grid, 256, 0, stream>>>(s->P, p, n, st, co, bl, s->d_evals);
+  else if (count) simple_kernel<false, true><<<grid, 256, 0, stream>>>(s->P, p, n, st, co, bl, s->d_evals);
+  else simple_kernel<false, false><<<grid, 256, 0, stream>>>(s->P, p, n, st, co, bl, s->d_evals);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fm_set_error(FM_ERR_CUDA, (std::string("simple_kernel: ") + cudaGetErrorString(e)).c_str());
+  return FM_OK;
+}
+
+// pip_calls: regions that received at least one polygon test (one batch
+// per region per resolve_level call in the reference; every region has a
+// single parent, so that is one call per tested region)
+fm_status collect_counters(const fm_simple* s, fm_assign_counters* out) {
+  unsigned long long ev = 0;
+  if (cudaMemcpy(&ev, s->d_evals, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    return fm_set_error(FM_ERR_CUDA, "counter readback failed");
+  }
+  std::uint64_t calls = 0;
+  for (int l = 0; l < 3; ++l) {
+    std::vector<unsigned char> t(s->n_regions[l]);
+    if (!t.empty() && cudaMemcpy(t.data(), s->P.L[l].tested, t.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      return fm_set_error(FM_ERR_CUDA, "counter readback failed");
+    }
+    for (unsigned char x : t) calls += x;
+  }
+  out->pip_point_evaluations += ev;
+  out->pip_calls += calls;
+  return FM_OK;
+}
+
+fm_status reset_counters(const fm_simple* s) {
+  if (cudaMemset(s->d_evals, 0, 8) != cudaSuccess) return fm_set_error(FM_ERR_CUDA, "counter reset failed");
+  for (int l = 0; l < 3; ++l) {
+    if (s->n_regions[l] && cudaMemset(s->P.L[l].tested, 0, s->n_regions[l]) != cudaSuccess) {
+      return fm_set_error(FM_ERR_CUDA, "counter reset failed");
+    }
+  }
+  return FM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fm_status fm_simple_build(const fm_hierarchy* h, int device, fm_simple** out) {
+  if (!h || !out) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    return fm_set_error(FM_ERR_NO_DEVICE, "no CUDA device available; the simple engine has no CPU fallback");
+  }
+  if (device < 0 || device >= count) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "CUDA device ordinal out of range");
+  fm_simple* s = new (std::nothrow) fm_simple();
+  if (!s) return fm_set_error(FM_ERR_OOM, "host allocation failed");
+  s->device = device;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  bool ok = true;
+  try {
+    for (int l = 0; l < 3 && ok; ++l) {
+      const fm::HierLevel& L = h->level[l];
+      HostLevel H;
+      build_level(L, H);
+      LevelDev& D = s->P.L[l];
+      D.n = static_cast<int>(L.n_regions());
+      s->n_regions[l] = L.n_regions();
+      D.gx0 = H.gx0;
+      D.gy0 = H.gy0;
+      D.inv_w = H.inv_w;
+      D.inv_h = H.inv_h;
+      D.gnx = H.gnx;
+      D.gny = H.gny;
+      std::vector<std::uint32_t> lo = L.child_lo, hi = L.child_hi;
+      ok = add(s, L.bbox, &D.bbox) && add(s, lo, &D.child_lo) && add(s, hi, &D.child_hi) &&
+           add(s, H.edges, &D.edges) && add(s, H.band_y0, &D.band_y0) &&
+           add(s, H.band_inv, &D.band_inv) && add(s, H.band_n, &D.band_n) &&
+           add(s, H.band_base, &D.band_base) && add(s, H.band_off, &D.band_off) &&
+           add(s, H.band_edges, &D.band_edges) && add(s, H.cell_off, &D.cell_off) &&
+           add(s, H.cell_ids, &D.cell_ids);
+      if (ok) {
+        unsigned char* t = nullptr;
+        ok = cudaMalloc(&t, std::max<std::uint64_t>(1, L.n_regions())) == cudaSuccess;
+        if (ok) {
+          s->allocs.push_back(t);
+          D.tested = t;
+        }
+      }
+    }
+    if (ok) {
+      ok = cudaMalloc(&s->d_evals, 8) == cudaSuccess;
+      if (ok) s->allocs.push_back(s->d_evals);
+    }
+  } catch (const std::bad_alloc&) {
+    ok = false;
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  if (!ok) {
+    release(s);
+    return fm_set_error(FM_ERR_OOM, "simple-engine build: allocation failed");
+  }
+  *out = s;
+  return FM_OK;
+}
+
+void fm_simple_destroy(fm_simple* s) {
+  if (s) release(s);
+}
+
+fm_status fm_simple_assign(const fm_simple* s, int mode, const double* d_lonlat, uint64_t n,
+                           int32_t* d_state, int32_t* d_county, int32_t* d_block,
+                           fm_assign_counters* counters, void* stream) {
+  if (!s) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "null engine");
+  if (mode != FM_ASSIGN_RELAXED && mode != FM_ASSIGN_STRICT) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "unknown assign mode");
+  if (n && (!d_lonlat || !d_state || !d_county || !d_block)) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "null buffer");
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s->device);
+  fm_status st = FM_OK;
+  if (counters) st = reset_counters(s);
+  if (st == FM_OK) {
+    st = launch_simple(s, mode, d_lonlat, n, d_state, d_county, d_block, counters != nullptr,
+                       static_cast<cudaStream_t>(stream));
+  }
+  if (st == FM_OK && counters) {  // counters make the call synchronous
+    if (cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess) st = fm_set_error(FM_ERR_CUDA, "simple_kernel failed");
+    else st = collect_counters(s, counters);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  return st;
+}
+
+fm_status fm_simple_assign_host(const fm_simple* s, int mode, const double* lonlat, uint64_t n,
+                                int32_t* state, int32_t* county, int32_t* block,
+                                fm_assign_counters* counters) {
+  if (!s) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "null engine");
+  if (mode != FM_ASSIGN_RELAXED && mode != FM_ASSIGN_STRICT) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "unknown assign mode");
+  if (n == 0) return FM_OK;
+  if (!lonlat || !state || !county || !block) return fm_set_error(FM_ERR_INVALID_ARGUMENT, "null buffer");
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s->device);
+  const std::uint64_t chunk = std::uint64_t{1} << 23;
+  void* buf = nullptr;
+  fm_status st = FM_OK;
+  if (cudaMalloc(&buf, std::min(chunk, n) * 28) != cudaSuccess) st = fm_set_error(FM_ERR_OOM, "device buffer");
+  if (st == FM_OK && counters) st = reset_counters(s);  // one batch: regions counted once
+  for (std::uint64_t off = 0; off < n && st == FM_OK; off += chunk) {
+    const std::uint64_t m = std::min(chunk, n - off);
+    double* d_p = static_cast<double*>(buf);
+    std::int32_t* d_s = reinterpret_cast<std::int32_t*>(d_p + 2 * m);
+    std::int32_t* d_c = d_s + m;
+    std::int32_t* d_b = d_c + m;
+    if (cudaMemcpy(d_p, lonlat + 2 * off, m * 16, cudaMemcpyHostToDevice) != cudaSuccess) {
+      st = fm_set_error(FM_ERR_CUDA, "copy failed");
+      break;
+    }
+    st = launch_simple(s, mode, d_p, m, d_s, d_c, d_b, counters != nullptr, nullptr);
+    if (st == FM_OK &&
+        (cudaMemcpy(state + off, d_s, m * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+         cudaMemcpy(county + off, d_c, m * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+         cudaMemcpy(block + off, d_b, m * 4, cudaMemcpyDeviceToHost) != cudaSuccess)) {
+      st = fm_set_error(FM_ERR_CUDA, "copy failed");
+    }
+  }
+  if (buf) cudaFree(buf);
+  if (st == FM_OK && counters) st = collect_counters(s, counters);
+  if (prev >= 0) cudaSetDevice(prev);
+  return st;
+}
+
+}  // extern "C"

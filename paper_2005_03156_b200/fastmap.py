@@ -23,6 +23,8 @@ reference (file:line)                        here
 FMCI save/load cell_index.hpp:641-726         :meth:`CellIndex.save` / :func:`load_index`
 ``read_points_f64`` io.hpp:154-167            :func:`read_points_f64`
 assign CSV tools/fastmap.cpp:288-301          :func:`write_assign_csv`
+``AssignMode``, ``assign`` simple_mapper.hpp  :class:`AssignMode`, :func:`assign` (the simple
+  :24, :119-166                               engine on the GPU, :class:`SimpleEngine`)
 ===========================================  =====================================
 
 Exceptions: ``std::invalid_argument`` -> ``ValueError``,
@@ -476,6 +478,64 @@ def query_leaves(trie, leaves, points, mode: CoverMode = CoverMode.exact) -> Ass
 
 def query(trie, leaves, points, mode: CoverMode = CoverMode.exact) -> AssignmentResult:
     return query_leaves(trie, leaves, points, mode)
+
+
+class AssignMode(enum.IntEnum):
+    """simple_mapper.hpp:24."""
+    relaxed = 0
+    strict = 1
+
+
+class SimpleEngine:
+    """The simple engine's device structures for one hierarchy (fm_simple)."""
+
+    def __init__(self, h: Hierarchy, device: int = 0) -> None:
+        self._s = None
+        s = C.c_void_p()
+        N.check(N.lib().fm_simple_build(h._h, int(device), C.byref(s)), "fm_simple_build")
+        self._s = s
+        self.device = device
+        self.hierarchy = h
+
+    def __del__(self) -> None:
+        if getattr(self, "_s", None):
+            lib = N.lib() if N is not None else None
+            if lib is not None:
+                lib.fm_simple_destroy(self._s)
+            self._s = None
+
+    def assign(self, points, mode: AssignMode = AssignMode.relaxed, counters: bool = True,
+               out=None, stream=None) -> AssignmentResult:
+        """Host numpy points -> AssignmentResult; CUDA tensors -> (state, county,
+        block) tensors written on ``stream`` (counters make it synchronous)."""
+        L = N.lib()
+        cnt = N.AssignCountersC()
+        cp = C.byref(cnt) if counters else None
+        if isinstance(points, np.ndarray):
+            pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+            n = pts.shape[0]
+            st, co, bl = (np.empty(n, dtype=np.int32) for _ in range(3))
+            N.check(L.fm_simple_assign_host(self._s, int(mode), N.ptr(pts, C.c_double), n,
+                                            N.ptr(st, C.c_int32), N.ptr(co, C.c_int32),
+                                            N.ptr(bl, C.c_int32), cp), "fm_simple_assign_host")
+            return AssignmentResult(st, co, bl, AssignCounters(int(cnt.pip_point_evaluations),
+                                                               int(cnt.pip_calls)))
+        import torch
+        n = points.numel() // 2
+        if out is None:
+            out = tuple(torch.empty(n, dtype=torch.int32, device=points.device) for _ in range(3))
+        if stream is None:
+            stream = torch.cuda.current_stream(points.device).cuda_stream
+        N.check(L.fm_simple_assign(self._s, int(mode), C.c_void_p(points.data_ptr()), n,
+                                   *[C.c_void_p(t.data_ptr()) for t in out], cp,
+                                   C.c_void_p(stream)), "fm_simple_assign")
+        return out
+
+
+def assign(h, points, mode: AssignMode = AssignMode.relaxed, device: int = 0) -> AssignmentResult:
+    """assign(h, points, mode) (simple_mapper.hpp:119-166) on the GPU."""
+    eng = h if isinstance(h, SimpleEngine) else SimpleEngine(h, device)
+    return eng.assign(points, mode)
 
 
 def exhaustive_assign(leaves, points, device: int = 0) -> np.ndarray:

@@ -138,3 +138,21 @@ def test_hierarchy_index_build_host_only():
     h = fastmap.load_hierarchy(GOLD / "hier_2x2x3.fmcb")
     idx = fastmap.build_cover(h, device=-1)
     assert idx.stats()["n_polys"] == 12
+
+
+def test_python_written_fmcb_loads_like_the_reference(tmp_path):
+    import fmcb_writer
+    p = tmp_path / "adv.fmcb"
+    states = fmcb_writer.random_hierarchy(5)
+    fmcb_writer.write_fmcb(p, states)
+    if oracle.ref_available():
+        assert oracle.ref_load_fmcb_status(p) == 0
+    h = fastmap.load_hierarchy(p)
+    assert (h.n_states, h.n_counties, h.n_leaves) == (3, 9, 36)
+    leaves = [b for s in states for c in s["children"] for b in c["children"]]
+    assert [f.decode() for f in h.fips12] == [b["fips"] for b in leaves]
+    for k, b in enumerate(leaves):  # rings in file order, collect_leaves order
+        got = h.soup.polygon(k)
+        assert len(got) == len(b["rings"])
+        for r, want in zip(got, b["rings"]):
+            assert np.array_equal(r, np.asarray(want, dtype=np.float64))
