@@ -33,6 +33,9 @@ METRIC = "points projected/sec (device-timed)"
 UNIT = "points/s"
 
 WORKLOADS = {
+    "c3s": "c3s: 320,000-leaf nested hierarchy (10x5 states, 8x8 counties, 10x10 blocks, "
+           "6 segs/edge), all three levels as FMCB, 100M clustered fp64 points",
+    "c3mini": "c3mini: 40,000-leaf nested hierarchy (2x2 states, 4x4 counties, 25x25 blocks)",
     "c1": "c1: 1,024-polygon 32x32 jittered tiling (8 segs/edge, ~32 v), 1M uniform fp64 points",
     "c2": "c2: 250,000-polygon 500x500 jittered tiling (12 segs/edge, ~48 v), "
           "100M clustered fp64 points (2000 Zipf(1.1) centres, sigma 0.2 deg, 10% uniform)",
@@ -44,7 +47,7 @@ WORKLOADS = {
           "histogram all-reduced with NCCL",
 }
 # reference cover depth for the CPU arm (SURVEY.md sec. 6 probes: best per config)
-REF_MAX_LEVEL = {"c1": 12, "c2": 16, "c4": 16, "c3": 18, "c5": 18}
+REF_MAX_LEVEL = {"c1": 12, "c2": 16, "c4": 16, "c3": 18, "c5": 18, "c3s": 16, "c3mini": 14}
 
 
 def parse():
@@ -56,8 +59,9 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--points", type=int, default=0, help="points per GPU (default: config size)")
     ap.add_argument("--hist", action="store_true", help="also build the per-block int64 histogram")
-    ap.add_argument("--mode", default="exact", choices=["exact", "approx"],
-                    help="CoverMode of the projection (approx: deemed leaves, error <= epsilon)")
+    ap.add_argument("--mode", default="exact", choices=["exact", "approx", "simple", "simple-strict"],
+                    help="CoverMode of the projection (approx: deemed leaves, error <= epsilon); "
+                         "simple[-strict]: the hierarchical simple engine (nested configs)")
     ap.add_argument("--epsilon", type=float, default=5e-3,
                     help="approx-mode cell diagonal bound in degrees")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -371,10 +375,117 @@ def run_ours(args):
     return 0 if mismatches == 0 else 3
 
 
+def run_simple(args):
+    """The simple engine (simple_mapper.hpp:119-166) on one nested config:
+    one step = assign() of the rank's resident points (one kernel)."""
+    import tempfile
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_03156_b200 import fastmap, synth
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    cfg = synth.config(args.config)
+    if not hasattr(cfg, "write_fmcb"):
+        raise SystemExit("--mode simple needs a nested config (c3s, c3mini, c3)")
+    mode = fastmap.AssignMode.strict if args.mode == "simple-strict" else fastmap.AssignMode.relaxed
+    n = args.points or cfg.n_points
+    pts_host = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    cfg.make_points(n, offset=rank * n, out=pts_host.numpy())
+    fd, path = tempfile.mkstemp(suffix=".fmcb")
+    os.close(fd)
+    t0 = time.perf_counter()
+    cfg.write_fmcb(path)
+    h = fastmap.load_hierarchy(path)
+    eng = fastmap.SimpleEngine(h, local)
+    build_s = time.perf_counter() - t0
+    d_pts = pts_host.to(dev)
+    outs = tuple(torch.empty(n, dtype=torch.int32, device=dev) for _ in range(3))
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eng.assign(d_pts, mode, counters=False, out=outs, stream=stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    # parity: the reference's own assign() on the same FMCB bytes (oracle/_ref)
+    import oracle
+    chk = np.random.default_rng(rank).choice(n, size=min(n, 20_000), replace=False)
+    parity = {"checked_points": int(len(chk))}
+    if oracle.ref_available():
+        st, co, bl, _ = oracle.ref_simple_assign(path, pts_host.numpy()[chk],
+                                                 mode == fastmap.AssignMode.strict)
+        got = [o.cpu().numpy()[chk] for o in outs]
+        parity["mismatches_vs_reference"] = int(((got[0] != st) | (got[1] != co) |
+                                                 (got[2] != bl)).sum())
+    e2e = None
+    if not args.no_e2e:
+        ph = pts_host.numpy()
+        eng.assign(ph[: min(n, 1 << 20)], mode, counters=False)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            eng.assign(ph, mode, counters=False)
+        el = time.perf_counter() - t0
+        e2e = {"value": n * world * args.e2e_steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 12 * n,
+               "path": "fm_simple_assign_host (8M-point chunks)"}
+    os.unlink(path)
+    peak, peak_kind = measured_peaks()
+    launch_ms = ms / args.steps
+    alg_bytes = 28.0 * n + 16.0 * (h.soup.n_vertices)  # 16 B in + 3 x 4 B out per point
+    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n * world * args.steps / (ms_max / 1e3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE recipe; see DESIGN.md sec. 3)",
+            "config": {"workload": WORKLOADS.get(args.config, args.config), "mode": args.mode,
+                       "points_per_gpu": n, "global_points": n * world,
+                       "states": int(h.n_states), "counties": int(h.n_counties),
+                       "blocks": int(h.n_leaves), "parallelism": f"point shards x{world}",
+                       "l2": "inputs larger than L2 (16 B/pt stream), no flush",
+                       "engine_build_s": build_s},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel": "fm_simple_assign = simple_kernel", "launch_ms": launch_ms},
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": args.steps,
+            "clocks": clk.summary(), "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if parity.get("mismatches_vs_reference", 0) == 0 else 3
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode in ("simple", "simple-strict"):
+        return run_simple(args)
     return run_ours(args)
 
 

@@ -183,6 +183,8 @@ def synth() -> C.CDLL:
         L.synth_nested.argtypes = [C.c_uint32] * 7 + [C.c_double] * 6 + [u64, C.c_int, PD, PU64,
                                                                         PU64, PU32]
         L.synth_points_uniform.restype = C.c_int
+        L.synth_nested_fmcb.argtypes = [C.c_uint32] * 7 + [C.c_double] * 6 + [u64, C.c_int, C.c_char_p]
+        L.synth_nested_fmcb.restype = C.c_int
         L.synth_points_uniform.argtypes = [PD, u64, u64, u64, C.c_int, PD]
         L.synth_points_clustered.restype = C.c_int
         L.synth_points_clustered.argtypes = [PD, PD, u64, u64, u64, C.c_uint32,

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -72,6 +73,179 @@ void parallel_for(std::uint64_t n, int threads, Fn fn) {
     if (b < e) pool.emplace_back(fn, b, e);
   }
   for (auto& th : pool) th.join();
+}
+
+// The conformal nested lattice of synth_nested: node positions and the
+// shared edge subdivision points, in lon/lat.  Regions spanning lattice
+// cells [i0, i1) x [j0, j1) (a block, a county or a state) take their ring
+// from the same shared points, so every level tiles its parent exactly.
+struct NestedLattice {
+  std::uint64_t NX = 0, NY = 0, S = 0;
+  std::vector<double> gx, gy, hxy, vxy_e;
+  // ring of the region [i0, i1) x [j0, j1), counter-clockwise from (i0, j0)
+  std::uint64_t ring(std::uint64_t i0, std::uint64_t i1, std::uint64_t j0, std::uint64_t j1,
+                     double* out) const {
+    std::uint64_t w = 0;
+    auto put = [&](double x, double y) {
+      out[2 * w] = x;
+      out[2 * w + 1] = y;
+      ++w;
+    };
+    auto node = [&](std::uint64_t i, std::uint64_t j) {
+      const std::uint64_t k = j * (NX + 1) + i;
+      put(gx[k], gy[k]);
+    };
+    for (std::uint64_t i = i0; i < i1; ++i) {  // bottom, left to right
+      node(i, j0);
+      const double* h = hxy.data() + 2 * (j0 * NX + i) * (S - 1);
+      for (std::uint64_t k = 0; k + 1 < S; ++k) put(h[2 * k], h[2 * k + 1]);
+    }
+    for (std::uint64_t j = j0; j < j1; ++j) {  // right, bottom to top
+      node(i1, j);
+      const double* v = vxy_e.data() + 2 * (j * (NX + 1) + i1) * (S - 1);
+      for (std::uint64_t k = 0; k + 1 < S; ++k) put(v[2 * k], v[2 * k + 1]);
+    }
+    for (std::uint64_t i = i1; i-- > i0;) {  // top, right to left
+      node(i + 1, j1);
+      const double* h = hxy.data() + 2 * (j1 * NX + i) * (S - 1);
+      for (std::uint64_t k = S - 1; k-- > 0;) put(h[2 * k], h[2 * k + 1]);
+    }
+    for (std::uint64_t j = j1; j-- > j0;) {  // left, top to bottom
+      node(i0, j + 1);
+      const double* v = vxy_e.data() + 2 * (j * (NX + 1) + i0) * (S - 1);
+      for (std::uint64_t k = S - 1; k-- > 0;) put(v[2 * k], v[2 * k + 1]);
+    }
+    return w;
+  }
+};
+
+bool build_nested(std::uint32_t sx, std::uint32_t sy, std::uint32_t cx, std::uint32_t cy,
+                  std::uint32_t bx, std::uint32_t by, std::uint32_t segs, double jitter,
+                  double sigma, double x0, double x1, double y0, double y1, std::uint64_t seed,
+                  int threads, NestedLattice& LAT) {
+  if (!sx || !sy || !cx || !cy || !bx || !by || !segs) return false;
+  const std::uint64_t NX = std::uint64_t{sx} * cx * bx, NY = std::uint64_t{sy} * cy * by;
+  const std::uint64_t S = segs;
+  const std::uint64_t CX = std::uint64_t{cx} * bx, CY = std::uint64_t{cy} * by;  // blocks per state
+  const double cw = (x1 - x0) / static_cast<double>(NX);
+  const double ch = (y1 - y0) / static_cast<double>(NY);
+  auto map_x = [&](double u) { return x0 + u * cw; };
+  auto map_y = [&](double v) { return y0 + v * ch; };
+  // state corners (lattice units of blocks)
+  std::vector<double> su((sx + 1) * (sy + 1)), sv((sx + 1) * (sy + 1));
+  for (std::uint32_t j = 0; j <= sy; ++j)
+    for (std::uint32_t i = 0; i <= sx; ++i) {
+      const std::uint64_t k = std::uint64_t{j} * (sx + 1) + i;
+      double u = static_cast<double>(i * CX), v = static_cast<double>(j * CY);
+      if (i > 0 && i < sx && j > 0 && j < sy && jitter > 0) {
+        u += jitter * CX * (2.0 * unit(draw(seed, 31, 2 * k)) - 1.0);
+        v += jitter * CY * (2.0 * unit(draw(seed, 31, 2 * k + 1)) - 1.0);
+      }
+      su[k] = u;
+      sv[k] = v;
+    }
+  // county corners: global county lattice (sx*cx + 1) x (sy*cy + 1)
+  const std::uint64_t KX = std::uint64_t{sx} * cx, KY = std::uint64_t{sy} * cy;
+  std::vector<double> ku((KX + 1) * (KY + 1)), kv((KX + 1) * (KY + 1));
+  auto bilerp = [](const double* q, double a, double b) {  // q: 00, 10, 01, 11
+    return (1 - a) * (1 - b) * q[0] + a * (1 - b) * q[1] + (1 - a) * b * q[2] + a * b * q[3];
+  };
+  parallel_for(KY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t J = jb; J < je; ++J)
+      for (std::uint64_t I = 0; I <= KX; ++I) {
+        const std::uint64_t si = std::min<std::uint64_t>(I / cx, sx - 1), sj = std::min<std::uint64_t>(J / cy, sy - 1);
+        const double a = static_cast<double>(I - si * cx) / cx, b = static_cast<double>(J - sj * cy) / cy;
+        const std::uint64_t c00 = sj * (sx + 1) + si;
+        const double qu[4] = {su[c00], su[c00 + 1], su[c00 + sx + 1], su[c00 + sx + 2]};
+        const double qv[4] = {sv[c00], sv[c00 + 1], sv[c00 + sx + 1], sv[c00 + sx + 2]};
+        double u = bilerp(qu, a, b), v = bilerp(qv, a, b);
+        const bool on_state_edge = (I % cx == 0) || (J % cy == 0);
+        if (!on_state_edge && jitter > 0) {
+          const std::uint64_t k = J * (KX + 1) + I;
+          u += jitter * bx * (2.0 * unit(draw(seed, 32, 2 * k)) - 1.0);
+          v += jitter * by * (2.0 * unit(draw(seed, 32, 2 * k + 1)) - 1.0);
+        }
+        ku[J * (KX + 1) + I] = u;
+        kv[J * (KX + 1) + I] = v;
+      }
+  });
+  // block lattice nodes (global), lattice units
+  std::vector<double> lu((NX + 1) * (NY + 1)), lv((NX + 1) * (NY + 1));
+  parallel_for(NY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t J = jb; J < je; ++J)
+      for (std::uint64_t I = 0; I <= NX; ++I) {
+        const std::uint64_t ki = std::min<std::uint64_t>(I / bx, KX - 1), kj = std::min<std::uint64_t>(J / by, KY - 1);
+        const double a = static_cast<double>(I - ki * bx) / bx, b = static_cast<double>(J - kj * by) / by;
+        const std::uint64_t c00 = kj * (KX + 1) + ki;
+        const double qu[4] = {ku[c00], ku[c00 + 1], ku[c00 + KX + 1], ku[c00 + KX + 2]};
+        const double qv[4] = {kv[c00], kv[c00 + 1], kv[c00 + KX + 1], kv[c00 + KX + 2]};
+        double u = bilerp(qu, a, b), v = bilerp(qv, a, b);
+        const bool on_county_edge = (I % bx == 0) || (J % by == 0);
+        if (!on_county_edge && jitter > 0) {
+          const std::uint64_t k = J * (NX + 1) + I;
+          u += jitter * (2.0 * unit(draw(seed, kStreamJitter, 2 * k)) - 1.0);
+          v += jitter * (2.0 * unit(draw(seed, kStreamJitter, 2 * k + 1)) - 1.0);
+        }
+        lu[J * (NX + 1) + I] = u;
+        lv[J * (NX + 1) + I] = v;
+      }
+  });
+  // edge subdivision points (lon/lat), shared by both neighbours
+  const std::uint64_t nh = NX * (NY + 1), nv = (NX + 1) * NY;
+  std::vector<double>& hxy = LAT.hxy;
+  std::vector<double>& vxy_e = LAT.vxy_e;
+  hxy.assign(2 * nh * (S - 1) + 2, 0.0);
+  vxy_e.assign(2 * nv * (S - 1) + 2, 0.0);
+  auto subdivide = [&](double au, double av, double bu, double bv, bool border,
+                       std::uint64_t stream, std::uint64_t e, double* dst) {
+    const double du = bu - au, dv = bv - av;
+    const double len = std::sqrt(du * du + dv * dv);
+    const double nu = len > 0 ? -dv / len : 0.0, nvv = len > 0 ? du / len : 0.0;
+    for (std::uint64_t k = 1; k < S; ++k) {
+      const double t = static_cast<double>(k) / static_cast<double>(S);
+      double u = au + du * t, v = av + dv * t;
+      if (!border && sigma > 0.0) {
+        const std::uint64_t idx = 2 * (e * S + k);
+        const double d = sigma * gauss(draw(seed, stream, idx), draw(seed, stream, idx + 1));
+        u += d * nu;
+        v += d * nvv;
+      }
+      dst[2 * (k - 1)] = map_x(u);
+      dst[2 * (k - 1) + 1] = map_y(v);
+    }
+  };
+  parallel_for(NY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t j = jb; j < je; ++j)
+      for (std::uint64_t i = 0; i < NX; ++i) {
+        const std::uint64_t e = j * NX + i, a = j * (NX + 1) + i;
+        subdivide(lu[a], lv[a], lu[a + 1], lv[a + 1], j == 0 || j == NY, kStreamHEdge, e,
+                  hxy.data() + 2 * e * (S - 1));
+      }
+  });
+  parallel_for(NY, threads, [&](std::uint64_t jb, std::uint64_t je) {
+    for (std::uint64_t j = jb; j < je; ++j)
+      for (std::uint64_t i = 0; i <= NX; ++i) {
+        const std::uint64_t e = j * (NX + 1) + i, a = e;
+        subdivide(lu[a], lv[a], lu[a + NX + 1], lv[a + NX + 1], i == 0 || i == NX, kStreamVEdge, e,
+                  vxy_e.data() + 2 * e * (S - 1));
+      }
+  });
+  std::vector<double>& gx = LAT.gx;
+  std::vector<double>& gy = LAT.gy;
+  gx.assign((NX + 1) * (NY + 1), 0.0);
+  gy.assign((NX + 1) * (NY + 1), 0.0);
+  for (std::uint64_t j = 0; j <= NY; ++j)
+    for (std::uint64_t i = 0; i <= NX; ++i) {
+      const std::uint64_t k = j * (NX + 1) + i;
+      gx[k] = (i == 0) ? x0 : (i == NX) ? x1 : map_x(lu[k]);
+      gy[k] = (j == 0) ? y0 : (j == NY) ? y1 : map_y(lv[k]);
+    }
+  std::vector<double>().swap(lu);
+  std::vector<double>().swap(lv);
+  LAT.NX = NX;
+  LAT.NY = NY;
+  LAT.S = S;
+  return true;
 }
 
 }  // namespace
@@ -221,119 +395,14 @@ int synth_nested(std::uint32_t sx, std::uint32_t sy, std::uint32_t cx, std::uint
                  double sigma, double x0, double x1, double y0, double y1, std::uint64_t seed,
                  int threads, double* vxy, std::uint64_t* ring_off, std::uint64_t* poly_ring,
                  std::uint32_t* scb) {
-  if (!sx || !sy || !cx || !cy || !bx || !by || !segs) return 1;
-  const std::uint64_t NX = std::uint64_t{sx} * cx * bx, NY = std::uint64_t{sy} * cy * by;
-  const std::uint64_t S = segs;
+  NestedLattice LAT;
+  if (!build_nested(sx, sy, cx, cy, bx, by, segs, jitter, sigma, x0, x1, y0, y1, seed, threads, LAT)) return 1;
+  const std::uint64_t NX = LAT.NX, NY = LAT.NY, S = LAT.S;
   const std::uint64_t CX = std::uint64_t{cx} * bx, CY = std::uint64_t{cy} * by;  // blocks per state
-  const double cw = (x1 - x0) / static_cast<double>(NX);
-  const double ch = (y1 - y0) / static_cast<double>(NY);
-  auto map_x = [&](double u) { return x0 + u * cw; };
-  auto map_y = [&](double v) { return y0 + v * ch; };
-  // state corners (lattice units of blocks)
-  std::vector<double> su((sx + 1) * (sy + 1)), sv((sx + 1) * (sy + 1));
-  for (std::uint32_t j = 0; j <= sy; ++j)
-    for (std::uint32_t i = 0; i <= sx; ++i) {
-      const std::uint64_t k = std::uint64_t{j} * (sx + 1) + i;
-      double u = static_cast<double>(i * CX), v = static_cast<double>(j * CY);
-      if (i > 0 && i < sx && j > 0 && j < sy && jitter > 0) {
-        u += jitter * CX * (2.0 * unit(draw(seed, 31, 2 * k)) - 1.0);
-        v += jitter * CY * (2.0 * unit(draw(seed, 31, 2 * k + 1)) - 1.0);
-      }
-      su[k] = u;
-      sv[k] = v;
-    }
-  // county corners: global county lattice (sx*cx + 1) x (sy*cy + 1)
-  const std::uint64_t KX = std::uint64_t{sx} * cx, KY = std::uint64_t{sy} * cy;
-  std::vector<double> ku((KX + 1) * (KY + 1)), kv((KX + 1) * (KY + 1));
-  auto bilerp = [](const double* q, double a, double b) {  // q: 00, 10, 01, 11
-    return (1 - a) * (1 - b) * q[0] + a * (1 - b) * q[1] + (1 - a) * b * q[2] + a * b * q[3];
-  };
-  parallel_for(KY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
-    for (std::uint64_t J = jb; J < je; ++J)
-      for (std::uint64_t I = 0; I <= KX; ++I) {
-        const std::uint64_t si = std::min<std::uint64_t>(I / cx, sx - 1), sj = std::min<std::uint64_t>(J / cy, sy - 1);
-        const double a = static_cast<double>(I - si * cx) / cx, b = static_cast<double>(J - sj * cy) / cy;
-        const std::uint64_t c00 = sj * (sx + 1) + si;
-        const double qu[4] = {su[c00], su[c00 + 1], su[c00 + sx + 1], su[c00 + sx + 2]};
-        const double qv[4] = {sv[c00], sv[c00 + 1], sv[c00 + sx + 1], sv[c00 + sx + 2]};
-        double u = bilerp(qu, a, b), v = bilerp(qv, a, b);
-        const bool on_state_edge = (I % cx == 0) || (J % cy == 0);
-        if (!on_state_edge && jitter > 0) {
-          const std::uint64_t k = J * (KX + 1) + I;
-          u += jitter * bx * (2.0 * unit(draw(seed, 32, 2 * k)) - 1.0);
-          v += jitter * by * (2.0 * unit(draw(seed, 32, 2 * k + 1)) - 1.0);
-        }
-        ku[J * (KX + 1) + I] = u;
-        kv[J * (KX + 1) + I] = v;
-      }
-  });
-  // block lattice nodes (global), lattice units
-  std::vector<double> lu((NX + 1) * (NY + 1)), lv((NX + 1) * (NY + 1));
-  parallel_for(NY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
-    for (std::uint64_t J = jb; J < je; ++J)
-      for (std::uint64_t I = 0; I <= NX; ++I) {
-        const std::uint64_t ki = std::min<std::uint64_t>(I / bx, KX - 1), kj = std::min<std::uint64_t>(J / by, KY - 1);
-        const double a = static_cast<double>(I - ki * bx) / bx, b = static_cast<double>(J - kj * by) / by;
-        const std::uint64_t c00 = kj * (KX + 1) + ki;
-        const double qu[4] = {ku[c00], ku[c00 + 1], ku[c00 + KX + 1], ku[c00 + KX + 2]};
-        const double qv[4] = {kv[c00], kv[c00 + 1], kv[c00 + KX + 1], kv[c00 + KX + 2]};
-        double u = bilerp(qu, a, b), v = bilerp(qv, a, b);
-        const bool on_county_edge = (I % bx == 0) || (J % by == 0);
-        if (!on_county_edge && jitter > 0) {
-          const std::uint64_t k = J * (NX + 1) + I;
-          u += jitter * (2.0 * unit(draw(seed, kStreamJitter, 2 * k)) - 1.0);
-          v += jitter * (2.0 * unit(draw(seed, kStreamJitter, 2 * k + 1)) - 1.0);
-        }
-        lu[J * (NX + 1) + I] = u;
-        lv[J * (NX + 1) + I] = v;
-      }
-  });
-  // edge subdivision points (lon/lat), shared by both neighbours
-  const std::uint64_t nh = NX * (NY + 1), nv = (NX + 1) * NY;
-  std::vector<double> hxy(2 * nh * (S - 1) + 2), vxy_e(2 * nv * (S - 1) + 2);
-  auto subdivide = [&](double au, double av, double bu, double bv, bool border,
-                       std::uint64_t stream, std::uint64_t e, double* dst) {
-    const double du = bu - au, dv = bv - av;
-    const double len = std::sqrt(du * du + dv * dv);
-    const double nu = len > 0 ? -dv / len : 0.0, nvv = len > 0 ? du / len : 0.0;
-    for (std::uint64_t k = 1; k < S; ++k) {
-      const double t = static_cast<double>(k) / static_cast<double>(S);
-      double u = au + du * t, v = av + dv * t;
-      if (!border && sigma > 0.0) {
-        const std::uint64_t idx = 2 * (e * S + k);
-        const double d = sigma * gauss(draw(seed, stream, idx), draw(seed, stream, idx + 1));
-        u += d * nu;
-        v += d * nvv;
-      }
-      dst[2 * (k - 1)] = map_x(u);
-      dst[2 * (k - 1) + 1] = map_y(v);
-    }
-  };
-  parallel_for(NY + 1, threads, [&](std::uint64_t jb, std::uint64_t je) {
-    for (std::uint64_t j = jb; j < je; ++j)
-      for (std::uint64_t i = 0; i < NX; ++i) {
-        const std::uint64_t e = j * NX + i, a = j * (NX + 1) + i;
-        subdivide(lu[a], lv[a], lu[a + 1], lv[a + 1], j == 0 || j == NY, kStreamHEdge, e,
-                  hxy.data() + 2 * e * (S - 1));
-      }
-  });
-  parallel_for(NY, threads, [&](std::uint64_t jb, std::uint64_t je) {
-    for (std::uint64_t j = jb; j < je; ++j)
-      for (std::uint64_t i = 0; i <= NX; ++i) {
-        const std::uint64_t e = j * (NX + 1) + i, a = e;
-        subdivide(lu[a], lv[a], lu[a + NX + 1], lv[a + NX + 1], i == 0 || i == NX, kStreamVEdge, e,
-                  vxy_e.data() + 2 * e * (S - 1));
-      }
-  });
-  std::vector<double> gx((NX + 1) * (NY + 1)), gy((NX + 1) * (NY + 1));
-  for (std::uint64_t j = 0; j <= NY; ++j)
-    for (std::uint64_t i = 0; i <= NX; ++i) {
-      const std::uint64_t k = j * (NX + 1) + i;
-      gx[k] = (i == 0) ? x0 : (i == NX) ? x1 : map_x(lu[k]);
-      gy[k] = (j == 0) ? y0 : (j == NY) ? y1 : map_y(lv[k]);
-    }
-  std::vector<double>().swap(lu);
-  std::vector<double>().swap(lv);
+  const std::vector<double>& gx = LAT.gx;
+  const std::vector<double>& gy = LAT.gy;
+  const std::vector<double>& hxy = LAT.hxy;
+  const std::vector<double>& vxy_e = LAT.vxy_e;
   const std::uint64_t per_poly = 4 * S;
   const std::uint64_t P = NX * NY;
   const std::uint64_t per_state = CX * CY, per_county = std::uint64_t{bx} * by;
@@ -380,6 +449,74 @@ int synth_nested(std::uint32_t sx, std::uint32_t sy, std::uint32_t cx, std::uint
 
 // Uniform points over box4 = {x0, x1, y0, y1}; point k of the stream is
 // global index offset + k.
+// The nested config as a full three-level FMCB hierarchy (the format of
+// save_hierarchy, hierarchy.hpp:102-202): state and county polygons are the
+// outlines of their lattice cells on the same shared points as the blocks,
+// bboxes are the polygon bboxes, FIPS = state+1, county+1, block/10,
+// block%10.  For the simple engine (simple_mapper.hpp), which needs every
+// level's geometry.  Returns 0, or 1 on bad arguments / IO failure.
+int synth_nested_fmcb(std::uint32_t sx, std::uint32_t sy, std::uint32_t cx, std::uint32_t cy,
+                      std::uint32_t bx, std::uint32_t by, std::uint32_t segs, double jitter,
+                      double sigma, double x0, double x1, double y0, double y1, std::uint64_t seed,
+                      int threads, const char* path) {
+  NestedLattice LAT;
+  if (!build_nested(sx, sy, cx, cy, bx, by, segs, jitter, sigma, x0, x1, y0, y1, seed, threads, LAT)) return 1;
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) return 1;
+  bool ok = true;
+  auto put = [&](const void* p, std::size_t n) { ok = ok && std::fwrite(p, 1, n, f) == n; };
+  auto u16 = [&](std::uint16_t v) { put(&v, 2); };
+  auto u32 = [&](std::uint32_t v) { put(&v, 4); };
+  auto u64 = [&](std::uint64_t v) { put(&v, 8); };
+  std::vector<double> ring;
+  auto region = [&](std::int64_t fp, const char* fips, std::uint64_t i0, std::uint64_t i1,
+                    std::uint64_t j0, std::uint64_t j1) {
+    ring.resize(2 * 2 * ((i1 - i0) + (j1 - j0)) * LAT.S);
+    const std::uint64_t nv = LAT.ring(i0, i1, j0, j1, ring.data());
+    double bx0 = ring[0], bx1 = ring[0], by0 = ring[1], by1 = ring[1];
+    for (std::uint64_t k = 0; k < nv; ++k) {
+      bx0 = std::min(bx0, ring[2 * k]);
+      bx1 = std::max(bx1, ring[2 * k]);
+      by0 = std::min(by0, ring[2 * k + 1]);
+      by1 = std::max(by1, ring[2 * k + 1]);
+    }
+    put(&fp, 8);
+    if (fips) put(fips, 12);
+    const double bb[4] = {bx0, bx1, by0, by1};
+    put(bb, 32);
+    u32(static_cast<std::uint32_t>(nv));
+    put(ring.data(), 16 * nv);
+    u32(1);
+    u32(0);
+  };
+  put("FMCB", 4);
+  u16(1);
+  u64(std::uint64_t{sx} * sy);
+  u64(std::uint64_t{sx} * sy * cx * cy);
+  u64(std::uint64_t{sx} * sy * cx * cy * bx * by);
+  char fips[16];
+  for (std::uint32_t s = 0; s < sx * sy && ok; ++s) {
+    const std::uint64_t si = s % sx, sj = s / sx;
+    const std::uint64_t CX = std::uint64_t{cx} * bx, CY = std::uint64_t{cy} * by;
+    region(s + 1, nullptr, si * CX, (si + 1) * CX, sj * CY, (sj + 1) * CY);
+    u32(cx * cy);
+    for (std::uint32_t c = 0; c < cx * cy; ++c) {
+      const std::uint64_t ci = c % cx, cj = c / cx;
+      const std::uint64_t i0 = (si * cx + ci) * bx, j0 = (sj * cy + cj) * by;
+      region(c + 1, nullptr, i0, i0 + bx, j0, j0 + by);
+      u32(bx * by);
+      for (std::uint32_t b = 0; b < bx * by; ++b) {
+        const std::uint64_t bi = b % bx, bj = b / bx;
+        std::snprintf(fips, sizeof(fips), "%02u%03u%06u%01u", (s + 1) % 100u, (c + 1) % 1000u,
+                      (b / 10u) % 1000000u, b % 10u);
+        region(b + 1, fips, i0 + bi, i0 + bi + 1, j0 + bj, j0 + bj + 1);
+      }
+    }
+  }
+  ok = (std::fclose(f) == 0) && ok;
+  return ok ? 0 : 1;
+}
+
 int synth_points_uniform(const double* box4, std::uint64_t n, std::uint64_t offset,
                          std::uint64_t seed, int threads, double* out) {
   const double w = box4[1] - box4[0], h = box4[3] - box4[2];

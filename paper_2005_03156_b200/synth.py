@@ -150,6 +150,16 @@ class NestedConfig:
         soup = Soup(vxy, ring_off, poly_ring)
         return (soup, scb) if with_scb else soup
 
+    def write_fmcb(self, path, threads: Optional[int] = None) -> None:
+        """The full three-level hierarchy (states, counties, blocks) as an
+        FMCB file -- the simple engine's input (simple_mapper.hpp)."""
+        x0, x1, y0, y1 = DOMAIN
+        rc = N.synth().synth_nested_fmcb(self.sx, self.sy, self.cx, self.cy, self.bx, self.by,
+                                         self.segs, self.jitter, self.sigma, x0, x1, y0, y1,
+                                         self.seed, threads or _threads(), str(path).encode())
+        if rc != 0:
+            raise RuntimeError(f"synth_nested_fmcb failed for {path}")
+
     def make_points(self, n: Optional[int] = None, offset: int = 0, soup=None,
                     threads: Optional[int] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
         n = self.n_points if n is None else int(n)
@@ -179,6 +189,9 @@ CONFIGS = {
     "c5": NestedConfig("c5", 10, 5, 20, 20, 25, 25, 6, 0.3, 0.05, 8_000_000_000),
     # reduced c3 with the same recipe, for parity tests (4 states, 40,000 leaves)
     "c3mini": NestedConfig("c3mini", 2, 2, 4, 4, 25, 25, 6, 0.3, 0.05, 2_000_000),
+    # the c3 recipe at 320,000 leaves (50 states x 64 counties x 100 blocks):
+    # the simple engine's bench hierarchy (written as FMCB with all levels)
+    "c3s": NestedConfig("c3s", 10, 5, 8, 8, 10, 10, 6, 0.3, 0.05, 100_000_000),
 }
 
 

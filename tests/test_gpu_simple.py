@@ -29,9 +29,21 @@ def probe_points(h, n, seed):
     # vertices, edge midpoints and points just off them
     idx = rng.integers(0, v.shape[0], 2000)
     nxt = np.minimum(idx + 1, v.shape[0] - 1)
-    extra = np.concatenate([v[idx], 0.5 * (v[idx] + v[nxt]), v[idx] + 1e-12,
-                            [[np.nan, 0.0], [0.0, np.inf]]])
+    extra = np.concatenate([v[idx], 0.5 * (v[idx] + v[nxt]), v[idx] + 1e-12])
     return np.ascontiguousarray(np.concatenate([pts, extra]))
+
+
+def test_non_finite_points_are_unassigned(tmp_path):
+    """The reference CLI drops non-finite rows before assign()
+    (tools/fastmap.cpp:240-251; its bbox_membership sorts by lon, which NaN
+    leaves unordered).  Here they are simply unresolved in both modes."""
+    p = tmp_path / "adv.fmcb"
+    fmcb_writer.write_fmcb(p, fmcb_writer.random_hierarchy(1))
+    eng = fastmap.SimpleEngine(fastmap.load_hierarchy(p))
+    pts = np.array([[np.nan, 0.0], [0.0, np.inf], [np.inf, np.nan], [-np.inf, 1.0]])
+    for mode in (AssignMode.relaxed, AssignMode.strict):
+        r = eng.assign(pts, mode)
+        assert (r.state == -1).all() and (r.block == -1).all()
 
 
 def check_against_reference(path, pts):
@@ -94,3 +106,21 @@ def test_golden_hierarchy_strict_equals_exhaustive():
     hit = leaf >= 0
     assert np.array_equal(res.block[hit], h.scb[leaf[hit], 2].astype(np.int32))
     assert np.array_equal(res.county[hit], h.scb[leaf[hit], 1].astype(np.int32))
+
+
+def test_nested_config_against_reference(tmp_path):
+    """The bench hierarchy recipe (c3mini scale): both modes vs the reference;
+    strict additionally equals the leaf-exact projection off the edges."""
+    from paper_2005_03156_b200 import synth
+    cfg = synth.config("c3mini")
+    p = tmp_path / "c3mini.fmcb"
+    cfg.write_fmcb(p)
+    pts = cfg.make_points(200_000)
+    if oracle.ref_available():
+        check_against_reference(p, pts[:50_000])
+    h = fastmap.load_hierarchy(p)
+    res = fastmap.assign(h, pts, AssignMode.strict)
+    leaf = oracle.assign(h.soup, pts)
+    hit = leaf >= 0
+    agree = (res.block[hit] == h.scb[leaf[hit], 2].astype(np.int32)).mean()
+    assert agree > 0.9999  # differs only for points on shared state/county borders

@@ -48,3 +48,20 @@ def test_point_streams_shard_and_distributions():
     # about 1% of the expanded box lies outside the domain
     out = (u[:, 0] < -125) | (u[:, 0] > -66) | (u[:, 1] < 24) | (u[:, 1] > 50)
     assert 0.005 < out.mean() < 0.03
+
+
+def test_nested_fmcb_carries_every_level(tmp_path):
+    """synth_nested_fmcb: the c3mini hierarchy with state and county polygons
+    on the same shared lattice points; its leaves are exactly c3mini's soup,
+    and the reference's own load_hierarchy accepts the file."""
+    import oracle
+    from paper_2005_03156_b200 import fastmap
+    cfg = synth.config("c3mini")
+    p = tmp_path / "c3mini.fmcb"
+    cfg.write_fmcb(p)
+    h = fastmap.load_hierarchy(p)
+    soup = cfg.make_soup()
+    assert (h.n_states, h.n_counties, h.n_leaves) == (4, 64, 40000)
+    assert np.array_equal(h.soup.vxy, soup.vxy) and np.array_equal(h.soup.ring_off, soup.ring_off)
+    if oracle.ref_available():
+        assert oracle.ref_load_fmcb_status(p) == 0
