@@ -40,21 +40,25 @@ __attribute__((visibility("hidden"))) fm_status fm_set_error(fm_status s, const 
 
 namespace {
 
+// One 64-byte record per region: everything a candidate test touches
+// before the edges (two sectors, one load each).
+struct alignas(64) RegionRec {
+  double bbox[4];            // file bbox: x0, x1, y0, y1
+  double band_y0, band_inv;  // latitude bands over the region's edges
+  std::uint32_t band_base;   // first band in band_off
+  std::uint32_t band_n;
+  std::uint32_t child_lo, child_hi;  // children in the next level (levels 0, 1)
+};
+static_assert(sizeof(RegionRec) == 64, "RegionRec is two sectors");
+
 struct LevelDev {
   int n = 0;
-  const double* bbox = nullptr;           // 4 per region
-  const std::uint32_t* child_lo = nullptr;
-  const std::uint32_t* child_hi = nullptr;
-  const double4* edges = nullptr;         // (lx, ly, hx, hy)
-  const double* band_y0 = nullptr;        // per region
-  const double* band_inv = nullptr;
-  const std::uint32_t* band_n = nullptr;
-  const std::uint64_t* band_base = nullptr;  // first band of the region in band_off
-  const std::uint64_t* band_off = nullptr;   // CSR into band_edges
-  const std::uint32_t* band_edges = nullptr; // global edge indices
+  const RegionRec* reg = nullptr;
+  const std::uint32_t* band_off = nullptr;  // per band: range into edges (edges replicated per band)
+  const double4* edges = nullptr;           // (lx, ly, hx, hy), upward
   double gx0 = 0, gy0 = 0, inv_w = 0, inv_h = 0;
   int gnx = 1, gny = 1;
-  const std::uint64_t* cell_off = nullptr;
+  const std::uint32_t* cell_off = nullptr;
   const std::uint32_t* cell_ids = nullptr;
   unsigned char* tested = nullptr;  // per region: received a polygon test (pip_calls)
 };
@@ -64,14 +68,12 @@ struct SimpleParams {
 };
 
 struct HostLevel {
+  std::vector<RegionRec> reg;
+  std::vector<std::uint32_t> band_off{0};
   std::vector<double4> edges;
-  std::vector<double> band_y0, band_inv;
-  std::vector<std::uint32_t> band_n;
-  std::vector<std::uint64_t> band_base, band_off{0};
-  std::vector<std::uint32_t> band_edges;
   double gx0 = 0, gy0 = 0, inv_w = 0, inv_h = 0;
   int gnx = 1, gny = 1;
-  std::vector<std::uint64_t> cell_off;
+  std::vector<std::uint32_t> cell_off;
   std::vector<std::uint32_t> cell_ids;
 };
 
@@ -86,12 +88,10 @@ inline long cell_of(double v, double x0, double inv, long n) {
 
 void build_level(const fm::HierLevel& L, HostLevel& H) {
   const std::uint64_t n = L.n_regions();
-  H.band_y0.resize(n);
-  H.band_inv.resize(n);
-  H.band_n.resize(n);
-  H.band_base.resize(n);
+  H.reg.resize(n);
+  std::vector<double4> redges;
   for (std::uint64_t r = 0; r < n; ++r) {
-    const std::size_t e0 = H.edges.size();
+    redges.clear();
     for (std::uint64_t k = L.poly_ring[r]; k < L.poly_ring[r + 1]; ++k) {
       const std::uint64_t b = L.ring_off[k], e = L.ring_off[k + 1], m = e - b;
       for (std::uint64_t i = 0; i < m; ++i) {  // closed ring (add_ring, geometry.hpp:73-85)
@@ -102,41 +102,46 @@ void build_level(const fm::HierLevel& L, HostLevel& H) {
           std::swap(lx, hx);
           std::swap(ly, hy);
         }
-        H.edges.push_back(make_double4(lx, ly, hx, hy));
+        redges.push_back(make_double4(lx, ly, hx, hy));
       }
     }
-    const std::size_t ne = H.edges.size() - e0;
+    const std::size_t ne = redges.size();
     double y0 = 0.0, y1 = 0.0;
     if (ne) {
-      y0 = H.edges[e0].y;
-      y1 = H.edges[e0].w;
-      for (std::size_t k = e0; k < H.edges.size(); ++k) {
-        y0 = std::min(y0, H.edges[k].y);
-        y1 = std::max(y1, H.edges[k].w);
+      y0 = redges[0].y;
+      y1 = redges[0].w;
+      for (const double4& e : redges) {
+        y0 = std::min(y0, e.y);
+        y1 = std::max(y1, e.w);
       }
     }
     std::uint32_t nb = static_cast<std::uint32_t>(std::clamp<std::size_t>(ne / 4, 1, 4096));
     double inv = 0.0;
     if (y1 > y0) inv = static_cast<double>(nb) / (y1 - y0);
     else nb = 1;
-    H.band_y0[r] = y0;
-    H.band_inv[r] = inv;
-    H.band_n[r] = nb;
-    H.band_base[r] = H.band_off.size() - 1;
+    RegionRec& R = H.reg[r];
+    for (int q = 0; q < 4; ++q) R.bbox[q] = L.bbox[4 * r + q];
+    R.band_y0 = y0;
+    R.band_inv = inv;
+    R.band_base = static_cast<std::uint32_t>(H.band_off.size() - 1);
+    R.band_n = nb;
+    R.child_lo = r < L.child_lo.size() ? L.child_lo[r] : 0;
+    R.child_hi = r < L.child_hi.size() ? L.child_hi[r] : 0;
     std::vector<std::vector<std::uint32_t>> bands(nb);
-    for (std::size_t k = e0; k < H.edges.size(); ++k) {
-      const long lo = cell_of(H.edges[k].y, y0, inv, nb), hi = cell_of(H.edges[k].w, y0, inv, nb);
+    for (std::size_t k = 0; k < ne; ++k) {
+      const long lo = cell_of(redges[k].y, y0, inv, nb), hi = cell_of(redges[k].w, y0, inv, nb);
       for (long q = lo; q <= hi; ++q) bands[static_cast<std::size_t>(q)].push_back(static_cast<std::uint32_t>(k));
     }
-    for (const auto& bl : bands) {
-      H.band_edges.insert(H.band_edges.end(), bl.begin(), bl.end());
-      H.band_off.push_back(H.band_edges.size());
+    for (const auto& bl : bands) {  // edges replicated into every band they span
+      for (std::uint32_t k : bl) H.edges.push_back(redges[k]);
+      if (H.edges.size() > 0xFFFFFFFFull) throw std::bad_alloc();
+      H.band_off.push_back(static_cast<std::uint32_t>(H.edges.size()));
     }
   }
   // bbox grid over the union of the regions' (finite) file bboxes
   double ux0 = INFINITY, ux1 = -INFINITY, uy0 = INFINITY, uy1 = -INFINITY;
   for (std::uint64_t r = 0; r < n; ++r) {
-    const double* bb = &L.bbox[4 * r];
+    const double* bb = H.reg[r].bbox;
     if (!(std::isfinite(bb[0]) && std::isfinite(bb[1]) && std::isfinite(bb[2]) && std::isfinite(bb[3]))) continue;
     ux0 = std::min(ux0, bb[0]);
     ux1 = std::max(ux1, bb[1]);
@@ -157,7 +162,7 @@ void build_level(const fm::HierLevel& L, HostLevel& H) {
   H.inv_h = H.gny / Hh;
   std::vector<std::uint32_t> count(static_cast<std::size_t>(H.gnx) * H.gny, 0);
   auto span = [&](std::uint64_t r, long* cx0, long* cx1, long* cy0, long* cy1) {
-    const double* bb = &L.bbox[4 * r];
+    const double* bb = H.reg[r].bbox;
     if (!(bb[0] < bb[1] && bb[2] < bb[3])) return false;  // no point is strictly inside
     *cx0 = cell_of(bb[0], H.gx0, H.inv_w, H.gnx);
     *cx1 = cell_of(bb[1], H.gx0, H.inv_w, H.gnx);
@@ -172,9 +177,14 @@ void build_level(const fm::HierLevel& L, HostLevel& H) {
       for (long x = a0; x <= a1; ++x) ++count[static_cast<std::size_t>(y) * H.gnx + x];
   }
   H.cell_off.assign(count.size() + 1, 0);
-  for (std::size_t c = 0; c < count.size(); ++c) H.cell_off[c + 1] = H.cell_off[c] + count[c];
+  std::uint64_t tot = 0;
+  for (std::size_t c = 0; c < count.size(); ++c) {
+    tot += count[c];
+    if (tot > 0xFFFFFFFFull) throw std::bad_alloc();
+    H.cell_off[c + 1] = static_cast<std::uint32_t>(tot);
+  }
   H.cell_ids.resize(H.cell_off.back());
-  std::vector<std::uint64_t> fill(H.cell_off.begin(), H.cell_off.end() - 1);
+  std::vector<std::uint32_t> fill(H.cell_off.begin(), H.cell_off.end() - 1);
   for (std::uint64_t r = 0; r < n; ++r) {  // ascending ids per cell
     if (!span(r, &a0, &a1, &b0, &b1)) continue;
     for (long y = b0; y <= b1; ++y)
@@ -182,8 +192,10 @@ void build_level(const fm::HierLevel& L, HostLevel& H) {
   }
 }
 
-__device__ __forceinline__ bool strictly_inside(const double* bb, double px, double py) {
-  return bb[0] < px && px < bb[1] && bb[2] < py && py < bb[3];  // bbox_contains, geometry.hpp:54-57
+__device__ __forceinline__ double4 ld4(const double4* p) {  // 32 bytes as two 16-byte loads
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
 }
 
 __device__ __forceinline__ int band_of(double v, double y0, double inv, int nb) {
@@ -193,14 +205,15 @@ __device__ __forceinline__ int band_of(double v, double y0, double inv, int nb) 
   return min(static_cast<int>(t), nb - 1);
 }
 
-// points_in_polygon's parity for one region (geometry.hpp:184-210).
-__device__ bool region_pip(const LevelDev& L, int r, double px, double py) {
-  const int nb = static_cast<int>(L.band_n[r]);
-  const int b = band_of(py, L.band_y0[r], L.band_inv[r], nb);
-  const std::uint64_t q = L.band_base[r] + static_cast<std::uint64_t>(b);
+// points_in_polygon's parity for one region (geometry.hpp:184-210); `b` is
+// the second half of the region record (band parameters).
+__device__ __forceinline__ bool region_pip(const LevelDev& L, const double4& b, double px, double py) {
+  const std::uint32_t base = __double2loint(b.z), nb = __double2hiint(b.z);
+  const int q = band_of(py, b.x, b.y, static_cast<int>(nb));
   std::uint32_t par = 0;
-  for (std::uint64_t k = L.band_off[q]; k < L.band_off[q + 1]; ++k) {
-    const double4 e = L.edges[L.band_edges[k]];
+  const std::uint32_t k1 = __ldg(L.band_off + base + q + 1);
+  for (std::uint32_t k = __ldg(L.band_off + base + q); k < k1; ++k) {
+    const double4 e = ld4(L.edges + k);
     if (e.y < py && py <= e.w && fm::ray_crosses(px, py, e.x, e.y, e.z, e.w)) par ^= 1u;
   }
   return par != 0;
@@ -224,29 +237,34 @@ __global__ void __launch_bounds__(256)
       // cells clamp; NaN maps to cell 0 and fails every strict bbox test
       const int cx = band_of(p.x, L.gx0, L.inv_w, L.gnx), cy = band_of(p.y, L.gy0, L.inv_h, L.gny);
       const std::uint64_t c = static_cast<std::uint64_t>(cy) * L.gnx + cx;
-      const std::uint64_t k0 = L.cell_off[c], k1 = L.cell_off[c + 1];
+      const std::uint32_t k0 = __ldg(L.cell_off + c), k1 = __ldg(L.cell_off + c + 1);
+      const double4* R = reinterpret_cast<const double4*>(L.reg);
       int cnt = 0, last = -1;
-      for (std::uint64_t k = k0; k < k1; ++k) {
-        const std::uint32_t r = L.cell_ids[k];
-        if (r >= lo && r < hi && strictly_inside(L.bbox + 4 * r, p.x, p.y)) {
-          ++cnt;
-          last = static_cast<int>(r);
+      for (std::uint32_t k = k0; k < k1; ++k) {
+        const std::uint32_t r = __ldg(L.cell_ids + k);
+        if (r >= lo && r < hi) {
+          const double4 a = ld4(R + 2 * r);
+          if (a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w) {
+            ++cnt;
+            last = static_cast<int>(r);
+          }
         }
       }
       if (cnt == 0) break;
       int win = -1;
       if (cnt >= (kStrict ? 1 : 2)) {  // the polygon-tested ("pending") points
-        for (std::uint64_t k = k0; k < k1; ++k) {
-          const std::uint32_t r = L.cell_ids[k];
-          if (r >= lo && r < hi && strictly_inside(L.bbox + 4 * r, p.x, p.y)) {
-            if (kCount) {
-              ++ev;
-              L.tested[r] = 1;
-            }
-            if (region_pip(L, static_cast<int>(r), p.x, p.y)) {
-              win = static_cast<int>(r);
-              break;  // first hit wins (simple_mapper.hpp:98-101)
-            }
+        for (std::uint32_t k = k0; k < k1; ++k) {
+          const std::uint32_t r = __ldg(L.cell_ids + k);
+          if (r < lo || r >= hi) continue;
+          const double4 a = ld4(R + 2 * r);
+          if (!(a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w)) continue;
+          if (kCount) {
+            ++ev;
+            L.tested[r] = 1;
+          }
+          if (region_pip(L, ld4(R + 2 * r + 1), p.x, p.y)) {
+            win = static_cast<int>(r);
+            break;  // first hit wins (simple_mapper.hpp:98-101)
           }
         }
       }
@@ -254,8 +272,10 @@ __global__ void __launch_bounds__(256)
       if (win < 0) break;
       res[l] = win - static_cast<int>(lo);
       if (l < 2) {
-        lo = L.child_lo[win];
-        hi = L.child_hi[win];
+        const double4 b = ld4(R + 2 * win + 1);
+        const unsigned long long ch = static_cast<unsigned long long>(__double_as_longlong(b.w));
+        lo = static_cast<std::uint32_t>(ch);
+        hi = static_cast<std::uint32_t>(ch >> 32);
       }
     }
     st[i] = res[0];
@@ -390,13 +410,8 @@ fm_status fm_simple_build(const fm_hierarchy* h, int device, fm_simple** out) {
       D.inv_h = H.inv_h;
       D.gnx = H.gnx;
       D.gny = H.gny;
-      std::vector<std::uint32_t> lo = L.child_lo, hi = L.child_hi;
-      ok = add(s, L.bbox, &D.bbox) && add(s, lo, &D.child_lo) && add(s, hi, &D.child_hi) &&
-           add(s, H.edges, &D.edges) && add(s, H.band_y0, &D.band_y0) &&
-           add(s, H.band_inv, &D.band_inv) && add(s, H.band_n, &D.band_n) &&
-           add(s, H.band_base, &D.band_base) && add(s, H.band_off, &D.band_off) &&
-           add(s, H.band_edges, &D.band_edges) && add(s, H.cell_off, &D.cell_off) &&
-           add(s, H.cell_ids, &D.cell_ids);
+      ok = add(s, H.reg, &D.reg) && add(s, H.band_off, &D.band_off) && add(s, H.edges, &D.edges) &&
+           add(s, H.cell_off, &D.cell_off) && add(s, H.cell_ids, &D.cell_ids);
       if (ok) {
         unsigned char* t = nullptr;
         ok = cudaMalloc(&t, std::max<std::uint64_t>(1, L.n_regions())) == cudaSuccess;
