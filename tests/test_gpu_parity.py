@@ -114,3 +114,46 @@ def test_folded_query_grid_odd_dims(dev):
     assert np.array_equal(project_device(idx, pts, dev), oracle.assign(soup, pts))
     c2 = fastmap.build_index(synth.config("c2").make_soup(), device=0).stats()
     assert c2["query_block_log2"] >= 1
+
+
+def test_more_than_one_launch_slice(dev):
+    """fm_query splits batches into 2^28-point slices (queue scratch bound):
+    a batch just past the slice size must match point for point, histogram
+    included."""
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    idx = fastmap.build_index(soup, device=0)
+    n = (1 << 28) + 4099
+    base = cfg.make_points(1 << 20, offset=11)
+    d = torch.from_numpy(base).to(dev).repeat((n + base.shape[0] - 1) // base.shape[0], 1)[:n].contiguous()
+    hist = torch.zeros(soup.n_polys, dtype=torch.int64, device=dev)
+    out = idx.project(d, hist=hist)
+    torch.cuda.synchronize()
+    want = oracle.assign(soup, base)
+    got = out.cpu().numpy()
+    reps = np.arange(n) % base.shape[0]
+    assert np.array_equal(got, want[reps])
+    assert np.array_equal(hist.cpu().numpy(), np.bincount(got[got >= 0], minlength=soup.n_polys))
+    del d, out
+
+
+def test_concurrent_streams_share_an_index(dev):
+    """Built indexes are immutable; fm_query on two streams at once gives the
+    same answers as one after the other (SURVEY.md sec. 8b threading)."""
+    cfg = synth.config("c2")
+    soup = cfg.make_soup()
+    idx = fastmap.build_index(soup, device=0)
+    a = torch.from_numpy(cfg.make_points(3_000_000, offset=1)).to(dev)
+    b = torch.from_numpy(cfg.make_points(3_000_000, offset=2)).to(dev)
+    ra, rb = idx.project(a), idx.project(b)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    oa = torch.empty_like(ra)
+    ob = torch.empty_like(rb)
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            idx.project(a, out=oa, stream=s1)
+        with torch.cuda.stream(s2):
+            idx.project(b, out=ob, stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(oa, ra) and torch.equal(ob, rb)
