@@ -191,6 +191,18 @@ fm_status fm_index_export(const fm_index* index, uint32_t* grid, uint64_t* grid_
 /* Device the index lives on. */
 int fm_index_device(const fm_index* index);
 
+/* Checker for the quick records (test infrastructure, no GPU needed): on a
+ * host-only index (device -1), for each point the answer the query kernel's
+ * inline quick path would give -- the grid answer for hit / empty cells, the
+ * quick record's certified answer for boundary cells, FM_QUICK_UNSURE (-3)
+ * where it hands the point to the exact path, FM_QUICK_NONE (-4) for cells
+ * without a quick record (split / overflow / not encodable).  Uses the same
+ * quick_encode / quick_eval code as the kernel (csrc/quick.h). */
+#define FM_QUICK_UNSURE (-3)
+#define FM_QUICK_NONE (-4)
+fm_status fm_index_quick_host(const fm_index* index, const double* h_lonlat, uint64_t n,
+                              int32_t* h_out);
+
 /* ---- artifacts and IO ---------------------- */
 
 /* Index persistence, the FMCI save/load analogue (cell_index.hpp:641-726):

@@ -88,7 +88,7 @@ EXPORTS = (
     "fm_index_save", "fm_index_load", "fm_hierarchy_load", "fm_hierarchy_destroy",
     "fm_hierarchy_sizes", "fm_hierarchy_leaves", "fm_index_build_hierarchy",
     "fm_read_points_f64", "fm_write_assign_csv", "fm_simple_build", "fm_simple_destroy",
-    "fm_simple_assign", "fm_simple_assign_host",
+    "fm_simple_assign", "fm_simple_assign_host", "fm_index_quick_host",
 )
 
 MODE_EXACT, MODE_APPROX = 0, 1  # fm_mode (CoverMode, cell_index.hpp:246)
@@ -165,6 +165,9 @@ def lib() -> C.CDLL:
                                             C.POINTER(AssignCountersC)]
         L.fm_index_export.restype = C.c_int
         L.fm_index_export.argtypes = [C.c_void_p, PU32, PU64, PU8, PU64, PD]
+        if hasattr(L, "fm_index_quick_host"):  # absent from older tuning builds
+            L.fm_index_quick_host.restype = C.c_int
+            L.fm_index_quick_host.argtypes = [C.c_void_p, PD, u64, PI32]
         L.fm_index_device.restype = C.c_int
         L.fm_index_device.argtypes = [C.c_void_p]
         _lib = L

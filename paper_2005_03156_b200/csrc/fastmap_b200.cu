@@ -15,6 +15,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -352,6 +353,68 @@ __global__ void __launch_bounds__(kBWarps * 32, FM_BMINB)
 
 constexpr int kSmemB = static_cast<int>(sizeof(WarpSmemB)) * kBWarps;
 
+// resolve_quick_kernel: the resolve pass through the quick records
+// (quick.h).  Each lane takes kRQ queue items per round, gathers their
+// 32-byte quick records (all in flight together) and evaluates them in
+// registers; the rare item a quick record cannot certify -- a near-tie, a
+// cell without an encodable record (split / overflow / over capacity) --
+// is resolved exactly from its slot in global memory.  Small register and
+// no shared-memory footprint, so many warps hide the record gathers.
+constexpr int kRQ = 2;
+#ifndef FM_QMINB
+#define FM_QMINB 4
+#endif
+template <bool kHist>
+__global__ void __launch_bounds__(256, FM_QMINB)
+    resolve_quick_kernel(fm::KParams P, const QItem* __restrict__ q,
+                         const std::uint32_t* __restrict__ qcount, std::uint64_t n_regions,
+                         std::uint64_t region_cap, unsigned long long* __restrict__ next_region,
+                         int* __restrict__ out, unsigned long long* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  fm::WorkCount wc;
+  for (;;) {
+    unsigned long long region = 0;
+    if (lane == 0) region = atomicAdd(next_region, 1ull);
+    region = __shfl_sync(0xFFFFFFFFu, region, 0);
+    if (region >= n_regions) break;
+    const QItem* items = q + region * region_cap;
+    const std::uint32_t cnt = qcount[region];
+    for (std::uint32_t b = 0; b < cnt; b += 32 * kRQ) {
+      QItem it[kRQ];
+      uint4 qa[kRQ], qb[kRQ];
+#pragma unroll
+      for (int r = 0; r < kRQ; ++r) it[r] = load_item(items, b + r * 32 + lane, cnt);
+#pragma unroll
+      for (int r = 0; r < kRQ; ++r) {
+        const std::uint32_t k = it[r].e & fm::kSlotIndexMask;
+        qa[r] = make_uint4(0u, 0u, 0u, 0u);
+        qb[r] = qa[r];
+        if (it[r].e != fm::kEmpty && k < P.n_quick) {
+          qa[r] = __ldg(P.quick + 2 * static_cast<std::size_t>(k));
+          qb[r] = __ldg(P.quick + 2 * static_cast<std::size_t>(k) + 1);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kRQ; ++r) {
+        if (it[r].e == fm::kEmpty) continue;  // past the region's count
+        // the point's position in its cell in quanta (quick.h frame)
+        const double fx = __dmul_rn(__dsub_rn(it[r].px, P.gx0), P.inv_w);
+        const double fy = __dmul_rn(__dsub_rn(it[r].py, P.gy0), P.inv_h);
+        const int ix = min(max(static_cast<int>(fx), 0), P.nx - 1);
+        const int iy = min(max(static_cast<int>(fy), 0), P.ny - 1);
+        const float pu = static_cast<float>(__dmul_rn(__dsub_rn(fx, static_cast<double>(ix)), fm::kQuickScale));
+        const float pv = static_cast<float>(__dmul_rn(__dsub_rn(fy, static_cast<double>(iy)), fm::kQuickScale));
+        const std::uint32_t w[8] = {qa[r].x, qa[r].y, qa[r].z, qa[r].w,
+                                    qb[r].x, qb[r].y, qb[r].z, qb[r].w};
+        int id = fm::quick_eval(w, pu, pv);  // no record (w = 0): unsure
+        if (id == fm::kQuickUnsure) id = fm::resolve_slot_global<false>(P, it[r].e, it[r].px, it[r].py, wc);
+        emit<kHist>(out, hist, it[r].i, id);
+      }
+    }
+  }
+}
+
+
 // ---------------------------------------------------------------------------
 // Fast-approx mode (CoverMode::approx, cell_index.hpp:558-560).  The approx
 // cover assigns every cell of an epsilon-fine grid one answer: hits and
@@ -396,12 +459,15 @@ __global__ void __launch_bounds__(kXThreads)
   }
 }
 
-// Per block of S x S fine cells: 0 when its entries are all equal, 1 when a
-// compact sub-block holds it, 1 << 32 when a full sub-block does.  The
-// exclusive scan of these u64 flags numbers both kinds at once.  Compact
-// kinds (`mode`): 1 = approx palette (<= 3 distinct answers, ls <= 3);
-// 2 = exact compact (<= 3 distinct hit/empty entries plus <= 12 phase-1
-// slot references with consecutive indices, ls <= 2 -- see renumber_slots).
+// Per block of S x S fine cells: 0 when its entries are all equal, the
+// number of compact units (low word) when a compact sub-block holds it,
+// 1 << 32 when a full sub-block does.  The exclusive scan of these u64 flags
+// numbers both kinds at once.  Compact kinds (`mode`): 1 = approx palette
+// (<= 3 distinct answers, ls <= 3; one unit = one palette); 2 = exact, in
+// 16-byte units (ls <= 2, phase-1 slot references with consecutive indices
+// -- see renumber_slots): a "small" sub-block (one unit) when the hit
+// entries take <= 2 distinct values besides empty, else a compact one (two
+// units: <= 3 distinct hit/empty entries, <= 12 slot references).
 __global__ void __launch_bounds__(256)
     block_flag_kernel(const std::uint32_t* __restrict__ fine, int nx, int ny, int bnx, int bny,
                       int ls, int mode, std::uint64_t n1, unsigned long long* __restrict__ flag) {
@@ -412,7 +478,7 @@ __global__ void __launch_bounds__(256)
   const int x0 = bx << ls, y0 = by << ls;
   std::uint32_t v[3];
   int nd = 0, nrec = 0;
-  bool far_rec = false;
+  bool far_rec = false, has_empty = false;
   std::uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
   for (int j = 0; j < S; ++j) {
     for (int i = 0; i < S; ++i) {
@@ -427,6 +493,7 @@ __global__ void __launch_bounds__(256)
         kmax = max(kmax, k);
         continue;
       }
+      has_empty |= x == fm::kEmpty;
       bool seen = false;
       for (int q = 0; q < nd && q < 3; ++q) seen |= v[q] == x;
       if (!seen) {
@@ -440,9 +507,13 @@ __global__ void __launch_bounds__(256)
     f = 0ull;
   } else if (mode == 1 && nrec == 0 && nd <= 3 && ls <= 3) {
     f = 1ull;
+  } else if (mode == 2 && ls <= 2 && !far_rec &&
+             (nrec == 0 || kmax - kmin + 1 == static_cast<std::uint32_t>(nrec)) &&
+             nd - (has_empty ? 1 : 0) <= 2) {
+    f = 1ull;  // small compact: one 16-byte unit
   } else if (mode == 2 && ls <= 2 && nd <= 3 && nrec <= 12 && !far_rec &&
              (nrec == 0 || kmax - kmin + 1 == static_cast<std::uint32_t>(nrec))) {
-    f = 1ull;
+    f = 2ull;  // compact: two 16-byte units
   } else {
     f = 1ull << 32;
   }
@@ -469,10 +540,47 @@ __global__ void __launch_bounds__(256)
     blocks[b] = fine[static_cast<std::size_t>(y0) * nx + x0];
     return;
   }
-  if (f == 1ull && mode == 2) {  // exact compact sub-block (32 bytes)
+  if (f == 1ull && mode == 2) {  // exact small sub-block (16 bytes)
+    const unsigned long long k = idx[b] & 0xFFFFFFFFull;
+    blocks[b] = fm::kRecordBit | fm::kHalfBit | fm::kSmallBit | static_cast<std::uint32_t>(k);
+    std::uint32_t* dst = pal + k * 4;
+    std::uint32_t v[2] = {fm::kEmpty, fm::kEmpty};
+    int nd = 0;
+    std::uint32_t base = 0xFFFFFFFFu, codes = 0u;
+    for (int j = 0; j < S; ++j) {
+      for (int i = 0; i < S; ++i) {
+        if (y0 + j >= ny || x0 + i >= nx) continue;
+        const std::uint32_t x = fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i];
+        if (x != fm::kEmpty && x >= fm::kRecordBit) base = min(base, x & fm::kSlotIndexMask);
+      }
+    }
+    for (int j = 0; j < S; ++j) {
+      for (int i = 0; i < S; ++i) {
+        const bool in = y0 + j < ny && x0 + i < nx;
+        const std::uint32_t x = in ? fine[static_cast<std::size_t>(y0 + j) * nx + x0 + i] : fm::kEmpty;
+        std::uint32_t code;
+        if (x == fm::kEmpty) {
+          code = 3u;
+        } else if (x >= fm::kRecordBit) {
+          code = 2u;  // slot base + rank among the block's slot cells
+        } else {
+          code = 0;
+          while (static_cast<int>(code) < nd && v[code] != x) ++code;
+          if (static_cast<int>(code) == nd) v[nd++] = x;
+        }
+        codes |= code << (2 * ((j << ls) + i));
+      }
+    }
+    dst[0] = v[0];
+    dst[1] = v[1];
+    dst[2] = base;
+    dst[3] = codes;
+    return;
+  }
+  if (f == 2ull && mode == 2) {  // exact compact sub-block (32 bytes)
     const unsigned long long k = idx[b] & 0xFFFFFFFFull;
     blocks[b] = fm::kRecordBit | fm::kHalfBit | static_cast<std::uint32_t>(k);
-    std::uint32_t* dst = pal + k * 8;
+    std::uint32_t* dst = pal + k * 4;
     std::uint32_t v[3] = {fm::kEmpty, fm::kEmpty, fm::kEmpty};
     int nd = 0;
     std::uint32_t base = 0xFFFFFFFFu;
@@ -591,6 +699,25 @@ __global__ void __launch_bounds__(256)
   grid[c] = (e & ~fm::kSlotIndexMask) | static_cast<std::uint32_t>(kn);
 }
 
+// Quick records (quick.h): one thread per cell; the cell of phase-1 slot k
+// writes record k.
+__global__ void __launch_bounds__(256)
+    quick_build_kernel(const std::uint32_t* __restrict__ grid, std::uint64_t ncell, int nx,
+                       const std::uint8_t* __restrict__ slots, std::uint64_t n1, double gx0,
+                       double gy0, double inv_w, double inv_h, uint4* __restrict__ quick) {
+  const std::uint64_t c = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  const std::uint32_t e = grid[c];
+  if (e == fm::kEmpty || e < fm::kRecordBit) return;
+  const std::uint64_t k = e & fm::kSlotIndexMask;
+  if (k >= n1) return;
+  std::uint32_t w[8];
+  fm::quick_encode(slots + k * fm::kSlotBytes, static_cast<std::int64_t>(c % nx),
+                   static_cast<std::int64_t>(c / nx), gx0, gy0, inv_w, inv_h, w);
+  quick[2 * k] = make_uint4(w[0], w[1], w[2], w[3]);
+  quick[2 * k + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 // Boundary cells of the exact grid -> (centre point, cell) lists.
 __global__ void __launch_bounds__(256)
     deem_collect_kernel(const std::uint32_t* __restrict__ grid, std::uint64_t ncell,
@@ -691,6 +818,8 @@ struct fm_index {
   Folded agrid;                        // fast-approx cover (folded), or empty
   std::uint8_t* d_slots = nullptr;     // boundary slots (128 B each)
   std::uint8_t* d_overflow = nullptr;  // overflow records
+  uint4* d_quick = nullptr;            // quick records (quick.h), one per phase-1 slot
+  std::uint64_t n_quick = 0;
   std::uint64_t grid_len = 0, slots_len = 0, overflow_len = 0;
   fm::HostIndex host;  // retained only for host-only (device < 0) indexes
   fm_index_stats stats{};
@@ -726,6 +855,8 @@ fm::KParams kparams(const fm_index* ix) {
   P.compact = ix->qgrid.compact;
   P.bnx = ix->qgrid.bnx;
   P.ls = ix->qgrid.ls;
+  P.quick = ix->d_quick;
+  P.n_quick = static_cast<std::uint32_t>(ix->n_quick);
   return P;
 }
 
@@ -757,12 +888,20 @@ fm_status launch_t(const fm_index* ix, const double2* pts, std::uint64_t n, int*
   }
   FM_CUDA(cudaMemsetAsync(next_region, 0, 8, stream));
   ka<<<grid_a, blk_a, 0, stream>>>(P, pts, n, d_out, d_hist, q, qcount, region_cap, d_counters);
-  // persistent resolve grid: resident CTAs pull regions from a counter
-  const int grid_b = static_cast<int>(std::min<std::uint64_t>(
-      (n_regions + kBWarps - 1) / kBWarps,
-      resident_blocks(ix->device, (const void*)kb, kBWarps * 32, kSmemB)));
-  kb<<<grid_b, kBWarps * 32, kSmemB, stream>>>(P, q, qcount, n_regions, region_cap, next_region,
-                                               d_out, d_hist, d_counters);
+  // persistent resolve grid: resident CTAs pull regions from a counter.
+  // Counting runs take the slot path, so the counters measure exact work.
+  if (!kCount && ix->n_quick > 0) {
+    auto kq = resolve_quick_kernel<kHist>;
+    const int grid_q = static_cast<int>(std::min<std::uint64_t>(
+        (n_regions + 7) / 8, resident_blocks(ix->device, (const void*)kq, 256, 0)));
+    kq<<<grid_q, 256, 0, stream>>>(P, q, qcount, n_regions, region_cap, next_region, d_out, d_hist);
+  } else {
+    const int grid_b = static_cast<int>(std::min<std::uint64_t>(
+        (n_regions + kBWarps - 1) / kBWarps,
+        resident_blocks(ix->device, (const void*)kb, kBWarps * 32, kSmemB)));
+    kb<<<grid_b, kBWarps * 32, kSmemB, stream>>>(P, q, qcount, n_regions, region_cap, next_region,
+                                                 d_out, d_hist, d_counters);
+  }
   const cudaError_t err = cudaGetLastError();
   FM_CUDA(cudaFreeAsync(scratch, stream));
   if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));
@@ -871,7 +1010,7 @@ fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, i
   }
   if (e == cudaSuccess) e = cudaMemcpy(&tot, idx + nblk, 8, cudaMemcpyDeviceToHost);
   const std::uint64_t n_pal = tot & 0xFFFFFFFFull, n_sub = tot >> 32;
-  const int pw0 = mode == 2 ? 8 : palette_words(ls);
+  const int pw0 = mode == 2 ? 4 : palette_words(ls);
   const double folded = static_cast<double>(nblk * 4 + (n_sub << (2 * ls + 2)) + n_pal * pw0 * 4);
   if (e == cudaSuccess && folded > max_ratio * 4.0 * nx * static_cast<double>(ny)) {
     // the fold would not shrink the grid enough to pay for its second
@@ -895,7 +1034,7 @@ fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, i
     e = cudaMalloc(&out->blocks, nblk * 4);
   }
   if (e == cudaSuccess) e = cudaMalloc(&out->sub, std::max<std::uint64_t>(n_sub, 1) << (2 * ls + 2));
-  const int pw = mode == 2 ? 8 : palette_words(ls);
+  const int pw = mode == 2 ? 4 : palette_words(ls);
   if (e == cudaSuccess) e = cudaMalloc(&out->pal, std::max<std::uint64_t>(n_pal, 1) * pw * 4);
   if (e == cudaSuccess) {
     block_write_kernel<<<g1, 256>>>(fine, nx, ny, bnx, bny, ls, mode, flag, idx, out->blocks,
@@ -1033,6 +1172,24 @@ fm_status build_approx(fm_index* ix) {
   return FM_OK;
 }
 
+// Quick records for the phase-1 slots (after renumbering: record k mirrors
+// slot k).  Disabled by FASTMAP_B200_NO_QUICK=1 (A/B runs) and when the
+// slot count does not fit the kernel's u32 bound.
+fm_status build_quick(fm_index* ix) {
+  const std::uint64_t n1 = ix->host.n_phase1_slots;
+  const char* off = std::getenv("FASTMAP_B200_NO_QUICK");
+  if (n1 == 0 || n1 >= fm::kMaxSlots || (off && off[0] == '1')) return FM_OK;
+  FM_CUDA(cudaMalloc(&ix->d_quick, n1 * fm::kQuickBytes));
+  const std::uint64_t ncell = ix->grid_len;
+  quick_build_kernel<<<static_cast<unsigned>((ncell + 255) / 256), 256>>>(
+      ix->d_grid, ncell, static_cast<int>(ix->g.nx), ix->d_slots, n1, ix->g.gx0, ix->g.gy0,
+      ix->g.inv_w, ix->g.inv_h, ix->d_quick);
+  FM_CUDA(cudaGetLastError());
+  FM_CUDA(cudaDeviceSynchronize());
+  ix->n_quick = n1;
+  return FM_OK;
+}
+
 // Query-side layout of a device index (shared by fm_index_build and
 // fm_index_load): mempool policy, block-major slot numbering + the folded
 // grid, and the approx cover when epsilon > 0.
@@ -1052,6 +1209,7 @@ fm_status finish_device(fm_index* ix, double approx_epsilon) {
     st = fold_grid(ix->d_grid, nx, ny, kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots,
                    kQueryMaxRatio, &ix->qgrid);
   }
+  if (st == FM_OK) st = build_quick(ix);
   if (st != FM_OK) return st;
   ix->stats.query_grid_bytes = ix->qgrid.bytes;
   ix->stats.query_block_log2 = ix->qgrid.ls;
@@ -1088,6 +1246,7 @@ void free_device(fm_index* ix) {
   ix->agrid.release();
   if (ix->d_slots) cudaFree(ix->d_slots);
   if (ix->d_overflow) cudaFree(ix->d_overflow);
+  if (ix->d_quick) cudaFree(ix->d_quick);
 }
 
 }  // namespace
@@ -1534,6 +1693,48 @@ fm_status fm_index_load(const char* path, int device, fm_index** out_index) {
     }
   }
   *out_index = ix;
+  return FM_OK;
+}
+
+fm_status fm_index_quick_host(const fm_index* index, const double* h_lonlat, std::uint64_t n,
+                              std::int32_t* h_out) {
+  if (!index || (n > 0 && (!h_lonlat || !h_out))) return set_err(FM_ERR_INVALID_ARGUMENT, "null argument");
+  if (index->device >= 0) return set_err(FM_ERR_INVALID_ARGUMENT, "fm_index_quick_host needs a host-only index");
+  const fm::GridGeom& g = index->g;
+  const fm::HostIndex& H = index->host;
+  for (std::uint64_t i = 0; i < n; ++i) {
+    const double px = h_lonlat[2 * i], py = h_lonlat[2 * i + 1];
+    const bool in = px >= index->ax0 && px <= index->ax1 && py >= index->ay0 && py <= index->ay1;
+    if (!in) {
+      h_out[i] = -1;
+      continue;
+    }
+    // the kernel's locate_n (query.cuh), on the flat grid
+    const double fx = (px - g.gx0) * g.inv_w, fy = (py - g.gy0) * g.inv_h;
+    std::int64_t ix = static_cast<std::int64_t>(static_cast<int>(fx));
+    std::int64_t iy = static_cast<std::int64_t>(static_cast<int>(fy));
+    ix = std::min<std::int64_t>(std::max<std::int64_t>(ix, 0), g.nx - 1);
+    iy = std::min<std::int64_t>(std::max<std::int64_t>(iy, 0), g.ny - 1);
+    const std::uint32_t e = H.grid[static_cast<std::size_t>(iy * g.nx + ix)];
+    if (e == fm::kEmpty || e < fm::kRecordBit) {
+      h_out[i] = e == fm::kEmpty ? -1 : static_cast<std::int32_t>(e);
+      continue;
+    }
+    const std::uint64_t k = e & fm::kSlotIndexMask;
+    std::uint32_t w[8];
+    if (k >= H.n_phase1_slots) {
+      h_out[i] = FM_QUICK_NONE;
+      continue;
+    }
+    fm::quick_encode(H.slots.data() + k * fm::kSlotBytes, ix, iy, g.gx0, g.gy0, g.inv_w, g.inv_h, w);
+    if (!(w[0] >> 31)) {
+      h_out[i] = FM_QUICK_NONE;
+      continue;
+    }
+    const float pu = static_cast<float>((fx - static_cast<double>(ix)) * fm::kQuickScale);
+    const float pv = static_cast<float>((fy - static_cast<double>(iy)) * fm::kQuickScale);
+    h_out[i] = fm::quick_eval(w, pu, pv);
+  }
   return FM_OK;
 }
 

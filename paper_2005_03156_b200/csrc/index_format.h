@@ -78,6 +78,11 @@ namespace fm {
 constexpr std::uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr std::uint32_t kRecordBit = 0x80000000u;
 constexpr std::uint32_t kHalfBit = 0x40000000u;     // slot content fits 64 bytes
+// query-side block entries (fold, KParams): kRecordBit | kHalfBit | unit k
+// names an exact compact sub-block at 16-byte unit k of the palette arena;
+// with kSmallBit it is a one-unit "small" sub-block
+constexpr std::uint32_t kSmallBit = 0x20000000u;
+constexpr std::uint32_t kUnitMask = 0x1FFFFFFFu;
 constexpr std::uint32_t kSlotIndexMask = 0x3FFFFFFFu;
 constexpr std::uint64_t kMaxSlots = 0x3FFFFFFFull;  // k + flags never equals kEmpty
 constexpr std::uint32_t kMaxLeaves = 0x7FFFFFFEu;

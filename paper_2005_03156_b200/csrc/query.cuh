@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "index_format.h"
+#include "quick.h"
 
 namespace fm {
 
@@ -31,6 +32,9 @@ struct KParams {
   int nx, ny;
   int bnx, ls;                // blocks per row, log2 block side
   int compact;                // `pal` format: 0 approx palettes, 1 exact compact sub-blocks
+  // quick records (quick.h): record k mirrors phase-1 slot k, k < n_quick
+  const uint4* __restrict__ quick;
+  std::uint32_t n_quick;
 };
 
 __device__ __forceinline__ const std::uint8_t* slot_ptr(const KParams& P, std::uint32_t e) {
@@ -80,7 +84,40 @@ __device__ __forceinline__ void locate_n(const KParams& P, const double2 (&p)[kN
                : kEmpty;
   }
   const uint4* pal4 = reinterpret_cast<const uint4*>(P.pal);
-  const bool two = kExact || P.ls == 3;  // 32-byte compact sub-blocks
+  if (kExact) {
+    // compact sub-blocks in 16-byte units: small (one unit: value[2], slot
+    // base, 2-bit codes -- 0/1 value, 2 slot base + rank, 3 empty) or
+    // compact (two units: value[3], slot base, 4-bit codes, half mask)
+#pragma unroll
+    for (int u = 0; u < kN; ++u) {
+      const std::uint32_t x = be[u];
+      const bool rec = P.ls != 0 && x != kEmpty && x >= kRecordBit;
+      const bool cmp = rec && (x & kHalfBit);
+      const bool small = x & kSmallBit;
+      const std::size_t k = x & kUnitMask;
+      uint4 a = make_uint4(0u, 0u, 0u, 0u), b = a;
+      std::uint32_t f = x;
+      if (cmp) a = __ldg(pal4 + k);
+      if (cmp && !small) b = __ldg(pal4 + k + 1);
+      if (rec && !cmp) f = __ldg(P.sub + ((x & kSlotIndexMask) << (2 * P.ls)) + cc[u]);
+      const int c = cc[u];
+      std::uint32_t ce;
+      if (small) {
+        const std::uint32_t code = (a.w >> (2 * c)) & 3u;
+        const std::uint32_t eq2 = (a.w >> 1) & ~a.w & 0x55555555u;
+        const std::uint32_t rank = __popc(eq2 & ((1u << (2 * c)) - 1u));
+        ce = code == 0u ? a.x : (code == 1u ? a.y : (code == 2u ? (kRecordBit | (a.z + rank)) : kEmpty));
+      } else {  // value[3], slot base, 4-bit codes[16], half mask
+        const std::uint32_t code = ((c < 8 ? b.x : b.y) >> (4 * (c & 7))) & 15u;
+        const std::uint32_t off = (code - 4u) & 31u;
+        ce = code < 3u ? (code == 0 ? a.x : (code == 1 ? a.y : a.z))
+                       : (kRecordBit | (((b.z >> off) & 1u) ? kHalfBit : 0u) | (a.w + off));
+      }
+      e[u] = cmp ? ce : f;
+    }
+    return;
+  }
+  const bool two = P.ls == 3;  // 32-byte approx palettes
 #pragma unroll
   for (int u = 0; u < kN; ++u) {
     const std::uint32_t x = be[u];
@@ -93,18 +130,11 @@ __device__ __forceinline__ void locate_n(const KParams& P, const double2 (&p)[kN
     if (cmp && two) b = __ldg(pal4 + 2 * k + 1);
     if (rec && !cmp) f = __ldg(P.sub + (k << (2 * P.ls)) + cc[u]);
     const int c = cc[u];
-    std::uint32_t ce;
-    if (kExact) {  // value[3], slot base, 4-bit codes[16], half mask
-      const std::uint32_t code = ((c < 8 ? b.x : b.y) >> (4 * (c & 7))) & 15u;
-      const std::uint32_t off = (code - 4u) & 31u;
-      ce = code < 3u ? (code == 0 ? a.x : (code == 1 ? a.y : a.z))
-                     : (kRecordBit | (((b.z >> off) & 1u) ? kHalfBit : 0u) | (a.w + off));
-    } else {  // value[3], 2-bit codes
-      const std::uint32_t wsel = (c >> 4) == 0 ? b.x : ((c >> 4) == 1 ? b.y : ((c >> 4) == 2 ? b.z : b.w));
-      const std::uint32_t word = two ? wsel : a.w;
-      const std::uint32_t code = (word >> (2 * (c & 15))) & 3u;
-      ce = code == 0 ? a.x : (code == 1 ? a.y : a.z);
-    }
+    // value[3], 2-bit codes
+    const std::uint32_t wsel = (c >> 4) == 0 ? b.x : ((c >> 4) == 1 ? b.y : ((c >> 4) == 2 ? b.z : b.w));
+    const std::uint32_t word = two ? wsel : a.w;
+    const std::uint32_t code = (word >> (2 * (c & 15))) & 3u;
+    const std::uint32_t ce = code == 0 ? a.x : (code == 1 ? a.y : a.z);
     e[u] = cmp ? ce : f;
   }
 }

@@ -1,13 +1,16 @@
-# tuning variants of the product library: args like B8_U2_M3 (resolve warps,
-# stream points per lane, resolve min blocks per SM for __launch_bounds__)
+# tuning variants of the product library: each arg is NAME=FLAGS, e.g.
+# q4="-DFM_QMINB=4"; builds _lib/var/lib_NAME.so (ptxas log beside it)
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p paper_2005_03156_b200/_lib/var
+rm -f paper_2005_03156_b200/_lib/var/*.so paper_2005_03156_b200/_lib/var/*.log
 for v in "$@"; do
-  B=$(echo $v | sed 's/B\([0-9]*\)_.*/\1/'); U=$(echo $v | sed 's/.*_U\([0-9]*\)_.*/\1/'); M=$(echo $v | sed 's/.*_M\([0-9]*\)/\1/')
+  N=${v%%=*}; F=${v#*=}
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 \
-    -DFM_BWARPS=$B -DFM_KU=$U -DFM_BMINB=$M -Xcompiler -fPIC,-O3,-ffp-contract=off,-pthread -shared \
+    $F -Xcompiler -fPIC,-O3,-ffp-contract=off,-pthread -shared \
     paper_2005_03156_b200/csrc/fastmap_b200.cu paper_2005_03156_b200/csrc/index_gpu.cu paper_2005_03156_b200/csrc/index_host.cpp \
-    -o paper_2005_03156_b200/_lib/var/lib_$v.so -Xptxas -v 2> paper_2005_03156_b200/_lib/var/ptxas_$v.log &
+    paper_2005_03156_b200/csrc/io.cpp paper_2005_03156_b200/csrc/simple.cu \
+    -o paper_2005_03156_b200/_lib/var/lib_$N.so -Xptxas -v 2> paper_2005_03156_b200/_lib/var/ptxas_$N.log &
 done
 wait
+for v in "$@"; do N=${v%%=*}; echo $N $(grep -A2 "Function properties for.*${KER:-resolve_quick_kernelILb0}" paper_2005_03156_b200/_lib/var/ptxas_$N.log | grep -oE "Used [0-9]+ registers|[0-9]+ bytes spill stores"); done
