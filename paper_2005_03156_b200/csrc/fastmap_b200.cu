@@ -1173,12 +1173,14 @@ fm_status build_approx(fm_index* ix) {
 }
 
 // Quick records for the phase-1 slots (after renumbering: record k mirrors
-// slot k).  Disabled by FASTMAP_B200_NO_QUICK=1 (A/B runs) and when the
-// slot count does not fit the kernel's u32 bound.
+// slot k), built when FASTMAP_B200_QUICK=1.  Off by default: on B200 the
+// resolve pass is bound by the rate of random DRAM accesses, one per
+// boundary point either way, so the 32-byte record measured no faster than
+// the 64-byte half slot ("quick records").
 fm_status build_quick(fm_index* ix) {
   const std::uint64_t n1 = ix->host.n_phase1_slots;
-  const char* off = std::getenv("FASTMAP_B200_NO_QUICK");
-  if (n1 == 0 || n1 >= fm::kMaxSlots || (off && off[0] == '1')) return FM_OK;
+  const char* on = std::getenv("FASTMAP_B200_QUICK");
+  if (n1 == 0 || n1 >= fm::kMaxSlots || !(on && on[0] == '1')) return FM_OK;
   FM_CUDA(cudaMalloc(&ix->d_quick, n1 * fm::kQuickBytes));
   const std::uint64_t ncell = ix->grid_len;
   quick_build_kernel<<<static_cast<unsigned>((ncell + 255) / 256), 256>>>(

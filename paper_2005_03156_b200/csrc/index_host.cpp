@@ -524,11 +524,13 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
     if (!(mh > 0.0)) mh = GH / side;
     double m = o.cells_per_polygon;
     if (!(m > 0.0)) {
-      // ~160M cells: fine enough that boundary cells are a minority and
-      // their records short, while the query's folded copy of the grid
-      // keeps an L2-resident block level
-      m = std::sqrt(160.0e6 / static_cast<double>(active));
-      m = std::min(64.0, std::max(4.0, m));
+      // ~450M cells (c2: 42 cells per polygon side, 9% boundary points;
+      // measured optimum 40-48 with 16-byte small sub-blocks), 4..48 per
+      // side; tilings of more than 4M leaves keep ~160M cells, which bounds
+      // their slot arena (c3: 45 GB)
+      const double budget = active > 4000000 ? 160.0e6 : 450.0e6;
+      m = std::sqrt(budget / static_cast<double>(active));
+      m = std::min(48.0, std::max(4.0, m));
     }
     nx = static_cast<std::int64_t>(std::ceil(GW / (mw / m)));
     ny = static_cast<std::int64_t>(std::ceil(GH / (mh / m)));

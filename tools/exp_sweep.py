@@ -34,7 +34,7 @@ def timeit(idx, reps=10):
     return e0.elapsed_time(e1) / reps
 
 
-lib = os.path.basename(os.environ.get("FASTMAP_B200_LIB", "default"))
+lib = os.environ.get("SWEEP_LIB_TAG") or os.path.basename(os.environ.get("FASTMAP_B200_LIB", "default"))
 ms_list = [float(x) for x in sys.argv[1:]] or [0.0]
 for m in ms_list:
     idx = fastmap.build_index(soup, fastmap.CoverParams(cells_per_polygon=m), device=0)

@@ -8,6 +8,7 @@ timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.log 
 fi
 for pass in 1 2; do
 timeout 400 python tools/exp_sweep.py ${SWEEP_MS:-0} >> gpurun_out/${TAG}_sweep.log 2>&1
+if [ -n "$QUICK" ]; then FASTMAP_B200_QUICK=1 SWEEP_LIB_TAG=quick timeout 400 python tools/exp_sweep.py ${SWEEP_MS:-0} >> gpurun_out/${TAG}_sweep.log 2>&1; fi
 for v in paper_2005_03156_b200/_lib/var/*.so; do
   FASTMAP_B200_LIB=$v timeout 400 python tools/exp_sweep.py ${SWEEP_MS:-0} >> gpurun_out/${TAG}_sweep.log 2>&1
 done
