@@ -64,12 +64,15 @@ __device__ __forceinline__ std::uint32_t edge_bit(double px, double py, double a
 // kExact: exact grid (compact sub-blocks: two 16-byte loads;
 // full: one 4-byte load); else an approx cover (palettes: one 16-byte load,
 // or two for 8x8 blocks; full: one 4-byte load).
-template <int kN, bool kExact>
+// kLs >= 0: the fold's block size as a compile-time constant (the query
+// kernels are instantiated per block size); -1: read it from ls.
+template <int kN, bool kExact, int kLs = -1>
 __device__ __forceinline__ void locate_n(const KParams& P, const double2 (&p)[kN],
                                          std::uint32_t (&e)[kN]) {
   std::uint32_t be[kN];
   int cc[kN];
-  const int m = (1 << P.ls) - 1;
+  const int ls = kLs >= 0 ? kLs : P.ls;
+  const int m = (1 << ls) - 1;
 #pragma unroll
   for (int u = 0; u < kN; ++u) {
     const double px = p[u].x, py = p[u].y;
@@ -78,9 +81,9 @@ __device__ __forceinline__ void locate_n(const KParams& P, const double2 (&p)[kN
     int iy = in ? static_cast<int>(__dmul_rn(__dsub_rn(py, P.gy0), P.inv_h)) : 0;
     ix = min(max(ix, 0), P.nx - 1);
     iy = min(max(iy, 0), P.ny - 1);
-    cc[u] = ((iy & m) << P.ls) + (ix & m);
-    be[u] = in ? __ldg(P.blocks + static_cast<std::size_t>(iy >> P.ls) * static_cast<std::size_t>(P.bnx) +
-                       (ix >> P.ls))
+    cc[u] = ((iy & m) << ls) + (ix & m);
+    be[u] = in ? __ldg(P.blocks + static_cast<std::size_t>(iy >> ls) * static_cast<std::size_t>(P.bnx) +
+                       (ix >> ls))
                : kEmpty;
   }
   const uint4* pal4 = reinterpret_cast<const uint4*>(P.pal);
@@ -91,7 +94,7 @@ __device__ __forceinline__ void locate_n(const KParams& P, const double2 (&p)[kN
 #pragma unroll
     for (int u = 0; u < kN; ++u) {
       const std::uint32_t x = be[u];
-      const bool rec = P.ls != 0 && x != kEmpty && x >= kRecordBit;
+      const bool rec = ls != 0 && x != kEmpty && x >= kRecordBit;
       const bool cmp = rec && (x & kHalfBit);
       const bool small = x & kSmallBit;
       const std::size_t k = x & kUnitMask;
@@ -99,7 +102,7 @@ __device__ __forceinline__ void locate_n(const KParams& P, const double2 (&p)[kN
       std::uint32_t f = x;
       if (cmp) a = __ldg(pal4 + k);
       if (cmp && !small) b = __ldg(pal4 + k + 1);
-      if (rec && !cmp) f = __ldg(P.sub + ((x & kSlotIndexMask) << (2 * P.ls)) + cc[u]);
+      if (rec && !cmp) f = __ldg(P.sub + ((x & kSlotIndexMask) << (2 * ls)) + cc[u]);
       const int c = cc[u];
       std::uint32_t ce;
       if (small) {
@@ -117,18 +120,18 @@ __device__ __forceinline__ void locate_n(const KParams& P, const double2 (&p)[kN
     }
     return;
   }
-  const bool two = P.ls == 3;  // 32-byte approx palettes
+  const bool two = ls == 3;  // 32-byte approx palettes
 #pragma unroll
   for (int u = 0; u < kN; ++u) {
     const std::uint32_t x = be[u];
-    const bool rec = P.ls != 0 && x != kEmpty && x >= kRecordBit;
+    const bool rec = ls != 0 && x != kEmpty && x >= kRecordBit;
     const bool cmp = rec && (x & kHalfBit);
     const std::size_t k = x & kSlotIndexMask;
     uint4 a = make_uint4(0u, 0u, 0u, 0u), b = a;
     std::uint32_t f = x;
     if (cmp) a = __ldg(pal4 + (two ? 2 * k : k));
     if (cmp && two) b = __ldg(pal4 + 2 * k + 1);
-    if (rec && !cmp) f = __ldg(P.sub + (k << (2 * P.ls)) + cc[u]);
+    if (rec && !cmp) f = __ldg(P.sub + (k << (2 * ls)) + cc[u]);
     const int c = cc[u];
     // value[3], 2-bit codes
     const std::uint32_t wsel = (c >> 4) == 0 ? b.x : ((c >> 4) == 1 ? b.y : ((c >> 4) == 2 ? b.z : b.w));
