@@ -1,3 +1,4 @@
-timeout 300 python tools/dbg_quick.py c2 4000000 > gpurun_out/dbg19.log 2>&1
-FASTMAP_B200_LIB=paper_2005_03156_b200/_lib/var/lib_a4.so timeout 300 python tools/dbg_quick.py c1 >> gpurun_out/dbg19.log 2>&1
-SWEEP_MS="0" bash tools/gpu_ab.sh ab19
+CMD="python bench.py --mode simple --config c3s --points 20000000 --steps 2 --warmup 3 --no-cpu --no-e2e"
+timeout 600 $CMD > gpurun_out/simple_plain.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:simple_kernel -s 3 -c 1 -o gpurun_out/simple_prof $CMD > gpurun_out/simple_ncu.log 2>&1
+echo ncu=$? >> gpurun_out/simple_ncu.log
