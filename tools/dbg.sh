@@ -1,4 +1,3 @@
-CMD="python bench.py --mode simple --config c3s --points 20000000 --steps 2 --warmup 3 --no-cpu --no-e2e"
-timeout 600 $CMD > gpurun_out/simple_plain.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:simple_kernel -s 3 -c 1 -o gpurun_out/simple_prof $CMD > gpurun_out/simple_ncu.log 2>&1
-echo ncu=$? >> gpurun_out/simple_ncu.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_approx.py -m gpu -x -q > gpurun_out/t22.log 2>&1; echo rc=$? >> gpurun_out/t22.log
+timeout 600 python bench.py --hist --no-cpu --no-e2e > gpurun_out/c2_hist32r.log 2>&1
+timeout 2400 python bench.py --config c5 --points 1000000000 --hist --no-cpu --no-e2e --steps 3 > gpurun_out/c5_hist32r.log 2>&1; echo rc=$? >> gpurun_out/c5_hist32r.log
