@@ -437,7 +437,10 @@ __global__ void __launch_bounds__(256, FM_QMINB)
 // major).  A query is one 16-byte point read, one or two 4-byte gathers and
 // one 4-byte write -- no queue, no crossing tests.
 constexpr int kXThreads = 256;
-constexpr int kXU = 4;
+#ifndef FM_XU
+#define FM_XU 4
+#endif
+constexpr int kXU = FM_XU;
 
 template <bool kHist, bool kCount>
 __global__ void __launch_bounds__(kXThreads)
@@ -447,12 +450,21 @@ __global__ void __launch_bounds__(kXThreads)
   const std::uint64_t chunk = static_cast<std::uint64_t>(kXThreads) * kXU;
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * chunk;
   unsigned long long done = 0;
-  for (std::uint64_t b = blockIdx.x * chunk + threadIdx.x; b < n + threadIdx.x; b += stride) {
+  // the next chunk's points are loaded while this chunk's gathers run
+  double2 pn[kXU];
+  const std::uint64_t b0 = blockIdx.x * chunk + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kXU; ++u) {
+    const std::uint64_t i = b0 + static_cast<std::uint64_t>(u) * kXThreads;
+    pn[u] = i < n ? __ldcs(pts + i) : make_double2(NAN, NAN);
+  }
+  for (std::uint64_t b = b0; b < n + threadIdx.x; b += stride) {
     double2 p[kXU];
 #pragma unroll
     for (int u = 0; u < kXU; ++u) {
-      const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kXThreads;
-      p[u] = i < n ? __ldcs(pts + i) : make_double2(NAN, NAN);
+      p[u] = pn[u];
+      const std::uint64_t i = b + stride + static_cast<std::uint64_t>(u) * kXThreads;
+      pn[u] = i < n ? __ldcs(pts + i) : make_double2(NAN, NAN);
     }
     std::uint32_t e[kXU];
     fm::locate_n<kXU, false>(A, p, e);
