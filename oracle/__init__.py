@@ -99,6 +99,12 @@ def ref():
         L.ref_simple_assign_fmcb.argtypes = [C.c_char_p, PD, u64, C.c_int, PI32, PI32, PI32, PU64]
         L.ref_simple_assign_fmcb.restype = C.c_int
         L.ref_cell_from_point.argtypes = [C.c_double, C.c_double, C.c_int, PU64]
+        if hasattr(L, "ref_ingest_geojson"):  # built with nlohmann json on the include path
+            L.ref_ingest_geojson.argtypes = [C.c_char_p] * 4
+            L.ref_ingest_geojson.restype = C.c_int
+            L.ref_write_synthetic_geojson.argtypes = [u64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                                      C.c_double, C.c_char_p]
+            L.ref_write_synthetic_geojson.restype = C.c_int
         _ref = L
     return _ref
 
@@ -265,6 +271,26 @@ def ref_save_synthetic_fmcb(seed, n_states, counties_per_state, blocks_per_count
 def ref_load_fmcb_status(path) -> int:
     """load_hierarchy's verdict: 0 ok, 1 runtime_error, 2 invalid_argument, 3 other."""
     return int(ref().ref_load_fmcb_status(str(path).encode()))
+
+
+def ref_geojson_available() -> bool:
+    return ref_available() and hasattr(ref(), "ref_ingest_geojson")
+
+
+def ref_ingest_geojson(states, counties, blocks, out_fmcb):
+    """The reference's `fastmap ingest` (load_boundaries + save_hierarchy):
+    (status, message) -- 0 ok, 1 runtime_error, 2 invalid_argument, 3 other."""
+    L = ref()
+    rc = L.ref_ingest_geojson(*(str(x).encode() for x in (states, counties, blocks, out_fmcb)))
+    return int(rc), (L.ref_last_error().decode() if rc else "")
+
+
+def ref_write_synthetic_geojson(seed, n_states, counties_per_state, blocks_per_county, jitter, out_dir):
+    """The reference's write_boundaries over its generate_synthetic hierarchy."""
+    rc = ref().ref_write_synthetic_geojson(seed, n_states, counties_per_state, blocks_per_county,
+                                           jitter, str(out_dir).encode())
+    if rc != 0:
+        raise RuntimeError("reference write_boundaries failed")
 
 
 def ref_simple_assign(path, pts, strict: bool):

@@ -378,3 +378,48 @@ int ref_simple_assign_fmcb(const char* path, const double* lonlat, std::uint64_t
 }
 
 }  // extern "C"
+
+// GeoJSON ingestion (geojson.hpp, needs nlohmann json.hpp on the include
+// path -- present in this container, see oracle/Makefile): the reference's
+// own `fastmap ingest` (tools/fastmap.cpp:163-170) and `generate` writer
+// (write_boundaries), as fixtures and verdicts for the product's loader.
+#if __has_include(<json.hpp>)
+#include "fastmap/geojson.hpp"
+extern "C" {
+
+// load_boundaries + save_hierarchy.  0 ok, 1 runtime_error, 2
+// invalid_argument, 3 any other exception (message: ref_last_error).
+int ref_ingest_geojson(const char* states, const char* counties, const char* blocks,
+                       const char* out_fmcb) {
+  try {
+    save_hierarchy(load_boundaries(states, counties, blocks), out_fmcb);
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 2);
+  } catch (const std::runtime_error& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
+// generate_synthetic + write_boundaries into `dir` (states/counties/blocks.geojson).
+int ref_write_synthetic_geojson(std::uint64_t seed, std::uint32_t n_states,
+                                std::uint32_t counties_per_state, std::uint32_t blocks_per_county,
+                                double jitter, const char* dir) {
+  try {
+    SyntheticSpec spec;
+    spec.seed = seed;
+    spec.n_states = n_states;
+    spec.counties_per_state = counties_per_state;
+    spec.blocks_per_county = blocks_per_county;
+    spec.jitter = jitter;
+    write_boundaries(generate_synthetic(spec), dir);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+
+}  // extern "C"
+#endif

@@ -23,6 +23,9 @@ reference (file:line)                        here
 FMCI save/load cell_index.hpp:641-726         :meth:`CellIndex.save` / :func:`load_index`
 ``read_points_f64`` io.hpp:154-167            :func:`read_points_f64`
 assign CSV tools/fastmap.cpp:288-301          :func:`write_assign_csv`
+``load_boundaries`` / ``write_boundaries``   :mod:`paper_2005_03156_b200.geojson`
+  geojson.hpp:154-271, :276-353; ``fastmap    (``load_boundaries``, ``ingest``,
+  ingest`` tools/fastmap.cpp:163-170          ``write_boundaries``)
 ``AssignMode``, ``assign`` simple_mapper.hpp  :class:`AssignMode`, :func:`assign` (the simple
   :24, :119-166                               engine on the GPU, :class:`SimpleEngine`)
 ===========================================  =====================================
