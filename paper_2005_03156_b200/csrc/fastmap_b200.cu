@@ -962,8 +962,8 @@ __global__ void __launch_bounds__(256)
   const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const HistT v = h32[i];
-  if (v) {
-    h64[i] += v;
+  if (v) {  // atomic: queries on other streams may add into the same histogram
+    atomicAdd(h64 + i, static_cast<unsigned long long>(v));
     h32[i] = 0;
   }
 }

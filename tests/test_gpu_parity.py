@@ -177,3 +177,27 @@ def test_quick_records_resolve_bit_exact(dev, monkeypatch, name, n, m):
     hist = torch.zeros(soup.n_polys, dtype=torch.int64, device=dev)
     idx.project(torch.from_numpy(pts).to(dev), hist=hist)
     assert np.array_equal(hist.cpu().numpy(), np.bincount(want[want >= 0], minlength=soup.n_polys))
+
+
+def test_histogram_shared_across_streams_and_host_chunks(dev):
+    """The per-launch u32 counters are folded into the caller's int64
+    histogram atomically: host-path chunks on 3 streams, and device queries
+    on 4 concurrent streams into one histogram, lose no counts."""
+    cfg = synth.config("c2")
+    soup = cfg.make_soup()
+    pts = cfg.make_points(30_000_000, soup=soup, offset=77)  # 4 host chunks of 8M points
+    idx = fastmap.build_index(soup, device=0)
+    hist = np.zeros(soup.n_polys, dtype=np.int64)
+    got = idx.project(pts, hist=hist)
+    assert np.array_equal(hist, np.bincount(got[got >= 0], minlength=soup.n_polys))
+    d = torch.from_numpy(pts).to(dev)
+    dh = torch.zeros(soup.n_polys, dtype=torch.int64, device=dev)
+    outs, streams = [], [torch.cuda.Stream(dev) for _ in range(4)]
+    torch.cuda.synchronize()
+    for k, s in enumerate(streams):
+        with torch.cuda.stream(s):
+            outs.append(idx.project(d[k * 7_000_000:(k + 1) * 7_000_000], hist=dh, stream=s.cuda_stream))
+    torch.cuda.synchronize()
+    allout = torch.cat(outs).cpu().numpy()
+    assert np.array_equal(allout, got[:28_000_000])
+    assert np.array_equal(dh.cpu().numpy(), np.bincount(allout[allout >= 0], minlength=soup.n_polys))
