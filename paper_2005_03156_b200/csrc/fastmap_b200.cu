@@ -972,7 +972,7 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
                  unsigned long long* d_hist, unsigned long long* d_counters,
                  cudaStream_t stream, int mode = FM_MODE_EXACT) {
   const double2* pts = reinterpret_cast<const double2*>(d_pts);
-  if (mode == FM_MODE_APPROX) {
+  if (mode == FM_MODE_APPROX && ix->agrid.blocks) {
     if (d_hist && d_counters) return launch_approx_t<true, true>(ix, pts, n, d_out, d_hist, d_counters, stream);
     if (d_hist) return launch_approx_t<true, false>(ix, pts, n, d_out, d_hist, d_counters, stream);
     if (d_counters) return launch_approx_t<false, true>(ix, pts, n, d_out, d_hist, d_counters, stream);
@@ -1266,7 +1266,9 @@ fm_status finish_device(fm_index* ix, double approx_epsilon) {
   ix->stats.query_grid_bytes = ix->qgrid.bytes;
   ix->stats.query_block_log2 = ix->qgrid.ls;
   ix->stats.approx_epsilon = approx_epsilon;
-  if (approx_epsilon > 0.0) return build_approx(ix);
+  // an epsilon too fine for the uniform approx grid: approximate queries
+  // take the exact path (fm_index_stats.approx_grid_bytes stays 0)
+  if (approx_epsilon > 0.0 && !ix->host.stats.approx_served_exact) return build_approx(ix);
   return FM_OK;
 }
 
@@ -1715,6 +1717,9 @@ fm_status fm_index_load(const char* path, int device, fm_index** out_index) {
   ix->ay0 = std::max(g.gy0, -90.0);
   ix->ay1 = std::min(g.gy1, 90.0);
   const double eps = ix->stats.approx_epsilon;
+  // the grid itself tells whether the approx cover fits (cells within epsilon)
+  ix->host.stats.approx_served_exact =
+      eps > 0.0 && !(std::hypot(ix->g.w + 2.0 * ix->g.margin, ix->g.h + 2.0 * ix->g.margin) <= eps);
   ix->stats.query_grid_bytes = 0;
   ix->stats.query_block_log2 = 0;
   ix->stats.approx_grid_bytes = 0;

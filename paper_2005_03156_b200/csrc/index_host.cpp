@@ -460,6 +460,7 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
   if (!(o.cells_per_polygon >= 0.0) || !(o.margin >= 0.0) || o.nx < 0 || o.ny < 0) {
     throw InvalidArgument("invalid index build parameters");
   }
+  bool served_exact = false;  // see BuildStats::approx_served_exact
   double ux0 = INFINITY, ux1 = -INFINITY, uy0 = INFINITY, uy1 = -INFINITY;
   double sum_w = 0.0, sum_h = 0.0;
   std::uint64_t active = 0, n_edges = 0;
@@ -548,15 +549,19 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
     if (!(side > 0.0)) throw InvalidArgument("approx epsilon is below the classification margin");
     const double ex = std::ceil(GW / side), ey = std::ceil(GH / side);
     if (ex * ey > static_cast<double>(std::int64_t{1} << 31)) {
-      throw InvalidArgument("approx epsilon " + std::to_string(o.approx_epsilon) + " needs " +
-                            std::to_string(ex * ey) +
-                            " uniform-grid cells over this extent (limit 2^31)");
+      // finer than a uniform grid of 2^31 cells can resolve over this
+      // extent: plan the exact grid and serve approximate queries exactly,
+      // which meets the reference's bound (answers within epsilon of the
+      // exact one, test_cell_index.cpp:381-435) with error 0
+      served_exact = true;
+      if (st) st->approx_served_exact = true;
+    } else {
+      // auto resolution: exactly what epsilon needs (the reference's approx
+      // cover stops refining there too); explicit resolutions are only raised
+      const bool explicit_res = (o.nx > 0 && o.ny > 0) || o.cells_per_polygon > 0.0;
+      nx = explicit_res ? std::max(nx, static_cast<std::int64_t>(ex)) : static_cast<std::int64_t>(ex);
+      ny = explicit_res ? std::max(ny, static_cast<std::int64_t>(ey)) : static_cast<std::int64_t>(ey);
     }
-    // auto resolution: exactly what epsilon needs (the reference's approx
-    // cover stops refining there too); explicit resolutions are only raised
-    const bool explicit_res = (o.nx > 0 && o.ny > 0) || o.cells_per_polygon > 0.0;
-    nx = explicit_res ? std::max(nx, static_cast<std::int64_t>(ex)) : static_cast<std::int64_t>(ex);
-    ny = explicit_res ? std::max(ny, static_cast<std::int64_t>(ey)) : static_cast<std::int64_t>(ey);
   }
   if (nx * ny > (std::int64_t{1} << 31)) throw InvalidArgument("grid too large");
   g.nx = nx;
@@ -565,7 +570,7 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
   g.h = GH / static_cast<double>(ny);
   g.inv_w = static_cast<double>(nx) / GW;
   g.inv_h = static_cast<double>(ny) / GH;
-  if (o.approx_epsilon > 0.0 &&
+  if (o.approx_epsilon > 0.0 && !served_exact &&
       !(std::hypot(g.w + 2.0 * g.margin, g.h + 2.0 * g.margin) <= o.approx_epsilon)) {
     throw InvalidArgument("grid cells exceed the approx epsilon");
   }

@@ -106,6 +106,9 @@ def test_approx_cover_params_and_resolution():
     fine = fastmap.build_index(soup, fastmap.CoverParams(mode=fastmap.CoverMode.approx, epsilon=eps,
                                                          nx=5000, ny=300), device=-1).stats()
     assert fine["nx"] == 5000 and fine["ny"] == s["ny"]
-    with pytest.raises(ValueError, match="needs .* cells"):  # bounded uniform grid
-        fastmap.build_index(soup, fastmap.CoverParams(mode=fastmap.CoverMode.approx,
-                                                      epsilon=1e-6), device=-1)
+    # an epsilon finer than a 2^31-cell uniform grid resolves: the exact grid,
+    # approximate queries answered exactly (error 0 <= epsilon)
+    tiny = fastmap.build_index(soup, fastmap.CoverParams(mode=fastmap.CoverMode.approx,
+                                                         epsilon=1e-6), device=-1).stats()
+    exact = fastmap.build_index(soup, device=-1).stats()
+    assert tiny["approx_epsilon"] == 1e-6 and (tiny["nx"], tiny["ny"]) == (exact["nx"], exact["ny"])

@@ -102,3 +102,25 @@ def test_query_mode_rejects_unknown_mode(dev):
     st = N.lib().fm_query_host_mode(idx.handle, 7, N.ptr(pts, N.C.c_double), 10,
                                     N.ptr(out, N.C.c_int32), None)
     assert st == 1
+
+
+def test_approx_epsilon_finer_than_the_uniform_grid_is_served_exactly(dev, tmp_path):
+    """epsilon = 1e-6 would need > 2^31 uniform approx cells over c1's extent:
+    the index is the exact one and approximate queries return the exact
+    answers (error 0 <= epsilon, the reference's bound,
+    test_cell_index.cpp:381-435); the choice survives save / load."""
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    pts = cfg.make_points(500_000, offset=31)
+    idx = fastmap.build_index(soup, CoverParams(mode=CoverMode.approx, epsilon=1e-6), device=0)
+    st = idx.stats()
+    assert st["approx_epsilon"] == 1e-6 and st["approx_grid_bytes"] == 0
+    want = oracle.assign(soup, pts)
+    d = torch.from_numpy(pts).to(dev)
+    assert np.array_equal(idx.project(d, mode=CoverMode.approx).cpu().numpy(), want)
+    assert np.array_equal(idx.project(pts, mode=CoverMode.approx), want)
+    p = tmp_path / "tiny.fmgi"
+    idx.save(p)
+    again = fastmap.load_index(p, device=0)
+    assert again.stats()["approx_grid_bytes"] == 0
+    assert np.array_equal(again.project(pts, mode=CoverMode.approx), want)
