@@ -1324,6 +1324,14 @@ const char* fm_last_error(void) { return g_err.c_str(); }
 
 const char* fm_version(void) { return "fastmap_b200 0.1 (sm_100a)"; }
 
+// For simple.cu (not part of the C-ABI): the query-side kernel parameters
+// of a device index, for device-side single-point lookups.
+__attribute__((visibility("hidden"))) bool fm_index_kparams(const fm_index* ix, fm::KParams* out) {
+  if (!ix || ix->device < 0) return false;
+  *out = kparams(ix);
+  return true;
+}
+
 fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_offsets,
                          std::uint64_t n_rings, const std::uint64_t* poly_ring_offsets,
                          std::uint64_t n_polys, const fm_build_params* params,
