@@ -265,59 +265,65 @@ __global__ void __launch_bounds__(256, FM_SIMPLE_MINB)
       // cells clamp; NaN maps to cell 0 and fails every strict bbox test
       const int cx = band_of(p.x, L.gx0, L.inv_w, L.gnx), cy = band_of(p.y, L.gy0, L.inv_h, L.gny);
       const std::uint64_t c = static_cast<std::uint64_t>(cy) * L.gnx + cx;
-      const std::uint32_t k0 = __ldg(L.cell_off + c), k1 = __ldg(L.cell_off + c + 1);
       const double4* R = reinterpret_cast<const double4*>(L.reg);
-      int cnt = 0, last = -1;
-      for (std::uint32_t k = k0; k < k1; ++k) {
-        const std::uint32_t r = __ldg(L.cell_ids + k);
-        if (r >= lo && r < hi) {
+      // The reference takes the first candidate (ascending) whose polygon
+      // holds p (relaxed: a unique candidate untested).  r = E(p) over the
+      // whole level, from the level's exact index, is the smallest region
+      // holding p: if r is a candidate (a child of this parent whose file
+      // bbox strictly contains p) it is the answer in both modes -- the first
+      // holding candidate, or the unique one -- with no candidate scan at
+      // all; if no region holds p, no candidate does (strict: unresolved;
+      // relaxed: the unique or highest candidate, from the scan).  Anything
+      // else -- r not a candidate, or p outside the world box, where the
+      // index answers -1 by query_leaves' rule -- takes the reference's own
+      // scan and crossing tests, as do counting runs (pip_calls).
+      int win = -1;
+      bool decided = false, none_holds = false;
+      if (!kCount && P.use_index && p.x >= -180.0 && p.x <= 180.0 && p.y >= -90.0 && p.y <= 90.0) {
+        const int r = level_lookup(P.Q[l], p.x, p.y);  // P.Q: global memory
+        if (r < 0) {
+          none_holds = true;
+          decided = kStrict;
+        } else if (static_cast<std::uint32_t>(r) >= lo && static_cast<std::uint32_t>(r) < hi) {
           const double4 a = ld4(R + 2 * r);
           if (a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w) {
-            ++cnt;
-            last = static_cast<int>(r);
+            win = r;
+            decided = true;
           }
         }
       }
-      if (cnt == 0) break;
-      int win = -1;
-      if (cnt >= (kStrict ? 1 : 2)) {  // the polygon-tested ("pending") points
-        // The reference takes the first candidate (ascending) whose polygon
-        // holds p.  r = E(p) over the whole level is the smallest region
-        // holding p: if r is a candidate (a child of this parent whose file
-        // bbox strictly contains p) it is that first candidate, and if no
-        // region holds p no candidate does.  Anything else -- r outside the
-        // candidates, or p outside the world box, where the index answers -1
-        // by the reference's query_leaves rule -- takes the crossing tests.
-        // Counting runs always take them (pip_calls / evaluations).
-        bool decided = false;
-        if (!kCount && P.use_index && p.x >= -180.0 && p.x <= 180.0 && p.y >= -90.0 && p.y <= 90.0) {
-          const int r = level_lookup(P.Q[l], p.x, p.y);  // P.Q: global memory
-          if (r < 0) {
-            decided = true;
-          } else if (static_cast<std::uint32_t>(r) >= lo && static_cast<std::uint32_t>(r) < hi) {
+      int cnt = 0, last = -1;
+      if (!decided) {
+        const std::uint32_t k0 = __ldg(L.cell_off + c), k1 = __ldg(L.cell_off + c + 1);
+        for (std::uint32_t k = k0; k < k1; ++k) {
+          const std::uint32_t r = __ldg(L.cell_ids + k);
+          if (r >= lo && r < hi) {
             const double4 a = ld4(R + 2 * r);
             if (a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w) {
-              win = r;
-              decided = true;
+              ++cnt;
+              last = static_cast<int>(r);
             }
           }
         }
-        for (std::uint32_t k = decided ? k1 : k0; k < k1; ++k) {
-          const std::uint32_t r = __ldg(L.cell_ids + k);
-          if (r < lo || r >= hi) continue;
-          const double4 a = ld4(R + 2 * r);
-          if (!(a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w)) continue;
-          if (kCount) {
-            ++ev;
-            L.tested[r] = 1;
-          }
-          if (region_pip(L, ld4(R + 2 * r + 1), p.x, p.y)) {
-            win = static_cast<int>(r);
-            break;  // first hit wins (simple_mapper.hpp:98-101)
+        if (cnt == 0) break;
+        if (cnt >= (kStrict ? 1 : 2) && !none_holds) {  // the polygon-tested ("pending") points
+          for (std::uint32_t k = k0; k < k1; ++k) {
+            const std::uint32_t r = __ldg(L.cell_ids + k);
+            if (r < lo || r >= hi) continue;
+            const double4 a = ld4(R + 2 * r);
+            if (!(a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w)) continue;
+            if (kCount) {
+              ++ev;
+              L.tested[r] = 1;
+            }
+            if (region_pip(L, ld4(R + 2 * r + 1), p.x, p.y)) {
+              win = static_cast<int>(r);
+              break;  // first hit wins (simple_mapper.hpp:98-101)
+            }
           }
         }
       }
-      if (win < 0 && !kStrict) win = last;  // unique or highest-indexed candidate
+      if (win < 0 && !kStrict && !decided) win = last;  // unique or highest-indexed candidate
       if (win < 0) break;
       res[l] = win - static_cast<int>(lo);
       if (l < 2) {

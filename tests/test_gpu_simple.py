@@ -124,3 +124,27 @@ def test_nested_config_against_reference(tmp_path):
     hit = leaf >= 0
     agree = (res.block[hit] == h.scb[leaf[hit], 2].astype(np.int32)).mean()
     assert agree > 0.9999  # differs only for points on shared state/county borders
+
+
+@needs_ref
+def test_hierarchy_straddling_the_world_box(tmp_path):
+    """Regions partly outside lon 180: there the level indexes answer -1 by
+    query_leaves' world rule (cell_index.hpp:549-552), which assign() does
+    not have, so the engine must fall back to the crossing tests."""
+    states = fmcb_writer.random_hierarchy(4)
+    def shift(node):
+        node["rings"] = [[(x + 177.5, y + 87.0) for x, y in r] for r in node["rings"]]
+        if node.get("bbox"):
+            x0, x1, y0, y1 = node["bbox"]
+            node["bbox"] = (x0 + 177.5, x1 + 177.5, y0 + 87.0, y1 + 87.0)
+        for c in node.get("children", []):
+            shift(c)
+    for s in states:
+        shift(s)
+    p = tmp_path / "edge.fmcb"
+    fmcb_writer.write_fmcb(p, states)
+    h = fastmap.load_hierarchy(p)
+    pts = probe_points(h, 30_000, 9)
+    assert (pts[:, 0] > 180.0).mean() > 0.1 and (pts[:, 1] > 90.0).mean() > 0.1
+    got = check_against_reference(p, pts)
+    assert (got.state[pts[:, 0] > 180.0] >= 0).any()  # assigned outside the world box
