@@ -201,3 +201,36 @@ def test_histogram_shared_across_streams_and_host_chunks(dev):
     allout = torch.cat(outs).cpu().numpy()
     assert np.array_equal(allout, got[:28_000_000])
     assert np.array_equal(dh.cpu().numpy(), np.bincount(allout[allout >= 0], minlength=soup.n_polys))
+
+
+def test_invariance_under_ring_rotation_and_power_of_two_translation(dev):
+    """test_geometry.cpp:145-184 through the GPU index: a soup of random
+    star polygons, the same soup with every ring's start rotated, and the
+    soup plus points translated by (64, -32) give identical answers (the
+    translated points off the edges by > 1e-9, as the reference requires)."""
+    rng = np.random.default_rng(17)
+    rings = []
+    for k in range(60):
+        c = rng.uniform(-20, 20, 2)
+        n = int(rng.integers(5, 40))
+        a = np.sort(rng.random(n)) * 2 * np.pi
+        r = rng.uniform(0.5, 2.0, n)
+        rings.append(np.stack([c[0] + r * np.cos(a), c[1] + r * np.sin(a)], 1))
+    pts = rng.uniform(-23, 23, (200_000, 2))
+    base_soup = fastmap.Soup.from_rings([[r] for r in rings])
+    want = oracle.assign(base_soup, pts)
+    got = project_device(fastmap.build_index(base_soup, device=0), pts, dev)
+    assert np.array_equal(got, want)
+    rot = fastmap.Soup.from_rings([[np.roll(r, 13 % len(r), axis=0)] for r in rings])
+    assert np.array_equal(project_device(fastmap.build_index(rot, device=0), pts, dev), want)
+    shift = np.array([64.0, -32.0])
+    moved = fastmap.Soup.from_rings([[r + shift] for r in rings])
+    far = np.ones(len(pts), dtype=bool)
+    for r in rings:  # keep points farther than 1e-9 from every edge
+        a, b = r, np.roll(r, -1, axis=0)
+        for j in range(len(r)):
+            d = b[j] - a[j]
+            t = np.clip(((pts - a[j]) @ d) / (d @ d), 0, 1)
+            far &= np.hypot(*(pts - (a[j] + t[:, None] * d)).T) > 1e-9
+    moved_got = project_device(fastmap.build_index(moved, device=0), pts + shift, dev)
+    assert np.array_equal(moved_got[far], want[far])
