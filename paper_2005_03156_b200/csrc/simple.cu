@@ -271,26 +271,32 @@ __global__ void __launch_bounds__(256, FM_SIMPLE_MINB)
       // whole level, from the level's exact index, is the smallest region
       // holding p: if r is a candidate (a child of this parent whose file
       // bbox strictly contains p) it is the answer in both modes -- the first
-      // holding candidate, or the unique one -- with no candidate scan at
-      // all; if no region holds p, no candidate does (strict: unresolved;
-      // relaxed: the unique or highest candidate, from the scan).  Anything
-      // else -- r not a candidate, or p outside the world box, where the
-      // index answers -1 by query_leaves' rule -- takes the reference's own
-      // scan and crossing tests, as do counting runs (pip_calls).
+      // holding candidate, or the unique one -- and if no region holds p, no
+      // candidate does (strict: unresolved; relaxed: the unique or highest
+      // candidate).  Anything else -- r not a candidate, or p outside the
+      // world box, where the index answers -1 by query_leaves' rule -- takes
+      // the reference's own crossing tests.  Counting runs scan the
+      // candidates either way: a pending point's evaluations are its
+      // candidates up to the first holder (simple_mapper.hpp:84-101).
       int win = -1;
-      bool decided = false, none_holds = false;
-      if (!kCount && P.use_index && p.x >= -180.0 && p.x <= 180.0 && p.y >= -90.0 && p.y <= 90.0) {
+      bool known = false;  // index answer usable: `holder` is the first holder or -1
+      int holder = -1;
+      if (P.use_index && p.x >= -180.0 && p.x <= 180.0 && p.y >= -90.0 && p.y <= 90.0) {
         const int r = level_lookup(P.Q[l], p.x, p.y);  // P.Q: global memory
         if (r < 0) {
-          none_holds = true;
-          decided = kStrict;
+          known = true;
         } else if (static_cast<std::uint32_t>(r) >= lo && static_cast<std::uint32_t>(r) < hi) {
           const double4 a = ld4(R + 2 * r);
           if (a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w) {
-            win = r;
-            decided = true;
+            known = true;
+            holder = r;
           }
         }
+      }
+      bool decided = false;
+      if (!kCount && known && (holder >= 0 || kStrict)) {  // no scan needed
+        win = holder;
+        decided = true;
       }
       int cnt = 0, last = -1;
       if (!decided) {
@@ -306,19 +312,33 @@ __global__ void __launch_bounds__(256, FM_SIMPLE_MINB)
           }
         }
         if (cnt == 0) break;
-        if (cnt >= (kStrict ? 1 : 2) && !none_holds) {  // the polygon-tested ("pending") points
-          for (std::uint32_t k = k0; k < k1; ++k) {
-            const std::uint32_t r = __ldg(L.cell_ids + k);
-            if (r < lo || r >= hi) continue;
-            const double4 a = ld4(R + 2 * r);
-            if (!(a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w)) continue;
-            if (kCount) {
-              ++ev;
-              L.tested[r] = 1;
+        if (cnt >= (kStrict ? 1 : 2)) {  // the polygon-tested ("pending") points
+          if (known) {
+            win = holder;
+            if (kCount) {  // the candidates the reference evaluates: up to the holder
+              for (std::uint32_t k = k0; k < k1; ++k) {
+                const std::uint32_t r = __ldg(L.cell_ids + k);
+                if (r < lo || r >= hi || (holder >= 0 && r > static_cast<std::uint32_t>(holder))) continue;
+                const double4 a = ld4(R + 2 * r);
+                if (!(a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w)) continue;
+                ++ev;
+                L.tested[r] = 1;
+              }
             }
-            if (region_pip(L, ld4(R + 2 * r + 1), p.x, p.y)) {
-              win = static_cast<int>(r);
-              break;  // first hit wins (simple_mapper.hpp:98-101)
+          } else {
+            for (std::uint32_t k = k0; k < k1; ++k) {
+              const std::uint32_t r = __ldg(L.cell_ids + k);
+              if (r < lo || r >= hi) continue;
+              const double4 a = ld4(R + 2 * r);
+              if (!(a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w)) continue;
+              if (kCount) {
+                ++ev;
+                L.tested[r] = 1;
+              }
+              if (region_pip(L, ld4(R + 2 * r + 1), p.x, p.y)) {
+                win = static_cast<int>(r);
+                break;  // first hit wins (simple_mapper.hpp:98-101)
+              }
             }
           }
         }
