@@ -73,7 +73,7 @@ typedef struct fm_index fm_index;
  * Zero-initialise and set what you need. */
 typedef struct fm_build_params {
   /* Grid resolution: cells per mean polygon bbox side.  0 = auto
-   * (about 450M cells in total, 160M above 4M leaves, clamped to [4, 48]
+   * (about 450M cells in total, 270M above 4M leaves, clamped to [4, 48]
    * per polygon side). */
   double cells_per_polygon;
   /* Explicit grid dimensions; both > 0 override cells_per_polygon. */

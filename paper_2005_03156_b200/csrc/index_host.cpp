@@ -527,9 +527,10 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
     if (!(m > 0.0)) {
       // ~450M cells (c2: 42 cells per polygon side, 9% boundary points;
       // measured optimum 40-48 with 16-byte small sub-blocks), 4..48 per
-      // side; tilings of more than 4M leaves keep ~160M cells, which bounds
-      // their slot arena (c3: 45 GB)
-      const double budget = active > 4000000 ? 160.0e6 : 450.0e6;
+      // side; tilings of more than 4M leaves take ~270M cells, which bounds
+      // their slot arena (c3: 50 GB; 8.83 -> 8.33 ms per 200M points against
+      // 160M cells)
+      const double budget = active > 4000000 ? 270.0e6 : 450.0e6;
       m = std::sqrt(budget / static_cast<double>(active));
       m = std::min(48.0, std::max(4.0, m));
     }
