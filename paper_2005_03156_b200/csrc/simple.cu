@@ -521,6 +521,15 @@ fm_status fm_simple_build(const fm_hierarchy* h, int device, fm_simple** out) {
       fm_build_params bp{};
       bp.device = device;
       bp.build_on_gpu = 1;
+      // the upper levels have few, large regions: their indexes get about
+      // as many cells as the leaf level's 48 per polygon side would, up to
+      // 64M, so boundary cells stay simple (c3s: relaxed 6.68 -> 6.18 ms,
+      // strict 6.54 -> 6.06 ms per 100M points, same box)
+      if (l < 2 && L.n_regions() > 0) {
+        const double leaf_cells = 2304.0 * static_cast<double>(h->level[2].n_regions());
+        bp.cells_per_polygon =
+            std::max(48.0, std::sqrt(std::min(64.0e6, leaf_cells) / static_cast<double>(L.n_regions())));
+      }
       const fm_status bs = fm_index_build(L.vxy.data(), L.ring_off.data(), L.ring_off.size() - 1,
                                           L.poly_ring.data(), L.n_regions(), &bp, &s->lidx[l]);
       ok = bs == FM_OK && fm_index_kparams(s->lidx[l], &q[l]);
