@@ -74,7 +74,7 @@ typedef struct fm_index fm_index;
 typedef struct fm_build_params {
   /* Grid resolution: cells per mean polygon bbox side.  0 = auto
    * (about 450M cells in total, 270M above 4M leaves, clamped to [4, 48]
-   * per polygon side). */
+   * per polygon side, and at least ~10M cells). */
   double cells_per_polygon;
   /* Explicit grid dimensions; both > 0 override cells_per_polygon. */
   int64_t nx, ny;

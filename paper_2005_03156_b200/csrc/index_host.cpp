@@ -533,6 +533,11 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
       const double budget = active > 4000000 ? 270.0e6 : 450.0e6;
       m = std::sqrt(budget / static_cast<double>(active));
       m = std::min(48.0, std::max(4.0, m));
+      // few polygons (>= 64): still at least ~10M cells (a ~40 MB grid, L2-sized),
+      // since the 48-per-side cap would leave a needlessly coarse grid
+      // (c1, 1,024 polygons: 48 -> 99 per side, 0.70 -> 0.62 ms per 100M
+      // points)
+      if (active >= 64) m = std::max(m, std::min(1024.0, std::sqrt(10.0e6 / static_cast<double>(active))));
     }
     nx = static_cast<std::int64_t>(std::ceil(GW / (mw / m)));
     ny = static_cast<std::int64_t>(std::ceil(GH / (mh / m)));
