@@ -29,6 +29,7 @@
 #pragma once
 
 #include <cstdint>
+#include <filesystem>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -204,6 +205,69 @@ inline std::vector<std::int32_t> exhaustive_assign(std::span<const LeafRegion> l
                                                    int device = 0) {
   const auto index = build_index(leaves, CoverParams{}, IndexParams{0.0, device, 0});
   return project(index, points);
+}
+
+namespace detail {
+struct HierarchyDeleter {
+  void operator()(fm_hierarchy* p) const { fm_hierarchy_destroy(p); }
+};
+struct SimpleDeleter {
+  void operator()(fm_simple* p) const { fm_simple_destroy(p); }
+};
+}  // namespace detail
+
+/// The simple engine (the paper's hierarchical descent, simple_mapper.hpp:
+/// 62-166) on the GPU.  The hierarchy is handed to the library as FMCB
+/// bytes written by the reference's own save_hierarchy (hierarchy.hpp:
+/// 187-198), through a temporary file.
+class SimpleEngine {
+ public:
+  explicit SimpleEngine(const RegionHierarchy& h, int device = 0) {
+    namespace fs = std::filesystem;
+    const fs::path tmp = fs::temp_directory_path() /
+                         ("fastmap_gpu_" + std::to_string(reinterpret_cast<std::uintptr_t>(this)) + ".fmcb");
+    save_hierarchy(h, tmp.string());
+    fm_hierarchy* hh = nullptr;
+    const fm_status st = fm_hierarchy_load(tmp.string().c_str(), &hh);
+    std::error_code ec;
+    fs::remove(tmp, ec);
+    detail::check(st, "fm_hierarchy_load");
+    h_.reset(hh);
+    fm_simple* e = nullptr;
+    detail::check(fm_simple_build(h_.get(), device, &e), "fm_simple_build");
+    e_.reset(e);
+  }
+  fm_simple* get() const { return e_.get(); }
+
+ private:
+  std::unique_ptr<fm_hierarchy, detail::HierarchyDeleter> h_;
+  std::unique_ptr<fm_simple, detail::SimpleDeleter> e_;
+};
+
+/// assign(h, points, mode) (simple_mapper.hpp:119-166): state / county /
+/// block per point (local indices, -1 unresolved) and the reference's
+/// AssignCounters, bit-identical to the reference's.
+inline AssignmentResult assign(const SimpleEngine& engine, std::span<const Point> points,
+                               AssignMode mode = AssignMode::relaxed) {
+  static_assert(sizeof(Point) == 16, "Point is two doubles");
+  AssignmentResult r;
+  r.state.resize(points.size());
+  r.county.resize(points.size());
+  r.block.resize(points.size());
+  fm_assign_counters c{};
+  detail::check(fm_simple_assign_host(engine.get(),
+                                      mode == AssignMode::strict ? FM_ASSIGN_STRICT : FM_ASSIGN_RELAXED,
+                                      reinterpret_cast<const double*>(points.data()), points.size(),
+                                      r.state.data(), r.county.data(), r.block.data(), &c),
+                "fm_simple_assign_host");
+  r.counters.pip_point_evaluations = c.pip_point_evaluations;
+  r.counters.pip_calls = c.pip_calls;
+  return r;
+}
+
+inline AssignmentResult assign(const RegionHierarchy& h, std::span<const Point> points,
+                               AssignMode mode = AssignMode::relaxed, int device = 0) {
+  return assign(SimpleEngine(h, device), points, mode);
 }
 
 }  // namespace fastmap::gpu

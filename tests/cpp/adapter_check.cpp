@@ -150,5 +150,16 @@ int main(int argc, char** argv) {
     std::puts("FAIL: reloaded index answers differently");
     return 1;
   }
+  // the simple engine through the adapter == the reference's assign()
+  for (const AssignMode mode : {AssignMode::relaxed, AssignMode::strict}) {
+    const auto got = gpu::assign(h, pts, mode);
+    const auto ref = assign(h, pts, mode);
+    if (got.state != ref.state || got.county != ref.county || got.block != ref.block ||
+        got.counters.pip_point_evaluations != ref.counters.pip_point_evaluations ||
+        got.counters.pip_calls != ref.counters.pip_calls) {
+      std::printf("FAIL: gpu::assign differs from assign (mode %d)\n", static_cast<int>(mode));
+      return 1;
+    }
+  }
   return check_approx();
 }
