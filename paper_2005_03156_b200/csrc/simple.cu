@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256, FM_SIMPLE_MINB)
                 const double4 a = ld4(R + 2 * r);
                 if (!(a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w)) continue;
                 ++ev;
-                L.tested[r] = 1;
+                if (!L.tested[r]) L.tested[r] = 1;  // most flags are set early: skip the store
               }
             }
           } else {
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256, FM_SIMPLE_MINB)
               if (!(a.x < p.x && p.x < a.y && a.z < p.y && p.y < a.w)) continue;
               if (kCount) {
                 ++ev;
-                L.tested[r] = 1;
+                if (!L.tested[r]) L.tested[r] = 1;  // most flags are set early: skip the store
               }
               if (region_pip(L, ld4(R + 2 * r + 1), p.x, p.y)) {
                 win = static_cast<int>(r);
