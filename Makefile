@@ -17,7 +17,7 @@ PRODUCT_SRC := $(PKG)/csrc/fastmap_b200.cu $(PKG)/csrc/index_gpu.cu $(PKG)/csrc/
                $(PKG)/csrc/io.cpp $(PKG)/csrc/simple.cu
 PRODUCT_HDR := include/fastmap_b200.h $(PKG)/csrc/index_format.h \
                $(PKG)/csrc/index_build.h $(PKG)/csrc/query.cuh $(PKG)/csrc/sweep.h \
-               $(PKG)/csrc/record_encode.h $(PKG)/csrc/hierarchy.h $(PKG)/csrc/quick.h
+               $(PKG)/csrc/record_encode.h $(PKG)/csrc/hierarchy.h
 
 all: product synth oracle ref
 
@@ -30,9 +30,12 @@ $(LIBDIR)/libfastmap_b200.so: $(PRODUCT_SRC) $(PRODUCT_HDR)
 	$(NVCC) $(NVFLAGS) -shared $(PRODUCT_SRC) -o $@ 2> $(LIBDIR)/ptxas.log || (cat $(LIBDIR)/ptxas.log; exit 1)
 	@grep -E "registers|spill" $(LIBDIR)/ptxas.log | sed 's/^/  /' | head -20
 
-$(LIBDIR)/libfastmap_synth.so: $(PKG)/csrc/synth.cpp
+# workload generators: host (synth.cpp) and device (synth_gpu.cu) streams
+# share synth_rng.h; both sides without FMA contraction
+$(LIBDIR)/libfastmap_synth.so: $(PKG)/csrc/synth.cpp $(PKG)/csrc/synth_gpu.cu $(PKG)/csrc/synth_rng.h
 	@mkdir -p $(LIBDIR)
-	$(CXX) -std=c++17 $(HOSTFLAGS) -shared $< -o $@
+	$(NVCC) $(ARCH) -O3 --fmad=false -std=c++17 -Xcompiler -fPIC,-O3,-ffp-contract=off,-pthread \
+	  -shared $(PKG)/csrc/synth.cpp $(PKG)/csrc/synth_gpu.cu -o $@
 
 oracle/liboracle.so: oracle/oracle.c oracle/Makefile
 	$(MAKE) --no-print-directory -f oracle/Makefile $(CURDIR)/oracle/liboracle.so

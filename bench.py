@@ -243,6 +243,7 @@ def run_ours(args):
     idx = fastmap.build_index(soup, params, device=local)
     build_s = time.perf_counter() - t0
     st = idx.stats()
+    plan = idx.query_plan(n)
 
     d_pts = pts_host.to(dev, non_blocking=False)
     d_out = torch.empty(n, dtype=torch.int32, device=dev)
@@ -351,6 +352,7 @@ def run_ours(args):
                                              "query_block_log2", "approx_grid_bytes",
                                              "approx_block_log2")},
                 "index_build_s": build_s,
+                "query_path": None if approx else plan,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -364,7 +366,7 @@ def run_ours(args):
             "e2e": e2e,
             # our kernels per step: stream_kernel + resolve_kernel (exact) or
             # approx_kernel (approx); the 8-byte queue-counter memset is not a kernel of ours
-            "gpu_launches": args.steps * (1 if approx else 2),
+            "gpu_launches": args.steps * (1 if approx else (4 if plan["path"] == "binned" else 2)),
             "clocks": clk.summary(),
             "parity": parity,
         }

@@ -181,6 +181,28 @@ fm_status fm_query_mode(const fm_index* index, int mode, const double* d_lonlat,
 fm_status fm_query_host_mode(const fm_index* index, int mode, const double* h_lonlat,
                              uint64_t n, int32_t* h_out, int64_t* h_hist);
 
+/* Query path of the exact mode.  Both paths answer every point with the
+ * same locate / exact crossing code, so the ids are identical; they differ
+ * only in memory order:
+ *   FM_PATH_STREAM  points in input order: a streaming pass answers true-hit
+ *                   and empty cells, a resolve pass the boundary points;
+ *   FM_PATH_BINNED  points first partitioned by tile of the cell grid (the
+ *                   analogue of query_leaves' pending sort, cell_index.hpp:
+ *                   546-588), queried tile by tile so each tile's grid and
+ *                   slots are fetched from HBM about once, then the ids are
+ *                   gathered back into input order (24 B of scratch/point);
+ *   FM_PATH_AUTO    (default) binned when the index is >= 1 GB with >= 25%
+ *                   boundary cells and the batch has >= 4M points.
+ * tile_bytes: index bytes per tile of the binned path (0 = 24 MB).  Not
+ * synchronised with queries in flight: set it before querying. */
+typedef enum fm_query_path { FM_PATH_AUTO = 0, FM_PATH_STREAM = 1, FM_PATH_BINNED = 2 } fm_query_path;
+fm_status fm_index_set_query_path(fm_index* index, int path, double tile_bytes);
+/* The path fm_query takes for a batch of n points (FM_PATH_STREAM or
+ * FM_PATH_BINNED) and the binned path's tile side (log2 cells) and tile
+ * count; any output may be NULL. */
+fm_status fm_index_query_plan(const fm_index* index, uint64_t n, int* path, int32_t* tile_log2,
+                              int32_t* n_tiles);
+
 /* Copy of the index arrays to host memory (the FMCI-save analogue,
  * cell_index.hpp:641-664).  Two-call protocol: null buffers -> sizes.
  * arena = the 128-byte slot arena followed by the overflow arena;
@@ -191,18 +213,6 @@ fm_status fm_index_export(const fm_index* index, uint32_t* grid, uint64_t* grid_
 
 /* Device the index lives on. */
 int fm_index_device(const fm_index* index);
-
-/* Checker for the quick records (test infrastructure, no GPU needed): on a
- * host-only index (device -1), for each point the answer the query kernel's
- * inline quick path would give -- the grid answer for hit / empty cells, the
- * quick record's certified answer for boundary cells, FM_QUICK_UNSURE (-3)
- * where it hands the point to the exact path, FM_QUICK_NONE (-4) for cells
- * without a quick record (split / overflow / not encodable).  Uses the same
- * quick_encode / quick_eval code as the kernel (csrc/quick.h). */
-#define FM_QUICK_UNSURE (-3)
-#define FM_QUICK_NONE (-4)
-fm_status fm_index_quick_host(const fm_index* index, const double* h_lonlat, uint64_t n,
-                              int32_t* h_out);
 
 /* ---- artifacts and IO ---------------------- */
 

@@ -88,10 +88,12 @@ EXPORTS = (
     "fm_index_save", "fm_index_load", "fm_hierarchy_load", "fm_hierarchy_destroy",
     "fm_hierarchy_sizes", "fm_hierarchy_leaves", "fm_index_build_hierarchy",
     "fm_read_points_f64", "fm_write_assign_csv", "fm_simple_build", "fm_simple_destroy",
-    "fm_simple_assign", "fm_simple_assign_host", "fm_index_quick_host",
+    "fm_simple_assign", "fm_simple_assign_host", "fm_index_set_query_path",
+    "fm_index_query_plan",
 )
 
 MODE_EXACT, MODE_APPROX = 0, 1  # fm_mode (CoverMode, cell_index.hpp:246)
+PATH_AUTO, PATH_STREAM, PATH_BINNED = 0, 1, 2  # fm_query_path
 
 _lib = None
 _synth = None
@@ -165,11 +167,12 @@ def lib() -> C.CDLL:
                                             C.POINTER(AssignCountersC)]
         L.fm_index_export.restype = C.c_int
         L.fm_index_export.argtypes = [C.c_void_p, PU32, PU64, PU8, PU64, PD]
-        if hasattr(L, "fm_index_quick_host"):  # absent from older tuning builds
-            L.fm_index_quick_host.restype = C.c_int
-            L.fm_index_quick_host.argtypes = [C.c_void_p, PD, u64, PI32]
         L.fm_index_device.restype = C.c_int
         L.fm_index_device.argtypes = [C.c_void_p]
+        L.fm_index_set_query_path.restype = C.c_int
+        L.fm_index_set_query_path.argtypes = [C.c_void_p, C.c_int, C.c_double]
+        L.fm_index_query_plan.restype = C.c_int
+        L.fm_index_query_plan.argtypes = [C.c_void_p, u64, C.POINTER(C.c_int), PI32, PI32]
         _lib = L
     return _lib
 
@@ -197,6 +200,15 @@ def synth() -> C.CDLL:
         L.synth_points_near_edge.argtypes = [PD, PU64, PU64, u64, C.c_double, C.c_double,
                                              C.c_double, C.c_double, PD, u64, u64, u64,
                                              C.c_int, PD]
+        L.synth_points_uniform_dev.restype = C.c_int
+        L.synth_points_uniform_dev.argtypes = [PD, u64, u64, u64, C.c_void_p, C.c_void_p]
+        L.synth_points_clustered_dev.restype = C.c_int
+        L.synth_points_clustered_dev.argtypes = [PD, PD, u64, u64, u64, C.c_uint32, C.c_double,
+                                                 C.c_double, C.c_double, C.c_void_p, C.c_void_p]
+        L.synth_points_near_edge_dev.restype = C.c_int
+        L.synth_points_near_edge_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, u64,
+                                                 C.c_double, C.c_double, C.c_double, C.c_double,
+                                                 PD, u64, u64, u64, C.c_void_p, C.c_void_p]
         _synth = L
     return _synth
 

@@ -1,0 +1,331 @@
+// binned.cuh -- the tile-binned query path (north star item 2, "point
+// binning"), included by fastmap_b200.cu inside its anonymous namespace
+// (it reuses QItem, stage_slots, eval_staged and emit from there).
+//
+// The reference sorts its pending (leaf, point) pairs and walks them leaf
+// by leaf (cell_index.hpp:546-588, std::sort at :567) so each polygon's
+// edges are touched once per batch.  Here the analogue is a one-pass
+// partition of the point stream by coarse *tile* of the cell grid (a
+// 2^ts x 2^ts block of cells whose grid entries and slots total a few tens
+// of MB), so that the query pass walks the index tile by tile and every
+// grid sector and boundary slot is fetched from HBM about once per tile
+// instead of once per point.  It pays off when the index is far larger
+// than L2 and most points land in boundary cells (c3, c4); the stream path
+// (stream_kernel + resolve_kernel) stays the choice for small or mostly
+// true-hit indexes (c1, c2) -- see choose_path() in fastmap_b200.cu.
+//
+// Four launches per batch of n <= 2^30 points:
+//   bin_count_kernel    one CTA per 256K-point *chunk*: a shared-memory
+//                       histogram of tile keys, stored as column c of the
+//                       tile-major count table (T+1 rows x n_chunks)
+//   (cub exclusive scan of the table in tile-major order: entry (t, c)
+//    becomes the first position of chunk c's points in tile t)
+//   bin_scatter_kernel  the same chunks, in 16K-point sub-chunks: ranks
+//                       within (sub-chunk, tile) from shared-memory atomics,
+//                       each point written to its tile at the chunk's cursor
+//                       (pts_b), its binned position to pos[i] (coalesced)
+//   binned_query_kernel the query over pts_b in order: locate, true hits
+//                       answered at once, boundary points through a
+//                       warp-private shared-memory ring whose batches of 32
+//                       slots are staged by cp.async one batch ahead of
+//                       their evaluation (exactly resolve_kernel's code);
+//                       answers to res[k]
+//   unbin_kernel        out[i] = res[pos[i]]
+// Within a tile, points keep their input order up to the sub-chunk (the
+// reservations are a scan, not atomics), so any window of consecutive input
+// points maps to one contiguous range per tile: the gather in unbin_kernel
+// and the scattered writes in bin_scatter_kernel stay sector-coherent in L2.
+// Points outside the acceptance box (and NaN) go to one extra bin; the
+// query pass answers them -1 like every other path.
+//
+// Only performance depends on the binning: every point is answered by the
+// same locate_n / eval_leaf_slot code as the stream path, so the answers
+// are identical whatever tile or order a point ends up in.
+
+#ifndef FM_QMINB
+#define FM_QMINB 2
+#endif
+
+constexpr int kBinThreads = 512;
+constexpr int kBinPerThread = 32;
+constexpr int kBinSub = kBinThreads * kBinPerThread;   // 16384-point sub-chunks
+constexpr int kBinSubs = 16;
+constexpr std::uint64_t kBinChunk = std::uint64_t{kBinSub} * kBinSubs;  // 256K points
+constexpr int kRankBits = 14;                           // rank < kBinSub
+static_assert(kBinSub <= (1 << kRankBits), "rank field too narrow");
+constexpr int kMaxTiles = 4096;                         // keys < kMaxTiles + 1
+
+struct TileGeom {
+  int ts = 0;        // log2 tile side in cells
+  int tnx = 1, tny = 1;
+  int n_tiles = 1;   // tnx * tny; key n_tiles = outside the acceptance box
+};
+
+__device__ __forceinline__ int tile_key(const fm::KParams& P, const TileGeom& T, double px,
+                                        double py) {
+  const bool in = px >= P.ax0 && px <= P.ax1 && py >= P.ay0 && py <= P.ay1;
+  int ix = in ? static_cast<int>(__dmul_rn(__dsub_rn(px, P.gx0), P.inv_w)) : 0;
+  int iy = in ? static_cast<int>(__dmul_rn(__dsub_rn(py, P.gy0), P.inv_h)) : 0;
+  ix = min(max(ix, 0), P.nx - 1);
+  iy = min(max(iy, 0), P.ny - 1);
+  return in ? (iy >> T.ts) * T.tnx + (ix >> T.ts) : T.n_tiles;
+}
+
+// table[t * n_chunks + c] = points of chunk c in tile t
+__global__ void __launch_bounds__(kBinThreads)
+    bin_count_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
+                     unsigned int* __restrict__ table) {
+  extern __shared__ unsigned int s_hist[];
+  const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
+  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) s_hist[k] = 0u;
+    __syncthreads();
+    const std::uint64_t base = c * kBinChunk;
+    const std::uint64_t end = min(n, base + kBinChunk);
+    for (std::uint64_t b = base + threadIdx.x; b < end; b += 4ull * kBinThreads) {
+      double2 p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kBinThreads;
+        p[u] = i < end ? __ldcs(pts + i) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kBinThreads;
+        if (i < end) atomicAdd(s_hist + tile_key(P, T, p[u].x, p[u].y), 1u);
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) {
+      table[static_cast<std::uint64_t>(k) * n_chunks + c] = s_hist[k];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kBinThreads, 2)
+    bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
+                       const unsigned int* __restrict__ table, double2* __restrict__ pts_b,
+                       unsigned int* __restrict__ pos) {
+  extern __shared__ unsigned int smem[];
+  const int nk = T.n_tiles + 1;
+  unsigned int* s_cur = smem;                      // nk: the chunk's cursor per tile
+  unsigned int* s_hist = smem + ((nk + 3) & ~3);   // nk: per sub-chunk counts
+  unsigned int* s_kr = s_hist + ((nk + 3) & ~3);   // kBinSub: key << 14 | rank
+  const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
+  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+      s_cur[k] = table[static_cast<std::uint64_t>(k) * n_chunks + c];
+      s_hist[k] = 0u;
+    }
+    __syncthreads();
+    for (int sub = 0; sub < kBinSubs; ++sub) {
+      const std::uint64_t base = c * kBinChunk + static_cast<std::uint64_t>(sub) * kBinSub;
+      if (base >= n) break;
+      // ranks within (sub-chunk, tile); the sub-chunk's points stay in L2
+      // for the second read below
+#pragma unroll 4
+      for (int j = 0; j < kBinPerThread; ++j) {
+        const int li = j * kBinThreads + threadIdx.x;
+        const std::uint64_t i = base + li;
+        if (i < n) {
+          const double2 p = __ldg(pts + i);
+          const int key = tile_key(P, T, p.x, p.y);
+          const unsigned int r = atomicAdd(s_hist + key, 1u);
+          s_kr[li] = (static_cast<unsigned int>(key) << kRankBits) | r;
+        }
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int j = 0; j < kBinPerThread; ++j) {
+        const int li = j * kBinThreads + threadIdx.x;
+        const std::uint64_t i = base + li;
+        if (i < n) {
+          const unsigned int kr = s_kr[li];
+          const unsigned int dst = s_cur[kr >> kRankBits] + (kr & ((1u << kRankBits) - 1u));
+          pts_b[dst] = __ldcs(pts + i);
+          __stcs(pos + i, dst);
+        }
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+        s_cur[k] += s_hist[k];
+        s_hist[k] = 0u;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// The query over the binned stream.  Warps take consecutive 32*kU-point
+// tiles with a grid stride, so at any moment the whole grid works on one
+// window of the binned array -- one or two index tiles.  Boundary points
+// wait in a warp-private ring (kQCap items).  Full batches of 32 are staged
+// into one of two slot pools by cp.async and evaluated one round later, so
+// the slot fetches of batch k+1 overlap the evaluation of batch k and the
+// next point tile's loads and grid gathers; split cells put their child
+// entry back into the ring.
+constexpr int kQWarps = 8;
+constexpr int kQCap = 128;
+struct WarpSmemQ {
+  alignas(16) std::uint8_t pool[2][32 * fm::kSlotBytes];
+  double qx[kQCap], qy[kQCap];
+  std::uint32_t qk[kQCap], qe[kQCap];
+};
+constexpr int kSmemQ = static_cast<int>(sizeof(WarpSmemQ)) * kQWarps;
+
+struct RingState {
+  int head = 0, qn = 0;  // ring items not yet staged
+  int pend = 0;          // items of the staged batch in pool[pb]
+  int pb = 0;
+  QItem pit;             // this lane's staged item
+};
+
+// Stage the next batch (when 32 items wait, or any when draining) and
+// evaluate the previously staged one; repeat while full batches remain.
+template <bool kHist, bool kCount>
+__device__ __forceinline__ void pump(const fm::KParams& P, WarpSmemQ& S, RingState& R, bool drain,
+                                     int lane, int* __restrict__ res, HistT* __restrict__ hist,
+                                     fm::WorkCount& wc) {
+  for (;;) {
+    const bool stage = R.qn >= 32 || (drain && R.qn > 0);
+    if (!stage && !(drain && R.pend > 0)) break;
+    int m = 0;
+    QItem nit;
+    nit.px = nit.py = 0.0;
+    nit.i = 0;
+    nit.e = fm::kEmpty;
+    if (stage) {
+      m = min(R.qn, 32);
+      if (lane < m) {
+        const int s = (R.head + lane) & (kQCap - 1);
+        nit.px = S.qx[s];
+        nit.py = S.qy[s];
+        nit.i = S.qk[s];
+        nit.e = S.qe[s];
+      }
+      R.head = (R.head + m) & (kQCap - 1);
+      R.qn -= m;
+      __syncwarp();
+      stage_slots(P, S.pool[R.pb ^ 1], nit.e, m, lane);  // commits one group
+    }
+    if (R.pend > 0) {
+      if (stage) {
+        cp_async_wait1();
+      } else {
+        cp_async_wait0();
+      }
+      __syncwarp();
+      const std::uint32_t ce = eval_staged<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res,
+                                                          hist, wc);
+      const std::uint32_t rq = __ballot_sync(0xFFFFFFFFu, ce != 0u);
+      if (ce != 0u) {  // split cell: the child entry goes back into the ring
+        const int s = (R.head + R.qn + __popc(rq & ((1u << lane) - 1u))) & (kQCap - 1);
+        S.qx[s] = R.pit.px;
+        S.qy[s] = R.pit.py;
+        S.qk[s] = R.pit.i;
+        S.qe[s] = ce;
+      }
+      R.qn += __popc(rq);
+      __syncwarp();
+    }
+    if (stage) R.pb ^= 1;
+    R.pit = nit;
+    R.pend = m;
+    if (!drain && R.qn < 32) break;
+  }
+}
+
+template <bool kHist, bool kCount, int kLs>
+__global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
+    binned_query_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
+                        int* __restrict__ res, HistT* __restrict__ hist,
+                        unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char dsmem[];
+  WarpSmemQ& S = reinterpret_cast<WarpSmemQ*>(dsmem)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const std::uint64_t tile = 32ull * kU;
+  const std::uint64_t n_tiles = (n + tile - 1) / tile;
+  const std::uint64_t gwarp = static_cast<std::uint64_t>(blockIdx.x) * kQWarps + (threadIdx.x >> 5);
+  const std::uint64_t nwarps = static_cast<std::uint64_t>(gridDim.x) * kQWarps;
+  const std::uint32_t lt_mask = (1u << lane) - 1u;
+  fm::WorkCount wc;
+  RingState R;
+  R.pit.px = R.pit.py = 0.0;
+  R.pit.i = 0;
+  R.pit.e = fm::kEmpty;
+  double2 pn[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const std::uint64_t i = gwarp * tile + u * 32 + lane;
+    pn[u] = (gwarp < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
+  }
+  for (std::uint64_t t = gwarp; t < n_tiles; t += nwarps) {
+    const std::uint64_t base = t * tile;
+    double2 p[kU];
+    std::uint32_t e[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) p[u] = pn[u];
+    fm::locate_n<kU, true, kLs>(P, p, e);
+    const std::uint64_t tn = t + nwarps;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const std::uint64_t i = tn * tile + u * 32 + lane;
+      pn[u] = (tn < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const std::uint64_t i = base + u * 32 + lane;
+      const bool valid = i < n;
+      const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
+      if (valid && !is_rec) emit<kHist>(res, hist, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
+      const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec);
+      if (is_rec) {
+        const int s = (R.head + R.qn + __popc(b & lt_mask)) & (kQCap - 1);
+        S.qx[s] = p[u].x;
+        S.qy[s] = p[u].y;
+        S.qk[s] = static_cast<std::uint32_t>(i);
+        S.qe[s] = e[u];
+      }
+      R.qn += __popc(b);
+    }
+    __syncwarp();
+    pump<kHist, kCount>(P, S, R, false, lane, res, hist, wc);
+  }
+  pump<kHist, kCount>(P, S, R, true, lane, res, hist, wc);
+  if (kCount) {
+    unsigned long long v[4] = {0ull, wc.boundary, wc.cands, wc.edges};
+    for (std::uint64_t t = gwarp; t < n_tiles; t += nwarps) v[0] += min(tile, n - t * tile);
+    if (lane != 0) v[0] = 0;
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xFFFFFFFFu, v[k], o);
+    }
+    if (lane == 0) {
+      for (int k = 0; k < 4; ++k) atomicAdd(counters + k, v[k]);
+    }
+  }
+}
+
+// out[i] = res[pos[i]], four points per thread (16-byte pos loads and id
+// stores when `out` is 16-byte aligned; otherwise one by one).
+__global__ void __launch_bounds__(256)
+    unbin_kernel(const unsigned int* __restrict__ pos, const int* __restrict__ res, std::uint64_t n,
+                 int* __restrict__ out) {
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool vec = (reinterpret_cast<std::uintptr_t>(out) & 15u) == 0;
+  const std::uint64_t n4 = vec ? n / 4 : 0;
+  const uint4* p4 = reinterpret_cast<const uint4*>(pos);
+  int4* o4 = reinterpret_cast<int4*>(out);
+  for (std::uint64_t q = t0; q < n4; q += stride) {
+    const uint4 k = __ldcs(p4 + q);
+    int4 v;
+    v.x = __ldg(res + k.x);
+    v.y = __ldg(res + k.y);
+    v.z = __ldg(res + k.z);
+    v.w = __ldg(res + k.w);
+    __stcs(o4 + q, v);
+  }
+  for (std::uint64_t i = n4 * 4 + t0; i < n; i += stride) __stcs(out + i, __ldg(res + __ldcs(pos + i)));
+}

@@ -365,67 +365,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FM_BMINB)
 
 constexpr int kSmemB = static_cast<int>(sizeof(WarpSmemB)) * kBWarps;
 
-// resolve_quick_kernel: the resolve pass through the quick records
-// (quick.h).  Each lane takes kRQ queue items per round, gathers their
-// 32-byte quick records (all in flight together) and evaluates them in
-// registers; the rare item a quick record cannot certify -- a near-tie, a
-// cell without an encodable record (split / overflow / over capacity) --
-// is resolved exactly from its slot in global memory.  Small register and
-// no shared-memory footprint, so many warps hide the record gathers.
-constexpr int kRQ = 2;
-#ifndef FM_QMINB
-#define FM_QMINB 4
-#endif
-template <bool kHist>
-__global__ void __launch_bounds__(256, FM_QMINB)
-    resolve_quick_kernel(fm::KParams P, const QItem* __restrict__ q,
-                         const std::uint32_t* __restrict__ qcount, std::uint64_t n_regions,
-                         std::uint64_t region_cap, unsigned long long* __restrict__ next_region,
-                         int* __restrict__ out, HistT* __restrict__ hist) {
-  const int lane = threadIdx.x & 31;
-  fm::WorkCount wc;
-  for (;;) {
-    unsigned long long region = 0;
-    if (lane == 0) region = atomicAdd(next_region, 1ull);
-    region = __shfl_sync(0xFFFFFFFFu, region, 0);
-    if (region >= n_regions) break;
-    const QItem* items = q + region * region_cap;
-    const std::uint32_t cnt = qcount[region];
-    for (std::uint32_t b = 0; b < cnt; b += 32 * kRQ) {
-      QItem it[kRQ];
-      uint4 qa[kRQ], qb[kRQ];
-#pragma unroll
-      for (int r = 0; r < kRQ; ++r) it[r] = load_item(items, b + r * 32 + lane, cnt);
-#pragma unroll
-      for (int r = 0; r < kRQ; ++r) {
-        const std::uint32_t k = it[r].e & fm::kSlotIndexMask;
-        qa[r] = make_uint4(0u, 0u, 0u, 0u);
-        qb[r] = qa[r];
-        if (it[r].e != fm::kEmpty && k < P.n_quick) {
-          qa[r] = __ldg(P.quick + 2 * static_cast<std::size_t>(k));
-          qb[r] = __ldg(P.quick + 2 * static_cast<std::size_t>(k) + 1);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < kRQ; ++r) {
-        if (it[r].e == fm::kEmpty) continue;  // past the region's count
-        // the point's position in its cell in quanta (quick.h frame)
-        const double fx = __dmul_rn(__dsub_rn(it[r].px, P.gx0), P.inv_w);
-        const double fy = __dmul_rn(__dsub_rn(it[r].py, P.gy0), P.inv_h);
-        const int ix = min(max(static_cast<int>(fx), 0), P.nx - 1);
-        const int iy = min(max(static_cast<int>(fy), 0), P.ny - 1);
-        const float pu = static_cast<float>(__dmul_rn(__dsub_rn(fx, static_cast<double>(ix)), fm::kQuickScale));
-        const float pv = static_cast<float>(__dmul_rn(__dsub_rn(fy, static_cast<double>(iy)), fm::kQuickScale));
-        const std::uint32_t w[8] = {qa[r].x, qa[r].y, qa[r].z, qa[r].w,
-                                    qb[r].x, qb[r].y, qb[r].z, qb[r].w};
-        int id = fm::quick_eval(w, pu, pv);  // no record (w = 0): unsure
-        if (id == fm::kQuickUnsure) id = fm::resolve_slot_global<false>(P, it[r].e, it[r].px, it[r].py, wc);
-        emit<kHist>(out, hist, it[r].i, id);
-      }
-    }
-  }
-}
-
+#include "binned.cuh"
 
 // ---------------------------------------------------------------------------
 // Fast-approx mode (CoverMode::approx, cell_index.hpp:558-560).  The approx
@@ -723,25 +663,6 @@ __global__ void __launch_bounds__(256)
   grid[c] = (e & ~fm::kSlotIndexMask) | static_cast<std::uint32_t>(kn);
 }
 
-// Quick records (quick.h): one thread per cell; the cell of phase-1 slot k
-// writes record k.
-__global__ void __launch_bounds__(256)
-    quick_build_kernel(const std::uint32_t* __restrict__ grid, std::uint64_t ncell, int nx,
-                       const std::uint8_t* __restrict__ slots, std::uint64_t n1, double gx0,
-                       double gy0, double inv_w, double inv_h, uint4* __restrict__ quick) {
-  const std::uint64_t c = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= ncell) return;
-  const std::uint32_t e = grid[c];
-  if (e == fm::kEmpty || e < fm::kRecordBit) return;
-  const std::uint64_t k = e & fm::kSlotIndexMask;
-  if (k >= n1) return;
-  std::uint32_t w[8];
-  fm::quick_encode(slots + k * fm::kSlotBytes, static_cast<std::int64_t>(c % nx),
-                   static_cast<std::int64_t>(c / nx), gx0, gy0, inv_w, inv_h, w);
-  quick[2 * k] = make_uint4(w[0], w[1], w[2], w[3]);
-  quick[2 * k + 1] = make_uint4(w[4], w[5], w[6], w[7]);
-}
-
 // Boundary cells of the exact grid -> (centre point, cell) lists.
 __global__ void __launch_bounds__(256)
     deem_collect_kernel(const std::uint32_t* __restrict__ grid, std::uint64_t ncell,
@@ -840,10 +761,11 @@ struct fm_index {
   std::uint32_t* d_grid = nullptr;
   Folded qgrid;                        // query-side folded copy of the exact grid
   Folded agrid;                        // fast-approx cover (folded), or empty
+  TileGeom tiles;                      // binned query path: the index tiles
+  int query_path = FM_PATH_AUTO;       // fm_query_path
+  double tile_bytes = 0.0;             // index bytes per tile (0 = default)
   std::uint8_t* d_slots = nullptr;     // boundary slots (128 B each)
   std::uint8_t* d_overflow = nullptr;  // overflow records
-  uint4* d_quick = nullptr;            // quick records (quick.h), one per phase-1 slot
-  std::uint64_t n_quick = 0;
   std::uint64_t grid_len = 0, slots_len = 0, overflow_len = 0;
   fm::HostIndex host;  // retained only for host-only (device < 0) indexes
   fm_index_stats stats{};
@@ -879,8 +801,6 @@ fm::KParams kparams(const fm_index* ix) {
   P.compact = ix->qgrid.compact;
   P.bnx = ix->qgrid.bnx;
   P.ls = ix->qgrid.ls;
-  P.quick = ix->d_quick;
-  P.n_quick = static_cast<std::uint32_t>(ix->n_quick);
   return P;
 }
 
@@ -915,25 +835,110 @@ fm_status launch_t(const fm_index* ix, const double2* pts, std::uint64_t n, int*
   }
   FM_CUDA(cudaMemsetAsync(next_region, 0, 8, stream));
   ka<<<grid_a, blk_a, 0, stream>>>(P, pts, n, d_out, d_hist, q, qcount, region_cap, d_counters);
-  // persistent resolve grid: resident CTAs pull regions from a counter.
-  // Counting runs take the slot path, so the counters measure exact work.
-  if (!kCount && ix->n_quick > 0) {
-    auto kq = resolve_quick_kernel<kHist>;
-    const int grid_q = static_cast<int>(std::min<std::uint64_t>(
-        (n_regions + 7) / 8, resident_blocks(ix->device, (const void*)kq, 256, 0)));
-    kq<<<grid_q, 256, 0, stream>>>(P, q, qcount, n_regions, region_cap, next_region, d_out, d_hist);
-  } else {
-    const int grid_b = static_cast<int>(std::min<std::uint64_t>(
-        (n_regions + kBWarps - 1) / kBWarps,
-        resident_blocks(ix->device, (const void*)kb, kBWarps * 32, kSmemB)));
-    kb<<<grid_b, kBWarps * 32, kSmemB, stream>>>(P, q, qcount, n_regions, region_cap, next_region,
-                                                 d_out, d_hist, d_counters);
-  }
+  // persistent resolve grid: resident CTAs pull regions from a counter
+  const int grid_b = static_cast<int>(std::min<std::uint64_t>(
+      (n_regions + kBWarps - 1) / kBWarps,
+      resident_blocks(ix->device, (const void*)kb, kBWarps * 32, kSmemB)));
+  kb<<<grid_b, kBWarps * 32, kSmemB, stream>>>(P, q, qcount, n_regions, region_cap, next_region,
+                                               d_out, d_hist, d_counters);
   const cudaError_t err = cudaGetLastError();
   FM_CUDA(cudaFreeAsync(scratch, stream));
   if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));
   return FM_OK;
 }
+
+// The binned path (binned.cuh) over one batch of n <= kBinnedBatch points.
+constexpr std::uint64_t kBinnedBatch = std::uint64_t{1} << 30;
+constexpr int kBinCountSmem = (kMaxTiles + 1) * 4;
+constexpr int kBinScatterSmem = 2 * ((kMaxTiles + 1 + 3) & ~3) * 4 + kBinSub * 4;
+
+std::uint64_t align256(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
+
+template <bool kHist, bool kCount>
+fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t n, int* d_out,
+                          HistT* d_hist, unsigned long long* d_counters, cudaStream_t stream) {
+  const fm::KParams P = kparams(ix);
+  const TileGeom& T = ix->tiles;
+  const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
+  const std::uint64_t n_tab = static_cast<std::uint64_t>(T.n_tiles + 1) * n_chunks;
+  std::size_t cub_bytes = 0;
+  FM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, static_cast<unsigned int*>(nullptr),
+                                        static_cast<unsigned int*>(nullptr),
+                                        static_cast<std::int64_t>(n_tab), stream));
+  // scratch: the (tile x chunk) count table and its scan, scan temp, binned
+  // points, binned positions, binned answers (24 B per point)
+  const std::uint64_t o_scan = align256(4 * n_tab);
+  const std::uint64_t o_tmp = o_scan + align256(4 * n_tab);
+  const std::uint64_t o_pts = o_tmp + align256(cub_bytes + 16);
+  const std::uint64_t o_pos = o_pts + align256(16 * n);
+  const std::uint64_t o_res = o_pos + align256(4 * n);
+  const std::uint64_t total = o_res + align256(4 * n);
+  char* scratch = nullptr;
+  FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), total, stream));
+  unsigned int* table = reinterpret_cast<unsigned int*>(scratch);
+  unsigned int* starts = reinterpret_cast<unsigned int*>(scratch + o_scan);
+  double2* pts_b = reinterpret_cast<double2*>(scratch + o_pts);
+  unsigned int* pos = reinterpret_cast<unsigned int*>(scratch + o_pos);
+  int* res = reinterpret_cast<int*>(scratch + o_res);
+  auto kc = bin_count_kernel;
+  const int grid_c = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+      n_chunks, resident_blocks(ix->device, (const void*)kc, kBinThreads, kBinCountSmem))));
+  kc<<<grid_c, kBinThreads, kBinCountSmem, stream>>>(P, T, pts, n, table);
+  FM_CUDA(cub::DeviceScan::ExclusiveSum(scratch + o_tmp, cub_bytes, table, starts,
+                                        static_cast<std::int64_t>(n_tab), stream));
+  auto ks = bin_scatter_kernel;
+  const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+      n_chunks, resident_blocks(ix->device, (const void*)ks, kBinThreads, kBinScatterSmem))));
+  ks<<<grid_s, kBinThreads, kBinScatterSmem, stream>>>(P, T, pts, n, starts, pts_b, pos);
+  auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<kHist, kCount, 0>
+                              : binned_query_kernel<kHist, kCount, -1>;
+  const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);
+  const int grid_q = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+      (n_tiles + kQWarps - 1) / kQWarps,
+      resident_blocks(ix->device, (const void*)kq, kQWarps * 32, kSmemQ))));
+  kq<<<grid_q, kQWarps * 32, kSmemQ, stream>>>(P, pts_b, n, res, d_hist, d_counters);
+  auto ku = unbin_kernel;
+  const int grid_u = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+      (n / 4 + 255) / 256, resident_blocks(ix->device, (const void*)ku, 256, 0))));
+  ku<<<grid_u, 256, 0, stream>>>(pos, res, n, d_out);
+  const cudaError_t err = cudaGetLastError();
+  FM_CUDA(cudaFreeAsync(scratch, stream));
+  if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));
+  return FM_OK;
+}
+
+// Query path for a batch of n points (fm_query_path): the binned path when
+// the index is far larger than L2 and mostly boundary slots -- then the
+// stream path's per-point gathers miss L2 (c3: 47 GB of slots, 60% boundary
+// cells; c4: 5.5 GB, 50%) -- and the batch is big enough to reuse tiles;
+// the stream path otherwise (c1; c2: 9% boundary cells).
+bool use_binned(const fm_index* ix, std::uint64_t n) {
+  if (ix->query_path == FM_PATH_STREAM) return false;
+  if (ix->query_path == FM_PATH_BINNED) return true;
+  const double cells = static_cast<double>(ix->g.nx) * static_cast<double>(ix->g.ny);
+  const double bfrac = cells > 0 ? static_cast<double>(ix->stats.cells_boundary) / cells : 0.0;
+  const double bytes = static_cast<double>(ix->stats.query_grid_bytes + ix->stats.arena_bytes);
+  return n >= (std::uint64_t{1} << 22) && bytes >= 1e9 && bfrac >= 0.25;
+}
+
+// Tiles of 2^ts x 2^ts cells holding about `tile_bytes` of index (grid
+// entries + slot arena, averaged over the grid), at most kMaxTiles.
+TileGeom plan_tiles(const fm_index* ix, double tile_bytes) {
+  const double cells = std::max(1.0, static_cast<double>(ix->g.nx) * static_cast<double>(ix->g.ny));
+  const double per_cell = static_cast<double>(ix->stats.query_grid_bytes + ix->stats.arena_bytes) / cells;
+  const double side = std::sqrt(tile_bytes / std::max(per_cell, 1.0));
+  int ts = std::max(2, static_cast<int>(std::lround(std::log2(std::max(side, 1.0)))));
+  TileGeom T;
+  for (;; ++ts) {
+    T.ts = ts;
+    T.tnx = static_cast<int>((ix->g.nx + (1ll << ts) - 1) >> ts);
+    T.tny = static_cast<int>((ix->g.ny + (1ll << ts) - 1) >> ts);
+    T.n_tiles = T.tnx * T.tny;
+    if (T.n_tiles <= kMaxTiles) break;
+  }
+  return T;
+}
+constexpr double kTileBytes = 32e6;
 
 template <bool kHist, bool kCount>
 fm_status launch_approx_t(const fm_index* ix, const double2* pts, std::uint64_t n, int* d_out,
@@ -978,8 +983,9 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
     if (d_counters) return launch_approx_t<false, true>(ix, pts, n, d_out, d_hist, d_counters, stream);
     return launch_approx_t<false, false>(ix, pts, n, d_out, d_hist, d_counters, stream);
   }
-  // slices of 2^28 points bound the queue scratch (24 B/point) to 6.4 GB
-  // and keep the u32 histogram counters from overflowing
+  // slices of 2^28 points bound the stream path's queue scratch (24 B/point)
+  // to 6.4 GB; binned batches of 2^30 points take 24 GB (binned.cuh).  Both
+  // keep the u32 histogram counters from overflowing.
   const std::uint64_t slice = std::uint64_t{1} << 28;
   const std::uint64_t nh = ix->stats.n_polys;
   HistT* h32 = nullptr;
@@ -988,9 +994,21 @@ fm_status launch(const fm_index* ix, const double* d_pts, std::uint64_t n, int* 
     FM_CUDA(cudaMemsetAsync(h32, 0, nh * sizeof(HistT), stream));
   }
   fm_status st = FM_OK;
-  for (std::uint64_t off = 0; off < n && st == FM_OK; off += slice) {
-    const std::uint64_t m = std::min(slice, n - off);
-    if (h32 && d_counters) {
+  const bool binned = use_binned(ix, n);
+  const std::uint64_t step = binned ? kBinnedBatch : slice;
+  for (std::uint64_t off = 0; off < n && st == FM_OK; off += step) {
+    const std::uint64_t m = std::min(step, n - off);
+    if (binned) {
+      if (h32 && d_counters) {
+        st = launch_binned_t<true, true>(ix, pts + off, m, d_out + off, h32, d_counters, stream);
+      } else if (h32) {
+        st = launch_binned_t<true, false>(ix, pts + off, m, d_out + off, h32, d_counters, stream);
+      } else if (d_counters) {
+        st = launch_binned_t<false, true>(ix, pts + off, m, d_out + off, nullptr, d_counters, stream);
+      } else {
+        st = launch_binned_t<false, false>(ix, pts + off, m, d_out + off, nullptr, d_counters, stream);
+      }
+    } else if (h32 && d_counters) {
       st = launch_t<true, true>(ix, pts + off, m, d_out + off, h32, d_counters, stream);
     } else if (h32) {
       st = launch_t<true, false>(ix, pts + off, m, d_out + off, h32, d_counters, stream);
@@ -1222,26 +1240,6 @@ fm_status build_approx(fm_index* ix) {
   return FM_OK;
 }
 
-// Quick records for the phase-1 slots (after renumbering: record k mirrors
-// slot k), built when FASTMAP_B200_QUICK=1.  Off by default: on B200 the
-// resolve pass is bound by the rate of random DRAM accesses, one per
-// boundary point either way, so the 32-byte record measured no faster than
-// the 64-byte half slot ("quick records").
-fm_status build_quick(fm_index* ix) {
-  const std::uint64_t n1 = ix->host.n_phase1_slots;
-  const char* on = std::getenv("FASTMAP_B200_QUICK");
-  if (n1 == 0 || n1 >= fm::kMaxSlots || !(on && on[0] == '1')) return FM_OK;
-  FM_CUDA(cudaMalloc(&ix->d_quick, n1 * fm::kQuickBytes));
-  const std::uint64_t ncell = ix->grid_len;
-  quick_build_kernel<<<static_cast<unsigned>((ncell + 255) / 256), 256>>>(
-      ix->d_grid, ncell, static_cast<int>(ix->g.nx), ix->d_slots, n1, ix->g.gx0, ix->g.gy0,
-      ix->g.inv_w, ix->g.inv_h, ix->d_quick);
-  FM_CUDA(cudaGetLastError());
-  FM_CUDA(cudaDeviceSynchronize());
-  ix->n_quick = n1;
-  return FM_OK;
-}
-
 // Query-side layout of a device index (shared by fm_index_build and
 // fm_index_load): mempool policy, block-major slot numbering + the folded
 // grid, and the approx cover when epsilon > 0.
@@ -1261,10 +1259,10 @@ fm_status finish_device(fm_index* ix, double approx_epsilon) {
     st = fold_grid(ix->d_grid, nx, ny, kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots,
                    kQueryMaxRatio, &ix->qgrid);
   }
-  if (st == FM_OK) st = build_quick(ix);
   if (st != FM_OK) return st;
   ix->stats.query_grid_bytes = ix->qgrid.bytes;
   ix->stats.query_block_log2 = ix->qgrid.ls;
+  ix->tiles = plan_tiles(ix, ix->tile_bytes > 0 ? ix->tile_bytes : kTileBytes);
   ix->stats.approx_epsilon = approx_epsilon;
   // an epsilon too fine for the uniform approx grid: approximate queries
   // take the exact path (fm_index_stats.approx_grid_bytes stays 0)
@@ -1300,7 +1298,6 @@ void free_device(fm_index* ix) {
   ix->agrid.release();
   if (ix->d_slots) cudaFree(ix->d_slots);
   if (ix->d_overflow) cudaFree(ix->d_overflow);
-  if (ix->d_quick) cudaFree(ix->d_quick);
 }
 
 }  // namespace
@@ -1761,45 +1758,28 @@ fm_status fm_index_load(const char* path, int device, fm_index** out_index) {
   return FM_OK;
 }
 
-fm_status fm_index_quick_host(const fm_index* index, const double* h_lonlat, std::uint64_t n,
-                              std::int32_t* h_out) {
-  if (!index || (n > 0 && (!h_lonlat || !h_out))) return set_err(FM_ERR_INVALID_ARGUMENT, "null argument");
-  if (index->device >= 0) return set_err(FM_ERR_INVALID_ARGUMENT, "fm_index_quick_host needs a host-only index");
-  const fm::GridGeom& g = index->g;
-  const fm::HostIndex& H = index->host;
-  for (std::uint64_t i = 0; i < n; ++i) {
-    const double px = h_lonlat[2 * i], py = h_lonlat[2 * i + 1];
-    const bool in = px >= index->ax0 && px <= index->ax1 && py >= index->ay0 && py <= index->ay1;
-    if (!in) {
-      h_out[i] = -1;
-      continue;
-    }
-    // the kernel's locate_n (query.cuh), on the flat grid
-    const double fx = (px - g.gx0) * g.inv_w, fy = (py - g.gy0) * g.inv_h;
-    std::int64_t ix = static_cast<std::int64_t>(static_cast<int>(fx));
-    std::int64_t iy = static_cast<std::int64_t>(static_cast<int>(fy));
-    ix = std::min<std::int64_t>(std::max<std::int64_t>(ix, 0), g.nx - 1);
-    iy = std::min<std::int64_t>(std::max<std::int64_t>(iy, 0), g.ny - 1);
-    const std::uint32_t e = H.grid[static_cast<std::size_t>(iy * g.nx + ix)];
-    if (e == fm::kEmpty || e < fm::kRecordBit) {
-      h_out[i] = e == fm::kEmpty ? -1 : static_cast<std::int32_t>(e);
-      continue;
-    }
-    const std::uint64_t k = e & fm::kSlotIndexMask;
-    std::uint32_t w[8];
-    if (k >= H.n_phase1_slots) {
-      h_out[i] = FM_QUICK_NONE;
-      continue;
-    }
-    fm::quick_encode(H.slots.data() + k * fm::kSlotBytes, ix, iy, g.gx0, g.gy0, g.inv_w, g.inv_h, w);
-    if (!(w[0] >> 31)) {
-      h_out[i] = FM_QUICK_NONE;
-      continue;
-    }
-    const float pu = static_cast<float>((fx - static_cast<double>(ix)) * fm::kQuickScale);
-    const float pv = static_cast<float>((fy - static_cast<double>(iy)) * fm::kQuickScale);
-    h_out[i] = fm::quick_eval(w, pu, pv);
+fm_status fm_index_set_query_path(fm_index* index, int path, double tile_bytes) {
+  g_err.clear();
+  if (!index) return set_err(FM_ERR_INVALID_ARGUMENT, "index is null");
+  if (path != FM_PATH_AUTO && path != FM_PATH_STREAM && path != FM_PATH_BINNED) {
+    return set_err(FM_ERR_INVALID_ARGUMENT, "unknown query path");
   }
+  if (!(tile_bytes >= 0.0) || std::isinf(tile_bytes)) {
+    return set_err(FM_ERR_INVALID_ARGUMENT, "tile_bytes must be finite and >= 0");
+  }
+  index->query_path = path;
+  index->tile_bytes = tile_bytes;
+  if (index->device >= 0) index->tiles = plan_tiles(index, tile_bytes > 0 ? tile_bytes : kTileBytes);
+  return FM_OK;
+}
+
+fm_status fm_index_query_plan(const fm_index* index, std::uint64_t n, int* path, std::int32_t* tile_log2,
+                              std::int32_t* n_tiles) {
+  g_err.clear();
+  if (!index) return set_err(FM_ERR_INVALID_ARGUMENT, "index is null");
+  if (path) *path = use_binned(index, n) ? FM_PATH_BINNED : FM_PATH_STREAM;
+  if (tile_log2) *tile_log2 = index->tiles.ts;
+  if (n_tiles) *n_tiles = index->tiles.n_tiles;
   return FM_OK;
 }
 

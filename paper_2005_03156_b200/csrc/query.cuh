@@ -12,7 +12,6 @@
 #include <cstdint>
 
 #include "index_format.h"
-#include "quick.h"
 
 namespace fm {
 
@@ -32,9 +31,6 @@ struct KParams {
   int nx, ny;
   int bnx, ls;                // blocks per row, log2 block side
   int compact;                // `pal` format: 0 approx palettes, 1 exact compact sub-blocks
-  // quick records (quick.h): record k mirrors phase-1 slot k, k < n_quick
-  const uint4* __restrict__ quick;
-  std::uint32_t n_quick;
 };
 
 __device__ __forceinline__ const std::uint8_t* slot_ptr(const KParams& P, std::uint32_t e) {

@@ -19,6 +19,8 @@
 #include <thread>
 #include <vector>
 
+#include "synth_rng.h"
+
 namespace {
 
 inline std::uint64_t mix64(std::uint64_t z) {
@@ -519,15 +521,26 @@ int synth_nested_fmcb(std::uint32_t sx, std::uint32_t sy, std::uint32_t cx, std:
 
 int synth_points_uniform(const double* box4, std::uint64_t n, std::uint64_t offset,
                          std::uint64_t seed, int threads, double* out) {
-  const double w = box4[1] - box4[0], h = box4[3] - box4[2];
   parallel_for(n, threads, [&](std::uint64_t b, std::uint64_t e) {
-    for (std::uint64_t k = b; k < e; ++k) {
-      const std::uint64_t i = offset + k;
-      out[2 * k] = box4[0] + w * unit(draw(seed, kStreamPoints, 4 * i + 2));
-      out[2 * k + 1] = box4[2] + h * unit(draw(seed, kStreamPoints, 4 * i + 3));
-    }
+    for (std::uint64_t k = b; k < e; ++k) synth::uniform_point(seed, offset + k, box4, out + 2 * k);
   });
   return 0;
+}
+
+// The clustered mixture's centre table: centres uniform over domain4, in
+// generation order k = Zipf rank; cdf[k] = sum_{j<=k} (j+1)^-zipf_s.
+// Returns the total weight.  The device generator (synth_gpu.cu) takes the
+// same table.
+double synth_centre_table(const double* domain4, std::uint64_t seed, std::uint32_t n_centres,
+                          double zipf_s, double* cxy, double* cdf) {
+  double acc = 0.0;
+  for (std::uint32_t k = 0; k < n_centres; ++k) {
+    cxy[2 * k] = domain4[0] + (domain4[1] - domain4[0]) * unit(draw(seed, kStreamCentres, 2 * k));
+    cxy[2 * k + 1] = domain4[2] + (domain4[3] - domain4[2]) * unit(draw(seed, kStreamCentres, 2 * k + 1));
+    acc += std::pow(static_cast<double>(k + 1), -zipf_s);
+    cdf[k] = acc;
+  }
+  return acc;
 }
 
 // Clustered mixture (BASELINE configs 2, 3, 5): with probability
@@ -542,31 +555,11 @@ int synth_points_clustered(const double* domain4, const double* box4,
                            int threads, double* out) {
   if (n_centres == 0) return 1;
   std::vector<double> cxy(2 * n_centres), cdf(n_centres);
-  double acc = 0.0;
-  for (std::uint32_t k = 0; k < n_centres; ++k) {
-    cxy[2 * k] = domain4[0] + (domain4[1] - domain4[0]) * unit(draw(seed, kStreamCentres, 2 * k));
-    cxy[2 * k + 1] = domain4[2] + (domain4[3] - domain4[2]) * unit(draw(seed, kStreamCentres, 2 * k + 1));
-    acc += std::pow(static_cast<double>(k + 1), -zipf_s);
-    cdf[k] = acc;
-  }
-  const double w = box4[1] - box4[0], h = box4[3] - box4[2];
+  const double acc = synth_centre_table(domain4, seed, n_centres, zipf_s, cxy.data(), cdf.data());
   parallel_for(n, threads, [&](std::uint64_t b, std::uint64_t e) {
     for (std::uint64_t k = b; k < e; ++k) {
-      const std::uint64_t i = offset + k;
-      const double u0 = unit(draw(seed, kStreamPoints, 4 * i));
-      if (u0 < frac_clustered) {
-        const double t = unit(draw(seed, kStreamPoints, 4 * i + 1)) * acc;
-        std::uint32_t c = static_cast<std::uint32_t>(
-            std::upper_bound(cdf.begin(), cdf.end(), t) - cdf.begin());
-        if (c >= n_centres) c = n_centres - 1;
-        double gx, gy;
-        gauss2(draw(seed, kStreamPoints, 4 * i + 2), draw(seed, kStreamPoints, 4 * i + 3), &gx, &gy);
-        out[2 * k] = cxy[2 * c] + sigma * gx;
-        out[2 * k + 1] = cxy[2 * c + 1] + sigma * gy;
-      } else {
-        out[2 * k] = box4[0] + w * unit(draw(seed, kStreamPoints, 4 * i + 2));
-        out[2 * k + 1] = box4[2] + h * unit(draw(seed, kStreamPoints, 4 * i + 3));
-      }
+      synth::clustered_point(seed, offset + k, cxy.data(), cdf.data(), n_centres, acc, sigma,
+                             frac_clustered, box4, out + 2 * k);
     }
   });
   return 0;
@@ -583,34 +576,10 @@ int synth_points_near_edge(const double* vxy, const std::uint64_t* ring_off,
                            std::uint64_t n, std::uint64_t offset,
                            std::uint64_t seed, int threads, double* out) {
   if (n_polys == 0) return 1;
-  const double w = box4[1] - box4[0], h = box4[3] - box4[2];
   parallel_for(n, threads, [&](std::uint64_t b, std::uint64_t e) {
     for (std::uint64_t k = b; k < e; ++k) {
-      const std::uint64_t i = offset + k;
-      const double u0 = unit(draw(seed, kStreamPoints, 4 * i));
-      if (u0 < frac_near) {
-        const std::uint64_t r1 = draw(seed, kStreamPoints, 4 * i + 1);
-        const std::uint64_t r2 = draw(seed, kStreamPoints, 4 * i + 2);
-        const std::uint64_t r3 = draw(seed, kStreamPoints, 4 * i + 3);
-        const std::uint64_t p = std::min<std::uint64_t>(
-            n_polys - 1, static_cast<std::uint64_t>(unit(r1) * n_polys));
-        const std::uint64_t r = poly_ring[p];
-        const std::uint64_t vb = ring_off[r], nvert = ring_off[r + 1] - vb;
-        const std::uint64_t ea = vb + (mix64(r1) % nvert);
-        const std::uint64_t eb = (ea + 1 < vb + nvert) ? ea + 1 : vb;
-        const double ax = vxy[2 * ea], ay = vxy[2 * ea + 1];
-        const double bx = vxy[2 * eb], by = vxy[2 * eb + 1];
-        const double t = unit(r2);
-        const double du = (bx - ax) / cw, dv = (by - ay) / ch;
-        const double len = std::sqrt(du * du + dv * dv);
-        const double d = eps_cells * (2.0 * unit(r3) - 1.0);
-        const double nu = len > 0 ? -dv / len : 0.0, nv = len > 0 ? du / len : 0.0;
-        out[2 * k] = ax + (bx - ax) * t + d * nu * cw;
-        out[2 * k + 1] = ay + (by - ay) * t + d * nv * ch;
-      } else {
-        out[2 * k] = box4[0] + w * unit(draw(seed, kStreamPoints, 4 * i + 2));
-        out[2 * k + 1] = box4[2] + h * unit(draw(seed, kStreamPoints, 4 * i + 3));
-      }
+      synth::near_edge_point(seed, offset + k, vxy, ring_off, poly_ring, n_polys, cw, ch, eps_cells,
+                             frac_near, box4, out + 2 * k);
     }
   });
   return 0;

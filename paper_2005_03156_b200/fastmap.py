@@ -316,6 +316,21 @@ class CellIndex:
         g["n_polys"] = int(g["n_polys"])
         return grid, arena, g
 
+    def set_query_path(self, path: str = "auto", tile_bytes: float = 0.0) -> None:
+        """Exact-mode query path: "auto" (default), "stream" or "binned"
+        (fm_index_set_query_path; the answers are the same on every path)."""
+        code = {"auto": N.PATH_AUTO, "stream": N.PATH_STREAM, "binned": N.PATH_BINNED}[path]
+        N.check(N.lib().fm_index_set_query_path(self.handle, code, float(tile_bytes)),
+                "fm_index_set_query_path")
+
+    def query_plan(self, n: int) -> dict:
+        """The path a batch of n points takes, and the binned path's tiles."""
+        p, ts, nt = C.c_int(0), C.c_int32(0), C.c_int32(0)
+        N.check(N.lib().fm_index_query_plan(self.handle, int(n), C.byref(p), C.byref(ts),
+                                            C.byref(nt)), "fm_index_query_plan")
+        return {"path": "binned" if p.value == N.PATH_BINNED else "stream",
+                "tile_log2": ts.value, "n_tiles": nt.value}
+
     def save(self, path: str) -> None:
         """Persist the built index (FMCI analogue); reload with :func:`load_index`."""
         N.check(N.lib().fm_index_save(self.handle, str(path).encode()), "fm_index_save")

@@ -32,6 +32,31 @@ def _threads() -> int:
     return max(1, min(64, os.cpu_count() or 1))
 
 
+def _dev_args(out, stream):
+    """(n, data pointer, cudaStream_t) of a CUDA float64 (n, 2) tensor."""
+    import torch
+    if not (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.float64
+            and out.is_contiguous() and out.dim() == 2 and out.shape[1] == 2):
+        raise ValueError("out must be a contiguous CUDA float64 (n, 2) tensor")
+    if stream is None:
+        stream = torch.cuda.current_stream(out.device)
+    s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return out.shape[0], C.c_void_p(out.data_ptr()), C.c_void_p(s)
+
+
+def _clustered_dev(cfg, out, offset, stream):
+    n, ptr, s = _dev_args(out, stream)
+    box = np.asarray(expanded_box(), dtype=np.float64)
+    dom = np.asarray(DOMAIN, dtype=np.float64)
+    rc = N.synth().synth_points_clustered_dev(N.ptr(dom, C.c_double), N.ptr(box, C.c_double), n,
+                                              offset, cfg.seed + 1, cfg.n_centres,
+                                              cfg.centre_sigma_deg, cfg.zipf_s,
+                                              cfg.frac_clustered, ptr, s)
+    if rc != 0:
+        raise RuntimeError(f"synth_points_clustered_dev failed ({rc})")
+    return out
+
+
 @dataclass(frozen=True)
 class TilingConfig:
     name: str
@@ -106,6 +131,40 @@ class TilingConfig:
             raise ValueError("point generation failed")
         return pts
 
+    def make_points_device(self, out, offset: int = 0, soup: Optional[Soup] = None,
+                           stream=None, soup_device=None):
+        """Points [offset, offset + n) of this config's stream written into the
+        CUDA float64 (n, 2) tensor ``out`` by the GPU generator -- bit-identical
+        to :meth:`make_points` (csrc/synth_rng.h).  ``soup_device``: the soup's
+        (vxy, ring_off, poly_ring) as CUDA tensors (near-edge streams; built
+        from ``soup`` when omitted)."""
+        if self.points == "clustered":
+            return _clustered_dev(self, out, offset, stream)
+        n, ptr, s = _dev_args(out, stream)
+        box = np.asarray(expanded_box(), dtype=np.float64)
+        L = N.synth()
+        if self.points == "uniform":
+            rc = L.synth_points_uniform_dev(N.ptr(box, C.c_double), n, offset, self.seed + 1, ptr, s)
+        elif self.points == "near_edge":
+            if soup_device is None:
+                import torch
+                sp = (soup or self.make_soup()).contiguous()
+                soup_device = (torch.from_numpy(sp.vxy).to(out.device),
+                               torch.from_numpy(sp.ring_off.view(np.int64)).to(out.device),
+                               torch.from_numpy(sp.poly_ring.view(np.int64)).to(out.device))
+            vd, rd, pd = soup_device
+            cw, ch = self.cell_size
+            rc = L.synth_points_near_edge_dev(C.c_void_p(vd.data_ptr()), C.c_void_p(rd.data_ptr()),
+                                              C.c_void_p(pd.data_ptr()), pd.shape[0] - 1, cw, ch,
+                                              self.near_eps_cells, self.frac_near,
+                                              N.ptr(box, C.c_double), n, offset, self.seed + 1,
+                                              ptr, s)
+        else:
+            raise ValueError(self.points)
+        if rc != 0:
+            raise RuntimeError(f"device point generation failed ({rc})")
+        return out
+
 
 @dataclass(frozen=True)
 class NestedConfig:
@@ -174,6 +233,11 @@ class NestedConfig:
         if rc != 0:
             raise ValueError("point generation failed")
         return pts
+
+    def make_points_device(self, out, offset: int = 0, soup=None, stream=None, soup_device=None):
+        """GPU-generated points [offset, offset + n) into the CUDA tensor
+        ``out``, bit-identical to :meth:`make_points`."""
+        return _clustered_dev(self, out, offset, stream)
 
 
 CONFIGS = {

@@ -159,26 +159,6 @@ def test_concurrent_streams_share_an_index(dev):
     assert torch.equal(oa, ra) and torch.equal(ob, rb)
 
 
-@pytest.mark.parametrize("name,n,m", [("c1", 1_000_000, 0.0), ("c2", 2_000_000, 8.0),
-                                      ("c4", 500_000, 0.0)])
-def test_quick_records_resolve_bit_exact(dev, monkeypatch, name, n, m):
-    """The opt-in quick-record resolve (FASTMAP_B200_QUICK=1, csrc/quick.h):
-    near-edge points included, every answer equals the oracle's."""
-    import test_quick_cpu
-    monkeypatch.setenv("FASTMAP_B200_QUICK", "1")
-    cfg = synth.config(name)
-    soup = cfg.make_soup()
-    pts = np.concatenate([cfg.make_points(n, soup=soup),
-                          test_quick_cpu.near_edge_points(soup, n // 4, seed=11)])
-    idx = fastmap.build_index(soup, fastmap.CoverParams(cells_per_polygon=m), device=0)
-    got = project_device(idx, pts, dev)
-    want = oracle.assign(soup, pts)
-    assert int((got != want).sum()) == 0
-    hist = torch.zeros(soup.n_polys, dtype=torch.int64, device=dev)
-    idx.project(torch.from_numpy(pts).to(dev), hist=hist)
-    assert np.array_equal(hist.cpu().numpy(), np.bincount(want[want >= 0], minlength=soup.n_polys))
-
-
 def test_histogram_shared_across_streams_and_host_chunks(dev):
     """The per-launch u32 counters are folded into the caller's int64
     histogram atomically: host-path chunks on 3 streams, and device queries
