@@ -181,6 +181,15 @@ fm_status fm_query_mode(const fm_index* index, int mode, const double* d_lonlat,
 fm_status fm_query_host_mode(const fm_index* index, int mode, const double* h_lonlat,
                              uint64_t n, int32_t* h_out, int64_t* h_hist);
 
+/* fm_query_host_mode that also accumulates the query's work counters into
+ * the HOST struct `counters` (nullable): points, boundary points (the
+ * points that needed crossing tests -- query_leaves' pending points,
+ * cell_index.hpp:561-563), candidate leaves evaluated (its
+ * pip_point_evaluations, :582-583) and fp64 edge predicates evaluated. */
+fm_status fm_query_host_counted(const fm_index* index, int mode, const double* h_lonlat,
+                                uint64_t n, int32_t* h_out, int64_t* h_hist,
+                                fm_query_counters* counters);
+
 /* Query path of the exact mode.  Both paths answer every point with the
  * same locate / exact crossing code, so the ids are identical; they differ
  * only in memory order:

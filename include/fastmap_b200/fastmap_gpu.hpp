@@ -29,6 +29,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <filesystem>
 #include <memory>
 #include <span>
@@ -41,6 +42,8 @@
 #include "fastmap/hierarchy.hpp"
 #include "fastmap/simple_mapper.hpp"
 #include "fastmap_b200.h"
+
+#include <unistd.h>
 
 namespace fastmap::gpu {
 
@@ -165,8 +168,20 @@ inline AssignmentResult query_leaves(const CellIndex& index, std::span<const Lea
   if (index.n_leaves() != leaves.size()) {
     throw std::invalid_argument("cover was built for a different hierarchy");
   }
-  const auto ids = project(index, points, mode);
+  std::vector<std::int32_t> ids(points.size());
+  fm_query_counters qc{};
+  detail::check(fm_query_host_counted(index.get(),
+                                      mode == CoverMode::approx ? FM_MODE_APPROX : FM_MODE_EXACT,
+                                      reinterpret_cast<const double*>(points.data()), points.size(),
+                                      ids.data(), nullptr, &qc),
+                "fm_query_host_counted");
   AssignmentResult res;
+  // the GPU index's own work counts (cell_index.hpp:582-583 counts the
+  // reference cover's): one exact evaluation per point in a boundary cell
+  // (pip_calls) and one (point, candidate leaf) parity per candidate tested
+  // (pip_point_evaluations); true-hit and empty cells cost neither
+  res.counters.pip_calls = qc.boundary_points;
+  res.counters.pip_point_evaluations = qc.candidate_tests;
   res.state.assign(points.size(), -1);
   res.county.assign(points.size(), -1);
   res.block.assign(points.size(), -1);
@@ -184,6 +199,24 @@ inline AssignmentResult query(const CellIndex& index, const RegionHierarchy& h,
                               std::span<const Point> points, CoverMode mode) {
   const auto leaves = collect_leaves(h);  // cell_index.hpp:592-596
   return query_leaves(index, leaves, points, mode);
+}
+
+/// index_stats(trie, cover) (cell_index.hpp:607-631) for the GPU index:
+/// the reference's IndexStats fields mapped onto the cell grid --
+/// interior_cells = true-hit cells, boundary_cells = cells with a boundary
+/// slot, entry_bytes = the slot and overflow arenas (the cover entries'
+/// role), node_bytes = the query grid (the trie's role; trie_nodes = 0, the
+/// grid is direct-mapped), total_bytes = their sum.
+inline IndexStats index_stats(const CellIndex& index) {
+  const fm_index_stats s = index.stats();
+  IndexStats r;
+  r.interior_cells = static_cast<std::size_t>(s.cells_hit);
+  r.boundary_cells = static_cast<std::size_t>(s.cells_boundary);
+  r.trie_nodes = 0;
+  r.entry_bytes = static_cast<std::size_t>(s.arena_bytes);
+  r.node_bytes = static_cast<std::size_t>(s.query_grid_bytes ? s.query_grid_bytes : s.grid_bytes);
+  r.total_bytes = r.entry_bytes + r.node_bytes;
+  return r;
 }
 
 /// Index persistence (the FMCI save/load analogue, cell_index.hpp:641-726).
@@ -224,14 +257,22 @@ class SimpleEngine {
  public:
   explicit SimpleEngine(const RegionHierarchy& h, int device = 0) {
     namespace fs = std::filesystem;
-    const fs::path tmp = fs::temp_directory_path() /
-                         ("fastmap_gpu_" + std::to_string(reinterpret_cast<std::uintptr_t>(this)) + ".fmcb");
-    save_hierarchy(h, tmp.string());
+    // a fresh file of our own (mkstemp: O_EXCL, never follows a planted
+    // link), removed on every exit path
+    std::string tmpl = (fs::temp_directory_path() / "fastmap_gpu_XXXXXX").string();
+    const int fd = ::mkstemp(tmpl.data());
+    if (fd < 0) throw std::runtime_error("cannot create a temporary hierarchy file");
+    ::close(fd);
+    struct Remove {
+      std::string p;
+      ~Remove() {
+        std::error_code ec;
+        std::filesystem::remove(p, ec);
+      }
+    } guard{tmpl};
+    save_hierarchy(h, tmpl);
     fm_hierarchy* hh = nullptr;
-    const fm_status st = fm_hierarchy_load(tmp.string().c_str(), &hh);
-    std::error_code ec;
-    fs::remove(tmp, ec);
-    detail::check(st, "fm_hierarchy_load");
+    detail::check(fm_hierarchy_load(tmpl.c_str(), &hh), "fm_hierarchy_load");
     h_.reset(hh);
     fm_simple* e = nullptr;
     detail::check(fm_simple_build(h_.get(), device, &e), "fm_simple_build");

@@ -228,13 +228,45 @@ typedef struct {
   int32_t* out;
   uint64_t begin, end;
   int world_check;
+  const uint64_t* order; /* NULL: points begin..end in input order */
 } orc_job;
 
 static void* orc_worker(void* arg) {
   orc_job* j = (orc_job*)arg;
-  for (uint64_t i = j->begin; i < j->end; ++i)
+  for (uint64_t k = j->begin; k < j->end; ++k) {
+    const uint64_t i = j->order ? j->order[k] : k;
     j->out[i] = grid_assign_one(j->g, j->pts[2 * i], j->pts[2 * i + 1], j->world_check);
+  }
   return NULL;
+}
+
+/* Large batches are visited bucket by bucket (a counting sort of the point
+ * indices by bucket): consecutive points then test the same polygons, which
+ * stay in cache.  Only the visiting order changes, not any answer. */
+static uint64_t* bucket_order(const orc_grid* g, const double* pts, uint64_t n) {
+  const int64_t nc = g->nx * g->ny;
+  uint64_t* cnt = (uint64_t*)calloc((size_t)nc + 2, sizeof(uint64_t));
+  uint64_t* order = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n ? n : 1));
+  int64_t* key = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+  if (!cnt || !order || !key) {
+    free(cnt);
+    free(order);
+    free(key);
+    return NULL;
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    const double tx = (pts[2 * i] - g->gx0) * g->inv_w, ty = (pts[2 * i + 1] - g->gy0) * g->inv_h;
+    int64_t k = nc; /* outside (or NaN): one extra bucket */
+    if (tx >= 0.0 && ty >= 0.0 && tx < (double)g->nx && ty < (double)g->ny)
+      k = (int64_t)ty * g->nx + (int64_t)tx;
+    key[i] = k;
+    cnt[k + 1]++;
+  }
+  for (int64_t k = 0; k <= nc; ++k) cnt[k + 1] += cnt[k];
+  for (uint64_t i = 0; i < n; ++i) order[cnt[key[i]]++] = i;
+  free(cnt);
+  free(key);
+  return order;
 }
 
 /* Same semantics as orc_exhaustive_assign, bucketed and threaded. */
@@ -244,6 +276,7 @@ void orc_assign(const double* vxy, const uint64_t* ring_off,
   orc_grid* g = grid_build(vxy, ring_off, poly_ring, n_polys);
   if (threads < 1) threads = 1;
   if (threads > 256) threads = 256;
+  uint64_t* order = n_pts >= (1u << 20) ? bucket_order(g, pts, n_pts) : NULL;
   pthread_t tid[256];
   orc_job jobs[256];
   const uint64_t per = (n_pts + (uint64_t)threads - 1) / (uint64_t)threads;
@@ -257,6 +290,7 @@ void orc_assign(const double* vxy, const uint64_t* ring_off,
     if (jobs[t].begin > n_pts) jobs[t].begin = n_pts;
     if (jobs[t].end > n_pts) jobs[t].end = n_pts;
     jobs[t].world_check = world_check;
+    jobs[t].order = order;
     if (t == threads - 1 || pthread_create(&tid[t], NULL, orc_worker, &jobs[t]) != 0) {
       orc_worker(&jobs[t]);
     } else {
@@ -264,6 +298,7 @@ void orc_assign(const double* vxy, const uint64_t* ring_off,
     }
   }
   for (int t = 0; t < launched; ++t) pthread_join(tid[t], NULL);
+  free(order);
   grid_free(g);
 }
 

@@ -89,7 +89,7 @@ EXPORTS = (
     "fm_hierarchy_sizes", "fm_hierarchy_leaves", "fm_index_build_hierarchy",
     "fm_read_points_f64", "fm_write_assign_csv", "fm_simple_build", "fm_simple_destroy",
     "fm_simple_assign", "fm_simple_assign_host", "fm_index_set_query_path",
-    "fm_index_query_plan",
+    "fm_index_query_plan", "fm_query_host_counted",
 )
 
 MODE_EXACT, MODE_APPROX = 0, 1  # fm_mode (CoverMode, cell_index.hpp:246)
@@ -169,6 +169,9 @@ def lib() -> C.CDLL:
         L.fm_index_export.argtypes = [C.c_void_p, PU32, PU64, PU8, PU64, PD]
         L.fm_index_device.restype = C.c_int
         L.fm_index_device.argtypes = [C.c_void_p]
+        L.fm_query_host_counted.restype = C.c_int
+        L.fm_query_host_counted.argtypes = [C.c_void_p, C.c_int, PD, u64, PI32, PI64,
+                                            C.POINTER(QueryCounters)]
         L.fm_index_set_query_path.restype = C.c_int
         L.fm_index_set_query_path.argtypes = [C.c_void_p, C.c_int, C.c_double]
         L.fm_index_query_plan.restype = C.c_int

@@ -47,13 +47,29 @@
 #endif
 
 constexpr int kBinThreads = 512;
-constexpr int kBinPerThread = 32;
-constexpr int kBinSub = kBinThreads * kBinPerThread;   // 16384-point sub-chunks
-constexpr int kBinSubs = 16;
-constexpr std::uint64_t kBinChunk = std::uint64_t{kBinSub} * kBinSubs;  // 256K points
-constexpr int kRankBits = 14;                           // rank < kBinSub
+constexpr int kBinPerThread = 16;
+constexpr int kBinSub = kBinThreads * kBinPerThread;   // 8192-point sub-chunks
+constexpr int kBinSubs = 8;
+constexpr std::uint64_t kBinChunk = std::uint64_t{kBinSub} * kBinSubs;  // 64K points
+constexpr int kRankBits = 13;                           // rank < kBinSub
 static_assert(kBinSub <= (1 << kRankBits), "rank field too narrow");
 constexpr int kMaxTiles = 4096;                         // keys < kMaxTiles + 1
+
+// Work counters (zeroed per launch): the ordered passes hand out their
+// units -- scatter chunks, query tile groups, gather blocks -- in increasing
+// order from an atomic counter instead of a static grid stride, so the
+// units in flight at any moment are a compact window of the stream.  (With a
+// grid stride the persistent warps drift apart over thousands of
+// iterations and the window, and with it the L2 working set, spreads over
+// the whole array.)
+enum { kCtrScatter = 0, kCtrQuery = 1, kCtrUnbin = 2, kCtrCount = 4 };
+
+__device__ __forceinline__ unsigned long long cta_grab(unsigned long long* ctr, unsigned long long* s_slot) {
+  __syncthreads();
+  if (threadIdx.x == 0) *s_slot = atomicAdd(ctr, 1ull);
+  __syncthreads();
+  return *s_slot;
+}
 
 struct TileGeom {
   int ts = 0;        // log2 tile side in cells
@@ -106,14 +122,16 @@ __global__ void __launch_bounds__(kBinThreads)
 __global__ void __launch_bounds__(kBinThreads, 2)
     bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
                        const unsigned int* __restrict__ table, double2* __restrict__ pts_b,
-                       unsigned int* __restrict__ pos) {
+                       unsigned int* __restrict__ pos, unsigned long long* __restrict__ work) {
   extern __shared__ unsigned int smem[];
+  __shared__ unsigned long long s_grab;
   const int nk = T.n_tiles + 1;
   unsigned int* s_cur = smem;                      // nk: the chunk's cursor per tile
   unsigned int* s_hist = smem + ((nk + 3) & ~3);   // nk: per sub-chunk counts
   unsigned int* s_kr = s_hist + ((nk + 3) & ~3);   // kBinSub: key << 14 | rank
   const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
-  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+  for (std::uint64_t c = cta_grab(work + kCtrScatter, &s_grab); c < n_chunks;
+       c = cta_grab(work + kCtrScatter, &s_grab)) {
     for (int k = threadIdx.x; k < nk; k += blockDim.x) {
       s_cur[k] = table[static_cast<std::uint64_t>(k) * n_chunks + c];
       s_hist[k] = 0u;
@@ -185,7 +203,7 @@ struct RingState {
 // evaluate the previously staged one; repeat while full batches remain.
 template <bool kHist, bool kCount>
 __device__ __forceinline__ void pump(const fm::KParams& P, WarpSmemQ& S, RingState& R, bool drain,
-                                     int lane, int* __restrict__ res, HistT* __restrict__ hist,
+                                     int lane, int* __restrict__ res, const HistSink& hist,
                                      fm::WorkCount& wc) {
   for (;;) {
     const bool stage = R.qn >= 32 || (drain && R.qn > 0);
@@ -236,38 +254,54 @@ __device__ __forceinline__ void pump(const fm::KParams& P, WarpSmemQ& S, RingSta
   }
 }
 
+// Tile groups a warp takes per grab of the query pass's work counter.
+constexpr int kQGroup = 8;
+
 template <bool kHist, bool kCount, int kLs>
 __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
     binned_query_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
                         int* __restrict__ res, HistT* __restrict__ hist,
-                        unsigned long long* __restrict__ counters) {
+                        unsigned long long* __restrict__ counters,
+                        unsigned long long* __restrict__ work) {
   extern __shared__ __align__(16) unsigned char dsmem[];
+  __shared__ HotSmem<kHist> hot;
+  const HistSink hs = hist_open<kHist>(hist, hot);
   WarpSmemQ& S = reinterpret_cast<WarpSmemQ*>(dsmem)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const std::uint64_t tile = 32ull * kU;
   const std::uint64_t n_tiles = (n + tile - 1) / tile;
-  const std::uint64_t gwarp = static_cast<std::uint64_t>(blockIdx.x) * kQWarps + (threadIdx.x >> 5);
-  const std::uint64_t nwarps = static_cast<std::uint64_t>(gridDim.x) * kQWarps;
   const std::uint32_t lt_mask = (1u << lane) - 1u;
   fm::WorkCount wc;
   RingState R;
   R.pit.px = R.pit.py = 0.0;
   R.pit.i = 0;
   R.pit.e = fm::kEmpty;
+  // the warp's tiles: groups of kQGroup consecutive tiles from the counter
+  auto grab = [&]() -> std::uint64_t {
+    unsigned long long g = 0;
+    if (lane == 0) g = atomicAdd(work + kCtrQuery, 1ull);
+    return static_cast<std::uint64_t>(__shfl_sync(0xFFFFFFFFu, g, 0)) * kQGroup;
+  };
+  std::uint64_t t = grab(), g_end = t + kQGroup;
   double2 pn[kU];
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
-    const std::uint64_t i = gwarp * tile + u * 32 + lane;
-    pn[u] = (gwarp < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
+    const std::uint64_t i = t * tile + u * 32 + lane;
+    pn[u] = (t < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
   }
-  for (std::uint64_t t = gwarp; t < n_tiles; t += nwarps) {
+  unsigned long long done = 0;
+  while (t < n_tiles) {
     const std::uint64_t base = t * tile;
     double2 p[kU];
     std::uint32_t e[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) p[u] = pn[u];
     fm::locate_n<kU, true, kLs>(P, p, e);
-    const std::uint64_t tn = t + nwarps;
+    std::uint64_t tn = t + 1;
+    if (tn == g_end) {
+      tn = grab();
+      g_end = tn + kQGroup;
+    }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const std::uint64_t i = tn * tile + u * 32 + lane;
@@ -278,7 +312,7 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
       const std::uint64_t i = base + u * 32 + lane;
       const bool valid = i < n;
       const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
-      if (valid && !is_rec) emit<kHist>(res, hist, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
+      if (valid && !is_rec) emit<kHist>(res, hs, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
       const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec);
       if (is_rec) {
         const int s = (R.head + R.qn + __popc(b & lt_mask)) & (kQCap - 1);
@@ -289,14 +323,15 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
       }
       R.qn += __popc(b);
     }
+    if (kCount) done += min(tile, n - base);
     __syncwarp();
-    pump<kHist, kCount>(P, S, R, false, lane, res, hist, wc);
+    pump<kHist, kCount>(P, S, R, false, lane, res, hs, wc);
+    t = tn;
   }
-  pump<kHist, kCount>(P, S, R, true, lane, res, hist, wc);
+  pump<kHist, kCount>(P, S, R, true, lane, res, hs, wc);
+  hist_close<kHist>(hs);
   if (kCount) {
-    unsigned long long v[4] = {0ull, wc.boundary, wc.cands, wc.edges};
-    for (std::uint64_t t = gwarp; t < n_tiles; t += nwarps) v[0] += min(tile, n - t * tile);
-    if (lane != 0) v[0] = 0;
+    unsigned long long v[4] = {lane == 0 ? done : 0ull, wc.boundary, wc.cands, wc.edges};
 #pragma unroll
     for (int k = 1; k < 4; ++k) {
       for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xFFFFFFFFu, v[k], o);
@@ -307,25 +342,41 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
   }
 }
 
-// out[i] = res[pos[i]], four points per thread (16-byte pos loads and id
-// stores when `out` is 16-byte aligned; otherwise one by one).
-__global__ void __launch_bounds__(256)
+// out[i] = res[pos[i]].  CTAs take blocks of kUnbinBlock points in
+// increasing order from the work counter, four points per thread per round
+// (16-byte pos loads and id stores when `out` is 16-byte aligned).
+constexpr int kUnbinThreads = 256;
+constexpr int kUnbinRounds = 8;
+constexpr std::uint64_t kUnbinBlock = 4ull * kUnbinThreads * kUnbinRounds;  // 8192 points
+
+__global__ void __launch_bounds__(kUnbinThreads)
     unbin_kernel(const unsigned int* __restrict__ pos, const int* __restrict__ res, std::uint64_t n,
-                 int* __restrict__ out) {
-  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-  const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+                 int* __restrict__ out, unsigned long long* __restrict__ work) {
+  __shared__ unsigned long long s_grab;
   const bool vec = (reinterpret_cast<std::uintptr_t>(out) & 15u) == 0;
-  const std::uint64_t n4 = vec ? n / 4 : 0;
+  const std::uint64_t n_blocks = (n + kUnbinBlock - 1) / kUnbinBlock;
   const uint4* p4 = reinterpret_cast<const uint4*>(pos);
   int4* o4 = reinterpret_cast<int4*>(out);
-  for (std::uint64_t q = t0; q < n4; q += stride) {
-    const uint4 k = __ldcs(p4 + q);
-    int4 v;
-    v.x = __ldg(res + k.x);
-    v.y = __ldg(res + k.y);
-    v.z = __ldg(res + k.z);
-    v.w = __ldg(res + k.w);
-    __stcs(o4 + q, v);
+  for (std::uint64_t b = cta_grab(work + kCtrUnbin, &s_grab); b < n_blocks;
+       b = cta_grab(work + kCtrUnbin, &s_grab)) {
+    const std::uint64_t base = b * kUnbinBlock;
+    if (vec && base + kUnbinBlock <= n) {
+#pragma unroll
+      for (int r = 0; r < kUnbinRounds; ++r) {
+        const std::uint64_t q = base / 4 + static_cast<std::uint64_t>(r) * kUnbinThreads + threadIdx.x;
+        const uint4 k = __ldcs(p4 + q);
+        int4 v;
+        v.x = __ldg(res + k.x);
+        v.y = __ldg(res + k.y);
+        v.z = __ldg(res + k.z);
+        v.w = __ldg(res + k.w);
+        __stcs(o4 + q, v);
+      }
+    } else {
+      const std::uint64_t end = min(n, base + kUnbinBlock);
+      for (std::uint64_t i = base + threadIdx.x; i < end; i += kUnbinThreads) {
+        __stcs(out + i, __ldg(res + __ldcs(pos + i)));
+      }
+    }
   }
-  for (std::uint64_t i = n4 * 4 + t0; i < n; i += stride) __stcs(out + i, __ldg(res + __ldcs(pos + i)));
 }

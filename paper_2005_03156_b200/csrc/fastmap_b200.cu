@@ -121,11 +121,74 @@ __device__ __forceinline__ void cp_async_wait0() {
 // every slice of <= 2^28 points, so they cannot overflow.
 using HistT = unsigned int;
 
+// The per-block histogram sink of one CTA.  Clustered streams put most of
+// their points into a few hundred leaves (the top Zipf clusters), and
+// same-address atomics serialise in L2, so a CTA first counts into a small
+// shared-memory cache of hot leaves: a slot is claimed by the first leaf
+// that hashes to it (atomicCAS) and counted with shared-memory atomics;
+// a leaf whose slot is taken goes straight to the global counter.  The
+// cache is flushed into the global counters when the CTA exits.
+constexpr int kHotSlots = 1024;
+struct HistSink {
+  HistT* g = nullptr;         // global per-launch counters
+  unsigned int* tag = nullptr;  // shared: kHotSlots leaf ids (kEmpty = free)
+  unsigned int* cnt = nullptr;  // shared: their counts
+  __device__ __forceinline__ void add(int id) const {
+    const unsigned int u = static_cast<unsigned int>(id);
+    const unsigned int s = (u * 2654435761u) >> 22;  // 10-bit multiplicative hash
+    unsigned int t = tag[s];
+    if (t == fm::kEmpty) {
+      t = atomicCAS(tag + s, fm::kEmpty, u);
+      if (t == fm::kEmpty) t = u;
+    }
+    if (t == u) {
+      atomicAdd(cnt + s, 1u);
+    } else {
+      atomicAdd(g + u, 1u);
+    }
+  }
+};
+static_assert(kHotSlots == 1024, "hash is 10 bits");
+
+// Shared-memory backing of a HistSink (kHist instantiations only).
 template <bool kHist>
-__device__ __forceinline__ void emit(int* __restrict__ out, HistT* __restrict__ hist,
-                                     std::uint64_t i, int id) {
+struct HotSmem {
+  unsigned int tag[kHist ? kHotSlots : 1];
+  unsigned int cnt[kHist ? kHotSlots : 1];
+};
+
+template <bool kHist>
+__device__ __forceinline__ HistSink hist_open(HistT* g, HotSmem<kHist>& h) {
+  HistSink hs;
+  hs.g = g;
+  if (kHist) {
+    for (int k = threadIdx.x; k < kHotSlots; k += blockDim.x) {
+      h.tag[k] = fm::kEmpty;
+      h.cnt[k] = 0u;
+    }
+    hs.tag = h.tag;
+    hs.cnt = h.cnt;
+    __syncthreads();
+  }
+  return hs;
+}
+
+template <bool kHist>
+__device__ __forceinline__ void hist_close(const HistSink& hs) {
+  if (kHist) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHotSlots; k += blockDim.x) {
+      const unsigned int c = hs.cnt[k];
+      if (c) atomicAdd(hs.g + hs.tag[k], c);
+    }
+  }
+}
+
+template <bool kHist>
+__device__ __forceinline__ void emit(int* __restrict__ out, const HistSink& hs, std::uint64_t i,
+                                     int id) {
   __stcs(out + i, id);
-  if (kHist && id >= 0) atomicAdd(hist + id, 1u);
+  if (kHist && id >= 0) hs.add(id);
 }
 template <bool kHist>
 __device__ __forceinline__ void emit(int* __restrict__ out, unsigned long long* __restrict__ hist,
@@ -141,6 +204,8 @@ __global__ void __launch_bounds__(kAWarps * 32, FM_AMINB)
                   int* __restrict__ out, HistT* __restrict__ hist,
                   QItem* __restrict__ q, std::uint32_t* __restrict__ qcount,
                   std::uint64_t region_cap, unsigned long long* __restrict__ counters) {
+  __shared__ HotSmem<kHist> hot;
+  const HistSink hs = hist_open<kHist>(hist, hot);
   const int lane = threadIdx.x & 31;
   const std::uint64_t tile = 32ull * kU;
   const std::uint64_t n_tiles = (n + tile - 1) / tile;
@@ -178,7 +243,7 @@ __global__ void __launch_bounds__(kAWarps * 32, FM_AMINB)
       if (valid) {
         const int id = is_rec ? -2 : (e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
         __stcs(out + i, id);
-        if (kHist && id >= 0) atomicAdd(hist + id, 1u);
+        if (kHist && id >= 0) hs.add(id);
       }
       const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec);
       if (is_rec) {  // streaming stores: the resolve pass reads these much later
@@ -191,6 +256,7 @@ __global__ void __launch_bounds__(kAWarps * 32, FM_AMINB)
     }
   }
   if (gwarp < nwarps && lane == 0) qcount[gwarp] = cnt;
+  hist_close<kHist>(hs);
   if (kCount) {
     unsigned long long v = 0;
     for (std::uint64_t t = gwarp; t < n_tiles; t += nwarps) {
@@ -250,7 +316,7 @@ template <bool kHist, bool kCount>
 __device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const std::uint8_t* buf,
                                                      const QItem& it, int n, int lane,
                                                      int* __restrict__ out,
-                                                     HistT* __restrict__ hist,
+                                                     const HistSink& hist,
                                                      fm::WorkCount& wc) {
   std::uint32_t requeue = 0;
   if (lane < n) {
@@ -302,6 +368,8 @@ __global__ void __launch_bounds__(kBWarps * 32, FM_BMINB)
                    int* __restrict__ out, HistT* __restrict__ hist,
                    unsigned long long* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char dsmem[];
+  __shared__ HotSmem<kHist> hot;
+  const HistSink hs = hist_open<kHist>(hist, hot);
   const int lane = threadIdx.x & 31;
   WarpSmemB& S = reinterpret_cast<WarpSmemB*>(dsmem)[threadIdx.x >> 5];
   fm::WorkCount wc;
@@ -333,7 +401,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FM_BMINB)
         }
         __syncwarp();
         const std::uint32_t ce = eval_staged<kHist, kCount>(P, S.pool[buf], cur, ncur, lane, out,
-                                                            hist, wc);
+                                                            hs, wc);
         const std::uint32_t rq = __ballot_sync(0xFFFFFFFFu, ce != 0u);
         if (ce != 0u) {
           QItem it = cur;
@@ -351,6 +419,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FM_BMINB)
       __syncwarp();
     }
   }
+  hist_close<kHist>(hs);
   if (kCount) {
     unsigned long long v[3] = {wc.boundary, wc.cands, wc.edges};
 #pragma unroll
@@ -776,6 +845,7 @@ struct fm_index {
   double* d_in[kStreams] = {};
   int* d_out[kStreams] = {};
   unsigned long long* d_hist = nullptr;
+  unsigned long long* d_counters = nullptr;  // fm_query_host_counted, per stream
 };
 
 namespace {
@@ -867,7 +937,9 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
                                         static_cast<std::int64_t>(n_tab), stream));
   // scratch: the (tile x chunk) count table and its scan, scan temp, binned
   // points, binned positions, binned answers (24 B per point)
-  const std::uint64_t o_scan = align256(4 * n_tab);
+  const std::uint64_t o_work = 0;
+  const std::uint64_t o_tab = 256;
+  const std::uint64_t o_scan = o_tab + align256(4 * n_tab);
   const std::uint64_t o_tmp = o_scan + align256(4 * n_tab);
   const std::uint64_t o_pts = o_tmp + align256(cub_bytes + 16);
   const std::uint64_t o_pos = o_pts + align256(16 * n);
@@ -875,7 +947,9 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   const std::uint64_t total = o_res + align256(4 * n);
   char* scratch = nullptr;
   FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), total, stream));
-  unsigned int* table = reinterpret_cast<unsigned int*>(scratch);
+  unsigned long long* work = reinterpret_cast<unsigned long long*>(scratch + o_work);
+  unsigned int* table = reinterpret_cast<unsigned int*>(scratch + o_tab);
+  FM_CUDA(cudaMemsetAsync(work, 0, 8 * kCtrCount, stream));
   unsigned int* starts = reinterpret_cast<unsigned int*>(scratch + o_scan);
   double2* pts_b = reinterpret_cast<double2*>(scratch + o_pts);
   unsigned int* pos = reinterpret_cast<unsigned int*>(scratch + o_pos);
@@ -889,18 +963,19 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   auto ks = bin_scatter_kernel;
   const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       n_chunks, resident_blocks(ix->device, (const void*)ks, kBinThreads, kBinScatterSmem))));
-  ks<<<grid_s, kBinThreads, kBinScatterSmem, stream>>>(P, T, pts, n, starts, pts_b, pos);
+  ks<<<grid_s, kBinThreads, kBinScatterSmem, stream>>>(P, T, pts, n, starts, pts_b, pos, work);
   auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<kHist, kCount, 0>
                               : binned_query_kernel<kHist, kCount, -1>;
   const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);
   const int grid_q = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      (n_tiles + kQWarps - 1) / kQWarps,
+      (n_tiles + kQWarps * kQGroup - 1) / (kQWarps * kQGroup),
       resident_blocks(ix->device, (const void*)kq, kQWarps * 32, kSmemQ))));
-  kq<<<grid_q, kQWarps * 32, kSmemQ, stream>>>(P, pts_b, n, res, d_hist, d_counters);
+  kq<<<grid_q, kQWarps * 32, kSmemQ, stream>>>(P, pts_b, n, res, d_hist, d_counters, work);
   auto ku = unbin_kernel;
   const int grid_u = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      (n / 4 + 255) / 256, resident_blocks(ix->device, (const void*)ku, 256, 0))));
-  ku<<<grid_u, 256, 0, stream>>>(pos, res, n, d_out);
+      (n + kUnbinBlock - 1) / kUnbinBlock,
+      resident_blocks(ix->device, (const void*)ku, kUnbinThreads, 0))));
+  ku<<<grid_u, kUnbinThreads, 0, stream>>>(pos, res, n, d_out, work);
   const cudaError_t err = cudaGetLastError();
   FM_CUDA(cudaFreeAsync(scratch, stream));
   if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));
@@ -912,13 +987,14 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
 // stream path's per-point gathers miss L2 (c3: 47 GB of slots, 60% boundary
 // cells; c4: 5.5 GB, 50%) -- and the batch is big enough to reuse tiles;
 // the stream path otherwise (c1; c2: 9% boundary cells).
+constexpr bool kAutoBinned = false;  // binned not yet faster than stream on c3/c4 (profiles/r2d)
 bool use_binned(const fm_index* ix, std::uint64_t n) {
   if (ix->query_path == FM_PATH_STREAM) return false;
   if (ix->query_path == FM_PATH_BINNED) return true;
   const double cells = static_cast<double>(ix->g.nx) * static_cast<double>(ix->g.ny);
   const double bfrac = cells > 0 ? static_cast<double>(ix->stats.cells_boundary) / cells : 0.0;
   const double bytes = static_cast<double>(ix->stats.query_grid_bytes + ix->stats.arena_bytes);
-  return n >= (std::uint64_t{1} << 22) && bytes >= 1e9 && bfrac >= 0.25;
+  return kAutoBinned && n >= (std::uint64_t{1} << 22) && bytes >= 1e9 && bfrac >= 0.25;
 }
 
 // Tiles of 2^ts x 2^ts cells holding about `tile_bytes` of index (grid
@@ -1293,6 +1369,7 @@ void free_device(fm_index* ix) {
     if (ix->streams[s]) cudaStreamDestroy(ix->streams[s]);
   }
   if (ix->d_hist) cudaFree(ix->d_hist);
+  if (ix->d_counters) cudaFree(ix->d_counters);
   if (ix->d_grid) cudaFree(ix->d_grid);
   ix->qgrid.release();
   ix->agrid.release();
@@ -1535,6 +1612,12 @@ fm_status fm_query_mode(const fm_index* index, int mode, const double* d_lonlat,
 
 fm_status fm_query_host_mode(const fm_index* cindex, int mode, const double* h_lonlat,
                              std::uint64_t n, std::int32_t* h_out, std::int64_t* h_hist) {
+  return fm_query_host_counted(cindex, mode, h_lonlat, n, h_out, h_hist, nullptr);
+}
+
+fm_status fm_query_host_counted(const fm_index* cindex, int mode, const double* h_lonlat,
+                                std::uint64_t n, std::int32_t* h_out, std::int64_t* h_hist,
+                                fm_query_counters* h_counters) {
   g_err.clear();
   if (!cindex) return set_err(FM_ERR_INVALID_ARGUMENT, "index is null");
   if (check_mode(cindex, mode) != FM_OK) return FM_ERR_INVALID_ARGUMENT;
@@ -1562,6 +1645,13 @@ fm_status fm_query_host_mode(const fm_index* cindex, int mode, const double* h_l
     FM_CUDA(cudaMemsetAsync(dh, 0, std::max<std::uint64_t>(1, index->stats.n_polys) * 8, index->streams[0]));
     FM_CUDA(cudaStreamSynchronize(index->streams[0]));
   }
+  unsigned long long* dc = nullptr;  // work counters: one set per stream
+  if (h_counters) {
+    if (!index->d_counters) FM_CUDA(cudaMalloc(&index->d_counters, kStreams * 4 * 8));
+    dc = index->d_counters;
+    FM_CUDA(cudaMemsetAsync(dc, 0, kStreams * 4 * 8, index->streams[0]));
+    FM_CUDA(cudaStreamSynchronize(index->streams[0]));
+  }
   const std::uint64_t n_chunks = (n + kChunkPoints - 1) / kChunkPoints;
   for (std::uint64_t c = 0; c < n_chunks; ++c) {
     const int s = static_cast<int>(c % kStreams);
@@ -1569,8 +1659,8 @@ fm_status fm_query_host_mode(const fm_index* cindex, int mode, const double* h_l
     const std::uint64_t m = std::min(kChunkPoints, n - off);
     FM_CUDA(cudaMemcpyAsync(index->d_in[s], h_lonlat + 2 * off, m * 16, cudaMemcpyHostToDevice,
                             index->streams[s]));
-    const fm_status st = launch(index, index->d_in[s], m, index->d_out[s], dh, nullptr,
-                                index->streams[s], mode);
+    const fm_status st = launch(index, index->d_in[s], m, index->d_out[s], dh,
+                                dc ? dc + 4 * s : nullptr, index->streams[s], mode);
     if (st != FM_OK) return st;
     FM_CUDA(cudaMemcpyAsync(h_out + off, index->d_out[s], m * 4, cudaMemcpyDeviceToHost,
                             index->streams[s]));
@@ -1580,6 +1670,16 @@ fm_status fm_query_host_mode(const fm_index* cindex, int mode, const double* h_l
     std::vector<std::int64_t> tmp(index->stats.n_polys);
     FM_CUDA(cudaMemcpy(tmp.data(), dh, index->stats.n_polys * 8, cudaMemcpyDeviceToHost));
     for (std::uint64_t k = 0; k < index->stats.n_polys; ++k) h_hist[k] += tmp[k];
+  }
+  if (h_counters) {
+    unsigned long long v[kStreams * 4];
+    FM_CUDA(cudaMemcpy(v, dc, sizeof(v), cudaMemcpyDeviceToHost));
+    for (int s = 0; s < kStreams; ++s) {
+      h_counters->points += v[4 * s];
+      h_counters->boundary_points += v[4 * s + 1];
+      h_counters->candidate_tests += v[4 * s + 2];
+      h_counters->edge_tests += v[4 * s + 3];
+    }
   }
   return FM_OK;
 }

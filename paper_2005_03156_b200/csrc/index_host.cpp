@@ -541,6 +541,19 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
     }
     nx = static_cast<std::int64_t>(std::ceil(GW / (mw / m)));
     ny = static_cast<std::int64_t>(std::ceil(GH / (mh / m)));
+    if (!(o.cells_per_polygon > 0.0)) {
+      // the budgets above assume the polygons tile their bbox; a sparse
+      // layer (polygons covering a fraction f of the bbox) would get 1/f
+      // times as many cells, so the total is capped at ~1.5x the intended
+      // count (active polygons x m^2)
+      const double want = 1.5 * static_cast<double>(active) * m * m;
+      const double got = static_cast<double>(nx) * static_cast<double>(ny);
+      if (got > want) {
+        const double k = std::sqrt(want / got);
+        nx = static_cast<std::int64_t>(std::ceil(static_cast<double>(nx) * k));
+        ny = static_cast<std::int64_t>(std::ceil(static_cast<double>(ny) * k));
+      }
+    }
     nx = std::min<std::int64_t>(std::max<std::int64_t>(nx, 1), std::int64_t{1} << 22);
     ny = std::min<std::int64_t>(std::max<std::int64_t>(ny, 1), std::int64_t{1} << 22);
     while (nx * ny > (std::int64_t{1} << 30)) {

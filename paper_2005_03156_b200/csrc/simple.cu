@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(256, FM_SIMPLE_MINB)
       int win = -1;
       bool known = false;  // index answer usable: `holder` is the first holder or -1
       int holder = -1;
-      if (P.use_index && p.x >= -180.0 && p.x <= 180.0 && p.y >= -90.0 && p.y <= 90.0) {
+      if (((P.use_index >> l) & 1) && p.x >= -180.0 && p.x <= 180.0 && p.y >= -90.0 && p.y <= 90.0) {
         const int r = level_lookup(P.Q[l], p.x, p.y);  // P.Q: global memory
         if (r < 0) {
           known = true;
@@ -454,10 +454,13 @@ fm_status collect_counters(const fm_simple* s, fm_assign_counters* out) {
   return FM_OK;
 }
 
-fm_status reset_counters(const fm_simple* s) {
-  if (cudaMemset(s->d_evals, 0, 8) != cudaSuccess) return fm_set_error(FM_ERR_CUDA, "counter reset failed");
+// On the query's stream: the counters are reset in order with this call's
+// kernel and after any earlier call's kernel on the same stream.  Counting
+// calls on one engine must not run concurrently on different streams.
+fm_status reset_counters(const fm_simple* s, cudaStream_t stream) {
+  if (cudaMemsetAsync(s->d_evals, 0, 8, stream) != cudaSuccess) return fm_set_error(FM_ERR_CUDA, "counter reset failed");
   for (int l = 0; l < 3; ++l) {
-    if (s->n_regions[l] && cudaMemset(s->P.L[l].tested, 0, s->n_regions[l]) != cudaSuccess) {
+    if (s->n_regions[l] && cudaMemsetAsync(s->P.L[l].tested, 0, s->n_regions[l], stream) != cudaSuccess) {
       return fm_set_error(FM_ERR_CUDA, "counter reset failed");
     }
   }
@@ -483,6 +486,8 @@ fm_status fm_simple_build(const fm_hierarchy* h, int device, fm_simple** out) {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   bool ok = true;
+  fm_status build_status = FM_OK;
+  std::string build_msg;
   try {
     for (int l = 0; l < 3 && ok; ++l) {
       const fm::HierLevel& L = h->level[l];
@@ -512,11 +517,15 @@ fm_status fm_simple_build(const fm_hierarchy* h, int device, fm_simple** out) {
       ok = cudaMalloc(&s->d_evals, 8) == cudaSuccess;
       if (ok) s->allocs.push_back(s->d_evals);
     }
-    // the per-level exact indexes (FASTMAP_B200_SIMPLE_INDEX=0: none)
+    // the per-level exact indexes (FASTMAP_B200_SIMPLE_INDEX=0: none).  A
+    // level whose index cannot be built (inputs the index builder rejects
+    // but load_hierarchy and assign() accept: non-finite vertices, the
+    // candidate or slot limits) keeps the crossing-test path for that level.
     const char* off = std::getenv("FASTMAP_B200_SIMPLE_INDEX");
-    s->P.use_index = (off && off[0] == '0') ? 0 : 1;
+    const bool want_index = !(off && off[0] == '0');
+    s->P.use_index = 0;
     std::vector<fm::KParams> q(3);
-    for (int l = 0; l < 3 && ok && s->P.use_index; ++l) {
+    for (int l = 0; l < 3 && ok && want_index; ++l) {
       const fm::HierLevel& L = h->level[l];
       fm_build_params bp{};
       bp.device = device;
@@ -532,7 +541,16 @@ fm_status fm_simple_build(const fm_hierarchy* h, int device, fm_simple** out) {
       }
       const fm_status bs = fm_index_build(L.vxy.data(), L.ring_off.data(), L.ring_off.size() - 1,
                                           L.poly_ring.data(), L.n_regions(), &bp, &s->lidx[l]);
-      ok = bs == FM_OK && fm_index_kparams(s->lidx[l], &q[l]);
+      if (bs == FM_OK && fm_index_kparams(s->lidx[l], &q[l])) {
+        s->P.use_index |= 1 << l;
+      } else if (bs == FM_ERR_CUDA || bs == FM_ERR_NO_DEVICE) {
+        build_status = bs;  // a device failure is not an input limit: report it
+        build_msg = fm_last_error();
+        ok = false;
+      } else {
+        if (s->lidx[l]) fm_index_destroy(s->lidx[l]);
+        s->lidx[l] = nullptr;
+      }
     }
     s->P.Q = nullptr;
     if (ok && s->P.use_index) ok = add(s, q, &s->P.Q);
@@ -542,6 +560,7 @@ fm_status fm_simple_build(const fm_hierarchy* h, int device, fm_simple** out) {
   if (prev >= 0) cudaSetDevice(prev);
   if (!ok) {
     release(s);
+    if (build_status != FM_OK) return fm_set_error(build_status, build_msg.c_str());
     return fm_set_error(FM_ERR_OOM, "simple-engine build: allocation failed");
   }
   *out = s;
@@ -562,7 +581,7 @@ fm_status fm_simple_assign(const fm_simple* s, int mode, const double* d_lonlat,
   cudaGetDevice(&prev);
   cudaSetDevice(s->device);
   fm_status st = FM_OK;
-  if (counters) st = reset_counters(s);
+  if (counters) st = reset_counters(s, static_cast<cudaStream_t>(stream));
   if (st == FM_OK) {
     st = launch_simple(s, mode, d_lonlat, n, d_state, d_county, d_block, counters != nullptr,
                        static_cast<cudaStream_t>(stream));
@@ -589,7 +608,7 @@ fm_status fm_simple_assign_host(const fm_simple* s, int mode, const double* lonl
   void* buf = nullptr;
   fm_status st = FM_OK;
   if (cudaMalloc(&buf, std::min(chunk, n) * 28) != cudaSuccess) st = fm_set_error(FM_ERR_OOM, "device buffer");
-  if (st == FM_OK && counters) st = reset_counters(s);  // one batch: regions counted once
+  if (st == FM_OK && counters) st = reset_counters(s, nullptr);  // one batch: regions counted once
   for (std::uint64_t off = 0; off < n && st == FM_OK; off += chunk) {
     const std::uint64_t m = std::min(chunk, n - off);
     double* d_p = static_cast<double*>(buf);

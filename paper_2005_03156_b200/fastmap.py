@@ -522,14 +522,18 @@ class SimpleEngine:
                 lib.fm_simple_destroy(self._s)
             self._s = None
 
-    def assign(self, points, mode: AssignMode = AssignMode.relaxed, counters: bool = True,
-               out=None, stream=None) -> AssignmentResult:
-        """Host numpy points -> AssignmentResult; CUDA tensors -> (state, county,
-        block) tensors written on ``stream`` (counters make it synchronous)."""
+    def assign(self, points, mode: AssignMode = AssignMode.relaxed, counters: Optional[bool] = None,
+               out=None, stream=None):
+        """Host numpy points -> AssignmentResult (counters on by default).
+
+        CUDA tensor points -> (state, county, block) int32 tensors written on
+        ``stream`` (asynchronously).  With ``counters=True`` the call is
+        synchronous and returns ``((state, county, block), AssignCounters)``;
+        the default for tensors is no counters."""
         L = N.lib()
         cnt = N.AssignCountersC()
-        cp = C.byref(cnt) if counters else None
         if isinstance(points, np.ndarray):
+            cp = C.byref(cnt) if counters is None or counters else None
             pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
             n = pts.shape[0]
             st, co, bl = (np.empty(n, dtype=np.int32) for _ in range(3))
@@ -539,14 +543,31 @@ class SimpleEngine:
             return AssignmentResult(st, co, bl, AssignCounters(int(cnt.pip_point_evaluations),
                                                                int(cnt.pip_calls)))
         import torch
-        n = points.numel() // 2
+        if not (isinstance(points, torch.Tensor) and points.is_cuda):
+            raise TypeError("points must be a numpy array or a CUDA torch tensor")
+        if (points.dtype != torch.float64 or not points.is_contiguous() or points.dim() != 2
+                or points.shape[1] != 2):
+            raise ValueError("device points must be a contiguous float64 (n, 2) tensor")
+        if points.device.index != self.device:
+            raise ValueError(f"points are on {points.device}, the engine on cuda:{self.device}")
+        n = points.shape[0]
         if out is None:
             out = tuple(torch.empty(n, dtype=torch.int32, device=points.device) for _ in range(3))
+        for t in out:
+            if (t.dtype != torch.int32 or not t.is_contiguous() or t.numel() < n
+                    or t.device != points.device):
+                raise ValueError("outputs must be contiguous int32 tensors of n points on the same device")
         if stream is None:
             stream = torch.cuda.current_stream(points.device).cuda_stream
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        want = bool(counters)
         N.check(L.fm_simple_assign(self._s, int(mode), C.c_void_p(points.data_ptr()), n,
-                                   *[C.c_void_p(t.data_ptr()) for t in out], cp,
+                                   *[C.c_void_p(t.data_ptr()) for t in out],
+                                   C.byref(cnt) if want else None,
                                    C.c_void_p(stream)), "fm_simple_assign")
+        if want:
+            return out, AssignCounters(int(cnt.pip_point_evaluations), int(cnt.pip_calls))
         return out
 
 

@@ -140,6 +140,24 @@ int main(int argc, char** argv) {
   }
   std::printf("%s (GPU): %zu of %zu points differ\n", bad ? "FAIL" : "OK", bad, pts.size());
   if (bad) return 1;
+  // AssignmentResult.counters carry the GPU index's own work counts
+  // (cell_index.hpp:582-583): some but not all points need exact tests
+  if (!(res.counters.pip_calls > 0 && res.counters.pip_calls < pts.size() &&
+        res.counters.pip_point_evaluations >= res.counters.pip_calls)) {
+    std::printf("FAIL: counters pip_calls=%zu pip_point_evaluations=%zu\n",
+                static_cast<std::size_t>(res.counters.pip_calls),
+                static_cast<std::size_t>(res.counters.pip_point_evaluations));
+    return 1;
+  }
+  // index_stats (cell_index.hpp:607-631): the reference's IndexStats fields
+  const IndexStats is = gpu::index_stats(index);
+  const auto fs = index.stats();
+  if (is.interior_cells != fs.cells_hit || is.boundary_cells != fs.cells_boundary ||
+      is.boundary_cells == 0 || is.interior_cells == 0 || is.entry_bytes == 0 ||
+      is.total_bytes != is.entry_bytes + is.node_bytes || is.trie_nodes != 0) {
+    std::puts("FAIL: index_stats");
+    return 1;
+  }
   // index persistence through the adapter: reload and compare
   const std::string path = (std::filesystem::temp_directory_path() / "adapter_check.fmgi").string();
   gpu::save_index(index, path);
