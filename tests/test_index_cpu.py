@@ -102,3 +102,19 @@ def test_slot_invariants():
             assert mk < (1 << max(nv - 1, 0)) or mk == 0
     assert n_half > 0
     assert n_leaf > 0
+
+
+@pytest.mark.parametrize("grid", [(64, 48), (257, 131), (1000, 999)])
+def test_margin_scale_cases_index_exact(grid):
+    """Vertices and edges at {0, 0.5, 1, 2, 4} x margin from cell borders,
+    points at +-k ulps of the borders, on vertices and edges and 1e-9 ..
+    1e-13 cell widths off them (tests/margin_cases.py)."""
+    import margin_cases
+    soup, pts, g = margin_cases.build(*grid)
+    got, idx, _ = walk(soup, pts, nx=grid[0], ny=grid[1])
+    st = idx.stats()
+    # the cases are built against the builder's own cell borders
+    assert st["gx0"] == g["gx0"] and st["gy0"] == g["gy0"]
+    assert st["cell_w"] == g["w"] and st["cell_h"] == g["h"] and st["margin"] == g["d"]
+    assert st["cells_boundary"] > 0
+    assert np.array_equal(got, oracle.exhaustive_assign(soup, pts))
