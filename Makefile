@@ -14,7 +14,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xptxas -v \
 HOSTFLAGS := -O3 -fPIC -ffp-contract=off -pthread
 
 PRODUCT_SRC := $(PKG)/csrc/fastmap_b200.cu $(PKG)/csrc/index_gpu.cu $(PKG)/csrc/index_host.cpp \
-               $(PKG)/csrc/io.cpp $(PKG)/csrc/simple.cu
+               $(PKG)/csrc/io.cpp $(PKG)/csrc/simple.cu $(PKG)/csrc/multi.cu
 PRODUCT_HDR := include/fastmap_b200.h $(PKG)/csrc/index_format.h \
                $(PKG)/csrc/index_build.h $(PKG)/csrc/query.cuh $(PKG)/csrc/sweep.h \
                $(PKG)/csrc/record_encode.h $(PKG)/csrc/hierarchy.h

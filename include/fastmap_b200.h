@@ -190,6 +190,29 @@ fm_status fm_query_host_counted(const fm_index* index, int mode, const double* h
                                 uint64_t n, int32_t* h_out, int64_t* h_hist,
                                 fm_query_counters* counters);
 
+/* Multi-GPU: run_chunked (parallel.hpp:30-82) one level up, for C++
+ * callers owning several GPUs in one process.  fm_multi_build builds one
+ * replica of the index (same arguments as fm_index_build; params->device is
+ * ignored) on each of the n_devices distinct devices, concurrently.
+ * fm_multi_query_host splits the host batch into contiguous, balanced
+ * shards (the first n % N devices take one extra point), runs each shard
+ * through the fm_query_host pipeline of its device from its own host
+ * thread, and -- when h_hist (n_polys int64, accumulated into) is given --
+ * sums the per-device histograms with one ncclAllReduce (NCCL is loaded at
+ * run time; without it a histogram query fails with FM_ERR_RUNTIME).
+ * h_out gets every point's id in input order, exactly as fm_query_host. */
+typedef struct fm_multi fm_multi;
+fm_status fm_multi_build(const double* vertex_lonlat, const uint64_t* ring_offsets,
+                         uint64_t n_rings, const uint64_t* poly_ring_offsets, uint64_t n_polys,
+                         const fm_build_params* params, const int* devices, int n_devices,
+                         fm_multi** out);
+fm_status fm_multi_query_host(fm_multi* multi, int mode, const double* h_lonlat, uint64_t n,
+                              int32_t* h_out, int64_t* h_hist);
+/* Number of replicas, and replica k (an ordinary fm_index owned by the multi). */
+int fm_multi_size(const fm_multi* multi);
+const fm_index* fm_multi_replica(const fm_multi* multi, int k);
+void fm_multi_destroy(fm_multi* multi);
+
 /* Query path of the exact mode.  Both paths answer every point with the
  * same locate / exact crossing code, so the ids are identical; they differ
  * only in memory order:

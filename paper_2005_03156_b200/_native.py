@@ -89,7 +89,8 @@ EXPORTS = (
     "fm_hierarchy_sizes", "fm_hierarchy_leaves", "fm_index_build_hierarchy",
     "fm_read_points_f64", "fm_write_assign_csv", "fm_simple_build", "fm_simple_destroy",
     "fm_simple_assign", "fm_simple_assign_host", "fm_index_set_query_path",
-    "fm_index_query_plan", "fm_query_host_counted",
+    "fm_index_query_plan", "fm_query_host_counted", "fm_multi_build", "fm_multi_query_host",
+    "fm_multi_size", "fm_multi_replica", "fm_multi_destroy",
 )
 
 MODE_EXACT, MODE_APPROX = 0, 1  # fm_mode (CoverMode, cell_index.hpp:246)
@@ -176,6 +177,17 @@ def lib() -> C.CDLL:
         L.fm_index_set_query_path.argtypes = [C.c_void_p, C.c_int, C.c_double]
         L.fm_index_query_plan.restype = C.c_int
         L.fm_index_query_plan.argtypes = [C.c_void_p, u64, C.POINTER(C.c_int), PI32, PI32]
+        L.fm_multi_build.restype = C.c_int
+        L.fm_multi_build.argtypes = [PD, PU64, u64, PU64, u64, C.POINTER(BuildParams),
+                                     C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
+        L.fm_multi_query_host.restype = C.c_int
+        L.fm_multi_query_host.argtypes = [C.c_void_p, C.c_int, PD, u64, PI32, PI64]
+        L.fm_multi_size.restype = C.c_int
+        L.fm_multi_size.argtypes = [C.c_void_p]
+        L.fm_multi_replica.restype = C.c_void_p
+        L.fm_multi_replica.argtypes = [C.c_void_p, C.c_int]
+        L.fm_multi_destroy.restype = None
+        L.fm_multi_destroy.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 

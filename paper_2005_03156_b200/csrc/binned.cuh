@@ -15,15 +15,16 @@
 // true-hit indexes (c1, c2) -- see choose_path() in fastmap_b200.cu.
 //
 // Four launches per batch of n <= 2^30 points:
-//   bin_count_kernel    one CTA per 256K-point *chunk*: a shared-memory
+//   bin_count_kernel    one CTA per 64K-point *chunk*: a shared-memory
 //                       histogram of tile keys, stored as column c of the
 //                       tile-major count table (T+1 rows x n_chunks)
 //   (cub exclusive scan of the table in tile-major order: entry (t, c)
 //    becomes the first position of chunk c's points in tile t)
-//   bin_scatter_kernel  the same chunks, in 16K-point sub-chunks: ranks
-//                       within (sub-chunk, tile) from shared-memory atomics,
-//                       each point written to its tile at the chunk's cursor
-//                       (pts_b), its binned position to pos[i] (coalesced)
+//   bin_scatter_kernel  the same chunks, in 4K-point sub-chunks held in
+//                       registers: ranks within (sub-chunk, tile) from
+//                       warp-aggregated shared-memory atomics, each point
+//                       written to its tile at the chunk's cursor (pts_b),
+//                       its binned position to pos[i] (coalesced)
 //   binned_query_kernel the query over pts_b in order: locate, true hits
 //                       answered at once, boundary points through a
 //                       warp-private shared-memory ring whose batches of 32
@@ -47,11 +48,11 @@
 #endif
 
 constexpr int kBinThreads = 512;
-constexpr int kBinPerThread = 16;
-constexpr int kBinSub = kBinThreads * kBinPerThread;   // 8192-point sub-chunks
-constexpr int kBinSubs = 8;
+constexpr int kBinPerThread = 8;
+constexpr int kBinSub = kBinThreads * kBinPerThread;   // 4096-point sub-chunks
+constexpr int kBinSubs = 16;
 constexpr std::uint64_t kBinChunk = std::uint64_t{kBinSub} * kBinSubs;  // 64K points
-constexpr int kRankBits = 13;                           // rank < kBinSub
+constexpr int kRankBits = 13;                           // rank <= kBinSub
 static_assert(kBinSub <= (1 << kRankBits), "rank field too narrow");
 constexpr int kMaxTiles = 4096;                         // keys < kMaxTiles + 1
 
@@ -119,6 +120,12 @@ __global__ void __launch_bounds__(kBinThreads)
   }
 }
 
+// The points of a sub-chunk are read once, into registers (kBinPerThread
+// per thread); ranks within (sub-chunk, tile) come from shared-memory
+// atomics aggregated per warp (__match_any_sync: clustered streams put many
+// lanes of a warp into the same hot tile, whose counter would otherwise
+// serialise them), and the points are written from registers once the
+// sub-chunk's counts are known.
 __global__ void __launch_bounds__(kBinThreads, 2)
     bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
                        const unsigned int* __restrict__ table, double2* __restrict__ pts_b,
@@ -128,7 +135,8 @@ __global__ void __launch_bounds__(kBinThreads, 2)
   const int nk = T.n_tiles + 1;
   unsigned int* s_cur = smem;                      // nk: the chunk's cursor per tile
   unsigned int* s_hist = smem + ((nk + 3) & ~3);   // nk: per sub-chunk counts
-  unsigned int* s_kr = s_hist + ((nk + 3) & ~3);   // kBinSub: key << 14 | rank
+  const int lane = threadIdx.x & 31;
+  const unsigned int lt_mask = (1u << lane) - 1u;
   const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
   for (std::uint64_t c = cta_grab(work + kCtrScatter, &s_grab); c < n_chunks;
        c = cta_grab(work + kCtrScatter, &s_grab)) {
@@ -140,28 +148,32 @@ __global__ void __launch_bounds__(kBinThreads, 2)
     for (int sub = 0; sub < kBinSubs; ++sub) {
       const std::uint64_t base = c * kBinChunk + static_cast<std::uint64_t>(sub) * kBinSub;
       if (base >= n) break;
-      // ranks within (sub-chunk, tile); the sub-chunk's points stay in L2
-      // for the second read below
-#pragma unroll 4
+      double2 p[kBinPerThread];
+      unsigned int kr[kBinPerThread];
+#pragma unroll
       for (int j = 0; j < kBinPerThread; ++j) {
-        const int li = j * kBinThreads + threadIdx.x;
-        const std::uint64_t i = base + li;
-        if (i < n) {
-          const double2 p = __ldg(pts + i);
-          const int key = tile_key(P, T, p.x, p.y);
-          const unsigned int r = atomicAdd(s_hist + key, 1u);
-          s_kr[li] = (static_cast<unsigned int>(key) << kRankBits) | r;
-        }
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kBinThreads + threadIdx.x;
+        p[j] = i < n ? __ldcs(pts + i) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < kBinPerThread; ++j) {
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kBinThreads + threadIdx.x;
+        const bool valid = i < n;
+        const int key = valid ? tile_key(P, T, p[j].x, p[j].y) : -1;
+        const unsigned int peers = __match_any_sync(0xFFFFFFFFu, key);
+        const int leader = __ffs(peers) - 1;
+        unsigned int r = 0;
+        if (valid && lane == leader) r = atomicAdd(s_hist + key, static_cast<unsigned int>(__popc(peers)));
+        r = __shfl_sync(0xFFFFFFFFu, r, leader) + __popc(peers & lt_mask);
+        kr[j] = valid ? ((static_cast<unsigned int>(key) << kRankBits) | r) : 0xFFFFFFFFu;
       }
       __syncthreads();
-#pragma unroll 4
+#pragma unroll
       for (int j = 0; j < kBinPerThread; ++j) {
-        const int li = j * kBinThreads + threadIdx.x;
-        const std::uint64_t i = base + li;
-        if (i < n) {
-          const unsigned int kr = s_kr[li];
-          const unsigned int dst = s_cur[kr >> kRankBits] + (kr & ((1u << kRankBits) - 1u));
-          pts_b[dst] = __ldcs(pts + i);
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kBinThreads + threadIdx.x;
+        if (kr[j] != 0xFFFFFFFFu) {
+          const unsigned int dst = s_cur[kr[j] >> kRankBits] + (kr[j] & ((1u << kRankBits) - 1u));
+          pts_b[dst] = p[j];
           __stcs(pos + i, dst);
         }
       }
@@ -361,16 +373,24 @@ __global__ void __launch_bounds__(kUnbinThreads)
        b = cta_grab(work + kCtrUnbin, &s_grab)) {
     const std::uint64_t base = b * kUnbinBlock;
     if (vec && base + kUnbinBlock <= n) {
+      // every pos load of the block, then every gather: 4 * kUnbinRounds
+      // independent loads in flight per thread
+      uint4 k[kUnbinRounds];
 #pragma unroll
       for (int r = 0; r < kUnbinRounds; ++r) {
-        const std::uint64_t q = base / 4 + static_cast<std::uint64_t>(r) * kUnbinThreads + threadIdx.x;
-        const uint4 k = __ldcs(p4 + q);
-        int4 v;
-        v.x = __ldg(res + k.x);
-        v.y = __ldg(res + k.y);
-        v.z = __ldg(res + k.z);
-        v.w = __ldg(res + k.w);
-        __stcs(o4 + q, v);
+        k[r] = __ldcs(p4 + base / 4 + static_cast<std::uint64_t>(r) * kUnbinThreads + threadIdx.x);
+      }
+      int4 v[kUnbinRounds];
+#pragma unroll
+      for (int r = 0; r < kUnbinRounds; ++r) {
+        v[r].x = __ldg(res + k[r].x);
+        v[r].y = __ldg(res + k[r].y);
+        v[r].z = __ldg(res + k[r].z);
+        v[r].w = __ldg(res + k[r].w);
+      }
+#pragma unroll
+      for (int r = 0; r < kUnbinRounds; ++r) {
+        __stcs(o4 + base / 4 + static_cast<std::uint64_t>(r) * kUnbinThreads + threadIdx.x, v[r]);
       }
     } else {
       const std::uint64_t end = min(n, base + kUnbinBlock);

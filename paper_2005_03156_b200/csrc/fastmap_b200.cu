@@ -920,7 +920,7 @@ fm_status launch_t(const fm_index* ix, const double2* pts, std::uint64_t n, int*
 // The binned path (binned.cuh) over one batch of n <= kBinnedBatch points.
 constexpr std::uint64_t kBinnedBatch = std::uint64_t{1} << 30;
 constexpr int kBinCountSmem = (kMaxTiles + 1) * 4;
-constexpr int kBinScatterSmem = 2 * ((kMaxTiles + 1 + 3) & ~3) * 4 + kBinSub * 4;
+constexpr int kBinScatterSmem = 2 * ((kMaxTiles + 1 + 3) & ~3) * 4;
 
 std::uint64_t align256(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
 
@@ -1578,6 +1578,10 @@ fm_status check_mode(const fm_index* index, int mode) {
 }
 }  // namespace
 
+__attribute__((visibility("hidden"))) fm_status query_host_impl(
+    const fm_index* cindex, int mode, const double* h_lonlat, std::uint64_t n, std::int32_t* h_out,
+    std::int64_t* h_hist, std::int64_t* d_hist_accum, fm_query_counters* h_counters);
+
 extern "C" {
 
 fm_status fm_query(const fm_index* index, const double* d_lonlat, std::uint64_t n,
@@ -1618,6 +1622,19 @@ fm_status fm_query_host_mode(const fm_index* cindex, int mode, const double* h_l
 fm_status fm_query_host_counted(const fm_index* cindex, int mode, const double* h_lonlat,
                                 std::uint64_t n, std::int32_t* h_out, std::int64_t* h_hist,
                                 fm_query_counters* h_counters) {
+  return query_host_impl(cindex, mode, h_lonlat, n, h_out, h_hist, nullptr, h_counters);
+}
+
+}  // extern "C"
+
+// The host-buffer pipeline behind fm_query_host*: 8M-point chunks over
+// kStreams streams (H2D copy, fm_query, D2H copy).  The histogram goes to
+// the HOST array h_hist (accumulated into), or -- for the multi-GPU entry
+// (multi.cu) -- stays on the device in d_hist_accum (n_polys int64 on the
+// index's device, accumulated into), so it can be reduced over NCCL there.
+__attribute__((visibility("hidden"))) fm_status query_host_impl(
+    const fm_index* cindex, int mode, const double* h_lonlat, std::uint64_t n, std::int32_t* h_out,
+    std::int64_t* h_hist, std::int64_t* d_hist_accum, fm_query_counters* h_counters) {
   g_err.clear();
   if (!cindex) return set_err(FM_ERR_INVALID_ARGUMENT, "index is null");
   if (check_mode(cindex, mode) != FM_OK) return FM_ERR_INVALID_ARGUMENT;
@@ -1638,8 +1655,8 @@ fm_status fm_query_host_counted(const fm_index* cindex, int mode, const double* 
     }
     index->staged = true;
   }
-  unsigned long long* dh = nullptr;
-  if (h_hist) {
+  unsigned long long* dh = reinterpret_cast<unsigned long long*>(d_hist_accum);
+  if (h_hist && !dh) {
     if (!index->d_hist) FM_CUDA(cudaMalloc(&index->d_hist, std::max<std::uint64_t>(1, index->stats.n_polys) * 8));
     dh = index->d_hist;
     FM_CUDA(cudaMemsetAsync(dh, 0, std::max<std::uint64_t>(1, index->stats.n_polys) * 8, index->streams[0]));
@@ -1666,7 +1683,7 @@ fm_status fm_query_host_counted(const fm_index* cindex, int mode, const double* 
                             index->streams[s]));
   }
   for (int s = 0; s < kStreams; ++s) FM_CUDA(cudaStreamSynchronize(index->streams[s]));
-  if (h_hist) {
+  if (h_hist && !d_hist_accum) {
     std::vector<std::int64_t> tmp(index->stats.n_polys);
     FM_CUDA(cudaMemcpy(tmp.data(), dh, index->stats.n_polys * 8, cudaMemcpyDeviceToHost));
     for (std::uint64_t k = 0; k < index->stats.n_polys; ++k) h_hist[k] += tmp[k];
@@ -1683,6 +1700,8 @@ fm_status fm_query_host_counted(const fm_index* cindex, int mode, const double* 
   }
   return FM_OK;
 }
+
+extern "C" {
 
 // ---------------------------------------------------------------------------
 // Index persistence (the FMCI save/load analogue, cell_index.hpp:641-726):

@@ -404,6 +404,72 @@ def build_index(soup: Soup, params: Optional[CoverParams] = None, device: int = 
     return CellIndex(h, s.n_polys, params, device)
 
 
+class MultiIndex:
+    """Owner of an ``fm_multi*``: one index replica per GPU of this process
+    and the sharded host-buffer query (run_chunked one level up,
+    parallel.hpp:30-82).  ``project`` splits a host batch into contiguous,
+    balanced shards, one per device, and sums the optional histogram with
+    one ncclAllReduce."""
+
+    def __init__(self, soup: Soup, devices: Sequence[int], params: Optional[CoverParams] = None):
+        params = params or CoverParams()
+        validate_cover_params(params)
+        s = soup.contiguous()
+        self._keep = s
+        self.n_leaves = s.n_polys
+        self.devices = [int(d) for d in devices]
+        bp = N.BuildParams(cells_per_polygon=float(params.cells_per_polygon), nx=int(params.nx),
+                           ny=int(params.ny), margin=float(params.margin), device=0,
+                           build_on_gpu=1, threads=int(params.threads),
+                           approx_epsilon=float(params.epsilon) if params.mode == CoverMode.approx
+                           else 0.0)
+        devs = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        self._h = None
+        N.check(N.lib().fm_multi_build(N.ptr(s.vxy, C.c_double), N.ptr(s.ring_off, C.c_uint64),
+                                       s.n_rings, N.ptr(s.poly_ring, C.c_uint64), s.n_polys,
+                                       C.byref(bp), devs, len(self.devices), C.byref(h)),
+                "fm_multi_build")
+        self._h = h
+
+    def __del__(self) -> None:
+        self.close()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            if N is not None:
+                N.lib().fm_multi_destroy(self._h)
+            self._h = None
+
+    def __len__(self) -> int:
+        return N.lib().fm_multi_size(self._h)
+
+    def replica_stats(self, k: int) -> dict:
+        s = N.IndexStats()
+        N.check(N.lib().fm_index_stats_get(N.lib().fm_multi_replica(self._h, int(k)), C.byref(s)),
+                "fm_index_stats_get")
+        return s.as_dict()
+
+    def project(self, points: np.ndarray, out: Optional[np.ndarray] = None,
+                hist: Optional[np.ndarray] = None, mode: "CoverMode" = None) -> np.ndarray:
+        """Leaf id per point of a HOST (n, 2) float64 batch; ``hist`` (int64
+        per leaf) is accumulated into."""
+        if not self._h:
+            raise ValueError("index is closed")
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+        n = pts.shape[0]
+        if out is None:
+            out = np.empty(n, dtype=np.int32)
+        hp = None
+        if hist is not None:
+            assert hist.dtype == np.int64 and hist.flags.c_contiguous and hist.size == self.n_leaves
+            hp = N.ptr(hist, C.c_int64)
+        m = int(CoverMode.exact if mode is None else mode)
+        N.check(N.lib().fm_multi_query_host(self._h, m, N.ptr(pts, C.c_double), n,
+                                            N.ptr(out, C.c_int32), hp), "fm_multi_query_host")
+        return out
+
+
 def load_index(path: str, device: int = 0, params: Optional[CoverParams] = None) -> CellIndex:
     """An index saved by :meth:`CellIndex.save`, onto ``device`` (-1 = host-only)."""
     h = C.c_void_p()

@@ -112,3 +112,12 @@ def test_approx_cover_params_and_resolution():
                                                          epsilon=1e-6), device=-1).stats()
     exact = fastmap.build_index(soup, device=-1).stats()
     assert tiny["approx_epsilon"] == 1e-6 and (tiny["nx"], tiny["ny"]) == (exact["nx"], exact["ny"])
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure")
+def test_multi_gpu_entry_fails_loudly_without_a_device():
+    soup = synth.config("c1").make_soup()
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        fastmap.MultiIndex(soup, [0])
+    with pytest.raises(ValueError):
+        fastmap.MultiIndex(soup, [])
