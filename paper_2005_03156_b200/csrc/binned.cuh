@@ -20,11 +20,11 @@
 //                       tile-major count table (T+1 rows x n_chunks)
 //   (cub exclusive scan of the table in tile-major order: entry (t, c)
 //    becomes the first position of chunk c's points in tile t)
-//   bin_scatter_kernel  the same chunks, in 4K-point sub-chunks held in
-//                       registers: ranks within (sub-chunk, tile) from
-//                       warp-aggregated shared-memory atomics, each point
-//                       written to its tile at the chunk's cursor (pts_b),
-//                       its binned position to pos[i] (coalesced)
+//   bin_scatter_kernel  the same chunks: each point takes the next position
+//                       of its tile's run from a warp-aggregated shared-
+//                       memory atomic on the chunk's cursor, is written
+//                       there (pts_b), and its binned position to pos[i]
+//                       (coalesced)
 //   binned_query_kernel the query over pts_b in order: locate, true hits
 //                       answered at once, boundary points through a
 //                       warp-private shared-memory ring whose batches of 32
@@ -32,10 +32,11 @@
 //                       their evaluation (exactly resolve_kernel's code);
 //                       answers to res[k]
 //   unbin_kernel        out[i] = res[pos[i]]
-// Within a tile, points keep their input order up to the sub-chunk (the
-// reservations are a scan, not atomics), so any window of consecutive input
-// points maps to one contiguous range per tile: the gather in unbin_kernel
-// and the scattered writes in bin_scatter_kernel stay sector-coherent in L2.
+// Within a tile, points keep their input order up to the chunk (the
+// chunks' reservations are a scan; inside a chunk the order is the
+// atomics'), so any window of consecutive input points maps to about one
+// contiguous range per tile: the gather in unbin_kernel and the scattered
+// writes in bin_scatter_kernel stay sector-coherent in L2.
 // Points outside the acceptance box (and NaN) go to one extra bin; the
 // query pass answers them -1 like every other path.
 //
@@ -49,11 +50,7 @@
 
 constexpr int kBinThreads = 512;
 constexpr int kBinPerThread = 8;
-constexpr int kBinSub = kBinThreads * kBinPerThread;   // 4096-point sub-chunks
-constexpr int kBinSubs = 16;
-constexpr std::uint64_t kBinChunk = std::uint64_t{kBinSub} * kBinSubs;  // 64K points
-constexpr int kRankBits = 13;                           // rank <= kBinSub
-static_assert(kBinSub <= (1 << kRankBits), "rank field too narrow");
+constexpr std::uint64_t kBinChunk = std::uint64_t{1} << 16;  // 64K points per table column
 constexpr int kMaxTiles = 4096;                         // keys < kMaxTiles + 1
 
 // Work counters (zeroed per launch): the ordered passes hand out their
@@ -120,21 +117,26 @@ __global__ void __launch_bounds__(kBinThreads)
   }
 }
 
-// The points of a sub-chunk are read once, into registers (kBinPerThread
-// per thread); ranks within (sub-chunk, tile) come from shared-memory
-// atomics aggregated per warp (__match_any_sync: clustered streams put many
-// lanes of a warp into the same hot tile, whose counter would otherwise
-// serialise them), and the points are written from registers once the
-// sub-chunk's counts are known.
-__global__ void __launch_bounds__(kBinThreads, 2)
+// The scatter needs no barrier inside a chunk: each point takes the next
+// position of its tile's run with a shared-memory atomic on the chunk's
+// cursor (s_cur starts at the chunk's scanned table entries, and the
+// chunk's per-tile counts are exactly the table's, so the runs fill
+// [start, start + count) whatever the order).  The atomics are aggregated
+// per warp with __match_any_sync -- clustered streams put many lanes of a
+// warp into the same hot tile, whose counter would otherwise serialise
+// them -- and each thread keeps kBinPerThread points in flight.  Small CTAs
+// (kScatterThreads) so several independent ones share an SM.
+constexpr int kScatterThreads = 256;
+constexpr int kScatterIter = kScatterThreads * kBinPerThread;  // points per CTA iteration
+static_assert(kBinChunk % kScatterIter == 0, "chunk must hold whole iterations");
+
+__global__ void __launch_bounds__(kScatterThreads)
     bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
                        const unsigned int* __restrict__ table, double2* __restrict__ pts_b,
                        unsigned int* __restrict__ pos, unsigned long long* __restrict__ work) {
-  extern __shared__ unsigned int smem[];
+  extern __shared__ unsigned int s_cur[];  // nk: the chunk's cursor per tile
   __shared__ unsigned long long s_grab;
   const int nk = T.n_tiles + 1;
-  unsigned int* s_cur = smem;                      // nk: the chunk's cursor per tile
-  unsigned int* s_hist = smem + ((nk + 3) & ~3);   // nk: per sub-chunk counts
   const int lane = threadIdx.x & 31;
   const unsigned int lt_mask = (1u << lane) - 1u;
   const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
@@ -142,48 +144,33 @@ __global__ void __launch_bounds__(kBinThreads, 2)
        c = cta_grab(work + kCtrScatter, &s_grab)) {
     for (int k = threadIdx.x; k < nk; k += blockDim.x) {
       s_cur[k] = table[static_cast<std::uint64_t>(k) * n_chunks + c];
-      s_hist[k] = 0u;
     }
     __syncthreads();
-    for (int sub = 0; sub < kBinSubs; ++sub) {
-      const std::uint64_t base = c * kBinChunk + static_cast<std::uint64_t>(sub) * kBinSub;
-      if (base >= n) break;
+    const std::uint64_t end = min(n, (c + 1) * kBinChunk);
+    for (std::uint64_t base = c * kBinChunk; base < end; base += kScatterIter) {
       double2 p[kBinPerThread];
-      unsigned int kr[kBinPerThread];
 #pragma unroll
       for (int j = 0; j < kBinPerThread; ++j) {
-        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kBinThreads + threadIdx.x;
-        p[j] = i < n ? __ldcs(pts + i) : make_double2(0.0, 0.0);
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+        p[j] = i < end ? __ldcs(pts + i) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int j = 0; j < kBinPerThread; ++j) {
-        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kBinThreads + threadIdx.x;
-        const bool valid = i < n;
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+        const bool valid = i < end;
         const int key = valid ? tile_key(P, T, p[j].x, p[j].y) : -1;
         const unsigned int peers = __match_any_sync(0xFFFFFFFFu, key);
         const int leader = __ffs(peers) - 1;
-        unsigned int r = 0;
-        if (valid && lane == leader) r = atomicAdd(s_hist + key, static_cast<unsigned int>(__popc(peers)));
-        r = __shfl_sync(0xFFFFFFFFu, r, leader) + __popc(peers & lt_mask);
-        kr[j] = valid ? ((static_cast<unsigned int>(key) << kRankBits) | r) : 0xFFFFFFFFu;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < kBinPerThread; ++j) {
-        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kBinThreads + threadIdx.x;
-        if (kr[j] != 0xFFFFFFFFu) {
-          const unsigned int dst = s_cur[kr[j] >> kRankBits] + (kr[j] & ((1u << kRankBits) - 1u));
+        unsigned int dst = 0;
+        if (valid && lane == leader) dst = atomicAdd(s_cur + key, static_cast<unsigned int>(__popc(peers)));
+        dst = __shfl_sync(0xFFFFFFFFu, dst, leader) + __popc(peers & lt_mask);
+        if (valid) {
           pts_b[dst] = p[j];
           __stcs(pos + i, dst);
         }
       }
-      __syncthreads();
-      for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-        s_cur[k] += s_hist[k];
-        s_hist[k] = 0u;
-      }
-      __syncthreads();
     }
+    __syncthreads();  // s_cur is reloaded for the next chunk
   }
 }
 
@@ -358,7 +345,13 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
 // increasing order from the work counter, four points per thread per round
 // (16-byte pos loads and id stores when `out` is 16-byte aligned).
 constexpr int kUnbinThreads = 256;
-constexpr int kUnbinRounds = 8;
+#ifndef FM_UNBIN_ROUNDS
+#define FM_UNBIN_ROUNDS 8
+#endif
+constexpr int kUnbinRounds = FM_UNBIN_ROUNDS;
+#ifndef FM_UNBIN_LD
+#define FM_UNBIN_LD __ldg
+#endif
 constexpr std::uint64_t kUnbinBlock = 4ull * kUnbinThreads * kUnbinRounds;  // 8192 points
 
 __global__ void __launch_bounds__(kUnbinThreads)
@@ -383,10 +376,10 @@ __global__ void __launch_bounds__(kUnbinThreads)
       int4 v[kUnbinRounds];
 #pragma unroll
       for (int r = 0; r < kUnbinRounds; ++r) {
-        v[r].x = __ldg(res + k[r].x);
-        v[r].y = __ldg(res + k[r].y);
-        v[r].z = __ldg(res + k[r].z);
-        v[r].w = __ldg(res + k[r].w);
+        v[r].x = FM_UNBIN_LD(res + k[r].x);
+        v[r].y = FM_UNBIN_LD(res + k[r].y);
+        v[r].z = FM_UNBIN_LD(res + k[r].z);
+        v[r].w = FM_UNBIN_LD(res + k[r].w);
       }
 #pragma unroll
       for (int r = 0; r < kUnbinRounds; ++r) {

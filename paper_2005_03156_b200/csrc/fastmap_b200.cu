@@ -920,7 +920,7 @@ fm_status launch_t(const fm_index* ix, const double2* pts, std::uint64_t n, int*
 // The binned path (binned.cuh) over one batch of n <= kBinnedBatch points.
 constexpr std::uint64_t kBinnedBatch = std::uint64_t{1} << 30;
 constexpr int kBinCountSmem = (kMaxTiles + 1) * 4;
-constexpr int kBinScatterSmem = 2 * ((kMaxTiles + 1 + 3) & ~3) * 4;
+constexpr int kBinScatterSmem = (kMaxTiles + 1) * 4;
 
 std::uint64_t align256(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
 
@@ -962,8 +962,8 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
                                         static_cast<std::int64_t>(n_tab), stream));
   auto ks = bin_scatter_kernel;
   const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      n_chunks, resident_blocks(ix->device, (const void*)ks, kBinThreads, kBinScatterSmem))));
-  ks<<<grid_s, kBinThreads, kBinScatterSmem, stream>>>(P, T, pts, n, starts, pts_b, pos, work);
+      n_chunks, resident_blocks(ix->device, (const void*)ks, kScatterThreads, kBinScatterSmem))));
+  ks<<<grid_s, kScatterThreads, kBinScatterSmem, stream>>>(P, T, pts, n, starts, pts_b, pos, work);
   auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<kHist, kCount, 0>
                               : binned_query_kernel<kHist, kCount, -1>;
   const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);

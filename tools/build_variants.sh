@@ -9,7 +9,7 @@ for v in "$@"; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 \
     $F -Xcompiler -fPIC,-O3,-ffp-contract=off,-pthread -shared \
     paper_2005_03156_b200/csrc/fastmap_b200.cu paper_2005_03156_b200/csrc/index_gpu.cu paper_2005_03156_b200/csrc/index_host.cpp \
-    paper_2005_03156_b200/csrc/io.cpp paper_2005_03156_b200/csrc/simple.cu \
+    paper_2005_03156_b200/csrc/io.cpp paper_2005_03156_b200/csrc/simple.cu paper_2005_03156_b200/csrc/multi.cu \
     -o paper_2005_03156_b200/_lib/var/lib_$N.so -Xptxas -v 2> paper_2005_03156_b200/_lib/var/ptxas_$N.log &
 done
 wait
