@@ -120,6 +120,7 @@ typedef struct fm_index_stats {
   uint64_t query_grid_bytes;  /* query-side folded copy of the grid (blocks + sub-blocks) */
   int32_t query_block_log2;   /* its block side, log2 cells (0 = the flat grid itself) */
   int32_t approx_block_log2;  /* same for the approx cover */
+  uint64_t slots_double;      /* 256-byte double leaf slots (polygon corners) */
 } fm_index_stats;
 
 /* Optional per-call work counters (diagnostics; device-side atomics). */

@@ -64,7 +64,7 @@ class IndexStats(C.Structure):
         ("cells_split", u64), ("slots_phase1", u64), ("slots_total", u64),
         ("approx_epsilon", C.c_double), ("approx_grid_bytes", u64),
         ("query_grid_bytes", u64), ("query_block_log2", C.c_int32),
-        ("approx_block_log2", C.c_int32),
+        ("approx_block_log2", C.c_int32), ("slots_double", u64),
     ]
 
     def as_dict(self) -> dict:

@@ -14,17 +14,16 @@
 // (stream_kernel + resolve_kernel) stays the choice for small or mostly
 // true-hit indexes (c1, c2) -- see choose_path() in fastmap_b200.cu.
 //
-// Four launches per batch of n <= 2^30 points:
-//   bin_count_kernel    one CTA per 64K-point *chunk*: a shared-memory
-//                       histogram of tile keys, stored as column c of the
-//                       tile-major count table (T+1 rows x n_chunks)
-//   (cub exclusive scan of the table in tile-major order: entry (t, c)
-//    becomes the first position of chunk c's points in tile t)
-//   bin_scatter_kernel  the same chunks: each point takes the next position
-//                       of its tile's run from a warp-aggregated shared-
-//                       memory atomic on the chunk's cursor, is written
-//                       there (pts_b), and its binned position to pos[i]
-//                       (coalesced)
+// Five launches per batch of n <= 2^30 points:
+//   bin_count_kernel    one CTA per 64K-point chunk: a shared-memory
+//                       histogram of tile keys added into per-tile totals
+//   bin_scan_kernel     one CTA: the totals' exclusive scan = each tile's
+//                       first binned position (its cursor)
+//   bin_scatter_kernel  2K-point sub-chunks held in registers: ranks within
+//                       (sub-chunk, tile) from warp-aggregated shared-memory
+//                       atomics, one run per touched tile reserved from the
+//                       tile's global cursor, each point written to its run
+//                       (pts_b) and its binned position to pos[i] (coalesced)
 //   binned_query_kernel the query over pts_b in order: locate, true hits
 //                       answered at once, boundary points through a
 //                       warp-private shared-memory ring whose batches of 32
@@ -32,11 +31,11 @@
 //                       their evaluation (exactly resolve_kernel's code);
 //                       answers to res[k]
 //   unbin_kernel        out[i] = res[pos[i]]
-// Within a tile, points keep their input order up to the chunk (the
-// chunks' reservations are a scan; inside a chunk the order is the
-// atomics'), so any window of consecutive input points maps to about one
-// contiguous range per tile: the gather in unbin_kernel and the scattered
-// writes in bin_scatter_kernel stay sector-coherent in L2.
+// Sub-chunks are taken in increasing order, so within a tile the points
+// stay in about input order and any window of consecutive input points maps
+// to about one contiguous range per tile: the gather in unbin_kernel and
+// the scattered writes in bin_scatter_kernel (n_tiles write fronts) stay
+// sector-coherent in L2.
 // Points outside the acceptance box (and NaN) go to one extra bin; the
 // query pass answers them -1 like every other path.
 //
@@ -50,7 +49,7 @@
 
 constexpr int kBinThreads = 512;
 constexpr int kBinPerThread = 8;
-constexpr std::uint64_t kBinChunk = std::uint64_t{1} << 16;  // 64K points per table column
+constexpr std::uint64_t kBinChunk = std::uint64_t{1} << 16;  // 64K points per counting CTA
 constexpr int kMaxTiles = 4096;                         // keys < kMaxTiles + 1
 
 // Work counters (zeroed per launch): the ordered passes hand out their
@@ -85,10 +84,11 @@ __device__ __forceinline__ int tile_key(const fm::KParams& P, const TileGeom& T,
   return in ? (iy >> T.ts) * T.tnx + (ix >> T.ts) : T.n_tiles;
 }
 
-// table[t * n_chunks + c] = points of chunk c in tile t
+// counts[t] += points of tile t (one CTA per 64K-point chunk: a shared-
+// memory histogram, then one global atomic per non-empty bin)
 __global__ void __launch_bounds__(kBinThreads)
     bin_count_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                     unsigned int* __restrict__ table) {
+                     unsigned int* __restrict__ counts) {
   extern __shared__ unsigned int s_hist[];
   const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
   for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
@@ -111,66 +111,115 @@ __global__ void __launch_bounds__(kBinThreads)
     }
     __syncthreads();
     for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) {
-      table[static_cast<std::uint64_t>(k) * n_chunks + c] = s_hist[k];
+      if (s_hist[k]) atomicAdd(counts + k, s_hist[k]);
     }
     __syncthreads();
   }
 }
 
-// The scatter needs no barrier inside a chunk: each point takes the next
-// position of its tile's run with a shared-memory atomic on the chunk's
-// cursor (s_cur starts at the chunk's scanned table entries, and the
-// chunk's per-tile counts are exactly the table's, so the runs fill
-// [start, start + count) whatever the order).  The atomics are aggregated
-// per warp with __match_any_sync -- clustered streams put many lanes of a
-// warp into the same hot tile, whose counter would otherwise serialise
-// them -- and each thread keeps kBinPerThread points in flight.  Small CTAs
-// (kScatterThreads) so several independent ones share an SM.
+// cursor[t] = first binned position of tile t (exclusive scan of counts,
+// n_tiles + 1 <= kMaxTiles + 1 entries: one CTA)
+__global__ void __launch_bounds__(1024) bin_scan_kernel(const unsigned int* __restrict__ counts, int nk,
+                                                        unsigned int* __restrict__ cursor) {
+  __shared__ unsigned int s_part[1024];
+  constexpr int kPer = (kMaxTiles + 1 + 1023) / 1024;
+  unsigned int v[kPer], sum = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int k = threadIdx.x * kPer + j;
+    v[j] = k < nk ? counts[k] : 0u;
+    sum += v[j];
+  }
+  s_part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan of the partial sums
+    const unsigned int x = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0u;
+    __syncthreads();
+    s_part[threadIdx.x] += x;
+    __syncthreads();
+  }
+  unsigned int run = threadIdx.x ? s_part[threadIdx.x - 1] : 0u;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int k = threadIdx.x * kPer + j;
+    if (k < nk) cursor[k] = run;
+    run += v[j];
+  }
+}
+
+// The scatter.  A CTA takes sub-chunks of kScatterIter consecutive points
+// (in increasing order from the work counter), ranks each point within
+// (sub-chunk, tile) with warp-aggregated shared-memory atomics
+// (__match_any_sync: clustered streams put many lanes of a warp into the
+// same hot tile), reserves one run per touched tile from the tile's global
+// cursor, and writes every point to its run.  With one cursor per tile the
+// writes of the whole grid advance through just n_tiles fronts, so L2
+// assembles them into whole lines before they reach DRAM; and a tile's
+// points stay in about input order (runs are reserved in sub-chunk order).
 constexpr int kScatterThreads = 256;
-constexpr int kScatterIter = kScatterThreads * kBinPerThread;  // points per CTA iteration
-static_assert(kBinChunk % kScatterIter == 0, "chunk must hold whole iterations");
+constexpr int kScatterIter = kScatterThreads * kBinPerThread;  // 2048 points
+constexpr int kScatterSmem = 3 * (kMaxTiles + 1) * 4;
 
 __global__ void __launch_bounds__(kScatterThreads)
     bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                       const unsigned int* __restrict__ table, double2* __restrict__ pts_b,
+                       unsigned int* __restrict__ cursor, double2* __restrict__ pts_b,
                        unsigned int* __restrict__ pos, unsigned long long* __restrict__ work) {
-  extern __shared__ unsigned int s_cur[];  // nk: the chunk's cursor per tile
+  extern __shared__ unsigned int smem[];
   __shared__ unsigned long long s_grab;
+  __shared__ int s_nt;
   const int nk = T.n_tiles + 1;
+  unsigned int* s_cnt = smem;                     // per-tile count of this sub-chunk
+  unsigned int* s_base = smem + (kMaxTiles + 1);  // its reserved run
+  unsigned int* s_list = smem + 2 * (kMaxTiles + 1);  // tiles touched
   const int lane = threadIdx.x & 31;
   const unsigned int lt_mask = (1u << lane) - 1u;
-  const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
-  for (std::uint64_t c = cta_grab(work + kCtrScatter, &s_grab); c < n_chunks;
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
+  if (threadIdx.x == 0) s_nt = 0;
+  const std::uint64_t n_iter = (n + kScatterIter - 1) / kScatterIter;
+  for (std::uint64_t c = cta_grab(work + kCtrScatter, &s_grab); c < n_iter;
        c = cta_grab(work + kCtrScatter, &s_grab)) {
-    for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-      s_cur[k] = table[static_cast<std::uint64_t>(k) * n_chunks + c];
+    const std::uint64_t base = c * kScatterIter;
+    double2 p[kBinPerThread];
+    unsigned int kr[kBinPerThread];
+#pragma unroll
+    for (int j = 0; j < kBinPerThread; ++j) {
+      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+      p[j] = i < n ? __ldcs(pts + i) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < kBinPerThread; ++j) {
+      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+      const bool valid = i < n;
+      const int key = valid ? tile_key(P, T, p[j].x, p[j].y) : -1;
+      const unsigned int peers = __match_any_sync(0xFFFFFFFFu, key);
+      const int leader = __ffs(peers) - 1;
+      unsigned int r = 0;
+      if (valid && lane == leader) {
+        r = atomicAdd(s_cnt + key, static_cast<unsigned int>(__popc(peers)));
+        if (r == 0u) s_list[atomicAdd(&s_nt, 1)] = static_cast<unsigned int>(key);
+      }
+      r = __shfl_sync(0xFFFFFFFFu, r, leader) + __popc(peers & lt_mask);
+      kr[j] = valid ? ((static_cast<unsigned int>(key) << 16) | r) : 0xFFFFFFFFu;
     }
     __syncthreads();
-    const std::uint64_t end = min(n, (c + 1) * kBinChunk);
-    for (std::uint64_t base = c * kBinChunk; base < end; base += kScatterIter) {
-      double2 p[kBinPerThread];
+    const int nt = s_nt;
+    for (int q = threadIdx.x; q < nt; q += blockDim.x) {
+      const unsigned int t = s_list[q];
+      s_base[t] = atomicAdd(cursor + t, s_cnt[t]);
+    }
+    __syncthreads();
 #pragma unroll
-      for (int j = 0; j < kBinPerThread; ++j) {
-        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-        p[j] = i < end ? __ldcs(pts + i) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int j = 0; j < kBinPerThread; ++j) {
-        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-        const bool valid = i < end;
-        const int key = valid ? tile_key(P, T, p[j].x, p[j].y) : -1;
-        const unsigned int peers = __match_any_sync(0xFFFFFFFFu, key);
-        const int leader = __ffs(peers) - 1;
-        unsigned int dst = 0;
-        if (valid && lane == leader) dst = atomicAdd(s_cur + key, static_cast<unsigned int>(__popc(peers)));
-        dst = __shfl_sync(0xFFFFFFFFu, dst, leader) + __popc(peers & lt_mask);
-        if (valid) {
-          pts_b[dst] = p[j];
-          __stcs(pos + i, dst);
-        }
+    for (int j = 0; j < kBinPerThread; ++j) {
+      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+      if (kr[j] != 0xFFFFFFFFu) {
+        const unsigned int dst = s_base[kr[j] >> 16] + (kr[j] & 0xFFFFu);
+        pts_b[dst] = p[j];
+        __stcs(pos + i, dst);
       }
     }
-    __syncthreads();  // s_cur is reloaded for the next chunk
+    for (int q = threadIdx.x; q < nt; q += blockDim.x) s_cnt[s_list[q]] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) s_nt = 0;
   }
 }
 

@@ -331,6 +331,11 @@ __device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const
     if (kind == fm::kSlotLeaf) {
       if (kCount) wc.boundary++;
       id = fm::eval_leaf_slot<kCount>(c, it.px, it.py, wc);
+    } else if (kind == fm::kSlotDouble) {  // second half from global memory
+      if (kCount) wc.boundary++;
+      uint4 b[8];
+      fm::load_double_tail(P, it.e, b);
+      id = fm::eval_double_slot<kCount>(c, b, it.px, it.py, wc);
     } else if (kind == fm::kSlotSplit) {
       const double x0 = fm::as_f64(c[0].z, c[0].w), y0 = fm::as_f64(c[1].x, c[1].y);
       const double ihw = fm::as_f64(c[1].z, c[1].w), ihh = fm::as_f64(c[2].x, c[2].y);
@@ -348,9 +353,10 @@ __device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const
         requeue = ce;
         done = false;
       }
-    } else {  // overflow record (past the split depth): from global memory
+    } else {  // overflow record: its offset is in the staged slot, the record in global memory
       if (kCount) wc.boundary++;
-      id = fm::resolve_slot_global<kCount>(P, it.e, it.px, it.py, wc);
+      id = fm::resolve_overflow<kCount>(P, (static_cast<std::uint64_t>(c[0].w) << 32) | c[0].z, it.px,
+                                        it.py, wc);
     }
     if (done) emit<kHist>(out, hist, it.i, id);
   }
@@ -920,7 +926,6 @@ fm_status launch_t(const fm_index* ix, const double2* pts, std::uint64_t n, int*
 // The binned path (binned.cuh) over one batch of n <= kBinnedBatch points.
 constexpr std::uint64_t kBinnedBatch = std::uint64_t{1} << 30;
 constexpr int kBinCountSmem = (kMaxTiles + 1) * 4;
-constexpr int kBinScatterSmem = (kMaxTiles + 1) * 4;
 
 std::uint64_t align256(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
 
@@ -930,40 +935,35 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   const fm::KParams P = kparams(ix);
   const TileGeom& T = ix->tiles;
   const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
-  const std::uint64_t n_tab = static_cast<std::uint64_t>(T.n_tiles + 1) * n_chunks;
-  std::size_t cub_bytes = 0;
-  FM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, static_cast<unsigned int*>(nullptr),
-                                        static_cast<unsigned int*>(nullptr),
-                                        static_cast<std::int64_t>(n_tab), stream));
-  // scratch: the (tile x chunk) count table and its scan, scan temp, binned
-  // points, binned positions, binned answers (24 B per point)
+  const int nk = T.n_tiles + 1;
+  // scratch: work counters, per-tile counts and cursors, binned points,
+  // binned positions, binned answers (24 B per point)
   const std::uint64_t o_work = 0;
-  const std::uint64_t o_tab = 256;
-  const std::uint64_t o_scan = o_tab + align256(4 * n_tab);
-  const std::uint64_t o_tmp = o_scan + align256(4 * n_tab);
-  const std::uint64_t o_pts = o_tmp + align256(cub_bytes + 16);
+  const std::uint64_t o_cnt = 256;
+  const std::uint64_t o_cur = o_cnt + align256(4ull * nk);
+  const std::uint64_t o_pts = o_cur + align256(4ull * nk);
   const std::uint64_t o_pos = o_pts + align256(16 * n);
   const std::uint64_t o_res = o_pos + align256(4 * n);
   const std::uint64_t total = o_res + align256(4 * n);
   char* scratch = nullptr;
   FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), total, stream));
   unsigned long long* work = reinterpret_cast<unsigned long long*>(scratch + o_work);
-  unsigned int* table = reinterpret_cast<unsigned int*>(scratch + o_tab);
-  FM_CUDA(cudaMemsetAsync(work, 0, 8 * kCtrCount, stream));
-  unsigned int* starts = reinterpret_cast<unsigned int*>(scratch + o_scan);
+  unsigned int* counts = reinterpret_cast<unsigned int*>(scratch + o_cnt);
+  unsigned int* cursor = reinterpret_cast<unsigned int*>(scratch + o_cur);
+  FM_CUDA(cudaMemsetAsync(scratch, 0, o_cur, stream));  // work counters + counts
   double2* pts_b = reinterpret_cast<double2*>(scratch + o_pts);
   unsigned int* pos = reinterpret_cast<unsigned int*>(scratch + o_pos);
   int* res = reinterpret_cast<int*>(scratch + o_res);
   auto kc = bin_count_kernel;
   const int grid_c = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       n_chunks, resident_blocks(ix->device, (const void*)kc, kBinThreads, kBinCountSmem))));
-  kc<<<grid_c, kBinThreads, kBinCountSmem, stream>>>(P, T, pts, n, table);
-  FM_CUDA(cub::DeviceScan::ExclusiveSum(scratch + o_tmp, cub_bytes, table, starts,
-                                        static_cast<std::int64_t>(n_tab), stream));
+  kc<<<grid_c, kBinThreads, kBinCountSmem, stream>>>(P, T, pts, n, counts);
+  bin_scan_kernel<<<1, 1024, 0, stream>>>(counts, nk, cursor);
   auto ks = bin_scatter_kernel;
+  const std::uint64_t n_iter = (n + kScatterIter - 1) / kScatterIter;
   const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      n_chunks, resident_blocks(ix->device, (const void*)ks, kScatterThreads, kBinScatterSmem))));
-  ks<<<grid_s, kScatterThreads, kBinScatterSmem, stream>>>(P, T, pts, n, starts, pts_b, pos, work);
+      n_iter, resident_blocks(ix->device, (const void*)ks, kScatterThreads, kScatterSmem))));
+  ks<<<grid_s, kScatterThreads, kScatterSmem, stream>>>(P, T, pts, n, cursor, pts_b, pos, work);
   auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<kHist, kCount, 0>
                               : binned_query_kernel<kHist, kCount, -1>;
   const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);
@@ -1492,6 +1492,7 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   s.arena_bytes = ix->host.n_slots * fm::kSlotBytes + (ix->overflow_len - 512);
   s.built_on_gpu = on_gpu ? 1 : 0;
   s.cells_split = ix->host.stats.cells_split;
+  s.slots_double = ix->host.stats.slots_double;
   s.slots_phase1 = ix->host.n_phase1_slots;
   s.slots_total = ix->host.n_slots;
   s.geometry_bytes = s.n_vertices * 16;

@@ -35,6 +35,7 @@ struct BuildStats {
   std::uint64_t records = 0;      // leaf slots + overflow records
   std::uint64_t records_overflow = 0;
   std::uint64_t cells_split = 0;  // split records (2x2 sub-cell nodes)
+  std::uint64_t slots_double = 0; // double leaf slots (kind 4, 256 bytes)
   // fast-approx epsilon finer than a uniform grid of <= 2^31 cells can
   // resolve: the grid is planned as for an exact index and approximate
   // queries are answered exactly (error 0 <= epsilon)

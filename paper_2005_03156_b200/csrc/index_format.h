@@ -41,6 +41,19 @@
 //   Edge i joins vertex i and i+1 unless bit i+1 of chain_mask is set; it
 //   is oriented exactly like the reference (lo = lower latitude,
 //   geometry.hpp:219), which reproduces its (lo, hi) bit for bit.
+//  kind 4, double leaf (256 bytes: slots k and k+1; the entry names k and
+//   is never half) -- a cell that fits no leaf slot but <= 8 candidates,
+//   <= 4 breakpoints and <= 10 chain vertices (typically a polygon corner:
+//   3-4 leaves and their chains meeting at one vertex):
+//   +0   u8 kind=4, u8 n_verts, u8 n_cands, u8 n_breaks
+//   +4   u32 chain_mask
+//   +8   i32 leaf[0..7]
+//   +40  u16 edge_mask[0..7]
+//   +56  u8 info[0..7]            bit 7 = c0, bits 0..3 = break mask
+//   +64  f64 break[0..3]
+//   +96  {f64 lon, f64 lat} vert[0..9]
+//   The query stages the first 128 bytes like any slot and loads the
+//   second (vert[2..9]) from global memory.
 //  kind 3, split: a cell whose content does not fit one slot is split 2x2
 //   (recursively, up to kMaxSplitDepth levels):
 //   +8   f64 x0, f64 y0          lower-left corner of the split cell
@@ -48,7 +61,8 @@
 //   +40  u32 child[4]            grid-format entries, index 2*j + i
 //   Child (i, j) covers [x0 + i*hw, x0 + (i+1)*hw] x [y0 + j*hh, ...]; a
 //   point goes to i = clamp(int((lon - x0) * inv_hw), 0, 1) (same for j).
-//  kind 2, overflow (past the split depth): +8 u64 byte offset of a
+//  kind 2, overflow (a cell whose compact record is <= kSmallRecordBytes,
+//   or past the split depth): +8 u64 byte offset of a
 //   variable-size record in the overflow arena, one of
 //   compact (kind 1, fits when n_verts <= 32, n_cands <= 15, n_breaks <= 7):
 //     +0   u8 kind=1, u8 n_verts, u8 n_cands, u8 n_breaks
@@ -95,21 +109,30 @@ constexpr std::uint32_t kMaxBreaksPerCand = 0x7FFFu;
 constexpr std::uint8_t kSlotLeaf = 1;
 constexpr std::uint8_t kSlotOverflow = 2;
 constexpr std::uint8_t kSlotSplit = 3;
+constexpr std::uint8_t kSlotDouble = 4;
+constexpr std::uint32_t kDblMaxCands = 8;
+constexpr std::uint32_t kDblMaxBreaks = 4;
+constexpr std::uint32_t kDblMaxVerts = 10;
 constexpr std::uint64_t kSlotBytes = 128;
 constexpr std::uint32_t kSlotMaxCands = 4;
 constexpr std::uint32_t kSlotMaxBreaks = 2;
 constexpr std::uint32_t kSlotMaxVerts = 5;
 constexpr int kMaxSplitDepth = 6;
+// A boundary cell that does not fit one slot but whose compact record is at
+// most this many bytes gets that record (overflow slot) instead of a split.
+constexpr std::uint64_t kSmallRecordBytes = 256;
 
 // Grid/child entry of slot k: split and overflow slots use only their first
 // 64 bytes; so does a leaf slot with <= 2 candidates and either <= 2
-// vertices and <= 1 breakpoint or 3 vertices and none (the layout above).
+// vertices and <= 1 breakpoint or 3 vertices and none (the layout above);
+// a double slot never does.
 FM_HD bool leaf_slot_half(std::uint32_t nv, std::uint32_t nc, std::uint32_t nb) {
   return nc <= 2 && ((nv <= 2 && nb <= 1) || (nv == 3 && nb == 0));
 }
 FM_HD std::uint32_t slot_entry(std::uint64_t k, std::uint32_t kind, std::uint32_t nv,
                                std::uint32_t nc, std::uint32_t nb) {
-  const bool half = kind != kSlotLeaf || leaf_slot_half(nv, nc, nb);
+  const bool half = kind == kSlotSplit || kind == kSlotOverflow ||
+                    (kind == kSlotLeaf && leaf_slot_half(nv, nc, nb));
   return kRecordBit | (half ? kHalfBit : 0u) | static_cast<std::uint32_t>(k);
 }
 // same, from the slot's first 4 bytes (u8 kind, nv, nc, nb)

@@ -732,6 +732,7 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
     out.stats.records += st2.records;
     out.stats.records_overflow += st2.records_overflow;
     out.stats.cells_split += st2.cells_split;
+    out.stats.slots_double += st2.slots_double;
     out.stats.records_compact += st2.records_compact;
     out.stats.records_wide += st2.records_wide;
     std::vector<std::uint32_t> vals(nd);

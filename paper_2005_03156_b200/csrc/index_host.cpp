@@ -287,7 +287,24 @@ struct RowWorker {
       *deferred = true;
       return kEmpty;
     }
-    if (depth < kMaxSplitDepth && cw > 256.0 * g.margin && chh > 256.0 * g.margin) {
+    std::uint8_t dbl[2 * kSlotBytes];
+    if (encode_double_slot(used, cin, dbl)) {  // e.g. a polygon corner: two slots, one read
+      const std::uint64_t k = slots.size() / kSlotBytes;
+      slots.insert(slots.end(), dbl, dbl + 2 * kSlotBytes);
+      note_leaf(used.size(), cin.size(), n_breaks);
+      es.compact++;
+      st.slots_double++;
+      return slot_entry(k, kSlotDouble, 0, 0, 0);
+    }
+    // A cell that fits neither a slot nor a double slot but a small compact
+    // record takes the record (an overflow slot pointing at it) rather than
+    // a split subtree: splitting recurses to kMaxSplitDepth around any
+    // vertex where several chains meet (every child holding it is as full),
+    // which is how c3's 12.5M corner cells once took 83M split nodes and
+    // 270M of its 352M slots.
+    const std::uint64_t rec_bytes = compact_record_bytes(used, cin);
+    const bool small_record = rec_bytes > 0 && rec_bytes <= kSmallRecordBytes;
+    if (!small_record && depth < kMaxSplitDepth && cw > 256.0 * g.margin && chh > 256.0 * g.margin) {
       // split 2x2: child (i, j) covers [rx0 + i*cw/2, rx0 + (i+1)*cw/2] x ...
       const double hw = 0.5 * cw, hh = 0.5 * chh;
       std::uint32_t child[4];
@@ -676,6 +693,7 @@ void merge_stats(BuildStats& into, const BuildStats& st) {
   into.records += st.records;
   into.records_overflow += st.records_overflow;
   into.cells_split += st.cells_split;
+  into.slots_double += st.slots_double;
 }
 
 }  // namespace

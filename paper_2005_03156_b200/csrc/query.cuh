@@ -284,6 +284,67 @@ __device__ __forceinline__ int eval_leaf_slot(const uint4 (&c)[8], double px, do
   return id;
 }
 
+// Double leaf slot (index_format.h, kind 4): a[] = its first 128 bytes (as
+// staged), b[] = the second (vert[2..9]).  Static offsets, predicated like
+// eval_leaf_slot.
+template <bool kCount>
+__device__ __forceinline__ int eval_double_slot(const uint4 (&a)[8], const uint4 (&b)[8], double px,
+                                                double py, WorkCount& wc) {
+  const std::uint32_t h = a[0].x;
+  const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
+  const std::uint32_t chain = a[0].y;
+  double vx[kDblMaxVerts], vy[kDblMaxVerts];
+#pragma unroll
+  for (int k = 0; k < static_cast<int>(kDblMaxVerts); ++k) {
+    const uint4 v = k < 2 ? a[6 + k] : b[k - 2];
+    vx[k] = as_f64(v.x, v.y);
+    vy[k] = as_f64(v.z, v.w);
+  }
+  std::uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k + 1 < static_cast<int>(kDblMaxVerts); ++k) {
+    if (static_cast<std::uint32_t>(k + 1) < nv && !((chain >> (k + 1)) & 1u)) {
+      if (kCount) wc.edges++;
+      m |= edge_bit(px, py, vx[k], vy[k], vx[k + 1], vy[k + 1]) << k;
+    }
+  }
+  const double br[4] = {as_f64(a[4].x, a[4].y), as_f64(a[4].z, a[4].w), as_f64(a[5].x, a[5].y),
+                        as_f64(a[5].z, a[5].w)};
+  std::uint32_t bm = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bm |= (static_cast<std::uint32_t>(j) < nb && py > br[j]) ? (1u << j) : 0u;
+  const std::uint32_t ids[8] = {a[0].z, a[0].w, a[1].x, a[1].y, a[1].z, a[1].w, a[2].x, a[2].y};
+  const std::uint32_t mk2[4] = {a[2].z, a[2].w, a[3].x, a[3].y};  // u16 edge masks, two per word
+  int id = -1;
+#pragma unroll
+  for (int q = 7; q >= 0; --q) {  // descending, so the smallest odd candidate wins
+    const std::uint32_t mk = (mk2[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+    const std::uint32_t inf = ((q < 4 ? a[3].z : a[3].w) >> (8 * (q & 3))) & 0xFFu;
+    const std::uint32_t par = (inf >> 7) ^ __popc(m & mk) ^ __popc(bm & inf & 15u);
+    if (static_cast<std::uint32_t>(q) < nc && (par & 1u)) id = static_cast<int>(ids[q]);
+  }
+  if (kCount) wc.cands += nc;
+  return id;
+}
+
+// The second half of double slot `e` from global memory.
+__device__ __forceinline__ void load_double_tail(const KParams& P, std::uint32_t e, uint4 (&b)[8]) {
+  const uint4* g = reinterpret_cast<const uint4*>(slot_ptr(P, e) + kSlotBytes);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) b[k] = __ldg(g + k);
+}
+
+// An overflow record (compact or wide) at byte offset `off` of the overflow
+// arena, evaluated from global memory.
+template <bool kCount>
+__device__ __noinline__ int resolve_overflow(const KParams& P, std::uint64_t off, double px, double py,
+                                             WorkCount& wc) {
+  const std::uint8_t* rec = P.overflow + off;
+  const std::uint32_t h = __ldg(reinterpret_cast<const std::uint32_t*>(rec));
+  if ((h & 0xFFu) == kKindCompact) return resolve_compact<kCount>(GlobalReader{rec}, h, px, py, wc);
+  return resolve_wide<kCount>(rec, px, py, wc);
+}
+
 // A boundary slot fetched straight from global memory (split descents and
 // overflow records; rare).
 template <bool kCount>
@@ -296,12 +357,13 @@ __device__ __noinline__ int resolve_slot_global(const KParams& P, std::uint32_t 
     for (int k = 0; k < 8; ++k) c[k] = __ldg(g + k);
     const std::uint32_t kind = c[0].x & 0xFFu;
     if (kind == kSlotLeaf) return eval_leaf_slot<kCount>(c, px, py, wc);
+    if (kind == kSlotDouble) {
+      uint4 b[8];
+      load_double_tail(P, e, b);
+      return eval_double_slot<kCount>(c, b, px, py, wc);
+    }
     if (kind == kSlotOverflow) {
-      const std::uint64_t off = (static_cast<std::uint64_t>(c[0].w) << 32) | c[0].z;
-      const std::uint8_t* rec = P.overflow + off;
-      const std::uint32_t h = __ldg(reinterpret_cast<const std::uint32_t*>(rec));
-      if ((h & 0xFFu) == kKindCompact) return resolve_compact<kCount>(GlobalReader{rec}, h, px, py, wc);
-      return resolve_wide<kCount>(rec, px, py, wc);
+      return resolve_overflow<kCount>(P, (static_cast<std::uint64_t>(c[0].w) << 32) | c[0].z, px, py, wc);
     }
     // split
     const double x0 = as_f64(c[0].z, c[0].w), y0 = as_f64(c[1].x, c[1].y);
@@ -337,7 +399,7 @@ static __device__ __noinline__ std::uint32_t min_leaf_of_entry(const KParams& P,
     const std::uint8_t* s = slot_ptr(P, x);
     const std::uint32_t h = __ldg(reinterpret_cast<const std::uint32_t*>(s));
     const std::uint32_t kind = h & 0xFFu;
-    if (kind == kSlotLeaf) {
+    if (kind == kSlotLeaf || kind == kSlotDouble) {  // first candidate at +8 in both
       if ((h >> 16) & 0xFFu) best = min(best, __ldg(reinterpret_cast<const std::uint32_t*>(s + 8)));
     } else if (kind == kSlotSplit) {
       for (int k = 0; k < 4 && sp < static_cast<int>(sizeof(stack) / 4); ++k) {

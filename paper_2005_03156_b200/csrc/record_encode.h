@@ -175,6 +175,25 @@ inline std::uint64_t encode_record(const std::vector<Edge4>& E, const std::vecto
   return off;
 }
 
+// Bytes of the compact record encode_record would write for this content
+// (compact_bytes), or 0 when it would need the wide format.
+inline std::uint64_t compact_record_bytes(const std::vector<Edge4>& E, const std::vector<CandIn>& C) {
+  if (C.size() > kCompactMaxCands) return 0;
+  std::vector<double> ub;
+  for (const auto& c : C) {
+    for (double b : c.breaks) {
+      if (std::find(ub.begin(), ub.end(), b) == ub.end()) ub.push_back(b);
+    }
+  }
+  if (ub.size() > kCompactMaxBreaks) return 0;
+  std::vector<double> vx, vy;
+  std::uint32_t chain_mask = 0;
+  std::vector<std::uint32_t> bit_of;
+  if (!detail::chain_edges(E, vx, vy, chain_mask, bit_of, kCompactMaxVerts)) return 0;
+  return compact_bytes(static_cast<std::uint32_t>(vx.size()), static_cast<std::uint32_t>(C.size()),
+                       static_cast<std::uint32_t>(ub.size()));
+}
+
 // Encodes a leaf slot (index_format.h, kind 1) into out[128] if the cell's
 // content fits one slot; returns false otherwise.
 inline bool encode_slot(const std::vector<Edge4>& E, const std::vector<CandIn>& C,
@@ -220,6 +239,49 @@ inline bool encode_slot(const std::vector<Edge4>& E, const std::vector<CandIn>& 
     const std::size_t o = k < 3 ? 16 + 16 * k : 96 + 16 * (k - 3);
     std::memcpy(out + o, &vx[k], 8);
     std::memcpy(out + o + 8, &vy[k], 8);
+  }
+  return true;
+}
+
+// Encodes a double leaf slot (index_format.h, kind 4) into out[256] if the
+// cell's content fits one; returns false otherwise.
+inline bool encode_double_slot(const std::vector<Edge4>& E, const std::vector<CandIn>& C,
+                               std::uint8_t* out) {
+  if (C.size() > kDblMaxCands) return false;
+  std::vector<double> ub;
+  for (const auto& c : C) {
+    for (double b : c.breaks) {
+      if (std::find(ub.begin(), ub.end(), b) == ub.end()) ub.push_back(b);
+    }
+  }
+  if (ub.size() > kDblMaxBreaks) return false;
+  std::sort(ub.begin(), ub.end());
+  std::vector<double> vx, vy;
+  std::uint32_t chain_mask = 0;
+  std::vector<std::uint32_t> bit_of;
+  if (!detail::chain_edges(E, vx, vy, chain_mask, bit_of, kDblMaxVerts)) return false;
+  std::memset(out, 0, 2 * kSlotBytes);
+  out[0] = kSlotDouble;
+  out[1] = static_cast<std::uint8_t>(vx.size());
+  out[2] = static_cast<std::uint8_t>(C.size());
+  out[3] = static_cast<std::uint8_t>(ub.size());
+  std::memcpy(out + 4, &chain_mask, 4);
+  for (std::size_t c = 0; c < C.size(); ++c) {
+    const std::int32_t id = static_cast<std::int32_t>(C[c].id);
+    std::memcpy(out + 8 + 4 * c, &id, 4);
+    std::uint16_t mask = 0;
+    for (std::uint32_t e : C[c].edges) mask |= static_cast<std::uint16_t>(1u << bit_of[e]);
+    std::memcpy(out + 40 + 2 * c, &mask, 2);
+    std::uint8_t info = static_cast<std::uint8_t>((C[c].c0 & 1u) << 7);
+    for (double b : C[c].breaks) {
+      info |= static_cast<std::uint8_t>(1u << (std::lower_bound(ub.begin(), ub.end(), b) - ub.begin()));
+    }
+    out[56 + c] = info;
+  }
+  for (std::size_t j = 0; j < ub.size(); ++j) std::memcpy(out + 64 + 8 * j, &ub[j], 8);
+  for (std::size_t k = 0; k < vx.size(); ++k) {
+    std::memcpy(out + 96 + 16 * k, &vx[k], 8);
+    std::memcpy(out + 104 + 16 * k, &vy[k], 8);
   }
   return true;
 }

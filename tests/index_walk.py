@@ -75,6 +75,34 @@ def _eval_leaf_slot(arena, off, px, py) -> int:
     return -1
 
 
+def _eval_double_slot(arena, off, px, py) -> int:
+    """kind 4 (index_format.h): 256 bytes, <= 8 candidates, <= 4 breaks, <= 10 vertices."""
+    buf = arena.data
+    nv, nc, nb = int(arena[off + 1]), int(arena[off + 2]), int(arena[off + 3])
+    chain = struct.unpack_from("<I", buf, off + 4)[0]
+    ids = struct.unpack_from("<8i", buf, off + 8)
+    masks = struct.unpack_from("<8H", buf, off + 40)
+    infos = arena[off + 56: off + 64].tolist()
+    breaks = struct.unpack_from("<4d", buf, off + 64)
+    v = np.frombuffer(buf, dtype="<f8", count=20, offset=off + 96).reshape(10, 2).tolist()
+    m = 0
+    for k in range(9):
+        if k + 1 < nv and not (chain >> (k + 1)) & 1:
+            (ax, ay), (bx, by) = v[k], v[k + 1]
+            lx, ly, hx, hy = (ax, ay, bx, by) if ay < by else (bx, by, ax, ay)
+            if ly < py <= hy and _cross(px, py, lx, ly, hx, hy):
+                m |= 1 << k
+    bm = 0
+    for j in range(nb):
+        if py > breaks[j]:
+            bm |= 1 << j
+    for c in range(nc):
+        par = (infos[c] >> 7) ^ bin(m & masks[c]).count("1") ^ bin(bm & infos[c] & 15).count("1")
+        if par & 1:
+            return ids[c]
+    return -1
+
+
 def _eval_overflow(arena, off, px, py) -> int:
     buf = arena.data
     kind = arena[off]
@@ -144,12 +172,14 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float, slot_bytes: int
     while True:
         off = (e & K_INDEX) * SLOT
         kind = arena[off]
-        half = kind != 1 or leaf_half(*arena[off + 1: off + 4].tolist())
+        half = kind in (2, 3) or (kind == 1 and leaf_half(*arena[off + 1: off + 4].tolist()))
         assert bool(e & K_HALF) == half, "half-slot flag disagrees with the slot"
         if half:  # the flag promises nothing past byte 64 is needed
             assert not arena[off + 64: off + SLOT].any()
         if kind == 1:
             return _eval_leaf_slot(arena, off, px, py)
+        if kind == 4:
+            return _eval_double_slot(arena, off, px, py)
         if kind == 2:
             ovf = struct.unpack_from("<Q", buf, off + 8)[0]
             return _eval_overflow(arena, slot_bytes + ovf, px, py)
@@ -168,9 +198,14 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float, slot_bytes: int
 def record_kinds(index_export) -> dict:
     grid, arena, g = index_export
     n_slots = g["slot_bytes"] // SLOT
-    kinds = arena[np.arange(n_slots) * SLOT] if n_slots else np.zeros(0, np.uint8)
-    return {"leaf": int((kinds == 1).sum()), "overflow": int((kinds == 2).sum()),
-            "split": int((kinds == 3).sum())}
+    count = {"leaf": 0, "overflow": 0, "split": 0, "double": 0}
+    names = {1: "leaf", 2: "overflow", 3: "split", 4: "double"}
+    k = 0
+    while k < n_slots:  # a double slot's second half is not a slot
+        kind = int(arena[k * SLOT])
+        count[names[kind]] += 1
+        k += 2 if kind == 4 else 1
+    return count
 
 
 def walk(index_export, pts: np.ndarray) -> np.ndarray:

@@ -80,12 +80,20 @@ def test_slot_invariants():
     recs = np.random.default_rng(0).choice(recs, min(3000, recs.size), replace=False)
     n_leaf = 0
     n_half = 0
+    n_double = 0
     for e in recs.tolist():
         off = (e & 0x3FFFFFFF) * 128
         kind, nv, nc, nb = arena[off:off + 4].tolist()
-        assert kind in (1, 2, 3)
+        assert kind in (1, 2, 3, 4)
         half = bool(e & 0x40000000)
         n_half += half
+        if kind == 4:  # double leaf slot: never half, within its capacity
+            n_double += 1
+            assert not half and 1 <= nc <= 8 and nb <= 4 and nv <= 10
+            assert nv > 5 or nc > 4 or nb > 2  # it did not fit a leaf slot
+            ids = list(struct.unpack_from("<8i", arena.data, off + 8))[:nc]
+            assert ids == sorted(ids) and len(set(ids)) == nc
+            continue
         if kind != 1:
             assert half and not arena[off + 64: off + 128].any()
             continue
@@ -102,6 +110,7 @@ def test_slot_invariants():
             assert mk < (1 << max(nv - 1, 0)) or mk == 0
     assert n_half > 0
     assert n_leaf > 0
+    assert n_double > 0  # c1's polygon corners
 
 
 @pytest.mark.parametrize("grid", [(64, 48), (257, 131), (1000, 999)])
