@@ -149,15 +149,25 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const unsigned int* __re
 
 // The scatter.  A CTA takes sub-chunks of kScatterIter consecutive points
 // (in increasing order from the work counter), ranks each point within
-// (sub-chunk, tile) with warp-aggregated shared-memory atomics
-// (__match_any_sync: clustered streams put many lanes of a warp into the
-// same hot tile), reserves one run per touched tile from the tile's global
-// cursor, and writes every point to its run.  With one cursor per tile the
+// (sub-chunk, tile) with a shared-memory atomic (hot tiles serialise a few
+// lanes; measured cheaper than aggregating with __match_any_sync, 19.3 ms
+// -> see profiles/README.md r2k), reserves one run per touched tile from
+// the tile's global cursor, and writes every point to its run.  With one cursor per tile the
 // writes of the whole grid advance through just n_tiles fronts, so L2
 // assembles them into whole lines before they reach DRAM; and a tile's
 // points stay in about input order (runs are reserved in sub-chunk order).
+#ifndef FM_SC_PER
+#define FM_SC_PER 8
+#endif
+#ifndef FM_SC_STORE
+#define FM_SC_STORE 1  // experiments: 0 = no point store, 2 = coalesced (wrong answers)
+#endif
+#ifndef FM_SC_STATIC
+#define FM_SC_STATIC 0  // experiments: 1 = grid-stride iterations instead of the work counter
+#endif
 constexpr int kScatterThreads = 256;
-constexpr int kScatterIter = kScatterThreads * kBinPerThread;  // 2048 points
+constexpr int kScPer = FM_SC_PER;
+constexpr int kScatterIter = kScatterThreads * kScPer;  // 2048 points
 constexpr int kScatterSmem = 3 * (kMaxTiles + 1) * 4;
 
 __global__ void __launch_bounds__(kScatterThreads)
@@ -171,35 +181,34 @@ __global__ void __launch_bounds__(kScatterThreads)
   unsigned int* s_cnt = smem;                     // per-tile count of this sub-chunk
   unsigned int* s_base = smem + (kMaxTiles + 1);  // its reserved run
   unsigned int* s_list = smem + 2 * (kMaxTiles + 1);  // tiles touched
-  const int lane = threadIdx.x & 31;
-  const unsigned int lt_mask = (1u << lane) - 1u;
   for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
   if (threadIdx.x == 0) s_nt = 0;
   const std::uint64_t n_iter = (n + kScatterIter - 1) / kScatterIter;
+#if FM_SC_STATIC
+  for (std::uint64_t c = blockIdx.x; c < n_iter; c += gridDim.x) {
+    __syncthreads();
+#else
   for (std::uint64_t c = cta_grab(work + kCtrScatter, &s_grab); c < n_iter;
        c = cta_grab(work + kCtrScatter, &s_grab)) {
+#endif
     const std::uint64_t base = c * kScatterIter;
-    double2 p[kBinPerThread];
-    unsigned int kr[kBinPerThread];
+    double2 p[kScPer];
+    unsigned int kr[kScPer];
 #pragma unroll
-    for (int j = 0; j < kBinPerThread; ++j) {
+    for (int j = 0; j < kScPer; ++j) {
       const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
       p[j] = i < n ? __ldcs(pts + i) : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int j = 0; j < kBinPerThread; ++j) {
+    for (int j = 0; j < kScPer; ++j) {
       const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-      const bool valid = i < n;
-      const int key = valid ? tile_key(P, T, p[j].x, p[j].y) : -1;
-      const unsigned int peers = __match_any_sync(0xFFFFFFFFu, key);
-      const int leader = __ffs(peers) - 1;
-      unsigned int r = 0;
-      if (valid && lane == leader) {
-        r = atomicAdd(s_cnt + key, static_cast<unsigned int>(__popc(peers)));
+      kr[j] = 0xFFFFFFFFu;
+      if (i < n) {
+        const int key = tile_key(P, T, p[j].x, p[j].y);
+        const unsigned int r = atomicAdd(s_cnt + key, 1u);
         if (r == 0u) s_list[atomicAdd(&s_nt, 1)] = static_cast<unsigned int>(key);
+        kr[j] = (static_cast<unsigned int>(key) << 16) | r;
       }
-      r = __shfl_sync(0xFFFFFFFFu, r, leader) + __popc(peers & lt_mask);
-      kr[j] = valid ? ((static_cast<unsigned int>(key) << 16) | r) : 0xFFFFFFFFu;
     }
     __syncthreads();
     const int nt = s_nt;
@@ -209,11 +218,15 @@ __global__ void __launch_bounds__(kScatterThreads)
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kBinPerThread; ++j) {
+    for (int j = 0; j < kScPer; ++j) {
       const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
       if (kr[j] != 0xFFFFFFFFu) {
         const unsigned int dst = s_base[kr[j] >> 16] + (kr[j] & 0xFFFFu);
+#if FM_SC_STORE == 1
         pts_b[dst] = p[j];
+#elif FM_SC_STORE == 2
+        pts_b[i] = p[j];
+#endif
         __stcs(pos + i, dst);
       }
     }
@@ -231,12 +244,18 @@ __global__ void __launch_bounds__(kScatterThreads)
 // the slot fetches of batch k+1 overlap the evaluation of batch k and the
 // next point tile's loads and grid gathers; split cells put their child
 // entry back into the ring.
+// Points in double slots (kDoubleBit; polygon corners) wait in a second
+// ring of (binned index, entry) pairs and are evaluated in whole batches of
+// 32 straight from global memory (both halves of the 256-byte slot loaded
+// at once), so the leaf-slot batches never run the wider double-slot code.
 constexpr int kQWarps = 8;
 constexpr int kQCap = 128;
+constexpr int kDCap = 128;
 struct WarpSmemQ {
   alignas(16) std::uint8_t pool[2][32 * fm::kSlotBytes];
   double qx[kQCap], qy[kQCap];
   std::uint32_t qk[kQCap], qe[kQCap];
+  std::uint32_t dk[kDCap], de[kDCap];
 };
 constexpr int kSmemQ = static_cast<int>(sizeof(WarpSmemQ)) * kQWarps;
 
@@ -245,7 +264,38 @@ struct RingState {
   int pend = 0;          // items of the staged batch in pool[pb]
   int pb = 0;
   QItem pit;             // this lane's staged item
+  int dhead = 0, dn = 0; // double-slot ring
 };
+
+// Evaluate double-slot points in batches of 32 (any remainder when draining).
+template <bool kHist, bool kCount>
+__device__ __forceinline__ void dpump(const fm::KParams& P, const double2* __restrict__ pts, WarpSmemQ& S,
+                                      RingState& R, bool drain, int lane, int* __restrict__ res,
+                                      const HistSink& hist, fm::WorkCount& wc) {
+  while (R.dn >= 32 || (drain && R.dn > 0)) {
+    const int m = min(R.dn, 32);
+    std::uint32_t k = 0, e = 0;
+    if (lane < m) {
+      const int s = (R.dhead + lane) & (kDCap - 1);
+      k = S.dk[s];
+      e = S.de[s];
+    }
+    R.dhead = (R.dhead + m) & (kDCap - 1);
+    R.dn -= m;
+    __syncwarp();
+    if (lane < m) {
+      const double2 p = __ldg(pts + k);
+      const uint4* g = reinterpret_cast<const uint4*>(fm::slot_ptr(P, e));
+      uint4 a[8], b[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = __ldg(g + j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = __ldg(g + 8 + j);
+      if (kCount) wc.boundary++;
+      emit<kHist>(res, hist, k, fm::eval_double_slot<kCount>(a, b, p.x, p.y, wc));
+    }
+  }
+}
 
 // Stage the next batch (when 32 items wait, or any when draining) and
 // evaluate the previously staged one; repeat while full batches remain.
@@ -360,9 +410,10 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
       const std::uint64_t i = base + u * 32 + lane;
       const bool valid = i < n;
       const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
+      const bool is_dbl = is_rec && (e[u] & fm::kDoubleBit) && !(e[u] & fm::kHalfBit);
       if (valid && !is_rec) emit<kHist>(res, hs, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
-      const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec);
-      if (is_rec) {
+      const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec && !is_dbl);
+      if (is_rec && !is_dbl) {
         const int s = (R.head + R.qn + __popc(b & lt_mask)) & (kQCap - 1);
         S.qx[s] = p[u].x;
         S.qy[s] = p[u].y;
@@ -370,12 +421,21 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
         S.qe[s] = e[u];
       }
       R.qn += __popc(b);
+      const std::uint32_t bd = __ballot_sync(0xFFFFFFFFu, is_dbl);
+      if (is_dbl) {
+        const int s = (R.dhead + R.dn + __popc(bd & lt_mask)) & (kDCap - 1);
+        S.dk[s] = static_cast<std::uint32_t>(i);
+        S.de[s] = e[u];
+      }
+      R.dn += __popc(bd);
     }
     if (kCount) done += min(tile, n - base);
     __syncwarp();
+    dpump<kHist, kCount>(P, pts, S, R, false, lane, res, hs, wc);
     pump<kHist, kCount>(P, S, R, false, lane, res, hs, wc);
     t = tn;
   }
+  dpump<kHist, kCount>(P, pts, S, R, true, lane, res, hs, wc);
   pump<kHist, kCount>(P, S, R, true, lane, res, hs, wc);
   hist_close<kHist>(hs);
   if (kCount) {

@@ -7,10 +7,12 @@
 // One u32 entry per cell, row-major:
 //   0xFFFFFFFF            empty: no leaf contains any point of the cell
 //   < 0x80000000          true hit: every point of the cell maps to this leaf
-//   0x80000000 | h<<30 | k boundary: slot k (< 2^30 - 1) of the slot arena
-//                         (128 bytes each); h = 1 when the slot's content
-//                         lies in its first 64 bytes, so the query fetches
-//                         only those (two sectors instead of four)
+//   0x80000000 | h<<30 | d<<29 | k  boundary: slot k (< 2^29 - 1) of the
+//                         slot arena (128 bytes each); h = 1 when the slot's
+//                         content lies in its first 64 bytes, so the query
+//                         fetches only those (two sectors instead of four);
+//                         d = 1 when slot k is a double slot (kind 4, slots
+//                         k and k+1), so the query can batch those apart
 //
 // A boundary cell's slot lists its candidate leaves in ascending id order
 // and the exact (fp64) polygon edges near the cell.  Point p maps to the
@@ -97,8 +99,11 @@ constexpr std::uint32_t kHalfBit = 0x40000000u;     // slot content fits 64 byte
 // with kSmallBit it is a one-unit "small" sub-block
 constexpr std::uint32_t kSmallBit = 0x20000000u;
 constexpr std::uint32_t kUnitMask = 0x1FFFFFFFu;
-constexpr std::uint32_t kSlotIndexMask = 0x3FFFFFFFu;
-constexpr std::uint64_t kMaxSlots = 0x3FFFFFFFull;  // k + flags never equals kEmpty
+// cell / child entries: kRecordBit | kDoubleBit | k names double slot k
+// (kind 4; never together with kHalfBit)
+constexpr std::uint32_t kDoubleBit = 0x20000000u;
+constexpr std::uint32_t kSlotIndexMask = 0x1FFFFFFFu;
+constexpr std::uint64_t kMaxSlots = 0x1FFFFFFFull;  // k + flags never equals kEmpty
 constexpr std::uint32_t kMaxLeaves = 0x7FFFFFFEu;
 constexpr std::uint64_t kRecordAlign = 16;
 constexpr std::uint32_t kMaxCands = 0xFFFFu;  // cell_index.hpp:339-341 limit
@@ -133,7 +138,8 @@ FM_HD std::uint32_t slot_entry(std::uint64_t k, std::uint32_t kind, std::uint32_
                                std::uint32_t nc, std::uint32_t nb) {
   const bool half = kind == kSlotSplit || kind == kSlotOverflow ||
                     (kind == kSlotLeaf && leaf_slot_half(nv, nc, nb));
-  return kRecordBit | (half ? kHalfBit : 0u) | static_cast<std::uint32_t>(k);
+  return kRecordBit | (half ? kHalfBit : 0u) | (kind == kSlotDouble ? kDoubleBit : 0u) |
+         static_cast<std::uint32_t>(k);
 }
 // same, from the slot's first 4 bytes (u8 kind, nv, nc, nb)
 FM_HD std::uint32_t slot_entry_hdr(std::uint64_t k, std::uint32_t h) {

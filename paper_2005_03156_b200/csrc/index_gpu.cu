@@ -674,7 +674,7 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
     return total;
   };
   const unsigned long long n1 = count_kind(kCellSlot);
-  if (n1 > kMaxSlots) throw RuntimeError("index needs more than 2^30 slots");
+  if (n1 > kMaxSlots) throw RuntimeError("index needs more than 2^29 slots");
   DevBuf d_slots1;
   dalloc<std::uint8_t>(d_slots1, std::max<unsigned long long>(n1, 1) * kSlotBytes, "slots");
   write_slots_kernel<<<grid1d(n_cells, 128), 128>>>(ds, d_off.as<unsigned long long>(), d_rec.as<Contrib>(),

@@ -733,7 +733,7 @@ void finish_deferred(const Soup& s, const GridGeom& g, const BuildOptions& o,
     n_slots += rs[r].size() / kSlotBytes;
     ovf_bytes += (ro[r].size() + 15) & ~std::uint64_t{15};
   }
-  if (slot_base + n_slots > kMaxSlots) throw RuntimeError("index needs more than 2^30 slots");
+  if (slot_base + n_slots > kMaxSlots) throw RuntimeError("index needs more than 2^29 slots");
   slots_out.assign(n_slots * kSlotBytes, 0);
   ovf_out.assign(ovf_bytes, 0);
   std::uint64_t so = 0;

@@ -14,7 +14,8 @@ import numpy as np
 K_EMPTY = 0xFFFFFFFF
 K_RECORD = 0x80000000
 K_HALF = 0x40000000      # slot content fits its first 64 bytes
-K_INDEX = 0x3FFFFFFF
+K_DOUBLE = 0x20000000    # double slot (kind 4)
+K_INDEX = 0x1FFFFFFF
 
 
 def _cross(px, py, lx, ly, hx, hy) -> bool:
@@ -174,6 +175,7 @@ def resolve(arena: np.ndarray, entry: int, px: float, py: float, slot_bytes: int
         kind = arena[off]
         half = kind in (2, 3) or (kind == 1 and leaf_half(*arena[off + 1: off + 4].tolist()))
         assert bool(e & K_HALF) == half, "half-slot flag disagrees with the slot"
+        assert bool(e & K_DOUBLE) == (kind == 4), "double-slot flag disagrees with the slot"
         if half:  # the flag promises nothing past byte 64 is needed
             assert not arena[off + 64: off + SLOT].any()
         if kind == 1:

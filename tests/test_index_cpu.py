@@ -82,11 +82,12 @@ def test_slot_invariants():
     n_half = 0
     n_double = 0
     for e in recs.tolist():
-        off = (e & 0x3FFFFFFF) * 128
+        off = (e & 0x1FFFFFFF) * 128
         kind, nv, nc, nb = arena[off:off + 4].tolist()
         assert kind in (1, 2, 3, 4)
         half = bool(e & 0x40000000)
         n_half += half
+        assert bool(e & 0x20000000) == (kind == 4)
         if kind == 4:  # double leaf slot: never half, within its capacity
             n_double += 1
             assert not half and 1 <= nc <= 8 and nb <= 4 and nv <= 10

@@ -1,0 +1,7 @@
+# r2k: double-slot ring in the binned query, per-lane scatter atomics; tests + c3 tiles + launch list
+mkdir -p gpurun_out/r2k
+timeout 1500 python -m pytest tests/test_gpu_build.py tests/test_gpu_parity.py tests/test_gpu_binned.py tests/test_gpu_margin.py tests/test_gpu_c3_full.py -x -q > gpurun_out/r2k/pytest.log 2>&1; echo rc=$? >> gpurun_out/r2k/pytest.log
+timeout 1200 python tools/exp_binned.py c3 1e9 16e6 32e6 64e6 128e6 > gpurun_out/r2k/c3.log 2>&1; echo rc=$? >> gpurun_out/r2k/c3.log
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum --clock-control none \
+  -k regex:"bin_|binned|unbin|stream_kernel|resolve_kernel" --csv --log-file gpurun_out/r2k/launches_c3.csv \
+  python tools/exp_binned.py c3 1e9 64e6 > gpurun_out/r2k/ncu_c3.log 2>&1; echo rc=$? >> gpurun_out/r2k/ncu_c3.log
