@@ -17,7 +17,7 @@ PRODUCT_SRC := $(PKG)/csrc/fastmap_b200.cu $(PKG)/csrc/index_gpu.cu $(PKG)/csrc/
                $(PKG)/csrc/io.cpp $(PKG)/csrc/simple.cu $(PKG)/csrc/multi.cu
 PRODUCT_HDR := include/fastmap_b200.h $(PKG)/csrc/index_format.h \
                $(PKG)/csrc/index_build.h $(PKG)/csrc/query.cuh $(PKG)/csrc/sweep.h \
-               $(PKG)/csrc/record_encode.h $(PKG)/csrc/hierarchy.h
+               $(PKG)/csrc/record_encode.h $(PKG)/csrc/hierarchy.h $(PKG)/csrc/binned.cuh
 
 all: product synth oracle ref
 

@@ -14,16 +14,17 @@
 // (stream_kernel + resolve_kernel) stays the choice for small or mostly
 // true-hit indexes (c1, c2) -- see choose_path() in fastmap_b200.cu.
 //
-// Five launches per batch of n <= 2^30 points:
-//   bin_count_kernel    one CTA per 64K-point chunk: a shared-memory
-//                       histogram of tile keys added into per-tile totals
-//   bin_scan_kernel     one CTA: the totals' exclusive scan = each tile's
-//                       first binned position (its cursor)
-//   bin_scatter_kernel  2K-point sub-chunks held in registers: ranks within
-//                       (sub-chunk, tile) from warp-aggregated shared-memory
-//                       atomics, one run per touched tile reserved from the
-//                       tile's global cursor, each point written to its run
-//                       (pts_b) and its binned position to pos[i] (coalesced)
+// Four launches (and a library scan) per batch of n <= 2^30 points
+// (DESIGN.md sec. 5.3); the stream is cut into G equal contiguous blocks,
+// one per CTA of the scatter:
+//   bin_count_kernel    per block, a shared-memory histogram of tile keys:
+//                       row b of the tile-major (n_tiles + 1) x G table
+//   (cub exclusive scan of the table: entry (t, b) becomes the first
+//    binned position of block b's points in tile t)
+//   bin_scatter_kernel  per block: each point takes the next position of
+//                       its tile's run from a shared-memory cursor and is
+//                       written there (pts_b), its binned position to
+//                       pos[i] (coalesced) -- no barrier, no global atomic
 //   binned_query_kernel the query over pts_b in order: locate, true hits
 //                       answered at once, boundary points through a
 //                       warp-private shared-memory ring whose batches of 32
@@ -31,11 +32,10 @@
 //                       their evaluation (exactly resolve_kernel's code);
 //                       answers to res[k]
 //   unbin_kernel        out[i] = res[pos[i]]
-// Sub-chunks are taken in increasing order, so within a tile the points
-// stay in about input order and any window of consecutive input points maps
-// to about one contiguous range per tile: the gather in unbin_kernel and
-// the scattered writes in bin_scatter_kernel (n_tiles write fronts) stay
-// sector-coherent in L2.
+// Within a tile the points stay grouped by block, i.e. in about input
+// order, so any window of consecutive input points maps to about one
+// contiguous range per tile: the gather in unbin_kernel and the scattered
+// writes of the scatter (G x n_tiles fronts) stay coherent in L2.
 // Points outside the acceptance box (and NaN) go to one extra bin; the
 // query pass answers them -1 like every other path.
 //
@@ -59,7 +59,7 @@ constexpr int kMaxTiles = 4096;                         // keys < kMaxTiles + 1
 // grid stride the persistent warps drift apart over thousands of
 // iterations and the window, and with it the L2 working set, spreads over
 // the whole array.)
-enum { kCtrScatter = 0, kCtrQuery = 1, kCtrUnbin = 2, kCtrCount = 4 };
+enum { kCtrQuery = 1, kCtrUnbin = 2, kCtrCount = 4 };
 
 __device__ __forceinline__ unsigned long long cta_grab(unsigned long long* ctr, unsigned long long* s_slot) {
   __syncthreads();
@@ -84,155 +84,93 @@ __device__ __forceinline__ int tile_key(const fm::KParams& P, const TileGeom& T,
   return in ? (iy >> T.ts) * T.tnx + (ix >> T.ts) : T.n_tiles;
 }
 
-// counts[t] += points of tile t (one CTA per 64K-point chunk: a shared-
-// memory histogram, then one global atomic per non-empty bin)
+// The point stream is cut into G equal contiguous blocks, one per CTA of
+// the scatter (G = its resident CTAs).  Block b: [block_lo(b), block_lo(b+1)).
+__device__ __forceinline__ std::uint64_t block_lo(std::uint64_t n, std::uint64_t G, std::uint64_t b) {
+  return n / G * b + min(b, n % G);
+}
+
+// table[t * G + b] = points of block b in tile t (one CTA per block: a
+// shared-memory histogram of its tile keys)
 __global__ void __launch_bounds__(kBinThreads)
     bin_count_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                     unsigned int* __restrict__ counts) {
+                     std::uint64_t G, unsigned int* __restrict__ table) {
   extern __shared__ unsigned int s_hist[];
-  const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
-  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+  for (std::uint64_t b = blockIdx.x; b < G; b += gridDim.x) {
     for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) s_hist[k] = 0u;
     __syncthreads();
-    const std::uint64_t base = c * kBinChunk;
-    const std::uint64_t end = min(n, base + kBinChunk);
-    for (std::uint64_t b = base + threadIdx.x; b < end; b += 4ull * kBinThreads) {
+    const std::uint64_t lo = block_lo(n, G, b), hi = block_lo(n, G, b + 1);
+    for (std::uint64_t i0 = lo + threadIdx.x; i0 < hi; i0 += 4ull * kBinThreads) {
       double2 p[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kBinThreads;
-        p[u] = i < end ? __ldcs(pts + i) : make_double2(0.0, 0.0);
+        const std::uint64_t i = i0 + static_cast<std::uint64_t>(u) * kBinThreads;
+        p[u] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const std::uint64_t i = b + static_cast<std::uint64_t>(u) * kBinThreads;
-        if (i < end) atomicAdd(s_hist + tile_key(P, T, p[u].x, p[u].y), 1u);
+        const std::uint64_t i = i0 + static_cast<std::uint64_t>(u) * kBinThreads;
+        if (i < hi) atomicAdd(s_hist + tile_key(P, T, p[u].x, p[u].y), 1u);
       }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) {
-      if (s_hist[k]) atomicAdd(counts + k, s_hist[k]);
-    }
+    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) table[static_cast<std::uint64_t>(k) * G + b] = s_hist[k];
     __syncthreads();
   }
 }
 
-// cursor[t] = first binned position of tile t (exclusive scan of counts,
-// n_tiles + 1 <= kMaxTiles + 1 entries: one CTA)
-__global__ void __launch_bounds__(1024) bin_scan_kernel(const unsigned int* __restrict__ counts, int nk,
-                                                        unsigned int* __restrict__ cursor) {
-  __shared__ unsigned int s_part[1024];
-  constexpr int kPer = (kMaxTiles + 1 + 1023) / 1024;
-  unsigned int v[kPer], sum = 0;
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int k = threadIdx.x * kPer + j;
-    v[j] = k < nk ? counts[k] : 0u;
-    sum += v[j];
-  }
-  s_part[threadIdx.x] = sum;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan of the partial sums
-    const unsigned int x = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0u;
-    __syncthreads();
-    s_part[threadIdx.x] += x;
-    __syncthreads();
-  }
-  unsigned int run = threadIdx.x ? s_part[threadIdx.x - 1] : 0u;
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int k = threadIdx.x * kPer + j;
-    if (k < nk) cursor[k] = run;
-    run += v[j];
-  }
-}
-
-// The scatter.  A CTA takes sub-chunks of kScatterIter consecutive points
-// (in increasing order from the work counter), ranks each point within
-// (sub-chunk, tile) with a shared-memory atomic (hot tiles serialise a few
-// lanes; measured cheaper than aggregating with __match_any_sync, 19.3 ms
-// -> see profiles/README.md r2k), reserves one run per touched tile from
-// the tile's global cursor, and writes every point to its run.  With one cursor per tile the
-// writes of the whole grid advance through just n_tiles fronts, so L2
-// assembles them into whole lines before they reach DRAM; and a tile's
-// points stay in about input order (runs are reserved in sub-chunk order).
+// The scatter: CTA b walks block b with kScPer points per thread in flight;
+// each point takes the next position of its tile's run with one shared-
+// memory atomic on the block's cursor (s_cur starts at the scanned table
+// entries, and the block's per-tile counts are exactly the table's, so the
+// runs fill [start, start + count) whatever the order) and is written there
+// (pts_b), its binned position to pos[i] (coalesced).  No barrier and no
+// global atomic inside the walk.  Within a tile the points stay grouped by
+// block, i.e. in about input order, so the gather in unbin_kernel is
+// coherent; the writes advance through G x n_tiles fronts that L2 turns
+// into whole lines.
 #ifndef FM_SC_PER
-#define FM_SC_PER 8
-#endif
-#ifndef FM_SC_STORE
-#define FM_SC_STORE 1  // experiments: 0 = no point store, 2 = coalesced (wrong answers)
-#endif
-#ifndef FM_SC_STATIC
-#define FM_SC_STATIC 0  // experiments: 1 = grid-stride iterations instead of the work counter
+#define FM_SC_PER 16
 #endif
 constexpr int kScatterThreads = 256;
 constexpr int kScPer = FM_SC_PER;
-constexpr int kScatterIter = kScatterThreads * kScPer;  // 2048 points
-constexpr int kScatterSmem = 3 * (kMaxTiles + 1) * 4;
 
 __global__ void __launch_bounds__(kScatterThreads)
     bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                       unsigned int* __restrict__ cursor, double2* __restrict__ pts_b,
-                       unsigned int* __restrict__ pos, unsigned long long* __restrict__ work) {
-  extern __shared__ unsigned int smem[];
-  __shared__ unsigned long long s_grab;
-  __shared__ int s_nt;
+                       std::uint64_t G, const unsigned int* __restrict__ starts,
+                       double2* __restrict__ pts_b, unsigned int* __restrict__ pos) {
+  extern __shared__ unsigned int s_cur[];
   const int nk = T.n_tiles + 1;
-  unsigned int* s_cnt = smem;                     // per-tile count of this sub-chunk
-  unsigned int* s_base = smem + (kMaxTiles + 1);  // its reserved run
-  unsigned int* s_list = smem + 2 * (kMaxTiles + 1);  // tiles touched
-  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
-  if (threadIdx.x == 0) s_nt = 0;
-  const std::uint64_t n_iter = (n + kScatterIter - 1) / kScatterIter;
-#if FM_SC_STATIC
-  for (std::uint64_t c = blockIdx.x; c < n_iter; c += gridDim.x) {
+  for (std::uint64_t b = blockIdx.x; b < G; b += gridDim.x) {
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cur[k] = starts[static_cast<std::uint64_t>(k) * G + b];
     __syncthreads();
-#else
-  for (std::uint64_t c = cta_grab(work + kCtrScatter, &s_grab); c < n_iter;
-       c = cta_grab(work + kCtrScatter, &s_grab)) {
-#endif
-    const std::uint64_t base = c * kScatterIter;
-    double2 p[kScPer];
-    unsigned int kr[kScPer];
+    const std::uint64_t lo = block_lo(n, G, b), hi = block_lo(n, G, b + 1);
+    for (std::uint64_t i0 = lo + threadIdx.x; i0 < hi; i0 += static_cast<std::uint64_t>(kScPer) * kScatterThreads) {
+      double2 p[kScPer];
 #pragma unroll
-    for (int j = 0; j < kScPer; ++j) {
-      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-      p[j] = i < n ? __ldcs(pts + i) : make_double2(0.0, 0.0);
-    }
+      for (int j = 0; j < kScPer; ++j) {
+        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
+        p[j] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
+      }
+      // all the cursor atomics first (independent, issued back to back),
+      // then all the stores: interleaved, each store would wait for its
+      // atomic's round trip before the next atomic issues
+      unsigned int dst[kScPer];
 #pragma unroll
-    for (int j = 0; j < kScPer; ++j) {
-      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-      kr[j] = 0xFFFFFFFFu;
-      if (i < n) {
-        const int key = tile_key(P, T, p[j].x, p[j].y);
-        const unsigned int r = atomicAdd(s_cnt + key, 1u);
-        if (r == 0u) s_list[atomicAdd(&s_nt, 1)] = static_cast<unsigned int>(key);
-        kr[j] = (static_cast<unsigned int>(key) << 16) | r;
+      for (int j = 0; j < kScPer; ++j) {
+        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
+        dst[j] = i < hi ? atomicAdd(s_cur + tile_key(P, T, p[j].x, p[j].y), 1u) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kScPer; ++j) {
+        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
+        if (i < hi) {
+          pts_b[dst[j]] = p[j];
+          __stcs(pos + i, dst[j]);
+        }
       }
     }
     __syncthreads();
-    const int nt = s_nt;
-    for (int q = threadIdx.x; q < nt; q += blockDim.x) {
-      const unsigned int t = s_list[q];
-      s_base[t] = atomicAdd(cursor + t, s_cnt[t]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kScPer; ++j) {
-      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-      if (kr[j] != 0xFFFFFFFFu) {
-        const unsigned int dst = s_base[kr[j] >> 16] + (kr[j] & 0xFFFFu);
-#if FM_SC_STORE == 1
-        pts_b[dst] = p[j];
-#elif FM_SC_STORE == 2
-        pts_b[i] = p[j];
-#endif
-        __stcs(pos + i, dst);
-      }
-    }
-    for (int q = threadIdx.x; q < nt; q += blockDim.x) s_cnt[s_list[q]] = 0u;
-    __syncthreads();
-    if (threadIdx.x == 0) s_nt = 0;
   }
 }
 
@@ -380,31 +318,40 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
     if (lane == 0) g = atomicAdd(work + kCtrQuery, 1ull);
     return static_cast<std::uint64_t>(__shfl_sync(0xFFFFFFFFu, g, 0)) * kQGroup;
   };
-  std::uint64_t t = grab(), g_end = t + kQGroup;
-  double2 pn[kU];
+  // software pipeline over the warp's tiles t < t1 < t2: the points of t2
+  // are loading and the grid entries of t1 are in flight while tile t is
+  // answered, so neither latency is exposed (16 warps per SM do not hide
+  // the grid gather on their own)
+  auto next_tile = [&](std::uint64_t x, std::uint64_t& g_end) -> std::uint64_t {
+    std::uint64_t y = x + 1;
+    if (y == g_end) {
+      y = grab();
+      g_end = y + kQGroup;
+    }
+    return y;
+  };
+  auto load_pts = [&](std::uint64_t x, double2 (&q)[kU]) {
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    const std::uint64_t i = t * tile + u * 32 + lane;
-    pn[u] = (t < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
-  }
+    for (int u = 0; u < kU; ++u) {
+      const std::uint64_t i = x * tile + u * 32 + lane;
+      q[u] = (x < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
+    }
+  };
+  std::uint64_t g_end = 0;
+  std::uint64_t t = grab();
+  g_end = t + kQGroup;
+  std::uint64_t t1 = t < n_tiles ? next_tile(t, g_end) : n_tiles;
+  double2 p[kU], p1[kU], p2[kU];
+  std::uint32_t e[kU], e1[kU];
+  load_pts(t, p);
+  load_pts(t1, p1);
+  fm::locate_n<kU, true, kLs>(P, p, e);
   unsigned long long done = 0;
   while (t < n_tiles) {
     const std::uint64_t base = t * tile;
-    double2 p[kU];
-    std::uint32_t e[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) p[u] = pn[u];
-    fm::locate_n<kU, true, kLs>(P, p, e);
-    std::uint64_t tn = t + 1;
-    if (tn == g_end) {
-      tn = grab();
-      g_end = tn + kQGroup;
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const std::uint64_t i = tn * tile + u * 32 + lane;
-      pn[u] = (tn < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
-    }
+    const std::uint64_t t2 = t1 < n_tiles ? next_tile(t1, g_end) : n_tiles;
+    load_pts(t2, p2);
+    fm::locate_n<kU, true, kLs>(P, p1, e1);
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const std::uint64_t i = base + u * 32 + lane;
@@ -433,7 +380,14 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
     __syncwarp();
     dpump<kHist, kCount>(P, pts, S, R, false, lane, res, hs, wc);
     pump<kHist, kCount>(P, S, R, false, lane, res, hs, wc);
-    t = tn;
+    t = t1;
+    t1 = t2;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      p[u] = p1[u];
+      p1[u] = p2[u];
+      e[u] = e1[u];
+    }
   }
   dpump<kHist, kCount>(P, pts, S, R, true, lane, res, hs, wc);
   pump<kHist, kCount>(P, S, R, true, lane, res, hs, wc);

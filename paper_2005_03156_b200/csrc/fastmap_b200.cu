@@ -295,9 +295,14 @@ __device__ __forceinline__ QItem load_item(const QItem* __restrict__ items, std:
   return it;
 }
 
-// Start copying the slots of the items held by lanes [0, n) into `buf`.
+// Start copying the slots of the items held by lanes [0, n) into `buf`; the
+// second half of a double slot (kDoubleBit) is prefetched into L2, where
+// its evaluation one batch later finds it.
 __device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* buf,
                                             std::uint32_t e, int n, int lane) {
+  if (lane < n && (e & fm::kDoubleBit) && !(e & fm::kHalfBit)) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(fm::slot_ptr(P, e) + fm::kSlotBytes));
+  }
   const int c = lane & 7;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -331,7 +336,7 @@ __device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const
     if (kind == fm::kSlotLeaf) {
       if (kCount) wc.boundary++;
       id = fm::eval_leaf_slot<kCount>(c, it.px, it.py, wc);
-    } else if (kind == fm::kSlotDouble) {  // second half from global memory
+    } else if (kind == fm::kSlotDouble) {  // second half from global memory (prefetched to L2)
       if (kCount) wc.boundary++;
       uint4 b[8];
       fm::load_double_tail(P, it.e, b);
@@ -934,36 +939,43 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
                           HistT* d_hist, unsigned long long* d_counters, cudaStream_t stream) {
   const fm::KParams P = kparams(ix);
   const TileGeom& T = ix->tiles;
-  const std::uint64_t n_chunks = (n + kBinChunk - 1) / kBinChunk;
   const int nk = T.n_tiles + 1;
-  // scratch: work counters, per-tile counts and cursors, binned points,
-  // binned positions, binned answers (24 B per point)
+  const int scatter_smem = nk * 4;
+  auto ks = bin_scatter_kernel;
+  // G blocks: one per resident scatter CTA, each at least 64K points
+  const std::uint64_t G = std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+      (n + 65535) / 65536, resident_blocks(ix->device, (const void*)ks, kScatterThreads, scatter_smem)));
+  const std::uint64_t n_tab = static_cast<std::uint64_t>(nk) * G;
+  std::size_t cub_bytes = 0;
+  FM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, static_cast<unsigned int*>(nullptr),
+                                        static_cast<unsigned int*>(nullptr),
+                                        static_cast<std::int64_t>(n_tab), stream));
+  // scratch: work counters, the (tile x block) table and its scan, scan
+  // temp, binned points, binned positions, binned answers (24 B per point)
   const std::uint64_t o_work = 0;
-  const std::uint64_t o_cnt = 256;
-  const std::uint64_t o_cur = o_cnt + align256(4ull * nk);
-  const std::uint64_t o_pts = o_cur + align256(4ull * nk);
+  const std::uint64_t o_tab = 256;
+  const std::uint64_t o_scan = o_tab + align256(4 * n_tab);
+  const std::uint64_t o_tmp = o_scan + align256(4 * n_tab);
+  const std::uint64_t o_pts = o_tmp + align256(cub_bytes + 16);
   const std::uint64_t o_pos = o_pts + align256(16 * n);
   const std::uint64_t o_res = o_pos + align256(4 * n);
   const std::uint64_t total = o_res + align256(4 * n);
   char* scratch = nullptr;
   FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), total, stream));
   unsigned long long* work = reinterpret_cast<unsigned long long*>(scratch + o_work);
-  unsigned int* counts = reinterpret_cast<unsigned int*>(scratch + o_cnt);
-  unsigned int* cursor = reinterpret_cast<unsigned int*>(scratch + o_cur);
-  FM_CUDA(cudaMemsetAsync(scratch, 0, o_cur, stream));  // work counters + counts
+  unsigned int* table = reinterpret_cast<unsigned int*>(scratch + o_tab);
+  unsigned int* starts = reinterpret_cast<unsigned int*>(scratch + o_scan);
+  FM_CUDA(cudaMemsetAsync(work, 0, 8 * kCtrCount, stream));
   double2* pts_b = reinterpret_cast<double2*>(scratch + o_pts);
   unsigned int* pos = reinterpret_cast<unsigned int*>(scratch + o_pos);
   int* res = reinterpret_cast<int*>(scratch + o_res);
   auto kc = bin_count_kernel;
   const int grid_c = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      n_chunks, resident_blocks(ix->device, (const void*)kc, kBinThreads, kBinCountSmem))));
-  kc<<<grid_c, kBinThreads, kBinCountSmem, stream>>>(P, T, pts, n, counts);
-  bin_scan_kernel<<<1, 1024, 0, stream>>>(counts, nk, cursor);
-  auto ks = bin_scatter_kernel;
-  const std::uint64_t n_iter = (n + kScatterIter - 1) / kScatterIter;
-  const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      n_iter, resident_blocks(ix->device, (const void*)ks, kScatterThreads, kScatterSmem))));
-  ks<<<grid_s, kScatterThreads, kScatterSmem, stream>>>(P, T, pts, n, cursor, pts_b, pos, work);
+      G, resident_blocks(ix->device, (const void*)kc, kBinThreads, kBinCountSmem))));
+  kc<<<grid_c, kBinThreads, kBinCountSmem, stream>>>(P, T, pts, n, G, table);
+  FM_CUDA(cub::DeviceScan::ExclusiveSum(scratch + o_tmp, cub_bytes, table, starts,
+                                        static_cast<std::int64_t>(n_tab), stream));
+  ks<<<static_cast<int>(G), kScatterThreads, scatter_smem, stream>>>(P, T, pts, n, G, starts, pts_b, pos);
   auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<kHist, kCount, 0>
                               : binned_query_kernel<kHist, kCount, -1>;
   const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);

@@ -1,0 +1,7 @@
+# r2o: scatter atomics-then-stores, pipelined locate in the binned query
+mkdir -p gpurun_out/r2o
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_binned.py tests/test_gpu_margin.py -x -q > gpurun_out/r2o/pytest.log 2>&1; echo rc=$? >> gpurun_out/r2o/pytest.log
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum --clock-control none \
+  -k regex:"bin_|binned|unbin|stream_kernel|resolve_kernel" --csv --log-file gpurun_out/r2o/launches_c3.csv \
+  python tools/exp_binned.py c3 1e9 32e6 > gpurun_out/r2o/ncu_c3.log 2>&1; echo rc=$? >> gpurun_out/r2o/ncu_c3.log
+timeout 1200 python tools/exp_binned.py c3 1e9 16e6 32e6 64e6 > gpurun_out/r2o/c3.log 2>&1; echo rc=$? >> gpurun_out/r2o/c3.log
