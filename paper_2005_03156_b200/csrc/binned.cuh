@@ -15,16 +15,16 @@
 // true-hit indexes (c1, c2) -- see choose_path() in fastmap_b200.cu.
 //
 // Four launches (and a library scan) per batch of n <= 2^30 points
-// (DESIGN.md sec. 5.3); the stream is cut into G equal contiguous blocks,
-// one per CTA of the scatter:
-//   bin_count_kernel    per block, a shared-memory histogram of tile keys:
-//                       row b of the tile-major (n_tiles + 1) x G table
-//   (cub exclusive scan of the table: entry (t, b) becomes the first
-//    binned position of block b's points in tile t)
-//   bin_scatter_kernel  per block: each point takes the next position of
+// (DESIGN.md sec. 5.3); the stream is cut into chunks of >= 4096 points:
+//   bin_count_kernel    per chunk, a shared-memory histogram of tile keys:
+//                       column c of the tile-major (n_tiles + 1) x n_chunks
+//                       table
+//   (cub exclusive scan of the table: entry (t, c) becomes the first
+//    binned position of chunk c's points in tile t)
+//   bin_scatter_kernel  per chunk: each point takes the next position of
 //                       its tile's run from a shared-memory cursor and is
 //                       written there (pts_b), its binned position to
-//                       pos[i] (coalesced) -- no barrier, no global atomic
+//                       pos[i] (coalesced)
 //   binned_query_kernel the query over pts_b in order: locate, true hits
 //                       answered at once, boundary points through a
 //                       warp-private shared-memory ring whose batches of 32
@@ -32,10 +32,10 @@
 //                       their evaluation (exactly resolve_kernel's code);
 //                       answers to res[k]
 //   unbin_kernel        out[i] = res[pos[i]]
-// Within a tile the points stay grouped by block, i.e. in about input
-// order, so any window of consecutive input points maps to about one
-// contiguous range per tile: the gather in unbin_kernel and the scattered
-// writes of the scatter (G x n_tiles fronts) stay coherent in L2.
+// Chunks are walked with a grid stride, so within a tile the points stay
+// in about input order and any window of consecutive input points maps to
+// about one contiguous range per tile: the gather in unbin_kernel and the
+// scattered writes of the scatter stay coherent in L2 and the TLB.
 // Points outside the acceptance box (and NaN) go to one extra bin; the
 // query pass answers them -1 like every other path.
 //
@@ -47,9 +47,6 @@
 #define FM_QMINB 2
 #endif
 
-constexpr int kBinThreads = 512;
-constexpr int kBinPerThread = 8;
-constexpr std::uint64_t kBinChunk = std::uint64_t{1} << 16;  // 64K points per counting CTA
 constexpr int kMaxTiles = 4096;                         // keys < kMaxTiles + 1
 
 // Work counters (zeroed per launch): the ordered passes hand out their
@@ -84,77 +81,78 @@ __device__ __forceinline__ int tile_key(const fm::KParams& P, const TileGeom& T,
   return in ? (iy >> T.ts) * T.tnx + (ix >> T.ts) : T.n_tiles;
 }
 
-// The point stream is cut into G equal contiguous blocks, one per CTA of
-// the scatter (G = its resident CTAs).  Block b: [block_lo(b), block_lo(b+1)).
-__device__ __forceinline__ std::uint64_t block_lo(std::uint64_t n, std::uint64_t G, std::uint64_t b) {
-  return n / G * b + min(b, n % G);
-}
-
-// table[t * G + b] = points of block b in tile t (one CTA per block: a
-// shared-memory histogram of its tile keys)
-__global__ void __launch_bounds__(kBinThreads)
-    bin_count_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                     std::uint64_t G, unsigned int* __restrict__ table) {
-  extern __shared__ unsigned int s_hist[];
-  for (std::uint64_t b = blockIdx.x; b < G; b += gridDim.x) {
-    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) s_hist[k] = 0u;
-    __syncthreads();
-    const std::uint64_t lo = block_lo(n, G, b), hi = block_lo(n, G, b + 1);
-    for (std::uint64_t i0 = lo + threadIdx.x; i0 < hi; i0 += 4ull * kBinThreads) {
-      double2 p[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const std::uint64_t i = i0 + static_cast<std::uint64_t>(u) * kBinThreads;
-        p[u] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const std::uint64_t i = i0 + static_cast<std::uint64_t>(u) * kBinThreads;
-        if (i < hi) atomicAdd(s_hist + tile_key(P, T, p[u].x, p[u].y), 1u);
-      }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) table[static_cast<std::uint64_t>(k) * G + b] = s_hist[k];
-    __syncthreads();
-  }
-}
-
-// The scatter: CTA b walks block b with kScPer points per thread in flight;
-// each point takes the next position of its tile's run with one shared-
-// memory atomic on the block's cursor (s_cur starts at the scanned table
-// entries, and the block's per-tile counts are exactly the table's, so the
-// runs fill [start, start + count) whatever the order) and is written there
-// (pts_b), its binned position to pos[i] (coalesced).  No barrier and no
-// global atomic inside the walk.  Within a tile the points stay grouped by
-// block, i.e. in about input order, so the gather in unbin_kernel is
-// coherent; the writes advance through G x n_tiles fronts that L2 turns
-// into whole lines.
+// The point stream is cut into chunks of ch = kScatterIter * m points
+// (m >= 1 keeps the (n_tiles + 1) x n_chunks table under kMaxTableEntries),
+// and both passes walk the chunks with a grid stride: at any moment the
+// whole grid reads one narrow window of the stream and, in every tile, writes
+// one narrow window of its runs.  (Contiguous per-CTA blocks measured 3.35
+// TB/s for the same copy against 5.7 TB/s for a grid stride: hundreds of
+// streams far apart in memory thrash the TLB -- tools/exp_copy.cu,
+// profiles/r2q.)
 #ifndef FM_SC_PER
 #define FM_SC_PER 16
 #endif
 constexpr int kScatterThreads = 256;
 constexpr int kScPer = FM_SC_PER;
+constexpr int kScatterIter = kScatterThreads * kScPer;  // 4096 points
+constexpr std::uint64_t kMaxTableEntries = std::uint64_t{64} << 20;
 
+// table[t * n_chunks + c] = points of chunk c in tile t (a shared-memory
+// histogram per chunk)
 __global__ void __launch_bounds__(kScatterThreads)
-    bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                       std::uint64_t G, const unsigned int* __restrict__ starts,
-                       double2* __restrict__ pts_b, unsigned int* __restrict__ pos) {
-  extern __shared__ unsigned int s_cur[];
-  const int nk = T.n_tiles + 1;
-  for (std::uint64_t b = blockIdx.x; b < G; b += gridDim.x) {
-    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cur[k] = starts[static_cast<std::uint64_t>(k) * G + b];
+    bin_count_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
+                     std::uint64_t ch, unsigned int* __restrict__ table) {
+  extern __shared__ unsigned int s_hist[];
+  const std::uint64_t n_chunks = (n + ch - 1) / ch;
+  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) s_hist[k] = 0u;
     __syncthreads();
-    const std::uint64_t lo = block_lo(n, G, b), hi = block_lo(n, G, b + 1);
-    for (std::uint64_t i0 = lo + threadIdx.x; i0 < hi; i0 += static_cast<std::uint64_t>(kScPer) * kScatterThreads) {
+    const std::uint64_t hi = min(n, (c + 1) * ch);
+    for (std::uint64_t i0 = c * ch + threadIdx.x; i0 < hi; i0 += kScatterIter) {
       double2 p[kScPer];
 #pragma unroll
       for (int j = 0; j < kScPer; ++j) {
         const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
         p[j] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
       }
-      // all the cursor atomics first (independent, issued back to back),
-      // then all the stores: interleaved, each store would wait for its
-      // atomic's round trip before the next atomic issues
+#pragma unroll
+      for (int j = 0; j < kScPer; ++j) {
+        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
+        if (i < hi) atomicAdd(s_hist + tile_key(P, T, p[j].x, p[j].y), 1u);
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) table[static_cast<std::uint64_t>(k) * n_chunks + c] = s_hist[k];
+    __syncthreads();
+  }
+}
+
+// The scatter: per chunk, the shared-memory cursors start at the scanned
+// table entries of the chunk; each point takes the next position of its
+// tile's run with one shared-memory atomic (the chunk's per-tile counts are
+// exactly the table's, so the runs fill [start, start + count) whatever the
+// order) and is written there (pts_b), its binned position to pos[i]
+// (coalesced).  The cursor atomics of a thread's kScPer points issue back to
+// back before its stores.  Within a tile the points stay in chunk order,
+// i.e. in about input order, so the gather in unbin_kernel is coherent.
+__global__ void __launch_bounds__(kScatterThreads)
+    bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
+                       std::uint64_t ch, const unsigned int* __restrict__ starts,
+                       double2* __restrict__ pts_b, unsigned int* __restrict__ pos) {
+  extern __shared__ unsigned int s_cur[];
+  const int nk = T.n_tiles + 1;
+  const std::uint64_t n_chunks = (n + ch - 1) / ch;
+  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cur[k] = starts[static_cast<std::uint64_t>(k) * n_chunks + c];
+    __syncthreads();
+    const std::uint64_t hi = min(n, (c + 1) * ch);
+    for (std::uint64_t i0 = c * ch + threadIdx.x; i0 < hi; i0 += kScatterIter) {
+      double2 p[kScPer];
+#pragma unroll
+      for (int j = 0; j < kScPer; ++j) {
+        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
+        p[j] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
+      }
       unsigned int dst[kScPer];
 #pragma unroll
       for (int j = 0; j < kScPer; ++j) {
@@ -170,7 +168,7 @@ __global__ void __launch_bounds__(kScatterThreads)
         }
       }
     }
-    __syncthreads();
+    __syncthreads();  // s_cur is reloaded for the next chunk
   }
 }
 

@@ -295,21 +295,24 @@ __device__ __forceinline__ QItem load_item(const QItem* __restrict__ items, std:
   return it;
 }
 
-// Start copying the slots of the items held by lanes [0, n) into `buf`; the
-// second half of a double slot (kDoubleBit) is prefetched into L2, where
-// its evaluation one batch later finds it.
+// Start copying the slots of the items held by lanes [0, n) into `buf`: each
+// lane copies its own item's slot (four 16-byte cp.async for a half slot,
+// eight for a full one) into its 128-byte pool entry, chunk c at c ^ (lane &
+// 7) so the reads in eval_staged are bank-conflict free.  The second half of
+// a double slot (kDoubleBit) is prefetched into L2, where its evaluation one
+// batch later finds it.
 __device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* buf,
                                             std::uint32_t e, int n, int lane) {
-  if (lane < n && (e & fm::kDoubleBit) && !(e & fm::kHalfBit)) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(fm::slot_ptr(P, e) + fm::kSlotBytes));
-  }
-  const int c = lane & 7;
+  if (lane < n) {
+    const std::uint8_t* g = fm::slot_ptr(P, e);
+    std::uint8_t* d = buf + lane * fm::kSlotBytes;
+    const int s = lane & 7;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int r = 4 * q + (lane >> 3);
-    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
-    if (r < n && (c < 4 || !(er & fm::kHalfBit))) {  // half slots: first 64 bytes only
-      cp_async16(buf + r * fm::kSlotBytes + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
+    for (int c = 0; c < 4; ++c) cp_async16(d + 16 * (c ^ s), g + 16 * c);
+    if (!(e & fm::kHalfBit)) {
+#pragma unroll
+      for (int c = 4; c < 8; ++c) cp_async16(d + 16 * (c ^ s), g + 16 * c);
+      if (e & fm::kDoubleBit) asm volatile("prefetch.global.L2 [%0];" ::"l"(g + fm::kSlotBytes));
     }
   }
   cp_async_commit();
@@ -699,28 +702,40 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Block-major renumbering of the phase-1 slots (renumber_slots): position p
-// walks blocks of 2^ls x 2^ls cells in row-major block order, cells
-// row-major inside each block.
-__device__ __forceinline__ bool block_major_cell(std::uint64_t p, int ls, int bnx, int nx, int ny,
-                                                 std::uint64_t* cell) {
-  const std::uint64_t b = p >> (2 * ls);
-  const int o = static_cast<int>(p & ((1ull << (2 * ls)) - 1));
-  const int by = static_cast<int>(b / bnx), bx = static_cast<int>(b - static_cast<std::uint64_t>(by) * bnx);
-  const int x = (bx << ls) + (o & ((1 << ls) - 1)), y = (by << ls) + (o >> ls);
-  if (x >= nx || y >= ny) return false;
-  *cell = static_cast<std::uint64_t>(y) * nx + x;
+// Tile-major, then block-major renumbering of the phase-1 slots
+// (renumber_slots): position p walks tiles of 2^ts x 2^ts cells (the binned
+// path's index tiles) in row-major tile order, inside each tile blocks of
+// 2^ls x 2^ls cells (the query-side fold) in row-major order, and cells
+// row-major inside each block.  So every block's slots are consecutive (the
+// fold's compact sub-blocks name them as base + offset) and every tile's
+// slots are one contiguous range of the arena (the binned query walks one
+// tile at a time).
+struct RenumGeom {
+  int ts, ls, tnx, nx, ny;
+};
+
+__device__ __forceinline__ bool block_major_cell(std::uint64_t p, const RenumGeom& R, std::uint64_t* cell) {
+  const std::uint64_t t = p >> (2 * R.ts);
+  const std::uint32_t o = static_cast<std::uint32_t>(p & ((1ull << (2 * R.ts)) - 1));
+  const int ty = static_cast<int>(t / R.tnx), tx = static_cast<int>(t - static_cast<std::uint64_t>(ty) * R.tnx);
+  const int bside = R.ts - R.ls;  // log2 blocks per tile side
+  const std::uint32_t b = o >> (2 * R.ls), q = o & ((1u << (2 * R.ls)) - 1);
+  const int bx = static_cast<int>(b & ((1u << bside) - 1)), by = static_cast<int>(b >> bside);
+  const int x = (tx << R.ts) + (bx << R.ls) + static_cast<int>(q & ((1u << R.ls) - 1));
+  const int y = (ty << R.ts) + (by << R.ls) + static_cast<int>(q >> R.ls);
+  if (x >= R.nx || y >= R.ny) return false;
+  *cell = static_cast<std::uint64_t>(y) * R.nx + x;
   return true;
 }
 
 __global__ void __launch_bounds__(256)
-    renum_flag_kernel(const std::uint32_t* __restrict__ grid, int nx, int ny, int bnx, int ls,
-                      std::uint64_t n_pos, std::uint64_t n1, std::uint32_t* __restrict__ flag) {
+    renum_flag_kernel(const std::uint32_t* __restrict__ grid, RenumGeom R, std::uint64_t n_pos,
+                      std::uint64_t n1, std::uint32_t* __restrict__ flag) {
   const std::uint64_t p = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n_pos) return;
   std::uint64_t c;
   std::uint32_t f = 0;
-  if (block_major_cell(p, ls, bnx, nx, ny, &c)) {
+  if (block_major_cell(p, R, &c)) {
     const std::uint32_t e = grid[c];
     f = (e != fm::kEmpty && e >= fm::kRecordBit && (e & fm::kSlotIndexMask) < n1) ? 1u : 0u;
   }
@@ -728,14 +743,13 @@ __global__ void __launch_bounds__(256)
 }
 
 __global__ void __launch_bounds__(256)
-    renum_apply_kernel(std::uint32_t* __restrict__ grid, int nx, int ny, int bnx, int ls,
-                       std::uint64_t n_pos, const std::uint32_t* __restrict__ flag,
-                       const std::uint32_t* __restrict__ idx, const uint4* __restrict__ old_slots,
-                       uint4* __restrict__ new_slots) {
+    renum_apply_kernel(std::uint32_t* __restrict__ grid, RenumGeom R, std::uint64_t n_pos,
+                       const std::uint32_t* __restrict__ flag, const std::uint32_t* __restrict__ idx,
+                       const uint4* __restrict__ old_slots, uint4* __restrict__ new_slots) {
   const std::uint64_t p = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n_pos || !flag[p]) return;
   std::uint64_t c;
-  block_major_cell(p, ls, bnx, nx, ny, &c);
+  block_major_cell(p, R, &c);
   const std::uint32_t e = grid[c];
   const std::uint64_t ko = e & fm::kSlotIndexMask, kn = idx[p];
 #pragma unroll
@@ -930,7 +944,6 @@ fm_status launch_t(const fm_index* ix, const double2* pts, std::uint64_t n, int*
 
 // The binned path (binned.cuh) over one batch of n <= kBinnedBatch points.
 constexpr std::uint64_t kBinnedBatch = std::uint64_t{1} << 30;
-constexpr int kBinCountSmem = (kMaxTiles + 1) * 4;
 
 std::uint64_t align256(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
 
@@ -940,17 +953,18 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   const fm::KParams P = kparams(ix);
   const TileGeom& T = ix->tiles;
   const int nk = T.n_tiles + 1;
-  const int scatter_smem = nk * 4;
-  auto ks = bin_scatter_kernel;
-  // G blocks: one per resident scatter CTA, each at least 64K points
-  const std::uint64_t G = std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      (n + 65535) / 65536, resident_blocks(ix->device, (const void*)ks, kScatterThreads, scatter_smem)));
-  const std::uint64_t n_tab = static_cast<std::uint64_t>(nk) * G;
+  const int tile_smem = nk * 4;
+  // chunks of kScatterIter * m points, m keeping the table under kMaxTableEntries
+  const std::uint64_t n_it = (n + kScatterIter - 1) / kScatterIter;
+  const std::uint64_t m = std::max<std::uint64_t>(1, (n_it * nk + kMaxTableEntries - 1) / kMaxTableEntries);
+  const std::uint64_t ch = static_cast<std::uint64_t>(kScatterIter) * m;
+  const std::uint64_t n_chunks = (n + ch - 1) / ch;
+  const std::uint64_t n_tab = static_cast<std::uint64_t>(nk) * n_chunks;
   std::size_t cub_bytes = 0;
   FM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, static_cast<unsigned int*>(nullptr),
                                         static_cast<unsigned int*>(nullptr),
                                         static_cast<std::int64_t>(n_tab), stream));
-  // scratch: work counters, the (tile x block) table and its scan, scan
+  // scratch: work counters, the (tile x chunk) table and its scan, scan
   // temp, binned points, binned positions, binned answers (24 B per point)
   const std::uint64_t o_work = 0;
   const std::uint64_t o_tab = 256;
@@ -971,11 +985,14 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   int* res = reinterpret_cast<int*>(scratch + o_res);
   auto kc = bin_count_kernel;
   const int grid_c = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      G, resident_blocks(ix->device, (const void*)kc, kBinThreads, kBinCountSmem))));
-  kc<<<grid_c, kBinThreads, kBinCountSmem, stream>>>(P, T, pts, n, G, table);
+      n_chunks, resident_blocks(ix->device, (const void*)kc, kScatterThreads, tile_smem))));
+  kc<<<grid_c, kScatterThreads, tile_smem, stream>>>(P, T, pts, n, ch, table);
   FM_CUDA(cub::DeviceScan::ExclusiveSum(scratch + o_tmp, cub_bytes, table, starts,
                                         static_cast<std::int64_t>(n_tab), stream));
-  ks<<<static_cast<int>(G), kScatterThreads, scatter_smem, stream>>>(P, T, pts, n, G, starts, pts_b, pos);
+  auto ks = bin_scatter_kernel;
+  const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+      n_chunks, resident_blocks(ix->device, (const void*)ks, kScatterThreads, tile_smem))));
+  ks<<<grid_s, kScatterThreads, tile_smem, stream>>>(P, T, pts, n, ch, starts, pts_b, pos);
   auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<kHist, kCount, 0>
                               : binned_query_kernel<kHist, kCount, -1>;
   const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);
@@ -1009,18 +1026,18 @@ bool use_binned(const fm_index* ix, std::uint64_t n) {
   return kAutoBinned && n >= (std::uint64_t{1} << 22) && bytes >= 1e9 && bfrac >= 0.25;
 }
 
-// Tiles of 2^ts x 2^ts cells holding about `tile_bytes` of index (grid
-// entries + slot arena, averaged over the grid), at most kMaxTiles.
-TileGeom plan_tiles(const fm_index* ix, double tile_bytes) {
-  const double cells = std::max(1.0, static_cast<double>(ix->g.nx) * static_cast<double>(ix->g.ny));
-  const double per_cell = static_cast<double>(ix->stats.query_grid_bytes + ix->stats.arena_bytes) / cells;
+// Tiles of 2^ts x 2^ts cells holding about `tile_bytes` of index (query
+// grid + slot arena, averaged over the grid), at most kMaxTiles.
+TileGeom plan_tiles(const fm::GridGeom& g, const fm_index_stats& st, double tile_bytes) {
+  const double cells = std::max(1.0, static_cast<double>(g.nx) * static_cast<double>(g.ny));
+  const double per_cell = static_cast<double>(st.query_grid_bytes + st.arena_bytes) / cells;
   const double side = std::sqrt(tile_bytes / std::max(per_cell, 1.0));
   int ts = std::max(2, static_cast<int>(std::lround(std::log2(std::max(side, 1.0)))));
   TileGeom T;
   for (;; ++ts) {
     T.ts = ts;
-    T.tnx = static_cast<int>((ix->g.nx + (1ll << ts) - 1) >> ts);
-    T.tny = static_cast<int>((ix->g.ny + (1ll << ts) - 1) >> ts);
+    T.tnx = static_cast<int>((g.nx + (1ll << ts) - 1) >> ts);
+    T.tny = static_cast<int>((g.ny + (1ll << ts) - 1) >> ts);
     T.n_tiles = T.tnx * T.tny;
     if (T.n_tiles <= kMaxTiles) break;
   }
@@ -1206,16 +1223,19 @@ fm_status fold_grid(std::uint32_t* fine, int nx, int ny, std::uint64_t budget, i
   return FM_OK;
 }
 
-// Renumber the phase-1 slots in block-major order for blocks of 2^ls cells,
-// so every block's phase-1 slots are consecutive and its sub-block can name
-// them as base + offset (exact compact sub-blocks).  Phase-2 slots (split /
-// overflow subtrees, referenced from split slots) keep their numbers.
-fm_status renumber_slots(fm_index* ix, int ls) {
+// Renumber the phase-1 slots tile-major (tiles of 2^ts cells), block-major
+// inside tiles (blocks of 2^ls cells), so every block's phase-1 slots are
+// consecutive and its sub-block can name them as base + offset (exact
+// compact sub-blocks), and every tile's are contiguous.  Phase-2 slots
+// (split / overflow subtrees and double slots) keep their numbers.
+fm_status renumber_slots(fm_index* ix, int ts, int ls) {
   const std::uint64_t n1 = ix->host.n_phase1_slots;
-  if (ls == 0 || n1 == 0) return FM_OK;
+  if (n1 == 0) return FM_OK;
   const int nx = static_cast<int>(ix->g.nx), ny = static_cast<int>(ix->g.ny);
-  const int bnx = (nx + (1 << ls) - 1) >> ls, bny = (ny + (1 << ls) - 1) >> ls;
-  const std::uint64_t n_pos = (static_cast<std::uint64_t>(bnx) * bny) << (2 * ls);
+  ts = std::max(ts, ls);
+  RenumGeom R{ts, ls, (nx + (1 << ts) - 1) >> ts, nx, ny};
+  const int tny = (ny + (1 << ts) - 1) >> ts;
+  const std::uint64_t n_pos = (static_cast<std::uint64_t>(R.tnx) * tny) << (2 * ts);
   std::uint32_t *flag = nullptr, *idx = nullptr;
   std::uint8_t* fresh = nullptr;
   void* tmp = nullptr;
@@ -1225,7 +1245,7 @@ fm_status renumber_slots(fm_index* ix, int ls) {
   if (e == cudaSuccess) e = cudaMalloc(&fresh, ix->slots_len);
   const unsigned g1 = static_cast<unsigned>((n_pos + 255) / 256);
   if (e == cudaSuccess) {
-    renum_flag_kernel<<<g1, 256>>>(ix->d_grid, nx, ny, bnx, ls, n_pos, n1, flag);
+    renum_flag_kernel<<<g1, 256>>>(ix->d_grid, R, n_pos, n1, flag);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) {
@@ -1236,7 +1256,7 @@ fm_status renumber_slots(fm_index* ix, int ls) {
     e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, idx, static_cast<std::int64_t>(n_pos));
   }
   if (e == cudaSuccess) {
-    renum_apply_kernel<<<g1, 256>>>(ix->d_grid, nx, ny, bnx, ls, n_pos, flag, idx,
+    renum_apply_kernel<<<g1, 256>>>(ix->d_grid, R, n_pos, flag, idx,
                                     reinterpret_cast<const uint4*>(ix->d_slots),
                                     reinterpret_cast<uint4*>(fresh));
     e = cudaGetLastError();
@@ -1342,7 +1362,12 @@ fm_status finish_device(fm_index* ix, double approx_epsilon) {
   }
   const int nx = static_cast<int>(ix->g.nx), ny = static_cast<int>(ix->g.ny);
   const int qls = fold_ls(nx, ny, kQueryBudget, kQueryMaxLs);
-  fm_status st = renumber_slots(ix, qls);
+  // the binned path's default tiles (index bytes per cell before the fold:
+  // the flat grid plus the slot arena)
+  fm_index_stats pre = ix->stats;
+  pre.query_grid_bytes = ix->grid_len * 4;
+  const TileGeom T0 = plan_tiles(ix->g, pre, kTileBytes);
+  fm_status st = renumber_slots(ix, T0.ts, qls);
   if (st == FM_OK) {
     st = fold_grid(ix->d_grid, nx, ny, kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots,
                    kQueryMaxRatio, &ix->qgrid);
@@ -1350,7 +1375,7 @@ fm_status finish_device(fm_index* ix, double approx_epsilon) {
   if (st != FM_OK) return st;
   ix->stats.query_grid_bytes = ix->qgrid.bytes;
   ix->stats.query_block_log2 = ix->qgrid.ls;
-  ix->tiles = plan_tiles(ix, ix->tile_bytes > 0 ? ix->tile_bytes : kTileBytes);
+  ix->tiles = ix->tile_bytes > 0 ? plan_tiles(ix->g, ix->stats, ix->tile_bytes) : T0;
   ix->stats.approx_epsilon = approx_epsilon;
   // an epsilon too fine for the uniform approx grid: approximate queries
   // take the exact path (fm_index_stats.approx_grid_bytes stays 0)
@@ -1901,7 +1926,7 @@ fm_status fm_index_set_query_path(fm_index* index, int path, double tile_bytes) 
   }
   index->query_path = path;
   index->tile_bytes = tile_bytes;
-  if (index->device >= 0) index->tiles = plan_tiles(index, tile_bytes > 0 ? tile_bytes : kTileBytes);
+  if (index->device >= 0) index->tiles = plan_tiles(index->g, index->stats, tile_bytes > 0 ? tile_bytes : kTileBytes);
   return FM_OK;
 }
 
