@@ -21,10 +21,10 @@
 //                       table
 //   (cub exclusive scan of the table: entry (t, c) becomes the first
 //    binned position of chunk c's points in tile t)
-//   bin_scatter_kernel  per chunk: each point takes the next position of
-//                       its tile's run from a shared-memory cursor and is
-//                       written there (pts_b), its binned position to
-//                       pos[i] (coalesced)
+//   bin_scatter_kernel  per chunk, 4K points at a time: a shared-memory
+//                       counting sort by tile, then the points written out
+//                       run by run at the chunk's cursors (pts_b), their
+//                       binned positions to pos[i] (coalesced)
 //   binned_query_kernel the query over pts_b in order: locate, true hits
 //                       answered at once, boundary points through a
 //                       warp-private shared-memory ring whose batches of 32
@@ -127,48 +127,101 @@ __global__ void __launch_bounds__(kScatterThreads)
   }
 }
 
-// The scatter: per chunk, the shared-memory cursors start at the scanned
-// table entries of the chunk; each point takes the next position of its
-// tile's run with one shared-memory atomic (the chunk's per-tile counts are
-// exactly the table's, so the runs fill [start, start + count) whatever the
-// order) and is written there (pts_b), its binned position to pos[i]
-// (coalesced).  The cursor atomics of a thread's kScPer points issue back to
-// back before its stores.  Within a tile the points stay in chunk order,
+// The scatter.  Per chunk, the global cursors start at the scanned table
+// entries of the chunk; each kScatterIter-point iteration is counting-sorted
+// by tile in shared memory and then written out run by run, so consecutive
+// lanes store consecutive points of one run (whole lines) instead of each
+// lane storing 16 bytes into a different tile's run: scattering 16-byte
+// points into >= 16 interleaved fronts runs at 0.8-2.6 TB/s against 5.6 for
+// a copy (tools/exp_copy.cu, profiles/r2s).  Each point's binned position
+// goes to pos[i] (coalesced).  Within a tile the points stay in chunk order,
 // i.e. in about input order, so the gather in unbin_kernel is coherent.
 __global__ void __launch_bounds__(kScatterThreads)
     bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
                        std::uint64_t ch, const unsigned int* __restrict__ starts,
                        double2* __restrict__ pts_b, unsigned int* __restrict__ pos) {
-  extern __shared__ unsigned int s_cur[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nk = T.n_tiles + 1;
+  const int nk4 = (nk + 3) & ~3;
+  double2* stage = reinterpret_cast<double2*>(smem_raw);
+  std::uint16_t* skey = reinterpret_cast<std::uint16_t*>(smem_raw + kScatterIter * 16);
+  unsigned int* s_cnt = reinterpret_cast<unsigned int*>(smem_raw + kScatterIter * 18);
+  unsigned int* s_off = s_cnt + nk4;
+  unsigned int* s_gst = s_off + nk4;
+  __shared__ unsigned int s_part[kScatterThreads];
+  constexpr int kScanPer = (kMaxTiles + 1 + kScatterThreads - 1) / kScatterThreads;
   const std::uint64_t n_chunks = (n + ch - 1) / ch;
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
   for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cur[k] = starts[static_cast<std::uint64_t>(k) * n_chunks + c];
-    __syncthreads();
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_gst[k] = starts[static_cast<std::uint64_t>(k) * n_chunks + c];
     const std::uint64_t hi = min(n, (c + 1) * ch);
-    for (std::uint64_t i0 = c * ch + threadIdx.x; i0 < hi; i0 += kScatterIter) {
+    for (std::uint64_t base = c * ch; base < hi; base += kScatterIter) {
       double2 p[kScPer];
+      unsigned int kr[kScPer];
 #pragma unroll
       for (int j = 0; j < kScPer; ++j) {
-        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
         p[j] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
       }
-      unsigned int dst[kScPer];
+      __syncthreads();  // s_cnt zeroed, s_gst loaded / advanced
 #pragma unroll
       for (int j = 0; j < kScPer; ++j) {
-        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
-        dst[j] = i < hi ? atomicAdd(s_cur + tile_key(P, T, p[j].x, p[j].y), 1u) : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < kScPer; ++j) {
-        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+        kr[j] = 0xFFFFFFFFu;
         if (i < hi) {
-          pts_b[dst[j]] = p[j];
-          __stcs(pos + i, dst[j]);
+          const unsigned int key = static_cast<unsigned int>(tile_key(P, T, p[j].x, p[j].y));
+          kr[j] = (key << 16) | atomicAdd(s_cnt + key, 1u);
         }
       }
+      __syncthreads();
+      {  // exclusive scan of s_cnt over the tiles -> s_off
+        const int k0 = threadIdx.x * kScanPer;
+        unsigned int v[kScanPer], sum = 0;
+#pragma unroll
+        for (int q = 0; q < kScanPer; ++q) {
+          v[q] = k0 + q < nk ? s_cnt[k0 + q] : 0u;
+          sum += v[q];
+        }
+        s_part[threadIdx.x] = sum;
+        __syncthreads();
+        for (int o = 1; o < kScatterThreads; o <<= 1) {
+          const unsigned int x = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0u;
+          __syncthreads();
+          s_part[threadIdx.x] += x;
+          __syncthreads();
+        }
+        unsigned int run = threadIdx.x ? s_part[threadIdx.x - 1] : 0u;
+#pragma unroll
+        for (int q = 0; q < kScanPer; ++q) {
+          if (k0 + q < nk) s_off[k0 + q] = run;
+          run += v[q];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kScPer; ++j) {
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+        if (kr[j] != 0xFFFFFFFFu) {
+          const unsigned int key = kr[j] >> 16, r = kr[j] & 0xFFFFu;
+          const unsigned int k = s_off[key] + r;
+          stage[k] = p[j];
+          skey[k] = static_cast<std::uint16_t>(key);
+          __stcs(pos + i, s_gst[key] + r);
+        }
+      }
+      __syncthreads();
+      const int cnt = static_cast<int>(min(static_cast<std::uint64_t>(kScatterIter), hi - base));
+#pragma unroll 4
+      for (int k = threadIdx.x; k < cnt; k += kScatterThreads) {  // run by run, whole lines
+        const unsigned int key = skey[k];
+        pts_b[s_gst[key] + (k - s_off[key])] = stage[k];
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+        s_gst[k] += s_cnt[k];
+        s_cnt[k] = 0u;
+      }
     }
-    __syncthreads();  // s_cur is reloaded for the next chunk
   }
 }
 

@@ -295,24 +295,26 @@ __device__ __forceinline__ QItem load_item(const QItem* __restrict__ items, std:
   return it;
 }
 
-// Start copying the slots of the items held by lanes [0, n) into `buf`: each
-// lane copies its own item's slot (four 16-byte cp.async for a half slot,
-// eight for a full one) into its 128-byte pool entry, chunk c at c ^ (lane &
-// 7) so the reads in eval_staged are bank-conflict free.  The second half of
-// a double slot (kDoubleBit) is prefetched into L2, where its evaluation one
-// batch later finds it.
+// Start copying the slots of the items held by lanes [0, n) into `buf`: 8
+// lanes per slot, 16 bytes each, so every cp.async instruction requests 4
+// whole slots (lines) -- per-lane copies of its own slot measured far slower
+// on the stream path (c3: 47 -> 111 ms; each line requested in 8 pieces at
+// different times).  Chunk c of slot r is stored at chunk c ^ (r & 7) so
+// the owner lane's reads in eval_staged are bank-conflict free.  The second
+// half of a double slot (kDoubleBit) is prefetched into L2, where its
+// evaluation one batch later finds it.
 __device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* buf,
                                             std::uint32_t e, int n, int lane) {
-  if (lane < n) {
-    const std::uint8_t* g = fm::slot_ptr(P, e);
-    std::uint8_t* d = buf + lane * fm::kSlotBytes;
-    const int s = lane & 7;
+  if (lane < n && (e & fm::kDoubleBit) && !(e & fm::kHalfBit)) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(fm::slot_ptr(P, e) + fm::kSlotBytes));
+  }
+  const int c = lane & 7;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) cp_async16(d + 16 * (c ^ s), g + 16 * c);
-    if (!(e & fm::kHalfBit)) {
-#pragma unroll
-      for (int c = 4; c < 8; ++c) cp_async16(d + 16 * (c ^ s), g + 16 * c);
-      if (e & fm::kDoubleBit) asm volatile("prefetch.global.L2 [%0];" ::"l"(g + fm::kSlotBytes));
+  for (int q = 0; q < 8; ++q) {
+    const int r = 4 * q + (lane >> 3);
+    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
+    if (r < n && (c < 4 || !(er & fm::kHalfBit))) {  // half slots: first 64 bytes only
+      cp_async16(buf + r * fm::kSlotBytes + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
     }
   }
   cp_async_commit();
@@ -805,24 +807,49 @@ __global__ void __launch_bounds__(256)
 }
 
 int resident_blocks(int device, const void* kernel, int block, int smem) {
-  // SM count x resident CTAs per SM, cached per (device, kernel)
+  // SM count x resident CTAs per SM, cached per (device, kernel, block,
+  // smem).  Dynamic shared memory above 48 KB needs the kernel's opt-in
+  // limit raised first -- per size, since the binned path's kernels size
+  // theirs by the tile count (a launch above the limit would not run).
   struct Slot {
     int device;
     const void* kernel;
+    int block, smem;
     int blocks;
+  };
+  struct Limit {
+    int device;
+    const void* kernel;
+    int smem;
   };
   static std::mutex mu;
   static std::vector<Slot> cache;
+  static std::vector<Limit> limits;
   std::lock_guard<std::mutex> lk(mu);
+  if (smem > 48 * 1024) {
+    bool raised = false;
+    for (Limit& l : limits) {
+      if (l.device == device && l.kernel == kernel) {
+        if (l.smem < smem) {
+          cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          l.smem = smem;
+        }
+        raised = true;
+      }
+    }
+    if (!raised) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      limits.push_back({device, kernel, smem});
+    }
+  }
   for (const Slot& s : cache) {
-    if (s.device == device && s.kernel == kernel) return s.blocks;
+    if (s.device == device && s.kernel == kernel && s.block == block && s.smem == smem) return s.blocks;
   }
   int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
   const int blocks = std::max(1, sms) * std::max(1, per_sm);
-  cache.push_back({device, kernel, blocks});
+  cache.push_back({device, kernel, block, smem, blocks});
   return blocks;
 }
 
@@ -990,9 +1017,10 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   FM_CUDA(cub::DeviceScan::ExclusiveSum(scratch + o_tmp, cub_bytes, table, starts,
                                         static_cast<std::int64_t>(n_tab), stream));
   auto ks = bin_scatter_kernel;
+  const int sc_smem = kScatterIter * 18 + 3 * ((nk + 3) & ~3) * 4;
   const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      n_chunks, resident_blocks(ix->device, (const void*)ks, kScatterThreads, tile_smem))));
-  ks<<<grid_s, kScatterThreads, tile_smem, stream>>>(P, T, pts, n, ch, starts, pts_b, pos);
+      n_chunks, resident_blocks(ix->device, (const void*)ks, kScatterThreads, sc_smem))));
+  ks<<<grid_s, kScatterThreads, sc_smem, stream>>>(P, T, pts, n, ch, starts, pts_b, pos);
   auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<kHist, kCount, 0>
                               : binned_query_kernel<kHist, kCount, -1>;
   const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);
