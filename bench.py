@@ -454,8 +454,20 @@ def run_ours(args):
         except (ValueError, OSError):
             traffic = None
     binned = (not approx) and qplan["path"] == "binned"
-    per_call = 1 if approx else (4 if binned else 2)
-    n_calls = args.steps * sum(1 for _ in plan.chunks())
+    # our kernels per fm_query call (fastmap_b200.cu launch()): the stream
+    # path runs stream_kernel + resolve_kernel per 2^28-point slice, the
+    # binned path count + scatter + query + unbin per 2^30-point batch (the
+    # cub scan between count and scatter is a library kernel), approx one
+    # kernel; with a histogram, one widen_hist_kernel per slice / batch
+    launches_per_call = []
+    for _, cnt in plan.chunks():
+        if approx:
+            launches_per_call.append(1 + (1 if plan.hist else 0))
+        else:
+            unit = (1 << 30) if binned else (1 << 28)
+            pieces = -(-cnt // unit)
+            launches_per_call.append(pieces * ((4 if binned else 2) + (1 if plan.hist else 0)))
+    n_launches = args.steps * sum(launches_per_call)
 
     if rank == 0:
         line = {
@@ -489,9 +501,7 @@ def run_ours(args):
                          "traffic_source": "profiles/%s (ncu, cold cache)" % prof.name},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            # our kernels per fm_query call: 4 on the binned path (the cub
-            # scan between them is a library kernel), 2 on the stream path, 1 approx
-            "gpu_launches": n_calls * per_call,
+            "gpu_launches": n_launches,
             "clocks": clk.summary(),
             "parity": parity,
             "histogram_check": hist_check,

@@ -1040,18 +1040,19 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
 }
 
 // Query path for a batch of n points (fm_query_path): the binned path when
-// the index is far larger than L2 and mostly boundary slots -- then the
-// stream path's per-point gathers miss L2 (c3: 47 GB of slots, 60% boundary
-// cells; c4: 5.5 GB, 50%) -- and the batch is big enough to reuse tiles;
-// the stream path otherwise (c1; c2: 9% boundary cells).
-constexpr bool kAutoBinned = false;  // binned not yet faster than stream on c3/c4 (profiles/r2d)
+// the index is far larger than L2 and mostly boundary cells -- then the
+// stream path's per-point gathers miss L2 (c3: 15 GB of slots, 60% boundary
+// cells, binned 37.0 ms vs stream 46.8 ms per 1B points; c4: 6 GB, 50%,
+// 8.2 vs 8.8 ms per 200M, profiles/r2u) -- and the batch is big enough to
+// reuse tiles; the stream path otherwise (c1; c2: 9% boundary cells, 1.13
+// vs 2.8 ms per 100M).
 bool use_binned(const fm_index* ix, std::uint64_t n) {
   if (ix->query_path == FM_PATH_STREAM) return false;
   if (ix->query_path == FM_PATH_BINNED) return true;
   const double cells = static_cast<double>(ix->g.nx) * static_cast<double>(ix->g.ny);
   const double bfrac = cells > 0 ? static_cast<double>(ix->stats.cells_boundary) / cells : 0.0;
   const double bytes = static_cast<double>(ix->stats.query_grid_bytes + ix->stats.arena_bytes);
-  return kAutoBinned && n >= (std::uint64_t{1} << 22) && bytes >= 1e9 && bfrac >= 0.25;
+  return n >= (std::uint64_t{1} << 24) && bytes >= 1e9 && bfrac >= 0.25;
 }
 
 // Tiles of 2^ts x 2^ts cells holding about `tile_bytes` of index (query
@@ -1071,7 +1072,7 @@ TileGeom plan_tiles(const fm::GridGeom& g, const fm_index_stats& st, double tile
   }
   return T;
 }
-constexpr double kTileBytes = 32e6;
+constexpr double kTileBytes = 64e6;  // c3: 162 tiles (37.2 ms) vs 630 (40.3), profiles/r2u
 
 template <bool kHist, bool kCount>
 fm_status launch_approx_t(const fm_index* ix, const double2* pts, std::uint64_t n, int* d_out,

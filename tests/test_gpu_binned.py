@@ -95,11 +95,13 @@ def test_binned_histogram_counters_and_unaligned_output(dev):
 
 
 def test_auto_path_choice_follows_index_statistics(dev):
-    """Auto never picks binned for small or mostly true-hit indexes."""
+    """Auto picks binned for big, mostly-boundary indexes and big batches
+    (c3, c4), never for small or mostly true-hit indexes (c1, c2)."""
     c2 = fastmap.build_index(synth.config("c2").make_soup(), device=0)
     assert c2.query_plan(100_000_000)["path"] == "stream"       # 9% boundary cells
     c4 = fastmap.build_index(synth.config("c4").make_soup(), device=0)
     assert c4.query_plan(1000)["path"] == "stream"              # batch too small to reuse tiles
+    assert c4.query_plan(200_000_000)["path"] == "binned"       # 6 GB index, 50% boundary cells
     c4.set_query_path("binned")
     assert c4.query_plan(1000)["path"] == "binned"
     c1 = fastmap.build_index(synth.config("c1").make_soup(), device=0)
