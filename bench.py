@@ -486,7 +486,8 @@ def run_ours(args):
                 "index": {k: st[k] for k in ("nx", "ny", "cells_hit", "cells_boundary",
                                              "grid_bytes", "arena_bytes", "query_grid_bytes",
                                              "query_block_log2", "approx_grid_bytes",
-                                             "approx_block_log2")},
+                                             "approx_block_log2", "slots_total", "slots_double",
+                                             "cells_split", "build_phase_seconds")},
                 "index_build_s": build_s,
                 "query_path": None if approx else qplan,
             },

@@ -121,6 +121,11 @@ typedef struct fm_index_stats {
   int32_t query_block_log2;   /* its block side, log2 cells (0 = the flat grid itself) */
   int32_t approx_block_log2;  /* same for the approx cover */
   uint64_t slots_double;      /* 256-byte double leaf slots (polygon corners) */
+  /* GPU builder wall time per phase, seconds: [0] plan + upload, [1] spans +
+   * candidate CSR, [2] edge contributions, [3] classify + phase-1 slots,
+   * [4] host phase 2 (cells that fit no phase-1 slot), [5] final arrays.
+   * The renumbering / fold / approx cover after it are in build_seconds. */
+  double build_phase_seconds[6];
 } fm_index_stats;
 
 /* Optional per-call work counters (diagnostics; device-side atomics). */

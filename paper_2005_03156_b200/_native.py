@@ -65,10 +65,13 @@ class IndexStats(C.Structure):
         ("approx_epsilon", C.c_double), ("approx_grid_bytes", u64),
         ("query_grid_bytes", u64), ("query_block_log2", C.c_int32),
         ("approx_block_log2", C.c_int32), ("slots_double", u64),
+        ("build_phase_seconds", C.c_double * 6),
     ]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["build_phase_seconds"] = list(d["build_phase_seconds"])
+        return d
 
 
 class AssignCountersC(C.Structure):

@@ -128,6 +128,9 @@ using HistT = unsigned int;
 // that hashes to it (atomicCAS) and counted with shared-memory atomics;
 // a leaf whose slot is taken goes straight to the global counter.  The
 // cache is flushed into the global counters when the CTA exits.
+#ifndef FM_HIST_MODE
+#define FM_HIST_MODE 0
+#endif
 constexpr int kHotSlots = 1024;
 struct HistSink {
   HistT* g = nullptr;         // global per-launch counters
@@ -135,6 +138,14 @@ struct HistSink {
   unsigned int* cnt = nullptr;  // shared: their counts
   __device__ __forceinline__ void add(int id) const {
     const unsigned int u = static_cast<unsigned int>(id);
+#if FM_HIST_MODE == 1  // experiment: straight to the global counters
+    atomicAdd(g + u, 1u);
+    return;
+#elif FM_HIST_MODE == 2  // experiment: aggregated over equal ids of the active lanes
+    const unsigned int peers = __match_any_sync(__activemask(), u);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(g + u, static_cast<unsigned int>(__popc(peers)));
+    return;
+#endif
     const unsigned int s = (u * 2654435761u) >> 22;  // 10-bit multiplicative hash
     unsigned int t = tag[s];
     if (t == fm::kEmpty) {
@@ -1559,6 +1570,7 @@ fm_status fm_index_build(const double* vertex_lonlat, const std::uint64_t* ring_
   s.built_on_gpu = on_gpu ? 1 : 0;
   s.cells_split = ix->host.stats.cells_split;
   s.slots_double = ix->host.stats.slots_double;
+  for (int k = 0; k < 6; ++k) s.build_phase_seconds[k] = ix->host.stats.phase_s[k];
   s.slots_phase1 = ix->host.n_phase1_slots;
   s.slots_total = ix->host.n_slots;
   s.geometry_bytes = s.n_vertices * 16;

@@ -36,6 +36,10 @@ struct BuildStats {
   std::uint64_t records_overflow = 0;
   std::uint64_t cells_split = 0;  // split records (2x2 sub-cell nodes)
   std::uint64_t slots_double = 0; // double leaf slots (kind 4, 256 bytes)
+  // GPU builder wall time per phase (s): 0 plan + upload, 1 spans + candidate
+  // CSR, 2 contributions, 3 classify + phase-1 slots, 4 host phase 2,
+  // 5 final arrays
+  double phase_s[6] = {0, 0, 0, 0, 0, 0};
   // fast-approx epsilon finer than a uniform grid of <= 2^31 cells can
   // resolve: the grid is planned as for an exact index and approximate
   // queries are answered exactly (error 0 <= epsilon)

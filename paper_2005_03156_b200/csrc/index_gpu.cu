@@ -20,6 +20,8 @@
 //      handed to the host's phase 2 with their candidate lists.
 #include <cuda_runtime.h>
 
+#include <chrono>
+
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -575,10 +577,36 @@ inline unsigned grid1d(std::uint64_t n, unsigned b = 256) {
 // Builds the index on `device`.  Returns device arrays in `dev_*` (owned by
 // the caller) and fills `out` with the geometry, stats and -- when
 // keep_host -- host copies for comparison tests.
+// cell kinds counted on the device: counts[kind] += cells of that kind
+__global__ void kind_count_kernel(const std::uint8_t* kind, std::uint64_t n, unsigned long long* counts) {
+  __shared__ unsigned int s[4];
+  if (threadIdx.x < 4) s[threadIdx.x] = 0u;
+  __syncthreads();
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  unsigned int c[4] = {0u, 0u, 0u, 0u};
+  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const std::uint8_t k = kind[i];
+    c[k < 4 ? k : 3]++;
+  }
+  for (int k = 0; k < 4; ++k) {
+    if (c[k]) atomicAdd(s + k, c[k]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && s[threadIdx.x]) atomicAdd(counts + threadIdx.x, static_cast<unsigned long long>(s[threadIdx.x]));
+}
+
 void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex& out,
                      std::uint32_t** dev_grid, std::uint8_t** dev_slots, std::uint64_t* slots_len,
                      std::uint8_t** dev_overflow, std::uint64_t* overflow_len) {
   ck(cudaSetDevice(device), "cudaSetDevice");
+  double phase_s[6] = {0, 0, 0, 0, 0, 0};
+  auto t_mark = std::chrono::steady_clock::now();
+  auto lap = [&](int k) {  // wall time of phase k (device work included)
+    ck(cudaDeviceSynchronize(), "phase sync");
+    const auto now = std::chrono::steady_clock::now();
+    phase_s[k] += std::chrono::duration<double>(now - t_mark).count();
+    t_mark = now;
+  };
   out = HostIndex{};
   out.g = plan_grid(s, o, &out.stats);
   const GridGeom g = out.g;
@@ -594,6 +622,7 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
   ck(cudaMemcpy(d_ro.p, s.ring_off, 8 * (s.n_rings + 1), cudaMemcpyHostToDevice), "upload ring_off");
   if (P) ck(cudaMemcpy(d_pr.p, s.poly_ring, 8 * (P + 1), cudaMemcpyHostToDevice), "upload poly_ring");
   DevSoup ds{d_vxy.as<double>(), d_ro.as<std::uint64_t>(), d_pr.as<std::uint64_t>(), P};
+  lap(0);
   // 1. spans
   DevBuf d_spans, d_cpp, d_rpp;
   dalloc<PolySpan>(d_spans, P, "spans");
@@ -645,6 +674,7 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
   sort_cells_kernel<<<grid1d(n_cells), 256>>>(d_off.as<unsigned long long>(), n_cells,
                                                d_cand.as<std::uint32_t>());
   ck(cudaGetLastError(), "sort_cells_kernel");
+  lap(1);
   // 3. contributions
   DevBuf d_rec;
   dalloc<Contrib>(d_rec, n_pairs_cells, "contributions");
@@ -655,6 +685,7 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
         d_cand.as<std::uint32_t>(), d_rec.as<Contrib>());
     ck(cudaGetLastError(), "contrib_kernel");
   }
+  lap(2);
   // 4. classify cells, allocate phase-1 slots (row-major), write them
   DevBuf d_grid, d_kind, d_flags, d_pos;
   dalloc<std::uint32_t>(d_grid, n_cells, "grid");
@@ -711,18 +742,22 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
       ck(cudaMemcpy(cand_ids.data(), d_cids.p, 4 * cand_off[nd], cudaMemcpyDeviceToHost), "cands");
     }
   }
-  // stats of the GPU phase (cell kinds)
+  // stats of the GPU phase (cell kinds), counted on the device
   {
-    std::vector<std::uint8_t> kind_h(n_cells);
-    ck(cudaMemcpy(kind_h.data(), d_kind.p, n_cells, cudaMemcpyDeviceToHost), "kinds");
-    for (const std::uint8_t k : kind_h) {
-      if (k == kCellEmpty) out.stats.cells_empty++;
-      else if (k == kCellHit) out.stats.cells_hit++;
-      else out.stats.cells_boundary++;
-    }
+    DevBuf d_kc;
+    dalloc<unsigned long long>(d_kc, 4, "kind counts");
+    ck(cudaMemset(d_kc.p, 0, 32), "memset kind counts");
+    kind_count_kernel<<<1184, 256>>>(d_kind.as<std::uint8_t>(), n_cells, d_kc.as<unsigned long long>());
+    ck(cudaGetLastError(), "kind_count_kernel");
+    unsigned long long kc[4];
+    ck(cudaMemcpy(kc, d_kc.p, 32, cudaMemcpyDeviceToHost), "kind counts");
+    out.stats.cells_empty += kc[kCellEmpty];
+    out.stats.cells_hit += kc[kCellHit];
+    out.stats.cells_boundary += n_cells - kc[kCellEmpty] - kc[kCellHit];
     out.stats.records += n1;
     out.stats.records_compact += n1;
   }
+  lap(3);
   std::vector<std::uint32_t> grid_h;  // only entries of deferred cells are used
   std::vector<std::uint8_t> slots2, ovf2;
   if (nd) {
@@ -746,6 +781,7 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
                                         d_grid.as<std::uint32_t>());
     ck(cudaGetLastError(), "scatter_kernel");
   }
+  lap(4);
   // final device arrays: slots = phase 1 ++ phase 2, overflow (+ zero tail)
   const std::uint64_t n_slots = n1 + slots2.size() / kSlotBytes;
   std::uint8_t* slots = nullptr;
@@ -768,7 +804,8 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
   *overflow_len = ovf2.size();
   out.n_slots = n_slots;
   out.n_phase1_slots = n1;
-  out.stats.n_edges = out.stats.n_edges;
+  lap(5);
+  for (int k = 0; k < 6; ++k) out.stats.phase_s[k] = phase_s[k];
 }
 
 }  // namespace fm

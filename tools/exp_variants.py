@@ -18,8 +18,10 @@ import torch
 from paper_2005_03156_b200 import _native as N
 from paper_2005_03156_b200 import fastmap, synth
 
+import os
 name, n, path, tb = sys.argv[1], int(float(sys.argv[2])), sys.argv[3], float(sys.argv[4])
 libs = sys.argv[5:]
+with_hist = os.environ.get("EXPV_HIST", "0") == "1"  # also build the per-block histogram
 cfg = synth.config(name)
 soup = cfg.make_soup()
 t0 = time.time()
@@ -28,6 +30,7 @@ print(json.dumps({"config": name, "n": n, "build_s": time.time() - t0}), flush=T
 pts = torch.empty((n, 2), dtype=torch.float64, device="cuda")
 cfg.make_points_device(pts, soup=soup)
 out = torch.empty(n, dtype=torch.int32, device="cuda")
+hist = torch.zeros(soup.n_polys, dtype=torch.int64, device="cuda") if with_hist else None
 code = {"stream": N.PATH_STREAM, "binned": N.PATH_BINNED}[path]
 
 
@@ -39,7 +42,8 @@ def run(L, reps=3):
     s = torch.cuda.current_stream().cuda_stream
 
     def q():
-        assert L.fm_query_mode(idx.handle, 0, pts.data_ptr(), n, out.data_ptr(), None, None, s) == 0
+        assert L.fm_query_mode(idx.handle, 0, pts.data_ptr(), n, out.data_ptr(),
+                               hist.data_ptr() if hist is not None else None, None, s) == 0
     for _ in range(2):
         q()
     torch.cuda.synchronize()
@@ -55,7 +59,7 @@ def run(L, reps=3):
 base = N.lib()
 ms = run(base)
 ref = out.clone()
-print(json.dumps({"lib": "default", "path": path, "ms": ms}), flush=True)
+print(json.dumps({"lib": "default", "path": path, "hist": with_hist, "ms": ms}), flush=True)
 for lp in libs:
     L = C.CDLL(lp, mode=C.RTLD_LOCAL)
     ms = run(L)
