@@ -455,6 +455,62 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
   }
 }
 
+// The per-block histogram of a binned batch, from res[] in binned order
+// (after binned_query_kernel, which then runs without histogram code).  A
+// CTA takes chunks of kHistChunk consecutive answers -- one tile's points,
+// so a few thousand distinct leaves at most and, in clustered streams, many
+// repeats -- and aggregates them in a shared-memory hash table (open
+// addressing, kHistSlots keys) before one global atomic per distinct leaf.
+// Answers whose probe sequence finds no free slot go straight to the global
+// counters.
+constexpr int kHistThreads = 512;
+constexpr int kHistChunk = 16384;
+constexpr int kHistSlots = 4096;
+constexpr int kHistProbes = 8;
+
+__global__ void __launch_bounds__(kHistThreads)
+    binned_hist_kernel(const int* __restrict__ res, std::uint64_t n, HistT* __restrict__ hist) {
+  __shared__ unsigned int s_key[kHistSlots];
+  __shared__ unsigned int s_cnt[kHistSlots];
+  for (int k = threadIdx.x; k < kHistSlots; k += blockDim.x) {
+    s_key[k] = fm::kEmpty;
+    s_cnt[k] = 0u;
+  }
+  const std::uint64_t n_chunks = (n + kHistChunk - 1) / kHistChunk;
+  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    __syncthreads();
+    const std::uint64_t lo = c * kHistChunk, hi = min(n, lo + kHistChunk);
+    for (std::uint64_t i = lo + threadIdx.x; i < hi; i += kHistThreads) {
+      const int id = __ldcs(res + i);
+      if (id < 0) continue;
+      const unsigned int u = static_cast<unsigned int>(id);
+      unsigned int h = (u * 2654435761u) >> 20;  // 12-bit multiplicative hash
+      bool done = false;
+      for (int q = 0; q < kHistProbes && !done; ++q, h = (h + 1) & (kHistSlots - 1)) {
+        unsigned int t = s_key[h];
+        if (t == fm::kEmpty) {
+          t = atomicCAS(s_key + h, fm::kEmpty, u);
+          if (t == fm::kEmpty) t = u;
+        }
+        if (t == u) {
+          atomicAdd(s_cnt + h, 1u);
+          done = true;
+        }
+      }
+      if (!done) atomicAdd(hist + u, 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHistSlots; k += blockDim.x) {
+      const unsigned int key = s_key[k];
+      if (key != fm::kEmpty) {
+        atomicAdd(hist + key, s_cnt[k]);
+        s_key[k] = fm::kEmpty;
+        s_cnt[k] = 0u;
+      }
+    }
+  }
+}
+
 // out[i] = res[pos[i]].  CTAs take blocks of kUnbinBlock points in
 // increasing order from the work counter, four points per thread per round
 // (16-byte pos loads and id stores when `out` is 16-byte aligned).

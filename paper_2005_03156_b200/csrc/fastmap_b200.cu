@@ -145,7 +145,14 @@ struct HistSink {
     const unsigned int peers = __match_any_sync(__activemask(), u);
     if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(g + u, static_cast<unsigned int>(__popc(peers)));
     return;
+#elif FM_HIST_MODE == 3  // experiment: aggregated, then the hot-leaf cache
+    const unsigned int peers = __match_any_sync(__activemask(), u);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) add_n(u, static_cast<unsigned int>(__popc(peers)));
+    return;
 #endif
+    add_n(u, 1u);
+  }
+  __device__ __forceinline__ void add_n(unsigned int u, unsigned int k) const {
     const unsigned int s = (u * 2654435761u) >> 22;  // 10-bit multiplicative hash
     unsigned int t = tag[s];
     if (t == fm::kEmpty) {
@@ -153,9 +160,9 @@ struct HistSink {
       if (t == fm::kEmpty) t = u;
     }
     if (t == u) {
-      atomicAdd(cnt + s, 1u);
+      atomicAdd(cnt + s, k);
     } else {
-      atomicAdd(g + u, 1u);
+      atomicAdd(g + u, k);
     }
   }
 };
@@ -748,9 +755,11 @@ __global__ void __launch_bounds__(256)
   if (p >= n_pos) return;
   std::uint64_t c;
   std::uint32_t f = 0;
-  if (block_major_cell(p, R, &c)) {
+  if (block_major_cell(p, R, &c)) {  // slot indices the cell's phase-1 slot takes (double: 2)
     const std::uint32_t e = grid[c];
-    f = (e != fm::kEmpty && e >= fm::kRecordBit && (e & fm::kSlotIndexMask) < n1) ? 1u : 0u;
+    f = (e != fm::kEmpty && e >= fm::kRecordBit && (e & fm::kSlotIndexMask) < n1)
+            ? ((e & fm::kDoubleBit) && !(e & fm::kHalfBit) ? 2u : 1u)
+            : 0u;
   }
   flag[p] = f;
 }
@@ -765,8 +774,8 @@ __global__ void __launch_bounds__(256)
   block_major_cell(p, R, &c);
   const std::uint32_t e = grid[c];
   const std::uint64_t ko = e & fm::kSlotIndexMask, kn = idx[p];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) new_slots[kn * 8 + q] = old_slots[ko * 8 + q];
+  const int nq = 8 * static_cast<int>(flag[p]);  // 16-byte chunks: 8 per slot index
+  for (int q = 0; q < nq; ++q) new_slots[kn * 8 + q] = old_slots[ko * 8 + q];
   grid[c] = (e & ~fm::kSlotIndexMask) | static_cast<std::uint32_t>(kn);
 }
 
@@ -1032,13 +1041,22 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       n_chunks, resident_blocks(ix->device, (const void*)ks, kScatterThreads, sc_smem))));
   ks<<<grid_s, kScatterThreads, sc_smem, stream>>>(P, T, pts, n, ch, starts, pts_b, pos);
-  auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<kHist, kCount, 0>
-                              : binned_query_kernel<kHist, kCount, -1>;
+  // the histogram is counted from res afterwards (binned_hist_kernel): in
+  // binned order its leaves repeat within a chunk, and the query kernel
+  // stays free of per-point counter atomics
+  auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<false, kCount, 0>
+                              : binned_query_kernel<false, kCount, -1>;
   const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);
   const int grid_q = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       (n_tiles + kQWarps * kQGroup - 1) / (kQWarps * kQGroup),
       resident_blocks(ix->device, (const void*)kq, kQWarps * 32, kSmemQ))));
-  kq<<<grid_q, kQWarps * 32, kSmemQ, stream>>>(P, pts_b, n, res, d_hist, d_counters, work);
+  kq<<<grid_q, kQWarps * 32, kSmemQ, stream>>>(P, pts_b, n, res, nullptr, d_counters, work);
+  if (kHist) {
+    auto kh = binned_hist_kernel;
+    const int grid_h = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+        (n + kHistChunk - 1) / kHistChunk, resident_blocks(ix->device, (const void*)kh, kHistThreads, 0))));
+    kh<<<grid_h, kHistThreads, 0, stream>>>(res, n, d_hist);
+  }
   auto ku = unbin_kernel;
   const int grid_u = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       (n + kUnbinBlock - 1) / kUnbinBlock,

@@ -269,11 +269,11 @@ __device__ __forceinline__ bool same_pt(double ax, double ay, double bx, double 
          __double_as_longlong(ay) == __double_as_longlong(by);
 }
 
-enum : int { kCellEmpty = 0, kCellHit = 1, kCellSlot = 2, kCellDefer = 3 };
+enum : int { kCellEmpty = 0, kCellHit = 1, kCellSlot = 2, kCellDefer = 3, kCellDouble = 4 };
 
-// Device port of RowWorker::finalize + encode_slot (phase 1 only).  Returns
-// the cell kind; for kCellHit sets *hit, for kCellSlot writes slot[128] when
-// non-null.
+// Device port of RowWorker::finalize + encode_slot / encode_double_slot
+// (phase 1 only).  Returns the cell kind; for kCellHit sets *hit, for
+// kCellSlot writes slot[128] and for kCellDouble slot[256] when non-null.
 __device__ int finalize_cell(const DevSoup& s, const Contrib* recs, std::uint64_t m,
                              std::uint32_t* hit, std::uint8_t* slot) {
   E4 U[kCellEdges];
@@ -352,8 +352,9 @@ __device__ int finalize_cell(const DevSoup& s, const Contrib* recs, std::uint64_
       ced[c][k] = static_cast<std::uint8_t>(remap[e]);
     }
   }
-  // encode_slot
-  if (nc > static_cast<int>(kSlotMaxCands)) return kCellDefer;
+  // encode_slot, else encode_double_slot: the same distinct breakpoints and
+  // chains, wider capacities
+  if (nc > static_cast<int>(kDblMaxCands)) return kCellDefer;
   double ub[kCellCands * kBreakCap];
   int nub = 0;
   for (int c = 0; c < nc; ++c) {
@@ -363,14 +364,18 @@ __device__ int finalize_cell(const DevSoup& s, const Contrib* recs, std::uint64_
       if (!found) ub[nub++] = cbr[c][k];
     }
   }
-  if (nub > static_cast<int>(kSlotMaxBreaks)) return kCellDefer;
-  if (nub == 2 && ub[1] < ub[0]) {
-    const double t = ub[0];
-    ub[0] = ub[1];
-    ub[1] = t;
+  if (nub > static_cast<int>(kDblMaxBreaks)) return kCellDefer;
+  for (int a = 1; a < nub; ++a) {  // ascending (std::sort)
+    const double t = ub[a];
+    int b = a - 1;
+    while (b >= 0 && ub[b] > t) {
+      ub[b + 1] = ub[b];
+      --b;
+    }
+    ub[b + 1] = t;
   }
   // chain_edges (record_encode.h), literal port
-  double vx[kSlotMaxVerts], vy[kSlotMaxVerts];
+  double vx[kDblMaxVerts], vy[kDblMaxVerts];
   int nv = 0;
   std::uint32_t chain_mask = 0;
   int bit_of[kCellEdges];
@@ -432,7 +437,7 @@ __device__ int finalize_cell(const DevSoup& s, const Contrib* recs, std::uint64_
         grew = true;
       }
     }
-    if (nv + len > static_cast<int>(kSlotMaxVerts)) return kCellDefer;
+    if (nv + len > static_cast<int>(kDblMaxVerts)) return kCellDefer;
     chain_mask |= 1u << nv;
     for (int q = 0; q < nce; ++q) bit_of[ce[q]] = nv + q;
     for (int q = 0; q < len; ++q) {
@@ -440,6 +445,43 @@ __device__ int finalize_cell(const DevSoup& s, const Contrib* recs, std::uint64_
       vy[nv + q] = cy[q];
     }
     nv += len;
+  }
+  const bool leaf = nc <= static_cast<int>(kSlotMaxCands) && nub <= static_cast<int>(kSlotMaxBreaks) &&
+                    nv <= static_cast<int>(kSlotMaxVerts);
+  if (!leaf) {  // double leaf slot (index_format.h, kind 4)
+    if (slot) {
+      std::uint32_t w[64];
+      for (int k = 0; k < 64; ++k) w[k] = 0;
+      w[0] = kSlotDouble | (static_cast<std::uint32_t>(nv) << 8) | (static_cast<std::uint32_t>(nc) << 16) |
+             (static_cast<std::uint32_t>(nub) << 24);
+      w[1] = chain_mask;
+      for (int c = 0; c < nc; ++c) {
+        w[2 + c] = cid[c];
+        std::uint32_t mask = 0;
+        for (int k = 0; k < nced[c]; ++k) mask |= 1u << bit_of[ced[c][k]];
+        std::uint32_t info = (cc0[c] & 1u) << 7;
+        for (int k = 0; k < cnb[c]; ++k) {
+          for (int j = 0; j < nub; ++j) info |= cbr[c][k] == ub[j] ? (1u << j) : 0u;
+        }
+        w[10 + c / 2] |= (mask & 0xFFFFu) << (16 * (c & 1));
+        w[14 + c / 4] |= (info & 0xFFu) << (8 * (c & 3));
+      }
+      for (int j = 0; j < nub; ++j) {
+        const unsigned long long b = __double_as_longlong(ub[j]);
+        w[16 + 2 * j] = static_cast<std::uint32_t>(b);
+        w[17 + 2 * j] = static_cast<std::uint32_t>(b >> 32);
+      }
+      for (int k = 0; k < nv; ++k) {
+        const unsigned long long x = __double_as_longlong(vx[k]), y = __double_as_longlong(vy[k]);
+        w[24 + 4 * k] = static_cast<std::uint32_t>(x);
+        w[25 + 4 * k] = static_cast<std::uint32_t>(x >> 32);
+        w[26 + 4 * k] = static_cast<std::uint32_t>(y);
+        w[27 + 4 * k] = static_cast<std::uint32_t>(y >> 32);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(slot);
+      for (int k = 0; k < 16; ++k) dst[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    }
+    return kCellDouble;
   }
   if (slot) {
     std::uint32_t w[32];
@@ -492,7 +534,7 @@ __global__ void write_slots_kernel(DevSoup s, const unsigned long long* off, con
                                    const unsigned long long* slot_idx, std::uint32_t* grid,
                                    std::uint8_t* slots) {
   const std::uint64_t cell = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-  if (cell >= n_cells || kind[cell] != kCellSlot) return;
+  if (cell >= n_cells || (kind[cell] != kCellSlot && kind[cell] != kCellDouble)) return;
   std::uint32_t hit = 0;
   const unsigned long long k = slot_idx[cell];
   std::uint8_t* slot = slots + k * kSlotBytes;
@@ -504,6 +546,12 @@ __global__ void flag_kernel(const std::uint8_t* kind, std::uint64_t n, int want,
                             unsigned long long* flags) {
   const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
   if (i < n) flags[i] = kind[i] == want ? 1ull : 0ull;
+}
+
+// phase-1 slot positions: a leaf slot takes one slot index, a double two
+__global__ void slot_flag_kernel(const std::uint8_t* kind, std::uint64_t n, unsigned long long* flags) {
+  const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) flags[i] = kind[i] == kCellSlot ? 1ull : (kind[i] == kCellDouble ? 2ull : 0ull);
 }
 
 __global__ void compact_kernel(const std::uint8_t* kind, std::uint64_t n, int want,
@@ -583,10 +631,10 @@ __global__ void kind_count_kernel(const std::uint8_t* kind, std::uint64_t n, uns
   if (threadIdx.x < 4) s[threadIdx.x] = 0u;
   __syncthreads();
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-  unsigned int c[4] = {0u, 0u, 0u, 0u};
+  unsigned int c[4] = {0u, 0u, 0u, 0u};  // empty, hit, other (boundary), -
   for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
     const std::uint8_t k = kind[i];
-    c[k < 4 ? k : 3]++;
+    c[k < 2 ? k : 2]++;
   }
   for (int k = 0; k < 4; ++k) {
     if (c[k]) atomicAdd(s + k, c[k]);
@@ -695,16 +743,21 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
   classify_cells_kernel<<<grid1d(n_cells, 128), 128>>>(ds, d_off.as<unsigned long long>(), d_rec.as<Contrib>(),
                                                   n_cells, d_grid.as<std::uint32_t>(), d_kind.as<std::uint8_t>());
   ck(cudaGetLastError(), "classify_cells_kernel");
-  auto count_kind = [&](int want) {
+  auto count_kind = [&](int want) {  // want < 0: phase-1 slot indices (slot 1, double 2)
     ck(cudaMemset(d_flags.p, 0, 8 * (n_cells + 1)), "memset flags");
-    flag_kernel<<<grid1d(n_cells), 256>>>(d_kind.as<std::uint8_t>(), n_cells, want,
-                                          d_flags.as<unsigned long long>());
+    if (want < 0) {
+      slot_flag_kernel<<<grid1d(n_cells), 256>>>(d_kind.as<std::uint8_t>(), n_cells,
+                                                 d_flags.as<unsigned long long>());
+    } else {
+      flag_kernel<<<grid1d(n_cells), 256>>>(d_kind.as<std::uint8_t>(), n_cells, want,
+                                            d_flags.as<unsigned long long>());
+    }
     exclusive_scan_u64(d_flags.as<unsigned long long>(), d_pos.as<unsigned long long>(), n_cells + 1);
     unsigned long long total = 0;
     ck(cudaMemcpy(&total, d_pos.as<unsigned long long>() + n_cells, 8, cudaMemcpyDeviceToHost), "count");
     return total;
   };
-  const unsigned long long n1 = count_kind(kCellSlot);
+  const unsigned long long n1 = count_kind(-1);
   if (n1 > kMaxSlots) throw RuntimeError("index needs more than 2^29 slots");
   DevBuf d_slots1;
   dalloc<std::uint8_t>(d_slots1, std::max<unsigned long long>(n1, 1) * kSlotBytes, "slots");
@@ -754,8 +807,10 @@ void build_index_gpu(const Soup& s, const BuildOptions& o, int device, HostIndex
     out.stats.cells_empty += kc[kCellEmpty];
     out.stats.cells_hit += kc[kCellHit];
     out.stats.cells_boundary += n_cells - kc[kCellEmpty] - kc[kCellHit];
-    out.stats.records += n1;
-    out.stats.records_compact += n1;
+    const unsigned long long n_dbl = count_kind(kCellDouble);
+    out.stats.slots_double += n_dbl;
+    out.stats.records += n1 - n_dbl;  // a double slot is one record in two slot indices
+    out.stats.records_compact += n1 - n_dbl;
   }
   lap(3);
   std::vector<std::uint32_t> grid_h;  // only entries of deferred cells are used

@@ -283,10 +283,6 @@ struct RowWorker {
       es.compact++;
       return slot_entry(k, slot[0], slot[1], slot[2], slot[3]);
     }
-    if (deferred) {  // phase 1: cells that need a split or overflow wait for phase 2
-      *deferred = true;
-      return kEmpty;
-    }
     std::uint8_t dbl[2 * kSlotBytes];
     if (encode_double_slot(used, cin, dbl)) {  // e.g. a polygon corner: two slots, one read
       const std::uint64_t k = slots.size() / kSlotBytes;
@@ -295,6 +291,10 @@ struct RowWorker {
       es.compact++;
       st.slots_double++;
       return slot_entry(k, kSlotDouble, 0, 0, 0);
+    }
+    if (deferred) {  // phase 1: cells that need a split or overflow wait for phase 2
+      *deferred = true;
+      return kEmpty;
     }
     // A cell that fits neither a slot nor a double slot but a small compact
     // record takes the record (an overflow slot pointing at it) rather than
