@@ -464,7 +464,13 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
 // Answers whose probe sequence finds no free slot go straight to the global
 // counters.
 constexpr int kHistThreads = 512;
-constexpr int kHistChunk = 16384;
+#ifndef FM_HIST_CHUNK
+#define FM_HIST_CHUNK 16384
+#endif
+#ifndef FM_HIST_AGG
+#define FM_HIST_AGG 0  // experiments: 1 = __match_any_sync aggregation before the table
+#endif
+constexpr int kHistChunk = FM_HIST_CHUNK;
 constexpr int kHistSlots = 4096;
 constexpr int kHistProbes = 8;
 
@@ -482,7 +488,14 @@ __global__ void __launch_bounds__(kHistThreads)
     const std::uint64_t lo = c * kHistChunk, hi = min(n, lo + kHistChunk);
     for (std::uint64_t i = lo + threadIdx.x; i < hi; i += kHistThreads) {
       const int id = __ldcs(res + i);
+#if FM_HIST_AGG
+      const unsigned int peers = __match_any_sync(__activemask(), static_cast<unsigned int>(id));
+      if (id < 0 || (threadIdx.x & 31) != static_cast<unsigned int>(__ffs(peers) - 1)) continue;
+      const unsigned int inc = static_cast<unsigned int>(__popc(peers));
+#else
       if (id < 0) continue;
+      const unsigned int inc = 1u;
+#endif
       const unsigned int u = static_cast<unsigned int>(id);
       unsigned int h = (u * 2654435761u) >> 20;  // 12-bit multiplicative hash
       bool done = false;
@@ -493,11 +506,11 @@ __global__ void __launch_bounds__(kHistThreads)
           if (t == fm::kEmpty) t = u;
         }
         if (t == u) {
-          atomicAdd(s_cnt + h, 1u);
+          atomicAdd(s_cnt + h, inc);
           done = true;
         }
       }
-      if (!done) atomicAdd(hist + u, 1u);
+      if (!done) atomicAdd(hist + u, inc);
     }
     __syncthreads();
     for (int k = threadIdx.x; k < kHistSlots; k += blockDim.x) {
