@@ -240,67 +240,12 @@ __global__ void __launch_bounds__(kScatterThreads)
 constexpr int kQWarps = 8;
 constexpr int kQCap = 128;
 constexpr int kDCap = 128;
-#ifndef FM_BULK
-#define FM_BULK 0
-#endif
-// FM_BULK: batches staged by one bulk copy (TMA, cp.async.bulk) per slot
-// into 144-byte entries (conflict-free rows without a swizzle), completion
-// tracked by one mbarrier per pool buffer; else 8 lanes x 16-byte cp.async
-// per slot (stage_slots)
-constexpr int kPoolStride = FM_BULK ? 144 : static_cast<int>(fm::kSlotBytes);
 struct WarpSmemQ {
-  alignas(16) std::uint8_t pool[2][32 * kPoolStride];
+  alignas(16) std::uint8_t pool[2][32 * fm::kSlotBytes];
   double qx[kQCap], qy[kQCap];
   std::uint32_t qk[kQCap], qe[kQCap];
   std::uint32_t dk[kDCap], de[kDCap];
-  alignas(8) unsigned long long mbar[2];
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* m) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned long long* m, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(m)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned long long* m) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(m))
-      : "memory");
-}
-
-// Bulk-copy staging of the items held by lanes [0, n) into buffer b.
-__device__ __forceinline__ void stage_bulk(const fm::KParams& P, WarpSmemQ& S, int b, std::uint32_t e,
-                                           int n, int lane) {
-  const unsigned bytes = lane < n ? ((e & fm::kHalfBit) ? 64u : 128u) : 0u;
-  const unsigned total = __reduce_add_sync(0xFFFFFFFFu, bytes);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier reads of the buffer first
-  if (lane == 0) mbar_expect(&S.mbar[b], total);
-  __syncwarp();
-  if (bytes) {
-    const std::uint8_t* g = fm::slot_ptr(P, e);
-    bulk_copy(S.pool[b] + lane * kPoolStride, g, bytes, &S.mbar[b]);
-    if ((e & fm::kDoubleBit) && !(e & fm::kHalfBit)) {
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(g + fm::kSlotBytes));
-    }
-  }
-}
 constexpr int kSmemQ = static_cast<int>(sizeof(WarpSmemQ)) * kQWarps;
 
 struct RingState {
@@ -309,7 +254,6 @@ struct RingState {
   int pb = 0;
   QItem pit;             // this lane's staged item
   int dhead = 0, dn = 0; // double-slot ring
-  unsigned ph = 0;       // FM_BULK: mbarrier phase parity per buffer (bit b)
 };
 
 // Evaluate double-slot points in batches of 32 (any remainder when draining).
@@ -368,26 +312,17 @@ __device__ __forceinline__ void pump(const fm::KParams& P, WarpSmemQ& S, RingSta
       R.head = (R.head + m) & (kQCap - 1);
       R.qn -= m;
       __syncwarp();
-#if FM_BULK
-      stage_bulk(P, S, R.pb ^ 1, nit.e, m, lane);
-#else
       stage_slots(P, S.pool[R.pb ^ 1], nit.e, m, lane);  // commits one group
-#endif
     }
     if (R.pend > 0) {
-#if FM_BULK
-      mbar_wait(&S.mbar[R.pb], (R.ph >> R.pb) & 1u);
-      R.ph ^= 1u << R.pb;
-#else
       if (stage) {
         cp_async_wait1();
       } else {
         cp_async_wait0();
       }
-#endif
       __syncwarp();
-      const std::uint32_t ce = eval_staged<kHist, kCount, FM_BULK ? kPoolStride : 0>(
-          P, S.pool[R.pb], R.pit, R.pend, lane, res, hist, wc);
+      const std::uint32_t ce = eval_staged<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res,
+                                                          hist, wc);
       const std::uint32_t rq = __ballot_sync(0xFFFFFFFFu, ce != 0u);
       if (ce != 0u) {  // split cell: the child entry goes back into the ring
         const int s = (R.head + R.qn + __popc(rq & ((1u << lane) - 1u))) & (kQCap - 1);
@@ -420,14 +355,6 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
   const HistSink hs = hist_open<kHist>(hist, hot);
   WarpSmemQ& S = reinterpret_cast<WarpSmemQ*>(dsmem)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
-#if FM_BULK
-  if (lane == 0) {
-    mbar_init(&S.mbar[0]);
-    mbar_init(&S.mbar[1]);
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-#endif
   const std::uint64_t tile = 32ull * kU;
   const std::uint64_t n_tiles = (n + tile - 1) / tile;
   const std::uint32_t lt_mask = (1u << lane) - 1u;

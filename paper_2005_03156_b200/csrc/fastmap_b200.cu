@@ -346,9 +346,7 @@ __device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* 
 
 // Evaluate the staged batch.  Returns, per lane, the child entry a split
 // cell descends to (to be re-queued) or 0 when the item is finished.
-// kStride 0: the stage_slots layout (128-byte entries, chunk c at c ^ (lane
-// & 7)); else plain entries kStride bytes apart (bulk-copy staging).
-template <bool kHist, bool kCount, int kStride = 0>
+template <bool kHist, bool kCount>
 __device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const std::uint8_t* buf,
                                                      const QItem& it, int n, int lane,
                                                      int* __restrict__ out,
@@ -356,17 +354,11 @@ __device__ __forceinline__ std::uint32_t eval_staged(const fm::KParams& P, const
                                                      fm::WorkCount& wc) {
   std::uint32_t requeue = 0;
   if (lane < n) {
+    const std::uint8_t* base = buf + lane * fm::kSlotBytes;
+    const int s = lane & 7;
     uint4 c[8];
-    if (kStride == 0) {
-      const std::uint8_t* base = buf + lane * fm::kSlotBytes;
-      const int s = lane & 7;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = *reinterpret_cast<const uint4*>(base + 16 * (k ^ s));
-    } else {
-      const std::uint8_t* base = buf + lane * kStride;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = *reinterpret_cast<const uint4*>(base + 16 * k);
-    }
+    for (int k = 0; k < 8; ++k) c[k] = *reinterpret_cast<const uint4*>(base + 16 * (k ^ s));
     const std::uint32_t kind = c[0].x & 0xFFu;
     int id = -1;
     bool done = true;
