@@ -144,11 +144,11 @@ __global__ void __launch_bounds__(kScatterThreads)
   const int nk = T.n_tiles + 1;
   const int nk4 = (nk + 3) & ~3;
   double2* stage = reinterpret_cast<double2*>(smem_raw);
-  std::uint16_t* skey = reinterpret_cast<std::uint16_t*>(smem_raw + kScatterIter * 16);
-  unsigned int* s_cnt = reinterpret_cast<unsigned int*>(smem_raw + kScatterIter * 18);
+  unsigned int* sdst = reinterpret_cast<unsigned int*>(smem_raw + kScatterIter * 16);
+  unsigned int* s_cnt = reinterpret_cast<unsigned int*>(smem_raw + kScatterIter * 20);
   unsigned int* s_off = s_cnt + nk4;
   unsigned int* s_gst = s_off + nk4;
-  __shared__ unsigned int s_part[kScatterThreads];
+  __shared__ unsigned int s_part[64];
   constexpr int kScanPer = (kMaxTiles + 1 + kScatterThreads - 1) / kScatterThreads;
   const std::uint64_t n_chunks = (n + ch - 1) / ch;
   for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
@@ -182,15 +182,29 @@ __global__ void __launch_bounds__(kScatterThreads)
           v[q] = k0 + q < nk ? s_cnt[k0 + q] : 0u;
           sum += v[q];
         }
-        s_part[threadIdx.x] = sum;
-        __syncthreads();
-        for (int o = 1; o < kScatterThreads; o <<= 1) {
-          const unsigned int x = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0u;
-          __syncthreads();
-          s_part[threadIdx.x] += x;
-          __syncthreads();
+        // block-wide exclusive scan of the per-thread sums: shuffles within
+        // each warp, the eight warp totals through shared memory (2 barriers)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        unsigned int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += x;
         }
-        unsigned int run = threadIdx.x ? s_part[threadIdx.x - 1] : 0u;
+        if (lane == 31) s_part[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+          const unsigned int w = lane < kScatterThreads / 32 ? s_part[lane] : 0u;
+          unsigned int wi = w;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= o) wi += x;
+          }
+          if (lane < kScatterThreads / 32) s_part[32 + lane] = wi - w;  // exclusive warp offsets
+        }
+        __syncthreads();
+        unsigned int run = s_part[32 + warp] + incl - sum;
 #pragma unroll
         for (int q = 0; q < kScanPer; ++q) {
           if (k0 + q < nk) s_off[k0 + q] = run;
@@ -203,19 +217,16 @@ __global__ void __launch_bounds__(kScatterThreads)
         const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
         if (kr[j] != 0xFFFFFFFFu) {
           const unsigned int key = kr[j] >> 16, r = kr[j] & 0xFFFFu;
-          const unsigned int k = s_off[key] + r;
+          const unsigned int k = s_off[key] + r, dst = s_gst[key] + r;
           stage[k] = p[j];
-          skey[k] = static_cast<std::uint16_t>(key);
-          __stcs(pos + i, s_gst[key] + r);
+          sdst[k] = dst;
+          __stcs(pos + i, dst);
         }
       }
       __syncthreads();
       const int cnt = static_cast<int>(min(static_cast<std::uint64_t>(kScatterIter), hi - base));
 #pragma unroll 4
-      for (int k = threadIdx.x; k < cnt; k += kScatterThreads) {  // run by run, whole lines
-        const unsigned int key = skey[k];
-        pts_b[s_gst[key] + (k - s_off[key])] = stage[k];
-      }
+      for (int k = threadIdx.x; k < cnt; k += kScatterThreads) pts_b[sdst[k]] = stage[k];  // run by run
       __syncthreads();
       for (int k = threadIdx.x; k < nk; k += blockDim.x) {
         s_gst[k] += s_cnt[k];

@@ -1043,7 +1043,7 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   FM_CUDA(cub::DeviceScan::ExclusiveSum(scratch + o_tmp, cub_bytes, table, starts,
                                         static_cast<std::int64_t>(n_tab), stream));
   auto ks = bin_scatter_kernel;
-  const int sc_smem = kScatterIter * 18 + 3 * ((nk + 3) & ~3) * 4;
+  const int sc_smem = kScatterIter * 20 + 3 * ((nk + 3) & ~3) * 4;
   const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       n_chunks, resident_blocks(ix->device, (const void*)ks, kScatterThreads, sc_smem))));
   ks<<<grid_s, kScatterThreads, sc_smem, stream>>>(P, T, pts, n, ch, starts, pts_b, pos);

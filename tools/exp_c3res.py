@@ -18,7 +18,7 @@ from paper_2005_03156_b200 import fastmap, synth
 name = sys.argv[1]
 n = int(float(sys.argv[2]))
 ms_list = [float(x) for x in sys.argv[3:]] or [0.0]
-tiles = [32e6, 128e6]
+tiles = [float(x) for x in __import__("os").environ.get("EXP_TILES", "32e6 128e6").split()]
 reps = 3
 cfg = synth.config(name)
 soup = cfg.make_soup()
