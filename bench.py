@@ -456,9 +456,9 @@ def run_ours(args):
     binned = (not approx) and qplan["path"] == "binned"
     # our kernels per fm_query call (fastmap_b200.cu launch()): the stream
     # path runs stream_kernel + resolve_kernel per 2^28-point slice, the
-    # binned path count + scatter + query + unbin per 2^30-point batch (the
-    # cub scan between count and scatter is a library kernel), approx one
-    # kernel; with a histogram, one widen_hist_kernel per slice / batch
+    # binned path sample + plan + scatter + seal + query + unbin + unplaced
+    # per 2^30-point batch, approx one kernel; with a histogram, one
+    # widen_hist_kernel per slice / batch (and binned_hist_kernel per batch)
     launches_per_call = []
     for _, cnt in plan.chunks():
         if approx:
@@ -466,7 +466,8 @@ def run_ours(args):
         else:
             unit = (1 << 30) if binned else (1 << 28)
             pieces = -(-cnt // unit)
-            launches_per_call.append(pieces * ((4 if binned else 2) + (1 if plan.hist else 0)))
+            launches_per_call.append(pieces * ((7 if binned else 2)
+                                               + ((2 if binned else 1) if plan.hist else 0)))
     n_launches = args.steps * sum(launches_per_call)
 
     if rank == 0:
@@ -496,7 +497,7 @@ def run_ours(args):
                          "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel": ("fm_query_mode(approx) = approx_kernel" if approx else
-                                    "fm_query = bin_count + bin_scatter + binned_query + unbin"
+                                    "fm_query = bin_sample + bin_plan + bin_scatter + bin_seal + binned_query + unbin + unplaced"
                                     if binned else "fm_query = stream_kernel + resolve_kernel"),
                          "launch_ms": launch_ms,
                          "traffic_source": "profiles/%s (ncu, cold cache)" % prof.name},

@@ -14,17 +14,15 @@
 // (stream_kernel + resolve_kernel) stays the choice for small or mostly
 // true-hit indexes (c1, c2) -- see choose_path() in fastmap_b200.cu.
 //
-// Four launches (and a library scan) per batch of n <= 2^30 points
-// (DESIGN.md sec. 5.3); the stream is cut into chunks of >= 4096 points:
-//   bin_count_kernel    per chunk, a shared-memory histogram of tile keys:
-//                       column c of the tile-major (n_tiles + 1) x n_chunks
-//                       table
-//   (cub exclusive scan of the table: entry (t, c) becomes the first
-//    binned position of chunk c's points in tile t)
-//   bin_scatter_kernel  per chunk, 4K points at a time: a shared-memory
-//                       counting sort by tile, then the points written out
-//                       run by run at the chunk's cursors (pts_b), their
-//                       binned positions to pos[i] (coalesced)
+// Per batch of n <= 2^30 points:
+//   bin_sample_kernel   one point per 64-point stratum: sampled bin counts
+//   bin_plan_kernel     bin capacities (estimate + 3 sigma + pad), their
+//                       scan as bin starts, the overflow bin after them
+//   bin_scatter_kernel 4K points at a time: a shared-memory counting sort
+//                       by tile, one global atomic per non-empty bin claims
+//                       the run's space, runs written whole (pts_b), each
+//                       point's binned position to pos[i] (coalesced)
+//   bin_seal_kernel     unused bin tails become NaN points; the binned length
 //   binned_query_kernel the query over pts_b in order: locate, true hits
 //                       answered at once, boundary points through a
 //                       warp-private shared-memory ring whose batches of 32
@@ -32,10 +30,11 @@
 //                       their evaluation (exactly resolve_kernel's code);
 //                       answers to res[k]
 //   unbin_kernel        out[i] = res[pos[i]]
-// Chunks are walked with a grid stride, so within a tile the points stay
-// in about input order and any window of consecutive input points maps to
-// about one contiguous range per tile: the gather in unbin_kernel and the
-// scattered writes of the scatter stay coherent in L2 and the TLB.
+//   unplaced_kernel     points no bin could take (returns at once normally)
+// Iterations are walked with a grid stride, so at any moment the grid reads
+// one window of the stream and every tile's points stay in about input
+// order: the scattered writes and the gather in unbin_kernel stay coherent
+// in L2 and the TLB.
 // Points outside the acceptance box (and NaN) go to one extra bin; the
 // query pass answers them -1 like every other path.
 //
@@ -95,51 +94,138 @@ __device__ __forceinline__ int tile_key(const fm::KParams& P, const TileGeom& T,
 constexpr int kScatterThreads = 256;
 constexpr int kScPer = FM_SC_PER;
 constexpr int kScatterIter = kScatterThreads * kScPer;  // 4096 points
-constexpr std::uint64_t kMaxTableEntries = std::uint64_t{64} << 20;
 
-// table[t * n_chunks + c] = points of chunk c in tile t (a shared-memory
-// histogram per chunk)
+// ---- single-pass binning with sampled bin capacities ----------------------
+// Sizing the bins exactly takes a counting pass over the whole stream (16
+// B/point: 2.8 ms per 1B c3 points, round 2's first cut).  Instead, one point per stratum of
+// kSampleStride points (at a hashed offset inside the stratum) is counted,
+// every bin gets the sampled estimate plus a kSigmas margin plus kBinPad,
+// and the scatter claims bin space with one global atomic per (iteration,
+// bin).  Points past their bin's capacity go to an overflow bin at the end
+// of the binned array; points past *that* (an adversarial stream whose
+// sample missed them) get pos = kUnplaced and unplaced_kernel answers them
+// straight from the index.  Only performance depends on the estimate: every
+// point is answered by the same code wherever it lands.
+constexpr int kSampleStride = 64;
+constexpr unsigned int kBinPad = 256;
+// bin margin in standard deviations of the sampled estimate: every unused
+// slot is a NaN point the query still reads, every overflowing point loses
+// its tile's locality
+constexpr double kSigmas = 3.0;
+constexpr unsigned int kUnplaced = 0xFFFFFFFFu;
+
+// The bin table in the batch's scratch: per bin start, capacity, fill
+// cursor; then the overflow bin and the binned length the query walks.
+struct BinTable {
+  unsigned int* start;
+  unsigned int* cap;
+  unsigned int* cur;
+  unsigned int* hdr;  // [0] overflow start, [1] overflow capacity, [2] overflow fill
+  unsigned long long* n_eff;  // points the query walks: overflow start + fill
+};
+
+__device__ __forceinline__ std::uint32_t stratum_hash(std::uint64_t j) {
+  std::uint64_t z = j * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
+  return static_cast<std::uint32_t>(z >> 40);
+}
+
 __global__ void __launch_bounds__(kScatterThreads)
-    bin_count_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                     std::uint64_t ch, unsigned int* __restrict__ table) {
+    bin_sample_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
+                      unsigned int* __restrict__ counts) {
   extern __shared__ unsigned int s_hist[];
-  const std::uint64_t n_chunks = (n + ch - 1) / ch;
-  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) s_hist[k] = 0u;
-    __syncthreads();
-    const std::uint64_t hi = min(n, (c + 1) * ch);
-    for (std::uint64_t i0 = c * ch + threadIdx.x; i0 < hi; i0 += kScatterIter) {
-      double2 p[kScPer];
-#pragma unroll
-      for (int j = 0; j < kScPer; ++j) {
-        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
-        p[j] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int j = 0; j < kScPer; ++j) {
-        const std::uint64_t i = i0 + static_cast<std::uint64_t>(j) * kScatterThreads;
-        if (i < hi) atomicAdd(s_hist + tile_key(P, T, p[j].x, p[j].y), 1u);
-      }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k <= T.n_tiles; k += blockDim.x) table[static_cast<std::uint64_t>(k) * n_chunks + c] = s_hist[k];
-    __syncthreads();
+  const int nk = T.n_tiles + 1;
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_hist[k] = 0u;
+  __syncthreads();
+  const std::uint64_t strata = (n + kSampleStride - 1) / kSampleStride;
+  for (std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < strata;
+       j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    const std::uint64_t lo = j * kSampleStride;
+    const std::uint64_t w = min(static_cast<std::uint64_t>(kSampleStride), n - lo);
+    const double2 p = __ldg(pts + lo + stratum_hash(j) % w);
+    atomicAdd(s_hist + tile_key(P, T, p.x, p.y), 1u);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+    if (s_hist[k]) atomicAdd(counts + k, s_hist[k]);
   }
 }
 
-// The scatter.  Per chunk, the global cursors start at the scanned table
-// entries of the chunk; each kScatterIter-point iteration is counting-sorted
-// by tile in shared memory and then written out run by run, so consecutive
-// lanes store consecutive points of one run (whole lines) instead of each
-// lane storing 16 bytes into a different tile's run: scattering 16-byte
-// points into >= 16 interleaved fronts runs at 0.8-2.6 TB/s against 5.6 for
-// a copy (tools/exp_copy.cu, profiles/r2s).  Each point's binned position
-// goes to pos[i] (coalesced).  Within a tile the points stay in chunk order,
-// i.e. in about input order, so the gather in unbin_kernel is coherent.
+// Upper bound of the planned bins' total capacity (host side, sizes the
+// scratch): sum est <= n + S, and by Cauchy-Schwarz the margins sum to at
+// most kSigmas sqrt(nk * sum(S est + S^2)).
+std::uint64_t bin_capacity_bound(std::uint64_t n, int nk) {
+  const double S = kSampleStride, K = nk, N = static_cast<double>(n) + S;
+  const double margin = kSigmas * std::sqrt(K * (S * N + K * S * S));
+  return static_cast<std::uint64_t>(N + margin) + static_cast<std::uint64_t>(nk) * (kBinPad + 8);  // + fp32 rounding of the margins
+}
+std::uint64_t bin_overflow_cap(std::uint64_t n) { return std::min<std::uint64_t>(n, n / 32 + 65536); }
+
+// One CTA: capacities from the sampled counts, their exclusive scan as bin
+// starts, cursors zeroed, the overflow bin after the last bin.
+constexpr int kPlanThreads = 1024;
+__global__ void __launch_bounds__(kPlanThreads)
+    bin_plan_kernel(int nk, std::uint64_t ovf_cap, const unsigned int* __restrict__ counts, BinTable B) {
+  constexpr int kPer = (kMaxTiles + 1 + kPlanThreads - 1) / kPlanThreads;
+  __shared__ unsigned long long s_warp[kPlanThreads / 32];
+  const int k0 = threadIdx.x * kPer;
+  unsigned long long c[kPer], sum = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    c[q] = 0;
+    if (k0 + q < nk) {
+      // the margin in fp32 (a size, not a predicate: no fp64 FMA in the library
+      // outside the builder's division, tests/test_sass.py)
+      const unsigned long long est = static_cast<unsigned long long>(counts[k0 + q]) * kSampleStride;
+      const float var = static_cast<float>(kSampleStride) * static_cast<float>(est + kSampleStride);
+      c[q] = est + static_cast<unsigned long long>(static_cast<float>(kSigmas) * sqrtf(var)) + 1 + kBinPad;
+    }
+    sum += c[q];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long w = s_warp[lane];
+    unsigned long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long x = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi += x;
+    }
+    s_warp[lane] = wi - w;
+  }
+  __syncthreads();
+  unsigned long long run = s_warp[warp] + incl - sum;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    if (k0 + q < nk) {
+      B.start[k0 + q] = static_cast<unsigned int>(run);
+      B.cap[k0 + q] = static_cast<unsigned int>(c[q]);
+      B.cur[k0 + q] = 0u;
+    }
+    run += c[q];
+  }
+  if (k0 < nk && nk <= k0 + kPer) {  // the thread holding the last bin
+    B.hdr[0] = static_cast<unsigned int>(run);
+    B.hdr[1] = static_cast<unsigned int>(ovf_cap);
+    B.hdr[2] = 0u;
+  }
+}
+
+// The scatter, one pass: each kScatterIter-point iteration is counting-sorted
+// by bin in shared memory (as in bin_scatter_kernel), then one thread per
+// non-empty bin claims the run's space with a global atomic; runs are
+// written whole, consecutive lanes storing consecutive points.
 __global__ void __launch_bounds__(kScatterThreads)
     bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                       std::uint64_t ch, const unsigned int* __restrict__ starts,
-                       double2* __restrict__ pts_b, unsigned int* __restrict__ pos) {
+                        BinTable B, double2* __restrict__ pts_b, unsigned int* __restrict__ pos) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nk = T.n_tiles + 1;
   const int nk4 = (nk + 3) & ~3;
@@ -147,92 +233,124 @@ __global__ void __launch_bounds__(kScatterThreads)
   unsigned int* sdst = reinterpret_cast<unsigned int*>(smem_raw + kScatterIter * 16);
   unsigned int* s_cnt = reinterpret_cast<unsigned int*>(smem_raw + kScatterIter * 20);
   unsigned int* s_off = s_cnt + nk4;
-  unsigned int* s_gst = s_off + nk4;
+  unsigned int* s_dst = s_off + nk4;  // destination of the run's first point
+  unsigned int* s_av = s_dst + nk4;   // points of the run that fit the bin
+  unsigned int* s_ob = s_av + nk4;    // overflow destination of the rest
   __shared__ unsigned int s_part[64];
   constexpr int kScanPer = (kMaxTiles + 1 + kScatterThreads - 1) / kScatterThreads;
-  const std::uint64_t n_chunks = (n + ch - 1) / ch;
+  const unsigned int ovf_base = B.hdr[0], ovf_cap = B.hdr[1];
+  const std::uint64_t n_it = (n + kScatterIter - 1) / kScatterIter;
   for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
-  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_gst[k] = starts[static_cast<std::uint64_t>(k) * n_chunks + c];
-    const std::uint64_t hi = min(n, (c + 1) * ch);
-    for (std::uint64_t base = c * ch; base < hi; base += kScatterIter) {
-      double2 p[kScPer];
-      unsigned int kr[kScPer];
+  for (std::uint64_t it = blockIdx.x; it < n_it; it += gridDim.x) {
+    const std::uint64_t base = it * kScatterIter;
+    const std::uint64_t hi = min(n, base + kScatterIter);
+    double2 p[kScPer];
+    unsigned int kr[kScPer];
 #pragma unroll
-      for (int j = 0; j < kScPer; ++j) {
-        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-        p[j] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
-      }
-      __syncthreads();  // s_cnt zeroed, s_gst loaded / advanced
+    for (int j = 0; j < kScPer; ++j) {
+      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+      p[j] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
+    }
+    __syncthreads();  // s_cnt zeroed
 #pragma unroll
-      for (int j = 0; j < kScPer; ++j) {
-        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-        kr[j] = 0xFFFFFFFFu;
-        if (i < hi) {
-          const unsigned int key = static_cast<unsigned int>(tile_key(P, T, p[j].x, p[j].y));
-          kr[j] = (key << 16) | atomicAdd(s_cnt + key, 1u);
-        }
-      }
-      __syncthreads();
-      {  // exclusive scan of s_cnt over the tiles -> s_off
-        const int k0 = threadIdx.x * kScanPer;
-        unsigned int v[kScanPer], sum = 0;
-#pragma unroll
-        for (int q = 0; q < kScanPer; ++q) {
-          v[q] = k0 + q < nk ? s_cnt[k0 + q] : 0u;
-          sum += v[q];
-        }
-        // block-wide exclusive scan of the per-thread sums: shuffles within
-        // each warp, the eight warp totals through shared memory (2 barriers)
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        unsigned int incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= o) incl += x;
-        }
-        if (lane == 31) s_part[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-          const unsigned int w = lane < kScatterThreads / 32 ? s_part[lane] : 0u;
-          unsigned int wi = w;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-            if (lane >= o) wi += x;
-          }
-          if (lane < kScatterThreads / 32) s_part[32 + lane] = wi - w;  // exclusive warp offsets
-        }
-        __syncthreads();
-        unsigned int run = s_part[32 + warp] + incl - sum;
-#pragma unroll
-        for (int q = 0; q < kScanPer; ++q) {
-          if (k0 + q < nk) s_off[k0 + q] = run;
-          run += v[q];
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < kScPer; ++j) {
-        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-        if (kr[j] != 0xFFFFFFFFu) {
-          const unsigned int key = kr[j] >> 16, r = kr[j] & 0xFFFFu;
-          const unsigned int k = s_off[key] + r, dst = s_gst[key] + r;
-          stage[k] = p[j];
-          sdst[k] = dst;
-          __stcs(pos + i, dst);
-        }
-      }
-      __syncthreads();
-      const int cnt = static_cast<int>(min(static_cast<std::uint64_t>(kScatterIter), hi - base));
-#pragma unroll 4
-      for (int k = threadIdx.x; k < cnt; k += kScatterThreads) pts_b[sdst[k]] = stage[k];  // run by run
-      __syncthreads();
-      for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-        s_gst[k] += s_cnt[k];
-        s_cnt[k] = 0u;
+    for (int j = 0; j < kScPer; ++j) {
+      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+      kr[j] = 0xFFFFFFFFu;
+      if (i < hi) {
+        const unsigned int key = static_cast<unsigned int>(tile_key(P, T, p[j].x, p[j].y));
+        kr[j] = (key << 16) | atomicAdd(s_cnt + key, 1u);
       }
     }
+    __syncthreads();
+    {  // exclusive scan of s_cnt -> s_off; claims of the non-empty bins
+      const int k0 = threadIdx.x * kScanPer;
+      unsigned int v[kScanPer], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kScanPer; ++q) {
+        v[q] = k0 + q < nk ? s_cnt[k0 + q] : 0u;
+        sum += v[q];
+      }
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      unsigned int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      if (lane == 31) s_part[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        const unsigned int w = lane < kScatterThreads / 32 ? s_part[lane] : 0u;
+        unsigned int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+          if (lane >= o) wi += x;
+        }
+        if (lane < kScatterThreads / 32) s_part[32 + lane] = wi - w;
+      }
+      __syncthreads();
+      unsigned int run = s_part[32 + warp] + incl - sum;
+#pragma unroll
+      for (int q = 0; q < kScanPer; ++q) {
+        if (k0 + q < nk) s_off[k0 + q] = run;
+        run += v[q];
+      }
+    }
+    // the claims: one bin per thread, so the atomics' round trips overlap
+    for (int k = threadIdx.x; k < nk; k += kScatterThreads) {
+      const unsigned int v = s_cnt[k];
+      if (v) {
+        const unsigned int got = atomicAdd(B.cur + k, v);
+        const unsigned int cap = __ldg(B.cap + k);
+        const unsigned int av = got < cap ? min(cap - got, v) : 0u;
+        s_dst[k] = __ldg(B.start + k) + got;
+        s_av[k] = av;
+        if (av < v) s_ob[k] = atomicAdd(B.hdr + 2, v - av);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kScPer; ++j) {
+      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
+      if (kr[j] != 0xFFFFFFFFu) {
+        const unsigned int key = kr[j] >> 16, r = kr[j] & 0xFFFFu;
+        const unsigned int k = s_off[key] + r, av = s_av[key];
+        unsigned int dst;
+        if (r < av) {
+          dst = s_dst[key] + r;
+        } else {
+          const unsigned int o = s_ob[key] + (r - av);
+          dst = o < ovf_cap ? ovf_base + o : kUnplaced;
+        }
+        stage[k] = p[j];
+        sdst[k] = dst;
+        __stcs(pos + i, dst);
+      }
+    }
+    __syncthreads();
+    const int cnt = static_cast<int>(hi - base);
+#pragma unroll 4
+    for (int k = threadIdx.x; k < cnt; k += kScatterThreads) {
+      const unsigned int d = sdst[k];
+      if (d != kUnplaced) pts_b[d] = stage[k];  // run by run
+    }
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
+  }
+}
+
+// After the scatter: every bin's unfilled tail becomes NaN points (answered
+// -1 and never read back), the query's length is the overflow bin's end,
+// and the point counter forgets the padding.
+__global__ void __launch_bounds__(256)
+    bin_seal_kernel(int nk, BinTable B, double2* __restrict__ pts_b, unsigned long long* __restrict__ counters) {
+  for (int k = blockIdx.x; k < nk; k += gridDim.x) {
+    const unsigned int cap = B.cap[k], fill = min(B.cur[k], cap), s = B.start[k];
+    for (unsigned int i = fill + threadIdx.x; i < cap; i += blockDim.x) pts_b[s + i] = make_double2(NAN, NAN);
+    if (counters && threadIdx.x == 0 && cap > fill) atomicAdd(counters, 0ull - static_cast<unsigned long long>(cap - fill));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *B.n_eff = static_cast<unsigned long long>(B.hdr[0]) + min(B.hdr[2], B.hdr[1]);
   }
 }
 
@@ -358,10 +476,11 @@ constexpr int kQGroup = 8;
 template <bool kHist, bool kCount, int kLs>
 __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
     binned_query_kernel(fm::KParams P, const double2* __restrict__ pts, std::uint64_t n,
-                        int* __restrict__ res, HistT* __restrict__ hist,
-                        unsigned long long* __restrict__ counters,
+                        const unsigned long long* __restrict__ n_dev, int* __restrict__ res,
+                        HistT* __restrict__ hist, unsigned long long* __restrict__ counters,
                         unsigned long long* __restrict__ work) {
   extern __shared__ __align__(16) unsigned char dsmem[];
+  if (n_dev) n = min(n, static_cast<std::uint64_t>(*n_dev));  // the sealed binned length
   __shared__ HotSmem<kHist> hot;
   const HistSink hs = hist_open<kHist>(hist, hot);
   WarpSmemQ& S = reinterpret_cast<WarpSmemQ*>(dsmem)[threadIdx.x >> 5];
@@ -486,8 +605,10 @@ constexpr int kHistSlots = 4096;
 constexpr int kHistProbes = 8;
 
 __global__ void __launch_bounds__(kHistThreads)
-    binned_hist_kernel(const int* __restrict__ res, std::uint64_t n, HistT* __restrict__ hist) {
+    binned_hist_kernel(const int* __restrict__ res, std::uint64_t n, const unsigned long long* __restrict__ n_dev,
+                       HistT* __restrict__ hist) {
   __shared__ unsigned int s_key[kHistSlots];
+  if (n_dev) n = min(n, static_cast<std::uint64_t>(*n_dev));
   __shared__ unsigned int s_cnt[kHistSlots];
   for (int k = threadIdx.x; k < kHistSlots; k += blockDim.x) {
     s_key[k] = fm::kEmpty;
@@ -548,6 +669,33 @@ constexpr int kUnbinRounds = FM_UNBIN_ROUNDS;
 #endif
 constexpr std::uint64_t kUnbinBlock = 4ull * kUnbinThreads * kUnbinRounds;  // 8192 points
 
+// A point the binning could not place (pos == kUnplaced; see the sampled
+// capacities above): answered straight from the index, histogram and
+// counters included.  Never taken when the sample represents the stream.
+__device__ __noinline__ int answer_unplaced(const fm::KParams& P, double2 p, HistT* __restrict__ hist,
+                                            unsigned long long* __restrict__ counters) {
+  double2 q[1] = {p};
+  std::uint32_t e[1];
+  fm::locate_n<1, true, -1>(P, q, e);
+  fm::WorkCount wc;
+  int id;
+  if (e[0] == fm::kEmpty) {
+    id = -1;
+  } else if (e[0] < fm::kRecordBit) {
+    id = static_cast<int>(e[0]);
+  } else {
+    id = fm::resolve_slot_global<true>(P, e[0], p.x, p.y, wc);
+  }
+  if (hist && id >= 0) atomicAdd(hist + id, 1u);
+  if (counters) {
+    atomicAdd(counters, 1ull);
+    atomicAdd(counters + 1, wc.boundary);
+    atomicAdd(counters + 2, wc.cands);
+    atomicAdd(counters + 3, wc.edges);
+  }
+  return id;
+}
+
 __global__ void __launch_bounds__(kUnbinThreads)
     unbin_kernel(const unsigned int* __restrict__ pos, const int* __restrict__ res, std::uint64_t n,
                  int* __restrict__ out, unsigned long long* __restrict__ work) {
@@ -563,9 +711,20 @@ __global__ void __launch_bounds__(kUnbinThreads)
       // every pos load of the block, then every gather: 4 * kUnbinRounds
       // independent loads in flight per thread
       uint4 k[kUnbinRounds];
+      bool bad = false;
 #pragma unroll
       for (int r = 0; r < kUnbinRounds; ++r) {
         k[r] = __ldcs(p4 + base / 4 + static_cast<std::uint64_t>(r) * kUnbinThreads + threadIdx.x);
+        bad |= (k[r].x == kUnplaced) | (k[r].y == kUnplaced) | (k[r].z == kUnplaced) | (k[r].w == kUnplaced);
+      }
+      if (bad) {  // kUnplaced entries are left to unplaced_kernel
+#pragma unroll 1
+        for (int r = 0; r < 4 * kUnbinRounds; ++r) {
+          const std::uint64_t i = base + 4 * (static_cast<std::uint64_t>(r >> 2) * kUnbinThreads + threadIdx.x) + (r & 3);
+          const unsigned int kk = pos[i];
+          if (kk != kUnplaced) out[i] = __ldg(res + kk);
+        }
+        continue;
       }
       int4 v[kUnbinRounds];
 #pragma unroll
@@ -582,8 +741,23 @@ __global__ void __launch_bounds__(kUnbinThreads)
     } else {
       const std::uint64_t end = min(n, base + kUnbinBlock);
       for (std::uint64_t i = base + threadIdx.x; i < end; i += kUnbinThreads) {
-        __stcs(out + i, __ldg(res + __ldcs(pos + i)));
+        const unsigned int k = __ldcs(pos + i);
+        if (k != kUnplaced) __stcs(out + i, __ldg(res + k));
       }
     }
+  }
+}
+
+// Points the binning could not place (the overflow bin filled up: a stream
+// whose sample missed where its points are): answered straight from the
+// index.  Returns at once in the normal case.
+__global__ void __launch_bounds__(256)
+    unplaced_kernel(BinTable B, const unsigned int* __restrict__ pos, std::uint64_t n, fm::KParams P,
+                    const double2* __restrict__ pts, int* __restrict__ out, HistT* __restrict__ hist,
+                    unsigned long long* __restrict__ counters) {
+  if (B.hdr[2] <= B.hdr[1]) return;
+  for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    if (__ldg(pos + i) == kUnplaced) out[i] = answer_unplaced(P, __ldg(pts + i), hist, counters);
   }
 }

@@ -327,20 +327,41 @@ __device__ __forceinline__ QItem load_item(const QItem* __restrict__ items, std:
 // the owner lane's reads in eval_staged are bank-conflict free.  The second
 // half of a double slot (kDoubleBit) is prefetched into L2, where its
 // evaluation one batch later finds it.
+template <int kOff>
+__device__ __forceinline__ void cp_async16_at(unsigned smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0+%2], [%1], 16;\n" ::"r"(smem), "l"(gmem), "n"(kOff) : "memory");
+}
+
 __device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* buf,
                                             std::uint32_t e, int n, int lane) {
   if (lane < n && (e & fm::kDoubleBit) && !(e & fm::kHalfBit)) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(fm::slot_ptr(P, e) + fm::kSlotBytes));
   }
-  const int c = lane & 7;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int r = 4 * q + (lane >> 3);
-    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
-    if (r < n && (c < 4 || !(er & fm::kHalfBit))) {  // half slots: first 64 bytes only
-      cp_async16(buf + r * fm::kSlotBytes + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
-    }
+  // Lane L copies chunk c = L & 7 of slots r = 4q + (L >> 3), q = 0..7, so
+  // r & 7 = 4 (q & 1) + (L >> 3): the swizzled shared address is one of two
+  // per-lane bases plus the constant 512 q.  The shuffled word carries the
+  // slot index, the half flag (bit 30) and validity (0xFFFFFFFF past n), so
+  // one unsigned compare against a per-lane threshold is the copy predicate
+  // (chunks 4..7 of half slots are not copied).
+  const int c = lane & 7, rl = lane >> 3;
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(buf)) + 128u * rl;
+  const unsigned sa0 = sbase + 16u * static_cast<unsigned>(c ^ rl);
+  const unsigned sa1 = sbase + 16u * static_cast<unsigned>(c ^ (4 + rl));
+  const std::uint64_t gbase = reinterpret_cast<std::uint64_t>(P.slots + 16 * c);
+  const std::uint32_t thr = c < 4 ? 0x80000000u : 0x40000000u;
+  const std::uint32_t v = lane < n ? (e & 0x7FFFFFFFu) : 0xFFFFFFFFu;
+#define FM_STAGE_Q(q)                                                                          \
+  {                                                                                            \
+    const std::uint32_t w = __shfl_sync(0xFFFFFFFFu, v, 4 * (q) + rl);                         \
+    if (w < thr) {                                                                             \
+      std::uint64_t ga;                                                                        \
+      asm("mad.wide.u32 %0, %1, 128, %2;" : "=l"(ga) : "r"(w & fm::kSlotIndexMask), "l"(gbase));  \
+      cp_async16_at<512 * (q)>((q) & 1 ? sa1 : sa0, reinterpret_cast<const void*>(ga));         \
+    }                                                                                          \
   }
+  FM_STAGE_Q(0) FM_STAGE_Q(1) FM_STAGE_Q(2) FM_STAGE_Q(3)
+  FM_STAGE_Q(4) FM_STAGE_Q(5) FM_STAGE_Q(6) FM_STAGE_Q(7)
+#undef FM_STAGE_Q
   cp_async_commit();
 }
 
@@ -1006,68 +1027,74 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   const fm::KParams P = kparams(ix);
   const TileGeom& T = ix->tiles;
   const int nk = T.n_tiles + 1;
+  const int nk4 = (nk + 3) & ~3;
   const int tile_smem = nk * 4;
-  // chunks of kScatterIter * m points, m keeping the table under kMaxTableEntries
-  const std::uint64_t n_it = (n + kScatterIter - 1) / kScatterIter;
-  const std::uint64_t m = std::max<std::uint64_t>(1, (n_it * nk + kMaxTableEntries - 1) / kMaxTableEntries);
-  const std::uint64_t ch = static_cast<std::uint64_t>(kScatterIter) * m;
-  const std::uint64_t n_chunks = (n + ch - 1) / ch;
-  const std::uint64_t n_tab = static_cast<std::uint64_t>(nk) * n_chunks;
-  std::size_t cub_bytes = 0;
-  FM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, static_cast<unsigned int*>(nullptr),
-                                        static_cast<unsigned int*>(nullptr),
-                                        static_cast<std::int64_t>(n_tab), stream));
-  // scratch: work counters, the (tile x chunk) table and its scan, scan
-  // temp, binned points, binned positions, binned answers (24 B per point)
+  // sampled bin capacities, one scatter pass (binned.cuh)
+  const std::uint64_t ovf_cap = bin_overflow_cap(n);
+  const std::uint64_t nb = bin_capacity_bound(n, nk) + ovf_cap;  // binned length bound
+  // scratch: work counters + binned length, sample counts, the bin table,
+  // binned points, binned positions, binned answers
   const std::uint64_t o_work = 0;
-  const std::uint64_t o_tab = 256;
-  const std::uint64_t o_scan = o_tab + align256(4 * n_tab);
-  const std::uint64_t o_tmp = o_scan + align256(4 * n_tab);
-  const std::uint64_t o_pts = o_tmp + align256(cub_bytes + 16);
-  const std::uint64_t o_pos = o_pts + align256(16 * n);
+  const std::uint64_t o_cnt = 256;
+  const std::uint64_t o_bin = o_cnt + align256(4 * static_cast<std::uint64_t>(nk));
+  const std::uint64_t o_pts = o_bin + align256(4 * (3 * static_cast<std::uint64_t>(nk4) + 4));
+  const std::uint64_t o_pos = o_pts + align256(16 * nb);
   const std::uint64_t o_res = o_pos + align256(4 * n);
-  const std::uint64_t total = o_res + align256(4 * n);
+  const std::uint64_t total = o_res + align256(4 * nb);
   char* scratch = nullptr;
   FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), total, stream));
   unsigned long long* work = reinterpret_cast<unsigned long long*>(scratch + o_work);
-  unsigned int* table = reinterpret_cast<unsigned int*>(scratch + o_tab);
-  unsigned int* starts = reinterpret_cast<unsigned int*>(scratch + o_scan);
-  FM_CUDA(cudaMemsetAsync(work, 0, 8 * kCtrCount, stream));
+  unsigned int* counts = reinterpret_cast<unsigned int*>(scratch + o_cnt);
+  BinTable B;
+  B.start = reinterpret_cast<unsigned int*>(scratch + o_bin);
+  B.cap = B.start + nk4;
+  B.cur = B.cap + nk4;
+  B.hdr = B.cur + nk4;
+  B.n_eff = work + kCtrCount;
+  FM_CUDA(cudaMemsetAsync(scratch, 0, o_bin, stream));  // work counters, n_eff, sample counts
   double2* pts_b = reinterpret_cast<double2*>(scratch + o_pts);
   unsigned int* pos = reinterpret_cast<unsigned int*>(scratch + o_pos);
   int* res = reinterpret_cast<int*>(scratch + o_res);
-  auto kc = bin_count_kernel;
-  const int grid_c = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      n_chunks, resident_blocks(ix->device, (const void*)kc, kScatterThreads, tile_smem))));
-  kc<<<grid_c, kScatterThreads, tile_smem, stream>>>(P, T, pts, n, ch, table);
-  FM_CUDA(cub::DeviceScan::ExclusiveSum(scratch + o_tmp, cub_bytes, table, starts,
-                                        static_cast<std::int64_t>(n_tab), stream));
+  {
+    auto k0 = bin_sample_kernel;
+    const std::uint64_t strata = (n + kSampleStride - 1) / kSampleStride;
+    const int grid0 = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
+        (strata + kScatterThreads - 1) / kScatterThreads,
+        resident_blocks(ix->device, (const void*)k0, kScatterThreads, tile_smem))));
+    k0<<<grid0, kScatterThreads, tile_smem, stream>>>(P, T, pts, n, counts);
+  }
+  bin_plan_kernel<<<1, kPlanThreads, 0, stream>>>(nk, ovf_cap, counts, B);
   auto ks = bin_scatter_kernel;
-  const int sc_smem = kScatterIter * 20 + 3 * ((nk + 3) & ~3) * 4;
+  const int sc_smem = kScatterIter * 20 + 5 * nk4 * 4;
+  const std::uint64_t n_it = (n + kScatterIter - 1) / kScatterIter;
   const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      n_chunks, resident_blocks(ix->device, (const void*)ks, kScatterThreads, sc_smem))));
-  ks<<<grid_s, kScatterThreads, sc_smem, stream>>>(P, T, pts, n, ch, starts, pts_b, pos);
+      n_it, resident_blocks(ix->device, (const void*)ks, kScatterThreads, sc_smem))));
+  ks<<<grid_s, kScatterThreads, sc_smem, stream>>>(P, T, pts, n, B, pts_b, pos);
+  bin_seal_kernel<<<std::min(nk, 1184), 256, 0, stream>>>(nk, B, pts_b, kCount ? d_counters : nullptr);
+  const unsigned long long* n_dev = B.n_eff;
   // the histogram is counted from res afterwards (binned_hist_kernel): in
   // binned order its leaves repeat within a chunk, and the query kernel
   // stays free of per-point counter atomics
   auto kq = ix->qgrid.ls == 0 ? binned_query_kernel<false, kCount, 0>
                               : binned_query_kernel<false, kCount, -1>;
-  const std::uint64_t n_tiles = (n + 32ull * kU - 1) / (32ull * kU);
+  const std::uint64_t n_qt = (nb + 32ull * kU - 1) / (32ull * kU);
   const int grid_q = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      (n_tiles + kQWarps * kQGroup - 1) / (kQWarps * kQGroup),
+      (n_qt + kQWarps * kQGroup - 1) / (kQWarps * kQGroup),
       resident_blocks(ix->device, (const void*)kq, kQWarps * 32, kSmemQ))));
-  kq<<<grid_q, kQWarps * 32, kSmemQ, stream>>>(P, pts_b, n, res, nullptr, d_counters, work);
+  kq<<<grid_q, kQWarps * 32, kSmemQ, stream>>>(P, pts_b, nb, n_dev, res, nullptr, d_counters, work);
   if (kHist) {
     auto kh = binned_hist_kernel;
     const int grid_h = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-        (n + kHistChunk - 1) / kHistChunk, resident_blocks(ix->device, (const void*)kh, kHistThreads, 0))));
-    kh<<<grid_h, kHistThreads, 0, stream>>>(res, n, d_hist);
+        (nb + kHistChunk - 1) / kHistChunk, resident_blocks(ix->device, (const void*)kh, kHistThreads, 0))));
+    kh<<<grid_h, kHistThreads, 0, stream>>>(res, nb, n_dev, d_hist);
   }
   auto ku = unbin_kernel;
   const int grid_u = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       (n + kUnbinBlock - 1) / kUnbinBlock,
       resident_blocks(ix->device, (const void*)ku, kUnbinThreads, 0))));
   ku<<<grid_u, kUnbinThreads, 0, stream>>>(pos, res, n, d_out, work);
+  unplaced_kernel<<<grid_u, 256, 0, stream>>>(B, pos, n, P, pts, d_out, kHist ? d_hist : nullptr,
+                                              kCount ? d_counters : nullptr);
   const cudaError_t err = cudaGetLastError();
   FM_CUDA(cudaFreeAsync(scratch, stream));
   if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));

@@ -544,10 +544,12 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
     if (!(m > 0.0)) {
       // ~450M cells (c2: 42 cells per polygon side, 9% boundary points;
       // measured optimum 40-48 with 16-byte small sub-blocks), 4..48 per
-      // side; tilings of more than 4M leaves take ~270M cells, which bounds
-      // their slot arena (c3: 50 GB; 8.83 -> 8.33 ms per 200M points against
-      // 160M cells)
-      const double budget = active > 4000000 ? 270.0e6 : 450.0e6;
+      // side.  With double slots and the binned path this also holds for
+      // the 12.5M-leaf c3: 6 per side (266M cells, 19 GB arena) queries 1B
+      // points in 32.5 ms against 36.7 at 3.6 per side (the round-1 270M
+      // budget's 160M cells) and 38-39 ms at 7-8 per side (profiles/r2af)
+      //
+      const double budget = 450.0e6;
       m = std::sqrt(budget / static_cast<double>(active));
       m = std::min(48.0, std::max(4.0, m));
       // few polygons (>= 64): still at least ~10M cells (a ~40 MB grid, L2-sized),

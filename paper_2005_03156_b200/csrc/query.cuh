@@ -346,7 +346,8 @@ __device__ __noinline__ int resolve_overflow(const KParams& P, std::uint64_t off
 }
 
 // A boundary slot fetched straight from global memory (split descents and
-// overflow records; rare).
+// overflow records; rare).  Counts like the staged evaluation: a point is a
+// boundary point once it reaches a leaf, double or overflow record.
 template <bool kCount>
 __device__ __noinline__ int resolve_slot_global(const KParams& P, std::uint32_t e, double px,
                                                 double py, WorkCount& wc) {
@@ -356,6 +357,7 @@ __device__ __noinline__ int resolve_slot_global(const KParams& P, std::uint32_t 
 #pragma unroll
     for (int k = 0; k < 8; ++k) c[k] = __ldg(g + k);
     const std::uint32_t kind = c[0].x & 0xFFu;
+    if (kCount && kind != kSlotSplit) wc.boundary++;
     if (kind == kSlotLeaf) return eval_leaf_slot<kCount>(c, px, py, wc);
     if (kind == kSlotDouble) {
       uint4 b[8];

@@ -122,3 +122,46 @@ def test_device_point_streams_equal_host_streams(dev, name):
         cfg.make_points_device(got, offset=off, soup=soup)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), want)
+
+
+def _stratum_offsets(n, stride=64):
+    """Index of the sampled point of every stratum (binned.cuh stratum_hash)."""
+    j = np.arange((n + stride - 1) // stride, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = j * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(31))) * np.uint64(0xBF58476D1CE4E5B9)
+    h = (z >> np.uint64(40)).astype(np.int64)
+    lo = j.astype(np.int64) * stride
+    w = np.minimum(stride, n - lo)
+    return lo + h % w
+
+
+def test_binned_sample_blind_stream_overflows_and_unplaced(dev):
+    """A stream built against the capacity sample: every sampled point is
+    spread over the domain, every other point sits in one small box, so that
+    box's bin is planned nearly empty.  Its points fill the bin, then the
+    overflow bin, and the rest are answered by unplaced_kernel -- ids,
+    histogram and counters must still equal the oracle's and the stream
+    path's."""
+    cfg = synth.config("c1")
+    soup = cfg.make_soup()
+    n = 2_000_000
+    spread = cfg.make_points(n, offset=5)
+    rng = np.random.default_rng(3)
+    box = np.column_stack([rng.uniform(-96.0, -95.2, n), rng.uniform(36.0, 36.6, n)])
+    pts = box.copy()
+    s = _stratum_offsets(n)
+    pts[s] = spread[s]
+    idx = fastmap.build_index(soup, device=0)
+    idx.set_query_path("binned", 2e5)
+    assert idx.query_plan(n)["n_tiles"] > 16
+    want = oracle.assign(soup, pts)
+    hist = torch.zeros(soup.n_polys, dtype=torch.int64, device=dev)
+    cnt_b = torch.zeros(4, dtype=torch.int64, device=dev)
+    got = run(idx, pts, dev, "binned", hist=hist, counters=cnt_b)
+    assert int((got != want).sum()) == 0
+    assert np.array_equal(hist.cpu().numpy(), np.bincount(want[want >= 0], minlength=soup.n_polys))
+    cnt_s = torch.zeros(4, dtype=torch.int64, device=dev)
+    run(idx, pts, dev, "stream", counters=cnt_s)
+    assert np.array_equal(cnt_b.cpu().numpy(), cnt_s.cpu().numpy())
+    assert cnt_b[0].item() == n

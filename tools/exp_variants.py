@@ -25,7 +25,7 @@ with_hist = os.environ.get("EXPV_HIST", "0") == "1"  # also build the per-block 
 cfg = synth.config(name)
 soup = cfg.make_soup()
 t0 = time.time()
-idx = fastmap.build_index(soup, device=0)
+idx = fastmap.build_index(soup, fastmap.CoverParams(cells_per_polygon=float(os.environ.get("EXPV_M", "0"))), device=0)
 print(json.dumps({"config": name, "n": n, "build_s": time.time() - t0}), flush=True)
 pts = torch.empty((n, 2), dtype=torch.float64, device="cuda")
 cfg.make_points_device(pts, soup=soup)
