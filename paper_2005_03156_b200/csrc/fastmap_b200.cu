@@ -326,42 +326,24 @@ __device__ __forceinline__ QItem load_item(const QItem* __restrict__ items, std:
 // different times).  Chunk c of slot r is stored at chunk c ^ (r & 7) so
 // the owner lane's reads in eval_staged are bank-conflict free.  The second
 // half of a double slot (kDoubleBit) is prefetched into L2, where its
-// evaluation one batch later finds it.
-template <int kOff>
-__device__ __forceinline__ void cp_async16_at(unsigned smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0+%2], [%1], 16;\n" ::"r"(smem), "l"(gmem), "n"(kOff) : "memory");
-}
-
+// evaluation one batch later finds it.  (Precomputing the swizzled shared
+// addresses and folding validity and the half flag into one compare cut
+// the instructions per copy from ~14 to 6 but measured slower on c3, 31.94
+// vs 31.43 ms, through register pressure: profiles/r2ak.)
 __device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* buf,
                                             std::uint32_t e, int n, int lane) {
   if (lane < n && (e & fm::kDoubleBit) && !(e & fm::kHalfBit)) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(fm::slot_ptr(P, e) + fm::kSlotBytes));
   }
-  // Lane L copies chunk c = L & 7 of slots r = 4q + (L >> 3), q = 0..7, so
-  // r & 7 = 4 (q & 1) + (L >> 3): the swizzled shared address is one of two
-  // per-lane bases plus the constant 512 q.  The shuffled word carries the
-  // slot index, the half flag (bit 30) and validity (0xFFFFFFFF past n), so
-  // one unsigned compare against a per-lane threshold is the copy predicate
-  // (chunks 4..7 of half slots are not copied).
-  const int c = lane & 7, rl = lane >> 3;
-  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(buf)) + 128u * rl;
-  const unsigned sa0 = sbase + 16u * static_cast<unsigned>(c ^ rl);
-  const unsigned sa1 = sbase + 16u * static_cast<unsigned>(c ^ (4 + rl));
-  const std::uint64_t gbase = reinterpret_cast<std::uint64_t>(P.slots + 16 * c);
-  const std::uint32_t thr = c < 4 ? 0x80000000u : 0x40000000u;
-  const std::uint32_t v = lane < n ? (e & 0x7FFFFFFFu) : 0xFFFFFFFFu;
-#define FM_STAGE_Q(q)                                                                          \
-  {                                                                                            \
-    const std::uint32_t w = __shfl_sync(0xFFFFFFFFu, v, 4 * (q) + rl);                         \
-    if (w < thr) {                                                                             \
-      std::uint64_t ga;                                                                        \
-      asm("mad.wide.u32 %0, %1, 128, %2;" : "=l"(ga) : "r"(w & fm::kSlotIndexMask), "l"(gbase));  \
-      cp_async16_at<512 * (q)>((q) & 1 ? sa1 : sa0, reinterpret_cast<const void*>(ga));         \
-    }                                                                                          \
+  const int c = lane & 7;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int r = 4 * q + (lane >> 3);
+    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
+    if (r < n && (c < 4 || !(er & fm::kHalfBit))) {  // half slots: first 64 bytes only
+      cp_async16(buf + r * fm::kSlotBytes + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
+    }
   }
-  FM_STAGE_Q(0) FM_STAGE_Q(1) FM_STAGE_Q(2) FM_STAGE_Q(3)
-  FM_STAGE_Q(4) FM_STAGE_Q(5) FM_STAGE_Q(6) FM_STAGE_Q(7)
-#undef FM_STAGE_Q
   cp_async_commit();
 }
 
