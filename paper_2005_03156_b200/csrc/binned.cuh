@@ -42,11 +42,14 @@
 // same locate_n / eval_leaf_slot code as the stream path, so the answers
 // are identical whatever tile or order a point ends up in.
 
+#ifndef FM_BIN2
+#define FM_BIN2 1  // 0: the register-held scatter and the per-point gather (A/B builds)
+#endif
 #ifndef FM_QMINB
 #define FM_QMINB 2
 #endif
 
-constexpr int kMaxTiles = 4096;                         // keys < kMaxTiles + 1
+constexpr int kMaxTiles = 2048;                         // keys < kMaxTiles + 1
 
 // Work counters (zeroed per launch): the ordered passes hand out their
 // units -- scatter chunks, query tile groups, gather blocks -- in increasing
@@ -91,7 +94,10 @@ __device__ __forceinline__ int tile_key(const fm::KParams& P, const TileGeom& T,
 #ifndef FM_SC_PER
 #define FM_SC_PER 16
 #endif
-constexpr int kScatterThreads = 256;
+#ifndef FM_SC_THREADS
+#define FM_SC_THREADS 256
+#endif
+constexpr int kScatterThreads = FM_SC_THREADS;
 constexpr int kScPer = FM_SC_PER;
 constexpr int kScatterIter = kScatterThreads * kScPer;  // 4096 points
 
@@ -337,6 +343,202 @@ __global__ void __launch_bounds__(kScatterThreads)
     }
     for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
   }
+}
+
+// ---- the pipelined scatter (bin_scatter2_kernel) and its gather (unbin2) ----
+// bin_scatter_kernel above holds its iteration's points in registers and
+// runs at 16 warps per SM through five barrier-separated phases, so the
+// DRAM pipes idle while a CTA counts, scans and claims (profiles/r2v: 49%
+// DRAM throughput, 32% issue slots, 12 cycles per issued instruction).
+// Here one CTA per SM streams its chunks through a double-buffered shared-
+// memory window filled by cp.async one chunk ahead, so chunk c+1 is in
+// flight during every phase of chunk c, and no point lives in a register:
+//   raw[2][kChunk]  the chunk's points as loaded (16 B each)
+//   perm[k]         source index of the point at sorted position k
+//   sdst[k]         its binned position
+// The chunk is counting-sorted by tile key as before; the runs are then
+// written whole, pts_b[sdst[k]] = raw[perm[k]] for consecutive k.
+// Instead of a 4-byte binned position per point, the scatter leaves
+//   pos16[i]        the point's sorted index k inside its chunk (2 B), and
+//   tab[c][key]     {binned position of the run's first point,
+//                    first sorted index | points that fit the bin << 16}
+//                   (+ the run's overflow-bin offset, read only for runs
+//                   that did not fit),
+// and unbin2_kernel turns the per-point gather res[pos[i]] -- one L2
+// sector per point, the L2 gather rate (4.3 ms per 1B points) -- into
+// coalesced reads: thread k of a chunk finds its run by binary search over
+// the first sorted indices and loads res[first + (k - first index)], so
+// consecutive threads read consecutive answers; the chunk's answers then
+// go out through shared memory, out[i] = s_res[pos16[i]].
+#ifndef FM_SC2_THREADS
+#define FM_SC2_THREADS 512
+#endif
+#ifndef FM_SC2_PER
+#define FM_SC2_PER 8
+#endif
+#ifndef FM_SC2_BUFS
+#define FM_SC2_BUFS 1  // 2: a double-buffered window, one CTA per SM (r2am: 9.4 vs 8.1 ms); 1: 1: one window per CTA (two CTAs per SM overlap instead)
+#endif
+#ifndef FM_SC2_MINB
+#define FM_SC2_MINB 2
+#endif
+constexpr int kSc2Threads = FM_SC2_THREADS;
+constexpr int kSc2Per = FM_SC2_PER;
+constexpr int kSc2Bufs = FM_SC2_BUFS;
+constexpr int kChunk = kSc2Threads * kSc2Per;  // points per chunk
+static_assert(kChunk <= 32768, "sorted indices and counts are 16-bit fields");
+constexpr int kUnplacedId = INT_MIN;  // out[i] of a point no bin could take, until unplaced2_kernel
+
+// Words per chunk of the run table: nk4 x {dst, off | av << 16}, nk4 x overflow offset.
+__host__ __device__ inline std::uint64_t tab_stride(int nk4) { return 3ull * static_cast<std::uint64_t>(nk4); }
+inline int sc2_smem(int nk4) { return kChunk * (kSc2Bufs * 16 + 4 + 2) + 5 * nk4 * 4; }
+
+__global__ void __launch_bounds__(kSc2Threads, FM_SC2_MINB)
+    bin_scatter2_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
+                        BinTable B, double2* __restrict__ pts_b, std::uint16_t* __restrict__ pos16,
+                        unsigned int* __restrict__ tab) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nk = T.n_tiles + 1;
+  const int nk4 = (nk + 3) & ~3;
+  double2* raw = reinterpret_cast<double2*>(smem_raw);  // [2][kChunk]
+  unsigned int* sdst = reinterpret_cast<unsigned int*>(smem_raw + kSc2Bufs * kChunk * 16);
+  unsigned int* s_cnt = sdst + kChunk;
+  unsigned int* s_off = s_cnt + nk4;
+  unsigned int* s_dst = s_off + nk4;  // destination of the run's first point
+  unsigned int* s_av = s_dst + nk4;   // points of the run that fit the bin
+  unsigned int* s_ob = s_av + nk4;    // overflow destination of the rest
+  std::uint16_t* perm = reinterpret_cast<std::uint16_t*>(s_ob + nk4);
+  __shared__ unsigned int s_part[64];
+  constexpr int kScanPer = (kMaxTiles + 1 + kSc2Threads - 1) / kSc2Threads;
+  const unsigned int ovf_base = B.hdr[0], ovf_cap = B.hdr[1];
+  const std::uint64_t n_it = (n + kChunk - 1) / kChunk;
+  const std::uint64_t stride = tab_stride(nk4);
+  const int tid = threadIdx.x;
+  auto prefetch = [&](std::uint64_t it, int buf) {
+    if (it < n_it) {
+      const std::uint64_t base = it * kChunk;
+      const std::uint64_t hi = min(n, base + kChunk);
+#pragma unroll
+      for (int j = 0; j < kSc2Per; ++j) {
+        const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kSc2Threads + tid;
+        if (i < hi) cp_async16(raw + buf * kChunk + j * kSc2Threads + tid, pts + i);
+      }
+    }
+    cp_async_commit();
+  };
+  for (int k = tid; k < nk; k += kSc2Threads) s_cnt[k] = 0u;
+  prefetch(blockIdx.x, 0);
+  int b = 0;
+  for (std::uint64_t it = blockIdx.x; it < n_it; it += gridDim.x, b ^= (kSc2Bufs - 1)) {
+    const std::uint64_t base = it * kChunk;
+    const std::uint64_t hi = min(n, base + kChunk);
+    const int cnt = static_cast<int>(hi - base);
+    const double2* rw = raw + b * kChunk;
+    if (kSc2Bufs == 2) {
+      prefetch(it + gridDim.x, b ^ 1);  // raw[b ^ 1] was last read before the barrier closing the previous round
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
+    __syncthreads();  // raw[b] landed, s_cnt zeroed
+    unsigned int kr[kSc2Per];
+#pragma unroll
+    for (int j = 0; j < kSc2Per; ++j) {
+      const int q = j * kSc2Threads + tid;
+      kr[j] = 0xFFFFFFFFu;
+      if (q < cnt) {
+        const double2 p = rw[q];
+        const unsigned int key = static_cast<unsigned int>(tile_key(P, T, p.x, p.y));
+        kr[j] = (key << 16) | atomicAdd(s_cnt + key, 1u);
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan of s_cnt -> s_off
+      const int k0 = tid * kScanPer;
+      unsigned int v[kScanPer], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kScanPer; ++q) {
+        v[q] = k0 + q < nk ? s_cnt[k0 + q] : 0u;
+        sum += v[q];
+      }
+      const int lane = tid & 31, warp = tid >> 5;
+      unsigned int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      if (lane == 31) s_part[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        const unsigned int w = lane < kSc2Threads / 32 ? s_part[lane] : 0u;
+        unsigned int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+          if (lane >= o) wi += x;
+        }
+        if (lane < kSc2Threads / 32) s_part[32 + lane] = wi - w;
+      }
+      __syncthreads();
+      unsigned int run = s_part[32 + warp] + incl - sum;
+#pragma unroll
+      for (int q = 0; q < kScanPer; ++q) {
+        if (k0 + q < nk) s_off[k0 + q] = run;
+        run += v[q];
+      }
+    }
+    __syncthreads();
+    // the claims (one bin per thread, so the atomics' round trips overlap) and the chunk's run table
+    unsigned int* tb = tab + it * stride;
+    for (int k = tid; k < nk; k += kSc2Threads) {
+      const unsigned int v = s_cnt[k];
+      unsigned int dst = 0u, av = 0u;
+      if (v) {
+        const unsigned int got = atomicAdd(B.cur + k, v);
+        const unsigned int cap = __ldg(B.cap + k);
+        av = got < cap ? min(cap - got, v) : 0u;
+        dst = __ldg(B.start + k) + got;
+        s_dst[k] = dst;
+        s_av[k] = av;
+        if (av < v) {
+          const unsigned int ob = atomicAdd(B.hdr + 2, v - av);
+          s_ob[k] = ob;
+          tb[2 * nk4 + k] = ob;
+        }
+      }
+      reinterpret_cast<uint2*>(tb)[k] = make_uint2(dst, s_off[k] | (av << 16));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSc2Per; ++j) {
+      const int q = j * kSc2Threads + tid;
+      if (q < cnt) {
+        const unsigned int key = kr[j] >> 16, r = kr[j] & 0xFFFFu;
+        const unsigned int k = s_off[key] + r, av = s_av[key];
+        unsigned int dst;
+        if (r < av) {
+          dst = s_dst[key] + r;
+        } else {
+          const unsigned int o = s_ob[key] + (r - av);
+          dst = o < ovf_cap ? ovf_base + o : kUnplaced;
+        }
+        perm[k] = static_cast<std::uint16_t>(q);
+        sdst[k] = dst;
+        __stcs(pos16 + base + q, static_cast<std::uint16_t>(k));
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = tid; k < cnt; k += kSc2Threads) {
+      const unsigned int d = sdst[k];
+      if (d != kUnplaced) pts_b[d] = rw[perm[k]];  // run by run
+    }
+    for (int k = tid; k < nk; k += kSc2Threads) s_cnt[k] = 0u;
+    __syncthreads();  // raw[b] free for the prefetch after next
+    if (kSc2Bufs == 1) prefetch(it + gridDim.x, 0);
+  }
+  cp_async_wait0();
 }
 
 // After the scatter: every bin's unfilled tail becomes NaN points (answered
@@ -759,5 +961,126 @@ __global__ void __launch_bounds__(256)
   for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
     if (__ldg(pos + i) == kUnplaced) out[i] = answer_unplaced(P, __ldg(pts + i), hist, counters);
+  }
+}
+
+// out[i] = res[binned position of i], through the chunk's run table (see
+// bin_scatter2_kernel): coalesced reads of res in sorted order, then the
+// chunk's answers through shared memory.
+#ifndef FM_UB2_THREADS
+#define FM_UB2_THREADS 512
+#endif
+constexpr int kUb2Threads = FM_UB2_THREADS;
+constexpr int kUb2Per = kChunk / kUb2Threads;
+static_assert(kChunk % kUb2Threads == 0, "whole rounds");
+inline int ub2_smem(int nk4) { return kChunk * 6 + (kChunk / 32) * 2 + 2 * nk4 * 4; }
+
+// Per chunk: the run table into shared memory; one flag per run head
+// (s_flag[first sorted index] = key + 1) and, per 32 sorted indices, the key
+// at the segment's start (binary search, one per segment); then sorted index
+// k's key is the running maximum of the flags over its segment (a warp
+// scan), its answer res[run's first position + (k - first index)] -- all of
+// a thread's loads issued before the first is used.
+__global__ void __launch_bounds__(kUb2Threads)
+    unbin2_kernel(const std::uint16_t* __restrict__ pos16, const unsigned int* __restrict__ tab, int nk,
+                  BinTable B, const int* __restrict__ res, std::uint64_t n, int* __restrict__ out,
+                  unsigned long long* __restrict__ work) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ unsigned long long s_grab;
+  const int nk4 = (nk + 3) & ~3;
+  int* s_res = reinterpret_cast<int*>(smem_raw);
+  unsigned int* s_dst = reinterpret_cast<unsigned int*>(smem_raw + kChunk * 4);
+  unsigned int* s_oa = s_dst + nk4;  // first sorted index | fitting points << 16
+  std::uint16_t* s_flag = reinterpret_cast<std::uint16_t*>(s_oa + nk4);
+  std::uint16_t* s_seg = s_flag + kChunk;
+  const unsigned int ovf_base = B.hdr[0], ovf_cap = B.hdr[1];
+  const std::uint64_t n_it = (n + kChunk - 1) / kChunk;
+  const std::uint64_t stride = tab_stride(nk4);
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int k = tid; k < kChunk; k += kUb2Threads) s_flag[k] = 0;
+  std::uint64_t it = cta_grab(work + kCtrUnbin, &s_grab);
+  while (it < n_it) {
+    unsigned long long nxt = 0;
+    if (tid == 0) nxt = atomicAdd(work + kCtrUnbin, 1ull);  // in flight while this chunk is answered
+    const std::uint64_t base = it * kChunk;
+    const int cnt = static_cast<int>(min(n, base + kChunk) - base);
+    const unsigned int* tb = tab + it * stride;
+    unsigned int kk[kUb2Per];
+#pragma unroll
+    for (int j = 0; j < kUb2Per; ++j) {
+      const int q = j * kUb2Threads + tid;
+      kk[j] = q < cnt ? __ldcs(pos16 + base + q) : 0u;
+    }
+    for (int k = tid; k < nk; k += kUb2Threads) {
+      const uint2 e = __ldcs(reinterpret_cast<const uint2*>(tb) + k);
+      s_dst[k] = e.x;
+      s_oa[k] = e.y;
+    }
+    __syncthreads();  // the table is in shared memory, every flag is zero
+    for (int k = tid; k < nk; k += kUb2Threads) {
+      const unsigned int off = s_oa[k] & 0xFFFFu;
+      const unsigned int end = k + 1 < nk ? (s_oa[k + 1] & 0xFFFFu) : static_cast<unsigned int>(cnt);
+      if (end > off) s_flag[off] = static_cast<std::uint16_t>(k + 1);
+    }
+    for (int sg = tid; sg * 32 < cnt; sg += kUb2Threads) {
+      int lo = 0, hi = nk;  // the last key whose first sorted index is <= 32 sg
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((s_oa[mid] & 0xFFFFu) <= static_cast<unsigned int>(32 * sg)) {
+          lo = mid + 1;
+        } else {
+          hi = mid;
+        }
+      }
+      s_seg[sg] = static_cast<std::uint16_t>(lo);  // key + 1
+    }
+    __syncthreads();
+    unsigned int idx[kUb2Per];
+#pragma unroll
+    for (int j = 0; j < kUb2Per; ++j) {
+      const int k = j * kUb2Threads + tid;
+      unsigned int f = s_flag[k];
+      s_flag[k] = 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, f, o);
+        if (lane >= o) f = max(f, x);
+      }
+      idx[j] = kUnplaced;
+      if (k < cnt) {
+        const int key = static_cast<int>(max(f, static_cast<unsigned int>(s_seg[k >> 5]))) - 1;
+        const unsigned int w = s_oa[key], r = static_cast<unsigned int>(k) - (w & 0xFFFFu), av = w >> 16;
+        if (r < av) {
+          idx[j] = s_dst[key] + r;
+        } else {  // the run's tail went to the overflow bin (or nowhere)
+          const unsigned int o = __ldg(tb + 2 * nk4 + key) + (r - av);
+          if (o < ovf_cap) idx[j] = ovf_base + o;
+        }
+      }
+    }
+    int v[kUb2Per];
+#pragma unroll
+    for (int j = 0; j < kUb2Per; ++j) v[j] = idx[j] != kUnplaced ? __ldcs(res + idx[j]) : kUnplacedId;
+#pragma unroll
+    for (int j = 0; j < kUb2Per; ++j) s_res[j * kUb2Threads + tid] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kUb2Per; ++j) {
+      const int q = j * kUb2Threads + tid;
+      if (q < cnt) __stcs(out + base + q, s_res[kk[j]]);
+    }
+    if (tid == 0) s_grab = nxt;
+    __syncthreads();
+    it = s_grab;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    unplaced2_kernel(BinTable B, std::uint64_t n, fm::KParams P, const double2* __restrict__ pts,
+                     int* __restrict__ out, HistT* __restrict__ hist, unsigned long long* __restrict__ counters) {
+  if (B.hdr[2] <= B.hdr[1]) return;
+  for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    if (out[i] == kUnplacedId) out[i] = answer_unplaced(P, __ldg(pts + i), hist, counters);
   }
 }
