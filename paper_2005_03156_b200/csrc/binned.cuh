@@ -18,18 +18,21 @@
 //   bin_sample_kernel   one point per 64-point stratum: sampled bin counts
 //   bin_plan_kernel     bin capacities (estimate + 3 sigma + pad), their
 //                       scan as bin starts, the overflow bin after them
-//   bin_scatter_kernel 4K points at a time: a shared-memory counting sort
-//                       by tile, one global atomic per non-empty bin claims
-//                       the run's space, runs written whole (pts_b), each
-//                       point's binned position to pos[i] (coalesced)
+//   bin_scatter_kernel  a chunk of 4K points at a time, copied into shared
+//                       memory by cp.async: a counting sort by tile, one
+//                       global atomic per non-empty bin claims the run's
+//                       space, runs written whole (pts_b); per point its
+//                       sorted index inside the chunk (pos16, 2 bytes), per
+//                       chunk the table of its runs
 //   bin_seal_kernel     unused bin tails become NaN points; the binned length
 //   binned_query_kernel the query over pts_b in order: locate, true hits
-//                       answered at once, boundary points through a
-//                       warp-private shared-memory ring whose batches of 32
-//                       slots are staged by cp.async one batch ahead of
-//                       their evaluation (exactly resolve_kernel's code);
-//                       answers to res[k]
-//   unbin_kernel        out[i] = res[pos[i]]
+//                       answered at once, boundary points through
+//                       warp-private shared-memory rings (full, half and
+//                       double slots apart) whose batches of 32 slots are
+//                       staged by cp.async one batch ahead of their
+//                       evaluation; answers to res[k]
+//   unbin_kernel        out[i] = res[binned position of i], read run by run
+//                       (coalesced) through the chunk's run table
 //   unplaced_kernel     points no bin could take (returns at once normally)
 // Iterations are walked with a grid stride, so at any moment the grid reads
 // one window of the stream and every tile's points stay in about input
@@ -42,9 +45,6 @@
 // same locate_n / eval_leaf_slot code as the stream path, so the answers
 // are identical whatever tile or order a point ends up in.
 
-#ifndef FM_BIN2
-#define FM_BIN2 1  // 0: the register-held scatter and the per-point gather (A/B builds)
-#endif
 #ifndef FM_QMINB
 #define FM_QMINB 2
 #endif
@@ -83,23 +83,7 @@ __device__ __forceinline__ int tile_key(const fm::KParams& P, const TileGeom& T,
   return in ? (iy >> T.ts) * T.tnx + (ix >> T.ts) : T.n_tiles;
 }
 
-// The point stream is cut into chunks of ch = kScatterIter * m points
-// (m >= 1 keeps the (n_tiles + 1) x n_chunks table under kMaxTableEntries),
-// and both passes walk the chunks with a grid stride: at any moment the
-// whole grid reads one narrow window of the stream and, in every tile, writes
-// one narrow window of its runs.  (Contiguous per-CTA blocks measured 3.35
-// TB/s for the same copy against 5.7 TB/s for a grid stride: hundreds of
-// streams far apart in memory thrash the TLB -- tools/exp_copy.cu,
-// profiles/r2q.)
-#ifndef FM_SC_PER
-#define FM_SC_PER 16
-#endif
-#ifndef FM_SC_THREADS
-#define FM_SC_THREADS 256
-#endif
-constexpr int kScatterThreads = FM_SC_THREADS;
-constexpr int kScPer = FM_SC_PER;
-constexpr int kScatterIter = kScatterThreads * kScPer;  // 4096 points
+constexpr int kSampleThreads = 256;
 
 // ---- single-pass binning with sampled bin capacities ----------------------
 // Sizing the bins exactly takes a counting pass over the whole stream (16
@@ -136,7 +120,7 @@ __device__ __forceinline__ std::uint32_t stratum_hash(std::uint64_t j) {
   return static_cast<std::uint32_t>(z >> 40);
 }
 
-__global__ void __launch_bounds__(kScatterThreads)
+__global__ void __launch_bounds__(kSampleThreads)
     bin_sample_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
                       unsigned int* __restrict__ counts) {
   extern __shared__ unsigned int s_hist[];
@@ -225,151 +209,27 @@ __global__ void __launch_bounds__(kPlanThreads)
   }
 }
 
-// The scatter, one pass: each kScatterIter-point iteration is counting-sorted
-// by bin in shared memory (as in bin_scatter_kernel), then one thread per
-// non-empty bin claims the run's space with a global atomic; runs are
-// written whole, consecutive lanes storing consecutive points.
-__global__ void __launch_bounds__(kScatterThreads)
-    bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
-                        BinTable B, double2* __restrict__ pts_b, unsigned int* __restrict__ pos) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nk = T.n_tiles + 1;
-  const int nk4 = (nk + 3) & ~3;
-  double2* stage = reinterpret_cast<double2*>(smem_raw);
-  unsigned int* sdst = reinterpret_cast<unsigned int*>(smem_raw + kScatterIter * 16);
-  unsigned int* s_cnt = reinterpret_cast<unsigned int*>(smem_raw + kScatterIter * 20);
-  unsigned int* s_off = s_cnt + nk4;
-  unsigned int* s_dst = s_off + nk4;  // destination of the run's first point
-  unsigned int* s_av = s_dst + nk4;   // points of the run that fit the bin
-  unsigned int* s_ob = s_av + nk4;    // overflow destination of the rest
-  __shared__ unsigned int s_part[64];
-  constexpr int kScanPer = (kMaxTiles + 1 + kScatterThreads - 1) / kScatterThreads;
-  const unsigned int ovf_base = B.hdr[0], ovf_cap = B.hdr[1];
-  const std::uint64_t n_it = (n + kScatterIter - 1) / kScatterIter;
-  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
-  for (std::uint64_t it = blockIdx.x; it < n_it; it += gridDim.x) {
-    const std::uint64_t base = it * kScatterIter;
-    const std::uint64_t hi = min(n, base + kScatterIter);
-    double2 p[kScPer];
-    unsigned int kr[kScPer];
-#pragma unroll
-    for (int j = 0; j < kScPer; ++j) {
-      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-      p[j] = i < hi ? __ldcs(pts + i) : make_double2(0.0, 0.0);
-    }
-    __syncthreads();  // s_cnt zeroed
-#pragma unroll
-    for (int j = 0; j < kScPer; ++j) {
-      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-      kr[j] = 0xFFFFFFFFu;
-      if (i < hi) {
-        const unsigned int key = static_cast<unsigned int>(tile_key(P, T, p[j].x, p[j].y));
-        kr[j] = (key << 16) | atomicAdd(s_cnt + key, 1u);
-      }
-    }
-    __syncthreads();
-    {  // exclusive scan of s_cnt -> s_off; claims of the non-empty bins
-      const int k0 = threadIdx.x * kScanPer;
-      unsigned int v[kScanPer], sum = 0;
-#pragma unroll
-      for (int q = 0; q < kScanPer; ++q) {
-        v[q] = k0 + q < nk ? s_cnt[k0 + q] : 0u;
-        sum += v[q];
-      }
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      unsigned int incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += x;
-      }
-      if (lane == 31) s_part[warp] = incl;
-      __syncthreads();
-      if (warp == 0) {
-        const unsigned int w = lane < kScatterThreads / 32 ? s_part[lane] : 0u;
-        unsigned int wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-          if (lane >= o) wi += x;
-        }
-        if (lane < kScatterThreads / 32) s_part[32 + lane] = wi - w;
-      }
-      __syncthreads();
-      unsigned int run = s_part[32 + warp] + incl - sum;
-#pragma unroll
-      for (int q = 0; q < kScanPer; ++q) {
-        if (k0 + q < nk) s_off[k0 + q] = run;
-        run += v[q];
-      }
-    }
-    // the claims: one bin per thread, so the atomics' round trips overlap
-    for (int k = threadIdx.x; k < nk; k += kScatterThreads) {
-      const unsigned int v = s_cnt[k];
-      if (v) {
-        const unsigned int got = atomicAdd(B.cur + k, v);
-        const unsigned int cap = __ldg(B.cap + k);
-        const unsigned int av = got < cap ? min(cap - got, v) : 0u;
-        s_dst[k] = __ldg(B.start + k) + got;
-        s_av[k] = av;
-        if (av < v) s_ob[k] = atomicAdd(B.hdr + 2, v - av);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kScPer; ++j) {
-      const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kScatterThreads + threadIdx.x;
-      if (kr[j] != 0xFFFFFFFFu) {
-        const unsigned int key = kr[j] >> 16, r = kr[j] & 0xFFFFu;
-        const unsigned int k = s_off[key] + r, av = s_av[key];
-        unsigned int dst;
-        if (r < av) {
-          dst = s_dst[key] + r;
-        } else {
-          const unsigned int o = s_ob[key] + (r - av);
-          dst = o < ovf_cap ? ovf_base + o : kUnplaced;
-        }
-        stage[k] = p[j];
-        sdst[k] = dst;
-        __stcs(pos + i, dst);
-      }
-    }
-    __syncthreads();
-    const int cnt = static_cast<int>(hi - base);
-#pragma unroll 4
-    for (int k = threadIdx.x; k < cnt; k += kScatterThreads) {
-      const unsigned int d = sdst[k];
-      if (d != kUnplaced) pts_b[d] = stage[k];  // run by run
-    }
-    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_cnt[k] = 0u;
-  }
-}
-
-// ---- the pipelined scatter (bin_scatter2_kernel) and its gather (unbin2) ----
-// bin_scatter_kernel above holds its iteration's points in registers and
-// runs at 16 warps per SM through five barrier-separated phases, so the
-// DRAM pipes idle while a CTA counts, scans and claims (profiles/r2v: 49%
-// DRAM throughput, 32% issue slots, 12 cycles per issued instruction).
-// Here one CTA per SM streams its chunks through a double-buffered shared-
-// memory window filled by cp.async one chunk ahead, so chunk c+1 is in
-// flight during every phase of chunk c, and no point lives in a register:
-//   raw[2][kChunk]  the chunk's points as loaded (16 B each)
+// ---- the scatter and its gather ---------------------------------------------
+// Two CTAs of 512 threads per SM each stream chunks of kChunk points through
+// a shared-memory window filled by cp.async (while one CTA waits for its
+// window the other sorts or writes), so no point lives in a register:
+//   raw[kChunk]     the chunk's points as loaded (16 B each)
 //   perm[k]         source index of the point at sorted position k
 //   sdst[k]         its binned position
-// The chunk is counting-sorted by tile key as before; the runs are then
-// written whole, pts_b[sdst[k]] = raw[perm[k]] for consecutive k.
+// The chunk is counting-sorted by tile key; the runs are then written
+// whole, pts_b[sdst[k]] = raw[perm[k]] for consecutive k.  Round 2's first
+// scatter held the points in registers (127 registers, 16 warps per SM):
+// 10.1 ms per 1B c3 points against 8.1 ms (profiles/r2al, r2am); a
+// double-buffered window with one 1024-thread CTA per SM measured 9.4 ms.
 // Instead of a 4-byte binned position per point, the scatter leaves
 //   pos16[i]        the point's sorted index k inside its chunk (2 B), and
 //   tab[c][key]     {binned position of the run's first point,
 //                    first sorted index | points that fit the bin << 16}
 //                   (+ the run's overflow-bin offset, read only for runs
 //                   that did not fit),
-// and unbin2_kernel turns the per-point gather res[pos[i]] -- one L2
-// sector per point, the L2 gather rate (4.3 ms per 1B points) -- into
-// coalesced reads: thread k of a chunk finds its run by binary search over
-// the first sorted indices and loads res[first + (k - first index)], so
-// consecutive threads read consecutive answers; the chunk's answers then
-// go out through shared memory, out[i] = s_res[pos16[i]].
+// and unbin_kernel turns the per-point gather res[pos[i]] -- one L2 sector
+// per point, bound by the L2 gather rate (4.3 ms per 1B points) -- into
+// coalesced reads of res in sorted order (3.4 ms).
 #ifndef FM_SC2_THREADS
 #define FM_SC2_THREADS 512
 #endif
@@ -384,24 +244,23 @@ __global__ void __launch_bounds__(kScatterThreads)
 #endif
 constexpr int kSc2Threads = FM_SC2_THREADS;
 constexpr int kSc2Per = FM_SC2_PER;
-constexpr int kSc2Bufs = FM_SC2_BUFS;
 constexpr int kChunk = kSc2Threads * kSc2Per;  // points per chunk
 static_assert(kChunk <= 32768, "sorted indices and counts are 16-bit fields");
-constexpr int kUnplacedId = INT_MIN;  // out[i] of a point no bin could take, until unplaced2_kernel
+constexpr int kUnplacedId = INT_MIN;  // out[i] of a point no bin could take, until unplaced_kernel
 
 // Words per chunk of the run table: nk4 x {dst, off | av << 16}, nk4 x overflow offset.
 __host__ __device__ inline std::uint64_t tab_stride(int nk4) { return 3ull * static_cast<std::uint64_t>(nk4); }
-inline int sc2_smem(int nk4) { return kChunk * (kSc2Bufs * 16 + 4 + 2) + 5 * nk4 * 4; }
+inline int sc2_smem(int nk4) { return kChunk * (16 + 4 + 2) + 5 * nk4 * 4; }
 
 __global__ void __launch_bounds__(kSc2Threads, FM_SC2_MINB)
-    bin_scatter2_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
+    bin_scatter_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
                         BinTable B, double2* __restrict__ pts_b, std::uint16_t* __restrict__ pos16,
                         unsigned int* __restrict__ tab) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nk = T.n_tiles + 1;
   const int nk4 = (nk + 3) & ~3;
-  double2* raw = reinterpret_cast<double2*>(smem_raw);  // [2][kChunk]
-  unsigned int* sdst = reinterpret_cast<unsigned int*>(smem_raw + kSc2Bufs * kChunk * 16);
+  double2* raw = reinterpret_cast<double2*>(smem_raw);
+  unsigned int* sdst = reinterpret_cast<unsigned int*>(smem_raw + kChunk * 16);
   unsigned int* s_cnt = sdst + kChunk;
   unsigned int* s_off = s_cnt + nk4;
   unsigned int* s_dst = s_off + nk4;  // destination of the run's first point
@@ -414,40 +273,33 @@ __global__ void __launch_bounds__(kSc2Threads, FM_SC2_MINB)
   const std::uint64_t n_it = (n + kChunk - 1) / kChunk;
   const std::uint64_t stride = tab_stride(nk4);
   const int tid = threadIdx.x;
-  auto prefetch = [&](std::uint64_t it, int buf) {
+  auto prefetch = [&](std::uint64_t it) {
     if (it < n_it) {
       const std::uint64_t base = it * kChunk;
       const std::uint64_t hi = min(n, base + kChunk);
 #pragma unroll
       for (int j = 0; j < kSc2Per; ++j) {
         const std::uint64_t i = base + static_cast<std::uint64_t>(j) * kSc2Threads + tid;
-        if (i < hi) cp_async16(raw + buf * kChunk + j * kSc2Threads + tid, pts + i);
+        if (i < hi) cp_async16(raw + j * kSc2Threads + tid, pts + i);
       }
     }
     cp_async_commit();
   };
   for (int k = tid; k < nk; k += kSc2Threads) s_cnt[k] = 0u;
-  prefetch(blockIdx.x, 0);
-  int b = 0;
-  for (std::uint64_t it = blockIdx.x; it < n_it; it += gridDim.x, b ^= (kSc2Bufs - 1)) {
+  prefetch(blockIdx.x);
+  for (std::uint64_t it = blockIdx.x; it < n_it; it += gridDim.x) {
     const std::uint64_t base = it * kChunk;
     const std::uint64_t hi = min(n, base + kChunk);
     const int cnt = static_cast<int>(hi - base);
-    const double2* rw = raw + b * kChunk;
-    if (kSc2Bufs == 2) {
-      prefetch(it + gridDim.x, b ^ 1);  // raw[b ^ 1] was last read before the barrier closing the previous round
-      cp_async_wait1();
-    } else {
-      cp_async_wait0();
-    }
-    __syncthreads();  // raw[b] landed, s_cnt zeroed
+    cp_async_wait0();
+    __syncthreads();  // the window landed, s_cnt zeroed
     unsigned int kr[kSc2Per];
 #pragma unroll
     for (int j = 0; j < kSc2Per; ++j) {
       const int q = j * kSc2Threads + tid;
       kr[j] = 0xFFFFFFFFu;
       if (q < cnt) {
-        const double2 p = rw[q];
+        const double2 p = raw[q];
         const unsigned int key = static_cast<unsigned int>(tile_key(P, T, p.x, p.y));
         kr[j] = (key << 16) | atomicAdd(s_cnt + key, 1u);
       }
@@ -532,11 +384,11 @@ __global__ void __launch_bounds__(kSc2Threads, FM_SC2_MINB)
 #pragma unroll 4
     for (int k = tid; k < cnt; k += kSc2Threads) {
       const unsigned int d = sdst[k];
-      if (d != kUnplaced) pts_b[d] = rw[perm[k]];  // run by run
+      if (d != kUnplaced) pts_b[d] = raw[perm[k]];  // run by run
     }
     for (int k = tid; k < nk; k += kSc2Threads) s_cnt[k] = 0u;
-    __syncthreads();  // raw[b] free for the prefetch after next
-    if (kSc2Bufs == 1) prefetch(it + gridDim.x, 0);
+    __syncthreads();  // the window is free
+    prefetch(it + gridDim.x);
   }
   cp_async_wait0();
 }
@@ -568,13 +420,26 @@ __global__ void __launch_bounds__(256)
 // ring of (binned index, entry) pairs and are evaluated in whole batches of
 // 32 straight from global memory (both halves of the 256-byte slot loaded
 // at once), so the leaf-slot batches never run the wider double-slot code.
-constexpr int kQWarps = 8;
+#ifndef FM_QWARPS
+#define FM_QWARPS 8
+#endif
+constexpr int kQWarps = FM_QWARPS;
 constexpr int kQCap = 128;
 constexpr int kDCap = 128;
+#ifndef FM_QLD
+#define FM_QLD __ldg  // the staged batch re-reads its points: ld.cs (evict-first) made those DRAM reads (r2ap: 49.9 vs 36.3 GB)
+#endif
+// Three rings of (binned index, entry) pairs: full leaf slots (and whatever
+// a split cell descends to), half slots (kHalfBit: the content lies in the
+// slot's first 64 bytes -- at most 2 candidates, 2 edges, 1 breakpoint; half
+// of c3's boundary cells), double slots.  A batch is all of one kind, so a
+// half batch runs half the copies, half the shared-memory reads and a
+// 2-edge, 2-candidate evaluation.  The point itself is re-read from pts_b
+// when its batch is staged (an L2 hit, one round before it is needed).
 struct WarpSmemQ {
   alignas(16) std::uint8_t pool[2][32 * fm::kSlotBytes];
-  double qx[kQCap], qy[kQCap];
   std::uint32_t qk[kQCap], qe[kQCap];
+  std::uint32_t hk[kQCap], he[kQCap];
   std::uint32_t dk[kDCap], de[kDCap];
 };
 constexpr int kSmemQ = static_cast<int>(sizeof(WarpSmemQ)) * kQWarps;
@@ -585,6 +450,8 @@ struct RingState {
   int pb = 0;
   QItem pit;             // this lane's staged item
   int dhead = 0, dn = 0; // double-slot ring
+  int hhead = 0, hn = 0; // half-slot ring
+  bool phalf = false;    // the staged batch is a half batch
 };
 
 // Evaluate double-slot points in batches of 32 (any remainder when draining).
@@ -617,33 +484,150 @@ __device__ __forceinline__ void dpump(const fm::KParams& P, const double2* __res
   }
 }
 
-// Stage the next batch (when 32 items wait, or any when draining) and
-// evaluate the previously staged one; repeat while full batches remain.
+// Start copying the first 64 bytes of the slots of the items held by lanes
+// [0, n): 4 lanes per slot, 8 slots per instruction.  Chunk c of slot r is
+// stored at chunk c ^ ((r >> 1) & 3) of its 64-byte row, so the owner lanes'
+// 16-byte reads are bank-conflict free.
+__device__ __forceinline__ void stage_half(const fm::KParams& P, std::uint8_t* buf, std::uint32_t e, int n,
+                                           int lane) {
+  const int c = lane & 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = 8 * q + (lane >> 2);
+    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
+    if (r < n) cp_async16(buf + r * 64 + 16 * (c ^ ((r >> 1) & 3)), fm::slot_ptr(P, er) + 16 * c);
+  }
+  cp_async_commit();
+}
+
+// A half leaf slot (index_format.h: bytes 0..63 of kind 1 with <= 2
+// candidates and <= 2 vertices + <= 1 breakpoint, or 3 vertices): one
+// chain, at most two edges.
+template <bool kCount>
+__device__ __forceinline__ int eval_half_leaf(const uint4 (&c)[4], double px, double py, fm::WorkCount& wc) {
+  const std::uint32_t h = c[0].x;
+  const std::uint32_t nv = (h >> 8) & 0xFFu, nc = (h >> 16) & 0xFFu, nb = h >> 24;
+  const double v0x = fm::as_f64(c[1].x, c[1].y), v0y = fm::as_f64(c[1].z, c[1].w);
+  const double v1x = fm::as_f64(c[2].x, c[2].y), v1y = fm::as_f64(c[2].z, c[2].w);
+  const double v2x = fm::as_f64(c[3].x, c[3].y), v2y = fm::as_f64(c[3].z, c[3].w);
+  std::uint32_t m = 0;
+  if (nv >= 2u) {
+    if (kCount) wc.edges++;
+    m |= fm::edge_bit(px, py, v0x, v0y, v1x, v1y);
+  }
+  if (nv >= 3u) {
+    if (kCount) wc.edges++;
+    m |= fm::edge_bit(px, py, v1x, v1y, v2x, v2y) << 1;
+  }
+  const std::uint32_t bm = (nv < 3u && nb > 0u && py > v2x) ? 1u : 0u;  // +48: break[0] when n_verts < 3
+  const std::uint32_t w = c[0].y;  // edge_mask[0..1], info[0..1]
+  int id = -1;
+#pragma unroll
+  for (int q = 1; q >= 0; --q) {  // descending, so the smallest odd candidate wins
+    const std::uint32_t mk = (w >> (8 * q)) & 0xFFu, inf = (w >> (16 + 8 * q)) & 0xFFu;
+    const std::uint32_t par = (inf >> 7) ^ __popc(m & mk) ^ __popc(bm & inf & 3u);
+    if (static_cast<std::uint32_t>(q) < nc && (par & 1u)) id = static_cast<int>(q == 0 ? c[0].z : c[0].w);
+  }
+  if (kCount) wc.cands += nc;
+  return id;
+}
+
+// Evaluate a staged half batch (leaf, split or overflow slots; all live in
+// their first 64 bytes).  Returns like eval_staged.
 template <bool kHist, bool kCount>
-__device__ __forceinline__ void pump(const fm::KParams& P, WarpSmemQ& S, RingState& R, bool drain,
-                                     int lane, int* __restrict__ res, const HistSink& hist,
-                                     fm::WorkCount& wc) {
+__device__ __forceinline__ std::uint32_t eval_staged_half(const fm::KParams& P, const std::uint8_t* buf,
+                                                          const QItem& it, int n, int lane,
+                                                          int* __restrict__ out, const HistSink& hist,
+                                                          fm::WorkCount& wc) {
+  std::uint32_t requeue = 0;
+  if (lane < n) {
+    const std::uint8_t* base = buf + lane * 64;
+    const int s = (lane >> 1) & 3;
+    uint4 c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = *reinterpret_cast<const uint4*>(base + 16 * (k ^ s));
+    const std::uint32_t kind = c[0].x & 0xFFu;
+    int id = -1;
+    bool done = true;
+    if (kind == fm::kSlotLeaf) {
+      if (kCount) wc.boundary++;
+      id = eval_half_leaf<kCount>(c, it.px, it.py, wc);
+    } else if (kind == fm::kSlotSplit) {
+      const double x0 = fm::as_f64(c[0].z, c[0].w), y0 = fm::as_f64(c[1].x, c[1].y);
+      const double ihw = fm::as_f64(c[1].z, c[1].w), ihh = fm::as_f64(c[2].x, c[2].y);
+      int ci = static_cast<int>(__dmul_rn(__dsub_rn(it.px, x0), ihw));
+      int cj = static_cast<int>(__dmul_rn(__dsub_rn(it.py, y0), ihh));
+      ci = min(max(ci, 0), 1);
+      cj = min(max(cj, 0), 1);
+      const std::uint32_t k2 = 2 * cj + ci;
+      const std::uint32_t ce = k2 == 0 ? c[2].z : k2 == 1 ? c[2].w : k2 == 2 ? c[3].x : c[3].y;
+      if (ce == fm::kEmpty) {
+        id = -1;
+      } else if (ce < fm::kRecordBit) {
+        id = static_cast<int>(ce);
+      } else {
+        requeue = ce;
+        done = false;
+      }
+    } else {  // overflow record
+      if (kCount) wc.boundary++;
+      id = fm::resolve_overflow<kCount>(P, (static_cast<std::uint64_t>(c[0].w) << 32) | c[0].z, it.px,
+                                        it.py, wc);
+    }
+    if (done) emit<kHist>(out, hist, it.i, id);
+  }
+  return requeue;
+}
+
+// Stage the next batch -- a full-slot batch when 32 such items wait, else a
+// half-slot batch (any when draining) -- and evaluate the previously staged
+// one; repeat while whole batches remain.  Split cells put their child
+// entry into the full ring, whose evaluation takes every slot kind.
+template <bool kHist, bool kCount>
+__device__ __forceinline__ void pump(const fm::KParams& P, const double2* __restrict__ pts, WarpSmemQ& S,
+                                     RingState& R, bool drain, int lane, int* __restrict__ res,
+                                     const HistSink& hist, fm::WorkCount& wc) {
   for (;;) {
-    const bool stage = R.qn >= 32 || (drain && R.qn > 0);
+    const bool sf = R.qn >= 32 || (drain && R.qn > 0);
+    const bool sh = !sf && (R.hn >= 32 || (drain && R.hn > 0));
+    const bool stage = sf || sh;
     if (!stage && !(drain && R.pend > 0)) break;
     int m = 0;
     QItem nit;
     nit.px = nit.py = 0.0;
     nit.i = 0;
     nit.e = fm::kEmpty;
-    if (stage) {
+    if (sf) {
       m = min(R.qn, 32);
       if (lane < m) {
         const int s = (R.head + lane) & (kQCap - 1);
-        nit.px = S.qx[s];
-        nit.py = S.qy[s];
         nit.i = S.qk[s];
         nit.e = S.qe[s];
       }
       R.head = (R.head + m) & (kQCap - 1);
       R.qn -= m;
+    } else if (sh) {
+      m = min(R.hn, 32);
+      if (lane < m) {
+        const int s = (R.hhead + lane) & (kQCap - 1);
+        nit.i = S.hk[s];
+        nit.e = S.he[s];
+      }
+      R.hhead = (R.hhead + m) & (kQCap - 1);
+      R.hn -= m;
+    }
+    if (stage) {
       __syncwarp();
-      stage_slots(P, S.pool[R.pb ^ 1], nit.e, m, lane);  // commits one group
+      if (lane < m) {
+        const double2 p = __ldg(pts + nit.i);
+        nit.px = p.x;
+        nit.py = p.y;
+      }
+      if (sf) {
+        stage_slots(P, S.pool[R.pb ^ 1], nit.e, m, lane);  // commits one group
+      } else {
+        stage_half(P, S.pool[R.pb ^ 1], nit.e, m, lane);
+      }
     }
     if (R.pend > 0) {
       if (stage) {
@@ -652,13 +636,12 @@ __device__ __forceinline__ void pump(const fm::KParams& P, WarpSmemQ& S, RingSta
         cp_async_wait0();
       }
       __syncwarp();
-      const std::uint32_t ce = eval_staged<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res,
-                                                          hist, wc);
+      const std::uint32_t ce =
+          R.phalf ? eval_staged_half<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res, hist, wc)
+                  : eval_staged<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res, hist, wc);
       const std::uint32_t rq = __ballot_sync(0xFFFFFFFFu, ce != 0u);
-      if (ce != 0u) {  // split cell: the child entry goes back into the ring
+      if (ce != 0u) {  // split cell: the child entry goes into the full ring
         const int s = (R.head + R.qn + __popc(rq & ((1u << lane) - 1u))) & (kQCap - 1);
-        S.qx[s] = R.pit.px;
-        S.qy[s] = R.pit.py;
         S.qk[s] = R.pit.i;
         S.qe[s] = ce;
       }
@@ -668,7 +651,8 @@ __device__ __forceinline__ void pump(const fm::KParams& P, WarpSmemQ& S, RingSta
     if (stage) R.pb ^= 1;
     R.pit = nit;
     R.pend = m;
-    if (!drain && R.qn < 32) break;
+    R.phalf = sh;
+    if (!drain && R.qn < 32 && R.hn < 32) break;
   }
 }
 
@@ -717,7 +701,7 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const std::uint64_t i = x * tile + u * 32 + lane;
-      q[u] = (x < n_tiles && i < n) ? __ldcs(pts + i) : make_double2(NAN, NAN);
+      q[u] = (x < n_tiles && i < n) ? FM_QLD(pts + i) : make_double2(NAN, NAN);
     }
   };
   std::uint64_t g_end = 0;
@@ -742,15 +726,21 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
       const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
       const bool is_dbl = is_rec && (e[u] & fm::kDoubleBit) && !(e[u] & fm::kHalfBit);
       if (valid && !is_rec) emit<kHist>(res, hs, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
-      const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec && !is_dbl);
-      if (is_rec && !is_dbl) {
+      const bool is_half = is_rec && (e[u] & fm::kHalfBit);
+      const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec && !is_dbl && !is_half);
+      if (is_rec && !is_dbl && !is_half) {
         const int s = (R.head + R.qn + __popc(b & lt_mask)) & (kQCap - 1);
-        S.qx[s] = p[u].x;
-        S.qy[s] = p[u].y;
         S.qk[s] = static_cast<std::uint32_t>(i);
         S.qe[s] = e[u];
       }
       R.qn += __popc(b);
+      const std::uint32_t bh = __ballot_sync(0xFFFFFFFFu, is_half);
+      if (is_half) {
+        const int s = (R.hhead + R.hn + __popc(bh & lt_mask)) & (kQCap - 1);
+        S.hk[s] = static_cast<std::uint32_t>(i);
+        S.he[s] = e[u];
+      }
+      R.hn += __popc(bh);
       const std::uint32_t bd = __ballot_sync(0xFFFFFFFFu, is_dbl);
       if (is_dbl) {
         const int s = (R.dhead + R.dn + __popc(bd & lt_mask)) & (kDCap - 1);
@@ -762,7 +752,7 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
     if (kCount) done += min(tile, n - base);
     __syncwarp();
     dpump<kHist, kCount>(P, pts, S, R, false, lane, res, hs, wc);
-    pump<kHist, kCount>(P, S, R, false, lane, res, hs, wc);
+    pump<kHist, kCount>(P, pts, S, R, false, lane, res, hs, wc);
     t = t1;
     t1 = t2;
 #pragma unroll
@@ -773,7 +763,7 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
     }
   }
   dpump<kHist, kCount>(P, pts, S, R, true, lane, res, hs, wc);
-  pump<kHist, kCount>(P, S, R, true, lane, res, hs, wc);
+  pump<kHist, kCount>(P, pts, S, R, true, lane, res, hs, wc);
   hist_close<kHist>(hs);
   if (kCount) {
     unsigned long long v[4] = {lane == 0 ? done : 0ull, wc.boundary, wc.cands, wc.edges};
@@ -858,20 +848,7 @@ __global__ void __launch_bounds__(kHistThreads)
   }
 }
 
-// out[i] = res[pos[i]].  CTAs take blocks of kUnbinBlock points in
-// increasing order from the work counter, four points per thread per round
-// (16-byte pos loads and id stores when `out` is 16-byte aligned).
-constexpr int kUnbinThreads = 256;
-#ifndef FM_UNBIN_ROUNDS
-#define FM_UNBIN_ROUNDS 8
-#endif
-constexpr int kUnbinRounds = FM_UNBIN_ROUNDS;
-#ifndef FM_UNBIN_LD
-#define FM_UNBIN_LD __ldg
-#endif
-constexpr std::uint64_t kUnbinBlock = 4ull * kUnbinThreads * kUnbinRounds;  // 8192 points
-
-// A point the binning could not place (pos == kUnplaced; see the sampled
+// A point the binning could not place (out[i] == kUnplacedId; see the sampled
 // capacities above): answered straight from the index, histogram and
 // counters included.  Never taken when the sample represents the stream.
 __device__ __noinline__ int answer_unplaced(const fm::KParams& P, double2 p, HistT* __restrict__ hist,
@@ -898,74 +875,8 @@ __device__ __noinline__ int answer_unplaced(const fm::KParams& P, double2 p, His
   return id;
 }
 
-__global__ void __launch_bounds__(kUnbinThreads)
-    unbin_kernel(const unsigned int* __restrict__ pos, const int* __restrict__ res, std::uint64_t n,
-                 int* __restrict__ out, unsigned long long* __restrict__ work) {
-  __shared__ unsigned long long s_grab;
-  const bool vec = (reinterpret_cast<std::uintptr_t>(out) & 15u) == 0;
-  const std::uint64_t n_blocks = (n + kUnbinBlock - 1) / kUnbinBlock;
-  const uint4* p4 = reinterpret_cast<const uint4*>(pos);
-  int4* o4 = reinterpret_cast<int4*>(out);
-  for (std::uint64_t b = cta_grab(work + kCtrUnbin, &s_grab); b < n_blocks;
-       b = cta_grab(work + kCtrUnbin, &s_grab)) {
-    const std::uint64_t base = b * kUnbinBlock;
-    if (vec && base + kUnbinBlock <= n) {
-      // every pos load of the block, then every gather: 4 * kUnbinRounds
-      // independent loads in flight per thread
-      uint4 k[kUnbinRounds];
-      bool bad = false;
-#pragma unroll
-      for (int r = 0; r < kUnbinRounds; ++r) {
-        k[r] = __ldcs(p4 + base / 4 + static_cast<std::uint64_t>(r) * kUnbinThreads + threadIdx.x);
-        bad |= (k[r].x == kUnplaced) | (k[r].y == kUnplaced) | (k[r].z == kUnplaced) | (k[r].w == kUnplaced);
-      }
-      if (bad) {  // kUnplaced entries are left to unplaced_kernel
-#pragma unroll 1
-        for (int r = 0; r < 4 * kUnbinRounds; ++r) {
-          const std::uint64_t i = base + 4 * (static_cast<std::uint64_t>(r >> 2) * kUnbinThreads + threadIdx.x) + (r & 3);
-          const unsigned int kk = pos[i];
-          if (kk != kUnplaced) out[i] = __ldg(res + kk);
-        }
-        continue;
-      }
-      int4 v[kUnbinRounds];
-#pragma unroll
-      for (int r = 0; r < kUnbinRounds; ++r) {
-        v[r].x = FM_UNBIN_LD(res + k[r].x);
-        v[r].y = FM_UNBIN_LD(res + k[r].y);
-        v[r].z = FM_UNBIN_LD(res + k[r].z);
-        v[r].w = FM_UNBIN_LD(res + k[r].w);
-      }
-#pragma unroll
-      for (int r = 0; r < kUnbinRounds; ++r) {
-        __stcs(o4 + base / 4 + static_cast<std::uint64_t>(r) * kUnbinThreads + threadIdx.x, v[r]);
-      }
-    } else {
-      const std::uint64_t end = min(n, base + kUnbinBlock);
-      for (std::uint64_t i = base + threadIdx.x; i < end; i += kUnbinThreads) {
-        const unsigned int k = __ldcs(pos + i);
-        if (k != kUnplaced) __stcs(out + i, __ldg(res + k));
-      }
-    }
-  }
-}
-
-// Points the binning could not place (the overflow bin filled up: a stream
-// whose sample missed where its points are): answered straight from the
-// index.  Returns at once in the normal case.
-__global__ void __launch_bounds__(256)
-    unplaced_kernel(BinTable B, const unsigned int* __restrict__ pos, std::uint64_t n, fm::KParams P,
-                    const double2* __restrict__ pts, int* __restrict__ out, HistT* __restrict__ hist,
-                    unsigned long long* __restrict__ counters) {
-  if (B.hdr[2] <= B.hdr[1]) return;
-  for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-    if (__ldg(pos + i) == kUnplaced) out[i] = answer_unplaced(P, __ldg(pts + i), hist, counters);
-  }
-}
-
 // out[i] = res[binned position of i], through the chunk's run table (see
-// bin_scatter2_kernel): coalesced reads of res in sorted order, then the
+// bin_scatter_kernel): coalesced reads of res in sorted order, then the
 // chunk's answers through shared memory.
 #ifndef FM_UB2_THREADS
 #define FM_UB2_THREADS 512
@@ -982,7 +893,7 @@ inline int ub2_smem(int nk4) { return kChunk * 6 + (kChunk / 32) * 2 + 2 * nk4 *
 // scan), its answer res[run's first position + (k - first index)] -- all of
 // a thread's loads issued before the first is used.
 __global__ void __launch_bounds__(kUb2Threads)
-    unbin2_kernel(const std::uint16_t* __restrict__ pos16, const unsigned int* __restrict__ tab, int nk,
+    unbin_kernel(const std::uint16_t* __restrict__ pos16, const unsigned int* __restrict__ tab, int nk,
                   BinTable B, const int* __restrict__ res, std::uint64_t n, int* __restrict__ out,
                   unsigned long long* __restrict__ work) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1076,7 +987,7 @@ __global__ void __launch_bounds__(kUb2Threads)
 }
 
 __global__ void __launch_bounds__(256)
-    unplaced2_kernel(BinTable B, std::uint64_t n, fm::KParams P, const double2* __restrict__ pts,
+    unplaced_kernel(BinTable B, std::uint64_t n, fm::KParams P, const double2* __restrict__ pts,
                      int* __restrict__ out, HistT* __restrict__ hist, unsigned long long* __restrict__ counters) {
   if (B.hdr[2] <= B.hdr[1]) return;
   for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;

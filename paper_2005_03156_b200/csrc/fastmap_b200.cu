@@ -1021,14 +1021,10 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   const std::uint64_t o_bin = o_cnt + align256(4 * static_cast<std::uint64_t>(nk));
   const std::uint64_t o_pts = o_bin + align256(4 * (3 * static_cast<std::uint64_t>(nk4) + 4));
   const std::uint64_t o_pos = o_pts + align256(16 * nb);
-#if FM_BIN2
   // per point its sorted index inside its chunk (2 B), per chunk the run table
   const std::uint64_t n_chunks = (n + kChunk - 1) / kChunk;
   const std::uint64_t o_tab = o_pos + align256(2 * n);
   const std::uint64_t o_res = o_tab + align256(4 * tab_stride(nk4) * n_chunks);
-#else
-  const std::uint64_t o_res = o_pos + align256(4 * n);
-#endif
   const std::uint64_t total = o_res + align256(4 * nb);
   char* scratch = nullptr;
   FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), total, stream));
@@ -1042,35 +1038,23 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   B.n_eff = work + kCtrCount;
   FM_CUDA(cudaMemsetAsync(scratch, 0, o_bin, stream));  // work counters, n_eff, sample counts
   double2* pts_b = reinterpret_cast<double2*>(scratch + o_pts);
-#if !FM_BIN2
-  unsigned int* pos = reinterpret_cast<unsigned int*>(scratch + o_pos);
-#endif
   int* res = reinterpret_cast<int*>(scratch + o_res);
   {
     auto k0 = bin_sample_kernel;
     const std::uint64_t strata = (n + kSampleStride - 1) / kSampleStride;
     const int grid0 = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-        (strata + kScatterThreads - 1) / kScatterThreads,
-        resident_blocks(ix->device, (const void*)k0, kScatterThreads, tile_smem))));
-    k0<<<grid0, kScatterThreads, tile_smem, stream>>>(P, T, pts, n, counts);
+        (strata + kSampleThreads - 1) / kSampleThreads,
+        resident_blocks(ix->device, (const void*)k0, kSampleThreads, tile_smem))));
+    k0<<<grid0, kSampleThreads, tile_smem, stream>>>(P, T, pts, n, counts);
   }
   bin_plan_kernel<<<1, kPlanThreads, 0, stream>>>(nk, ovf_cap, counts, B);
-#if FM_BIN2
   std::uint16_t* pos16 = reinterpret_cast<std::uint16_t*>(scratch + o_pos);
   unsigned int* tab = reinterpret_cast<unsigned int*>(scratch + o_tab);
-  auto ks = bin_scatter2_kernel;
+  auto ks = bin_scatter_kernel;
   const int sc_smem = sc2_smem(nk4);
   const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       n_chunks, resident_blocks(ix->device, (const void*)ks, kSc2Threads, sc_smem))));
   ks<<<grid_s, kSc2Threads, sc_smem, stream>>>(P, T, pts, n, B, pts_b, pos16, tab);
-#else
-  auto ks = bin_scatter_kernel;
-  const int sc_smem = kScatterIter * 20 + 5 * nk4 * 4;
-  const std::uint64_t n_it = (n + kScatterIter - 1) / kScatterIter;
-  const int grid_s = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      n_it, resident_blocks(ix->device, (const void*)ks, kScatterThreads, sc_smem))));
-  ks<<<grid_s, kScatterThreads, sc_smem, stream>>>(P, T, pts, n, B, pts_b, pos);
-#endif
   bin_seal_kernel<<<std::min(nk, 1184), 256, 0, stream>>>(nk, B, pts_b, kCount ? d_counters : nullptr);
   const unsigned long long* n_dev = B.n_eff;
   // the histogram is counted from res afterwards (binned_hist_kernel): in
@@ -1089,23 +1073,13 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
         (nb + kHistChunk - 1) / kHistChunk, resident_blocks(ix->device, (const void*)kh, kHistThreads, 0))));
     kh<<<grid_h, kHistThreads, 0, stream>>>(res, nb, n_dev, d_hist);
   }
-#if FM_BIN2
-  auto ku = unbin2_kernel;
+  auto ku = unbin_kernel;
   const int ub_smem = ub2_smem(nk4);
   const int grid_u = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
       n_chunks, resident_blocks(ix->device, (const void*)ku, kUb2Threads, ub_smem))));
   ku<<<grid_u, kUb2Threads, ub_smem, stream>>>(pos16, tab, nk, B, res, n, d_out, work);
-  unplaced2_kernel<<<grid_u, 256, 0, stream>>>(B, n, P, pts, d_out, kHist ? d_hist : nullptr,
+  unplaced_kernel<<<grid_u, 256, 0, stream>>>(B, n, P, pts, d_out, kHist ? d_hist : nullptr,
                                                kCount ? d_counters : nullptr);
-#else
-  auto ku = unbin_kernel;
-  const int grid_u = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-      (n + kUnbinBlock - 1) / kUnbinBlock,
-      resident_blocks(ix->device, (const void*)ku, kUnbinThreads, 0))));
-  ku<<<grid_u, kUnbinThreads, 0, stream>>>(pos, res, n, d_out, work);
-  unplaced_kernel<<<grid_u, 256, 0, stream>>>(B, pos, n, P, pts, d_out, kHist ? d_hist : nullptr,
-                                              kCount ? d_counters : nullptr);
-#endif
   const cudaError_t err = cudaGetLastError();
   FM_CUDA(cudaFreeAsync(scratch, stream));
   if (err != cudaSuccess) return set_err(FM_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(err));
