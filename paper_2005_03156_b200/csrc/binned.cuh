@@ -456,38 +456,8 @@ struct RingState {
   QItem pit;             // this lane's staged item
   int dhead = 0, dn = 0; // double-slot ring
   int hhead = 0, hn = 0; // half-slot ring
-  bool phalf = false;    // the staged batch is a half batch
+  int pkind = 0;         // kind of the staged batch: 0 full, 1 half, 2 double
 };
-
-// Evaluate double-slot points in batches of 32 (any remainder when draining).
-template <bool kHist, bool kCount>
-__device__ __forceinline__ void dpump(const fm::KParams& P, const double2* __restrict__ pts, WarpSmemQ& S,
-                                      RingState& R, bool drain, int lane, int* __restrict__ res,
-                                      const HistSink& hist, fm::WorkCount& wc) {
-  while (R.dn >= 32 || (drain && R.dn > 0)) {
-    const int m = min(R.dn, 32);
-    std::uint32_t k = 0, e = 0;
-    if (lane < m) {
-      const int s = (R.dhead + lane) & (kDCap - 1);
-      k = S.dk[s];
-      e = S.de[s];
-    }
-    R.dhead = (R.dhead + m) & (kDCap - 1);
-    R.dn -= m;
-    __syncwarp();
-    if (lane < m) {
-      const double2 p = __ldg(pts + k);
-      const uint4* g = reinterpret_cast<const uint4*>(fm::slot_ptr(P, e));
-      uint4 a[8], b[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) a[j] = __ldg(g + j);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = __ldg(g + 8 + j);
-      if (kCount) wc.boundary++;
-      emit<kHist>(res, hist, k, fm::eval_double_slot<kCount>(a, b, p.x, p.y, wc));
-    }
-  }
-}
 
 // Start copying the first 64 bytes of the slots of the items held by lanes
 // [0, n): 4 lanes per slot, 8 slots per instruction.  Chunk c of slot r is
@@ -584,6 +554,41 @@ __device__ __forceinline__ std::uint32_t eval_staged_half(const fm::KParams& P, 
   return requeue;
 }
 
+// Double slots (256 bytes) go through the same pools 16 at a time: 16 lanes
+// per slot, 2 slots per instruction; chunk c of slot r is stored at chunk
+// c ^ (r & 7) of its 256-byte row.  (Loading them straight from global
+// memory, 16 uncoalesced 16-byte loads per lane, cost 16 L1 tag cycles per
+// item against about 5 here; the kernel is bound by L1 throughput.)
+constexpr int kDblBatch = 16;
+__device__ __forceinline__ void stage_double(const fm::KParams& P, std::uint8_t* buf, std::uint32_t e, int n,
+                                             int lane) {
+  const int c = lane & 15;
+#pragma unroll
+  for (int q = 0; q < kDblBatch / 2; ++q) {
+    const int r = 2 * q + (lane >> 4);
+    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
+    if (r < n) cp_async16(buf + r * 256 + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
+  }
+  cp_async_commit();
+}
+
+template <bool kHist, bool kCount>
+__device__ __forceinline__ void eval_staged_double(const std::uint8_t* buf, const QItem& it, int n, int lane,
+                                                   int* __restrict__ out, const HistSink& hist,
+                                                   fm::WorkCount& wc) {
+  if (lane < n) {
+    const std::uint8_t* base = buf + lane * 256;
+    const int s = lane & 7;
+    uint4 a[8], b[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = *reinterpret_cast<const uint4*>(base + 16 * (k ^ s));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) b[k] = *reinterpret_cast<const uint4*>(base + 128 + 16 * (k ^ s));
+    if (kCount) wc.boundary++;
+    emit<kHist>(out, hist, it.i, fm::eval_double_slot<kCount>(a, b, it.px, it.py, wc));
+  }
+}
+
 // Stage the next batch -- a full-slot batch when 32 such items wait, else a
 // half-slot batch (any when draining) -- and evaluate the previously staged
 // one; repeat while whole batches remain.  Split cells put their child
@@ -595,7 +600,8 @@ __device__ __forceinline__ void pump(const fm::KParams& P, const double2* __rest
   for (;;) {
     const bool sf = R.qn >= 32 || (drain && R.qn > 0);
     const bool sh = !sf && (R.hn >= 32 || (drain && R.hn > 0));
-    const bool stage = sf || sh;
+    const bool sd = !sf && !sh && (R.dn >= kDblBatch || (drain && R.dn > 0));
+    const bool stage = sf || sh || sd;
     if (!stage && !(drain && R.pend > 0)) break;
     int m = 0;
     QItem nit;
@@ -620,6 +626,15 @@ __device__ __forceinline__ void pump(const fm::KParams& P, const double2* __rest
       }
       R.hhead = (R.hhead + m) & (kQCap - 1);
       R.hn -= m;
+    } else if (sd) {
+      m = min(R.dn, kDblBatch);
+      if (lane < m) {
+        const int s = (R.dhead + lane) & (kDCap - 1);
+        nit.i = S.dk[s];
+        nit.e = S.de[s];
+      }
+      R.dhead = (R.dhead + m) & (kDCap - 1);
+      R.dn -= m;
     }
     if (stage) {
       __syncwarp();
@@ -630,8 +645,10 @@ __device__ __forceinline__ void pump(const fm::KParams& P, const double2* __rest
       }
       if (sf) {
         stage_slots(P, S.pool[R.pb ^ 1], nit.e, m, lane);  // commits one group
-      } else {
+      } else if (sh) {
         stage_half(P, S.pool[R.pb ^ 1], nit.e, m, lane);
+      } else {
+        stage_double(P, S.pool[R.pb ^ 1], nit.e, m, lane);
       }
     }
     if (R.pend > 0) {
@@ -641,9 +658,14 @@ __device__ __forceinline__ void pump(const fm::KParams& P, const double2* __rest
         cp_async_wait0();
       }
       __syncwarp();
-      const std::uint32_t ce =
-          R.phalf ? eval_staged_half<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res, hist, wc)
-                  : eval_staged<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res, hist, wc);
+      std::uint32_t ce = 0u;
+      if (R.pkind == 0) {
+        ce = eval_staged<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res, hist, wc);
+      } else if (R.pkind == 1) {
+        ce = eval_staged_half<kHist, kCount>(P, S.pool[R.pb], R.pit, R.pend, lane, res, hist, wc);
+      } else {
+        eval_staged_double<kHist, kCount>(S.pool[R.pb], R.pit, R.pend, lane, res, hist, wc);
+      }
       const std::uint32_t rq = __ballot_sync(0xFFFFFFFFu, ce != 0u);
       if (ce != 0u) {  // split cell: the child entry goes into the full ring
         const int s = (R.head + R.qn + __popc(rq & ((1u << lane) - 1u))) & (kQCap - 1);
@@ -656,8 +678,8 @@ __device__ __forceinline__ void pump(const fm::KParams& P, const double2* __rest
     if (stage) R.pb ^= 1;
     R.pit = nit;
     R.pend = m;
-    R.phalf = sh;
-    if (!drain && R.qn < 32 && R.hn < 32) break;
+    R.pkind = sf ? 0 : (sh ? 1 : 2);
+    if (!drain && R.qn < 32 && R.hn < 32 && R.dn < kDblBatch) break;
   }
 }
 
@@ -756,7 +778,6 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
     }
     if (kCount) done += min(tile, n - base);
     __syncwarp();
-    dpump<kHist, kCount>(P, pts, S, R, false, lane, res, hs, wc);
     pump<kHist, kCount>(P, pts, S, R, false, lane, res, hs, wc);
     t = t1;
     t1 = t2;
@@ -767,7 +788,6 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
       e[u] = e1[u];
     }
   }
-  dpump<kHist, kCount>(P, pts, S, R, true, lane, res, hs, wc);
   pump<kHist, kCount>(P, pts, S, R, true, lane, res, hs, wc);
   hist_close<kHist>(hs);
   if (kCount) {
