@@ -459,18 +459,65 @@ struct RingState {
   int pkind = 0;         // kind of the staged batch: 0 full, 1 half, 2 double
 };
 
-// Start copying the first 64 bytes of the slots of the items held by lanes
-// [0, n): 4 lanes per slot, 8 slots per instruction.  Chunk c of slot r is
-// stored at chunk c ^ ((r >> 1) & 3) of its 64-byte row, so the owner lanes'
-// 16-byte reads are bank-conflict free.
+// Slot staging of the binned query.  A batch's slots are copied by cp.async,
+// 16 bytes per lane: 8 lanes per full slot (4 slots per instruction), 4 per
+// half slot (8), 16 per double slot (2).  The copy's source is
+// slots + 16 * (8 * index + chunk): the entry shifted left by 3 drops its
+// flag bits, so one integer multiply-add and one wide multiply-add form the
+// address; its destination is a per-lane constant plus 512 bytes per
+// instruction.  (stage_slots, the stream path's copy, recomputed both per
+// copy: about 14 instructions each, 17% of this kernel's instructions, most
+// on the integer pipe that bounds it -- profiles/r2ax.)
+__device__ __forceinline__ void cp_async16_s(unsigned saddr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ const std::uint8_t* chunk_ptr(const std::uint8_t* slots, std::uint32_t er, int c) {
+  return slots + static_cast<std::size_t>(er * 8u + static_cast<std::uint32_t>(c)) * 16u;
+}
+
+// Full slots (128 bytes): chunk c of slot r at chunk c ^ (r & 7) of row r.
+__device__ __forceinline__ void stage_full(const fm::KParams& P, std::uint8_t* buf, std::uint32_t e, int n,
+                                           int lane) {
+  const int c = lane & 7, j = lane >> 3;
+  const std::uint8_t* slots = P.slots;
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(buf)) + j * 128;
+  const unsigned d0 = b + 16 * (c ^ j), d1 = b + (16 * (c ^ j) ^ 64);  // r & 7 = 4 (q & 1) + j
+  if (n == 32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, 4 * q + j);
+      cp_async16_s(((q & 1) ? d1 : d0) + q * 512, chunk_ptr(slots, er, c));
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, 4 * q + j);
+      if (4 * q + j < n) cp_async16_s(((q & 1) ? d1 : d0) + q * 512, chunk_ptr(slots, er, c));
+    }
+  }
+  cp_async_commit();
+}
+
+// Half slots (their first 64 bytes): chunk c of slot r at chunk
+// c ^ ((r >> 1) & 3) of its 64-byte row, so the owner lanes' 16-byte reads
+// are bank-conflict free.
 __device__ __forceinline__ void stage_half(const fm::KParams& P, std::uint8_t* buf, std::uint32_t e, int n,
                                            int lane) {
-  const int c = lane & 3;
+  const int c = lane & 3, j = lane >> 2;
+  const std::uint8_t* slots = P.slots;
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(buf)) + j * 64 + 16 * (c ^ ((j >> 1) & 3));
+  if (n == 32) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int r = 8 * q + (lane >> 2);
-    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
-    if (r < n) cp_async16(buf + r * 64 + 16 * (c ^ ((r >> 1) & 3)), fm::slot_ptr(P, er) + 16 * c);
+    for (int q = 0; q < 4; ++q) {
+      const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, 8 * q + j);
+      cp_async16_s(d + q * 512, chunk_ptr(slots, er, c));
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, 8 * q + j);
+      if (8 * q + j < n) cp_async16_s(d + q * 512, chunk_ptr(slots, er, c));
+    }
   }
   cp_async_commit();
 }
@@ -562,12 +609,14 @@ __device__ __forceinline__ std::uint32_t eval_staged_half(const fm::KParams& P, 
 constexpr int kDblBatch = 16;
 __device__ __forceinline__ void stage_double(const fm::KParams& P, std::uint8_t* buf, std::uint32_t e, int n,
                                              int lane) {
-  const int c = lane & 15;
+  const int c = lane & 15, j = lane >> 4;
+  const std::uint8_t* slots = P.slots;
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(buf)) + j * 256;
+  const unsigned t = 16 * (c ^ j);  // r & 7 = (2 (q & 3)) ^ j
 #pragma unroll
   for (int q = 0; q < kDblBatch / 2; ++q) {
-    const int r = 2 * q + (lane >> 4);
-    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
-    if (r < n) cp_async16(buf + r * 256 + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
+    const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, 2 * q + j);
+    if (2 * q + j < n) cp_async16_s(b + (t ^ (32 * (q & 3))) + q * 512, chunk_ptr(slots, er, c));
   }
   cp_async_commit();
 }
@@ -644,7 +693,7 @@ __device__ __forceinline__ void pump(const fm::KParams& P, const double2* __rest
         nit.py = p.y;
       }
       if (sf) {
-        stage_slots(P, S.pool[R.pb ^ 1], nit.e, m, lane);  // commits one group
+        stage_full(P, S.pool[R.pb ^ 1], nit.e, m, lane);  // commits one group
       } else if (sh) {
         stage_half(P, S.pool[R.pb ^ 1], nit.e, m, lane);
       } else {
