@@ -852,66 +852,42 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
 }
 
 // The per-block histogram of a binned batch, from res[] in binned order
-// (after binned_query_kernel, which then runs without histogram code).  A
-// CTA takes chunks of kHistChunk consecutive answers -- one tile's points,
-// so a few thousand distinct leaves at most and, in clustered streams, many
+// (after binned_query_kernel, which then runs without histogram code).
+// One CTA per SM takes one contiguous range of the answers -- a few index
+// tiles at most, so a bounded set of leaves and, in clustered streams, long
 // repeats -- and aggregates them in a shared-memory hash table (open
-// addressing, kHistSlots keys) before one global atomic per distinct leaf.
-// Answers whose probe sequence finds no free slot go straight to the global
-// counters.
-constexpr int kHistThreads = 512;
-#ifndef FM_HIST_CHUNK
-#define FM_HIST_CHUNK 4096  // r2aa: 12.7 ms per 1B c3 answers (16384: 14.2, 65536: 15.4)
-#endif
-#ifndef FM_HIST_AGG
-#define FM_HIST_AGG 0  // experiments: 1 = __match_any_sync aggregation before the table
-#endif
-constexpr int kHistChunk = FM_HIST_CHUNK;
-constexpr int kHistSlots = 4096;
-constexpr int kHistProbes = 8;
+// addressing, kHistSlots keys) that lives across the whole range: it is
+// flushed to the global counters (one atomic per distinct leaf) only when
+// half full and at the end.  Answers whose probe sequence finds no slot go
+// straight to the global counters.  (Round 2's first version flushed a
+// 4096-slot table after every 4096 answers: 12.7 ms per 1B c3 answers,
+// close to one global atomic per answer; profiles/r2aa.)
+constexpr int kHistThreads = 1024;
+constexpr int kHistSlots = 16384;
+constexpr int kHistProbes = 16;
+constexpr int kHistSmem = kHistSlots * 8;
+constexpr int kHistStep = kHistThreads * 4;  // answers per round: one 16-byte load per thread
 
-__global__ void __launch_bounds__(kHistThreads)
+__global__ void __launch_bounds__(kHistThreads, 1)
     binned_hist_kernel(const int* __restrict__ res, std::uint64_t n, const unsigned long long* __restrict__ n_dev,
                        HistT* __restrict__ hist) {
-  __shared__ unsigned int s_key[kHistSlots];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned int* s_key = reinterpret_cast<unsigned int*>(smem_raw);
+  unsigned int* s_cnt = s_key + kHistSlots;
+  __shared__ unsigned int s_ins;
   if (n_dev) n = min(n, static_cast<std::uint64_t>(*n_dev));
-  __shared__ unsigned int s_cnt[kHistSlots];
-  for (int k = threadIdx.x; k < kHistSlots; k += blockDim.x) {
+  for (int k = threadIdx.x; k < kHistSlots; k += kHistThreads) {
     s_key[k] = fm::kEmpty;
     s_cnt[k] = 0u;
   }
-  const std::uint64_t n_chunks = (n + kHistChunk - 1) / kHistChunk;
-  for (std::uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+  if (threadIdx.x == 0) s_ins = 0u;
+  // the CTA's range: whole steps, so every 16-byte load is aligned
+  const std::uint64_t steps = (n + kHistStep - 1) / kHistStep;
+  const std::uint64_t per = (steps + gridDim.x - 1) / gridDim.x;
+  const std::uint64_t s0 = min(steps, per * blockIdx.x), s1 = min(steps, s0 + per);
+  auto flush = [&]() {
     __syncthreads();
-    const std::uint64_t lo = c * kHistChunk, hi = min(n, lo + kHistChunk);
-    for (std::uint64_t i = lo + threadIdx.x; i < hi; i += kHistThreads) {
-      const int id = __ldcs(res + i);
-#if FM_HIST_AGG
-      const unsigned int peers = __match_any_sync(__activemask(), static_cast<unsigned int>(id));
-      if (id < 0 || (threadIdx.x & 31) != static_cast<unsigned int>(__ffs(peers) - 1)) continue;
-      const unsigned int inc = static_cast<unsigned int>(__popc(peers));
-#else
-      if (id < 0) continue;
-      const unsigned int inc = 1u;
-#endif
-      const unsigned int u = static_cast<unsigned int>(id);
-      unsigned int h = (u * 2654435761u) >> 20;  // 12-bit multiplicative hash
-      bool done = false;
-      for (int q = 0; q < kHistProbes && !done; ++q, h = (h + 1) & (kHistSlots - 1)) {
-        unsigned int t = s_key[h];
-        if (t == fm::kEmpty) {
-          t = atomicCAS(s_key + h, fm::kEmpty, u);
-          if (t == fm::kEmpty) t = u;
-        }
-        if (t == u) {
-          atomicAdd(s_cnt + h, inc);
-          done = true;
-        }
-      }
-      if (!done) atomicAdd(hist + u, inc);
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < kHistSlots; k += blockDim.x) {
+    for (int k = threadIdx.x; k < kHistSlots; k += kHistThreads) {
       const unsigned int key = s_key[k];
       if (key != fm::kEmpty) {
         atomicAdd(hist + key, s_cnt[k]);
@@ -919,7 +895,44 @@ __global__ void __launch_bounds__(kHistThreads)
         s_cnt[k] = 0u;
       }
     }
+    if (threadIdx.x == 0) s_ins = 0u;
+    __syncthreads();
+  };
+  auto add = [&](int id) {
+    if (id < 0) return;
+    const unsigned int u = static_cast<unsigned int>(id);
+    unsigned int h = (u * 2654435761u) >> 18;  // 14-bit multiplicative hash
+    for (int q = 0; q < kHistProbes; ++q, h = (h + 1) & (kHistSlots - 1)) {
+      unsigned int t = s_key[h];
+      if (t == fm::kEmpty) {
+        t = atomicCAS(s_key + h, fm::kEmpty, u);
+        if (t == fm::kEmpty) {
+          atomicAdd(&s_ins, 1u);
+          t = u;
+        }
+      }
+      if (t == u) {
+        atomicAdd(s_cnt + h, 1u);
+        return;
+      }
+    }
+    atomicAdd(hist + u, 1u);
+  };
+  __syncthreads();
+  for (std::uint64_t st = s0; st < s1; ++st) {
+    const std::uint64_t i = st * kHistStep + 4ull * threadIdx.x;
+    if (i + 4 <= n) {
+      const int4 v = __ldcs(reinterpret_cast<const int4*>(res + i));
+      add(v.x);
+      add(v.y);
+      add(v.z);
+      add(v.w);
+    } else {
+      for (std::uint64_t k = i; k < n; ++k) add(__ldcs(res + k));
+    }
+    if (__syncthreads_or(s_ins > kHistSlots / 2)) flush();  // a uniform vote, whenever each thread read s_ins
   }
+  flush();
 }
 
 // A point the binning could not place (out[i] == kUnplacedId; see the sampled

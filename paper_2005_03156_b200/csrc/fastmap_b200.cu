@@ -1070,8 +1070,8 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   if (kHist) {
     auto kh = binned_hist_kernel;
     const int grid_h = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
-        (nb + kHistChunk - 1) / kHistChunk, resident_blocks(ix->device, (const void*)kh, kHistThreads, 0))));
-    kh<<<grid_h, kHistThreads, 0, stream>>>(res, nb, n_dev, d_hist);
+        (nb + kHistStep - 1) / kHistStep, resident_blocks(ix->device, (const void*)kh, kHistThreads, kHistSmem))));
+    kh<<<grid_h, kHistThreads, kHistSmem, stream>>>(res, nb, n_dev, d_hist);
   }
   auto ku = unbin_kernel;
   const int ub_smem = ub2_smem(nk4);
