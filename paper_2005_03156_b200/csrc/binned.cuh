@@ -73,16 +73,32 @@ struct TileGeom {
   int n_tiles = 1;   // tnx * tny (bin n_tiles stays empty: points outside the grid are clamped into border tiles)
 };
 
-// The tile of a point.  Points outside the grid (and NaN, which converts to
-// 0) are clamped into the border tiles: only locality depends on the
-// binning, and the query answers them -1 by its own acceptance test.
-__device__ __forceinline__ int tile_key(const fm::KParams& P, const TileGeom& T, double px,
-                                        double py) {
-  int ix = static_cast<int>(__dmul_rn(__dsub_rn(px, P.gx0), P.inv_w));
-  int iy = static_cast<int>(__dmul_rn(__dsub_rn(py, P.gy0), P.inv_h));
-  ix = min(max(ix, 0), P.nx - 1);
-  iy = min(max(iy, 0), P.ny - 1);
-  return (iy >> T.ts) * T.tnx + (ix >> T.ts);
+// The tile of a point, straight from the tile's inverse width: only locality
+// depends on the binning (the query locates every point exactly by itself),
+// so a point within rounding of a tile border may land in the neighbouring
+// tile, and points outside the grid (and NaN, which converts to 0) are
+// clamped into the border tiles.
+struct TileKey {
+  double gx0, gy0, inv_tw, inv_th;
+  int tnx, tny;
+};
+__device__ __forceinline__ TileKey tile_key_params(const fm::KParams& P, const TileGeom& T) {
+  TileKey K;
+  K.gx0 = P.gx0;
+  K.gy0 = P.gy0;
+  const double scale = __longlong_as_double(static_cast<long long>(1023 - T.ts) << 52);  // 2^-ts, exactly
+  K.inv_tw = __dmul_rn(P.inv_w, scale);
+  K.inv_th = __dmul_rn(P.inv_h, scale);
+  K.tnx = T.tnx;
+  K.tny = T.tny;
+  return K;
+}
+__device__ __forceinline__ int tile_key(const TileKey& K, double px, double py) {
+  int tx = static_cast<int>(__dmul_rn(__dsub_rn(px, K.gx0), K.inv_tw));
+  int ty = static_cast<int>(__dmul_rn(__dsub_rn(py, K.gy0), K.inv_th));
+  tx = min(max(tx, 0), K.tnx - 1);
+  ty = min(max(ty, 0), K.tny - 1);
+  return ty * K.tnx + tx;
 }
 
 constexpr int kSampleThreads = 256;
@@ -126,6 +142,7 @@ __global__ void __launch_bounds__(kSampleThreads)
     bin_sample_kernel(fm::KParams P, TileGeom T, const double2* __restrict__ pts, std::uint64_t n,
                       unsigned int* __restrict__ counts) {
   extern __shared__ unsigned int s_hist[];
+  const TileKey K = tile_key_params(P, T);
   const int nk = T.n_tiles + 1;
   for (int k = threadIdx.x; k < nk; k += blockDim.x) s_hist[k] = 0u;
   __syncthreads();
@@ -135,7 +152,7 @@ __global__ void __launch_bounds__(kSampleThreads)
     const std::uint64_t lo = j * kSampleStride;
     const std::uint64_t w = min(static_cast<std::uint64_t>(kSampleStride), n - lo);
     const double2 p = __ldg(pts + lo + stratum_hash(j) % w);
-    atomicAdd(s_hist + tile_key(P, T, p.x, p.y), 1u);
+    atomicAdd(s_hist + tile_key(K, p.x, p.y), 1u);
   }
   __syncthreads();
   for (int k = threadIdx.x; k < nk; k += blockDim.x) {
@@ -223,6 +240,9 @@ __global__ void __launch_bounds__(kPlanThreads)
 // scatter held the points in registers (127 registers, 16 warps per SM):
 // 10.1 ms per 1B c3 points against 8.1 ms (profiles/r2al, r2am); a
 // double-buffered window with one 1024-thread CTA per SM measured 9.4 ms.
+// (A placement pass specialised for chunks without overflow cut the
+// kernel's instructions by a quarter but measured 7.9 against 7.4 ms, with
+// 76 GB instead of 55 GB of L2 traffic: profiles/r2bl, r2bm.)
 // Instead of a 4-byte binned position per point, the scatter leaves
 //   pos16[i]        the point's sorted index k inside its chunk (2 B), and
 //   tab[c][key]     {binned position of the run's first point,
@@ -272,6 +292,7 @@ __global__ void __launch_bounds__(kSc2Threads, FM_SC2_MINB)
   unsigned int* s_ob = s_av + nk4;    // overflow destination of the rest
   std::uint16_t* perm = reinterpret_cast<std::uint16_t*>(s_ob + nk4);
   __shared__ unsigned int s_part[64];
+  const TileKey K = tile_key_params(P, T);
   constexpr int kScanPer = (kMaxTiles + 1 + kSc2Threads - 1) / kSc2Threads;
   const unsigned int ovf_base = B.hdr[0], ovf_cap = B.hdr[1];
   const std::uint64_t n_it = (n + kChunk - 1) / kChunk;
@@ -298,15 +319,25 @@ __global__ void __launch_bounds__(kSc2Threads, FM_SC2_MINB)
     const int cnt = static_cast<int>(hi - base);
     cp_async_wait0();
     __syncthreads();  // the window landed, s_cnt zeroed
+    const bool full = cnt == kChunk;  // every chunk but the stream's last: no per-point bounds tests
     unsigned int kr[kSc2Per];
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < kSc2Per; ++j) {
-      const int q = j * kSc2Threads + tid;
-      kr[j] = 0xFFFFFFFFu;
-      if (q < cnt) {
-        const double2 p = raw[q];
-        const unsigned int key = static_cast<unsigned int>(tile_key(P, T, p.x, p.y));
+      for (int j = 0; j < kSc2Per; ++j) {
+        const double2 p = raw[j * kSc2Threads + tid];
+        const unsigned int key = static_cast<unsigned int>(tile_key(K, p.x, p.y));
         kr[j] = (key << 16) | atomicAdd(s_cnt + key, 1u);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kSc2Per; ++j) {
+        const int q = j * kSc2Threads + tid;
+        kr[j] = 0xFFFFFFFFu;
+        if (q < cnt) {
+          const double2 p = raw[q];
+          const unsigned int key = static_cast<unsigned int>(tile_key(K, p.x, p.y));
+          kr[j] = (key << 16) | atomicAdd(s_cnt + key, 1u);
+        }
       }
     }
     __syncthreads();
@@ -367,22 +398,24 @@ __global__ void __launch_bounds__(kSc2Threads, FM_SC2_MINB)
       reinterpret_cast<uint2*>(tb)[k] = make_uint2(dst, s_off[k] | (av << 16));
     }
     __syncthreads();
+    {
 #pragma unroll
-    for (int j = 0; j < kSc2Per; ++j) {
-      const int q = j * kSc2Threads + tid;
-      if (q < cnt) {
-        const unsigned int key = kr[j] >> 16, r = kr[j] & 0xFFFFu;
-        const unsigned int k = s_off[key] + r, av = s_av[key];
-        unsigned int dst;
-        if (r < av) {
-          dst = s_dst[key] + r;
-        } else {
-          const unsigned int o = s_ob[key] + (r - av);
-          dst = o < ovf_cap ? ovf_base + o : kUnplaced;
+      for (int j = 0; j < kSc2Per; ++j) {
+        const int q = j * kSc2Threads + tid;
+        if (q < cnt) {
+          const unsigned int key = kr[j] >> 16, r = kr[j] & 0xFFFFu;
+          const unsigned int k = s_off[key] + r, av = s_av[key];
+          unsigned int dst;
+          if (r < av) {
+            dst = s_dst[key] + r;
+          } else {
+            const unsigned int o = s_ob[key] + (r - av);
+            dst = o < ovf_cap ? ovf_base + o : kUnplaced;
+          }
+          perm[k] = static_cast<std::uint16_t>(q);
+          sdst[k] = dst;
+          __stcs(pos16 + base + q, static_cast<std::uint16_t>(k));
         }
-        perm[k] = static_cast<std::uint16_t>(q);
-        sdst[k] = dst;
-        __stcs(pos16 + base + q, static_cast<std::uint16_t>(k));
       }
     }
     __syncthreads();
@@ -1039,14 +1072,15 @@ __global__ void __launch_bounds__(kUb2Threads)
       const int k = j * kUb2Threads + tid;
       unsigned int f = s_flag[k];
       s_flag[k] = 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int x = __shfl_up_sync(0xFFFFFFFFu, f, o);
-        if (lane >= o) f = max(f, x);
-      }
+      // the last run head at or before this lane (run heads are sparse: one
+      // ballot and one shuffle instead of a five-step scan), else the
+      // segment's carry-in
+      const unsigned int heads = __ballot_sync(0xFFFFFFFFu, f != 0u) & (0xFFFFFFFFu >> (31 - lane));
+      const unsigned int hf = __shfl_sync(0xFFFFFFFFu, f, heads ? 31 - __clz(heads) : 0);
+      f = heads ? hf : static_cast<unsigned int>(s_seg[k >> 5]);
       idx[j] = kUnplaced;
       if (k < cnt) {
-        const int key = static_cast<int>(max(f, static_cast<unsigned int>(s_seg[k >> 5]))) - 1;
+        const int key = static_cast<int>(f) - 1;
         const unsigned int w = s_oa[key], r = static_cast<unsigned int>(k) - (w & 0xFFFFu), av = w >> 16;
         if (r < av) {
           idx[j] = s_dst[key] + r;
