@@ -1012,7 +1012,10 @@ inline int ub2_smem(int nk4) { return kChunk * 6 + (kChunk / 32) * 2 + 2 * nk4 *
 // k's key is the running maximum of the flags over its segment (a warp
 // scan), its answer res[run's first position + (k - first index)] -- all of
 // a thread's loads issued before the first is used.
-__global__ void __launch_bounds__(kUb2Threads)
+#ifndef FM_UB_MINB
+#define FM_UB_MINB 4  // 32 registers: 4 x 512 threads per SM (3: 3.14 ms, 4: 2.8 ms per 1B points)
+#endif
+__global__ void __launch_bounds__(kUb2Threads, FM_UB_MINB)
     unbin_kernel(const std::uint16_t* __restrict__ pos16, const unsigned int* __restrict__ tab, int nk,
                   BinTable B, const int* __restrict__ res, std::uint64_t n, int* __restrict__ out,
                   unsigned long long* __restrict__ work) {
@@ -1020,14 +1023,14 @@ __global__ void __launch_bounds__(kUb2Threads)
   __shared__ unsigned long long s_grab;
   const int nk4 = (nk + 3) & ~3;
   int* s_res = reinterpret_cast<int*>(smem_raw);
-  unsigned int* s_dst = reinterpret_cast<unsigned int*>(smem_raw + kChunk * 4);
-  unsigned int* s_oa = s_dst + nk4;  // first sorted index | fitting points << 16
-  std::uint16_t* s_flag = reinterpret_cast<std::uint16_t*>(s_oa + nk4);
+  uint2* s_tab = reinterpret_cast<uint2*>(smem_raw + kChunk * 4);  // {first position, first sorted index | fitting points << 16}
+  std::uint16_t* s_flag = reinterpret_cast<std::uint16_t*>(s_tab + nk4);
   std::uint16_t* s_seg = s_flag + kChunk;
   const unsigned int ovf_base = B.hdr[0], ovf_cap = B.hdr[1];
   const std::uint64_t n_it = (n + kChunk - 1) / kChunk;
   const std::uint64_t stride = tab_stride(nk4);
   const int tid = threadIdx.x, lane = tid & 31;
+  const bool vec = (reinterpret_cast<std::uintptr_t>(out) & 15u) == 0;
   for (int k = tid; k < kChunk; k += kUb2Threads) s_flag[k] = 0;
   std::uint64_t it = cta_grab(work + kCtrUnbin, &s_grab);
   while (it < n_it) {
@@ -1036,28 +1039,41 @@ __global__ void __launch_bounds__(kUb2Threads)
     const std::uint64_t base = it * kChunk;
     const int cnt = static_cast<int>(min(n, base + kChunk) - base);
     const unsigned int* tb = tab + it * stride;
+    // whole chunks (every one but the stream's last) with a 16-byte aligned
+    // output: four consecutive points per thread, one 8-byte load of their
+    // sorted indices and one 16-byte store of their ids
+    const bool whole = vec && cnt == kChunk && kUb2Per % 4 == 0;
     unsigned int kk[kUb2Per];
+    if (whole) {
 #pragma unroll
-    for (int j = 0; j < kUb2Per; ++j) {
-      const int q = j * kUb2Threads + tid;
-      kk[j] = q < cnt ? __ldcs(pos16 + base + q) : 0u;
+      for (int j = 0; j < kUb2Per / 4; ++j) {
+        const uint2 w = __ldcs(reinterpret_cast<const uint2*>(pos16 + base) + j * kUb2Threads + tid);
+        kk[4 * j + 0] = w.x & 0xFFFFu;
+        kk[4 * j + 1] = w.x >> 16;
+        kk[(4 * j + 2) % kUb2Per] = w.y & 0xFFFFu;
+        kk[(4 * j + 3) % kUb2Per] = w.y >> 16;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kUb2Per; ++j) {
+        const int q = j * kUb2Threads + tid;
+        kk[j] = q < cnt ? __ldcs(pos16 + base + q) : 0u;
+      }
     }
-    for (int k = tid; k < nk; k += kUb2Threads) {
-      const uint2 e = __ldcs(reinterpret_cast<const uint2*>(tb) + k);
-      s_dst[k] = e.x;
-      s_oa[k] = e.y;
-    }
+    for (int k = tid; k < nk; k += kUb2Threads) s_tab[k] = __ldcs(reinterpret_cast<const uint2*>(tb) + k);
     __syncthreads();  // the table is in shared memory, every flag is zero
+    bool ovf = false;
     for (int k = tid; k < nk; k += kUb2Threads) {
-      const unsigned int off = s_oa[k] & 0xFFFFu;
-      const unsigned int end = k + 1 < nk ? (s_oa[k + 1] & 0xFFFFu) : static_cast<unsigned int>(cnt);
+      const unsigned int w = s_tab[k].y, off = w & 0xFFFFu;
+      const unsigned int end = k + 1 < nk ? (s_tab[k + 1].y & 0xFFFFu) : static_cast<unsigned int>(cnt);
       if (end > off) s_flag[off] = static_cast<std::uint16_t>(k + 1);
+      ovf |= end - off > (w >> 16);  // some of the run went to the overflow bin
     }
     for (int sg = tid; sg * 32 < cnt; sg += kUb2Threads) {
       int lo = 0, hi = nk;  // the last key whose first sorted index is <= 32 sg
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if ((s_oa[mid] & 0xFFFFu) <= static_cast<unsigned int>(32 * sg)) {
+        if ((s_tab[mid].y & 0xFFFFu) <= static_cast<unsigned int>(32 * sg)) {
           lo = mid + 1;
         } else {
           hi = mid;
@@ -1065,7 +1081,7 @@ __global__ void __launch_bounds__(kUb2Threads)
       }
       s_seg[sg] = static_cast<std::uint16_t>(lo);  // key + 1
     }
-    __syncthreads();
+    const bool plain = !__syncthreads_or(ovf) && cnt == kChunk;  // whole chunk, every run in its bin
     unsigned int idx[kUb2Per];
 #pragma unroll
     for (int j = 0; j < kUb2Per; ++j) {
@@ -1078,28 +1094,48 @@ __global__ void __launch_bounds__(kUb2Threads)
       const unsigned int heads = __ballot_sync(0xFFFFFFFFu, f != 0u) & (0xFFFFFFFFu >> (31 - lane));
       const unsigned int hf = __shfl_sync(0xFFFFFFFFu, f, heads ? 31 - __clz(heads) : 0);
       f = heads ? hf : static_cast<unsigned int>(s_seg[k >> 5]);
-      idx[j] = kUnplaced;
-      if (k < cnt) {
-        const int key = static_cast<int>(f) - 1;
-        const unsigned int w = s_oa[key], r = static_cast<unsigned int>(k) - (w & 0xFFFFu), av = w >> 16;
-        if (r < av) {
-          idx[j] = s_dst[key] + r;
-        } else {  // the run's tail went to the overflow bin (or nowhere)
-          const unsigned int o = __ldg(tb + 2 * nk4 + key) + (r - av);
-          if (o < ovf_cap) idx[j] = ovf_base + o;
+      if (plain) {
+        const uint2 e = s_tab[f - 1u];
+        idx[j] = e.x + (static_cast<unsigned int>(k) - (e.y & 0xFFFFu));
+      } else {
+        idx[j] = kUnplaced;
+        if (k < cnt) {
+          const int key = static_cast<int>(f) - 1;
+          const uint2 e = s_tab[key];
+          const unsigned int r = static_cast<unsigned int>(k) - (e.y & 0xFFFFu), av = e.y >> 16;
+          if (r < av) {
+            idx[j] = e.x + r;
+          } else {  // the run's tail went to the overflow bin (or nowhere)
+            const unsigned int o = __ldg(tb + 2 * nk4 + key) + (r - av);
+            if (o < ovf_cap) idx[j] = ovf_base + o;
+          }
         }
       }
     }
     int v[kUb2Per];
+    if (plain) {
 #pragma unroll
-    for (int j = 0; j < kUb2Per; ++j) v[j] = idx[j] != kUnplaced ? __ldcs(res + idx[j]) : kUnplacedId;
+      for (int j = 0; j < kUb2Per; ++j) v[j] = __ldcs(res + idx[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kUb2Per; ++j) v[j] = idx[j] != kUnplaced ? __ldcs(res + idx[j]) : kUnplacedId;
+    }
 #pragma unroll
     for (int j = 0; j < kUb2Per; ++j) s_res[j * kUb2Threads + tid] = v[j];
     __syncthreads();
+    if (whole) {
+      int4* o4 = reinterpret_cast<int4*>(out + base);
 #pragma unroll
-    for (int j = 0; j < kUb2Per; ++j) {
-      const int q = j * kUb2Threads + tid;
-      if (q < cnt) __stcs(out + base + q, s_res[kk[j]]);
+      for (int j = 0; j < kUb2Per / 4; ++j) {
+        __stcs(o4 + j * kUb2Threads + tid, make_int4(s_res[kk[4 * j]], s_res[kk[4 * j + 1]],
+                                                     s_res[kk[(4 * j + 2) % kUb2Per]], s_res[kk[(4 * j + 3) % kUb2Per]]));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kUb2Per; ++j) {
+        const int q = j * kUb2Threads + tid;
+        if (q < cnt) __stcs(out + base + q, s_res[kk[j]]);
+      }
     }
     if (tid == 0) s_grab = nxt;
     __syncthreads();
