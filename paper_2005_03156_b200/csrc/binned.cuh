@@ -105,8 +105,10 @@ constexpr int kSampleThreads = 256;
 
 // ---- single-pass binning with sampled bin capacities ----------------------
 // Sizing the bins exactly takes a counting pass over the whole stream (16
-// B/point: 2.8 ms per 1B c3 points, round 2's first cut).  Instead, one point per stratum of
-// kSampleStride points (at a hashed offset inside the stratum) is counted,
+// B/point: 2.8 ms per 1B c3 points, round 2's first cut).  Instead, one point in
+// kSampleStride (kSampleGroup consecutive points at a hashed place of every
+// stratum of kSampleStride * kSampleGroup; a spatially correlated stream
+// just sees a noisier estimate and uses more of the overflow bin) is counted,
 // every bin gets the sampled estimate plus a kSigmas margin plus kBinPad,
 // and the scatter claims bin space with one global atomic per (iteration,
 // bin).  Points past their bin's capacity go to an overflow bin at the end
@@ -115,6 +117,7 @@ constexpr int kSampleThreads = 256;
 // straight from the index.  Only performance depends on the estimate: every
 // point is answered by the same code wherever it lands.
 constexpr int kSampleStride = 64;
+constexpr int kSampleGroup = 4;
 constexpr unsigned int kBinPad = 256;
 // bin margin in standard deviations of the sampled estimate: every unused
 // slot is a NaN point the query still reads, every overflowing point loses
@@ -146,13 +149,24 @@ __global__ void __launch_bounds__(kSampleThreads)
   const int nk = T.n_tiles + 1;
   for (int k = threadIdx.x; k < nk; k += blockDim.x) s_hist[k] = 0u;
   __syncthreads();
-  const std::uint64_t strata = (n + kSampleStride - 1) / kSampleStride;
+  // kSampleGroup consecutive points (one 64-byte DRAM burst) at a hashed
+  // place of every stratum of kSampleStride * kSampleGroup points: the same
+  // sampling rate as one point per kSampleStride, a quarter of the bursts
+  // (consecutive points of a stream are independent draws)
+  constexpr std::uint64_t kSpan = static_cast<std::uint64_t>(kSampleStride) * kSampleGroup;
+  const std::uint64_t strata = (n + kSpan - 1) / kSpan;
   for (std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < strata;
        j += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-    const std::uint64_t lo = j * kSampleStride;
-    const std::uint64_t w = min(static_cast<std::uint64_t>(kSampleStride), n - lo);
-    const double2 p = __ldg(pts + lo + stratum_hash(j) % w);
-    atomicAdd(s_hist + tile_key(K, p.x, p.y), 1u);
+    const std::uint64_t lo = j * kSpan;
+    const std::uint64_t groups = (min(kSpan, n - lo) + kSampleGroup - 1) / kSampleGroup;
+    const std::uint64_t g0 = lo + (stratum_hash(j) % groups) * kSampleGroup;
+#pragma unroll
+    for (int c = 0; c < kSampleGroup; ++c) {
+      if (g0 + c < n) {
+        const double2 p = __ldg(pts + g0 + c);
+        atomicAdd(s_hist + tile_key(K, p.x, p.y), 1u);
+      }
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < nk; k += blockDim.x) {

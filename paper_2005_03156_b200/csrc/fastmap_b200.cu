@@ -1041,7 +1041,8 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   int* res = reinterpret_cast<int*>(scratch + o_res);
   {
     auto k0 = bin_sample_kernel;
-    const std::uint64_t strata = (n + kSampleStride - 1) / kSampleStride;
+    const std::uint64_t span = static_cast<std::uint64_t>(kSampleStride) * kSampleGroup;
+    const std::uint64_t strata = (n + span - 1) / span;
     const int grid0 = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(
         (strata + kSampleThreads - 1) / kSampleThreads,
         resident_blocks(ix->device, (const void*)k0, kSampleThreads, tile_smem))));
