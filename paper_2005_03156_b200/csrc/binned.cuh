@@ -790,12 +790,14 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
                         unsigned long long* __restrict__ work) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   if (n_dev) n = min(n, static_cast<std::uint64_t>(*n_dev));  // the sealed binned length
+  // a batch (<= 2^30 points) and its bin padding stay below 2^31 points: 32-bit indices throughout
+  const std::uint32_t n32 = static_cast<std::uint32_t>(n);
   __shared__ HotSmem<kHist> hot;
   const HistSink hs = hist_open<kHist>(hist, hot);
   WarpSmemQ& S = reinterpret_cast<WarpSmemQ*>(dsmem)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
-  const std::uint64_t tile = 32ull * kU;
-  const std::uint64_t n_tiles = (n + tile - 1) / tile;
+  constexpr std::uint32_t tile = 32u * kU;
+  const std::uint32_t n_tiles = (n32 + tile - 1) / tile;
   const std::uint32_t lt_mask = (1u << lane) - 1u;
   fm::WorkCount wc;
   RingState R;
@@ -803,34 +805,34 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
   R.pit.i = 0;
   R.pit.e = fm::kEmpty;
   // the warp's tiles: groups of kQGroup consecutive tiles from the counter
-  auto grab = [&]() -> std::uint64_t {
-    unsigned long long g = 0;
-    if (lane == 0) g = atomicAdd(work + kCtrQuery, 1ull);
-    return static_cast<std::uint64_t>(__shfl_sync(0xFFFFFFFFu, g, 0)) * kQGroup;
+  auto grab = [&]() -> std::uint32_t {
+    std::uint32_t g = 0;
+    if (lane == 0) g = static_cast<std::uint32_t>(min(atomicAdd(work + kCtrQuery, 1ull), 0x3FFFFFFull));
+    return __shfl_sync(0xFFFFFFFFu, g, 0) * kQGroup;
   };
   // software pipeline over the warp's tiles t < t1 < t2: the points of t2
   // are loading and the grid entries of t1 are in flight while tile t is
   // answered, so neither latency is exposed (16 warps per SM do not hide
   // the grid gather on their own)
-  auto next_tile = [&](std::uint64_t x, std::uint64_t& g_end) -> std::uint64_t {
-    std::uint64_t y = x + 1;
+  auto next_tile = [&](std::uint32_t x, std::uint32_t& g_end) -> std::uint32_t {
+    std::uint32_t y = x + 1;
     if (y == g_end) {
       y = grab();
       g_end = y + kQGroup;
     }
     return y;
   };
-  auto load_pts = [&](std::uint64_t x, double2 (&q)[kU]) {
+  auto load_pts = [&](std::uint32_t x, double2 (&q)[kU]) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const std::uint64_t i = x * tile + u * 32 + lane;
-      q[u] = (x < n_tiles && i < n) ? FM_QLD(pts + i) : make_double2(NAN, NAN);
+      const std::uint32_t i = x * tile + u * 32 + lane;
+      q[u] = (x < n_tiles && i < n32) ? FM_QLD(pts + i) : make_double2(NAN, NAN);
     }
   };
-  std::uint64_t g_end = 0;
-  std::uint64_t t = grab();
+  std::uint32_t g_end = 0;
+  std::uint32_t t = grab();
   g_end = t + kQGroup;
-  std::uint64_t t1 = t < n_tiles ? next_tile(t, g_end) : n_tiles;
+  std::uint32_t t1 = t < n_tiles ? next_tile(t, g_end) : n_tiles;
   double2 p[kU], p1[kU], p2[kU];
   std::uint32_t e[kU], e1[kU];
   load_pts(t, p);
@@ -838,14 +840,14 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
   fm::locate_n<kU, true, kLs>(P, p, e);
   unsigned long long done = 0;
   while (t < n_tiles) {
-    const std::uint64_t base = t * tile;
-    const std::uint64_t t2 = t1 < n_tiles ? next_tile(t1, g_end) : n_tiles;
+    const std::uint32_t base = t * tile;
+    const std::uint32_t t2 = t1 < n_tiles ? next_tile(t1, g_end) : n_tiles;
     load_pts(t2, p2);
     fm::locate_n<kU, true, kLs>(P, p1, e1);
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const std::uint64_t i = base + u * 32 + lane;
-      const bool valid = i < n;
+      const std::uint32_t i = base + u * 32 + lane;
+      const bool valid = i < n32;
       const bool is_rec = valid && e[u] >= fm::kRecordBit && e[u] != fm::kEmpty;
       const bool is_dbl = is_rec && (e[u] & fm::kDoubleBit) && !(e[u] & fm::kHalfBit);
       if (valid && !is_rec) emit<kHist>(res, hs, i, e[u] < fm::kRecordBit ? static_cast<int>(e[u]) : -1);
@@ -853,26 +855,26 @@ __global__ void __launch_bounds__(kQWarps * 32, FM_QMINB)
       const std::uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rec && !is_dbl && !is_half);
       if (is_rec && !is_dbl && !is_half) {
         const int s = (R.head + R.qn + __popc(b & lt_mask)) & (kQCap - 1);
-        S.qk[s] = static_cast<std::uint32_t>(i);
+        S.qk[s] = i;
         S.qe[s] = e[u];
       }
       R.qn += __popc(b);
       const std::uint32_t bh = __ballot_sync(0xFFFFFFFFu, is_half);
       if (is_half) {
         const int s = (R.hhead + R.hn + __popc(bh & lt_mask)) & (kQCap - 1);
-        S.hk[s] = static_cast<std::uint32_t>(i);
+        S.hk[s] = i;
         S.he[s] = e[u];
       }
       R.hn += __popc(bh);
       const std::uint32_t bd = __ballot_sync(0xFFFFFFFFu, is_dbl);
       if (is_dbl) {
         const int s = (R.dhead + R.dn + __popc(bd & lt_mask)) & (kDCap - 1);
-        S.dk[s] = static_cast<std::uint32_t>(i);
+        S.dk[s] = i;
         S.de[s] = e[u];
       }
       R.dn += __popc(bd);
     }
-    if (kCount) done += min(tile, n - base);
+    if (kCount) done += min(tile, n32 - base);
     __syncwarp();
     pump<kHist, kCount>(P, pts, S, R, false, lane, res, hs, wc);
     t = t1;

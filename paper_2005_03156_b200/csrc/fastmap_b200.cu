@@ -1014,6 +1014,7 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
   // sampled bin capacities, one scatter pass (binned.cuh)
   const std::uint64_t ovf_cap = bin_overflow_cap(n);
   const std::uint64_t nb = bin_capacity_bound(n, nk) + ovf_cap;  // binned length bound
+  if (nb >= (std::uint64_t{1} << 31)) return set_err(FM_ERR_RUNTIME, "binned batch too large");  // the kernels index it in 32 bits
   // scratch: work counters + binned length, sample counts, the bin table,
   // binned points, binned positions, binned answers
   const std::uint64_t o_work = 0;
