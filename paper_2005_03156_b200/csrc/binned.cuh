@@ -38,12 +38,14 @@
 // one window of the stream and every tile's points stay in about input
 // order: the scattered writes and the gather in unbin_kernel stay coherent
 // in L2 and the TLB.
-// Points outside the acceptance box (and NaN) go to one extra bin; the
-// query pass answers them -1 like every other path.
+// Points outside the grid (and NaN) are clamped into the border tiles; the
+// query pass answers them -1 by its own acceptance test, like every path.
 //
 // Only performance depends on the binning: every point is answered by the
-// same locate_n / eval_leaf_slot code as the stream path, so the answers
-// are identical whatever tile or order a point ends up in.
+// same locate_n and the same slot algebra (edge_bit, eval_leaf_slot,
+// eval_double_slot; eval_half_leaf is eval_leaf_slot over a half slot's 64
+// bytes) as the stream path, so the answers are identical whatever tile or
+// order a point ends up in.
 
 #ifndef FM_QMINB
 #define FM_QMINB 2
@@ -468,10 +470,9 @@ __global__ void __launch_bounds__(256)
 // the slot fetches of batch k+1 overlap the evaluation of batch k and the
 // next point tile's loads and grid gathers; split cells put their child
 // entry back into the ring.
-// Points in double slots (kDoubleBit; polygon corners) wait in a second
-// ring of (binned index, entry) pairs and are evaluated in whole batches of
-// 32 straight from global memory (both halves of the 256-byte slot loaded
-// at once), so the leaf-slot batches never run the wider double-slot code.
+// Points in half slots and in double slots (kDoubleBit; polygon corners)
+// wait in rings of their own (below), so every batch is of one slot width
+// and the leaf-slot batches never run the wider double-slot code.
 #ifndef FM_QWARPS
 #define FM_QWARPS 8
 #endif
