@@ -335,13 +335,21 @@ __device__ __forceinline__ void stage_slots(const fm::KParams& P, std::uint8_t* 
   if (lane < n && (e & fm::kDoubleBit) && !(e & fm::kHalfBit)) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(fm::slot_ptr(P, e) + fm::kSlotBytes));
   }
-  const int c = lane & 7;
+  // source: slots + 16 * (8 * index + chunk) (the entry shifted left by 3
+  // drops its flag bits); destination: a per-lane constant + 512 bytes per
+  // instruction (r & 7 = 4 (q & 1) + j for r = 4 q + j)
+  const int c = lane & 7, j = lane >> 3;
+  const std::uint8_t* slots = P.slots;
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(buf)) + j * 128;
+  const unsigned d0 = b + 16 * (c ^ j), d1 = b + (16 * (c ^ j) ^ 64);
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const int r = 4 * q + (lane >> 3);
+    const int r = 4 * q + j;
     const std::uint32_t er = __shfl_sync(0xFFFFFFFFu, e, r);
     if (r < n && (c < 4 || !(er & fm::kHalfBit))) {  // half slots: first 64 bytes only
-      cp_async16(buf + r * fm::kSlotBytes + 16 * (c ^ (r & 7)), fm::slot_ptr(P, er) + 16 * c);
+      const unsigned dst = ((q & 1) ? d1 : d0) + q * 512;
+      const std::uint8_t* src = slots + static_cast<std::size_t>(er * 8u + static_cast<std::uint32_t>(c)) * 16u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
     }
   }
   cp_async_commit();
