@@ -1103,13 +1103,17 @@ fm_status launch_binned_t(const fm_index* ix, const double2* pts, std::uint64_t 
 // 8.2 vs 8.8 ms per 200M, profiles/r2u) -- and the batch is big enough to
 // reuse tiles; the stream path otherwise (c1; c2: 9% boundary cells, 1.13
 // vs 2.8 ms per 100M).
+// The index side of the choice: far larger than L2 and mostly boundary cells.
+bool binned_index(const fm_index* ix) {
+  const double cells = static_cast<double>(ix->g.nx) * static_cast<double>(ix->g.ny);
+  const double bfrac = cells > 0 ? static_cast<double>(ix->stats.cells_boundary) / cells : 0.0;
+  const double bytes = static_cast<double>(ix->grid_len * 4 + ix->stats.arena_bytes);
+  return bytes >= 1e9 && bfrac >= 0.25;
+}
 bool use_binned(const fm_index* ix, std::uint64_t n) {
   if (ix->query_path == FM_PATH_STREAM) return false;
   if (ix->query_path == FM_PATH_BINNED) return true;
-  const double cells = static_cast<double>(ix->g.nx) * static_cast<double>(ix->g.ny);
-  const double bfrac = cells > 0 ? static_cast<double>(ix->stats.cells_boundary) / cells : 0.0;
-  const double bytes = static_cast<double>(ix->stats.query_grid_bytes + ix->stats.arena_bytes);
-  return n >= (std::uint64_t{1} << 24) && bytes >= 1e9 && bfrac >= 0.25;
+  return n >= (std::uint64_t{1} << 24) && binned_index(ix);
 }
 
 // Tiles of 2^ts x 2^ts cells holding about `tile_bytes` of index (query
@@ -1447,7 +1451,13 @@ fm_status finish_device(fm_index* ix, double approx_epsilon) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   const int nx = static_cast<int>(ix->g.nx), ny = static_cast<int>(ix->g.ny);
-  const int qls = fold_ls(nx, ny, kQueryBudget, kQueryMaxLs);
+  // An index the binned path will take (binned_index below) keeps its flat
+  // grid: a tile's 4 MB of flat entries are L2-resident while the tile is
+  // walked, so the fold only adds a dependent gather (c3 at 7 / 8 cells per
+  // leaf side: 31.5 / 30.6 ms per 1B points folded, 23.2 / 22.3 flat; the
+  // stream path 43.4 / 43.1 against 40.4 / 39.3 -- profiles/r2bz, r2ca).
+  const int max_ls = binned_index(ix) ? 0 : kQueryMaxLs;
+  const int qls = fold_ls(nx, ny, kQueryBudget, max_ls);
   // the binned path's default tiles (index bytes per cell before the fold:
   // the flat grid plus the slot arena)
   fm_index_stats pre = ix->stats;
@@ -1455,7 +1465,7 @@ fm_status finish_device(fm_index* ix, double approx_epsilon) {
   const TileGeom T0 = plan_tiles(ix->g, pre, kTileBytes);
   fm_status st = renumber_slots(ix, T0.ts, qls);
   if (st == FM_OK) {
-    st = fold_grid(ix->d_grid, nx, ny, kQueryBudget, kQueryMaxLs, 2, ix->host.n_phase1_slots,
+    st = fold_grid(ix->d_grid, nx, ny, kQueryBudget, max_ls, 2, ix->host.n_phase1_slots,
                    kQueryMaxRatio, &ix->qgrid);
   }
   if (st != FM_OK) return st;

@@ -544,12 +544,13 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
     if (!(m > 0.0)) {
       // ~450M cells (c2: 42 cells per polygon side, 9% boundary points;
       // measured optimum 40-48 with 16-byte small sub-blocks), 4..48 per
-      // side.  With double slots and the binned path this also holds for
-      // the 12.5M-leaf c3: 6 per side (266M cells, 19 GB arena) queries 1B
-      // points in 32.5 ms against 36.7 at 3.6 per side (the round-1 270M
-      // budget's 160M cells) and 38-39 ms at 7-8 per side (profiles/r2af)
-      //
-      const double budget = 450.0e6;
+      // side.  Tilings of more than 4M leaves (c3: 12.5M) get ~800M: their
+      // indexes take the binned path on a flat grid, where a finer grid
+      // only trades boundary points for arena bytes -- c3 queries 1B points
+      // in 22.3 ms at 8 cells per leaf side (474M cells, 25.7 GB arena)
+      // against 23.2 at 7 and 24.5 at 6 (profiles/r2ca); 9 per side does
+      // not build next to 1B resident points.
+      const double budget = active > 4000000 ? 800.0e6 : 450.0e6;
       m = std::sqrt(budget / static_cast<double>(active));
       m = std::min(48.0, std::max(4.0, m));
       // few polygons (>= 64): still at least ~10M cells (a ~40 MB grid, L2-sized),
