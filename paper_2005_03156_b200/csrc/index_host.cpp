@@ -543,7 +543,7 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
     double m = o.cells_per_polygon;
     if (!(m > 0.0)) {
       // ~450M cells (c2: 42 cells per polygon side, 9% boundary points;
-      // measured optimum 40-48 with 16-byte small sub-blocks), 4..48 per
+      // measured optimum 40-48 with 16-byte small sub-blocks), 4..64 per
       // side.  Tilings of more than 4M leaves (c3: 12.5M) get ~800M: their
       // indexes take the binned path on a flat grid, where a finer grid
       // only trades boundary points for arena bytes -- c3 queries 1B points
@@ -552,7 +552,9 @@ GridGeom plan_grid(const Soup& s, const BuildOptions& o, BuildStats* st) {
       // not build next to 1B resident points.
       const double budget = active > 4000000 ? 800.0e6 : 450.0e6;
       m = std::sqrt(budget / static_cast<double>(active));
-      m = std::min(48.0, std::max(4.0, m));
+      // (cap 64: c4, 100k concave polygons on the binned path, 4.76 ms per 200M
+      // points at 64 per side against 5.13 at 48, 4.82 at 80: profiles/r2cd)
+      m = std::min(64.0, std::max(4.0, m));
       // few polygons (>= 64): still at least ~10M cells (a ~40 MB grid, L2-sized),
       // since the 48-per-side cap would leave a needlessly coarse grid
       // (c1, 1,024 polygons: 48 -> 99 per side, 0.70 -> 0.62 ms per 100M
