@@ -1,6 +1,6 @@
 // binned.cuh -- the tile-binned query path (north star item 2, "point
 // binning"), included by fastmap_b200.cu inside its anonymous namespace
-// (it reuses QItem, stage_slots, eval_staged and emit from there).
+// (it reuses QItem, eval_staged and emit from there).
 //
 // The reference sorts its pending (leaf, point) pairs and walks them leaf
 // by leaf (cell_index.hpp:546-588, std::sort at :567) so each polygon's
@@ -12,10 +12,13 @@
 // instead of once per point.  It pays off when the index is far larger
 // than L2 and most points land in boundary cells (c3, c4); the stream path
 // (stream_kernel + resolve_kernel) stays the choice for small or mostly
-// true-hit indexes (c1, c2) -- see choose_path() in fastmap_b200.cu.
+// true-hit indexes (c1, c2) -- see use_binned() in fastmap_b200.cu.  An
+// index this path takes keeps a flat query grid (finish_device): a tile's
+// entries are L2-resident while the tile is walked.
 //
 // Per batch of n <= 2^30 points:
-//   bin_sample_kernel   one point per 64-point stratum: sampled bin counts
+//   bin_sample_kernel   one point in 64 (four consecutive ones per 256-point
+//                       stratum): sampled bin counts
 //   bin_plan_kernel     bin capacities (estimate + 3 sigma + pad), their
 //                       scan as bin starts, the overflow bin after them
 //   bin_scatter_kernel  a chunk of 4K points at a time, copied into shared
